@@ -1,0 +1,127 @@
+/* fairkv.h -- C ABI of the B200-native FairKV hot path (libfairkv.so).
+ *
+ * Everything a foreign caller binds: plain pointers, sizes and a cudaStream_t
+ * passed as void*.  No torch types cross this boundary.  Kernels never
+ * allocate: the caller owns every buffer (workspaces included) and every call
+ * is stream-ordered with no host synchronisation inside.
+ *
+ * Return convention: >= 0 success (solvers: 1 = found, 0 = none), < 0 error;
+ * the message of the most recent error on the calling thread is
+ * fkv_last_error().
+ *
+ * Two groups of entry points:
+ *
+ *   B1  AHA placement plugin.  Replaces the reference's search-kernel
+ *       backend  headbalance._kernel.solve_equal_split / solve_free_split
+ *       (reference pkg/src/headbalance/_kernel/__init__.py:49-57; contract
+ *       pkg/src/headbalance/_kernel/reference.py:80-100, 238-244).  Host
+ *       C++; bit-identical to the reference including node counts.
+ *       fkv_select_best / fkv_optimize_plan additionally replace the Python
+ *       scheme loop select_best (reference allocate.py:236-277) and the
+ *       process-pool layer loop optimize_plan (reference allocate.py:353-389).
+ *
+ *   B3  Compressed-cache decode path (no reference implementation exists:
+ *       SPEC.md:8 puts inference out of the reference's scope; the paper used
+ *       KVPress AdaKV on A100s).  sm_100a CUDA kernels.
+ *
+ * Cache layout used by B3: a layer's compressed
+ * K and V on one GPU are two bf16 arrays of rows of head_dim = 128 elements
+ * (256 B).  Row r stores its sixteen 16-byte chunks XOR-swizzled:
+ * logical chunk c lives at physical chunk c ^ (r & 7).  A *segment* is the
+ * retained tokens of one (request, KV-head copy); it occupies seg_len
+ * consecutive rows starting at seg_row0, which is a multiple of FKV_PAGE.
+ * Rows between seg_row0 + seg_len and the next page boundary are zero.
+ */
+#ifndef FAIRKV_H_
+#define FAIRKV_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FKV_OK 0
+#define FKV_ERR_INVALID (-1)      /* bad argument / shape */
+#define FKV_ERR_CUDA (-2)         /* CUDA launch / runtime error */
+#define FKV_ERR_VALIDATION (-3)   /* maps to headbalance ValidationError */
+#define FKV_ERR_INFEASIBLE (-4)   /* maps to headbalance InfeasibleError */
+#define FKV_ERR_SEARCH_SPACE (-5) /* maps to headbalance SearchSpaceError */
+
+#define FKV_HEAD_DIM 128
+#define FKV_PAGE 64 /* tokens per page; segment starts are page aligned */
+
+const char* fkv_last_error(void);
+int fkv_version(void);
+
+/* ------------------------------------------------------------ B1 planner -- */
+
+/* Best equal-cardinality grouping of m copies into tp groups with spread
+ * strictly below cutoff.  w: adjusted copy weights, heaviest first (ties by
+ * head id); heads: owning head per copy.  hint_spread == NULL means no hint,
+ * else (*hint_spread, hint_rgs[m]) is a known grouping.  On return 1,
+ * (*out_spread, out_rgs[m]) is the grouping (restricted-growth labels);
+ * 0 = nothing below cutoff.  *out_nodes = B&B nodes visited (<= node_budget).
+ * Replaces reference _kernel/reference.py:80-235 (and _fastpath.pyx:136-226). */
+int fkv_solve_equal_split(const double* w, const int32_t* heads, int32_t m, int32_t tp,
+                          double cutoff, int64_t node_budget, const double* hint_spread,
+                          const int32_t* hint_rgs, double* out_spread, int32_t* out_rgs,
+                          int64_t* out_nodes);
+
+/* Relaxed variant: groups only need to be nonempty.
+ * Replaces reference _kernel/reference.py:238-340 (pure Python in the reference). */
+int fkv_solve_free_split(const double* w, const int32_t* heads, int32_t m, int32_t tp,
+                         double cutoff, int64_t node_budget, const double* hint_spread,
+                         const int32_t* hint_rgs, double* out_spread, int32_t* out_rgs,
+                         int64_t* out_nodes);
+
+/* Whole per-layer search (reference allocate.py:236-277): every scheme in
+ * (total copies, replicas) order, canonical copies, SHA hint for the identity
+ * scheme, strict-improvement cutoff.  Outputs the winning scheme
+ * out_replicas[n], its canonical copy heads out_heads_c[m] and groups
+ * out_rgs[m] (m = *out_m <= n + ch_budget) and spread *out_delta. */
+int fkv_select_best(const double* layer_weights, int32_t n, int32_t tp, int32_t ch_budget,
+                    int32_t r_max, int32_t equal_split, int64_t max_schemes, int64_t node_budget,
+                    int32_t* out_replicas, int32_t* out_heads_c, int32_t* out_rgs, int32_t* out_m,
+                    double* out_delta);
+
+/* fkv_select_best over num_layers rows of weights[num_layers][n] with a
+ * thread pool of `workers`.  Per-layer outputs are strided: replicas by n,
+ * heads_c / rgs by (n + ch_budget). */
+int fkv_optimize_plan(const double* weights, int32_t num_layers, int32_t n, int32_t tp,
+                      int32_t ch_budget, int32_t r_max, int32_t equal_split, int64_t max_schemes,
+                      int64_t node_budget, int32_t workers, int32_t* out_replicas,
+                      int32_t* out_heads_c, int32_t* out_rgs, int32_t* out_m, double* out_delta);
+
+/* ------------------------------------------------- B3 decode over the cache -- */
+
+/* K4: split-KV decode attention over ragged segments (one layer, one GPU).
+ *   q        bf16 [*, 128]   query rows; segment s uses rows seg_qrow[s] .. +group-1
+ *   k, v     bf16 [rows,128] swizzled cache rows (layout above)
+ *   seg_row0 int64 [n_seg]   first cache row of each segment (page aligned)
+ *   seg_len  int32 [n_seg]   retained tokens per segment
+ *   seg_qrow int32 [n_seg]
+ *   item_seg, item_t0, item_t1 int32 [n_items]: work item = tokens [t0,t1) of a segment
+ *   part_o   f32 [n_items, group, 128]  softmax-normalised partial output
+ *   part_lse f32 [n_items, group]       natural-log sum-exp of the scaled scores
+ * group (= Hq/Hkv) must be 4 or 8; softmax scale = sm_scale. */
+int fkv_decode_partial(const void* q, const void* k, const void* v, const int64_t* seg_row0,
+                       const int32_t* seg_len, const int32_t* seg_qrow, const int32_t* item_seg,
+                       const int32_t* item_t0, const int32_t* item_t1, int32_t n_items,
+                       int32_t group, float sm_scale, float* part_o, float* part_lse,
+                       void* stream);
+
+/* K5 (local / post-all-gather half): log-sum-exp merge.  Output row-group g
+ * (group rows of 128) merges partial rows src_idx[grp_ptr[g] .. grp_ptr[g+1]).
+ * If out_bf16 != NULL writes o bf16 [*,128] at rows out_row[g] .. +group-1;
+ * if out_f32 != NULL writes the merged normalised o (f32) there instead, and
+ * out_lse (optional) receives the merged lse at the same row index. */
+int fkv_merge_lse(const float* part_o, const float* part_lse, const int32_t* grp_ptr,
+                  const int32_t* src_idx, const int32_t* out_row, int32_t n_groups, int32_t group,
+                  void* out_bf16, float* out_f32, float* out_lse, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FAIRKV_H_ */

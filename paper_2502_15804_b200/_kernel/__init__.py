@@ -1,0 +1,46 @@
+"""Search-kernel plugin registry (drop-in for pkg/src/headbalance/_kernel/__init__.py:1-57).
+
+One backend: ``"native"``, the C++ planner inside libfairkv.so.  The
+reference's pure-Python kernel is not part of this product; its CPU
+restatement lives in ``oracle/`` and is used only by the tests as the
+checker.  ``HEADBALANCE_KERNEL`` keeps the reference's spelling: unset /
+"auto" / "native" / "compiled" / "c" / "ext" select the native kernel; asking
+for the Python kernel ("python", "py", "pure", "reference") fails loudly
+instead of silently running something else; any other value is a
+``ValueError`` as in the reference (_kernel/__init__.py:28-29).
+"""
+
+import os
+
+from . import native
+from .native import DEFAULT_NODE_BUDGET
+
+_NATIVE_NAMES = {"", "auto", "native", "compiled", "c", "ext"}
+_PY_NAMES = {"python", "py", "pure", "reference"}
+
+_choice = os.environ.get("HEADBALANCE_KERNEL", "").strip().lower()
+if _choice in _PY_NAMES:
+    raise ImportError(
+        "HEADBALANCE_KERNEL selects the pure-Python kernel, which this B200 build does not ship; "
+        "unset it (the native C++ kernel is bit-identical, including node counts)"
+    )
+if _choice not in _NATIVE_NAMES:
+    raise ValueError(f"unrecognized HEADBALANCE_KERNEL value: {_choice!r}")
+
+
+def backend() -> str:
+    """Name of the active kernel backend."""
+    return "native"
+
+
+def implementations() -> dict:
+    """All kernel implementations shipped, for parity tests and benchmarks."""
+    return {"native": native}
+
+
+def solve_equal_split(weights, heads, tp, cutoff, node_budget=DEFAULT_NODE_BUDGET, hint=None):
+    return native.solve_equal_split(weights, heads, tp, cutoff, node_budget, hint)
+
+
+def solve_free_split(weights, heads, tp, cutoff, node_budget=DEFAULT_NODE_BUDGET, hint=None):
+    return native.solve_free_split(weights, heads, tp, cutoff, node_budget, hint)

@@ -1,0 +1,115 @@
+"""K4 + K5 parity: CUDA split-KV decode over the ragged swizzled cache vs the
+float64 oracle (oracle/kv.py).  Tolerance (north_star): bf16 rtol 2e-2 on o
+(atol 1e-2 for near-zero entries); lse within 2e-3 absolute (fp32 log-sum-exp
+of bf16 scores)."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import kv as okv
+
+pytestmark = pytest.mark.gpu
+
+
+def _bf16(x: torch.Tensor) -> torch.Tensor:
+    return x.to(torch.bfloat16)
+
+
+def build_cache(seg_lens, group, hkv, bt, device, seed=0, chunk=None):
+    from paper_2502_15804_b200.cache import LayerCache, segment_offsets
+    g = torch.Generator().manual_seed(seed)
+    hq = hkv * group
+    seg_qrow = [b * hq + h * group for b in range(bt) for h in range(hkv)]
+    cache = LayerCache.allocate(seg_lens, seg_qrow, seg_qrow, group, device, chunk=chunk)
+    row0, _ = segment_offsets(seg_lens)
+    ks, vs = [], []
+    kh = torch.zeros(cache.k.shape, dtype=torch.bfloat16)
+    vh = torch.zeros(cache.v.shape, dtype=torch.bfloat16)
+    for r0, n in zip(row0, seg_lens):
+        k = _bf16(torch.randn(n, 128, generator=g))
+        v = _bf16(torch.randn(n, 128, generator=g))
+        ks.append(k.float().numpy().astype(np.float64))
+        vs.append(v.float().numpy().astype(np.float64))
+        # store swizzled rows (pure permutation of 16-byte chunks)
+        kh[r0:r0 + n] = torch.from_numpy(okv.swizzle_rows(k.view(torch.int16).numpy(), r0)).view(torch.bfloat16)
+        vh[r0:r0 + n] = torch.from_numpy(okv.swizzle_rows(v.view(torch.int16).numpy(), r0)).view(torch.bfloat16)
+    cache.k.copy_(kh)
+    cache.v.copy_(vh)
+    q = _bf16(torch.randn(bt, hq, 128, generator=g))
+    return cache, q, ks, vs
+
+
+@pytest.mark.parametrize("group", [8, 4])
+@pytest.mark.parametrize("chunk", [None, 64, 128])
+def test_decode_matches_oracle(cuda_device, group, chunk):
+    from paper_2502_15804_b200 import ops
+    rng = np.random.default_rng(group * 100 + (chunk or 0))
+    hkv, bt = 8, 3
+    seg_lens = rng.integers(1, 700, size=bt * hkv).tolist()
+    seg_lens[0] = 1
+    seg_lens[1] = 16
+    seg_lens[2] = 17
+    seg_lens[3] = 64
+    seg_lens[4] = 65
+    cache, q, ks, vs = build_cache(seg_lens, group, hkv, bt, cuda_device, chunk=chunk)
+    o, lse = ops.decode(q.to(cuda_device), cache)
+    torch.cuda.synchronize()
+    o_ref, lse_ref = okv.decode_heads(q.float().numpy().astype(np.float64), ks, vs, group)
+    torch.testing.assert_close(o.float().cpu().double(), torch.from_numpy(o_ref), rtol=2e-2, atol=1e-2)
+    torch.testing.assert_close(lse.cpu().double(), torch.from_numpy(lse_ref), rtol=0, atol=2e-3)
+
+
+def test_decode_large_scores_stable(cuda_device):
+    """Large-magnitude logits must not overflow the online softmax."""
+    from paper_2502_15804_b200 import ops
+    hkv, bt, group = 8, 1, 8
+    seg_lens = [300] * hkv
+    cache, q, ks, vs = build_cache(seg_lens, group, hkv, bt, cuda_device, seed=3)
+    q = (q.float() * 30).to(torch.bfloat16)
+    o, lse = ops.decode(q.to(cuda_device), cache)
+    o_ref, lse_ref = okv.decode_heads(q.float().numpy().astype(np.float64), ks, vs, group)
+    assert torch.isfinite(o).all()
+    torch.testing.assert_close(o.float().cpu().double(), torch.from_numpy(o_ref), rtol=2e-2, atol=2e-2)
+    torch.testing.assert_close(lse.cpu().double(), torch.from_numpy(lse_ref), rtol=1e-3, atol=5e-2)
+
+
+def test_lse_merge_of_token_split_equals_whole(cuda_device):
+    """AHA-DP: a head split along tokens into r copies, merged by LSE, equals
+    attention over the whole head (the identity the sharded decode relies on)."""
+    from paper_2502_15804_b200 import ops
+    group, hkv = 8, 1
+    n = 1000
+    cuts = [0, 333, 334, 1000]  # includes an empty copy
+    lens = [cuts[i + 1] - cuts[i] for i in range(3)]
+    g = torch.Generator().manual_seed(7)
+    k = _bf16(torch.randn(n, 128, generator=g))
+    v = _bf16(torch.randn(n, 128, generator=g))
+    q = _bf16(torch.randn(1, group, 128, generator=g)).to(cuda_device)
+    from paper_2502_15804_b200.cache import LayerCache, segment_offsets
+    cache = LayerCache.allocate(lens, [0, 0, 0], [0, group, 2 * group], group, cuda_device)
+    row0, _ = segment_offsets(lens)
+    kh = torch.zeros(cache.k.shape, dtype=torch.bfloat16)
+    vh = torch.zeros(cache.v.shape, dtype=torch.bfloat16)
+    for i, r0 in enumerate(row0):
+        a, b = cuts[i], cuts[i + 1]
+        kh[r0:r0 + b - a] = torch.from_numpy(okv.swizzle_rows(k[a:b].view(torch.int16).numpy(), r0)).view(torch.bfloat16)
+        vh[r0:r0 + b - a] = torch.from_numpy(okv.swizzle_rows(v[a:b].view(torch.int16).numpy(), r0)).view(torch.bfloat16)
+    cache.k.copy_(kh)
+    cache.v.copy_(vh)
+    # per-copy partials (f32 o + lse) into slots, then merge the 3 slots
+    slots_o = torch.zeros(3 * group, 128, device=cuda_device)
+    slots_lse = torch.zeros(3 * group, device=cuda_device)
+    part_o, part_lse = ops.decode_partial(q, cache)
+    ops.merge_lse(part_o, part_lse, cache.grp_ptr, cache.src_idx, cache.seg_out_row, group,
+                  out_f32=slots_o, out_lse=slots_lse)
+    dev = cuda_device
+    o = torch.empty(1, group, 128, dtype=torch.bfloat16, device=dev)
+    lse = torch.empty(1, group, device=dev)
+    ops.merge_lse(slots_o.view(3, group, 128), slots_lse.view(3, group),
+                  torch.tensor([0, 3], dtype=torch.int32, device=dev),
+                  torch.arange(3, dtype=torch.int32, device=dev),
+                  torch.zeros(1, dtype=torch.int32, device=dev), group, out_bf16=o, out_lse=lse)
+    o_ref, lse_ref = okv.attend(q[0].float().cpu().numpy(), k.float().numpy(), v.float().numpy())
+    torch.testing.assert_close(o[0].float().cpu().double(), torch.from_numpy(o_ref), rtol=2e-2, atol=1e-2)
+    torch.testing.assert_close(lse[0].cpu().double(), torch.from_numpy(lse_ref), rtol=0, atol=2e-3)
