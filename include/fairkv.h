@@ -29,8 +29,10 @@
  * (256 B).  Row r stores its sixteen 16-byte chunks XOR-swizzled:
  * logical chunk c lives at physical chunk c ^ (r & 7).  A *segment* is the
  * retained tokens of one (request, KV-head copy); it occupies seg_len
- * consecutive rows starting at seg_row0, which is a multiple of FKV_PAGE.
- * Rows between seg_row0 + seg_len and the next page boundary are zero.
+ * consecutive rows starting at seg_row0.  Storage for a segment is allocated
+ * page aligned (FKV_PAGE) with zero rows up to the next page boundary; a
+ * DP copy of a head may address a sub-range of such storage, so kernels only
+ * require seg_row0 % FKV_SPLIT == 0.
  */
 #ifndef FAIRKV_H_
 #define FAIRKV_H_
@@ -50,6 +52,8 @@ extern "C" {
 
 #define FKV_HEAD_DIM 128
 #define FKV_PAGE 64 /* tokens per page; segment starts are page aligned */
+#define FKV_SPLIT 16 /* DP-copy token cuts are multiples of this (16-token tiles) */
+#define FKV_REC 132 /* floats per partial record: o[128], lse, 3 pad (16-B aligned) */
 
 const char* fkv_last_error(void);
 int fkv_version(void);
@@ -95,30 +99,46 @@ int fkv_optimize_plan(const double* weights, int32_t num_layers, int32_t n, int3
 
 /* ------------------------------------------------- B3 decode over the cache -- */
 
-/* K4: split-KV decode attention over ragged segments (one layer, one GPU).
- *   q        bf16 [*, 128]   query rows; segment s uses rows seg_qrow[s] .. +group-1
- *   k, v     bf16 [rows,128] swizzled cache rows (layout above)
- *   seg_row0 int64 [n_seg]   first cache row of each segment (page aligned)
- *   seg_len  int32 [n_seg]   retained tokens per segment
- *   seg_qrow int32 [n_seg]
- *   item_seg, item_t0, item_t1 int32 [n_items]: work item = tokens [t0,t1) of a segment
- *   part_o   f32 [n_items, group, 128]  softmax-normalised partial output
- *   part_lse f32 [n_items, group]       natural-log sum-exp of the scaled scores
- * group (= Hq/Hkv) must be 4 or 8; softmax scale = sm_scale. */
-int fkv_decode_partial(const void* q, const void* k, const void* v, const int64_t* seg_row0,
-                       const int32_t* seg_len, const int32_t* seg_qrow, const int32_t* item_seg,
-                       const int32_t* item_t0, const int32_t* item_t1, int32_t n_items,
-                       int32_t group, float sm_scale, float* part_o, float* part_lse,
-                       void* stream);
+/* K4 (+ fused K5): split-KV decode attention over ragged segments (one
+ * layer, one GPU), one CTA per work item.
+ *   q            bf16 [*, 128]   query rows; segment s uses rows seg_qrow[s] .. +group-1
+ *   k, v         bf16 [rows,128] swizzled cache rows (layout above)
+ *   seg_row0     int64 [n_seg]   first cache row of each segment (multiple of FKV_SPLIT)
+ *   seg_len      int32 [n_seg]   retained tokens per segment
+ *   seg_qrow     int32 [n_seg]
+ *   seg_out_row  int32 [n_seg]   first output row of the segment's group heads
+ *   seg_item_ptr int32 [n_seg+1] items of segment s are [ptr[s], ptr[s+1])
+ *   item_seg, item_t0, item_t1 int32 [n_items]: work item = tokens [t0,t1) of a
+ *                segment, t0 a multiple of 64
+ *   part         f32 [n_items, group, FKV_REC]  partial records: softmax-normalised
+ *                o[128] and lse = natural-log sum-exp of the scaled scores
+ *   counters     int32 [n_seg], zero on entry; left zero on exit
+ * With all of out_bf16 / out_rec / out_lse NULL every item just writes its
+ * partial record (split-K partials).  Otherwise the last CTA to finish a
+ * segment merges its chunks by log-sum-exp and writes rows
+ * seg_out_row[s] + h (h < group) of out_bf16 (bf16 [*,128]), out_rec
+ * (f32 [*,FKV_REC]) and/or out_lse (f32 [*]) -- one launch per layer.
+ * group (= Hq/Hkv) must be 4 or 8; softmax scale = sm_scale.
+ * Nothing in the reference is replaced (it has no decode); its cost model of
+ * this kernel is reference latency.py:85-91 (predict_compute). */
+int fkv_decode(const void* q, const void* k, const void* v, const int64_t* seg_row0,
+               const int32_t* seg_len, const int32_t* seg_qrow, const int32_t* seg_out_row,
+               const int32_t* seg_item_ptr, const int32_t* item_seg, const int32_t* item_t0,
+               const int32_t* item_t1, int32_t n_items, int32_t group, float sm_scale,
+               float* part, int32_t* counters, void* out_bf16, float* out_rec, float* out_lse,
+               void* stream);
 
-/* K5 (local / post-all-gather half): log-sum-exp merge.  Output row-group g
- * (group rows of 128) merges partial rows src_idx[grp_ptr[g] .. grp_ptr[g+1]).
- * If out_bf16 != NULL writes o bf16 [*,128] at rows out_row[g] .. +group-1;
- * if out_f32 != NULL writes the merged normalised o (f32) there instead, and
- * out_lse (optional) receives the merged lse at the same row index. */
-int fkv_merge_lse(const float* part_o, const float* part_lse, const int32_t* grp_ptr,
-                  const int32_t* src_idx, const int32_t* out_row, int32_t n_groups, int32_t group,
-                  void* out_bf16, float* out_f32, float* out_lse, void* stream);
+/* K5: log-sum-exp merge of partial records.  Output group g merges records
+ * src_idx[grp_ptr[g] .. grp_ptr[g+1]) (each `group` heads of FKV_REC floats)
+ * and writes, for heads h < group, row out_row[g] + h of any of:
+ *   out_bf16 bf16 [*,128] normalised o;  out_rec f32 [*,FKV_REC] record;
+ *   out_lse f32 [*] merged lse.
+ * Used for chunk->segment, segment->send-slot, and (after the all-gather)
+ * DP-copy->head merges.  The all-gather itself stands in for the reference's
+ * modeled allreduce (reference latency.py:94-101, simulate.py:132-133). */
+int fkv_merge_lse(const float* part, const int32_t* grp_ptr, const int32_t* src_idx,
+                  const int32_t* out_row, int32_t n_groups, int32_t group, void* out_bf16,
+                  float* out_rec, float* out_lse, void* stream);
 
 #ifdef __cplusplus
 }

@@ -37,17 +37,16 @@ _SIGS = {
                                   _vp, _vp, _vp, _vp, _vp]),
     "fkv_optimize_plan": (C.c_int, [_vp, _i32, _i32, _i32, _i32, _i32, _i32, _i64, _i64, _i32,
                                     _vp, _vp, _vp, _vp, _vp]),
-    "fkv_decode_partial": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32,
-                                     _f32, _vp, _vp, _vp]),
-    "fkv_merge_lse": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp]),
-    "fkv_score_stats": (C.c_int, [_vp, _vp, _i32, _i32, _i32, _i32, _i32, _f32, _vp, _i32, _vp]),
-    "fkv_score_columns": (C.c_int, [_vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _f32, _i32,
-                                    _vp, _i32, _vp]),
-    "fkv_ada_budgets": (C.c_int, [_vp, _i32, _i32, _i32, _i32, _i32, _i32, _f32, _vp, _vp, _i32,
-                                  _vp]),
-    "fkv_topk_select": (C.c_int, [_vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _i32, _vp]),
-    "fkv_compact": (C.c_int, [_vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _vp]),
-    "fkv_workspace_bytes": (C.c_int64, [_i32, _i32, _i32, _i32]),
+    "fkv_decode": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32,
+                             _f32, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "fkv_merge_lse": (C.c_int, [_vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp]),
+    "fkv_snapkv_score": (C.c_int, [_vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _f32, _vp, _vp,
+                                   _vp]),
+    "fkv_score_workspace_bytes": (C.c_int64, [_i32, _i32, _i32, _i32, _i32]),
+    "fkv_ada_budgets": (C.c_int, [_vp, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _vp]),
+    "fkv_topk_select": (C.c_int, [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _vp]),
+    "fkv_compact": (C.c_int, [_vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _vp,
+                              _vp]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -79,6 +79,7 @@ class LayerCache:
     item_t1: torch.Tensor
     grp_ptr: torch.Tensor
     src_idx: torch.Tensor
+    counters: torch.Tensor
     host: dict = field(default_factory=dict, repr=False)
 
     @property
@@ -132,6 +133,34 @@ class LayerCache:
             seg_len=i32(seg_len), seg_qrow=i32(seg_qrow), seg_out_row=i32(seg_out_row),
             item_seg=i32(item_seg), item_t0=i32(t0), item_t1=i32(t1),
             grp_ptr=i32(ptr), src_idx=i32(np.arange(ptr[-1])),
+            counters=torch.zeros(max(len(seg_len), 1), dtype=torch.int32, device=dev),
             host={"seg_len": seg_len, "seg_row0": row0, "chunk": chunk,
+                  "seg_qrow": np.asarray(seg_qrow), "seg_out_row": np.asarray(seg_out_row)},
+        )
+
+    @staticmethod
+    def view(k: torch.Tensor, v: torch.Tensor, seg_row0, seg_len, seg_qrow, seg_out_row,
+             group: int, chunk: int | None = None) -> "LayerCache":
+        """A segment table over existing storage (e.g. the DP copies / shards
+        of a base cache: each copy is a 16-aligned sub-range of its head's
+        rows).  No data moves."""
+        seg_row0 = np.asarray(seg_row0, dtype=np.int64)
+        seg_len = np.asarray(seg_len, dtype=np.int64)
+        if np.any(seg_row0 % 16):
+            raise ValueError("segment starts must be multiples of 16 rows")
+        chunk = chunk or choose_chunk(seg_len)
+        item_seg, t0, t1, ptr = plan_items(seg_len, chunk)
+        dev = k.device
+
+        def i32(a):
+            return torch.as_tensor(np.ascontiguousarray(a, dtype=np.int32), device=dev)
+
+        return LayerCache(
+            k=k, v=v, group=int(group), seg_row0=torch.as_tensor(seg_row0, device=dev),
+            seg_len=i32(seg_len), seg_qrow=i32(seg_qrow), seg_out_row=i32(seg_out_row),
+            item_seg=i32(item_seg), item_t0=i32(t0), item_t1=i32(t1), grp_ptr=i32(ptr),
+            src_idx=i32(np.arange(ptr[-1])),
+            counters=torch.zeros(max(len(seg_len), 1), dtype=torch.int32, device=dev),
+            host={"seg_len": seg_len, "seg_row0": seg_row0, "chunk": chunk,
                   "seg_qrow": np.asarray(seg_qrow), "seg_out_row": np.asarray(seg_out_row)},
         )

@@ -34,26 +34,41 @@ constexpr int kSmemBytes = kWarps * kWarpSmem;           // 96 KiB
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 
+struct DecodeParams {
+  const __nv_bfloat16* q;
+  const __nv_bfloat16* k;
+  const __nv_bfloat16* v;
+  const int64_t* seg_row0;
+  const int32_t* seg_len;
+  const int32_t* seg_qrow;
+  const int32_t* seg_out_row;
+  const int32_t* seg_item_ptr;
+  const int32_t* item_seg;
+  const int32_t* item_t0;
+  const int32_t* item_t1;
+  float scale_log2;
+  float* part;        // [n_items, G, FKV_REC] partial records (multi-item segments)
+  int32_t* counters;  // [n_seg] arrival counters, zero between launches (self-resetting)
+  __nv_bfloat16* out_bf16;
+  float* out_rec;
+  float* out_lse;
+};
+
 template <int G>
-__global__ void __launch_bounds__(kWarps * 32, 2)
-    decode_partial_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ kc,
-                          const __nv_bfloat16* __restrict__ vc, const int64_t* __restrict__ seg_row0,
-                          const int32_t* __restrict__ seg_len, const int32_t* __restrict__ seg_qrow,
-                          const int32_t* __restrict__ item_seg, const int32_t* __restrict__ item_t0,
-                          const int32_t* __restrict__ item_t1, float scale_log2,
-                          float* __restrict__ part_o, float* __restrict__ part_lse) {
+__global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodeParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bars[kWarps][kStages];
+  __shared__ int s_last;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int item = blockIdx.x;
-  const int seg = item_seg[item];
-  const int t0 = item_t0[item];
-  const int t1 = min(item_t1[item], seg_len[seg]);
-  const int64_t row0 = seg_row0[seg];
-  const __nv_bfloat16* kseg = kc + row0 * FKV_HEAD_DIM;
-  const __nv_bfloat16* vseg = vc + row0 * FKV_HEAD_DIM;
+  const int seg = p.item_seg[item];
+  const int t0 = p.item_t0[item];
+  const int t1 = min(p.item_t1[item], p.seg_len[seg]);
+  const int64_t row0 = p.seg_row0[seg];
+  const __nv_bfloat16* kseg = p.k + row0 * FKV_HEAD_DIM;
+  const __nv_bfloat16* vseg = p.v + row0 * FKV_HEAD_DIM;
 
   const int n_tiles = t1 > t0 ? (t1 - t0 + kTileTok - 1) / kTileTok : 0;
   const int my_tiles = n_tiles > warp ? (n_tiles - warp + kWarps - 1) / kWarps : 0;
@@ -84,7 +99,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
     const int n = lane >> 2;
     const int kq = 2 * (lane & 3);
     if (n < G) {
-      const __nv_bfloat16* qr = q + static_cast<int64_t>(seg_qrow[seg] + n) * FKV_HEAD_DIM;
+      const __nv_bfloat16* qr = p.q + static_cast<int64_t>(p.seg_qrow[seg] + n) * FKV_HEAD_DIM;
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) {
         qb[kk][0] = *reinterpret_cast<const uint32_t*>(qr + 16 * kk + kq);
@@ -119,10 +134,10 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
       mma_bf16_16816(sc, a0, a1, a2, a3, qb[kk][0], qb[kk][1]);
     }
     const int ta = tok_base + (lane >> 2);
-    const float s0 = ta < t1 ? sc[0] * scale_log2 : -CUDART_INF_F;
-    const float s1 = ta < t1 ? sc[1] * scale_log2 : -CUDART_INF_F;
-    const float s2 = ta + 8 < t1 ? sc[2] * scale_log2 : -CUDART_INF_F;
-    const float s3 = ta + 8 < t1 ? sc[3] * scale_log2 : -CUDART_INF_F;
+    const float s0 = ta < t1 ? sc[0] * p.scale_log2 : -CUDART_INF_F;
+    const float s1 = ta < t1 ? sc[1] * p.scale_log2 : -CUDART_INF_F;
+    const float s2 = ta + 8 < t1 ? sc[2] * p.scale_log2 : -CUDART_INF_F;
+    const float s3 = ta + 8 < t1 ? sc[3] * p.scale_log2 : -CUDART_INF_F;
     float mx0 = fmaxf(s0, s2), mx1 = fmaxf(s1, s3);
 #pragma unroll
     for (int off = 4; off < 32; off <<= 1) {
@@ -191,6 +206,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
 
   // ---- cross-warp log-sum-exp combine: thread = one head_dim column
   const int d = threadIdx.x;
+  float on[G], ls[G];
 #pragma unroll
   for (int g = 0; g < G; ++g) {
     float M = -CUDART_INF_F;
@@ -207,112 +223,188 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
         o += b[g * FKV_HEAD_DIM + d] * f;
       }
     }
-    const int64_t orow = static_cast<int64_t>(item) * G + g;
-    part_o[orow * FKV_HEAD_DIM + d] = L > 0.f ? o / L : 0.f;
-    if (d == 0) part_lse[orow] = L > 0.f ? (M + log2f(L)) * kLn2 : -CUDART_INF_F;
+    on[g] = L > 0.f ? o / L : 0.f;
+    ls[g] = L > 0.f ? (M + log2f(L)) * kLn2 : -CUDART_INF_F;
   }
-}
 
-template <int G>
-__global__ void __launch_bounds__(128)
-    merge_lse_kernel(const float* __restrict__ part_o, const float* __restrict__ part_lse,
-                     const int32_t* __restrict__ grp_ptr, const int32_t* __restrict__ src_idx,
-                     const int32_t* __restrict__ out_row, __nv_bfloat16* __restrict__ out_bf16,
-                     float* __restrict__ out_f32, float* __restrict__ out_lse) {
-  const int grp = blockIdx.x;
-  const int d = threadIdx.x;
-  const int i0 = grp_ptr[grp], i1 = grp_ptr[grp + 1];
-  const int64_t row = out_row[grp];
+  const bool fused = p.out_bf16 || p.out_rec || p.out_lse;
+  const int i0 = p.seg_item_ptr[seg];
+  const int n_it = p.seg_item_ptr[seg + 1] - i0;
+  if (!fused || n_it > 1) {
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      float* rec = p.part + (static_cast<int64_t>(item) * G + g) * FKV_REC;
+      rec[d] = on[g];
+      if (d == 0) rec[FKV_HEAD_DIM] = ls[g];
+    }
+  }
+  if (!fused) return;
+  if (n_it > 1) {
+    // last-arriving CTA of the segment merges every chunk's record (K5 fused)
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(&p.counters[seg], 1) == n_it - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    // Latency-tolerant merge: all (item, head) lse values are fetched in one
+    // parallel round trip, weights are formed in shared memory, then every
+    // thread streams its head_dim column of all records with independent loads.
+    float* s_w = reinterpret_cast<float*>(smem);  // [n_it][G] weights (stage buffers are free)
+    float* s_lse = s_w + n_it * G;                // [G] merged lse
+    for (int x = threadIdx.x; x < n_it * G; x += blockDim.x)
+      s_w[x] = __ldcg(p.part + (static_cast<int64_t>(i0) * G + x) * FKV_REC + FKV_HEAD_DIM);
+    __syncthreads();
+    if (threadIdx.x < G) {
+      const int g = threadIdx.x;
+      float M = -CUDART_INF_F;
+      for (int i = 0; i < n_it; ++i) M = fmaxf(M, s_w[i * G + g]);
+      float S = 0.f;
+      if (M != -CUDART_INF_F)
+        for (int i = 0; i < n_it; ++i) S += __expf(s_w[i * G + g] - M);
+      const float inv = S > 0.f ? 1.f / S : 0.f;
+      for (int i = 0; i < n_it; ++i)
+        s_w[i * G + g] = M != -CUDART_INF_F ? __expf(s_w[i * G + g] - M) * inv : 0.f;
+      s_lse[g] = S > 0.f ? M + __logf(S) : -CUDART_INF_F;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int g = 0; g < G; ++g) on[g] = 0.f;
+    const float* base = p.part + static_cast<int64_t>(i0) * G * FKV_REC + d;
+#pragma unroll 2
+    for (int i = 0; i < n_it; ++i) {
+      float v[G];
+#pragma unroll
+      for (int g = 0; g < G; ++g) v[g] = __ldcg(base + (i * G + g) * FKV_REC);
+#pragma unroll
+      for (int g = 0; g < G; ++g) on[g] = fmaf(s_w[i * G + g], v[g], on[g]);
+    }
+#pragma unroll
+    for (int g = 0; g < G; ++g) ls[g] = s_lse[g];
+    if (threadIdx.x == 0) p.counters[seg] = 0;  // ready for the next launch / graph replay
+  }
+  const int64_t orow = p.seg_out_row[seg];
 #pragma unroll
   for (int g = 0; g < G; ++g) {
-    float M = -CUDART_INF_F;
-    for (int i = i0; i < i1; ++i) M = fmaxf(M, part_lse[static_cast<int64_t>(src_idx[i]) * G + g]);
-    float S = 0.f, o = 0.f;
-    if (M != -CUDART_INF_F) {
-      for (int i = i0; i < i1; ++i) {
-        const int64_t r = static_cast<int64_t>(src_idx[i]) * G + g;
-        const float w = __expf(part_lse[r] - M);
-        S += w;
-        o += w * part_o[r * FKV_HEAD_DIM + d];
-      }
+    if (p.out_bf16) p.out_bf16[(orow + g) * FKV_HEAD_DIM + d] = __float2bfloat16_rn(on[g]);
+    if (p.out_rec) {
+      p.out_rec[(orow + g) * FKV_REC + d] = on[g];
+      if (d == 0) p.out_rec[(orow + g) * FKV_REC + FKV_HEAD_DIM] = ls[g];
     }
-    const float ov = S > 0.f ? o / S : 0.f;
-    if (out_bf16) out_bf16[(row + g) * FKV_HEAD_DIM + d] = __float2bfloat16_rn(ov);
-    if (out_f32) out_f32[(row + g) * FKV_HEAD_DIM + d] = ov;
-    if (out_lse && d == 0) out_lse[row + g] = S > 0.f ? M + __logf(S) : -CUDART_INF_F;
+    if (p.out_lse && d == 0) p.out_lse[orow + g] = ls[g];
   }
 }
 
+// K5 standalone (after the all-gather): warp g of the CTA merges head g of
+// one output group in a single online-LSE pass; lane = 4 head_dim columns.
 template <int G>
-int launch_decode(const void* q, const void* k, const void* v, const int64_t* seg_row0,
-                  const int32_t* seg_len, const int32_t* seg_qrow, const int32_t* item_seg,
-                  const int32_t* item_t0, const int32_t* item_t1, int n_items, float sm_scale,
-                  float* part_o, float* part_lse, cudaStream_t st) {
-  static bool configured = false;  // idempotent; attribute set is per-function
+__global__ void __launch_bounds__(G * 32)
+    merge_lse_kernel(const float* __restrict__ part, const int32_t* __restrict__ grp_ptr,
+                     const int32_t* __restrict__ src_idx, const int32_t* __restrict__ out_row,
+                     __nv_bfloat16* __restrict__ out_bf16, float* __restrict__ out_rec,
+                     float* __restrict__ out_lse) {
+  const int grp = blockIdx.x;
+  const int g = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i0 = grp_ptr[grp], i1 = grp_ptr[grp + 1];
+  float m = -CUDART_INF_F, S = 0.f;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int i = i0; i < i1; ++i) {
+    const float* rec = part + (static_cast<int64_t>(src_idx[i]) * G + g) * FKV_REC;
+    const float l = rec[FKV_HEAD_DIM];
+    if (l == -CUDART_INF_F) continue;
+    const float4 o = reinterpret_cast<const float4*>(rec)[lane];
+    const float nm = fmaxf(m, l);
+    const float a = __expf(m - nm), b = __expf(l - nm);
+    S = S * a + b;
+    acc.x = acc.x * a + o.x * b;
+    acc.y = acc.y * a + o.y * b;
+    acc.z = acc.z * a + o.z * b;
+    acc.w = acc.w * a + o.w * b;
+    m = nm;
+  }
+  const float inv = S > 0.f ? 1.f / S : 0.f;
+  acc.x *= inv;
+  acc.y *= inv;
+  acc.z *= inv;
+  acc.w *= inv;
+  const float lse = S > 0.f ? m + __logf(S) : -CUDART_INF_F;
+  const int64_t row = static_cast<int64_t>(out_row[grp]) + g;
+  if (out_bf16) {
+    __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(out_bf16 + row * FKV_HEAD_DIM) + 2 * lane;
+    ob[0] = __floats2bfloat162_rn(acc.x, acc.y);
+    ob[1] = __floats2bfloat162_rn(acc.z, acc.w);
+  }
+  if (out_rec) {
+    reinterpret_cast<float4*>(out_rec + row * FKV_REC)[lane] = acc;
+    if (lane == 0) out_rec[row * FKV_REC + FKV_HEAD_DIM] = lse;
+  }
+  if (out_lse && lane == 0) out_lse[row] = lse;
+}
+
+template <int G>
+int launch_decode(const DecodeParams& p, int n_items, cudaStream_t st) {
+  static bool configured = false;  // attribute set is per-function, idempotent
   if (!configured) {
-    if (int rc = cuda_check(cudaFuncSetAttribute(decode_partial_kernel<G>,
+    if (int rc = cuda_check(cudaFuncSetAttribute(decode_kernel<G>,
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  kSmemBytes),
                             "decode smem attribute"))
       return rc;
     configured = true;
   }
-  decode_partial_kernel<G><<<n_items, kWarps * 32, kSmemBytes, st>>>(
-      static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(k),
-      static_cast<const __nv_bfloat16*>(v), seg_row0, seg_len, seg_qrow, item_seg, item_t0,
-      item_t1, sm_scale * kLog2e, part_o, part_lse);
-  return cuda_check(cudaGetLastError(), "decode_partial launch");
+  decode_kernel<G><<<n_items, kWarps * 32, kSmemBytes, st>>>(p);
+  return cuda_check(cudaGetLastError(), "decode launch");
 }
 
 }  // namespace
 }  // namespace fkv
 
-extern "C" int fkv_decode_partial(const void* q, const void* k, const void* v,
-                                  const int64_t* seg_row0, const int32_t* seg_len,
-                                  const int32_t* seg_qrow, const int32_t* item_seg,
-                                  const int32_t* item_t0, const int32_t* item_t1, int32_t n_items,
-                                  int32_t group, float sm_scale, float* part_o, float* part_lse,
-                                  void* stream) {
+extern "C" int fkv_decode(const void* q, const void* k, const void* v, const int64_t* seg_row0,
+                          const int32_t* seg_len, const int32_t* seg_qrow,
+                          const int32_t* seg_out_row, const int32_t* seg_item_ptr,
+                          const int32_t* item_seg, const int32_t* item_t0, const int32_t* item_t1,
+                          int32_t n_items, int32_t group, float sm_scale, float* part,
+                          int32_t* counters, void* out_bf16, float* out_rec, float* out_lse,
+                          void* stream) {
   using namespace fkv;
   if (n_items < 0) return set_error(FKV_ERR_INVALID, "n_items < 0");
   if (n_items == 0) return FKV_OK;
+  const bool fused = out_bf16 || out_rec || out_lse;
   if (!q || !k || !v || !seg_row0 || !seg_len || !seg_qrow || !item_seg || !item_t0 || !item_t1 ||
-      !part_o || !part_lse)
-    return set_error(FKV_ERR_INVALID, "fkv_decode_partial: null pointer");
+      !part || (fused && (!seg_out_row || !seg_item_ptr || !counters)))
+    return set_error(FKV_ERR_INVALID, "fkv_decode: null pointer");
   if ((reinterpret_cast<uintptr_t>(k) | reinterpret_cast<uintptr_t>(v)) & 15)
-    return set_error(FKV_ERR_INVALID, "fkv_decode_partial: cache not 16-byte aligned");
+    return set_error(FKV_ERR_INVALID, "fkv_decode: cache not 16-byte aligned");
+  DecodeParams p{static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(k),
+                 static_cast<const __nv_bfloat16*>(v), seg_row0, seg_len, seg_qrow, seg_out_row,
+                 seg_item_ptr, item_seg, item_t0, item_t1, sm_scale * kLog2e, part, counters,
+                 static_cast<__nv_bfloat16*>(out_bf16), out_rec, out_lse};
   auto st = static_cast<cudaStream_t>(stream);
   switch (group) {
-    case 4:
-      return launch_decode<4>(q, k, v, seg_row0, seg_len, seg_qrow, item_seg, item_t0, item_t1,
-                              n_items, sm_scale, part_o, part_lse, st);
-    case 8:
-      return launch_decode<8>(q, k, v, seg_row0, seg_len, seg_qrow, item_seg, item_t0, item_t1,
-                              n_items, sm_scale, part_o, part_lse, st);
-    default:
-      return set_error(FKV_ERR_INVALID, "fkv_decode_partial: group must be 4 or 8");
+    case 4: return launch_decode<4>(p, n_items, st);
+    case 8: return launch_decode<8>(p, n_items, st);
+    default: return set_error(FKV_ERR_INVALID, "fkv_decode: group must be 4 or 8");
   }
 }
 
-extern "C" int fkv_merge_lse(const float* part_o, const float* part_lse, const int32_t* grp_ptr,
-                             const int32_t* src_idx, const int32_t* out_row, int32_t n_groups,
-                             int32_t group, void* out_bf16, float* out_f32, float* out_lse,
-                             void* stream) {
+extern "C" int fkv_merge_lse(const float* part, const int32_t* grp_ptr, const int32_t* src_idx,
+                             const int32_t* out_row, int32_t n_groups, int32_t group,
+                             void* out_bf16, float* out_rec, float* out_lse, void* stream) {
   using namespace fkv;
   if (n_groups < 0) return set_error(FKV_ERR_INVALID, "n_groups < 0");
   if (n_groups == 0) return FKV_OK;
-  if (!part_o || !part_lse || !grp_ptr || !src_idx || !out_row || (!out_bf16 && !out_f32))
+  if (!part || !grp_ptr || !src_idx || !out_row || (!out_bf16 && !out_rec && !out_lse))
     return set_error(FKV_ERR_INVALID, "fkv_merge_lse: null pointer");
   auto st = static_cast<cudaStream_t>(stream);
   auto ob = static_cast<__nv_bfloat16*>(out_bf16);
   switch (group) {
     case 4:
-      merge_lse_kernel<4><<<n_groups, 128, 0, st>>>(part_o, part_lse, grp_ptr, src_idx, out_row,
-                                                    ob, out_f32, out_lse);
+      merge_lse_kernel<4><<<n_groups, 4 * 32, 0, st>>>(part, grp_ptr, src_idx, out_row, ob, out_rec,
+                                                    out_lse);
       break;
     case 8:
-      merge_lse_kernel<8><<<n_groups, 128, 0, st>>>(part_o, part_lse, grp_ptr, src_idx, out_row,
-                                                    ob, out_f32, out_lse);
+      merge_lse_kernel<8><<<n_groups, 8 * 32, 0, st>>>(part, grp_ptr, src_idx, out_row, ob, out_rec,
+                                                    out_lse);
       break;
     default:
       return set_error(FKV_ERR_INVALID, "fkv_merge_lse: group must be 4 or 8");

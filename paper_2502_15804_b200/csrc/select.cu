@@ -1,0 +1,263 @@
+// A18 Ada cross-head budget split + K2 per-head top-k selection.
+//
+// No reference implementation exists (the paper used KVPress
+// AdaKV).  Definitions and tie rules are fixed in DESIGN.md
+// "Algorithm definitions" and restated in oracle/kv.py:
+//   per-head order  (score desc, token asc)
+//   global order    (score desc, head asc, token asc)
+// Both are made total by a 64-bit composite key
+//   key64 = orderable(score) << 32 | (0xffffffff - index)
+// (index = token, or head * n + token for the global order), so a radix
+// select over key64 returns exactly k elements and results are exact
+// functions of the fp32 score tensor -- bit-exact against the oracle fed the
+// same scores.
+//
+// Radix select: one CTA, MSB-first 8-bit digits, warp-aggregated
+// shared-memory histograms (__match_any_sync: the top digits of float keys
+// are nearly all equal, so naive per-thread atomics would serialise), early
+// exit when the threshold bucket is taken whole.
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace fkv {
+namespace {
+
+constexpr int kThreads = 1024;
+constexpr uint64_t kNone = ~0ull;
+
+__device__ __forceinline__ uint32_t orderable(float f) {
+  const uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+__device__ __forceinline__ uint64_t compose(float s, uint32_t index) {
+  return (static_cast<uint64_t>(orderable(s)) << 32) | (0xffffffffu - index);
+}
+
+struct SelectSmem {
+  uint32_t hist[256];
+  uint32_t digit, above;
+  uint32_t warp_tot[32];
+  uint64_t tau_head[64];
+  uint32_t count_head[64];
+};
+
+// Threshold tau such that exactly k of the valid elements have key >= tau
+// (1 <= k <= #valid).  key_of(i, &key) -> valid.
+template <class KeyOf>
+__device__ uint64_t cta_select_kth(KeyOf key_of, int n, uint32_t k, SelectSmem& sm) {
+  uint64_t prefix = 0, mask = 0;
+  uint32_t need = k;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) sm.hist[i] = 0;
+    __syncthreads();
+    for (int base = 0; base < n; base += blockDim.x) {
+      const int i = base + threadIdx.x;
+      uint64_t key = 0;
+      const bool ok = i < n && key_of(i, key) && (key & mask) == prefix;
+      const uint32_t d = ok ? static_cast<uint32_t>(key >> shift) & 255u : 256u;
+      const uint32_t peers = __match_any_sync(0xffffffffu, d);
+      if (ok && lane == __ffs(peers) - 1) atomicAdd(&sm.hist[d], __popc(peers));
+    }
+    __syncthreads();
+    if (warp == 0) {
+      // lane L owns bins [8L, 8L+8); find the bin holding the need-th largest
+      uint32_t local = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) local += sm.hist[8 * lane + j];
+      uint32_t incl = local;  // inclusive suffix sum over lanes >= this one
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t v = __shfl_down_sync(0xffffffffu, incl, off);
+        if (lane + off < 32) incl += v;
+      }
+      const uint32_t suffix = incl - local;
+      if (suffix < need && suffix + local >= need) {
+        uint32_t acc = suffix;
+        for (int j = 7; j >= 0; --j) {
+          const uint32_t c = sm.hist[8 * lane + j];
+          if (acc + c >= need) {
+            sm.digit = 8 * lane + j;
+            sm.above = acc;
+            break;
+          }
+          acc += c;
+        }
+      }
+    }
+    __syncthreads();
+    const uint32_t d = sm.digit;
+    need -= sm.above;
+    prefix |= static_cast<uint64_t>(d) << shift;
+    mask |= 255ull << shift;
+    const bool whole = sm.hist[d] == need;
+    __syncthreads();
+    if (whole) return prefix;
+  }
+  return prefix;
+}
+
+// Exclusive block scan of a 0/1 flag (one per thread), returns the total.
+__device__ uint32_t block_flag_scan(bool flag, uint32_t& before, SelectSmem& sm) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t ballot = __ballot_sync(0xffffffffu, flag);
+  const uint32_t in_warp = __popc(ballot & ((1u << lane) - 1u));
+  if (lane == 0) sm.warp_tot[warp] = __popc(ballot);
+  __syncthreads();
+  uint32_t warp_base = 0, total = 0;
+  const int nw = blockDim.x >> 5;
+  for (int w = 0; w < nw; ++w) {
+    const uint32_t t = sm.warp_tot[w];
+    if (w < warp) warp_base += t;
+    total += t;
+  }
+  __syncthreads();
+  before = warp_base + in_warp;
+  return total;
+}
+
+__device__ uint32_t block_sum(uint32_t v, SelectSmem& sm) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  if (lane == 0) sm.warp_tot[warp] = v;
+  __syncthreads();
+  uint32_t total = 0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) total += sm.warp_tot[w];
+  __syncthreads();
+  return total;
+}
+
+// ---------------------------------------------------------------- A18 ----
+// grid = Bt, one CTA per request.  scores f32 [Bt, Hkv, n] (pooled).
+__global__ void __launch_bounds__(kThreads)
+    ada_budgets_kernel(const float* __restrict__ scores, int hkv, int n, int window, int floor_k,
+                       int rest_total, int32_t* __restrict__ budgets) {
+  __shared__ SelectSmem sm;
+  const int b = blockIdx.x;
+  const float* s = scores + static_cast<int64_t>(b) * hkv * n;
+  // phase 1: per-head floors (top floor_k by (score desc, token asc))
+  for (int h = 0; h < hkv; ++h) {
+    uint64_t tau = kNone;
+    if (floor_k > 0) {
+      const float* sh = s + static_cast<int64_t>(h) * n;
+      tau = cta_select_kth(
+          [&](int i, uint64_t& key) {
+            key = compose(sh[i], static_cast<uint32_t>(i));
+            return true;
+          },
+          n, static_cast<uint32_t>(floor_k), sm);
+    }
+    if (threadIdx.x == 0) sm.tau_head[h] = tau;
+    __syncthreads();
+  }
+  auto in_floor = [&](int h, int t) -> bool {
+    const uint64_t tau = sm.tau_head[h];
+    return tau != kNone && compose(s[static_cast<int64_t>(h) * n + t], static_cast<uint32_t>(t)) >= tau;
+  };
+  // phase 2: global top rest_total over the non-floor elements
+  const int total = hkv * n;
+  uint64_t gtau = kNone;
+  if (rest_total > 0) {
+    gtau = cta_select_kth(
+        [&](int i, uint64_t& key) {
+          const int h = i / n, t = i - h * n;
+          if (in_floor(h, t)) return false;
+          key = compose(s[i], static_cast<uint32_t>(i));
+          return true;
+        },
+        total, static_cast<uint32_t>(rest_total), sm);
+  }
+  // phase 3: per-head counts of globally chosen elements
+  for (int h = 0; h < hkv; ++h) {
+    uint32_t c = 0;
+    if (gtau != kNone) {
+      for (int t = threadIdx.x; t < n; t += blockDim.x) {
+        const int i = h * n + t;
+        if (!in_floor(h, t) && compose(s[i], static_cast<uint32_t>(i)) >= gtau) ++c;
+      }
+    }
+    const uint32_t tot = block_sum(c, sm);
+    if (threadIdx.x == 0) budgets[b * hkv + h] = window + floor_k + static_cast<int32_t>(tot);
+  }
+}
+
+// ----------------------------------------------------------------- K2 ----
+// grid = Bt * Hkv.  Writes offsets[bh] (exclusive prefix of budgets) and the
+// selected tokens of head (b,h) ascending, then the window tokens n..n+w-1.
+__global__ void __launch_bounds__(kThreads)
+    topk_select_kernel(const float* __restrict__ scores, const int32_t* __restrict__ budgets,
+                       int n, int window, int64_t* __restrict__ offsets,
+                       int32_t* __restrict__ idx) {
+  __shared__ SelectSmem sm;
+  const int bh = blockIdx.x;
+  // offset = sum of budgets before this head
+  uint32_t part = 0;
+  for (int j = threadIdx.x; j < bh; j += blockDim.x) part += static_cast<uint32_t>(budgets[j]);
+  const int64_t off = block_sum(part, sm);
+  if (threadIdx.x == 0) {
+    offsets[bh] = off;
+    if (bh == gridDim.x - 1) offsets[bh + 1] = off + budgets[bh];
+  }
+  const int k = budgets[bh] - window;
+  const float* s = scores + static_cast<int64_t>(bh) * n;
+  int32_t* out = idx + off;
+  if (k > 0) {
+    const uint64_t tau =
+        k >= n ? 0ull
+               : cta_select_kth(
+                     [&](int i, uint64_t& key) {
+                       key = compose(s[i], static_cast<uint32_t>(i));
+                       return true;
+                     },
+                     n, static_cast<uint32_t>(k), sm);
+    uint32_t written = 0;
+    for (int base = 0; base < n; base += blockDim.x) {
+      const int t = base + threadIdx.x;
+      const bool take = t < n && compose(s[t], static_cast<uint32_t>(t)) >= tau;
+      uint32_t before;
+      const uint32_t tot = block_flag_scan(take, before, sm);
+      if (take) out[written + before] = t;
+      written += tot;
+    }
+  }
+  for (int i = threadIdx.x; i < window; i += blockDim.x) out[max(k, 0) + i] = n + i;
+}
+
+}  // namespace
+}  // namespace fkv
+
+extern "C" int fkv_ada_budgets(const float* scores, int32_t batch, int32_t hkv, int32_t n,
+                               int32_t budget, int32_t window, int32_t floor_k, int32_t* budgets,
+                               void* stream) {
+  using namespace fkv;
+  if (!scores || !budgets) return set_error(FKV_ERR_INVALID, "fkv_ada_budgets: null pointer");
+  if (batch < 0 || hkv < 1 || hkv > 64 || n < 0 || window < 0 || floor_k < 0)
+    return set_error(FKV_ERR_INVALID, "fkv_ada_budgets: bad sizes");
+  const int sel = budget - window;
+  if (sel < 0 || sel > n || floor_k > sel)
+    return set_error(FKV_ERR_INVALID, "fkv_ada_budgets: need 0 <= floor <= budget-window <= n");
+  if (static_cast<int64_t>(hkv) * n >= 0x7fffffffLL)
+    return set_error(FKV_ERR_INVALID, "fkv_ada_budgets: Hkv * n too large");
+  if (batch == 0) return FKV_OK;
+  const int rest = hkv * sel - hkv * floor_k;
+  ada_budgets_kernel<<<batch, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+      scores, hkv, n, window, floor_k, rest, budgets);
+  return cuda_check(cudaGetLastError(), "ada_budgets launch");
+}
+
+extern "C" int fkv_topk_select(const float* scores, const int32_t* budgets, int32_t batch,
+                               int32_t hkv, int32_t n, int32_t window, int64_t* offsets,
+                               int32_t* idx, void* stream) {
+  using namespace fkv;
+  if (!scores || !budgets || !offsets || !idx)
+    return set_error(FKV_ERR_INVALID, "fkv_topk_select: null pointer");
+  if (batch < 0 || hkv < 1 || n < 0 || window < 0)
+    return set_error(FKV_ERR_INVALID, "fkv_topk_select: bad sizes");
+  if (batch == 0) return FKV_OK;
+  topk_select_kernel<<<batch * hkv, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+      scores, budgets, n, window, offsets, idx);
+  return cuda_check(cudaGetLastError(), "topk_select launch");
+}

@@ -1,0 +1,84 @@
+"""Decode step of the attention sub-stack on one rank (SURVEY §8d metric).
+
+For every layer: K4 over this rank's segments (its fused K5 merging chunks
+straight into fixed send slots) ->
+all-gather of the slot records across the TP group -> K5 over the DP copies
+of each head -> o [Bt, Hq, 128] bf16 on every rank.  At tp == 1 K5 writes o
+directly.  The per-layer order is the synchronous barrier model of the
+reference simulator (reference simulate.py:118-136): the all-gather is the
+layer barrier.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import ops
+from .cache import LayerCache
+from .sharding import FinalMerge, LayerShard
+
+
+def rank_caches(shards: list[LayerShard], bt: int, hq: int, group: int, tp: int, device,
+                *, base: list[LayerCache] | None = None, base_index=None, fill: str = "random",
+                seed: int = 0) -> list[LayerCache]:
+    """Per-layer caches of one rank.  With ``base`` (full per-head caches, one
+    segment per (b, h) in b-major order) the rank's segments are views into
+    it (DP copies = 16-aligned sub-ranges); otherwise fresh storage filled
+    with ``fill``."""
+    hkv = hq // group
+    out = []
+    gen = torch.Generator(device=device).manual_seed(seed)
+    for l, sh in enumerate(shards):
+        qrow = sh.seg_b * hq + sh.seg_h * group
+        out_row = np.arange(sh.n_segments) if tp > 1 else qrow
+        lens = sh.seg_hi - sh.seg_lo
+        if base is not None:
+            b0 = base[l].host["seg_row0"]
+            row0 = b0[sh.seg_b * hkv + sh.seg_h] + sh.seg_lo
+            out.append(LayerCache.view(base[l].k, base[l].v, row0, lens, qrow, out_row, group))
+        else:
+            out.append(LayerCache.allocate(lens, qrow, out_row, group, device, fill=fill,
+                                           generator=gen))
+    return out
+
+
+class StackDecoder:
+    def __init__(self, caches: list[LayerCache], finals: list[FinalMerge] | None, *, tp: int,
+                 bt: int, hq: int, group: int, process_group=None):
+        self.caches = caches
+        self.tp = tp
+        self.group = group
+        self.bt, self.hq = bt, hq
+        self.pg = process_group
+        dev = caches[0].k.device
+        self.ws = [ops.DecodeWorkspace(c) for c in caches]
+        self.send, self.recv, self.final = [], [], []
+        if tp > 1:
+            for c, f in zip(caches, finals):
+                self.send.append(torch.zeros((f.slots, group, ops.REC), dtype=torch.float32, device=dev))
+                self.recv.append(torch.zeros((tp * f.slots, group, ops.REC), dtype=torch.float32, device=dev))
+                self.final.append(tuple(torch.as_tensor(x, device=dev) for x in (f.grp_ptr, f.src_idx, f.out_row)))
+        self.kernel_launches_per_step = len(caches) * (2 if tp > 1 else 1)
+
+    def layer(self, l: int, q: torch.Tensor, out: torch.Tensor, out_lse: torch.Tensor | None = None):
+        c = self.caches[l]
+        if self.tp == 1:
+            ops.decode_into(q, c, self.ws[l], out_bf16=out, out_lse=out_lse)
+            return
+        ops.decode_into(q, c, self.ws[l], out_rec=self.send[l])
+        self.exchange(l)
+        ptr, src, row = self.final[l]
+        ops.merge_lse(self.recv[l], ptr, src, row, self.group, out_bf16=out, out_lse=out_lse)
+
+    def exchange(self, l: int):
+        import torch.distributed as dist
+        dist.all_gather_into_tensor(self.recv[l], self.send[l], group=self.pg)
+
+    def step(self, q_layers: torch.Tensor, out_layers: torch.Tensor):
+        """q_layers / out_layers: [L, Bt, Hq, 128] bf16."""
+        for l in range(len(self.caches)):
+            self.layer(l, q_layers[l], out_layers[l])
+
+    def kv_bytes(self) -> int:
+        return sum(c.kv_bytes() for c in self.caches)

@@ -43,56 +43,176 @@ def _p(t):
 
 
 # -------------------------------------------------------------- decode ----
+REC = 132  # floats per partial record (FKV_REC): o[128], lse, pad
+
+
 class DecodeWorkspace:
-    """Persistent partial-output buffers for one cache (graph-capturable)."""
+    """Persistent partial-record buffer for one cache (graph-capturable)."""
 
     def __init__(self, cache: LayerCache):
-        dev = cache.k.device
-        self.part_o = torch.empty((max(cache.n_items, 1), cache.group, HEAD_DIM), dtype=torch.float32,
-                                  device=dev)
-        self.part_lse = torch.empty((max(cache.n_items, 1), cache.group), dtype=torch.float32, device=dev)
+        self.part = torch.empty((max(cache.n_items, 1), cache.group, REC), dtype=torch.float32,
+                                device=cache.k.device)
 
 
-def decode_partial(q: torch.Tensor, cache: LayerCache, ws: DecodeWorkspace | None = None,
-                   sm_scale: float | None = None):
-    """K4: per work item (o, lse) partials.  q: bf16 [..., 128] contiguous."""
+def _decode(q, cache: LayerCache, ws: DecodeWorkspace | None, sm_scale, out_bf16, out_rec, out_lse):
     _need_cuda(q, cache.k)
     if q.dtype != torch.bfloat16 or q.shape[-1] != HEAD_DIM or not q.is_contiguous():
         raise NativeError("q must be contiguous bf16 [..., 128]")
     ws = ws or DecodeWorkspace(cache)
     scale = 1.0 / math.sqrt(HEAD_DIM) if sm_scale is None else sm_scale
-    _native.check(_lib.fkv_decode_partial(
+    _native.check(_lib.fkv_decode(
         q.data_ptr(), cache.k.data_ptr(), cache.v.data_ptr(), cache.seg_row0.data_ptr(),
-        cache.seg_len.data_ptr(), cache.seg_qrow.data_ptr(), cache.item_seg.data_ptr(),
-        cache.item_t0.data_ptr(), cache.item_t1.data_ptr(), cache.n_items, cache.group, scale,
-        ws.part_o.data_ptr(), ws.part_lse.data_ptr(), _stream()))
-    return ws.part_o, ws.part_lse
+        cache.seg_len.data_ptr(), cache.seg_qrow.data_ptr(), cache.seg_out_row.data_ptr(),
+        cache.grp_ptr.data_ptr(), cache.item_seg.data_ptr(), cache.item_t0.data_ptr(),
+        cache.item_t1.data_ptr(), cache.n_items, cache.group, scale, ws.part.data_ptr(),
+        cache.counters.data_ptr(), _p(out_bf16), _p(out_rec), _p(out_lse), _stream()))
+    return ws.part
 
 
-def merge_lse(part_o, part_lse, grp_ptr, src_idx, out_row, group: int, *, out_bf16=None,
-              out_f32=None, out_lse=None):
-    """K5: out rows out_row[g]..+group-1 <- LSE merge of partial rows
-    src_idx[grp_ptr[g]:grp_ptr[g+1]]."""
-    _need_cuda(part_o, part_lse, grp_ptr, src_idx, out_row)
+def decode_partial(q: torch.Tensor, cache: LayerCache, ws: DecodeWorkspace | None = None,
+                   sm_scale: float | None = None) -> torch.Tensor:
+    """K4 alone: one (o, lse) record per (work item, head), no merge."""
+    return _decode(q, cache, ws, sm_scale, None, None, None)
+
+
+def decode_into(q: torch.Tensor, cache: LayerCache, ws: DecodeWorkspace | None = None, *,
+                out_bf16=None, out_rec=None, out_lse=None, sm_scale: float | None = None):
+    """K4 with the fused per-segment LSE merge: segment s writes rows
+    seg_out_row[s] .. + G - 1 of the given outputs (one launch)."""
+    if out_bf16 is None and out_rec is None and out_lse is None:
+        raise NativeError("decode_into needs at least one output")
+    _decode(q, cache, ws, sm_scale, out_bf16, out_rec, out_lse)
+
+
+def merge_lse(part, grp_ptr, src_idx, out_row, group: int, *, out_bf16=None, out_rec=None,
+              out_lse=None):
+    """K5: rows out_row[g] .. +group-1 <- LSE merge of the records
+    src_idx[grp_ptr[g]:grp_ptr[g+1]] of ``part`` ([*, group, REC] f32)."""
+    _need_cuda(part, grp_ptr, src_idx, out_row)
     n_groups = int(out_row.shape[0])
     _native.check(_lib.fkv_merge_lse(
-        part_o.data_ptr(), part_lse.data_ptr(), grp_ptr.data_ptr(), src_idx.data_ptr(),
-        out_row.data_ptr(), n_groups, int(group), _p(out_bf16), _p(out_f32), _p(out_lse),
-        _stream()))
+        part.data_ptr(), grp_ptr.data_ptr(), src_idx.data_ptr(), out_row.data_ptr(), n_groups,
+        int(group), _p(out_bf16), _p(out_rec), _p(out_lse), _stream()))
 
 
 def decode(q: torch.Tensor, cache: LayerCache, *, out: torch.Tensor | None = None,
            out_lse: torch.Tensor | None = None, ws: DecodeWorkspace | None = None):
-    """Decode attention of one layer over a single-GPU cache.
+    """Decode attention of one layer over a single-GPU cache (one launch).
 
     q [Bt, Hq, 128] bf16 -> o [Bt, Hq, 128] bf16 and lse [Bt, Hq] f32
     (rows not covered by any segment are left untouched)."""
-    ws = ws or DecodeWorkspace(cache)
     if out is None:
         out = torch.empty_like(q)
     if out_lse is None:
         out_lse = torch.empty(q.shape[:-1], dtype=torch.float32, device=q.device)
-    part_o, part_lse = decode_partial(q, cache, ws)
-    merge_lse(part_o, part_lse, cache.grp_ptr, cache.src_idx, cache.seg_out_row, cache.group,
-              out_bf16=out, out_lse=out_lse)
+    decode_into(q, cache, ws, out_bf16=out, out_lse=out_lse)
     return out, out_lse
+
+
+# ------------------------------------------------- compression (prefill) ----
+def score(q_win: torch.Tensor, k: torch.Tensor, window: int | None = None, pool_k: int = 7,
+          sm_scale: float | None = None, workspace: torch.Tensor | None = None) -> torch.Tensor:
+    """K1: Ada-SnapKV observation-window scores (tcgen05 two-pass kernel).
+
+    q_win bf16 [Bt, Hq, w, 128] (the last w query positions), k bf16
+    [Bt, Hkv, T, 128] -> pooled scores f32 [Bt, Hkv, T - w]; G*w must be 128
+    or 256 (Llama-3.1-8B: G=4, 70B: G=8, with w=32)."""
+    _need_cuda(q_win, k)
+    if q_win.dtype != torch.bfloat16 or k.dtype != torch.bfloat16 or q_win.shape[-1] != HEAD_DIM \
+            or k.shape[-1] != HEAD_DIM or not (q_win.is_contiguous() and k.is_contiguous()):
+        raise NativeError("q_win / k must be contiguous bf16 [..., 128]")
+    bt, hq, w, _ = q_win.shape
+    _, hkv, T, _ = k.shape
+    if window is not None and window != w:
+        raise NativeError(f"window {window} != q_win.shape[2] {w}")
+    scale = 1.0 / math.sqrt(HEAD_DIM) if sm_scale is None else sm_scale
+    out = torch.empty((bt, hkv, T - w), dtype=torch.float32, device=k.device)
+    need = int(_lib.fkv_score_workspace_bytes(bt, hkv, T, w, hq // hkv))
+    if workspace is None or workspace.numel() * workspace.element_size() < need:
+        workspace = torch.empty(need, dtype=torch.uint8, device=k.device)
+    _native.check(_lib.fkv_snapkv_score(q_win.data_ptr(), k.data_ptr(), bt, hq, hkv, T, w,
+                                        int(pool_k), scale, out.data_ptr(), workspace.data_ptr(),
+                                        _stream()))
+    return out
+
+
+def ada_floor(budget: int, window: int, alpha: float) -> int:
+    """Per-head Ada safeguard floor floor(alpha * (B - w))."""
+    return int(math.floor(alpha * (budget - window)))
+
+
+def budgets(scores: torch.Tensor, budget: int, window: int = 32, alpha: float = 0.2) -> torch.Tensor:
+    """A18: Ada cross-head split of Hkv*budget retained tokens per request.
+
+    scores f32 [Bt, Hkv, T-w] (pooled Ada-SnapKV scores) -> int32 [Bt, Hkv],
+    every row summing to Hkv*budget, every head >= window + floor."""
+    _need_cuda(scores)
+    if scores.dtype != torch.float32 or scores.dim() != 3 or not scores.is_contiguous():
+        raise NativeError("scores must be contiguous f32 [Bt, Hkv, n]")
+    bt, hkv, n = scores.shape
+    out = torch.empty((bt, hkv), dtype=torch.int32, device=scores.device)
+    _native.check(_lib.fkv_ada_budgets(scores.data_ptr(), bt, hkv, n, int(budget), int(window),
+                                       ada_floor(budget, window, alpha), out.data_ptr(), _stream()))
+    return out
+
+
+def select(scores: torch.Tensor, head_budgets: torch.Tensor, window: int = 32,
+           total: int | None = None):
+    """K2: per-head top-(b_h - w) tokens by (score desc, token asc), ascending,
+    then the window tokens.  Returns (offsets int64 [Bt*Hkv+1], idx int32).
+    ``total`` = sum of budgets (Hkv*budget*Bt when they come from
+    ``budgets``); if omitted it is read back (one device sync)."""
+    _need_cuda(scores, head_budgets)
+    bt, hkv, n = scores.shape
+    if total is None:
+        total = int(head_budgets.sum().item())
+    offsets = torch.empty(bt * hkv + 1, dtype=torch.int64, device=scores.device)
+    idx = torch.empty(max(total, 1), dtype=torch.int32, device=scores.device)
+    _native.check(_lib.fkv_topk_select(scores.data_ptr(), head_budgets.data_ptr(), bt, hkv, n,
+                                       int(window), offsets.data_ptr(), idx.data_ptr(), _stream()))
+    return offsets, idx[:total]
+
+
+def compact(k: torch.Tensor, v: torch.Tensor, offsets: torch.Tensor, idx: torch.Tensor,
+            seg_bh, seg_lo, seg_hi, seg_qrow, seg_out_row, group: int,
+            chunk: int | None = None) -> LayerCache:
+    """K3: gather selected rows of k/v [Bt, Hkv, T, 128] (bf16, contiguous)
+    into a fresh page-aligned, swizzled LayerCache.  Segment i takes entries
+    [seg_lo[i], seg_hi[i]) of head seg_bh[i]'s selection (host int arrays;
+    one segment per head for TP=1, the owned copies for a sharded rank)."""
+    import numpy as np
+    _need_cuda(k, v, offsets, idx)
+    if k.dtype != torch.bfloat16 or k.shape != v.shape or k.shape[-1] != HEAD_DIM \
+            or not (k.is_contiguous() and v.is_contiguous()):
+        raise NativeError("k/v must be contiguous bf16 [Bt, Hkv, T, 128]")
+    T = k.shape[2]
+    seg_lo = np.asarray(seg_lo, dtype=np.int64)
+    seg_hi = np.asarray(seg_hi, dtype=np.int64)
+    cache = LayerCache.allocate(seg_hi - seg_lo, seg_qrow, seg_out_row, group, k.device, chunk=chunk)
+    dev = k.device
+    i32 = lambda a: torch.as_tensor(np.ascontiguousarray(a, dtype=np.int32), device=dev)  # noqa: E731
+    sbh, slo, shi = i32(seg_bh), i32(seg_lo), i32(seg_hi)
+    _native.check(_lib.fkv_compact(k.data_ptr(), v.data_ptr(), T, len(seg_lo), offsets.data_ptr(),
+                                   idx.data_ptr(), sbh.data_ptr(), slo.data_ptr(), shi.data_ptr(),
+                                   cache.seg_row0.data_ptr(), 1, cache.k.data_ptr(),
+                                   cache.v.data_ptr(), _stream()))
+    cache.host["compact_args"] = (sbh, slo, shi)  # keep alive until the stream consumes them
+    return cache
+
+
+def compress_layer(q_win: torch.Tensor, k: torch.Tensor, v: torch.Tensor, budget: int,
+                   window: int = 32, alpha: float = 0.2, pool_k: int = 7):
+    """Prefill of one layer on one GPU: K1 score -> A18 budgets -> K2 select
+    -> K3 compact (TP=1 layout).  Returns (cache, head_budgets, scores)."""
+    import numpy as np
+    bt, hq = q_win.shape[0], q_win.shape[1]
+    hkv = k.shape[1]
+    group = hq // hkv
+    sc = score(q_win, k, window=window, pool_k=pool_k)
+    hb = budgets(sc, budget, window, alpha)
+    offsets, idx = select(sc, hb, window, total=bt * hkv * budget)
+    hb_host = hb.cpu().numpy().reshape(-1)
+    bh = np.arange(bt * hkv)
+    qrow = (bh // hkv) * hq + (bh % hkv) * group
+    cache = compact(k, v, offsets, idx, bh, np.zeros_like(bh), hb_host, qrow, qrow, group)
+    return cache, hb, sc

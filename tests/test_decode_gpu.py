@@ -98,15 +98,12 @@ def test_lse_merge_of_token_split_equals_whole(cuda_device):
     cache.k.copy_(kh)
     cache.v.copy_(vh)
     # per-copy partials (f32 o + lse) into slots, then merge the 3 slots
-    slots_o = torch.zeros(3 * group, 128, device=cuda_device)
-    slots_lse = torch.zeros(3 * group, device=cuda_device)
-    part_o, part_lse = ops.decode_partial(q, cache)
-    ops.merge_lse(part_o, part_lse, cache.grp_ptr, cache.src_idx, cache.seg_out_row, group,
-                  out_f32=slots_o, out_lse=slots_lse)
+    slots = torch.zeros(3 * group, ops.REC, device=cuda_device)
+    ops.decode_into(q, cache, out_rec=slots)
     dev = cuda_device
     o = torch.empty(1, group, 128, dtype=torch.bfloat16, device=dev)
     lse = torch.empty(1, group, device=dev)
-    ops.merge_lse(slots_o.view(3, group, 128), slots_lse.view(3, group),
+    ops.merge_lse(slots.view(3, group, ops.REC),
                   torch.tensor([0, 3], dtype=torch.int32, device=dev),
                   torch.arange(3, dtype=torch.int32, device=dev),
                   torch.zeros(1, dtype=torch.int32, device=dev), group, out_bf16=o, out_lse=lse)
