@@ -369,6 +369,8 @@ def run_fairkv(args):
                                "sample": sample}
     if rank == 0 and world == 1 and not args.no_emulate:
         out["emulated_tp"] = emulate_tp(args, budgets, caches[0].k.device)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        out["planner"] = planner_compare(budgets)
     if rank == 0:
         print(json.dumps(out))
     if world > 1:
@@ -439,6 +441,46 @@ def emulate_tp(args, budgets, dev):
                        "max over ranks; all-gather not included (single GPU); sim = reference simulator, "
                        "pure-cache latency model")
     return results
+
+
+def planner_compare(budgets):
+    """AHA placement of this workload's profile: the native C++ planner vs the
+    reference's own optimize_plan (baseline/_ref, compiled Cython equal-split
+    kernel; its free split is pure Python), same workers, identical plans."""
+    import paper_2502_15804_b200 as fk
+    from paper_2502_15804_b200.sharding import budgets_profile
+    prof = budgets_profile(budgets, int(budgets.mean()))
+    ref = None
+    ref_dir = ROOT / "baseline" / "_ref"
+    if (ref_dir / "headbalance").exists():
+        sys.path.append(str(ref_dir))
+        try:
+            import headbalance as ref  # noqa: F811
+        except Exception:
+            ref = None
+    workers = os.cpu_count() or 1
+    rows = {}
+    for tp, ch, eq in ((4, 4, True), (8, 8, True), (8, 4, False)):
+        t0 = time.perf_counter()
+        mine = fk.optimize_plan(prof, tp, fk.EnumerationConfig(ch, 2, True, tp), equal_split=eq,
+                                workers=workers)
+        t_native = time.perf_counter() - t0
+        row = {"native_s": t_native}
+        if ref is not None:
+            rp = ref.ModelProfile(prof.model_name, prof.kv_budget, prof.num_layers,
+                                  prof.heads_per_layer, prof.weights)
+            t0 = time.perf_counter()
+            theirs = ref.optimize_plan(rp, tp, ref.EnumerationConfig(ch, 2, True, tp), equal_split=eq,
+                                       workers=workers)
+            row["reference_s"] = time.perf_counter() - t0
+            row["identical"] = all(
+                [[(c.head_id, c.replica_count) for c in g] for g in a.groups] ==
+                [[(c.head_id, c.replica_count) for c in g] for g in b.groups] and a.delta == b.delta
+                for a, b in zip(mine.layers, theirs.layers))
+            row["speedup"] = row["reference_s"] / t_native
+        rows[f"tp{tp}_ch{ch}_{'equal' if eq else 'free'}"] = row
+    return {"workers": workers, "layers": prof.num_layers, "heads": prof.heads_per_layer,
+            "kind": "reference" if ref is not None else "unavailable", "results": rows}
 
 
 # ------------------------------------------------------ reference arm -----

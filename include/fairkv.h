@@ -109,10 +109,13 @@ int fkv_optimize_plan(const double* weights, int32_t num_layers, int32_t n, int3
  *   seg_out_row  int32 [n_seg]   first output row of the segment's group heads
  *   seg_item_ptr int32 [n_seg+1] items of segment s are [ptr[s], ptr[s+1])
  *   item_seg, item_t0, item_t1 int32 [n_items]: work item = tokens [t0,t1) of a
- *                segment, t0 a multiple of 64
+ *                segment, t0 a multiple of 16
+ *   item_order   int32 [n_items]  processing order (persistent CTAs claim items
+ *                from an atomic queue in this order; longest first)
  *   part         f32 [n_items, group, FKV_REC]  partial records: softmax-normalised
  *                o[128] and lse = natural-log sum-exp of the scaled scores
- *   counters     int32 [n_seg], zero on entry; left zero on exit
+ *   counters     int32 [n_seg + 2], zero on entry; left zero on exit (segment
+ *                arrival counters + the work queue)
  * With all of out_bf16 / out_rec / out_lse NULL every item just writes its
  * partial record (split-K partials).  Otherwise the last CTA to finish a
  * segment merges its chunks by log-sum-exp and writes rows
@@ -124,9 +127,9 @@ int fkv_optimize_plan(const double* weights, int32_t num_layers, int32_t n, int3
 int fkv_decode(const void* q, const void* k, const void* v, const int64_t* seg_row0,
                const int32_t* seg_len, const int32_t* seg_qrow, const int32_t* seg_out_row,
                const int32_t* seg_item_ptr, const int32_t* item_seg, const int32_t* item_t0,
-               const int32_t* item_t1, int32_t n_items, int32_t group, float sm_scale,
-               float* part, int32_t* counters, void* out_bf16, float* out_rec, float* out_lse,
-               void* stream);
+               const int32_t* item_t1, const int32_t* item_order, int32_t n_items, int32_t n_seg,
+               int32_t group, float sm_scale, float* part, int32_t* counters, void* out_bf16,
+               float* out_rec, float* out_lse, void* stream);
 
 /* K5: log-sum-exp merge of partial records.  Output group g merges records
  * src_idx[grp_ptr[g] .. grp_ptr[g+1]) (each `group` heads of FKV_REC floats)
@@ -139,6 +142,44 @@ int fkv_decode(const void* q, const void* k, const void* v, const int64_t* seg_r
 int fkv_merge_lse(const float* part, const int32_t* grp_ptr, const int32_t* src_idx,
                   const int32_t* out_row, int32_t n_groups, int32_t group, void* out_bf16,
                   float* out_rec, float* out_lse, void* stream);
+
+/* ------------------------------------------- B3 compression (prefill) -- */
+
+/* K1: Ada-SnapKV observation-window scores (two tcgen05/TMEM/TMA passes +
+ * max-pool).  q_win bf16 [batch, hq, window, 128], k bf16 [batch, hkv, T, 128];
+ * scores f32 [batch, hkv, T - window]:
+ *   s[t] = maxpool_{pool_k}( (1/G) sum_{g,i} softmax_t(q_{g,i} . k_t * sm_scale) ),
+ * causal inside the window.  G*window must be 128 or 256.  workspace: device
+ * bytes >= fkv_score_workspace_bytes(...).  No reference implementation
+ * (the paper used KVPress SnapKV). */
+int64_t fkv_score_workspace_bytes(int32_t batch, int32_t hkv, int32_t T, int32_t window,
+                                  int32_t group);
+int fkv_snapkv_score(const void* q_win, const void* k, int32_t batch, int32_t hq, int32_t hkv,
+                     int32_t T, int32_t window, int32_t pool_k, float sm_scale, float* scores,
+                     void* workspace, void* stream);
+
+/* A18: Ada cross-head budget split.  scores f32 [batch, hkv, n] -> budgets
+ * int32 [batch, hkv] = window + floor_k + (# of the head's tokens in the
+ * global top-(hkv*(budget-window-floor_k)) of the non-floor scores), order
+ * (score desc, head asc, token asc); floor = per-head top-floor_k by (score
+ * desc, token asc).  Every row sums to hkv*budget. */
+int fkv_ada_budgets(const float* scores, int32_t batch, int32_t hkv, int32_t n, int32_t budget,
+                    int32_t window, int32_t floor_k, int32_t* budgets, void* stream);
+
+/* K2: per-head top-(budgets - window) by (score desc, token asc), written
+ * ascending at idx[offsets[bh]..], followed by the window tokens n..n+window-1;
+ * offsets int64 [batch*hkv + 1] is the exclusive prefix sum of budgets. */
+int fkv_topk_select(const float* scores, const int32_t* budgets, int32_t batch, int32_t hkv,
+                    int32_t n, int32_t window, int64_t* offsets, int32_t* idx, void* stream);
+
+/* K3: compaction.  For each destination segment s, rows j in [seg_lo, seg_hi)
+ * of head seg_bh[s]'s selection are copied from k_src/v_src (bf16
+ * [batch*hkv, T, 128]) to cache rows seg_row0[s] + (j - seg_lo), swizzled;
+ * zero_pad != 0 also zeroes the rows up to the next FKV_PAGE boundary. */
+int fkv_compact(const void* k_src, const void* v_src, int32_t T, int32_t n_segments,
+                const int64_t* offsets, const int32_t* idx, const int32_t* seg_bh,
+                const int32_t* seg_lo, const int32_t* seg_hi, const int64_t* seg_row0,
+                int32_t zero_pad, void* k_dst, void* v_dst, void* stream);
 
 #ifdef __cplusplus
 }

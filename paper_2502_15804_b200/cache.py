@@ -7,7 +7,7 @@ HBM layout (include/fairkv.h):
              [seg_row0[s], seg_row0[s] + seg_len[s]), seg_row0 % PAGE == 0,
              padding rows up to the next page are zero
 Work plan (built on the host once per cache, uploaded once):
-  items      chunks [t0, t1) of segments, ~equal size, t0 % 64 == 0
+  items      chunks [t0, t1) of segments, ~equal size, t0 % 16 == 0
   groups     one per segment: items of the segment are merged by LSE into the
              segment's output rows (o rows = seg_out_row .. + G - 1)
 """
@@ -21,8 +21,9 @@ import torch
 
 HEAD_DIM = 128
 PAGE = 64
-CHUNK_QUANTUM = 64  # 4 warps x 16-token tiles
+CHUNK_QUANTUM = 16  # one 16-token tile
 NUM_SMS = 148
+WORKERS = NUM_SMS * 8  # persistent decode warps (2 CTAs x 4 warps per SM)
 
 
 def page_rows(n_tok) -> np.ndarray:
@@ -40,14 +41,24 @@ def segment_offsets(seg_len) -> tuple[np.ndarray, int]:
     return row0, max(total, PAGE)
 
 
-def choose_chunk(seg_len, target_items: int | None = None, max_chunk: int = 1024) -> int:
-    """Tokens per work item: enough items for >= ~4 waves of 2 CTAs/SM,
-    never below one 64-token quantum."""
+def choose_chunk(seg_len, target_items: int | None = None, max_chunk: int = 2048,
+                 min_chunk: int = 128) -> int:
+    """Tokens per work item for the warp-persistent decode kernel: about
+    three items per worker warp (the longest-first queue then drains with a
+    short tail), at least ``min_chunk`` tokens so the per-item record/merge
+    overhead stays a few percent, multiple of the 16-token tile."""
     total = int(np.asarray(seg_len, dtype=np.int64).sum())
-    target = target_items or NUM_SMS * 2 * 4
+    target = target_items or WORKERS * 3
     c = -(-total // max(target, 1))
     c = -(-c // CHUNK_QUANTUM) * CHUNK_QUANTUM
-    return int(min(max(c, CHUNK_QUANTUM), max_chunk))
+    return int(min(max(c, min_chunk), max_chunk))
+
+
+def longest_first(t0, t1) -> np.ndarray:
+    """Item processing order for the persistent decode kernel: longest
+    first (LPT), ties by item id, so the queue drains with a short tail."""
+    n = np.asarray(t1, dtype=np.int64) - np.asarray(t0, dtype=np.int64)
+    return np.lexsort((np.arange(len(n)), -n)).astype(np.int32)
 
 
 def plan_items(seg_len, chunk: int) -> tuple[np.ndarray, np.ndarray, np.ndarray, np.ndarray]:
@@ -79,6 +90,7 @@ class LayerCache:
     item_t1: torch.Tensor
     grp_ptr: torch.Tensor
     src_idx: torch.Tensor
+    item_order: torch.Tensor
     counters: torch.Tensor
     host: dict = field(default_factory=dict, repr=False)
 
@@ -133,7 +145,8 @@ class LayerCache:
             seg_len=i32(seg_len), seg_qrow=i32(seg_qrow), seg_out_row=i32(seg_out_row),
             item_seg=i32(item_seg), item_t0=i32(t0), item_t1=i32(t1),
             grp_ptr=i32(ptr), src_idx=i32(np.arange(ptr[-1])),
-            counters=torch.zeros(max(len(seg_len), 1), dtype=torch.int32, device=dev),
+            item_order=i32(longest_first(t0, t1)),
+            counters=torch.zeros(len(seg_len) + 2, dtype=torch.int32, device=dev),
             host={"seg_len": seg_len, "seg_row0": row0, "chunk": chunk,
                   "seg_qrow": np.asarray(seg_qrow), "seg_out_row": np.asarray(seg_out_row)},
         )
@@ -160,7 +173,8 @@ class LayerCache:
             seg_len=i32(seg_len), seg_qrow=i32(seg_qrow), seg_out_row=i32(seg_out_row),
             item_seg=i32(item_seg), item_t0=i32(t0), item_t1=i32(t1), grp_ptr=i32(ptr),
             src_idx=i32(np.arange(ptr[-1])),
-            counters=torch.zeros(max(len(seg_len), 1), dtype=torch.int32, device=dev),
+            item_order=i32(longest_first(t0, t1)),
+            counters=torch.zeros(len(seg_len) + 2, dtype=torch.int32, device=dev),
             host={"seg_len": seg_len, "seg_row0": seg_row0, "chunk": chunk,
                   "seg_qrow": np.asarray(seg_qrow), "seg_out_row": np.asarray(seg_out_row)},
         )

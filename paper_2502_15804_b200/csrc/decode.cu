@@ -1,22 +1,28 @@
-// K4 + K5(local): split-KV decode attention over the ragged, swizzled,
-// page-aligned compressed cache, and the log-sum-exp merge.
+// K4 + fused K5: warp-persistent split-KV decode attention over the ragged,
+// swizzled, page-aligned compressed cache, with the log-sum-exp merges.
 //
 // No reference implementation exists; the reference only models
 // this kernel's time as c0 + c1*B + c2*C + c3*B*C (pkg/src/headbalance/latency.py:85-91).
 //
 // Design:
-//  * one CTA = 4 warps = one work item (a chunk of one segment); each warp
-//    owns every 4th 16-token tile of the chunk and runs its own 3-stage TMA
-//    bulk-copy ring (cp.async.bulk + mbarrier): no CTA barrier in the loop;
+//  * every warp is an independent persistent worker: it claims work items
+//    (chunks of segments, host-sorted longest first) from an atomic queue and
+//    never synchronises with the other warps of its CTA -- no block barriers
+//    anywhere.  The queue resets itself when the last warp leaves, so a
+//    captured CUDA graph can replay;
+//  * each warp runs its own S-stage TMA bulk-copy ring (cp.async.bulk +
+//    mbarrier, 16-token K+V tiles of 8 KiB) that streams ACROSS item
+//    boundaries: the producer lane claims the next item and lands its first
+//    tiles while the warp is still finishing the current one;
 //  * the cache rows are stored pre-swizzled in HBM, so a 1-D bulk copy lands
 //    a bank-conflict-free tile for ldmatrix -- no tensor map, no address math;
 //  * GQA: every K/V tile is read once for all G query heads.  S^T = K Q^T
 //    (m16n8k16: 16 tokens x 8 heads, no padding waste for G=8), online
 //    softmax per head column (warp-shuffle max), P^T via movmatrix, then
 //    O^T += V^T P^T with ldmatrix.trans on the V tile;
-//  * 4 warp partials merge through shared memory into one (o, lse) partial
-//    per item; K5 merges items of a segment (and, after the all-gather,
-//    DP copies of a head) by log-sum-exp.
+//  * an item's (o, lse) goes straight from registers to its output rows when
+//    the segment is one item; otherwise to a partial record, and the last
+//    warp to finish one of the segment's items merges them (K5 fused).
 #include <cuda_bf16.h>
 #include <math_constants.h>
 
@@ -29,8 +35,9 @@ constexpr int kWarps = 4;
 constexpr int kStages = 3;
 constexpr int kTileTok = 16;
 constexpr int kTileBytes = kTileTok * FKV_HEAD_DIM * 2;  // 4 KiB per K or V tile
-constexpr int kWarpSmem = kStages * 2 * kTileBytes;      // 24 KiB
-constexpr int kSmemBytes = kWarps * kWarpSmem;           // 96 KiB
+constexpr int kRingBytes = kStages * 2 * kTileBytes;     // per warp
+constexpr int kSmemBytes = kWarps * kRingBytes;
+constexpr int kQueue = 4;                                // claimed-item ring per warp (> kStages)
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 
@@ -46,33 +53,35 @@ struct DecodeParams {
   const int32_t* item_seg;
   const int32_t* item_t0;
   const int32_t* item_t1;
+  const int32_t* item_order;  // processing order (longest first)
+  int n_items, n_seg;
   float scale_log2;
   float* part;        // [n_items, G, FKV_REC] partial records (multi-item segments)
-  int32_t* counters;  // [n_seg] arrival counters, zero between launches (self-resetting)
+  int32_t* counters;  // [n_seg] segment arrivals + [2] work queue; zero between launches
   __nv_bfloat16* out_bf16;
   float* out_rec;
   float* out_lse;
 };
 
+__device__ __forceinline__ int n_tiles_of(const DecodeParams& p, int it, int& t0, int& t1,
+                                          int& seg) {
+  seg = p.item_seg[it];
+  t0 = p.item_t0[it];
+  t1 = min(p.item_t1[it], p.seg_len[seg]);
+  return t1 > t0 ? (t1 - t0 + kTileTok - 1) / kTileTok : 0;
+}
+
 template <int G>
 __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodeParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bars[kWarps][kStages];
-  __shared__ int s_last;
+  __shared__ int queue[kWarps][kQueue];
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int item = blockIdx.x;
-  const int seg = p.item_seg[item];
-  const int t0 = p.item_t0[item];
-  const int t1 = min(p.item_t1[item], p.seg_len[seg]);
-  const int64_t row0 = p.seg_row0[seg];
-  const __nv_bfloat16* kseg = p.k + row0 * FKV_HEAD_DIM;
-  const __nv_bfloat16* vseg = p.v + row0 * FKV_HEAD_DIM;
-
-  const int n_tiles = t1 > t0 ? (t1 - t0 + kTileTok - 1) / kTileTok : 0;
-  const int my_tiles = n_tiles > warp ? (n_tiles - warp + kWarps - 1) / kWarps : 0;
-  uint8_t* wsm = smem + warp * kWarpSmem;
+  uint8_t* ring = smem + warp * kRingBytes;
+  int* q_items = queue[warp];
+  int* work = p.counters + p.n_seg;
 
   if (lane == 0) {
     for (int s = 0; s < kStages; ++s) mbar_init(&bars[warp][s], 1);
@@ -80,218 +89,279 @@ __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodePara
   }
   __syncwarp();
 
-  auto issue = [&](int i) {  // lane 0 only: tile i of this warp into stage i % kStages
-    const int s = i % kStages;
-    const int ts = t0 + kTileTok * (warp + kWarps * i);
-    uint8_t* dst = wsm + s * 2 * kTileBytes;
-    mbar_arrive_expect_tx(&bars[warp][s], 2 * kTileBytes);
-    bulk_g2s(dst, kseg + static_cast<int64_t>(ts) * FKV_HEAD_DIM, kTileBytes, &bars[warp][s]);
-    bulk_g2s(dst + kTileBytes, vseg + static_cast<int64_t>(ts) * FKV_HEAD_DIM, kTileBytes,
-             &bars[warp][s]);
-  };
-  if (lane == 0)
-    for (int i = 0; i < my_tiles && i < kStages; ++i) issue(i);
-
-  // Q^T as the B operand (k = head_dim, n = query head of the group), kept in
-  // registers for the whole item.
-  uint32_t qb[8][2];
-  {
-    const int n = lane >> 2;
-    const int kq = 2 * (lane & 3);
-    if (n < G) {
-      const __nv_bfloat16* qr = p.q + static_cast<int64_t>(p.seg_qrow[seg] + n) * FKV_HEAD_DIM;
-#pragma unroll
-      for (int kk = 0; kk < 8; ++kk) {
-        qb[kk][0] = *reinterpret_cast<const uint32_t*>(qr + 16 * kk + kq);
-        qb[kk][1] = *reinterpret_cast<const uint32_t*>(qr + 16 * kk + 8 + kq);
-      }
-    } else {
-#pragma unroll
-      for (int kk = 0; kk < 8; ++kk) qb[kk][0] = qb[kk][1] = 0u;
-    }
-  }
-
-  float m0 = -CUDART_INF_F, m1 = -CUDART_INF_F;  // running max (log2 domain), heads h0, h1
-  float l0 = 0.f, l1 = 0.f;                      // thread-partial denominators
-  float acc[8][4];
-#pragma unroll
-  for (int dt = 0; dt < 8; ++dt) acc[dt][0] = acc[dt][1] = acc[dt][2] = acc[dt][3] = 0.f;
-
-  const int mi = lane >> 3, ri = lane & 7;
-  for (int i = 0; i < my_tiles; ++i) {
-    const int s = i % kStages;
-    mbar_wait(&bars[warp][s], (i / kStages) & 1);
-    const uint32_t kt = smem_u32(wsm + s * 2 * kTileBytes);
-    const uint32_t vt = kt + kTileBytes;
-    const int tok_base = t0 + kTileTok * (warp + kWarps * i);
-
-    // S^T[16 tok x 8 heads] = K_tile . Q^T
-    float sc[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-    for (int kk = 0; kk < 8; ++kk) {
-      uint32_t a0, a1, a2, a3;
-      ldmatrix_x4(kt + swz_off(ri + 8 * (mi & 1), 2 * kk + (mi >> 1)), a0, a1, a2, a3);
-      mma_bf16_16816(sc, a0, a1, a2, a3, qb[kk][0], qb[kk][1]);
-    }
-    const int ta = tok_base + (lane >> 2);
-    const float s0 = ta < t1 ? sc[0] * p.scale_log2 : -CUDART_INF_F;
-    const float s1 = ta < t1 ? sc[1] * p.scale_log2 : -CUDART_INF_F;
-    const float s2 = ta + 8 < t1 ? sc[2] * p.scale_log2 : -CUDART_INF_F;
-    const float s3 = ta + 8 < t1 ? sc[3] * p.scale_log2 : -CUDART_INF_F;
-    float mx0 = fmaxf(s0, s2), mx1 = fmaxf(s1, s3);
-#pragma unroll
-    for (int off = 4; off < 32; off <<= 1) {
-      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, off));
-      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, off));
-    }
-    const float nm0 = fmaxf(m0, mx0), nm1 = fmaxf(m1, mx1);
-    const float r0 = nm0 == -CUDART_INF_F ? 0.f : nm0;
-    const float r1 = nm1 == -CUDART_INF_F ? 0.f : nm1;
-    const float c0 = fast_exp2(m0 - r0), c1 = fast_exp2(m1 - r1);
-    const float p0 = fast_exp2(s0 - r0), p1 = fast_exp2(s1 - r1);
-    const float p2 = fast_exp2(s2 - r0), p3 = fast_exp2(s3 - r1);
-    l0 = l0 * c0 + p0 + p2;
-    l1 = l1 * c1 + p1 + p3;
-    m0 = nm0;
-    m1 = nm1;
-#pragma unroll
-    for (int dt = 0; dt < 8; ++dt) {
-      acc[dt][0] *= c0;
-      acc[dt][1] *= c1;
-      acc[dt][2] *= c0;
-      acc[dt][3] *= c1;
-    }
-    // P^T fragments (k = token, n = head) from the S^T accumulator layout
-    const uint32_t pb0 = movmatrix_trans(pack_bf16x2(p0, p1));
-    const uint32_t pb1 = movmatrix_trans(pack_bf16x2(p2, p3));
-    // O^T[128 d x 8 heads] += V^T . P^T
-#pragma unroll
-    for (int dt = 0; dt < 8; ++dt) {
-      uint32_t a0, a1, a2, a3;
-      ldmatrix_x4_trans(vt + swz_off(ri + 8 * (mi >> 1), 2 * dt + (mi & 1)), a0, a1, a2, a3);
-      mma_bf16_16816(acc[dt], a0, a1, a2, a3, pb0, pb1);
+  // Claimed items: ordinals 0..claimed live in q_items[ord % kQueue].
+  int claimed = -1;
+  auto claim_next = [&]() {
+    int it = -1;
+    if (lane == 0) {
+      const int x = atomicAdd(work, 1);
+      it = x < p.n_items ? p.item_order[x] : -1;
+      q_items[(claimed + 1) % kQueue] = it;
     }
     __syncwarp();
-    if (lane == 0 && i + kStages < my_tiles) issue(i + kStages);
-  }
+    ++claimed;
+  };
+  auto item_at = [&](int ord) -> int {
+    while (claimed < ord) claim_next();
+    return q_items[ord % kQueue];
+  };
 
-#pragma unroll
-  for (int off = 4; off < 32; off <<= 1) {
-    l0 += __shfl_xor_sync(0xffffffffu, l0, off);
-    l1 += __shfl_xor_sync(0xffffffffu, l1, off);
-  }
+  int p_ord = 0, p_t = 0;  // producer cursor: item ordinal, tile within item
+  uint32_t p_seq = 0, c_seq = 0;
+  bool p_done = false;
+  auto refill = [&]() {
+    while (!p_done && p_seq - c_seq < kStages) {
+      const int it = item_at(p_ord);
+      if (it < 0) {
+        p_done = true;
+        break;
+      }
+      int t0, t1, seg;
+      const int nt = n_tiles_of(p, it, t0, t1, seg);
+      if (p_t >= nt) {
+        ++p_ord;
+        p_t = 0;
+        continue;
+      }
+      if (lane == 0) {
+        const int s = p_seq % kStages;
+        const int64_t row = p.seg_row0[seg] + t0 + kTileTok * p_t;
+        uint8_t* dst = ring + s * 2 * kTileBytes;
+        mbar_arrive_expect_tx(&bars[warp][s], 2 * kTileBytes);
+        bulk_g2s(dst, p.k + row * FKV_HEAD_DIM, kTileBytes, &bars[warp][s]);
+        bulk_g2s(dst + kTileBytes, p.v + row * FKV_HEAD_DIM, kTileBytes, &bars[warp][s]);
+      }
+      ++p_t;
+      ++p_seq;
+    }
+  };
+  refill();
 
-  // ---- per-warp partial -> own smem region (all its copies have landed)
-  float* wo = reinterpret_cast<float*>(wsm);  // [G][128]
-  float* wm = wo + G * FKV_HEAD_DIM;          // [8]
-  float* wl = wm + 8;                         // [8]
+  const int mi = lane >> 3, ri = lane & 7;
   const int h0 = 2 * (lane & 3), h1 = h0 + 1;
   const int dr = lane >> 2;
-#pragma unroll
-  for (int dt = 0; dt < 8; ++dt) {
-    if (h0 < G) {
-      wo[h0 * FKV_HEAD_DIM + 16 * dt + dr] = acc[dt][0];
-      wo[h0 * FKV_HEAD_DIM + 16 * dt + dr + 8] = acc[dt][2];
-    }
-    if (h1 < G) {
-      wo[h1 * FKV_HEAD_DIM + 16 * dt + dr] = acc[dt][1];
-      wo[h1 * FKV_HEAD_DIM + 16 * dt + dr + 8] = acc[dt][3];
-    }
-  }
-  if (lane < 4) {
-    if (h0 < G) { wm[h0] = m0; wl[h0] = l0; }
-    if (h1 < G) { wm[h1] = m1; wl[h1] = l1; }
-  }
-  __syncthreads();
+  const bool fused = p.out_bf16 || p.out_rec || p.out_lse;
 
-  // ---- cross-warp log-sum-exp combine: thread = one head_dim column
-  const int d = threadIdx.x;
-  float on[G], ls[G];
+  for (int ord = 0;; ++ord) {
+    const int it = item_at(ord);
+    if (it < 0) break;
+    int t0, t1, seg;
+    const int nt = n_tiles_of(p, it, t0, t1, seg);
+
+    // Q^T as the B operand (k = head_dim, n = query head), in registers.
+    uint32_t qb[8][2];
+    {
+      const int n = lane >> 2, kq = 2 * (lane & 3);
+      if (n < G) {
+        const __nv_bfloat16* qr = p.q + static_cast<int64_t>(p.seg_qrow[seg] + n) * FKV_HEAD_DIM;
 #pragma unroll
-  for (int g = 0; g < G; ++g) {
-    float M = -CUDART_INF_F;
+        for (int kk = 0; kk < 8; ++kk) {
+          qb[kk][0] = __ldg(reinterpret_cast<const unsigned int*>(qr + 16 * kk + kq));
+          qb[kk][1] = __ldg(reinterpret_cast<const unsigned int*>(qr + 16 * kk + 8 + kq));
+        }
+      } else {
 #pragma unroll
-    for (int w = 0; w < kWarps; ++w)
-      M = fmaxf(M, reinterpret_cast<const float*>(smem + w * kWarpSmem)[G * FKV_HEAD_DIM + g]);
-    float L = 0.f, o = 0.f;
-    if (M != -CUDART_INF_F) {
-#pragma unroll
-      for (int w = 0; w < kWarps; ++w) {
-        const float* b = reinterpret_cast<const float*>(smem + w * kWarpSmem);
-        const float f = fast_exp2(b[G * FKV_HEAD_DIM + g] - M);
-        L += b[G * FKV_HEAD_DIM + 8 + g] * f;
-        o += b[g * FKV_HEAD_DIM + d] * f;
+        for (int kk = 0; kk < 8; ++kk) qb[kk][0] = qb[kk][1] = 0u;
       }
     }
-    on[g] = L > 0.f ? o / L : 0.f;
-    ls[g] = L > 0.f ? (M + log2f(L)) * kLn2 : -CUDART_INF_F;
+
+    float m0 = -CUDART_INF_F, m1 = -CUDART_INF_F;  // running max (log2 domain), heads h0, h1
+    float l0 = 0.f, l1 = 0.f;                      // thread-partial denominators
+    float acc[8][4];
+#pragma unroll
+    for (int dt = 0; dt < 8; ++dt) acc[dt][0] = acc[dt][1] = acc[dt][2] = acc[dt][3] = 0.f;
+
+    for (int i = 0; i < nt; ++i) {
+      const int s = c_seq % kStages;
+      mbar_wait(&bars[warp][s], (c_seq / kStages) & 1);
+      const uint32_t kt = smem_u32(ring + s * 2 * kTileBytes);
+      const uint32_t vt = kt + kTileBytes;
+
+      // S^T[16 tok x 8 heads] = K_tile . Q^T, two independent accumulation chains
+      float sa[4] = {0.f, 0.f, 0.f, 0.f}, sb[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int kk = 0; kk < 8; kk += 2) {
+        uint32_t a0, a1, a2, a3, b0, b1, b2, b3;
+        ldmatrix_x4(kt + swz_off(ri + 8 * (mi & 1), 2 * kk + (mi >> 1)), a0, a1, a2, a3);
+        ldmatrix_x4(kt + swz_off(ri + 8 * (mi & 1), 2 * kk + 2 + (mi >> 1)), b0, b1, b2, b3);
+        mma_bf16_16816(sa, a0, a1, a2, a3, qb[kk][0], qb[kk][1]);
+        mma_bf16_16816(sb, b0, b1, b2, b3, qb[kk + 1][0], qb[kk + 1][1]);
+      }
+      const int ta = t0 + kTileTok * i + (lane >> 2);
+      const float s0 = ta < t1 ? (sa[0] + sb[0]) * p.scale_log2 : -CUDART_INF_F;
+      const float s1 = ta < t1 ? (sa[1] + sb[1]) * p.scale_log2 : -CUDART_INF_F;
+      const float s2 = ta + 8 < t1 ? (sa[2] + sb[2]) * p.scale_log2 : -CUDART_INF_F;
+      const float s3 = ta + 8 < t1 ? (sa[3] + sb[3]) * p.scale_log2 : -CUDART_INF_F;
+      float mx0 = fmaxf(s0, s2), mx1 = fmaxf(s1, s3);
+#pragma unroll
+      for (int off = 4; off < 32; off <<= 1) {
+        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, off));
+        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, off));
+      }
+      const float nm0 = fmaxf(m0, mx0), nm1 = fmaxf(m1, mx1);
+      const float r0 = nm0 == -CUDART_INF_F ? 0.f : nm0;
+      const float r1 = nm1 == -CUDART_INF_F ? 0.f : nm1;
+      const float c0 = fast_exp2(m0 - r0), c1 = fast_exp2(m1 - r1);
+      const float p0 = fast_exp2(s0 - r0), p1 = fast_exp2(s1 - r1);
+      const float p2 = fast_exp2(s2 - r0), p3 = fast_exp2(s3 - r1);
+      l0 = l0 * c0 + p0 + p2;
+      l1 = l1 * c1 + p1 + p3;
+      m0 = nm0;
+      m1 = nm1;
+#pragma unroll
+      for (int dt = 0; dt < 8; ++dt) {
+        acc[dt][0] *= c0;
+        acc[dt][1] *= c1;
+        acc[dt][2] *= c0;
+        acc[dt][3] *= c1;
+      }
+      // P^T fragments (k = token, n = head) from the S^T accumulator layout
+      const uint32_t pb0 = movmatrix_trans(pack_bf16x2(p0, p1));
+      const uint32_t pb1 = movmatrix_trans(pack_bf16x2(p2, p3));
+      // O^T[128 d x 8 heads] += V^T . P^T
+#pragma unroll
+      for (int dt = 0; dt < 8; ++dt) {
+        uint32_t a0, a1, a2, a3;
+        ldmatrix_x4_trans(vt + swz_off(ri + 8 * (mi >> 1), 2 * dt + (mi & 1)), a0, a1, a2, a3);
+        mma_bf16_16816(acc[dt], a0, a1, a2, a3, pb0, pb1);
+      }
+      __syncwarp();
+      ++c_seq;
+      refill();
+    }
+
+    // ---- finalise this item from registers
+#pragma unroll
+    for (int off = 4; off < 32; off <<= 1) {
+      l0 += __shfl_xor_sync(0xffffffffu, l0, off);
+      l1 += __shfl_xor_sync(0xffffffffu, l1, off);
+    }
+    const float inv0 = l0 > 0.f ? 1.f / l0 : 0.f, inv1 = l1 > 0.f ? 1.f / l1 : 0.f;
+    const float lse0 = l0 > 0.f ? (m0 + log2f(l0)) * kLn2 : -CUDART_INF_F;
+    const float lse1 = l1 > 0.f ? (m1 + log2f(l1)) * kLn2 : -CUDART_INF_F;
+    const int i0 = p.seg_item_ptr[seg];
+    const int n_it = p.seg_item_ptr[seg + 1] - i0;
+    const int64_t orow = p.seg_out_row[seg];
+
+    if (fused && n_it == 1) {
+      // whole segment in one item: registers -> output rows
+#pragma unroll
+      for (int dt = 0; dt < 8; ++dt) {
+        const int d0 = 16 * dt + dr;
+        if (h0 < G) {
+          if (p.out_bf16) {
+            p.out_bf16[(orow + h0) * FKV_HEAD_DIM + d0] = __float2bfloat16_rn(acc[dt][0] * inv0);
+            p.out_bf16[(orow + h0) * FKV_HEAD_DIM + d0 + 8] = __float2bfloat16_rn(acc[dt][2] * inv0);
+          }
+          if (p.out_rec) {
+            p.out_rec[(orow + h0) * FKV_REC + d0] = acc[dt][0] * inv0;
+            p.out_rec[(orow + h0) * FKV_REC + d0 + 8] = acc[dt][2] * inv0;
+          }
+        }
+        if (h1 < G) {
+          if (p.out_bf16) {
+            p.out_bf16[(orow + h1) * FKV_HEAD_DIM + d0] = __float2bfloat16_rn(acc[dt][1] * inv1);
+            p.out_bf16[(orow + h1) * FKV_HEAD_DIM + d0 + 8] = __float2bfloat16_rn(acc[dt][3] * inv1);
+          }
+          if (p.out_rec) {
+            p.out_rec[(orow + h1) * FKV_REC + d0] = acc[dt][1] * inv1;
+            p.out_rec[(orow + h1) * FKV_REC + d0 + 8] = acc[dt][3] * inv1;
+          }
+        }
+      }
+      if (lane < 4) {
+        if (h0 < G) {
+          if (p.out_rec) p.out_rec[(orow + h0) * FKV_REC + FKV_HEAD_DIM] = lse0;
+          if (p.out_lse) p.out_lse[orow + h0] = lse0;
+        }
+        if (h1 < G) {
+          if (p.out_rec) p.out_rec[(orow + h1) * FKV_REC + FKV_HEAD_DIM] = lse1;
+          if (p.out_lse) p.out_lse[orow + h1] = lse1;
+        }
+      }
+      continue;
+    }
+
+    // partial record of this item
+    float* rec = p.part + static_cast<int64_t>(it) * G * FKV_REC;
+#pragma unroll
+    for (int dt = 0; dt < 8; ++dt) {
+      const int d0 = 16 * dt + dr;
+      if (h0 < G) {
+        rec[h0 * FKV_REC + d0] = acc[dt][0] * inv0;
+        rec[h0 * FKV_REC + d0 + 8] = acc[dt][2] * inv0;
+      }
+      if (h1 < G) {
+        rec[h1 * FKV_REC + d0] = acc[dt][1] * inv1;
+        rec[h1 * FKV_REC + d0 + 8] = acc[dt][3] * inv1;
+      }
+    }
+    if (lane < 4) {
+      if (h0 < G) rec[h0 * FKV_REC + FKV_HEAD_DIM] = lse0;
+      if (h1 < G) rec[h1 * FKV_REC + FKV_HEAD_DIM] = lse1;
+    }
+    if (!fused) continue;
+
+    // the last warp to finish one of the segment's items merges them all
+    __threadfence();
+    __syncwarp();
+    int last = 0;
+    if (lane == 0) last = atomicAdd(&p.counters[seg], 1) == n_it - 1;
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (!last) continue;
+    __threadfence();
+    const float* base = p.part + static_cast<int64_t>(i0) * G * FKV_REC;
+#pragma unroll 1
+    for (int g = 0; g < G; ++g) {
+      // weights: lane i holds item i's lse (segments have <= a few dozen items)
+      float M = -CUDART_INF_F;
+      for (int i = lane; i < n_it; i += 32) M = fmaxf(M, __ldcg(base + (i * G + g) * FKV_REC + FKV_HEAD_DIM));
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+      float S = 0.f;
+      float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (M != -CUDART_INF_F) {
+#pragma unroll 4
+        for (int i = 0; i < n_it; ++i) {
+          const float* r = base + (i * G + g) * FKV_REC;
+          const float w = __expf(__ldcg(r + FKV_HEAD_DIM) - M);
+          const float4 v4 = __ldcg(reinterpret_cast<const float4*>(r) + lane);
+          S += w;
+          o.x = fmaf(w, v4.x, o.x);
+          o.y = fmaf(w, v4.y, o.y);
+          o.z = fmaf(w, v4.z, o.z);
+          o.w = fmaf(w, v4.w, o.w);
+        }
+      }
+      const float inv = S > 0.f ? 1.f / S : 0.f;
+      o.x *= inv;
+      o.y *= inv;
+      o.z *= inv;
+      o.w *= inv;
+      const float lse = S > 0.f ? M + __logf(S) : -CUDART_INF_F;
+      const int64_t row = orow + g;
+      if (p.out_bf16) {
+        __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(p.out_bf16 + row * FKV_HEAD_DIM) + 2 * lane;
+        ob[0] = __floats2bfloat162_rn(o.x, o.y);
+        ob[1] = __floats2bfloat162_rn(o.z, o.w);
+      }
+      if (p.out_rec) {
+        reinterpret_cast<float4*>(p.out_rec + row * FKV_REC)[lane] = o;
+        if (lane == 0) p.out_rec[row * FKV_REC + FKV_HEAD_DIM] = lse;
+      }
+      if (p.out_lse && lane == 0) p.out_lse[row] = lse;
+    }
+    if (lane == 0) p.counters[seg] = 0;  // ready for the next launch / graph replay
   }
 
-  const bool fused = p.out_bf16 || p.out_rec || p.out_lse;
-  const int i0 = p.seg_item_ptr[seg];
-  const int n_it = p.seg_item_ptr[seg + 1] - i0;
-  if (!fused || n_it > 1) {
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      float* rec = p.part + (static_cast<int64_t>(item) * G + g) * FKV_REC;
-      rec[d] = on[g];
-      if (d == 0) rec[FKV_HEAD_DIM] = ls[g];
-    }
-  }
-  if (!fused) return;
-  if (n_it > 1) {
-    // last-arriving CTA of the segment merges every chunk's record (K5 fused)
+  // the last warp out resets the work queue for the next launch / graph replay
+  if (lane == 0) {
     __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) s_last = atomicAdd(&p.counters[seg], 1) == n_it - 1;
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    // Latency-tolerant merge: all (item, head) lse values are fetched in one
-    // parallel round trip, weights are formed in shared memory, then every
-    // thread streams its head_dim column of all records with independent loads.
-    float* s_w = reinterpret_cast<float*>(smem);  // [n_it][G] weights (stage buffers are free)
-    float* s_lse = s_w + n_it * G;                // [G] merged lse
-    for (int x = threadIdx.x; x < n_it * G; x += blockDim.x)
-      s_w[x] = __ldcg(p.part + (static_cast<int64_t>(i0) * G + x) * FKV_REC + FKV_HEAD_DIM);
-    __syncthreads();
-    if (threadIdx.x < G) {
-      const int g = threadIdx.x;
-      float M = -CUDART_INF_F;
-      for (int i = 0; i < n_it; ++i) M = fmaxf(M, s_w[i * G + g]);
-      float S = 0.f;
-      if (M != -CUDART_INF_F)
-        for (int i = 0; i < n_it; ++i) S += __expf(s_w[i * G + g] - M);
-      const float inv = S > 0.f ? 1.f / S : 0.f;
-      for (int i = 0; i < n_it; ++i)
-        s_w[i * G + g] = M != -CUDART_INF_F ? __expf(s_w[i * G + g] - M) * inv : 0.f;
-      s_lse[g] = S > 0.f ? M + __logf(S) : -CUDART_INF_F;
+    if (atomicAdd(work + 1, 1) == static_cast<int>(gridDim.x) * kWarps - 1) {
+      work[0] = 0;
+      work[1] = 0;
+      __threadfence();
     }
-    __syncthreads();
-#pragma unroll
-    for (int g = 0; g < G; ++g) on[g] = 0.f;
-    const float* base = p.part + static_cast<int64_t>(i0) * G * FKV_REC + d;
-#pragma unroll 2
-    for (int i = 0; i < n_it; ++i) {
-      float v[G];
-#pragma unroll
-      for (int g = 0; g < G; ++g) v[g] = __ldcg(base + (i * G + g) * FKV_REC);
-#pragma unroll
-      for (int g = 0; g < G; ++g) on[g] = fmaf(s_w[i * G + g], v[g], on[g]);
-    }
-#pragma unroll
-    for (int g = 0; g < G; ++g) ls[g] = s_lse[g];
-    if (threadIdx.x == 0) p.counters[seg] = 0;  // ready for the next launch / graph replay
-  }
-  const int64_t orow = p.seg_out_row[seg];
-#pragma unroll
-  for (int g = 0; g < G; ++g) {
-    if (p.out_bf16) p.out_bf16[(orow + g) * FKV_HEAD_DIM + d] = __float2bfloat16_rn(on[g]);
-    if (p.out_rec) {
-      p.out_rec[(orow + g) * FKV_REC + d] = on[g];
-      if (d == 0) p.out_rec[(orow + g) * FKV_REC + FKV_HEAD_DIM] = ls[g];
-    }
-    if (p.out_lse && d == 0) p.out_lse[orow + g] = ls[g];
   }
 }
 
@@ -342,17 +412,23 @@ __global__ void __launch_bounds__(G * 32)
 }
 
 template <int G>
-int launch_decode(const DecodeParams& p, int n_items, cudaStream_t st) {
-  static bool configured = false;  // attribute set is per-function, idempotent
-  if (!configured) {
+int launch_decode(const DecodeParams& p, cudaStream_t st) {
+  static int grid_cap = 0;  // 2 persistent CTAs per SM
+  if (!grid_cap) {
     if (int rc = cuda_check(cudaFuncSetAttribute(decode_kernel<G>,
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  kSmemBytes),
                             "decode smem attribute"))
       return rc;
-    configured = true;
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_kernel<G>, kWarps * 32,
+                                                  kSmemBytes);
+    grid_cap = sms * (per_sm > 0 ? per_sm : 1);
   }
-  decode_kernel<G><<<n_items, kWarps * 32, kSmemBytes, st>>>(p);
+  const int grid = p.n_items < grid_cap ? p.n_items : grid_cap;
+  decode_kernel<G><<<grid, kWarps * 32, kSmemBytes, st>>>(p);
   return cuda_check(cudaGetLastError(), "decode launch");
 }
 
@@ -363,26 +439,27 @@ extern "C" int fkv_decode(const void* q, const void* k, const void* v, const int
                           const int32_t* seg_len, const int32_t* seg_qrow,
                           const int32_t* seg_out_row, const int32_t* seg_item_ptr,
                           const int32_t* item_seg, const int32_t* item_t0, const int32_t* item_t1,
-                          int32_t n_items, int32_t group, float sm_scale, float* part,
-                          int32_t* counters, void* out_bf16, float* out_rec, float* out_lse,
-                          void* stream) {
+                          const int32_t* item_order, int32_t n_items, int32_t n_seg,
+                          int32_t group, float sm_scale, float* part, int32_t* counters,
+                          void* out_bf16, float* out_rec, float* out_lse, void* stream) {
   using namespace fkv;
-  if (n_items < 0) return set_error(FKV_ERR_INVALID, "n_items < 0");
+  if (n_items < 0 || n_seg < 0) return set_error(FKV_ERR_INVALID, "fkv_decode: negative size");
   if (n_items == 0) return FKV_OK;
-  const bool fused = out_bf16 || out_rec || out_lse;
-  if (!q || !k || !v || !seg_row0 || !seg_len || !seg_qrow || !item_seg || !item_t0 || !item_t1 ||
-      !part || (fused && (!seg_out_row || !seg_item_ptr || !counters)))
+  if (!q || !k || !v || !seg_row0 || !seg_len || !seg_qrow || !seg_item_ptr || !item_seg ||
+      !item_t0 || !item_t1 || !item_order || !part || !counters ||
+      ((out_bf16 || out_rec || out_lse) && !seg_out_row))
     return set_error(FKV_ERR_INVALID, "fkv_decode: null pointer");
   if ((reinterpret_cast<uintptr_t>(k) | reinterpret_cast<uintptr_t>(v)) & 15)
     return set_error(FKV_ERR_INVALID, "fkv_decode: cache not 16-byte aligned");
   DecodeParams p{static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(k),
                  static_cast<const __nv_bfloat16*>(v), seg_row0, seg_len, seg_qrow, seg_out_row,
-                 seg_item_ptr, item_seg, item_t0, item_t1, sm_scale * kLog2e, part, counters,
-                 static_cast<__nv_bfloat16*>(out_bf16), out_rec, out_lse};
+                 seg_item_ptr, item_seg, item_t0, item_t1, item_order, n_items, n_seg,
+                 sm_scale * kLog2e, part, counters, static_cast<__nv_bfloat16*>(out_bf16),
+                 out_rec, out_lse};
   auto st = static_cast<cudaStream_t>(stream);
   switch (group) {
-    case 4: return launch_decode<4>(p, n_items, st);
-    case 8: return launch_decode<8>(p, n_items, st);
+    case 4: return launch_decode<4>(p, st);
+    case 8: return launch_decode<8>(p, st);
     default: return set_error(FKV_ERR_INVALID, "fkv_decode: group must be 4 or 8");
   }
 }
