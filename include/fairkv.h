@@ -110,12 +110,13 @@ int fkv_optimize_plan(const double* weights, int32_t num_layers, int32_t n, int3
  *   seg_item_ptr int32 [n_seg+1] items of segment s are [ptr[s], ptr[s+1])
  *   item_seg, item_t0, item_t1 int32 [n_items]: work item = tokens [t0,t1) of a
  *                segment, t0 a multiple of 16
- *   item_order   int32 [n_items]  processing order (persistent CTAs claim items
- *                from an atomic queue in this order; longest first)
+ *   warp_ptr     int32 [n_workers+1]  static schedule: persistent worker warp w
+ *                processes items [warp_ptr[w], warp_ptr[w+1]) in order
+ *                (launch: ceil(n_workers/4) CTAs of 4 warps, 2 CTAs per SM)
  *   part         f32 [n_items, group, FKV_REC]  partial records: softmax-normalised
  *                o[128] and lse = natural-log sum-exp of the scaled scores
- *   counters     int32 [n_seg + 2], zero on entry; left zero on exit (segment
- *                arrival counters + the work queue)
+ *   counters     int32 [n_seg] segment arrival counters, zero on entry; left
+ *                zero on exit
  * With all of out_bf16 / out_rec / out_lse NULL every item just writes its
  * partial record (split-K partials).  Otherwise the last CTA to finish a
  * segment merges its chunks by log-sum-exp and writes rows
@@ -127,9 +128,9 @@ int fkv_optimize_plan(const double* weights, int32_t num_layers, int32_t n, int3
 int fkv_decode(const void* q, const void* k, const void* v, const int64_t* seg_row0,
                const int32_t* seg_len, const int32_t* seg_qrow, const int32_t* seg_out_row,
                const int32_t* seg_item_ptr, const int32_t* item_seg, const int32_t* item_t0,
-               const int32_t* item_t1, const int32_t* item_order, int32_t n_items, int32_t n_seg,
-               int32_t group, float sm_scale, float* part, int32_t* counters, void* out_bf16,
-               float* out_rec, float* out_lse, void* stream);
+               const int32_t* item_t1, const int32_t* warp_ptr, int32_t n_workers,
+               int32_t n_items, int32_t n_seg, int32_t group, float sm_scale, float* part,
+               int32_t* counters, void* out_bf16, float* out_rec, float* out_lse, void* stream);
 
 /* K5: log-sum-exp merge of partial records.  Output group g merges records
  * src_idx[grp_ptr[g] .. grp_ptr[g+1]) (each `group` heads of FKV_REC floats)

@@ -7,7 +7,8 @@ HBM layout (include/fairkv.h):
              [seg_row0[s], seg_row0[s] + seg_len[s]), seg_row0 % PAGE == 0,
              padding rows up to the next page are zero
 Work plan (built on the host once per cache, uploaded once):
-  items      chunks [t0, t1) of segments, ~equal size, t0 % 16 == 0
+  items      pieces [t0, t1) of segments, t0 % 16 == 0, dealt to the persistent
+             decode warps so every warp streams the same number of tiles
   groups     one per segment: items of the segment are merged by LSE into the
              segment's output rows (o rows = seg_out_row .. + G - 1)
 """
@@ -21,9 +22,7 @@ import torch
 
 HEAD_DIM = 128
 PAGE = 64
-CHUNK_QUANTUM = 16  # one 16-token tile
 NUM_SMS = 148
-WORKERS = NUM_SMS * 8  # persistent decode warps (2 CTAs x 4 warps per SM)
 
 
 def page_rows(n_tok) -> np.ndarray:
@@ -41,37 +40,82 @@ def segment_offsets(seg_len) -> tuple[np.ndarray, int]:
     return row0, max(total, PAGE)
 
 
-def choose_chunk(seg_len, target_items: int | None = None, max_chunk: int = 2048,
-                 min_chunk: int = 128) -> int:
-    """Tokens per work item for the warp-persistent decode kernel: about
-    three items per worker warp (the longest-first queue then drains with a
-    short tail), at least ``min_chunk`` tokens so the per-item record/merge
-    overhead stays a few percent, multiple of the 16-token tile."""
-    total = int(np.asarray(seg_len, dtype=np.int64).sum())
-    target = target_items or WORKERS * 3
-    c = -(-total // max(target, 1))
-    c = -(-c // CHUNK_QUANTUM) * CHUNK_QUANTUM
-    return int(min(max(c, min_chunk), max_chunk))
+MAX_ITEMS_PER_SEGMENT = 32  # kMergeMax in decode.cu
+TILE = 16
 
 
-def longest_first(t0, t1) -> np.ndarray:
-    """Item processing order for the persistent decode kernel: longest
-    first (LPT), ties by item id, so the queue drains with a short tail."""
-    n = np.asarray(t1, dtype=np.int64) - np.asarray(t0, dtype=np.int64)
-    return np.lexsort((np.arange(len(n)), -n)).astype(np.int32)
+def default_workers(device=None) -> int:
+    """Persistent decode warps: 2 CTAs x 4 warps on every SM."""
+    try:
+        sms = torch.cuda.get_device_properties(device).multi_processor_count
+    except Exception:  # no device visible (host-side planning / CPU tests)
+        sms = NUM_SMS
+    return sms * 8
 
 
-def plan_items(seg_len, chunk: int) -> tuple[np.ndarray, np.ndarray, np.ndarray, np.ndarray]:
-    """-> item_seg, item_t0, item_t1 (int32) and per-segment item CSR ptr."""
+def plan_work(seg_len, n_workers: int, chunk: int | None = None):
+    """Static decode schedule.
+
+    The segments' 16-token tiles are laid end to end and the stream is cut
+    into n_workers equal ranges (``chunk=None``), or every segment is cut into
+    ``chunk``-token pieces and consecutive pieces are dealt to workers by
+    equal token count.  Either way a piece never straddles a worker, pieces of
+    a segment are consecutive item ids, and every segment has at least one
+    item (an empty one still produces o = 0, lse = -inf).
+
+    Returns item_seg, item_t0, item_t1 (int32), seg_item_ptr (int32
+    [n_seg+1]) and warp_ptr (int32 [n_workers+1]).
+    """
     seg_len = np.asarray(seg_len, dtype=np.int64)
-    counts = np.maximum(1, -(-seg_len // chunk))  # an empty segment still gets one item
-    ptr = np.zeros(len(seg_len) + 1, dtype=np.int32)
-    ptr[1:] = np.cumsum(counts)
-    item_seg = np.repeat(np.arange(len(seg_len), dtype=np.int32), counts)
-    local = np.arange(ptr[-1], dtype=np.int64) - np.repeat(ptr[:-1], counts)
-    t0 = (local * chunk).astype(np.int32)
-    t1 = np.minimum(t0.astype(np.int64) + chunk, seg_len[item_seg]).astype(np.int32)
-    return item_seg, t0, t1, ptr
+    n_seg = len(seg_len)
+    tiles = (seg_len + TILE - 1) // TILE
+    total = int(tiles.sum())
+    W = max(1, int(n_workers))
+    if chunk is None:
+        per = max(1, -(-total // W))
+        longest = int(tiles.max()) if n_seg else 0
+        per = max(per, -(-longest // (MAX_ITEMS_PER_SEGMENT - 1)))
+        start = np.zeros(n_seg, dtype=np.int64)
+        if n_seg:
+            start[1:] = np.cumsum(tiles)[:-1]
+        seg_i, t0s, t1s, owner = [], [], [], []
+        for s in range(n_seg):
+            a, n = int(start[s]), int(tiles[s])
+            cut = a
+            while True:
+                nxt = min(a + n, (cut // per + 1) * per)
+                seg_i.append(s)
+                t0s.append((cut - a) * TILE)
+                t1s.append(min(int(seg_len[s]), (nxt - a) * TILE))
+                owner.append(min(cut // per, W - 1))
+                if nxt >= a + n:
+                    break
+                cut = nxt
+    else:
+        ch = max(TILE, -(-int(chunk) // TILE) * TILE)
+        longest = int(seg_len.max()) if n_seg else 0
+        need = -(-longest // MAX_ITEMS_PER_SEGMENT)  # keep <= MAX_ITEMS_PER_SEGMENT pieces
+        ch = max(ch, -(-need // TILE) * TILE)
+        counts = np.maximum(1, -(-seg_len // ch))
+        seg_i = np.repeat(np.arange(n_seg), counts)
+        ptr0 = np.zeros(n_seg + 1, dtype=np.int64)
+        ptr0[1:] = np.cumsum(counts)
+        local = np.arange(ptr0[-1]) - np.repeat(ptr0[:-1], counts)
+        t0s = local * ch
+        t1s = np.minimum(t0s + ch, seg_len[seg_i])
+        lens = np.maximum(t1s - t0s, 0)
+        cum = np.concatenate([[0], np.cumsum(lens)[:-1]])
+        per = max(1, -(-int(lens.sum()) // W))
+        owner = np.minimum(cum // per, W - 1)
+    item_seg = np.asarray(seg_i, dtype=np.int32)
+    t0 = np.asarray(t0s, dtype=np.int32)
+    t1 = np.asarray(t1s, dtype=np.int32)
+    owner = np.asarray(owner, dtype=np.int64)
+    seg_item_ptr = np.zeros(n_seg + 1, dtype=np.int32)
+    seg_item_ptr[1:] = np.cumsum(np.bincount(item_seg, minlength=n_seg))
+    warp_ptr = np.zeros(W + 1, dtype=np.int32)
+    warp_ptr[1:] = np.cumsum(np.bincount(owner, minlength=W))
+    return item_seg, t0, t1, seg_item_ptr, warp_ptr
 
 
 @dataclass
@@ -90,7 +134,7 @@ class LayerCache:
     item_t1: torch.Tensor
     grp_ptr: torch.Tensor
     src_idx: torch.Tensor
-    item_order: torch.Tensor
+    warp_ptr: torch.Tensor
     counters: torch.Tensor
     host: dict = field(default_factory=dict, repr=False)
 
@@ -120,9 +164,8 @@ class LayerCache:
         rows zero."""
         seg_len = np.asarray(seg_len, dtype=np.int64)
         row0, rows = segment_offsets(seg_len)
-        chunk = chunk or choose_chunk(seg_len)
-        item_seg, t0, t1, ptr = plan_items(seg_len, chunk)
         dev = torch.device(device)
+        item_seg, t0, t1, ptr, wptr = plan_work(seg_len, default_workers(dev), chunk)
         k = torch.zeros((rows, HEAD_DIM), dtype=torch.bfloat16, device=dev)
         v = torch.zeros((rows, HEAD_DIM), dtype=torch.bfloat16, device=dev)
         if fill == "random":
@@ -145,9 +188,9 @@ class LayerCache:
             seg_len=i32(seg_len), seg_qrow=i32(seg_qrow), seg_out_row=i32(seg_out_row),
             item_seg=i32(item_seg), item_t0=i32(t0), item_t1=i32(t1),
             grp_ptr=i32(ptr), src_idx=i32(np.arange(ptr[-1])),
-            item_order=i32(longest_first(t0, t1)),
-            counters=torch.zeros(len(seg_len) + 2, dtype=torch.int32, device=dev),
-            host={"seg_len": seg_len, "seg_row0": row0, "chunk": chunk,
+            warp_ptr=i32(wptr),
+            counters=torch.zeros(max(len(seg_len), 1), dtype=torch.int32, device=dev),
+            host={"seg_len": seg_len, "seg_row0": row0, "chunk": chunk, "n_workers": len(wptr) - 1,
                   "seg_qrow": np.asarray(seg_qrow), "seg_out_row": np.asarray(seg_out_row)},
         )
 
@@ -161,9 +204,8 @@ class LayerCache:
         seg_len = np.asarray(seg_len, dtype=np.int64)
         if np.any(seg_row0 % 16):
             raise ValueError("segment starts must be multiples of 16 rows")
-        chunk = chunk or choose_chunk(seg_len)
-        item_seg, t0, t1, ptr = plan_items(seg_len, chunk)
         dev = k.device
+        item_seg, t0, t1, ptr, wptr = plan_work(seg_len, default_workers(dev), chunk)
 
         def i32(a):
             return torch.as_tensor(np.ascontiguousarray(a, dtype=np.int32), device=dev)
@@ -173,8 +215,8 @@ class LayerCache:
             seg_len=i32(seg_len), seg_qrow=i32(seg_qrow), seg_out_row=i32(seg_out_row),
             item_seg=i32(item_seg), item_t0=i32(t0), item_t1=i32(t1), grp_ptr=i32(ptr),
             src_idx=i32(np.arange(ptr[-1])),
-            item_order=i32(longest_first(t0, t1)),
-            counters=torch.zeros(len(seg_len) + 2, dtype=torch.int32, device=dev),
-            host={"seg_len": seg_len, "seg_row0": seg_row0, "chunk": chunk,
+            warp_ptr=i32(wptr),
+            counters=torch.zeros(max(len(seg_len), 1), dtype=torch.int32, device=dev),
+            host={"seg_len": seg_len, "seg_row0": seg_row0, "chunk": chunk, "n_workers": len(wptr) - 1,
                   "seg_qrow": np.asarray(seg_qrow), "seg_out_row": np.asarray(seg_out_row)},
         )

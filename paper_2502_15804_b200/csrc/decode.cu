@@ -5,15 +5,15 @@
 // this kernel's time as c0 + c1*B + c2*C + c3*B*C (pkg/src/headbalance/latency.py:85-91).
 //
 // Design:
-//  * every warp is an independent persistent worker: it claims work items
-//    (chunks of segments, host-sorted longest first) from an atomic queue and
-//    never synchronises with the other warps of its CTA -- no block barriers
-//    anywhere.  The queue resets itself when the last warp leaves, so a
-//    captured CUDA graph can replay;
+//  * every warp is an independent persistent worker with a static, host-built
+//    schedule: the concatenated 16-token tile stream of all segments is cut
+//    into equal ranges, one per worker warp (so every warp streams the same
+//    number of bytes), and a warp never synchronises with the other warps of
+//    its CTA -- no block barriers anywhere;
 //  * each warp runs its own S-stage TMA bulk-copy ring (cp.async.bulk +
 //    mbarrier, 16-token K+V tiles of 8 KiB) that streams ACROSS item
-//    boundaries: the producer lane claims the next item and lands its first
-//    tiles while the warp is still finishing the current one;
+//    boundaries: the producer lane lands the first tiles of the next item
+//    while the warp is still finishing the current one;
 //  * the cache rows are stored pre-swizzled in HBM, so a 1-D bulk copy lands
 //    a bank-conflict-free tile for ldmatrix -- no tensor map, no address math;
 //  * GQA: every K/V tile is read once for all G query heads.  S^T = K Q^T
@@ -37,7 +37,7 @@ constexpr int kTileTok = 16;
 constexpr int kTileBytes = kTileTok * FKV_HEAD_DIM * 2;  // 4 KiB per K or V tile
 constexpr int kRingBytes = kStages * 2 * kTileBytes;     // per warp
 constexpr int kSmemBytes = kWarps * kRingBytes;
-constexpr int kQueue = 4;                                // claimed-item ring per warp (> kStages)
+constexpr int kMergeMax = 32;                            // max items per segment (host-enforced)
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 
@@ -53,11 +53,11 @@ struct DecodeParams {
   const int32_t* item_seg;
   const int32_t* item_t0;
   const int32_t* item_t1;
-  const int32_t* item_order;  // processing order (longest first)
-  int n_items, n_seg;
+  const int32_t* warp_ptr;  // worker w processes items [warp_ptr[w], warp_ptr[w+1])
+  int n_items, n_seg, n_workers;
   float scale_log2;
   float* part;        // [n_items, G, FKV_REC] partial records (multi-item segments)
-  int32_t* counters;  // [n_seg] segment arrivals + [2] work queue; zero between launches
+  int32_t* counters;  // [n_seg] segment arrival counters; zero between launches
   __nv_bfloat16* out_bf16;
   float* out_rec;
   float* out_lse;
@@ -75,13 +75,14 @@ template <int G>
 __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodeParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bars[kWarps][kStages];
-  __shared__ int queue[kWarps][kQueue];
+  __shared__ float scratch[kWarps][kMergeMax * 8];
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   uint8_t* ring = smem + warp * kRingBytes;
-  int* q_items = queue[warp];
-  int* work = p.counters + p.n_seg;
+  const int worker = blockIdx.x * kWarps + warp;
+  const int w_beg = worker < p.n_workers ? p.warp_ptr[worker] : 0;
+  const int w_end = worker < p.n_workers ? p.warp_ptr[worker + 1] : 0;
 
   if (lane == 0) {
     for (int s = 0; s < kStages; ++s) mbar_init(&bars[warp][s], 1);
@@ -89,43 +90,34 @@ __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodePara
   }
   __syncwarp();
 
-  // Claimed items: ordinals 0..claimed live in q_items[ord % kQueue].
-  int claimed = -1;
-  auto claim_next = [&]() {
-    int it = -1;
-    if (lane == 0) {
-      const int x = atomicAdd(work, 1);
-      it = x < p.n_items ? p.item_order[x] : -1;
-      q_items[(claimed + 1) % kQueue] = it;
-    }
-    __syncwarp();
-    ++claimed;
-  };
-  auto item_at = [&](int ord) -> int {
-    while (claimed < ord) claim_next();
-    return q_items[ord % kQueue];
-  };
+  auto item_at = [&](int ord) -> int { return w_beg + ord < w_end ? w_beg + ord : -1; };
 
   int p_ord = 0, p_t = 0;  // producer cursor: item ordinal, tile within item
+  int p_nt = -1;           // cached tile count / row of the producer's item (-1: reload)
+  int64_t p_row = 0;
   uint32_t p_seq = 0, c_seq = 0;
   bool p_done = false;
   auto refill = [&]() {
     while (!p_done && p_seq - c_seq < kStages) {
-      const int it = item_at(p_ord);
-      if (it < 0) {
-        p_done = true;
-        break;
+      if (p_nt < 0) {
+        const int it = item_at(p_ord);
+        if (it < 0) {
+          p_done = true;
+          break;
+        }
+        int t0, t1, seg;
+        p_nt = n_tiles_of(p, it, t0, t1, seg);
+        p_row = p.seg_row0[seg] + t0;
       }
-      int t0, t1, seg;
-      const int nt = n_tiles_of(p, it, t0, t1, seg);
-      if (p_t >= nt) {
+      if (p_t >= p_nt) {
         ++p_ord;
         p_t = 0;
+        p_nt = -1;
         continue;
       }
       if (lane == 0) {
         const int s = p_seq % kStages;
-        const int64_t row = p.seg_row0[seg] + t0 + kTileTok * p_t;
+        const int64_t row = p_row + kTileTok * p_t;
         uint8_t* dst = ring + s * 2 * kTileBytes;
         mbar_arrive_expect_tx(&bars[warp][s], 2 * kTileBytes);
         bulk_g2s(dst, p.k + row * FKV_HEAD_DIM, kTileBytes, &bars[warp][s]);
@@ -142,27 +134,36 @@ __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodePara
   const int dr = lane >> 2;
   const bool fused = p.out_bf16 || p.out_rec || p.out_lse;
 
+  uint32_t qn[8][2];  // q fragments of the next item, loaded one item ahead
+  auto load_q = [&](int it) {
+    const int n = lane >> 2, kq = 2 * (lane & 3);
+    if (it >= 0 && n < G) {
+      const __nv_bfloat16* qr =
+          p.q + static_cast<int64_t>(p.seg_qrow[p.item_seg[it]] + n) * FKV_HEAD_DIM;
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        qn[kk][0] = __ldg(reinterpret_cast<const unsigned int*>(qr + 16 * kk + kq));
+        qn[kk][1] = __ldg(reinterpret_cast<const unsigned int*>(qr + 16 * kk + 8 + kq));
+      }
+    } else {
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) qn[kk][0] = qn[kk][1] = 0u;
+    }
+  };
+  load_q(item_at(0));
+
   for (int ord = 0;; ++ord) {
     const int it = item_at(ord);
     if (it < 0) break;
     int t0, t1, seg;
     const int nt = n_tiles_of(p, it, t0, t1, seg);
 
-    // Q^T as the B operand (k = head_dim, n = query head), in registers.
+    // Q^T (B operand: k = head_dim, n = query head) was prefetched into qn
     uint32_t qb[8][2];
-    {
-      const int n = lane >> 2, kq = 2 * (lane & 3);
-      if (n < G) {
-        const __nv_bfloat16* qr = p.q + static_cast<int64_t>(p.seg_qrow[seg] + n) * FKV_HEAD_DIM;
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          qb[kk][0] = __ldg(reinterpret_cast<const unsigned int*>(qr + 16 * kk + kq));
-          qb[kk][1] = __ldg(reinterpret_cast<const unsigned int*>(qr + 16 * kk + 8 + kq));
-        }
-      } else {
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) qb[kk][0] = qb[kk][1] = 0u;
-      }
+    for (int kk = 0; kk < 8; ++kk) {
+      qb[kk][0] = qn[kk][0];
+      qb[kk][1] = qn[kk][1];
     }
 
     float m0 = -CUDART_INF_F, m1 = -CUDART_INF_F;  // running max (log2 domain), heads h0, h1
@@ -229,6 +230,8 @@ __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodePara
       ++c_seq;
       refill();
     }
+
+    load_q(item_at(ord + 1));  // overlaps the epilogue below
 
     // ---- finalise this item from registers
 #pragma unroll
@@ -310,59 +313,60 @@ __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodePara
     last = __shfl_sync(0xffffffffu, last, 0);
     if (!last) continue;
     __threadfence();
+    // All (item, head) lse values in one parallel round trip, weights in the
+    // warp's scratch, then every lane streams its 4 head_dim columns of all
+    // records with n_it*G independent 16-B loads.
     const float* base = p.part + static_cast<int64_t>(i0) * G * FKV_REC;
-#pragma unroll 1
-    for (int g = 0; g < G; ++g) {
-      // weights: lane i holds item i's lse (segments have <= a few dozen items)
+    float* sw = scratch[warp];
+    for (int x = lane; x < n_it * G; x += 32) sw[x] = __ldcg(base + x * FKV_REC + FKV_HEAD_DIM);
+    __syncwarp();
+    float lse_g = -CUDART_INF_F;
+    if (lane < G) {
       float M = -CUDART_INF_F;
-      for (int i = lane; i < n_it; i += 32) M = fmaxf(M, __ldcg(base + (i * G + g) * FKV_REC + FKV_HEAD_DIM));
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+      for (int i = 0; i < n_it; ++i) M = fmaxf(M, sw[i * G + lane]);
       float S = 0.f;
-      float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (M != -CUDART_INF_F) {
-#pragma unroll 4
-        for (int i = 0; i < n_it; ++i) {
-          const float* r = base + (i * G + g) * FKV_REC;
-          const float w = __expf(__ldcg(r + FKV_HEAD_DIM) - M);
-          const float4 v4 = __ldcg(reinterpret_cast<const float4*>(r) + lane);
-          S += w;
-          o.x = fmaf(w, v4.x, o.x);
-          o.y = fmaf(w, v4.y, o.y);
-          o.z = fmaf(w, v4.z, o.z);
-          o.w = fmaf(w, v4.w, o.w);
-        }
-      }
+      if (M != -CUDART_INF_F)
+        for (int i = 0; i < n_it; ++i) S += __expf(sw[i * G + lane] - M);
       const float inv = S > 0.f ? 1.f / S : 0.f;
-      o.x *= inv;
-      o.y *= inv;
-      o.z *= inv;
-      o.w *= inv;
-      const float lse = S > 0.f ? M + __logf(S) : -CUDART_INF_F;
+      for (int i = 0; i < n_it; ++i)
+        sw[i * G + lane] = M != -CUDART_INF_F ? __expf(sw[i * G + lane] - M) * inv : 0.f;
+      lse_g = S > 0.f ? M + __logf(S) : -CUDART_INF_F;
+    }
+    __syncwarp();
+    float4 o[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) o[g] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 2
+    for (int i = 0; i < n_it; ++i) {
+      float4 v4[G];
+#pragma unroll
+      for (int g = 0; g < G; ++g) v4[g] = __ldcg(reinterpret_cast<const float4*>(base + (i * G + g) * FKV_REC) + lane);
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const float w = sw[i * G + g];
+        o[g].x = fmaf(w, v4[g].x, o[g].x);
+        o[g].y = fmaf(w, v4[g].y, o[g].y);
+        o[g].z = fmaf(w, v4[g].z, o[g].z);
+        o[g].w = fmaf(w, v4[g].w, o[g].w);
+      }
+    }
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
       const int64_t row = orow + g;
       if (p.out_bf16) {
         __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(p.out_bf16 + row * FKV_HEAD_DIM) + 2 * lane;
-        ob[0] = __floats2bfloat162_rn(o.x, o.y);
-        ob[1] = __floats2bfloat162_rn(o.z, o.w);
+        ob[0] = __floats2bfloat162_rn(o[g].x, o[g].y);
+        ob[1] = __floats2bfloat162_rn(o[g].z, o[g].w);
       }
-      if (p.out_rec) {
-        reinterpret_cast<float4*>(p.out_rec + row * FKV_REC)[lane] = o;
-        if (lane == 0) p.out_rec[row * FKV_REC + FKV_HEAD_DIM] = lse;
-      }
-      if (p.out_lse && lane == 0) p.out_lse[row] = lse;
+      if (p.out_rec) reinterpret_cast<float4*>(p.out_rec + row * FKV_REC)[lane] = o[g];
+    }
+    if (lane < G) {
+      if (p.out_rec) p.out_rec[(orow + lane) * FKV_REC + FKV_HEAD_DIM] = lse_g;
+      if (p.out_lse) p.out_lse[orow + lane] = lse_g;
     }
     if (lane == 0) p.counters[seg] = 0;  // ready for the next launch / graph replay
   }
 
-  // the last warp out resets the work queue for the next launch / graph replay
-  if (lane == 0) {
-    __threadfence();
-    if (atomicAdd(work + 1, 1) == static_cast<int>(gridDim.x) * kWarps - 1) {
-      work[0] = 0;
-      work[1] = 0;
-      __threadfence();
-    }
-  }
 }
 
 // K5 standalone (after the all-gather): warp g of the CTA merges head g of
@@ -427,7 +431,8 @@ int launch_decode(const DecodeParams& p, cudaStream_t st) {
                                                   kSmemBytes);
     grid_cap = sms * (per_sm > 0 ? per_sm : 1);
   }
-  const int grid = p.n_items < grid_cap ? p.n_items : grid_cap;
+  (void)grid_cap;
+  const int grid = (p.n_workers + kWarps - 1) / kWarps;
   decode_kernel<G><<<grid, kWarps * 32, kSmemBytes, st>>>(p);
   return cuda_check(cudaGetLastError(), "decode launch");
 }
@@ -439,21 +444,22 @@ extern "C" int fkv_decode(const void* q, const void* k, const void* v, const int
                           const int32_t* seg_len, const int32_t* seg_qrow,
                           const int32_t* seg_out_row, const int32_t* seg_item_ptr,
                           const int32_t* item_seg, const int32_t* item_t0, const int32_t* item_t1,
-                          const int32_t* item_order, int32_t n_items, int32_t n_seg,
+                          const int32_t* warp_ptr, int32_t n_workers, int32_t n_items,
+                          int32_t n_seg,
                           int32_t group, float sm_scale, float* part, int32_t* counters,
                           void* out_bf16, float* out_rec, float* out_lse, void* stream) {
   using namespace fkv;
   if (n_items < 0 || n_seg < 0) return set_error(FKV_ERR_INVALID, "fkv_decode: negative size");
   if (n_items == 0) return FKV_OK;
   if (!q || !k || !v || !seg_row0 || !seg_len || !seg_qrow || !seg_item_ptr || !item_seg ||
-      !item_t0 || !item_t1 || !item_order || !part || !counters ||
+      !item_t0 || !item_t1 || !warp_ptr || n_workers < 1 || !part || !counters ||
       ((out_bf16 || out_rec || out_lse) && !seg_out_row))
     return set_error(FKV_ERR_INVALID, "fkv_decode: null pointer");
   if ((reinterpret_cast<uintptr_t>(k) | reinterpret_cast<uintptr_t>(v)) & 15)
     return set_error(FKV_ERR_INVALID, "fkv_decode: cache not 16-byte aligned");
   DecodeParams p{static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(k),
                  static_cast<const __nv_bfloat16*>(v), seg_row0, seg_len, seg_qrow, seg_out_row,
-                 seg_item_ptr, item_seg, item_t0, item_t1, item_order, n_items, n_seg,
+                 seg_item_ptr, item_seg, item_t0, item_t1, warp_ptr, n_items, n_seg, n_workers,
                  sm_scale * kLog2e, part, counters, static_cast<__nv_bfloat16*>(out_bf16),
                  out_rec, out_lse};
   auto st = static_cast<cudaStream_t>(stream);

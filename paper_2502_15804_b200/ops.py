@@ -64,8 +64,8 @@ def _decode(q, cache: LayerCache, ws: DecodeWorkspace | None, sm_scale, out_bf16
         q.data_ptr(), cache.k.data_ptr(), cache.v.data_ptr(), cache.seg_row0.data_ptr(),
         cache.seg_len.data_ptr(), cache.seg_qrow.data_ptr(), cache.seg_out_row.data_ptr(),
         cache.grp_ptr.data_ptr(), cache.item_seg.data_ptr(), cache.item_t0.data_ptr(),
-        cache.item_t1.data_ptr(), cache.item_order.data_ptr(), cache.n_items, cache.n_segments,
-        cache.group, scale, ws.part.data_ptr(),
+        cache.item_t1.data_ptr(), cache.warp_ptr.data_ptr(), int(cache.warp_ptr.shape[0]) - 1,
+        cache.n_items, cache.n_segments, cache.group, scale, ws.part.data_ptr(),
         cache.counters.data_ptr(), _p(out_bf16), _p(out_rec), _p(out_lse), _stream()))
     return ws.part
 

@@ -15,7 +15,7 @@ hq = hkv * G
 qrow = [b * hq + h * G for b in range(bt) for h in range(hkv)]
 q = torch.randn(bt, hq, 128, device=dev).to(torch.bfloat16)
 o = torch.empty_like(q)
-for chunk in (None, 64, 128, 192, 256, 384, 512, 1024):
+for chunk in (None, 128, 256, 512, 1024):
     cache = LayerCache.allocate(lens, qrow, qrow, G, dev, chunk=chunk, fill='random')
     ws = ops.DecodeWorkspace(cache)
     for mode in ("partial", "fused"):
@@ -30,5 +30,5 @@ for chunk in (None, 64, 128, 192, 256, 384, 512, 1024):
         e0.record(); g.replay(); e1.record(); torch.cuda.synchronize()
         t = e0.elapsed_time(e1) / 20 * 1e-3
         byts = cache.kv_bytes()
-        print(f"bt={bt} B={B} chunk={cache.host['chunk']:5d} items={cache.n_items:5d} {mode:7s} "
+        print(f"bt={bt} B={B} chunk={str(cache.host['chunk']):>5s} items={cache.n_items:5d} {mode:7s} "
               f"kv={byts/1e6:.1f}MB t={t*1e6:.1f}us {byts/t/1e9:.0f} GB/s (KV only)")
