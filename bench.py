@@ -59,6 +59,8 @@ def parse():
     p.add_argument("--no-emulate", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--seed", type=int, default=0)
+    p.add_argument("--exchange", choices=["p2p", "nccl"], default="p2p",
+                   help="N>1 per-layer exchange: fused NVLink P2P stores (default) or NCCL all-gather")
     return p.parse_args()
 
 
@@ -234,7 +236,12 @@ def run_fairkv(args):
     shards, finals = plan_layouts(plan, budgets, GROUP)
     my = [s[rank] for s in shards]
     caches = rank_caches(my, args.batch, HQ, GROUP, tp, dev, fill="random", seed=args.seed + rank)
-    dec = StackDecoder(caches, finals if tp > 1 else None, tp=tp, bt=args.batch, hq=HQ, group=GROUP)
+    endpoint = None
+    if tp > 1 and args.exchange == "p2p":
+        from paper_2502_15804_b200.exchange import P2PGroup
+        endpoint = P2PGroup.connect(rank, tp, finals[0].slots, GROUP).endpoints[0]
+    dec = StackDecoder(caches, finals if tp > 1 else None, tp=tp, bt=args.batch, hq=HQ, group=GROUP,
+                       exchange=args.exchange, endpoint=endpoint)
     gq = torch.Generator(device=dev).manual_seed(123)
     q = torch.randn((args.layers, args.batch, HQ, HEAD_DIM), generator=gq, device=dev).to(torch.bfloat16)
     o = torch.empty_like(q)
@@ -345,7 +352,8 @@ def run_fairkv(args):
             "layers": args.layers,
             "avg_budget": args.budget,
             "context": args.context,
-            "parallelism": f"tp{tp} ({'uniform head-sharded' if mode == 'sha' else 'AHA-' + mode + f' CH={args.ch}'})",
+            "parallelism": f"tp{tp} ({'uniform head-sharded' if mode == 'sha' else 'AHA-' + mode + f' CH={args.ch}'})"
+                           + (f", exchange {args.exchange}" if tp > 1 else ""),
             "l2": f"inputs larger than L2: {dec.kv_bytes() / 1e9:.1f} GB KV read per step per GPU",
             "graph": tp == 1,
         },
@@ -354,7 +362,7 @@ def run_fairkv(args):
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "fkv decode_kernel<8> (K4, partial-record mode)",
+                     "kernel": "fkv decode_kernel<8> (K4 with fused LSE merge)",
                      "bytes_per_launch": bytes_k4, "us_per_launch": t4 * 1e6,
                      "k4_share_of_step": (t4 * args.layers) / (t / args.steps),
                      "bytes_note": "retained K+V + q + o + chunk partial records (write+read)",

@@ -54,6 +54,7 @@ extern "C" {
 #define FKV_PAGE 64 /* tokens per page; segment starts are page aligned */
 #define FKV_SPLIT 16 /* DP-copy token cuts are multiples of this (16-token tiles) */
 #define FKV_REC 132 /* floats per partial record: o[128], lse, 3 pad (16-B aligned) */
+#define FKV_MAX_PEERS 8 /* GPUs of one NVLink/NVSwitch node */
 
 const char* fkv_last_error(void);
 int fkv_version(void);
@@ -110,9 +111,11 @@ int fkv_optimize_plan(const double* weights, int32_t num_layers, int32_t n, int3
  *   seg_item_ptr int32 [n_seg+1] items of segment s are [ptr[s], ptr[s+1])
  *   item_seg, item_t0, item_t1 int32 [n_items]: work item = tokens [t0,t1) of a
  *                segment, t0 a multiple of 16
- *   warp_ptr     int32 [n_workers+1]  static schedule: persistent worker warp w
- *                processes items [warp_ptr[w], warp_ptr[w+1]) in order
- *                (launch: ceil(n_workers/4) CTAs of 4 warps, 2 CTAs per SM)
+ *   warp_ptr     int32 [n_workers+1], work_list int32 [n_items]: static
+ *                schedule -- persistent worker w processes items
+ *                work_list[warp_ptr[w] .. warp_ptr[w+1]) in order; worker w is
+ *                warp (w / grid) of CTA (w % grid), grid = ceil(n_workers/4),
+ *                so short schedules still spread over every SM
  *   part         f32 [n_items, group, FKV_REC]  partial records: softmax-normalised
  *                o[128] and lse = natural-log sum-exp of the scaled scores
  *   counters     int32 [n_seg] segment arrival counters, zero on entry; left
@@ -128,9 +131,10 @@ int fkv_optimize_plan(const double* weights, int32_t num_layers, int32_t n, int3
 int fkv_decode(const void* q, const void* k, const void* v, const int64_t* seg_row0,
                const int32_t* seg_len, const int32_t* seg_qrow, const int32_t* seg_out_row,
                const int32_t* seg_item_ptr, const int32_t* item_seg, const int32_t* item_t0,
-               const int32_t* item_t1, const int32_t* warp_ptr, int32_t n_workers,
-               int32_t n_items, int32_t n_seg, int32_t group, float sm_scale, float* part,
-               int32_t* counters, void* out_bf16, float* out_rec, float* out_lse, void* stream);
+               const int32_t* item_t1, const int32_t* warp_ptr, const int32_t* work_list,
+               int32_t n_workers, int32_t n_items, int32_t n_seg, int32_t group, float sm_scale,
+               float* part, int32_t* counters, void* out_bf16, float* out_rec, float* out_lse,
+               void* stream);
 
 /* K5: log-sum-exp merge of partial records.  Output group g merges records
  * src_idx[grp_ptr[g] .. grp_ptr[g+1]) (each `group` heads of FKV_REC floats)
@@ -143,6 +147,39 @@ int fkv_decode(const void* q, const void* k, const void* v, const int64_t* seg_r
 int fkv_merge_lse(const float* part, const int32_t* grp_ptr, const int32_t* src_idx,
                   const int32_t* out_row, int32_t n_groups, int32_t group, void* out_bf16,
                   float* out_rec, float* out_lse, void* stream);
+
+/* Fused NVLink all-gather variant of fkv_decode (same tables).  Every
+ * segment's final record is written to all n_rec destinations (each peer's
+ * receive block for this rank, mapped with fkv_ipc_open; P2P stores over
+ * NVLink) instead of one local slot array, and when the last warp finishes,
+ * after a system-scope fence, it atomically increments sig_flags[j][my_rank]
+ * in every peer's memory (n_sig peers).  sig_done: local int32, zero between
+ * launches.  Replaces NCCL all_gather for the per-layer exchange. */
+int fkv_decode_exchange(const void* q, const void* k, const void* v, const int64_t* seg_row0,
+                        const int32_t* seg_len, const int32_t* seg_qrow, const int32_t* seg_out_row,
+                        const int32_t* seg_item_ptr, const int32_t* item_seg,
+                        const int32_t* item_t0, const int32_t* item_t1, const int32_t* warp_ptr,
+                        const int32_t* work_list, int32_t n_workers, int32_t n_items,
+                        int32_t n_seg, int32_t group,
+                        float sm_scale, float* part, int32_t* counters, void* out_bf16,
+                        float* const* out_recs, int32_t n_rec, float* out_lse, int32_t* sig_done,
+                        int32_t* const* sig_flags, int32_t n_sig, int32_t my_rank, void* stream);
+
+/* fkv_merge_lse preceded by the consumer side of the fused all-gather: every
+ * CTA waits (acquire, system scope) until flags[r] >= consumed[0] + 1 for all
+ * r < tp, merges, and the last CTA advances consumed[0] (consumed[1] is its
+ * arrival counter, zero between launches).  flags == NULL: plain merge. */
+int fkv_merge_wait(const float* part, const int32_t* grp_ptr, const int32_t* src_idx,
+                   const int32_t* out_row, int32_t n_groups, int32_t group, void* out_bf16,
+                   float* out_rec, float* out_lse, const int32_t* flags, int32_t tp,
+                   int32_t* consumed, void* stream);
+
+/* Device memory that can be shared with the other GPUs of the node. */
+int fkv_dev_alloc(int64_t bytes, void** out_ptr);
+int fkv_dev_free(void* ptr);
+int fkv_ipc_get(void* dev_ptr, void* handle /* 64 bytes */);
+int fkv_ipc_open(const void* handle, void** out_ptr);
+int fkv_ipc_close(void* ptr);
 
 /* ------------------------------------------- B3 compression (prefill) -- */
 
@@ -172,6 +209,14 @@ int fkv_ada_budgets(const float* scores, int32_t batch, int32_t hkv, int32_t n, 
  * offsets int64 [batch*hkv + 1] is the exclusive prefix sum of budgets. */
 int fkv_topk_select(const float* scores, const int32_t* budgets, int32_t batch, int32_t hkv,
                     int32_t n, int32_t window, int64_t* offsets, int32_t* idx, void* stream);
+
+/* A18 + K2 fused: one thread-block cluster per request (one CTA per KV head,
+ * Hkv <= 8) computes the budgets, the offsets (request b starts at
+ * b*hkv*budget) and the ascending index lists in a single launch; results are
+ * identical to fkv_ada_budgets followed by fkv_topk_select. */
+int fkv_ada_select(const float* scores, int32_t batch, int32_t hkv, int32_t n, int32_t budget,
+                   int32_t window, int32_t floor_k, int32_t* budgets, int64_t* offsets,
+                   int32_t* idx, void* stream);
 
 /* K3: compaction.  For each destination segment s, rows j in [seg_lo, seg_hi)
  * of head seg_bh[s]'s selection are copied from k_src/v_src (bf16

@@ -37,13 +37,24 @@ _SIGS = {
                                   _vp, _vp, _vp, _vp, _vp]),
     "fkv_optimize_plan": (C.c_int, [_vp, _i32, _i32, _i32, _i32, _i32, _i32, _i64, _i64, _i32,
                                     _vp, _vp, _vp, _vp, _vp]),
-    "fkv_decode": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32,
-                             _i32, _i32, _i32, _f32, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "fkv_decode": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                             _i32, _i32, _i32, _i32, _f32, _vp, _vp, _vp, _vp, _vp, _vp]),
     "fkv_merge_lse": (C.c_int, [_vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp]),
+    "fkv_decode_exchange": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                                      _vp, _vp, _i32, _i32, _i32, _i32, _f32, _vp, _vp, _vp,
+                                      _vp, _i32, _vp, _vp, _vp, _i32, _i32, _vp]),
+    "fkv_merge_wait": (C.c_int, [_vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _i32, _vp,
+                                 _vp]),
+    "fkv_dev_alloc": (C.c_int, [_i64, _vp]),
+    "fkv_dev_free": (C.c_int, [_vp]),
+    "fkv_ipc_get": (C.c_int, [_vp, _vp]),
+    "fkv_ipc_open": (C.c_int, [_vp, _vp]),
+    "fkv_ipc_close": (C.c_int, [_vp]),
     "fkv_snapkv_score": (C.c_int, [_vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _f32, _vp, _vp,
                                    _vp]),
     "fkv_score_workspace_bytes": (C.c_int64, [_i32, _i32, _i32, _i32, _i32]),
     "fkv_ada_budgets": (C.c_int, [_vp, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _vp]),
+    "fkv_ada_select": (C.c_int, [_vp, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp]),
     "fkv_topk_select": (C.c_int, [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _vp]),
     "fkv_compact": (C.c_int, [_vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _vp,
                               _vp]),

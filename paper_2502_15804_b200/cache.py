@@ -53,27 +53,34 @@ def default_workers(device=None) -> int:
     return sms * 8
 
 
-def plan_work(seg_len, n_workers: int, chunk: int | None = None):
-    """Static decode schedule.
+MIN_TILES_PER_WORKER = 4  # floor on tiles per worker (small problems: fewer, longer pieces)
 
-    The segments' 16-token tiles are laid end to end and the stream is cut
-    into n_workers equal ranges (``chunk=None``), or every segment is cut into
-    ``chunk``-token pieces and consecutive pieces are dealt to workers by
-    equal token count.  Either way a piece never straddles a worker, pieces of
-    a segment are consecutive item ids, and every segment has at least one
-    item (an empty one still produces o = 0, lse = -inf).
 
-    Returns item_seg, item_t0, item_t1 (int32), seg_item_ptr (int32
-    [n_seg+1]) and warp_ptr (int32 [n_workers+1]).
+def plan_work(seg_len, n_workers: int, chunk: int | None = None,
+              min_tiles: int = MIN_TILES_PER_WORKER):
+    """Static decode schedule for the warp-persistent K4 kernel.
+
+    Default: the segments' 16-token tiles are laid end to end and the stream
+    is cut into equal ranges of R = max(ceil(total_tiles / n_workers),
+    min_tiles) tiles, one range per worker: every busy worker streams the
+    same number of bytes and at most one segment per range boundary is split
+    (and needs an LSE merge).  With ``chunk``, every segment is cut into
+    ``chunk``-token pieces instead and consecutive pieces are dealt to
+    workers by equal token count.  Every segment has at least one piece (an
+    empty one still produces o = 0, lse = -inf), pieces of a segment are
+    consecutive item ids and start on a 16-token tile.
+
+    Returns item_seg, item_t0, item_t1 (int32 [n_items]), seg_item_ptr (int32
+    [n_seg+1]), warp_ptr (int32 [n_workers+1]) and work_list (int32
+    [n_items], item ids grouped by worker).
     """
     seg_len = np.asarray(seg_len, dtype=np.int64)
     n_seg = len(seg_len)
     tiles = (seg_len + TILE - 1) // TILE
-    total = int(tiles.sum())
     W = max(1, int(n_workers))
+    longest = int(tiles.max()) if n_seg else 0
     if chunk is None:
-        per = max(1, -(-total // W))
-        longest = int(tiles.max()) if n_seg else 0
+        per = max(-(-int(tiles.sum()) // W), int(min_tiles), 1)
         per = max(per, -(-longest // (MAX_ITEMS_PER_SEGMENT - 1)))
         start = np.zeros(n_seg, dtype=np.int64)
         if n_seg:
@@ -92,10 +99,8 @@ def plan_work(seg_len, n_workers: int, chunk: int | None = None):
                     break
                 cut = nxt
     else:
-        ch = max(TILE, -(-int(chunk) // TILE) * TILE)
-        longest = int(seg_len.max()) if n_seg else 0
-        need = -(-longest // MAX_ITEMS_PER_SEGMENT)  # keep <= MAX_ITEMS_PER_SEGMENT pieces
-        ch = max(ch, -(-need // TILE) * TILE)
+        ch = max(1, -(-int(chunk) // TILE))
+        ch = max(ch, -(-longest // MAX_ITEMS_PER_SEGMENT)) * TILE
         counts = np.maximum(1, -(-seg_len // ch))
         seg_i = np.repeat(np.arange(n_seg), counts)
         ptr0 = np.zeros(n_seg + 1, dtype=np.int64)
@@ -115,7 +120,8 @@ def plan_work(seg_len, n_workers: int, chunk: int | None = None):
     seg_item_ptr[1:] = np.cumsum(np.bincount(item_seg, minlength=n_seg))
     warp_ptr = np.zeros(W + 1, dtype=np.int32)
     warp_ptr[1:] = np.cumsum(np.bincount(owner, minlength=W))
-    return item_seg, t0, t1, seg_item_ptr, warp_ptr
+    work_list = np.arange(len(item_seg), dtype=np.int32)  # owners are non-decreasing
+    return item_seg, t0, t1, seg_item_ptr, warp_ptr, work_list
 
 
 @dataclass
@@ -135,6 +141,7 @@ class LayerCache:
     grp_ptr: torch.Tensor
     src_idx: torch.Tensor
     warp_ptr: torch.Tensor
+    work_list: torch.Tensor
     counters: torch.Tensor
     host: dict = field(default_factory=dict, repr=False)
 
@@ -165,7 +172,7 @@ class LayerCache:
         seg_len = np.asarray(seg_len, dtype=np.int64)
         row0, rows = segment_offsets(seg_len)
         dev = torch.device(device)
-        item_seg, t0, t1, ptr, wptr = plan_work(seg_len, default_workers(dev), chunk)
+        item_seg, t0, t1, ptr, wptr, wlist = plan_work(seg_len, default_workers(dev), chunk)
         k = torch.zeros((rows, HEAD_DIM), dtype=torch.bfloat16, device=dev)
         v = torch.zeros((rows, HEAD_DIM), dtype=torch.bfloat16, device=dev)
         if fill == "random":
@@ -188,7 +195,7 @@ class LayerCache:
             seg_len=i32(seg_len), seg_qrow=i32(seg_qrow), seg_out_row=i32(seg_out_row),
             item_seg=i32(item_seg), item_t0=i32(t0), item_t1=i32(t1),
             grp_ptr=i32(ptr), src_idx=i32(np.arange(ptr[-1])),
-            warp_ptr=i32(wptr),
+            warp_ptr=i32(wptr), work_list=i32(wlist),
             counters=torch.zeros(max(len(seg_len), 1), dtype=torch.int32, device=dev),
             host={"seg_len": seg_len, "seg_row0": row0, "chunk": chunk, "n_workers": len(wptr) - 1,
                   "seg_qrow": np.asarray(seg_qrow), "seg_out_row": np.asarray(seg_out_row)},
@@ -205,7 +212,7 @@ class LayerCache:
         if np.any(seg_row0 % 16):
             raise ValueError("segment starts must be multiples of 16 rows")
         dev = k.device
-        item_seg, t0, t1, ptr, wptr = plan_work(seg_len, default_workers(dev), chunk)
+        item_seg, t0, t1, ptr, wptr, wlist = plan_work(seg_len, default_workers(dev), chunk)
 
         def i32(a):
             return torch.as_tensor(np.ascontiguousarray(a, dtype=np.int32), device=dev)
@@ -215,7 +222,7 @@ class LayerCache:
             seg_len=i32(seg_len), seg_qrow=i32(seg_qrow), seg_out_row=i32(seg_out_row),
             item_seg=i32(item_seg), item_t0=i32(t0), item_t1=i32(t1), grp_ptr=i32(ptr),
             src_idx=i32(np.arange(ptr[-1])),
-            warp_ptr=i32(wptr),
+            warp_ptr=i32(wptr), work_list=i32(wlist),
             counters=torch.zeros(max(len(seg_len), 1), dtype=torch.int32, device=dev),
             host={"seg_len": seg_len, "seg_row0": seg_row0, "chunk": chunk, "n_workers": len(wptr) - 1,
                   "seg_qrow": np.asarray(seg_qrow), "seg_out_row": np.asarray(seg_out_row)},

@@ -31,7 +31,7 @@ NVCC_FLAGS = [
 # bit for bit (reference pkg/setup.py:20-29 builds its kernel the same way).
 CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-I", str(INCLUDE)]
 
-CU_SOURCES = ["decode.cu", "capi.cu", "select.cu", "compact.cu", "score.cu", "sharded.cu"]
+CU_SOURCES = ["decode.cu", "capi.cu", "select.cu", "compact.cu", "score.cu", "p2p.cu"]
 CXX_SOURCES = ["planner.cpp"]
 
 

@@ -53,15 +53,30 @@ struct DecodeParams {
   const int32_t* item_seg;
   const int32_t* item_t0;
   const int32_t* item_t1;
-  const int32_t* warp_ptr;  // worker w processes items [warp_ptr[w], warp_ptr[w+1])
+  const int32_t* warp_ptr;   // worker w processes work_list[warp_ptr[w] .. warp_ptr[w+1])
+  const int32_t* work_list;  // item ids grouped by worker
   int n_items, n_seg, n_workers;
   float scale_log2;
   float* part;        // [n_items, G, FKV_REC] partial records (multi-item segments)
   int32_t* counters;  // [n_seg] segment arrival counters; zero between launches
   __nv_bfloat16* out_bf16;
-  float* out_rec;
+  float* out_rec[FKV_MAX_PEERS];  // record destinations: local slots, or every peer's
+  int n_rec;                      // receive block for this rank (fused NVLink all-gather)
   float* out_lse;
+  int32_t* sig_done;              // warps-finished counter (local), zero between launches
+  int32_t* sig_flag[FKV_MAX_PEERS];  // per peer: flags[tp] in that peer's memory
+  int n_sig, my_rank;
 };
+
+__device__ __forceinline__ void put_rec(const DecodeParams& p, int64_t idx, float v) {
+#pragma unroll 1
+  for (int j = 0; j < p.n_rec; ++j) p.out_rec[j][idx] = v;
+}
+
+__device__ __forceinline__ void put_rec4(const DecodeParams& p, int64_t row, int lane, float4 v) {
+#pragma unroll 1
+  for (int j = 0; j < p.n_rec; ++j) reinterpret_cast<float4*>(p.out_rec[j] + row * FKV_REC)[lane] = v;
+}
 
 __device__ __forceinline__ int n_tiles_of(const DecodeParams& p, int it, int& t0, int& t1,
                                           int& seg) {
@@ -80,7 +95,8 @@ __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodePara
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   uint8_t* ring = smem + warp * kRingBytes;
-  const int worker = blockIdx.x * kWarps + warp;
+  // worker ids are spread over CTAs first so a short schedule still uses every SM
+  const int worker = warp * gridDim.x + blockIdx.x;
   const int w_beg = worker < p.n_workers ? p.warp_ptr[worker] : 0;
   const int w_end = worker < p.n_workers ? p.warp_ptr[worker + 1] : 0;
 
@@ -90,7 +106,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodePara
   }
   __syncwarp();
 
-  auto item_at = [&](int ord) -> int { return w_beg + ord < w_end ? w_beg + ord : -1; };
+  auto item_at = [&](int ord) -> int { return w_beg + ord < w_end ? p.work_list[w_beg + ord] : -1; };
 
   int p_ord = 0, p_t = 0;  // producer cursor: item ordinal, tile within item
   int p_nt = -1;           // cached tile count / row of the producer's item (-1: reload)
@@ -132,7 +148,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodePara
   const int mi = lane >> 3, ri = lane & 7;
   const int h0 = 2 * (lane & 3), h1 = h0 + 1;
   const int dr = lane >> 2;
-  const bool fused = p.out_bf16 || p.out_rec || p.out_lse;
+  const bool fused = p.out_bf16 || p.n_rec > 0 || p.out_lse;
 
   uint32_t qn[8][2];  // q fragments of the next item, loaded one item ahead
   auto load_q = [&](int it) {
@@ -256,9 +272,9 @@ __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodePara
             p.out_bf16[(orow + h0) * FKV_HEAD_DIM + d0] = __float2bfloat16_rn(acc[dt][0] * inv0);
             p.out_bf16[(orow + h0) * FKV_HEAD_DIM + d0 + 8] = __float2bfloat16_rn(acc[dt][2] * inv0);
           }
-          if (p.out_rec) {
-            p.out_rec[(orow + h0) * FKV_REC + d0] = acc[dt][0] * inv0;
-            p.out_rec[(orow + h0) * FKV_REC + d0 + 8] = acc[dt][2] * inv0;
+          if (p.n_rec) {
+            put_rec(p, (orow + h0) * FKV_REC + d0, acc[dt][0] * inv0);
+            put_rec(p, (orow + h0) * FKV_REC + d0 + 8, acc[dt][2] * inv0);
           }
         }
         if (h1 < G) {
@@ -266,19 +282,19 @@ __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodePara
             p.out_bf16[(orow + h1) * FKV_HEAD_DIM + d0] = __float2bfloat16_rn(acc[dt][1] * inv1);
             p.out_bf16[(orow + h1) * FKV_HEAD_DIM + d0 + 8] = __float2bfloat16_rn(acc[dt][3] * inv1);
           }
-          if (p.out_rec) {
-            p.out_rec[(orow + h1) * FKV_REC + d0] = acc[dt][1] * inv1;
-            p.out_rec[(orow + h1) * FKV_REC + d0 + 8] = acc[dt][3] * inv1;
+          if (p.n_rec) {
+            put_rec(p, (orow + h1) * FKV_REC + d0, acc[dt][1] * inv1);
+            put_rec(p, (orow + h1) * FKV_REC + d0 + 8, acc[dt][3] * inv1);
           }
         }
       }
       if (lane < 4) {
         if (h0 < G) {
-          if (p.out_rec) p.out_rec[(orow + h0) * FKV_REC + FKV_HEAD_DIM] = lse0;
+          if (p.n_rec) put_rec(p, (orow + h0) * FKV_REC + FKV_HEAD_DIM, lse0);
           if (p.out_lse) p.out_lse[orow + h0] = lse0;
         }
         if (h1 < G) {
-          if (p.out_rec) p.out_rec[(orow + h1) * FKV_REC + FKV_HEAD_DIM] = lse1;
+          if (p.n_rec) put_rec(p, (orow + h1) * FKV_REC + FKV_HEAD_DIM, lse1);
           if (p.out_lse) p.out_lse[orow + h1] = lse1;
         }
       }
@@ -358,15 +374,27 @@ __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodePara
         ob[0] = __floats2bfloat162_rn(o[g].x, o[g].y);
         ob[1] = __floats2bfloat162_rn(o[g].z, o[g].w);
       }
-      if (p.out_rec) reinterpret_cast<float4*>(p.out_rec + row * FKV_REC)[lane] = o[g];
+      if (p.n_rec) put_rec4(p, row, lane, o[g]);
     }
     if (lane < G) {
-      if (p.out_rec) p.out_rec[(orow + lane) * FKV_REC + FKV_HEAD_DIM] = lse_g;
+      if (p.n_rec) put_rec(p, (orow + lane) * FKV_REC + FKV_HEAD_DIM, lse_g);
       if (p.out_lse) p.out_lse[orow + lane] = lse_g;
     }
     if (lane == 0) p.counters[seg] = 0;  // ready for the next launch / graph replay
   }
 
+  // Fused all-gather completion: the last warp out publishes this rank's
+  // records to every peer by bumping its flag there (system-scope release).
+  if (p.n_sig > 0) {
+    __threadfence_system();
+    __syncwarp();
+    if (lane == 0 &&
+        atomicAdd(p.sig_done, 1) == static_cast<int>(gridDim.x) * kWarps - 1) {
+      *p.sig_done = 0;
+      __threadfence_system();
+      for (int j = 0; j < p.n_sig; ++j) atomicAdd_system(p.sig_flag[j] + p.my_rank, 1);
+    }
+  }
 }
 
 // K5 standalone (after the all-gather): warp g of the CTA merges head g of
@@ -376,7 +404,26 @@ __global__ void __launch_bounds__(G * 32)
     merge_lse_kernel(const float* __restrict__ part, const int32_t* __restrict__ grp_ptr,
                      const int32_t* __restrict__ src_idx, const int32_t* __restrict__ out_row,
                      __nv_bfloat16* __restrict__ out_bf16, float* __restrict__ out_rec,
-                     float* __restrict__ out_lse) {
+                     float* __restrict__ out_lse, const int32_t* flags, int tp,
+                     int32_t* consumed) {
+  // Fused all-gather consumer: wait until every peer has published this
+  // layer's records (their flag reached consumed+1), read them from L2.
+  __shared__ int s_target;
+  if (flags) {
+    if (threadIdx.x == 0) {
+      const int target = *reinterpret_cast<volatile int32_t*>(consumed) + 1;
+      for (int r = 0; r < tp; ++r) {
+        int v;
+        do {
+          asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(flags + r) : "memory");
+          if (v < target) __nanosleep(32);
+        } while (v < target);
+      }
+      s_target = target;
+    }
+    __syncthreads();
+    __threadfence_system();
+  }
   const int grp = blockIdx.x;
   const int g = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int i0 = grp_ptr[grp], i1 = grp_ptr[grp + 1];
@@ -413,6 +460,13 @@ __global__ void __launch_bounds__(G * 32)
     if (lane == 0) out_rec[row * FKV_REC + FKV_HEAD_DIM] = lse;
   }
   if (out_lse && lane == 0) out_lse[row] = lse;
+  if (flags) {
+    __syncthreads();
+    if (threadIdx.x == 0 && atomicAdd(consumed + 1, 1) == static_cast<int>(gridDim.x) - 1) {
+      consumed[1] = 0;
+      atomicExch(consumed, s_target);  // this layer consumed: next wait targets +1
+    }
+  }
 }
 
 template <int G>
@@ -440,40 +494,102 @@ int launch_decode(const DecodeParams& p, cudaStream_t st) {
 }  // namespace
 }  // namespace fkv
 
-extern "C" int fkv_decode(const void* q, const void* k, const void* v, const int64_t* seg_row0,
-                          const int32_t* seg_len, const int32_t* seg_qrow,
-                          const int32_t* seg_out_row, const int32_t* seg_item_ptr,
-                          const int32_t* item_seg, const int32_t* item_t0, const int32_t* item_t1,
-                          const int32_t* warp_ptr, int32_t n_workers, int32_t n_items,
-                          int32_t n_seg,
-                          int32_t group, float sm_scale, float* part, int32_t* counters,
-                          void* out_bf16, float* out_rec, float* out_lse, void* stream) {
-  using namespace fkv;
-  if (n_items < 0 || n_seg < 0) return set_error(FKV_ERR_INVALID, "fkv_decode: negative size");
-  if (n_items == 0) return FKV_OK;
-  if (!q || !k || !v || !seg_row0 || !seg_len || !seg_qrow || !seg_item_ptr || !item_seg ||
-      !item_t0 || !item_t1 || !warp_ptr || n_workers < 1 || !part || !counters ||
-      ((out_bf16 || out_rec || out_lse) && !seg_out_row))
-    return set_error(FKV_ERR_INVALID, "fkv_decode: null pointer");
-  if ((reinterpret_cast<uintptr_t>(k) | reinterpret_cast<uintptr_t>(v)) & 15)
-    return set_error(FKV_ERR_INVALID, "fkv_decode: cache not 16-byte aligned");
-  DecodeParams p{static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(k),
-                 static_cast<const __nv_bfloat16*>(v), seg_row0, seg_len, seg_qrow, seg_out_row,
-                 seg_item_ptr, item_seg, item_t0, item_t1, warp_ptr, n_items, n_seg, n_workers,
-                 sm_scale * kLog2e, part, counters, static_cast<__nv_bfloat16*>(out_bf16),
-                 out_rec, out_lse};
-  auto st = static_cast<cudaStream_t>(stream);
+namespace fkv {
+namespace {
+int decode_entry(DecodeParams& p, int group, cudaStream_t st) {
   switch (group) {
     case 4: return launch_decode<4>(p, st);
     case 8: return launch_decode<8>(p, st);
     default: return set_error(FKV_ERR_INVALID, "fkv_decode: group must be 4 or 8");
   }
 }
+}  // namespace
+}  // namespace fkv
+
+extern "C" int fkv_decode(const void* q, const void* k, const void* v, const int64_t* seg_row0,
+                          const int32_t* seg_len, const int32_t* seg_qrow,
+                          const int32_t* seg_out_row, const int32_t* seg_item_ptr,
+                          const int32_t* item_seg, const int32_t* item_t0, const int32_t* item_t1,
+                          const int32_t* warp_ptr, const int32_t* work_list, int32_t n_workers,
+                          int32_t n_items, int32_t n_seg, int32_t group, float sm_scale,
+                          float* part, int32_t* counters, void* out_bf16, float* out_rec,
+                          float* out_lse, void* stream) {
+  return fkv_decode_exchange(q, k, v, seg_row0, seg_len, seg_qrow, seg_out_row, seg_item_ptr,
+                             item_seg, item_t0, item_t1, warp_ptr, work_list, n_workers, n_items,
+                             n_seg,
+                             group, sm_scale, part, counters, out_bf16, out_rec ? &out_rec : nullptr,
+                             out_rec ? 1 : 0, out_lse, nullptr, nullptr, 0, 0, stream);
+}
+
+extern "C" int fkv_decode_exchange(const void* q, const void* k, const void* v,
+                                   const int64_t* seg_row0, const int32_t* seg_len,
+                                   const int32_t* seg_qrow, const int32_t* seg_out_row,
+                                   const int32_t* seg_item_ptr, const int32_t* item_seg,
+                                   const int32_t* item_t0, const int32_t* item_t1,
+                                   const int32_t* warp_ptr, const int32_t* work_list,
+                                   int32_t n_workers, int32_t n_items,
+                                   int32_t n_seg, int32_t group, float sm_scale, float* part,
+                                   int32_t* counters, void* out_bf16, float* const* out_recs,
+                                   int32_t n_rec, float* out_lse, int32_t* sig_done,
+                                   int32_t* const* sig_flags, int32_t n_sig, int32_t my_rank,
+                                   void* stream) {
+  using namespace fkv;
+  if (n_items < 0 || n_seg < 0) return set_error(FKV_ERR_INVALID, "fkv_decode: negative size");
+  if (n_rec < 0 || n_rec > FKV_MAX_PEERS || n_sig < 0 || n_sig > FKV_MAX_PEERS)
+    return set_error(FKV_ERR_INVALID, "fkv_decode: too many record destinations / peers");
+  if (n_items == 0) return FKV_OK;
+  if (!q || !k || !v || !seg_row0 || !seg_len || !seg_qrow || !seg_item_ptr || !item_seg ||
+      !item_t0 || !item_t1 || !warp_ptr || !work_list || n_workers < 1 || !part || !counters ||
+      ((out_bf16 || n_rec || out_lse) && !seg_out_row) || (n_rec && !out_recs) ||
+      (n_sig && (!sig_done || !sig_flags)))
+    return set_error(FKV_ERR_INVALID, "fkv_decode: null pointer");
+  if ((reinterpret_cast<uintptr_t>(k) | reinterpret_cast<uintptr_t>(v)) & 15)
+    return set_error(FKV_ERR_INVALID, "fkv_decode: cache not 16-byte aligned");
+  DecodeParams p{};
+  p.q = static_cast<const __nv_bfloat16*>(q);
+  p.k = static_cast<const __nv_bfloat16*>(k);
+  p.v = static_cast<const __nv_bfloat16*>(v);
+  p.seg_row0 = seg_row0;
+  p.seg_len = seg_len;
+  p.seg_qrow = seg_qrow;
+  p.seg_out_row = seg_out_row;
+  p.seg_item_ptr = seg_item_ptr;
+  p.item_seg = item_seg;
+  p.item_t0 = item_t0;
+  p.item_t1 = item_t1;
+  p.warp_ptr = warp_ptr;
+  p.work_list = work_list;
+  p.n_items = n_items;
+  p.n_seg = n_seg;
+  p.n_workers = n_workers;
+  p.scale_log2 = sm_scale * kLog2e;
+  p.part = part;
+  p.counters = counters;
+  p.out_bf16 = static_cast<__nv_bfloat16*>(out_bf16);
+  for (int j = 0; j < n_rec; ++j) p.out_rec[j] = out_recs[j];
+  p.n_rec = n_rec;
+  p.out_lse = out_lse;
+  p.sig_done = sig_done;
+  for (int j = 0; j < n_sig; ++j) p.sig_flag[j] = sig_flags[j];
+  p.n_sig = n_sig;
+  p.my_rank = my_rank;
+  return decode_entry(p, group, static_cast<cudaStream_t>(stream));
+}
 
 extern "C" int fkv_merge_lse(const float* part, const int32_t* grp_ptr, const int32_t* src_idx,
                              const int32_t* out_row, int32_t n_groups, int32_t group,
                              void* out_bf16, float* out_rec, float* out_lse, void* stream) {
+  return fkv_merge_wait(part, grp_ptr, src_idx, out_row, n_groups, group, out_bf16, out_rec,
+                        out_lse, nullptr, 0, nullptr, stream);
+}
+
+extern "C" int fkv_merge_wait(const float* part, const int32_t* grp_ptr, const int32_t* src_idx,
+                              const int32_t* out_row, int32_t n_groups, int32_t group,
+                              void* out_bf16, float* out_rec, float* out_lse,
+                              const int32_t* flags, int32_t tp, int32_t* consumed, void* stream) {
   using namespace fkv;
+  if (flags && (!consumed || tp < 1 || tp > FKV_MAX_PEERS))
+    return set_error(FKV_ERR_INVALID, "fkv_merge_wait: bad flags / consumed / tp");
   if (n_groups < 0) return set_error(FKV_ERR_INVALID, "n_groups < 0");
   if (n_groups == 0) return FKV_OK;
   if (!part || !grp_ptr || !src_idx || !out_row || (!out_bf16 && !out_rec && !out_lse))
@@ -483,11 +599,11 @@ extern "C" int fkv_merge_lse(const float* part, const int32_t* grp_ptr, const in
   switch (group) {
     case 4:
       merge_lse_kernel<4><<<n_groups, 4 * 32, 0, st>>>(part, grp_ptr, src_idx, out_row, ob, out_rec,
-                                                    out_lse);
+                                                       out_lse, flags, tp, consumed);
       break;
     case 8:
       merge_lse_kernel<8><<<n_groups, 8 * 32, 0, st>>>(part, grp_ptr, src_idx, out_row, ob, out_rec,
-                                                    out_lse);
+                                                       out_lse, flags, tp, consumed);
       break;
     default:
       return set_error(FKV_ERR_INVALID, "fkv_merge_lse: group must be 4 or 8");

@@ -16,9 +16,12 @@
 // shared-memory histograms (__match_any_sync: the top digits of float keys
 // are nearly all equal, so naive per-thread atomics would serialise), early
 // exit when the threshold bucket is taken whole.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include "common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace fkv {
 namespace {
@@ -37,6 +40,8 @@ __device__ __forceinline__ uint64_t compose(float s, uint32_t index) {
 
 struct SelectSmem {
   uint32_t hist[256];
+  uint32_t gh[256];  // cluster-summed histogram
+  uint32_t count;
   uint32_t digit, above;
   uint32_t warp_tot[32];
   uint64_t tau_head[64];
@@ -226,6 +231,161 @@ __global__ void __launch_bounds__(kThreads)
   for (int i = threadIdx.x; i < window; i += blockDim.x) out[max(k, 0) + i] = n + i;
 }
 
+// ------------------------------------------------ A18 + K2, one cluster ----
+// One thread-block cluster per request, one CTA per KV head (cluster size =
+// Hkv <= 8).  Each CTA stages its head's scores in shared memory when they
+// fit, finds its floor threshold, then the cluster runs the global radix
+// select together: per 8-bit digit every CTA histograms its own head's
+// non-floor keys and the histograms are summed through distributed shared
+// memory, so all CTAs derive the same digit.  Budgets, offsets (request b
+// starts at b*Hkv*budget: every request keeps exactly Hkv*budget tokens) and
+// the ascending index lists are written by the same launch.
+constexpr int kStageLimit = 40 * 1024;  // scores staged in smem up to 160 KiB
+
+template <class KeyOf>
+__device__ uint64_t cluster_select_kth(KeyOf key_of, int n, uint32_t k, SelectSmem& sm,
+                                       cg::cluster_group& cluster) {
+  uint64_t prefix = 0, mask = 0;
+  uint32_t need = k;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned ranks = cluster.num_blocks();
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) sm.hist[i] = 0;
+    __syncthreads();
+    for (int base = 0; base < n; base += blockDim.x) {
+      const int i = base + threadIdx.x;
+      uint64_t key = 0;
+      const bool ok = i < n && key_of(i, key) && (key & mask) == prefix;
+      const uint32_t d = ok ? static_cast<uint32_t>(key >> shift) & 255u : 256u;
+      const uint32_t peers = __match_any_sync(0xffffffffu, d);
+      if (ok && lane == __ffs(peers) - 1) atomicAdd(&sm.hist[d], __popc(peers));
+    }
+    cluster.sync();  // every CTA's histogram is complete
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+      uint32_t t = 0;
+      for (unsigned r = 0; r < ranks; ++r) t += cluster.map_shared_rank(sm.hist, r)[i];
+      sm.gh[i] = t;
+    }
+    cluster.sync();  // remote reads done before anyone zeroes its histogram
+    if (warp == 0) {
+      uint32_t local = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) local += sm.gh[8 * lane + j];
+      uint32_t incl = local;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t v = __shfl_down_sync(0xffffffffu, incl, off);
+        if (lane + off < 32) incl += v;
+      }
+      const uint32_t suffix = incl - local;
+      if (suffix < need && suffix + local >= need) {
+        uint32_t acc = suffix;
+        for (int j = 7; j >= 0; --j) {
+          const uint32_t c = sm.gh[8 * lane + j];
+          if (acc + c >= need) {
+            sm.digit = 8 * lane + j;
+            sm.above = acc;
+            break;
+          }
+          acc += c;
+        }
+      }
+    }
+    __syncthreads();
+    const uint32_t d = sm.digit;
+    need -= sm.above;
+    prefix |= static_cast<uint64_t>(d) << shift;
+    mask |= 255ull << shift;
+    const bool whole = sm.gh[d] == need;
+    __syncthreads();
+    if (whole) return prefix;
+  }
+  return prefix;
+}
+
+__global__ void __launch_bounds__(kThreads)
+    ada_select_kernel(const float* __restrict__ scores, int n, int window, int floor_k,
+                      int rest_total, int budget, int32_t* __restrict__ budgets,
+                      int64_t* __restrict__ offsets, int32_t* __restrict__ idx) {
+  extern __shared__ __align__(16) uint8_t dyn[];
+  __shared__ SelectSmem sm;
+  __shared__ int32_t s_budget;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int hkv = static_cast<int>(cluster.num_blocks());
+  const int h = static_cast<int>(cluster.block_rank());
+  const int b = blockIdx.y;
+  const float* src = scores + (static_cast<int64_t>(b) * hkv + h) * n;
+  const bool staged = n <= kStageLimit;
+  float* sv = reinterpret_cast<float*>(dyn);
+  uint32_t* floor_bits = reinterpret_cast<uint32_t*>(dyn + (staged ? n * 4 : 0));
+  if (staged)
+    for (int t = threadIdx.x; t < n; t += blockDim.x) sv[t] = src[t];
+  __syncthreads();
+  const float* s = staged ? sv : src;
+
+  // phase 1: this head's floor (top floor_k by (score desc, token asc)) as a bitmap
+  uint64_t tau = kNone;
+  if (floor_k > 0)
+    tau = cta_select_kth(
+        [&](int i, uint64_t& key) {
+          key = compose(s[i], static_cast<uint32_t>(i));
+          return true;
+        },
+        n, static_cast<uint32_t>(floor_k), sm);
+  for (int base = 0; base < n; base += blockDim.x) {
+    const int t = base + threadIdx.x;
+    const bool fl = t < n && tau != kNone && compose(s[t], static_cast<uint32_t>(t)) >= tau;
+    const uint32_t word = __ballot_sync(0xffffffffu, fl);
+    if ((threadIdx.x & 31) == 0 && t < n) floor_bits[t >> 5] = word;
+  }
+  __syncthreads();
+  auto in_floor = [&](int t) { return (floor_bits[t >> 5] >> (t & 31)) & 1u; };
+  const uint32_t gbase = static_cast<uint32_t>(h) * n;
+
+  // phase 2: global top rest_total of the non-floor scores, cluster-wide
+  uint64_t gtau = kNone;
+  if (rest_total > 0)
+    gtau = cluster_select_kth(
+        [&](int t, uint64_t& key) {
+          if (in_floor(t)) return false;
+          key = compose(s[t], gbase + t);
+          return true;
+        },
+        n, static_cast<uint32_t>(rest_total), sm, cluster);
+  auto chosen = [&](int t) {
+    return in_floor(t) || (gtau != kNone && compose(s[t], gbase + t) >= gtau);
+  };
+
+  // phase 3: this head's budget, then the request's head offsets via DSMEM
+  uint32_t c = 0;
+  for (int t = threadIdx.x; t < n; t += blockDim.x) c += (!in_floor(t) && chosen(t)) ? 1u : 0u;
+  const uint32_t tot = block_sum(c, sm);
+  if (threadIdx.x == 0) s_budget = window + floor_k + static_cast<int32_t>(tot);
+  cluster.sync();
+  int64_t off = static_cast<int64_t>(b) * hkv * budget;
+  for (int r = 0; r < h; ++r) off += *cluster.map_shared_rank(&s_budget, r);
+  const int bh = b * hkv + h;
+  if (threadIdx.x == 0) {
+    budgets[bh] = s_budget;
+    offsets[bh] = off;
+    if (b == static_cast<int>(gridDim.y) - 1 && h == hkv - 1) offsets[bh + 1] = off + s_budget;
+  }
+
+  // phase 4: selected tokens ascending, then the window
+  int32_t* out = idx + off;
+  uint32_t written = 0;
+  for (int base = 0; base < n; base += blockDim.x) {
+    const int t = base + threadIdx.x;
+    const bool take = t < n && chosen(t);
+    uint32_t before;
+    const uint32_t got = block_flag_scan(take, before, sm);
+    if (take) out[written + before] = t;
+    written += got;
+  }
+  for (int i = threadIdx.x; i < window; i += blockDim.x) out[s_budget - window + i] = n + i;
+  cluster.sync();  // keep this CTA's shared memory alive until every peer is done reading it
+}
+
 }  // namespace
 }  // namespace fkv
 
@@ -260,4 +420,47 @@ extern "C" int fkv_topk_select(const float* scores, const int32_t* budgets, int3
   topk_select_kernel<<<batch * hkv, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
       scores, budgets, n, window, offsets, idx);
   return cuda_check(cudaGetLastError(), "topk_select launch");
+}
+
+extern "C" int fkv_ada_select(const float* scores, int32_t batch, int32_t hkv, int32_t n,
+                              int32_t budget, int32_t window, int32_t floor_k, int32_t* budgets,
+                              int64_t* offsets, int32_t* idx, void* stream) {
+  using namespace fkv;
+  if (!scores || !budgets || !offsets || !idx)
+    return set_error(FKV_ERR_INVALID, "fkv_ada_select: null pointer");
+  if (batch < 0 || hkv < 1 || hkv > 8 || n < 0 || window < 0 || floor_k < 0)
+    return set_error(FKV_ERR_INVALID, "fkv_ada_select: bad sizes (Hkv must be 1..8)");
+  const int sel = budget - window;
+  if (sel < 0 || sel > n || floor_k > sel)
+    return set_error(FKV_ERR_INVALID, "fkv_ada_select: need 0 <= floor <= budget-window <= n");
+  if (static_cast<int64_t>(hkv) * n >= 0x7fffffffLL)
+    return set_error(FKV_ERR_INVALID, "fkv_ada_select: Hkv * n too large");
+  if (batch == 0) return FKV_OK;
+  const int rest = hkv * sel - hkv * floor_k;
+  const size_t smem = (n <= kStageLimit ? static_cast<size_t>(n) * 4 : 0) +
+                      static_cast<size_t>((n + 31) / 32) * 4;
+  static size_t configured = 0;
+  if (smem > configured) {
+    if (int rc = cuda_check(cudaFuncSetAttribute(ada_select_kernel,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 static_cast<int>(smem)),
+                            "ada_select smem attribute"))
+      return rc;
+    configured = smem;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(hkv, batch, 1);
+  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = static_cast<cudaStream_t>(stream);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = hkv;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cuda_check(cudaLaunchKernelEx(&cfg, ada_select_kernel, scores, n, window, floor_k, rest,
+                                       budget, budgets, offsets, idx),
+                    "ada_select launch");
 }

@@ -31,7 +31,8 @@ def rank_caches(shards: list[LayerShard], bt: int, hq: int, group: int, tp: int,
     gen = torch.Generator(device=device).manual_seed(seed)
     for l, sh in enumerate(shards):
         qrow = sh.seg_b * hq + sh.seg_h * group
-        out_row = np.arange(sh.n_segments) if tp > 1 else qrow
+        # tp > 1: segment i's record rows are slot i's G heads; tp == 1: o rows
+        out_row = np.arange(sh.n_segments) * group if tp > 1 else qrow
         lens = sh.seg_hi - sh.seg_lo
         if base is not None:
             b0 = base[l].host["seg_row0"]
@@ -44,10 +45,17 @@ def rank_caches(shards: list[LayerShard], bt: int, hq: int, group: int, tp: int,
 
 
 class StackDecoder:
+    """exchange = "p2p" (default for tp > 1): fused NVLink all-gather inside
+    the decode kernel (exchange.P2PGroup, one endpoint = this rank);
+    "nccl": K4 into local slots + torch.distributed all_gather_into_tensor."""
+
     def __init__(self, caches: list[LayerCache], finals: list[FinalMerge] | None, *, tp: int,
-                 bt: int, hq: int, group: int, process_group=None):
+                 bt: int, hq: int, group: int, process_group=None, exchange: str = "nccl",
+                 endpoint=None):
         self.caches = caches
         self.tp = tp
+        self.exchange_mode = exchange
+        self.endpoint = endpoint
         self.group = group
         self.bt, self.hq = bt, hq
         self.pg = process_group
@@ -65,6 +73,12 @@ class StackDecoder:
         c = self.caches[l]
         if self.tp == 1:
             ops.decode_into(q, c, self.ws[l], out_bf16=out, out_lse=out_lse)
+            return
+        if self.exchange_mode == "p2p":
+            ptr, src, row = self.final[l]
+            ops.decode_exchange(q, c, self.endpoint, l & 1, self.ws[l])
+            ops.merge_wait(self.endpoint, l & 1, ptr, src, row, self.group, out_bf16=out,
+                           out_lse=out_lse)
             return
         ops.decode_into(q, c, self.ws[l], out_rec=self.send[l])
         self.exchange(l)

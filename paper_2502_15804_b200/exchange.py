@@ -1,0 +1,142 @@
+"""Fused NVLink all-gather for the sharded decode (replaces NCCL all_gather).
+
+Each rank owns, in memory it allocated with ``fkv_dev_alloc`` and exported
+with CUDA IPC, a receive area ``recv[parity][tp, slots, G, 132]`` and a flag
+array ``flags[tp]``.  Per layer the decode kernel of rank r writes every
+segment's final (o, lse) record straight into ``recv[parity][r]`` of *every*
+rank (P2P stores over NVLink, ``fkv_decode_exchange``); its last warp then
+bumps ``flags[r]`` on every rank (system-scope atomics after a system
+fence).  The merge kernel on each rank waits until all ``flags`` reached
+this layer's count, merges the DP copies and writes o (``fkv_merge_wait``).
+Layer parity double-buffers ``recv``: a rank can run at most one layer
+ahead of any peer (layer l+1's merge needs every peer's layer l+1 decode,
+which follows that peer's layer l merge in stream order), so the buffer a
+fast rank writes is never the one a slow rank is still reading.
+
+``P2PGroup.connect`` maps peers via torch.distributed (one process per GPU);
+``P2PGroup.loopback`` builds tp virtual ranks inside one process on one GPU
+(all "peer" pointers local) -- the same kernels and protocol, used by the
+single-GPU tests and the emulated-TP bench.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import _native
+
+REC = 132
+
+
+class _Buf:
+    def __init__(self, nbytes: int):
+        ptr = C.c_void_p()
+        _native.check(_native.lib.fkv_dev_alloc(int(nbytes), C.byref(ptr)))
+        self.ptr = ptr.value
+        self.nbytes = nbytes
+
+    def handle(self) -> bytes:
+        h = (C.c_char * 64)()
+        _native.check(_native.lib.fkv_ipc_get(self.ptr, h))
+        return bytes(h)
+
+    def free(self):
+        if self.ptr:
+            _native.check(_native.lib.fkv_dev_free(self.ptr))
+            self.ptr = None
+
+
+def _open(handle: bytes) -> int:
+    ptr = C.c_void_p()
+    buf = (C.c_char * 64).from_buffer_copy(handle)
+    _native.check(_native.lib.fkv_ipc_open(buf, C.byref(ptr)))
+    return ptr.value
+
+
+class RankEndpoint:
+    """One rank's view: its own buffers plus every peer's mapped addresses."""
+
+    def __init__(self, rank: int, tp: int, slots: int, group: int):
+        self.rank, self.tp, self.slots, self.group = rank, tp, slots, group
+        self.block = slots * group * REC * 4          # bytes of one rank's block
+        self.recv = [_Buf(tp * self.block), _Buf(tp * self.block)]  # layer parity
+        self.flags = _Buf(4 * max(tp, 2))
+        self.ctr = _Buf(16)                            # [0] sig_done, [2:4] consumed
+        self.peer_recv: list[list[int]] = [[], []]    # [parity][peer] base address
+        self.peer_flags: list[int] = []
+
+    # -- pointers handed to the kernels
+    def dest_records(self, parity: int) -> list[int]:
+        """Where this rank's records go: its block in every peer's receive area."""
+        return [base + self.rank * self.block for base in self.peer_recv[parity]]
+
+    def recv_tensor(self, parity: int) -> torch.Tensor:
+        return _as_tensor(self.recv[parity].ptr, self.tp * self.slots * self.group * REC,
+                          (self.tp * self.slots, self.group, REC))
+
+    @property
+    def sig_done(self) -> int:
+        return self.ctr.ptr
+
+    @property
+    def consumed(self) -> int:
+        return self.ctr.ptr + 8
+
+    def free(self):
+        for b in (*self.recv, self.flags, self.ctr):
+            b.free()
+
+
+def _as_tensor(ptr: int, numel: int, shape) -> torch.Tensor:
+    """Zero-copy float32 CUDA tensor over library-owned device memory."""
+    class _Ifc:
+        __cuda_array_interface__ = {"shape": (numel,), "typestr": "<f4", "data": (ptr, False),
+                                    "version": 3, "strides": None}
+    return torch.as_tensor(_Ifc(), device="cuda").view(*shape)
+
+
+class P2PGroup:
+    def __init__(self, endpoints: list[RankEndpoint], owned_remote: list[int] | None = None):
+        self.endpoints = endpoints
+        self._remote = owned_remote or []
+
+    @staticmethod
+    def loopback(tp: int, slots: int, group: int) -> "P2PGroup":
+        eps = [RankEndpoint(r, tp, slots, group) for r in range(tp)]
+        for ep in eps:
+            ep.peer_recv = [[e.recv[par].ptr for e in eps] for par in (0, 1)]
+            ep.peer_flags = [e.flags.ptr for e in eps]
+        return P2PGroup(eps)
+
+    @staticmethod
+    def connect(rank: int, tp: int, slots: int, group: int, process_group=None) -> "P2PGroup":
+        import torch.distributed as dist
+        ep = RankEndpoint(rank, tp, slots, group)
+        mine = {"recv": [ep.recv[0].handle(), ep.recv[1].handle()], "flags": ep.flags.handle()}
+        allh = [None] * tp
+        dist.all_gather_object(allh, mine, group=process_group)
+        opened = []
+        for par in (0, 1):
+            row = []
+            for r, h in enumerate(allh):
+                if r == rank:
+                    row.append(ep.recv[par].ptr)
+                else:
+                    row.append(_open(h["recv"][par]))
+                    opened.append(row[-1])
+            ep.peer_recv[par] = row
+        for r, h in enumerate(allh):
+            if r == rank:
+                ep.peer_flags.append(ep.flags.ptr)
+            else:
+                ep.peer_flags.append(_open(h["flags"]))
+                opened.append(ep.peer_flags[-1])
+        return P2PGroup([ep], opened)
+
+    def close(self):
+        for p in self._remote:
+            _native.check(_native.lib.fkv_ipc_close(p))
+        for ep in self.endpoints:
+            ep.free()

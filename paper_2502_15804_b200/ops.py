@@ -64,9 +64,10 @@ def _decode(q, cache: LayerCache, ws: DecodeWorkspace | None, sm_scale, out_bf16
         q.data_ptr(), cache.k.data_ptr(), cache.v.data_ptr(), cache.seg_row0.data_ptr(),
         cache.seg_len.data_ptr(), cache.seg_qrow.data_ptr(), cache.seg_out_row.data_ptr(),
         cache.grp_ptr.data_ptr(), cache.item_seg.data_ptr(), cache.item_t0.data_ptr(),
-        cache.item_t1.data_ptr(), cache.warp_ptr.data_ptr(), int(cache.warp_ptr.shape[0]) - 1,
-        cache.n_items, cache.n_segments, cache.group, scale, ws.part.data_ptr(),
-        cache.counters.data_ptr(), _p(out_bf16), _p(out_rec), _p(out_lse), _stream()))
+        cache.item_t1.data_ptr(), cache.warp_ptr.data_ptr(), cache.work_list.data_ptr(),
+        int(cache.warp_ptr.shape[0]) - 1, cache.n_items, cache.n_segments, cache.group, scale,
+        ws.part.data_ptr(), cache.counters.data_ptr(), _p(out_bf16), _p(out_rec), _p(out_lse),
+        _stream()))
     return ws.part
 
 
@@ -83,6 +84,43 @@ def decode_into(q: torch.Tensor, cache: LayerCache, ws: DecodeWorkspace | None =
     if out_bf16 is None and out_rec is None and out_lse is None:
         raise NativeError("decode_into needs at least one output")
     _decode(q, cache, ws, sm_scale, out_bf16, out_rec, out_lse)
+
+
+def decode_exchange(q: torch.Tensor, cache: LayerCache, endpoint, parity: int,
+                    ws: DecodeWorkspace | None = None, sm_scale: float | None = None):
+    """K4 with the fused NVLink all-gather: every segment's final record goes
+    to this rank's block of every peer's receive area (P2P stores), then the
+    last warp signals all peers (``exchange.RankEndpoint``)."""
+    import ctypes as C
+    _need_cuda(q, cache.k)
+    if q.dtype != torch.bfloat16 or q.shape[-1] != HEAD_DIM or not q.is_contiguous():
+        raise NativeError("q must be contiguous bf16 [..., 128]")
+    ws = ws or DecodeWorkspace(cache)
+    scale = 1.0 / math.sqrt(HEAD_DIM) if sm_scale is None else sm_scale
+    dests = endpoint.dest_records(parity)
+    recs = (C.c_void_p * len(dests))(*dests)
+    flags = (C.c_void_p * len(endpoint.peer_flags))(*endpoint.peer_flags)
+    _native.check(_lib.fkv_decode_exchange(
+        q.data_ptr(), cache.k.data_ptr(), cache.v.data_ptr(), cache.seg_row0.data_ptr(),
+        cache.seg_len.data_ptr(), cache.seg_qrow.data_ptr(), cache.seg_out_row.data_ptr(),
+        cache.grp_ptr.data_ptr(), cache.item_seg.data_ptr(), cache.item_t0.data_ptr(),
+        cache.item_t1.data_ptr(), cache.warp_ptr.data_ptr(), cache.work_list.data_ptr(),
+        int(cache.warp_ptr.shape[0]) - 1, cache.n_items, cache.n_segments, cache.group, scale,
+        ws.part.data_ptr(), cache.counters.data_ptr(), None, recs, len(dests), None,
+        endpoint.sig_done, flags,
+        len(endpoint.peer_flags), endpoint.rank, _stream()))
+
+
+def merge_wait(endpoint, parity: int, grp_ptr, src_idx, out_row, group: int, *, out_bf16=None,
+               out_lse=None):
+    """K5 after the fused all-gather: wait for every peer's flag, then merge
+    the DP copies of each head from this rank's receive area."""
+    _need_cuda(grp_ptr, src_idx, out_row)
+    n_groups = int(out_row.shape[0])
+    _native.check(_lib.fkv_merge_wait(
+        endpoint.recv[parity].ptr, grp_ptr.data_ptr(), src_idx.data_ptr(), out_row.data_ptr(),
+        n_groups, int(group), _p(out_bf16), None, _p(out_lse), endpoint.flags.ptr, endpoint.tp,
+        endpoint.consumed, _stream()))
 
 
 def merge_lse(part, grp_ptr, src_idx, out_row, group: int, *, out_bf16=None, out_rec=None,
@@ -174,6 +212,24 @@ def select(scores: torch.Tensor, head_budgets: torch.Tensor, window: int = 32,
     return offsets, idx[:total]
 
 
+def ada_select(scores: torch.Tensor, budget: int, window: int = 32, alpha: float = 0.2):
+    """A18 + K2 in one cluster launch: -> (budgets int32 [Bt, Hkv],
+    offsets int64 [Bt*Hkv+1], idx int32 [Bt*Hkv*budget]); identical to
+    ``budgets`` followed by ``select``."""
+    _need_cuda(scores)
+    if scores.dtype != torch.float32 or scores.dim() != 3 or not scores.is_contiguous():
+        raise NativeError("scores must be contiguous f32 [Bt, Hkv, n]")
+    bt, hkv, n = scores.shape
+    dev = scores.device
+    hb = torch.empty((bt, hkv), dtype=torch.int32, device=dev)
+    offsets = torch.empty(bt * hkv + 1, dtype=torch.int64, device=dev)
+    idx = torch.empty(max(bt * hkv * budget, 1), dtype=torch.int32, device=dev)
+    _native.check(_lib.fkv_ada_select(scores.data_ptr(), bt, hkv, n, int(budget), int(window),
+                                      ada_floor(budget, window, alpha), hb.data_ptr(),
+                                      offsets.data_ptr(), idx.data_ptr(), _stream()))
+    return hb, offsets, idx[:bt * hkv * budget]
+
+
 def compact(k: torch.Tensor, v: torch.Tensor, offsets: torch.Tensor, idx: torch.Tensor,
             seg_bh, seg_lo, seg_hi, seg_qrow, seg_out_row, group: int,
             chunk: int | None = None) -> LayerCache:
@@ -203,15 +259,15 @@ def compact(k: torch.Tensor, v: torch.Tensor, offsets: torch.Tensor, idx: torch.
 
 def compress_layer(q_win: torch.Tensor, k: torch.Tensor, v: torch.Tensor, budget: int,
                    window: int = 32, alpha: float = 0.2, pool_k: int = 7):
-    """Prefill of one layer on one GPU: K1 score -> A18 budgets -> K2 select
-    -> K3 compact (TP=1 layout).  Returns (cache, head_budgets, scores)."""
+    """Prefill of one layer on one GPU: K1 score -> A18+K2 (one cluster
+    launch) -> K3 compact (TP=1 layout).  Returns (cache, head_budgets, scores).
+    The host reads the budgets back once to lay out the ragged cache."""
     import numpy as np
     bt, hq = q_win.shape[0], q_win.shape[1]
     hkv = k.shape[1]
     group = hq // hkv
     sc = score(q_win, k, window=window, pool_k=pool_k)
-    hb = budgets(sc, budget, window, alpha)
-    offsets, idx = select(sc, hb, window, total=bt * hkv * budget)
+    hb, offsets, idx = ada_select(sc, budget, window, alpha)
     hb_host = hb.cpu().numpy().reshape(-1)
     bh = np.arange(bt * hkv)
     qrow = (bh // hkv) * hq + (bh % hkv) * group

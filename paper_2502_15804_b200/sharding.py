@@ -132,9 +132,10 @@ def head_copies(plan: AllocationPlan, layer: int) -> dict[int, list[int]]:
     return out
 
 
-def layer_layout(plan: AllocationPlan, layer: int, budgets_l: np.ndarray, group: int
-                 ) -> tuple[list[LayerShard], FinalMerge]:
-    """budgets_l: [Bt, Hkv] retained tokens of this layer."""
+def layer_layout(plan: AllocationPlan, layer: int, budgets_l: np.ndarray, group: int,
+                 slots: int | None = None) -> tuple[list[LayerShard], FinalMerge]:
+    """budgets_l: [Bt, Hkv] retained tokens of this layer.  ``slots`` fixes
+    the per-rank slot count (default: this layer's maximum)."""
     bt, hkv = budgets_l.shape
     hq = hkv * group
     owners = head_copies(plan, layer)
@@ -158,7 +159,10 @@ def layer_layout(plan: AllocationPlan, layer: int, budgets_l: np.ndarray, group:
                 lo.append(cuts[c])
                 hi.append(cuts[c + 1])
         shards.append(LayerShard(*(np.asarray(x, dtype=np.int64) for x in (sb, sh, sc, lo, hi))))
-    slots = max(1, max(s.n_segments for s in shards))
+    need = max(1, max(s.n_segments for s in shards))
+    slots = need if slots is None else slots
+    if slots < need:
+        raise ValueError(f"layer {layer}: {need} slots needed, {slots} given")
     ptr = [0]
     src = []
     out_row = []
@@ -174,10 +178,17 @@ def layer_layout(plan: AllocationPlan, layer: int, budgets_l: np.ndarray, group:
 
 
 def plan_layouts(plan: AllocationPlan, budgets: np.ndarray, group: int):
-    """All layers: ([per-layer list over ranks of LayerShard], [per-layer FinalMerge])."""
+    """All layers: ([per-layer list over ranks of LayerShard], [per-layer
+    FinalMerge]); one slot count for every layer (the receive areas of the
+    fused all-gather are sized once)."""
+    L = budgets.shape[0]
+    slots = 1
+    for l in range(L):
+        for g, grp in enumerate(plan.layers[l].groups):
+            slots = max(slots, len(grp) * budgets.shape[1])
     shards, finals = [], []
-    for l in range(budgets.shape[0]):
-        s, f = layer_layout(plan, l, budgets[l], group)
+    for l in range(L):
+        s, f = layer_layout(plan, l, budgets[l], group, slots)
         shards.append(s)
         finals.append(f)
     return shards, finals

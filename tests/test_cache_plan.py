@@ -12,8 +12,9 @@ def test_plan_covers_each_segment_once(chunk, workers):
     rng = np.random.default_rng(workers + (chunk or 0))
     seg_len = rng.integers(0, 3000, size=300)
     seg_len[:3] = [0, 1, 16]
-    item_seg, t0, t1, sptr, wptr = plan_work(seg_len, workers, chunk)
+    item_seg, t0, t1, sptr, wptr, wlist = plan_work(seg_len, workers, chunk)
     assert wptr[0] == 0 and wptr[-1] == len(item_seg) and (np.diff(wptr) >= 0).all()
+    assert sorted(wlist.tolist()) == list(range(len(item_seg)))
     assert sptr[-1] == len(item_seg)
     assert (t0 % 16 == 0).all()
     for s in range(len(seg_len)):
@@ -29,9 +30,9 @@ def test_balanced_plan_equalises_tiles_per_worker():
     rng = np.random.default_rng(0)
     seg_len = rng.integers(300, 3000, size=512)
     W = 1184
-    item_seg, t0, t1, sptr, wptr = plan_work(seg_len, W)
+    item_seg, t0, t1, sptr, wptr, wlist = plan_work(seg_len, W)
     tiles = -(-(t1 - t0) // 16)
-    per = np.add.reduceat(np.append(tiles, 0), wptr[:-1])[:W] * (np.diff(wptr) > 0)
+    per = np.array([tiles[wlist[wptr[w]:wptr[w + 1]]].sum() for w in range(W)])
     assert per.max() <= -(-tiles.sum() // W) + 1
 
 

@@ -133,3 +133,22 @@ def test_selection_agreement_with_oracle_scores(cuda_device):
     agree = len(a & r) / len(r)
     print(f"selection agreement GPU-scores vs oracle-scores: {agree:.4f}")
     assert agree >= 0.98
+
+
+@pytest.mark.parametrize("bt,T,budget,ties", [(3, 4096, 256, False), (2, 2048, 64, True),
+                                              (1, 65600, 1024, False), (2, 40000, 512, True)])
+def test_fused_ada_select_bit_exact(cuda_device, bt, T, budget, ties):
+    """The one-launch cluster kernel == oracle budgets + selection (also past
+    the shared-memory staging limit, n > 40960)."""
+    from paper_2502_15804_b200 import ops
+    g = torch.Generator().manual_seed(bt * 7 + T)
+    n = T - 32
+    sc = torch.randint(0, 5, (bt, 8, n), generator=g).float() if ties else torch.rand(bt, 8, n, generator=g)
+    hb, off, idx = ops.ada_select(sc.to(cuda_device), budget, 32)
+    torch.cuda.synchronize()
+    s64 = sc.double().numpy()
+    ref_b = okv.ada_budgets(s64, budget, 32, 0.2)
+    np.testing.assert_array_equal(hb.cpu().numpy(), ref_b)
+    ref_off, ref_idx = okv.topk_select(s64, ref_b, 32)
+    np.testing.assert_array_equal(off.cpu().numpy(), ref_off)
+    np.testing.assert_array_equal(idx.cpu().numpy(), ref_idx)

@@ -139,3 +139,22 @@ def test_gloo_two_rank_exchange_matches_unsharded():
         assert p.exitcode == 0
     for _, err in res:
         assert err < 1e-10
+
+
+def test_rank_cache_tables_for_exchange():
+    """Host tables of a rank's caches (built on CPU tensors here): slot i's
+    record rows are i*G .. i*G+G-1 and the final merge sources address
+    rank*slots + slot -- the layout both exchanges (NCCL / P2P) rely on."""
+    from paper_2502_15804_b200.decoder import rank_caches
+    G, hkv, bt = 8, 8, 3
+    budgets = synthetic_budgets(2, bt, hkv, 128, seed=4)
+    plan = _plan(budgets, 4, "dp")
+    shards, finals = plan_layouts(plan, budgets, G)
+    for r in range(4):
+        caches = rank_caches([s[r] for s in shards], bt, G * hkv, G, 4, "cpu", fill="zeros")
+        for l, c in enumerate(caches):
+            n = c.n_segments
+            assert c.host["seg_out_row"].tolist() == [i * G for i in range(n)]
+            assert n <= finals[l].slots
+    f = finals[0]
+    assert f.src_idx.max() < 4 * f.slots

@@ -25,7 +25,11 @@ for (bt, hq, hkv, T, B) in [(1, 32, 8, 16384, 256), (4, 32, 8, 16384, 256), (1, 
     t_b = timeit(lambda: ops.budgets(sc, B, w))
     hb = ops.budgets(sc, B, w)
     t_k = timeit(lambda: ops.select(sc, hb, w, total=bt * hkv * B))
+    t_f = timeit(lambda: ops.ada_select(sc, B, w))
+    hb2, off2, idx2 = ops.ada_select(sc, B, w)
+    off1, idx1 = ops.select(sc, hb, w, total=bt * hkv * B)
+    same = bool((hb2 == hb).all() and (idx2 == idx1).all())
     flops = 2 * 2 * hq * w * T * 128 * bt  # two passes
     kbytes = bt * hkv * T * 256
     print(f"bt={bt} Hq={hq} T={T}: score {t_s*1e6:.0f}us  {flops/t_s/1e12:.0f} TFLOP/s (2 passes)  K-read {kbytes/t_s/1e9:.0f} GB/s (1x K)  "
-          f"budgets {t_b*1e6:.0f}us  select {t_k*1e6:.0f}us")
+          f"budgets {t_b*1e6:.0f}us  select {t_k*1e6:.0f}us  fused ada_select {t_f*1e6:.0f}us (same={same})")
