@@ -16,8 +16,10 @@
 // shared memory; K tiles (128 keys x 128 d, 32 KiB) stream through a 3-stage
 // TMA ring with 128-B swizzle; one elected thread issues
 // tcgen05.mma.cta_group::1.kind::f16 (M=128, N=128 or GW, K=16) into a
-// double-buffered fp32 TMEM accumulator; four epilogue warps drain it with
-// tcgen05.ld.  Warp roles: 0-3 epilogue, 4 TMA producer, 5 MMA issuer.
+// double-buffered fp32 TMEM accumulator; eight epilogue warps drain it with
+// tcgen05.ld (warp e reads TMEM lanes 32*(e%4) and half e/4 of the columns).
+// Warp roles: 0-7 epilogue, 8 TMA producer, 9 MMA issuer.  Grid: one wave
+// of one CTA per SM ((Bt*Hkv) x chunks <= #SMs when possible).
 // The second pass re-reads K mostly from L2 (a layer's K for one request is
 // 32 MiB at 16k context, well inside the 126 MB L2).
 #include <cuda.h>
@@ -33,7 +35,9 @@ namespace {
 constexpr int kBN = 128;                 // keys per tile
 constexpr int kStages = 3;
 constexpr int kTileBytes = kBN * 256;    // 128 keys x 128 d x bf16
-constexpr int kThreads = 192;            // 4 epilogue warps + TMA warp + MMA warp
+constexpr int kEpiWarps = 8;
+constexpr int kTmaWarp = kEpiWarps, kMmaWarp = kEpiWarps + 1;
+constexpr int kThreads = 32 * (kEpiWarps + 2);
 constexpr float kLog2e = 1.4426950408889634f;
 
 struct ScoreParams {
@@ -132,6 +136,8 @@ struct __align__(1024) ScoreSmem {
   uint64_t full[kStages], empty[kStages], tfull[2], tempty[2], qbar;
   uint32_t tmem_base;
   float m2[GW], invl[GW];
+  float red[2][2][kBN];      // pass 2: [tile parity][column half][key] partial sums
+  float ml[kBN][2];          // pass 1, GW=128: second column half's (max, sum) per row
 };
 
 template <int PASS, int GW>
@@ -153,7 +159,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int krow0 = bh * p.T;
   const int qrow0 = b * p.q_rows_per_req + h * GW;
 
-  if (warp == 4 && lane == 0) {
+  if (warp == kTmaWarp && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_q)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_k)) : "memory");
     for (int s = 0; s < kStages; ++s) {
@@ -162,15 +168,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&sm.tfull[i], 1);
-      mbar_init(&sm.tempty[i], 4);
+      mbar_init(&sm.tempty[i], kEpiWarps);
     }
     mbar_init(&sm.qbar, 1);
     fence_mbar_init();
   }
-  if (warp == 5) tmem_alloc(&sm.tmem_base, kCols);
-  if (PASS == 2 && warp < 4) {
+  if (warp == kMmaWarp) tmem_alloc(&sm.tmem_base, kCols);
+  if (PASS == 2 && warp < kEpiWarps) {
     // combine the pass-1 partial statistics of all chunks (log2 domain)
-    for (int r = threadIdx.x; r < GW; r += 128) {
+    for (int r = threadIdx.x; r < GW; r += 32 * kEpiWarps) {
       float M = -CUDART_INF_F, L = 0.f;
       const float* st = p.stats + (static_cast<int64_t>(bh) * p.n_chunks) * GW * 2;
       for (int c = 0; c < p.n_chunks; ++c) {
@@ -189,7 +195,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
 
-  if (warp == 4) {
+  if (warp == kTmaWarp) {
     // ------------------------------------------------ TMA producer ----
     if (lane == 0 && j1 > j0) {
       mbar_arrive_expect_tx(&sm.qbar, GW * 256);
@@ -204,7 +210,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tma_load_2d(&sm.k[s][c][0][0], &tm_k, 64 * c, krow0 + j * kBN, &sm.full[s]);
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == kMmaWarp) {
     // -------------------------------------------------- MMA issuer ----
     if (lane == 0 && j1 > j0) {
       mbar_wait(&sm.qbar, 0);
@@ -237,64 +243,75 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ---------------------------------------------------- epilogue ----
-    const uint32_t lane_base = static_cast<uint32_t>(32 * warp) << 16;
+    const int quad = warp & 3, half = warp >> 2;
+    const uint32_t lane_base = static_cast<uint32_t>(32 * quad) << 16;
     if (PASS == 1) {
+      // GW=256: warp half = row half (one whole row per thread);
+      // GW=128: warp half = column half (per-row partials, combined at the end)
       constexpr int MH = GW / 128;
-      float m[MH], l[MH];
-#pragma unroll
-      for (int mh = 0; mh < MH; ++mh) {
-        m[mh] = -CUDART_INF_F;
-        l[mh] = 0.f;
-      }
+      const int mh = MH == 2 ? half : 0;
+      const int cb0 = MH == 2 ? 0 : 2 * half, cb1 = MH == 2 ? 4 : 2 * half + 2;
+      const int r = mh * 128 + 32 * quad + lane;
+      const int limit = min(p.T - 1, p.T - p.window + (r % p.window));  // last visible key
+      float m = -CUDART_INF_F, l = 0.f;
       for (int j = j0; j < j1; ++j) {
         const int it = j - j0, buf = it & 1;
         mbar_wait(&sm.tfull[buf], (it >> 1) & 1);
         tc_fence_after();
         const int ts = j * kBN;
 #pragma unroll 1
-        for (int mh = 0; mh < MH; ++mh) {
-          const int r = mh * 128 + 32 * warp + lane;
-          const int limit = min(p.T - 1, p.T - p.window + (r % p.window));  // last visible key
-#pragma unroll 1
-          for (int cb = 0; cb < 4; ++cb) {
-            float v[32];
-            tmem_ld32(tmem + lane_base + buf * GW + mh * kBN + cb * 32, v);
-            const int c0 = ts + cb * 32;
-            float bmax = -CUDART_INF_F;
+        for (int cb = cb0; cb < cb1; ++cb) {
+          float v[32];
+          tmem_ld32(tmem + lane_base + buf * GW + mh * kBN + cb * 32, v);
+          const int c0 = ts + cb * 32;
+          float bmax = -CUDART_INF_F;
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              v[i] = c0 + i <= limit ? v[i] * p.scale_log2 : -CUDART_INF_F;
-              bmax = fmaxf(bmax, v[i]);
-            }
-            if (bmax == -CUDART_INF_F) continue;
-            const float nm = fmaxf(m[mh], bmax);
-            float acc = 0.f;
-#pragma unroll
-            for (int i = 0; i < 32; ++i) acc += fast_exp2(v[i] - nm);
-            l[mh] = l[mh] * fast_exp2(m[mh] - nm) + acc;
-            m[mh] = nm;
+          for (int i = 0; i < 32; ++i) {
+            v[i] = c0 + i <= limit ? v[i] * p.scale_log2 : -CUDART_INF_F;
+            bmax = fmaxf(bmax, v[i]);
           }
+          if (bmax == -CUDART_INF_F) continue;
+          const float nm = fmaxf(m, bmax);
+          float acc = 0.f;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) acc += fast_exp2(v[i] - nm);
+          l = l * fast_exp2(m - nm) + acc;
+          m = nm;
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.tempty[buf]);
       }
-#pragma unroll
-      for (int mh = 0; mh < MH; ++mh) {
-        const int r = mh * 128 + 32 * warp + lane;
+      if (MH == 1) {
+        if (half == 1) {
+          sm.ml[32 * quad + lane][0] = m;
+          sm.ml[32 * quad + lane][1] = l;
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps));
+        if (half == 0) {
+          const float m1 = sm.ml[32 * quad + lane][0], l1 = sm.ml[32 * quad + lane][1];
+          const float nm = fmaxf(m, m1);
+          if (nm != -CUDART_INF_F) {
+            l = l * exp2f(m - nm) + l1 * exp2f(m1 - nm);
+            m = nm;
+          }
+        }
+      }
+      if (MH == 2 || half == 0) {
         float* st = p.stats + ((static_cast<int64_t>(bh) * p.n_chunks + chunk) * GW + r) * 2;
-        st[0] = m[mh];
-        st[1] = l[mh];
+        st[0] = m;
+        st[1] = l;
       }
     } else {
       const int n = p.T - p.window;
+      const int key = 32 * quad + lane;
       for (int j = j0; j < j1; ++j) {
         const int it = j - j0, buf = it & 1;
         mbar_wait(&sm.tfull[buf], (it >> 1) & 1);
         tc_fence_after();
         float acc = 0.f;
 #pragma unroll 1
-        for (int cb = 0; cb < GW / 32; ++cb) {
+        for (int cb = half * (GW / 64); cb < (half + 1) * (GW / 64); ++cb) {
           float v[32];
           tmem_ld32(tmem + lane_base + buf * GW + cb * 32, v);
 #pragma unroll
@@ -306,14 +323,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.tempty[buf]);
-        const int t = j * kBN + 32 * warp + lane;
-        if (t < n) p.raw[static_cast<int64_t>(bh) * n + t] = acc;
+        sm.red[it & 1][half][key] = acc;
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps));
+        const int t = j * kBN + key;
+        if (half == 0 && t < n)
+          p.raw[static_cast<int64_t>(bh) * n + t] = acc + sm.red[it & 1][1][key];
       }
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 5) {
+  if (warp == kMmaWarp) {
     tc_fence_after();
     tmem_dealloc(tmem, kCols);
   }
@@ -367,6 +387,25 @@ int make_map(CUtensorMap* map, const void* base, int64_t rows, int box_rows) {
   return FKV_OK;
 }
 
+}  // namespace
+
+// Key chunks per (request, KV head): one wave of one CTA per SM when the
+// heads alone do not fill the GPU; never more chunks than tiles.
+int score_chunks(int bh, int n_tiles) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0)
+      sms = 148;
+  }
+  int c = sms / bh;
+  if (c < 1) c = 1;
+  return c > n_tiles ? n_tiles : c;
+}
+
+namespace {
+
 template <int GW>
 int launch_score(const CUtensorMap& tq, const CUtensorMap& tk, const ScoreParams& p, int batch_heads,
                  cudaStream_t st) {
@@ -398,8 +437,7 @@ extern "C" int64_t fkv_score_workspace_bytes(int32_t batch, int32_t hkv, int32_t
   const int gw = group * window;
   const int n_tiles = (T + fkv::kBN - 1) / fkv::kBN;
   const int bh = batch * hkv;
-  int chunks = (2 * 148 + bh - 1) / (bh > 0 ? bh : 1);
-  chunks = chunks < 1 ? 1 : (chunks > n_tiles ? n_tiles : chunks);
+  const int chunks = fkv::score_chunks(bh > 0 ? bh : 1, n_tiles);
   const int64_t stats = static_cast<int64_t>(bh) * chunks * gw * 2 * 4;
   const int64_t raw = static_cast<int64_t>(bh) * (T - window) * 4;
   return stats + raw + 256;
@@ -421,8 +459,7 @@ extern "C" int fkv_snapkv_score(const void* q_win, const void* k, int32_t batch,
     return set_error(FKV_ERR_INVALID, "fkv_snapkv_score: Bt * Hkv * T too large");
   const int n_tiles = (T + kBN - 1) / kBN;
   const int bh = batch * hkv;
-  int chunks = (2 * 148 + bh - 1) / bh;
-  chunks = chunks < 1 ? 1 : (chunks > n_tiles ? n_tiles : chunks);
+  int chunks = score_chunks(bh, n_tiles);
   const int tiles_per_chunk = (n_tiles + chunks - 1) / chunks;
   chunks = (n_tiles + tiles_per_chunk - 1) / tiles_per_chunk;
 
