@@ -221,11 +221,12 @@ int fkv_ada_select(const float* scores, int32_t batch, int32_t hkv, int32_t n, i
 /* K3: compaction.  For each destination segment s, rows j in [seg_lo, seg_hi)
  * of head seg_bh[s]'s selection are copied from k_src/v_src (bf16
  * [batch*hkv, T, 128]) to cache rows seg_row0[s] + (j - seg_lo), swizzled;
- * zero_pad != 0 also zeroes the rows up to the next FKV_PAGE boundary. */
+ * zero_pad != 0 also zeroes the rows up to the next FKV_PAGE boundary.
+ * max_tokens >= max(seg_hi - seg_lo) sizes the grid (64 rows per CTA). */
 int fkv_compact(const void* k_src, const void* v_src, int32_t T, int32_t n_segments,
                 const int64_t* offsets, const int32_t* idx, const int32_t* seg_bh,
                 const int32_t* seg_lo, const int32_t* seg_hi, const int64_t* seg_row0,
-                int32_t zero_pad, void* k_dst, void* v_dst, void* stream);
+                int32_t zero_pad, int32_t max_tokens, void* k_dst, void* v_dst, void* stream);
 
 #ifdef __cplusplus
 }

@@ -54,6 +54,7 @@ def default_workers(device=None) -> int:
 
 
 MIN_TILES_PER_WORKER = 4  # floor on tiles per worker (small problems: fewer, longer pieces)
+MAX_PIECES_PER_SEGMENT = 4  # typical split bound: merge cost grows with pieces per segment
 
 
 def plan_work(seg_len, n_workers: int, chunk: int | None = None,
@@ -62,7 +63,7 @@ def plan_work(seg_len, n_workers: int, chunk: int | None = None,
 
     Default: the segments' 16-token tiles are laid end to end and the stream
     is cut into equal ranges of R = max(ceil(total_tiles / n_workers),
-    min_tiles) tiles, one range per worker: every busy worker streams the
+    min_tiles, ceil(mean_segment_tiles / 4)) tiles, one range per worker: every busy worker streams the
     same number of bytes and at most one segment per range boundary is split
     (and needs an LSE merge).  With ``chunk``, every segment is cut into
     ``chunk``-token pieces instead and consecutive pieces are dealt to
@@ -81,6 +82,10 @@ def plan_work(seg_len, n_workers: int, chunk: int | None = None,
     longest = int(tiles.max()) if n_seg else 0
     if chunk is None:
         per = max(-(-int(tiles.sum()) // W), int(min_tiles), 1)
+        # keep the average segment within a few pieces: the last warp of a split
+        # segment merges every piece's record, so many pieces lengthen the tail
+        avg = int(tiles.sum()) // max(n_seg, 1)
+        per = max(per, -(-avg // MAX_PIECES_PER_SEGMENT))
         per = max(per, -(-longest // (MAX_ITEMS_PER_SEGMENT - 1)))
         start = np.zeros(n_seg, dtype=np.int64)
         if n_seg:

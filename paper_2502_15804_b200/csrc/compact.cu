@@ -21,35 +21,50 @@ namespace {
 
 constexpr int kThreads = 256;
 
+constexpr int kRowsPerCta = 64;  // 16 half-warps x 4 rows
+
+// grid = (row blocks, segments): CTA (x, s) moves rows [64x, 64x+64) of
+// segment s, so even a handful of long segments spreads over every SM.
 __global__ void __launch_bounds__(kThreads)
     compact_kernel(const uint4* __restrict__ k_src, const uint4* __restrict__ v_src, int T,
                    const int64_t* __restrict__ offsets, const int32_t* __restrict__ idx,
                    const int32_t* __restrict__ seg_bh, const int32_t* __restrict__ seg_lo,
                    const int32_t* __restrict__ seg_hi, const int64_t* __restrict__ seg_row0,
                    int zero_pad, uint4* __restrict__ k_dst, uint4* __restrict__ v_dst) {
-  const int s = blockIdx.x;
-  const int bh = seg_bh[s];
+  const int s = blockIdx.y;
   const int lo = seg_lo[s], hi = seg_hi[s];
-  const int64_t row0 = seg_row0[s];
   const int n = hi - lo;
   const int rows = zero_pad ? (n + FKV_PAGE - 1) / FKV_PAGE * FKV_PAGE : n;
+  const int r_begin = blockIdx.x * kRowsPerCta;
+  if (r_begin >= rows) return;
+  const int bh = seg_bh[s];
+  const int64_t row0 = seg_row0[s];
   const int32_t* sel = idx + offsets[bh] + lo;
   const int64_t src_base = static_cast<int64_t>(bh) * T;  // row index of (b, h, token 0)
   const int half = threadIdx.x >> 4;                        // 16 half-warps per CTA
   const int c = threadIdx.x & 15;                           // 16-byte chunk of the row
-  for (int r = half; r < rows; r += kThreads / 16) {
-    const int64_t dst = row0 + r;
-    const int64_t o = dst * 16 + (c ^ static_cast<int>(dst & 7));
-    if (r < n) {
-      const int64_t src = (src_base + sel[r]) * 16 + c;
-      const uint4 kv = __ldg(k_src + src);
-      const uint4 vv = __ldg(v_src + src);
-      k_dst[o] = kv;
-      v_dst[o] = vv;
+  const int r_end = min(rows, r_begin + kRowsPerCta);
+  // issue every load of this CTA's rows before any store (4 rows per half-warp in flight)
+  uint4 kv[4], vv[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int r = r_begin + half + 16 * u;
+    if (r < min(r_end, n)) {
+      const int64_t src = (src_base + __ldg(sel + r)) * 16 + c;
+      kv[u] = __ldg(k_src + src);
+      vv[u] = __ldg(v_src + src);
     } else {
-      const uint4 z = make_uint4(0, 0, 0, 0);
-      k_dst[o] = z;
-      v_dst[o] = z;
+      kv[u] = vv[u] = make_uint4(0, 0, 0, 0);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int r = r_begin + half + 16 * u;
+    if (r < r_end) {
+      const int64_t dst = row0 + r;
+      const int64_t o = dst * 16 + (c ^ static_cast<int>(dst & 7));
+      k_dst[o] = kv[u];
+      v_dst[o] = vv[u];
     }
   }
 }
@@ -60,9 +75,13 @@ __global__ void __launch_bounds__(kThreads)
 extern "C" int fkv_compact(const void* k_src, const void* v_src, int32_t T, int32_t n_segments,
                            const int64_t* offsets, const int32_t* idx, const int32_t* seg_bh,
                            const int32_t* seg_lo, const int32_t* seg_hi, const int64_t* seg_row0,
-                           int32_t zero_pad, void* k_dst, void* v_dst, void* stream) {
+                           int32_t zero_pad, int32_t max_tokens, void* k_dst, void* v_dst,
+                           void* stream) {
   using namespace fkv;
-  if (n_segments < 0 || T < 0) return set_error(FKV_ERR_INVALID, "fkv_compact: bad sizes");
+  if (n_segments < 0 || T < 0 || max_tokens < 0)
+    return set_error(FKV_ERR_INVALID, "fkv_compact: bad sizes");
+  max_tokens = (max_tokens + FKV_PAGE - 1) / FKV_PAGE * FKV_PAGE;  // padding rows too
+  if (max_tokens == 0) max_tokens = FKV_PAGE;
   if (n_segments == 0) return FKV_OK;
   if (!k_src || !v_src || !offsets || !idx || !seg_bh || !seg_lo || !seg_hi || !seg_row0 ||
       !k_dst || !v_dst)
@@ -70,7 +89,9 @@ extern "C" int fkv_compact(const void* k_src, const void* v_src, int32_t T, int3
   if ((reinterpret_cast<uintptr_t>(k_src) | reinterpret_cast<uintptr_t>(v_src) |
        reinterpret_cast<uintptr_t>(k_dst) | reinterpret_cast<uintptr_t>(v_dst)) & 15)
     return set_error(FKV_ERR_INVALID, "fkv_compact: buffers must be 16-byte aligned");
-  compact_kernel<<<n_segments, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+  // rows per segment are bounded by the host's layout; size the grid for the longest
+  dim3 grid((max_tokens + kRowsPerCta - 1) / kRowsPerCta, n_segments);
+  compact_kernel<<<grid, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const uint4*>(k_src), static_cast<const uint4*>(v_src), T, offsets, idx, seg_bh,
       seg_lo, seg_hi, seg_row0, zero_pad, static_cast<uint4*>(k_dst), static_cast<uint4*>(v_dst));
   return cuda_check(cudaGetLastError(), "compact launch");

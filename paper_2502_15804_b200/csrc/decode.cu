@@ -166,6 +166,12 @@ __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodePara
       for (int kk = 0; kk < 8; ++kk) qn[kk][0] = qn[kk][1] = 0u;
     }
   };
+  // Programmatic dependent launch: everything above (barrier init, schedule
+  // reads, the first K/V tiles in flight) touches only the static cache and
+  // overlaps the previous kernel's tail; q and every global write come after
+  // the previous grid has completed.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
   load_q(item_at(0));
 
   for (int ord = 0;; ++ord) {
@@ -352,7 +358,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodePara
     float4 o[G];
 #pragma unroll
     for (int g = 0; g < G; ++g) o[g] = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 2
+#pragma unroll 4
     for (int i = 0; i < n_it; ++i) {
       float4 v4[G];
 #pragma unroll
@@ -487,8 +493,17 @@ int launch_decode(const DecodeParams& p, cudaStream_t st) {
   }
   (void)grid_cap;
   const int grid = (p.n_workers + kWarps - 1) / kWarps;
-  decode_kernel<G><<<grid, kWarps * 32, kSmemBytes, st>>>(p);
-  return cuda_check(cudaGetLastError(), "decode launch");
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid, 1, 1);
+  cfg.blockDim = dim3(kWarps * 32, 1, 1);
+  cfg.dynamicSmemBytes = kSmemBytes;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL (see kernel)
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cuda_check(cudaLaunchKernelEx(&cfg, decode_kernel<G>, p), "decode launch");
 }
 
 }  // namespace

@@ -111,6 +111,26 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
+// Same, with an L2 eviction-priority policy (createpolicy): pass 1 keeps K in
+// L2 for pass 2 (evict_last), pass 2 streams it out (evict_first).
+__device__ __forceinline__ void tma_load_2d_hint(void* dst, const CUtensorMap* map, int x, int y,
+                                                 uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
+__device__ __forceinline__ uint64_t l2_policy(bool keep) {
+  uint64_t pol;
+  if (keep)
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  else
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
 // K-major, 128-B swizzled UMMA shared-memory descriptor (rows of 128 B,
 // 8-row core groups 1024 B apart).
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
@@ -135,7 +155,7 @@ struct __align__(1024) ScoreSmem {
   __nv_bfloat16 k[kStages][2][kBN][64];
   uint64_t full[kStages], empty[kStages], tfull[2], tempty[2], qbar;
   uint32_t tmem_base;
-  float m2[GW], invl[GW];
+  alignas(16) float bias[GW];  // pass 2: per query row, m_r + log2(G * l_r) (log2 units)
   float red[2][2][kBN];      // pass 2: [tile parity][column half][key] partial sums
   float ml[kBN][2];          // pass 1, GW=128: second column half's (max, sum) per row
 };
@@ -186,8 +206,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         L = L * exp2f(M - nm) + l * exp2f(m - nm);
         M = nm;
       }
-      sm.m2[r] = M;
-      sm.invl[r] = L > 0.f ? 1.f / (L * static_cast<float>(p.group)) : 0.f;  // folds the 1/G mean
+      // exp2(s*c - m) / (G*l) == exp2(s*c - bias): one FFMA + one MUFU per score
+      sm.bias[r] = L > 0.f ? M + log2f(L * static_cast<float>(p.group)) : CUDART_INF_F;
     }
   }
   tc_fence_before();
@@ -202,12 +222,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int c = 0; c < 2; ++c)
         for (int rh = 0; rh < GW / 128; ++rh)
           tma_load_2d(&sm.q[c][rh * 128][0], &tm_q, 64 * c, qrow0 + 128 * rh, &sm.qbar);
+      const uint64_t pol = l2_policy(PASS == 1);
       for (int j = j0; j < j1; ++j) {
         const int it = j - j0, s = it % kStages;
         mbar_wait(&sm.empty[s], ((it / kStages) & 1) ^ 1);
         mbar_arrive_expect_tx(&sm.full[s], kTileBytes);
         for (int c = 0; c < 2; ++c)
-          tma_load_2d(&sm.k[s][c][0][0], &tm_k, 64 * c, krow0 + j * kBN, &sm.full[s]);
+          tma_load_2d_hint(&sm.k[s][c][0][0], &tm_k, 64 * c, krow0 + j * kBN, &sm.full[s], pol);
       }
     }
   } else if (warp == kMmaWarp) {
@@ -265,23 +286,31 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_ld32(tmem + lane_base + buf * GW + mh * kBN + cb * 32, v);
           const int c0 = ts + cb * 32;
           float bmax = -CUDART_INF_F;
+          if (c0 + 31 > limit) {  // only the window's tiles (and the tail) need masking
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            v[i] = c0 + i <= limit ? v[i] * p.scale_log2 : -CUDART_INF_F;
-            bmax = fmaxf(bmax, v[i]);
+            for (int i = 0; i < 32; ++i) {
+              v[i] = c0 + i <= limit ? v[i] : -CUDART_INF_F;
+              bmax = fmaxf(bmax, v[i]);
+            }
+            if (bmax == -CUDART_INF_F) continue;
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) bmax = fmaxf(bmax, v[i]);
           }
-          if (bmax == -CUDART_INF_F) continue;
+          // running max kept in raw-score units, exponents via one FFMA each
           const float nm = fmaxf(m, bmax);
+          const float nms = nm * p.scale_log2;
           float acc = 0.f;
 #pragma unroll
-          for (int i = 0; i < 32; ++i) acc += fast_exp2(v[i] - nm);
-          l = l * fast_exp2(m - nm) + acc;
+          for (int i = 0; i < 32; ++i) acc += fast_exp2(fmaf(v[i], p.scale_log2, -nms));
+          l = l * fast_exp2((m - nm) * p.scale_log2) + acc;
           m = nm;
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.tempty[buf]);
       }
+      m = m == -CUDART_INF_F ? m : m * p.scale_log2;  // to log2 units
       if (MH == 1) {
         if (half == 1) {
           sm.ml[32 * quad + lane][0] = m;
@@ -314,10 +343,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int cb = half * (GW / 64); cb < (half + 1) * (GW / 64); ++cb) {
           float v[32];
           tmem_ld32(tmem + lane_base + buf * GW + cb * 32, v);
+          const float4* b4 = reinterpret_cast<const float4*>(sm.bias + cb * 32);
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const int r = cb * 32 + i;
-            acc += fast_exp2(fmaf(v[i], p.scale_log2, -sm.m2[r])) * sm.invl[r];
+          for (int i = 0; i < 32; i += 4) {
+            const float4 b = b4[i / 4];  // broadcast: every lane reads the same columns
+            acc += fast_exp2(fmaf(v[i], p.scale_log2, -b.x));
+            acc += fast_exp2(fmaf(v[i + 1], p.scale_log2, -b.y));
+            acc += fast_exp2(fmaf(v[i + 2], p.scale_log2, -b.z));
+            acc += fast_exp2(fmaf(v[i + 3], p.scale_log2, -b.w));
           }
         }
         tc_fence_before();

@@ -251,8 +251,9 @@ def compact(k: torch.Tensor, v: torch.Tensor, offsets: torch.Tensor, idx: torch.
     sbh, slo, shi = i32(seg_bh), i32(seg_lo), i32(seg_hi)
     _native.check(_lib.fkv_compact(k.data_ptr(), v.data_ptr(), T, len(seg_lo), offsets.data_ptr(),
                                    idx.data_ptr(), sbh.data_ptr(), slo.data_ptr(), shi.data_ptr(),
-                                   cache.seg_row0.data_ptr(), 1, cache.k.data_ptr(),
-                                   cache.v.data_ptr(), _stream()))
+                                   cache.seg_row0.data_ptr(), 1,
+                                   int((seg_hi - seg_lo).max()) if len(seg_lo) else 0,
+                                   cache.k.data_ptr(), cache.v.data_ptr(), _stream()))
     cache.host["compact_args"] = (sbh, slo, shi)  # keep alive until the stream consumes them
     return cache
 
