@@ -379,6 +379,8 @@ def run_fairkv(args):
         out["emulated_tp"] = emulate_tp(args, budgets, caches[0].k.device)
     if rank == 0 and world == 1 and not args.no_cpu:
         out["planner"] = planner_compare(budgets)
+    if rank == 0 and world == 1 and not args.no_emulate:
+        out["prefill"] = prefill_compress(peaks)
     if rank == 0:
         print(json.dumps(out))
     if world > 1:
@@ -449,6 +451,47 @@ def emulate_tp(args, budgets, dev):
                        "max over ranks; all-gather not included (single GPU); sim = reference simulator, "
                        "pure-cache latency model")
     return results
+
+
+def prefill_compress(peaks):
+    """Per-layer prefill compression on the GPU (K1 score -> A18+K2 -> K3),
+    cfg2 (Llama-3.1-8B shape, 16k context, budget 256) and the 70B shape at
+    32k, timed with CUDA events; K1 against the tensor roofline."""
+    import torch
+    from paper_2502_15804_b200 import ops
+    dev = torch.device("cuda")
+    rows = {}
+    for name, (bt, hq, hkv, T, B) in {"llama-3.1-8b_T16k_B256": (1, 32, 8, 16384, 256),
+                                     "llama-3.1-8b_T16k_B256_batch4": (4, 32, 8, 16384, 256),
+                                     "llama-3.3-70b_T32k_B1024": (1, 64, 8, 32768, 1024)}.items():
+        w = WINDOW
+        g = torch.Generator(device=dev).manual_seed(5)
+        q = torch.randn((bt, hq, w, HEAD_DIM), generator=g, device=dev).to(torch.bfloat16)
+        k = torch.randn((bt, hkv, T, HEAD_DIM), generator=g, device=dev).to(torch.bfloat16)
+        v = torch.randn((bt, hkv, T, HEAD_DIM), generator=g, device=dev).to(torch.bfloat16)
+        ws = torch.empty(int(ops._lib.fkv_score_workspace_bytes(bt, hkv, T, w, hq // hkv)),
+                         dtype=torch.uint8, device=dev)
+        sc = ops.score(q, k, workspace=ws)
+        hb, off, idx = ops.ada_select(sc, B, w)
+        t_score = timed(lambda: ops.score(q, k, workspace=ws), 10) / 10
+        t_sel = timed(lambda: ops.ada_select(sc, B, w), 10) / 10
+        cache, _, _ = ops.compress_layer(q, k, v, B, w)
+        hbh = hb.cpu().numpy().reshape(-1)
+        import numpy as np
+        bh = np.arange(bt * hkv)
+        qrow = (bh // hkv) * hq + (bh % hkv) * (hq // hkv)
+        t_cmp = timed(lambda: ops.compact(k, v, off, idx, bh, np.zeros_like(bh), hbh, qrow, qrow,
+                                          hq // hkv), 5) / 5
+        flops = 2 * 2.0 * bt * hq * w * T * HEAD_DIM  # two passes of Q_win.K^T
+        kbytes = bt * hkv * T * HEAD_DIM * 2
+        tf_peak = float(peaks.get("bf16_tflops", 1590.0))
+        rows[name] = {
+            "score_us": t_score * 1e6, "ada_select_us": t_sel * 1e6, "compact_us": t_cmp * 1e6,
+            "score_tflops": flops / t_score / 1e12, "score_tflops_frac": flops / t_score / 1e12 / tf_peak,
+            "score_K_read_GBs_per_pass": kbytes / (t_score / 2) / 1e9,
+            "roofline_us": max(flops / (tf_peak * 1e12), 2 * kbytes / (float(peaks.get("hbm_gbs", 6650.0)) * 1e9)) * 1e6,
+        }
+    return rows
 
 
 def planner_compare(budgets):

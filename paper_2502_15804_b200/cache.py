@@ -72,8 +72,9 @@ def plan_work(seg_len, n_workers: int, chunk: int | None = None,
     consecutive item ids and start on a 16-token tile.
 
     Returns item_seg, item_t0, item_t1 (int32 [n_items]), seg_item_ptr (int32
-    [n_seg+1]), warp_ptr (int32 [n_workers+1]) and work_list (int32
-    [n_items], item ids grouped by worker).
+    [n_seg+1]), warp_ptr (int32 [busy+1], busy <= n_workers: only busy
+    workers are launched, and fewer busy warps per CTA get deeper rings) and
+    work_list (int32 [n_items], item ids grouped by worker).
     """
     seg_len = np.asarray(seg_len, dtype=np.int64)
     n_seg = len(seg_len)
@@ -123,9 +124,14 @@ def plan_work(seg_len, n_workers: int, chunk: int | None = None,
     owner = np.asarray(owner, dtype=np.int64)
     seg_item_ptr = np.zeros(n_seg + 1, dtype=np.int32)
     seg_item_ptr[1:] = np.cumsum(np.bincount(item_seg, minlength=n_seg))
-    warp_ptr = np.zeros(W + 1, dtype=np.int32)
-    warp_ptr[1:] = np.cumsum(np.bincount(owner, minlength=W))
-    work_list = np.arange(len(item_seg), dtype=np.int32)  # owners are non-decreasing
+    busy = int(owner.max()) + 1 if len(owner) else 1  # owners are 0..busy-1, non-decreasing
+    warp_ptr = np.zeros(busy + 1, dtype=np.int32)
+    warp_ptr[1:] = np.cumsum(np.bincount(owner, minlength=busy))
+    # Within a worker, pieces of split segments go first: their LSE merges
+    # (done by whichever piece finishes last) then overlap the streaming of
+    # whole segments instead of all landing in the kernel's tail.
+    split = (np.diff(seg_item_ptr) > 1)[item_seg]
+    work_list = np.lexsort((np.arange(len(item_seg)), ~split, owner)).astype(np.int32)
     return item_seg, t0, t1, seg_item_ptr, warp_ptr, work_list
 
 

@@ -32,11 +32,10 @@ namespace fkv {
 namespace {
 
 constexpr int kWarps = 4;
-constexpr int kStages = 3;
+constexpr int kRingStages = 12;  // per CTA: split over the active warps (12/6/4/3 each)
 constexpr int kTileTok = 16;
 constexpr int kTileBytes = kTileTok * FKV_HEAD_DIM * 2;  // 4 KiB per K or V tile
-constexpr int kRingBytes = kStages * 2 * kTileBytes;     // per warp
-constexpr int kSmemBytes = kWarps * kRingBytes;
+constexpr int kSmemBytes = kRingStages * 2 * kTileBytes;  // 96 KiB per CTA
 constexpr int kMergeMax = 32;                            // max items per segment (host-enforced)
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
@@ -89,19 +88,23 @@ __device__ __forceinline__ int n_tiles_of(const DecodeParams& p, int it, int& t0
 template <int G>
 __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodeParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ uint64_t bars[kWarps][kStages];
+  __shared__ uint64_t bars[kRingStages];
   __shared__ float scratch[kWarps][kMergeMax * 8];
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  uint8_t* ring = smem + warp * kRingBytes;
+  // a short schedule leaves warps idle: the active warps split the CTA's 12
+  // ring stages, so a lone worker keeps 96 KiB in flight instead of 24 KiB
+  const int kStages = kRingStages / static_cast<int>(blockDim.x >> 5);
+  uint8_t* ring = smem + warp * kStages * 2 * kTileBytes;
+  uint64_t* wbars = bars + warp * kStages;
   // worker ids are spread over CTAs first so a short schedule still uses every SM
   const int worker = warp * gridDim.x + blockIdx.x;
   const int w_beg = worker < p.n_workers ? p.warp_ptr[worker] : 0;
   const int w_end = worker < p.n_workers ? p.warp_ptr[worker + 1] : 0;
 
   if (lane == 0) {
-    for (int s = 0; s < kStages; ++s) mbar_init(&bars[warp][s], 1);
+    for (int s = 0; s < kStages; ++s) mbar_init(&wbars[s], 1);
     fence_mbar_init();
   }
   __syncwarp();
@@ -135,9 +138,9 @@ __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodePara
         const int s = p_seq % kStages;
         const int64_t row = p_row + kTileTok * p_t;
         uint8_t* dst = ring + s * 2 * kTileBytes;
-        mbar_arrive_expect_tx(&bars[warp][s], 2 * kTileBytes);
-        bulk_g2s(dst, p.k + row * FKV_HEAD_DIM, kTileBytes, &bars[warp][s]);
-        bulk_g2s(dst + kTileBytes, p.v + row * FKV_HEAD_DIM, kTileBytes, &bars[warp][s]);
+        mbar_arrive_expect_tx(&wbars[s], 2 * kTileBytes);
+        bulk_g2s(dst, p.k + row * FKV_HEAD_DIM, kTileBytes, &wbars[s]);
+        bulk_g2s(dst + kTileBytes, p.v + row * FKV_HEAD_DIM, kTileBytes, &wbars[s]);
       }
       ++p_t;
       ++p_seq;
@@ -196,7 +199,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodePara
 
     for (int i = 0; i < nt; ++i) {
       const int s = c_seq % kStages;
-      mbar_wait(&bars[warp][s], (c_seq / kStages) & 1);
+      mbar_wait(&wbars[s], (c_seq / kStages) & 1);
       const uint32_t kt = smem_u32(ring + s * 2 * kTileBytes);
       const uint32_t vt = kt + kTileBytes;
 
@@ -395,7 +398,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodePara
     __threadfence_system();
     __syncwarp();
     if (lane == 0 &&
-        atomicAdd(p.sig_done, 1) == static_cast<int>(gridDim.x) * kWarps - 1) {
+        atomicAdd(p.sig_done, 1) == static_cast<int>(gridDim.x * (blockDim.x >> 5)) - 1) {
       *p.sig_done = 0;
       __threadfence_system();
       for (int j = 0; j < p.n_sig; ++j) atomicAdd_system(p.sig_flag[j] + p.my_rank, 1);
@@ -491,11 +494,12 @@ int launch_decode(const DecodeParams& p, cudaStream_t st) {
                                                   kSmemBytes);
     grid_cap = sms * (per_sm > 0 ? per_sm : 1);
   }
-  (void)grid_cap;
-  const int grid = (p.n_workers + kWarps - 1) / kWarps;
+  // up to 2 CTAs per SM; 1-4 active warps per CTA (worker w -> CTA w % grid)
+  const int grid = p.n_workers < grid_cap ? p.n_workers : grid_cap;
+  const int wpc = (p.n_workers + grid - 1) / grid;  // 12 stages split 12/6/4/3
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid, 1, 1);
-  cfg.blockDim = dim3(kWarps * 32, 1, 1);
+  cfg.blockDim = dim3(wpc * 32, 1, 1);
   cfg.dynamicSmemBytes = kSmemBytes;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];

@@ -234,133 +234,127 @@ __global__ void __launch_bounds__(kThreads)
 // ------------------------------------------------ A18 + K2, one cluster ----
 // One thread-block cluster per request, one CTA per KV head (cluster size =
 // Hkv <= 8).  Each CTA stages its head's scores in shared memory when they
-// fit, finds its floor threshold, then the cluster runs the global radix
-// select together: per 8-bit digit every CTA histograms its own head's
-// non-floor keys and the histograms are summed through distributed shared
-// memory, so all CTAs derive the same digit.  Budgets, offsets (request b
-// starts at b*Hkv*budget: every request keeps exactly Hkv*budget tokens) and
-// the ascending index lists are written by the same launch.
+// fit; budgets, offsets (request b starts at b*Hkv*budget: every request
+// keeps exactly Hkv*budget tokens) and the ascending index lists are written
+// by the same launch.
 constexpr int kStageLimit = 40 * 1024;  // scores staged in smem up to 160 KiB
 
-template <class KeyOf>
-__device__ uint64_t cluster_select_kth(KeyOf key_of, int n, uint32_t k, SelectSmem& sm,
-                                       cg::cluster_group& cluster) {
-  uint64_t prefix = 0, mask = 0;
-  uint32_t need = k;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const unsigned ranks = cluster.num_blocks();
-  for (int shift = 56; shift >= 0; shift -= 8) {
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) sm.hist[i] = 0;
-    __syncthreads();
-    for (int base = 0; base < n; base += blockDim.x) {
-      const int i = base + threadIdx.x;
-      uint64_t key = 0;
-      const bool ok = i < n && key_of(i, key) && (key & mask) == prefix;
-      const uint32_t d = ok ? static_cast<uint32_t>(key >> shift) & 255u : 256u;
-      const uint32_t peers = __match_any_sync(0xffffffffu, d);
-      if (ok && lane == __ffs(peers) - 1) atomicAdd(&sm.hist[d], __popc(peers));
-    }
-    cluster.sync();  // every CTA's histogram is complete
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) {
-      uint32_t t = 0;
-      for (unsigned r = 0; r < ranks; ++r) t += cluster.map_shared_rank(sm.hist, r)[i];
-      sm.gh[i] = t;
-    }
-    cluster.sync();  // remote reads done before anyone zeroes its histogram
-    if (warp == 0) {
-      uint32_t local = 0;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) local += sm.gh[8 * lane + j];
-      uint32_t incl = local;
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const uint32_t v = __shfl_down_sync(0xffffffffu, incl, off);
-        if (lane + off < 32) incl += v;
-      }
-      const uint32_t suffix = incl - local;
-      if (suffix < need && suffix + local >= need) {
-        uint32_t acc = suffix;
-        for (int j = 7; j >= 0; --j) {
-          const uint32_t c = sm.gh[8 * lane + j];
-          if (acc + c >= need) {
-            sm.digit = 8 * lane + j;
-            sm.above = acc;
-            break;
-          }
-          acc += c;
-        }
-      }
-    }
-    __syncthreads();
-    const uint32_t d = sm.digit;
-    need -= sm.above;
-    prefix |= static_cast<uint64_t>(d) << shift;
-    mask |= 255ull << shift;
-    const bool whole = sm.gh[d] == need;
-    __syncthreads();
-    if (whole) return prefix;
-  }
-  return prefix;
-}
-
+// Ada split without materialising the floors: with N_h(tau) = #{t : gkey_h(t)
+// >= tau}, the number of globally chosen (non-floor) elements of head h above
+// tau is max(0, N_h(tau) - floor) (a head's floor is its own top-floor in the
+// same order), so the global threshold is the largest tau with
+// G(tau) = sum_h max(0, N_h(tau) - floor) >= R.  A cluster-wide MSB-first radix
+// search finds it: per 8-bit digit every CTA (one head) builds its histogram,
+// turns it into suffix counts S_h[d] = N_h(prefix.d...) and publishes them in
+// shared memory; every CTA evaluates G[d] for all 256 digits from the
+// peers' S arrays (DSMEM) and takes d* = max{d : G[d] >= R}.  Only heads that
+// end below their floor (N_h(tau) < floor) need their own top-floor select.
 __global__ void __launch_bounds__(kThreads)
     ada_select_kernel(const float* __restrict__ scores, int n, int window, int floor_k,
                       int rest_total, int budget, int32_t* __restrict__ budgets,
                       int64_t* __restrict__ offsets, int32_t* __restrict__ idx) {
   extern __shared__ __align__(16) uint8_t dyn[];
   __shared__ SelectSmem sm;
+  __shared__ int32_t suffix[256];
   __shared__ int32_t s_budget;
   cg::cluster_group cluster = cg::this_cluster();
   const int hkv = static_cast<int>(cluster.num_blocks());
   const int h = static_cast<int>(cluster.block_rank());
   const int b = blockIdx.y;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const float* src = scores + (static_cast<int64_t>(b) * hkv + h) * n;
   const bool staged = n <= kStageLimit;
   float* sv = reinterpret_cast<float*>(dyn);
-  uint32_t* floor_bits = reinterpret_cast<uint32_t*>(dyn + (staged ? n * 4 : 0));
   if (staged)
     for (int t = threadIdx.x; t < n; t += blockDim.x) sv[t] = src[t];
   __syncthreads();
   const float* s = staged ? sv : src;
+  const uint32_t gbase = static_cast<uint32_t>(h) * n;
 
-  // phase 1: this head's floor (top floor_k by (score desc, token asc)) as a bitmap
-  uint64_t tau = kNone;
-  if (floor_k > 0)
-    tau = cta_select_kth(
+  // ---- cluster radix search for tau over the global keys of all heads
+  uint64_t prefix = 0, mask = 0;
+  int above = 0;          // this head's elements strictly above the current prefix range
+  int n_at_tau = 0;       // N_h(tau) once found
+  bool have_tau = rest_total > 0;
+  if (have_tau) {
+    for (int shift = 56; shift >= 0; shift -= 8) {
+      for (int i = threadIdx.x; i < 256; i += blockDim.x) sm.hist[i] = 0;
+      __syncthreads();
+      for (int base = 0; base < n; base += blockDim.x) {
+        const int t = base + threadIdx.x;
+        uint64_t key = t < n ? compose(s[t], gbase + t) : 0;
+        const bool ok = t < n && (key & mask) == prefix;
+        const uint32_t d = ok ? static_cast<uint32_t>(key >> shift) & 255u : 256u;
+        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        if (ok && lane == __ffs(peers) - 1) atomicAdd(&sm.hist[d], __popc(peers));
+      }
+      __syncthreads();
+      if (warp == 0) {  // suffix[d] = above + sum_{d' >= d} hist[d']
+        uint32_t loc[8], run = 0;
+#pragma unroll
+        for (int j = 7; j >= 0; --j) {
+          run += sm.hist[8 * lane + j];
+          loc[j] = run;
+        }
+        uint32_t incl = run;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const uint32_t v = __shfl_down_sync(0xffffffffu, incl, off);
+          if (lane + off < 32) incl += v;
+        }
+        const uint32_t higher = incl - run;  // bins owned by higher lanes
+#pragma unroll
+        for (int j = 0; j < 8; ++j) suffix[8 * lane + j] = above + static_cast<int>(higher + loc[j]);
+      }
+      cluster.sync();  // every head's suffix counts are published
+      bool ge = false;
+      int gd = 0;
+      if (threadIdx.x < 256) {
+        for (int r = 0; r < hkv; ++r) {
+          const int v = cluster.map_shared_rank(suffix, r)[threadIdx.x] - floor_k;
+          gd += v > 0 ? v : 0;
+        }
+        ge = gd >= rest_total;
+      }
+      // G is non-increasing in d: d* = (#digits with G >= R) - 1
+      const uint32_t cnt = block_sum(ge ? 1u : 0u, sm);
+      const int dstar = static_cast<int>(cnt) - 1;
+      if (threadIdx.x == dstar) {
+        sm.digit = dstar;
+        sm.above = gd == rest_total;  // exact: the whole bucket is taken
+      }
+      __syncthreads();
+      const int d = static_cast<int>(sm.digit);
+      const bool exact = sm.above != 0;
+      n_at_tau = suffix[d];
+      const int next_above = d < 255 ? suffix[d + 1] : above;
+      prefix |= static_cast<uint64_t>(d) << shift;
+      mask |= 255ull << shift;
+      cluster.sync();  // peers are done reading `suffix` before it is rewritten
+      if (exact) break;
+      above = next_above;
+    }
+  }
+  const uint64_t tau = prefix;
+  const int c_h = have_tau ? (n_at_tau - floor_k > 0 ? n_at_tau - floor_k : 0) : 0;
+  const bool below_floor = !have_tau || n_at_tau < floor_k;
+
+  // heads that end below their floor keep exactly their own top-floor tokens
+  uint64_t ltau = kNone;
+  if (below_floor && floor_k > 0)
+    ltau = cta_select_kth(
         [&](int i, uint64_t& key) {
           key = compose(s[i], static_cast<uint32_t>(i));
           return true;
         },
         n, static_cast<uint32_t>(floor_k), sm);
-  for (int base = 0; base < n; base += blockDim.x) {
-    const int t = base + threadIdx.x;
-    const bool fl = t < n && tau != kNone && compose(s[t], static_cast<uint32_t>(t)) >= tau;
-    const uint32_t word = __ballot_sync(0xffffffffu, fl);
-    if ((threadIdx.x & 31) == 0 && t < n) floor_bits[t >> 5] = word;
-  }
-  __syncthreads();
-  auto in_floor = [&](int t) { return (floor_bits[t >> 5] >> (t & 31)) & 1u; };
-  const uint32_t gbase = static_cast<uint32_t>(h) * n;
-
-  // phase 2: global top rest_total of the non-floor scores, cluster-wide
-  uint64_t gtau = kNone;
-  if (rest_total > 0)
-    gtau = cluster_select_kth(
-        [&](int t, uint64_t& key) {
-          if (in_floor(t)) return false;
-          key = compose(s[t], gbase + t);
-          return true;
-        },
-        n, static_cast<uint32_t>(rest_total), sm, cluster);
-  auto chosen = [&](int t) {
-    return in_floor(t) || (gtau != kNone && compose(s[t], gbase + t) >= gtau);
+  auto chosen = [&](int t) -> bool {
+    if (!below_floor) return compose(s[t], gbase + t) >= tau;
+    return ltau != kNone && compose(s[t], static_cast<uint32_t>(t)) >= ltau;
   };
 
-  // phase 3: this head's budget, then the request's head offsets via DSMEM
-  uint32_t c = 0;
-  for (int t = threadIdx.x; t < n; t += blockDim.x) c += (!in_floor(t) && chosen(t)) ? 1u : 0u;
-  const uint32_t tot = block_sum(c, sm);
-  if (threadIdx.x == 0) s_budget = window + floor_k + static_cast<int32_t>(tot);
+  // ---- budget, offsets within the request via DSMEM, ascending indices
+  if (threadIdx.x == 0) s_budget = window + floor_k + c_h;
   cluster.sync();
   int64_t off = static_cast<int64_t>(b) * hkv * budget;
   for (int r = 0; r < h; ++r) off += *cluster.map_shared_rank(&s_budget, r);
@@ -370,8 +364,6 @@ __global__ void __launch_bounds__(kThreads)
     offsets[bh] = off;
     if (b == static_cast<int>(gridDim.y) - 1 && h == hkv - 1) offsets[bh + 1] = off + s_budget;
   }
-
-  // phase 4: selected tokens ascending, then the window
   int32_t* out = idx + off;
   uint32_t written = 0;
   for (int base = 0; base < n; base += blockDim.x) {
@@ -437,8 +429,7 @@ extern "C" int fkv_ada_select(const float* scores, int32_t batch, int32_t hkv, i
     return set_error(FKV_ERR_INVALID, "fkv_ada_select: Hkv * n too large");
   if (batch == 0) return FKV_OK;
   const int rest = hkv * sel - hkv * floor_k;
-  const size_t smem = (n <= kStageLimit ? static_cast<size_t>(n) * 4 : 0) +
-                      static_cast<size_t>((n + 31) / 32) * 4;
+  const size_t smem = n <= kStageLimit ? static_cast<size_t>(n) * 4 : 16;
   static size_t configured = 0;
   if (smem > configured) {
     if (int rc = cuda_check(cudaFuncSetAttribute(ada_select_kernel,

@@ -136,14 +136,18 @@ def test_selection_agreement_with_oracle_scores(cuda_device):
 
 
 @pytest.mark.parametrize("bt,T,budget,ties", [(3, 4096, 256, False), (2, 2048, 64, True),
-                                              (1, 65600, 1024, False), (2, 40000, 512, True)])
+                                              (1, 65600, 1024, False), (2, 40000, 512, True),
+                                              (2, 3000, 256, "zero-head"), (1, 1000, 32, False)])
 def test_fused_ada_select_bit_exact(cuda_device, bt, T, budget, ties):
     """The one-launch cluster kernel == oracle budgets + selection (also past
     the shared-memory staging limit, n > 40960)."""
     from paper_2502_15804_b200 import ops
     g = torch.Generator().manual_seed(bt * 7 + T)
     n = T - 32
-    sc = torch.randint(0, 5, (bt, 8, n), generator=g).float() if ties else torch.rand(bt, 8, n, generator=g)
+    sc = torch.randint(0, 5, (bt, 8, n), generator=g).float() if ties is True else torch.rand(bt, 8, n, generator=g)
+    if ties == "zero-head":  # a head that can only keep its floor
+        sc[:, 2] = 0.0
+        sc[:, 5] *= 1e-3
     hb, off, idx = ops.ada_select(sc.to(cuda_device), budget, 32)
     torch.cuda.synchronize()
     s64 = sc.double().numpy()

@@ -8,7 +8,8 @@ from paper_2502_15804_b200.cache import LayerCache
 dev = torch.device('cuda:0')
 bt = int(sys.argv[1]) if len(sys.argv) > 1 else 64
 B = int(sys.argv[2]) if len(sys.argv) > 2 else 1024
-hkv, G = 8, 8
+hkv = int(sys.argv[3]) if len(sys.argv) > 3 else 8
+G = 8
 rng = np.random.default_rng(0)
 lens = np.maximum(64, (B * rng.dirichlet(np.full(hkv, 8.0), size=bt) * hkv).round()).astype(int).ravel()
 hq = hkv * G
