@@ -303,24 +303,27 @@ def run_fairkv(args):
     qh.copy_(q)
     oh = torch.empty(o.shape, dtype=o.dtype, pin_memory=True)
     s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
-    ev_in = [torch.cuda.Event() for _ in range(args.layers)]
-    ev_out = [torch.cuda.Event() for _ in range(args.layers)]
+    cg = 8  # layers per copy (fewer, larger PCIe transfers; compute waits per group)
+    groups = [(a, min(a + cg, args.layers)) for a in range(0, args.layers, cg)]
+    ev_in = [torch.cuda.Event() for _ in groups]
+    ev_out = [torch.cuda.Event() for _ in groups]
 
     def e2e_body():
         cur = torch.cuda.current_stream()
         s_in.wait_stream(cur)
         s_out.wait_stream(cur)
         with torch.cuda.stream(s_in):
-            for l in range(args.layers):
-                q[l].copy_(qh[l], non_blocking=True)
-                ev_in[l].record(s_in)
-        for l in range(args.layers):
-            cur.wait_event(ev_in[l])
-            dec.layer(l, q[l], o[l])
-            ev_out[l].record(cur)
+            for gi, (a, b) in enumerate(groups):
+                q[a:b].copy_(qh[a:b], non_blocking=True)
+                ev_in[gi].record(s_in)
+        for gi, (a, b) in enumerate(groups):
+            cur.wait_event(ev_in[gi])
+            for l in range(a, b):
+                dec.layer(l, q[l], o[l])
+            ev_out[gi].record(cur)
             with torch.cuda.stream(s_out):
-                s_out.wait_event(ev_out[l])
-                oh[l].copy_(o[l], non_blocking=True)
+                s_out.wait_event(ev_out[gi])
+                oh[a:b].copy_(o[a:b], non_blocking=True)
         cur.wait_stream(s_in)
         cur.wait_stream(s_out)
     if tp == 1:
@@ -476,12 +479,9 @@ def prefill_compress(peaks):
         t_score = timed(lambda: ops.score(q, k, workspace=ws), 10) / 10
         t_sel = timed(lambda: ops.ada_select(sc, B, w), 10) / 10
         cache, _, _ = ops.compress_layer(q, k, v, B, w)
-        hbh = hb.cpu().numpy().reshape(-1)
-        import numpy as np
-        bh = np.arange(bt * hkv)
-        qrow = (bh // hkv) * hq + (bh % hkv) * (hq // hkv)
-        t_cmp = timed(lambda: ops.compact(k, v, off, idx, bh, np.zeros_like(bh), hbh, qrow, qrow,
-                                          hq // hkv), 5) / 5
+        sbh, slo, shi = cache.host["compact_args"]
+        t_cmp = timed(lambda: ops.compact_into(cache, k, v, off, idx, sbh, slo, shi,
+                                               int(hb.max().item())), 5) / 5
         flops = 2 * 2.0 * bt * hq * w * T * HEAD_DIM  # two passes of Q_win.K^T
         kbytes = bt * hkv * T * HEAD_DIM * 2
         tf_peak = float(peaks.get("bf16_tflops", 1590.0))

@@ -46,6 +46,9 @@ struct ScoreParams {
   float scale_log2;    // log2(e) / sqrt(d)
   float* stats;        // [Bt*Hkv, n_chunks, GW, 2] (max, sum) in log2 units
   float* raw;          // [Bt*Hkv, T - w]
+  float* scores;       // pooled output (fused mode)
+  int pool_r;          // pooling radius (pool_k / 2)
+  struct GridBar* gridbar;  // fused mode: zeroed counter + generation
 };
 
 // ------------------------------------------------------------ tcgen05 ----
@@ -160,7 +163,33 @@ struct __align__(1024) ScoreSmem {
   float ml[kBN][2];          // pass 1, GW=128: second column half's (max, sum) per row
 };
 
-template <int PASS, int GW>
+struct GridBar {
+  unsigned count, gen;
+};
+
+// Grid-wide barrier among the epilogue warps of co-resident CTAs (cooperative
+// launch); the TMA and MMA warps keep streaming while the epilogue waits.
+__device__ __forceinline__ void epi_grid_sync(GridBar* gb) {
+  asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps));
+  if (threadIdx.x == 0) {
+    const unsigned g = *reinterpret_cast<volatile unsigned*>(&gb->gen);
+    __threadfence();
+    if (atomicAdd(&gb->count, 1) == gridDim.x * gridDim.y - 1) {
+      gb->count = 0;
+      __threadfence();
+      atomicAdd(&gb->gen, 1);
+    } else {
+      while (*reinterpret_cast<volatile unsigned*>(&gb->gen) == g) __nanosleep(64);
+    }
+    __threadfence();
+  }
+  asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps));
+}
+
+// MODE 1: pass 1 only; MODE 2: pass 2 only; MODE 3: both passes + pooling in
+// one cooperative launch (stats combined after a grid barrier, K re-read from
+// L2, raw scores pooled after a second barrier).
+template <int MODE, int GW>
 __global__ void __launch_bounds__(kThreads, 1)
     score_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                  const ScoreParams p) {
@@ -168,14 +197,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   ScoreSmem<GW>& sm = *reinterpret_cast<ScoreSmem<GW>*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   constexpr uint32_t kCols = 2 * GW;  // two accumulator buffers of GW fp32 columns
+  constexpr bool kP1 = MODE != 2, kP2 = MODE != 1;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int bh = blockIdx.y, chunk = blockIdx.x;
   const int b = bh / p.hkv, h = bh - b * p.hkv;
-  const int n_keys = PASS == 1 ? p.T : p.T - p.window;
-  const int n_tiles_total = (n_keys + kBN - 1) / kBN;
-  const int j0 = chunk * p.tiles_per_chunk;
-  const int j1 = min(j0 + p.tiles_per_chunk, n_tiles_total);
+  const int n = p.T - p.window;
+  const int nt1 = (p.T + kBN - 1) / kBN, nt2 = (n + kBN - 1) / kBN;
+  const int a1 = chunk * p.tiles_per_chunk, e1 = kP1 ? min(a1 + p.tiles_per_chunk, nt1) : a1;
+  const int a2 = chunk * p.tiles_per_chunk, e2 = kP2 ? min(a2 + p.tiles_per_chunk, nt2) : a2;
+  const int n1 = max(e1 - a1, 0), n2 = max(e2 - a2, 0);  // tiles of each pass; iterations continue
   const int krow0 = bh * p.T;
   const int qrow0 = b * p.q_rows_per_req + h * GW;
 
@@ -194,13 +225,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     fence_mbar_init();
   }
   if (warp == kMmaWarp) tmem_alloc(&sm.tmem_base, kCols);
-  if (PASS == 2 && warp < kEpiWarps) {
-    // combine the pass-1 partial statistics of all chunks (log2 domain)
+
+  // combine every chunk's pass-1 statistics (log2 domain) into per-row biases
+  auto combine_stats = [&]() {
     for (int r = threadIdx.x; r < GW; r += 32 * kEpiWarps) {
       float M = -CUDART_INF_F, L = 0.f;
       const float* st = p.stats + (static_cast<int64_t>(bh) * p.n_chunks) * GW * 2;
       for (int c = 0; c < p.n_chunks; ++c) {
-        const float m = st[(c * GW + r) * 2], l = st[(c * GW + r) * 2 + 1];
+        const float m = __ldcg(st + (c * GW + r) * 2), l = __ldcg(st + (c * GW + r) * 2 + 1);
         if (l <= 0.f) continue;
         const float nm = fmaxf(M, m);
         L = L * exp2f(M - nm) + l * exp2f(m - nm);
@@ -209,7 +241,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       // exp2(s*c - m) / (G*l) == exp2(s*c - bias): one FFMA + one MUFU per score
       sm.bias[r] = L > 0.f ? M + log2f(L * static_cast<float>(p.group)) : CUDART_INF_F;
     }
-  }
+  };
+  if (MODE == 2 && warp < kEpiWarps) combine_stats();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -217,39 +250,43 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == kTmaWarp) {
     // ------------------------------------------------ TMA producer ----
-    if (lane == 0 && j1 > j0) {
+    if (lane == 0 && n1 + n2 > 0) {
       mbar_arrive_expect_tx(&sm.qbar, GW * 256);
       for (int c = 0; c < 2; ++c)
         for (int rh = 0; rh < GW / 128; ++rh)
           tma_load_2d(&sm.q[c][rh * 128][0], &tm_q, 64 * c, qrow0 + 128 * rh, &sm.qbar);
-      const uint64_t pol = l2_policy(PASS == 1);
-      for (int j = j0; j < j1; ++j) {
-        const int it = j - j0, s = it % kStages;
+      const uint64_t keep = l2_policy(true), stream = l2_policy(false);
+      for (int it = 0; it < n1 + n2; ++it) {
+        const bool p1 = it < n1;
+        const int j = p1 ? a1 + it : a2 + (it - n1);
+        const int s = it % kStages;
         mbar_wait(&sm.empty[s], ((it / kStages) & 1) ^ 1);
         mbar_arrive_expect_tx(&sm.full[s], kTileBytes);
         for (int c = 0; c < 2; ++c)
-          tma_load_2d_hint(&sm.k[s][c][0][0], &tm_k, 64 * c, krow0 + j * kBN, &sm.full[s], pol);
+          tma_load_2d_hint(&sm.k[s][c][0][0], &tm_k, 64 * c, krow0 + j * kBN, &sm.full[s],
+                           p1 ? keep : stream);
       }
     }
   } else if (warp == kMmaWarp) {
     // -------------------------------------------------- MMA issuer ----
-    if (lane == 0 && j1 > j0) {
+    if (lane == 0 && n1 + n2 > 0) {
       mbar_wait(&sm.qbar, 0);
       constexpr uint32_t kIdesc1 = idesc_bf16(128, kBN);
       constexpr uint32_t kIdesc2 = idesc_bf16(128, GW);
       const uint32_t q_base = smem_u32(&sm.q[0][0][0]);
-      for (int j = j0; j < j1; ++j) {
-        const int it = j - j0, s = it % kStages, buf = it & 1;
+      for (int it = 0; it < n1 + n2; ++it) {
+        const int s = it % kStages, buf = it & 1;
         mbar_wait(&sm.full[s], (it / kStages) & 1);
         mbar_wait(&sm.tempty[buf], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t k_base = smem_u32(&sm.k[s][0][0][0]);
         const uint32_t d_buf = tmem + buf * GW;
+        const bool p1 = it < n1;
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           const uint32_t koff = (kk >> 2) * (kBN * 128) + (kk & 3) * 32;
           const uint32_t qoff = (kk >> 2) * (GW * 128) + (kk & 3) * 32;
-          if (PASS == 1) {
+          if (p1) {
 #pragma unroll
             for (int mh = 0; mh < GW / 128; ++mh)
               umma_bf16(d_buf + mh * kBN, sw128_desc(q_base + qoff + mh * 128 * 128),
@@ -266,7 +303,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---------------------------------------------------- epilogue ----
     const int quad = warp & 3, half = warp >> 2;
     const uint32_t lane_base = static_cast<uint32_t>(32 * quad) << 16;
-    if (PASS == 1) {
+    if (kP1) {
       // GW=256: warp half = row half (one whole row per thread);
       // GW=128: warp half = column half (per-row partials, combined at the end)
       constexpr int MH = GW / 128;
@@ -275,11 +312,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int r = mh * 128 + 32 * quad + lane;
       const int limit = min(p.T - 1, p.T - p.window + (r % p.window));  // last visible key
       float m = -CUDART_INF_F, l = 0.f;
-      for (int j = j0; j < j1; ++j) {
-        const int it = j - j0, buf = it & 1;
+      for (int it = 0; it < n1; ++it) {
+        const int buf = it & 1;
         mbar_wait(&sm.tfull[buf], (it >> 1) & 1);
         tc_fence_after();
-        const int ts = j * kBN;
+        const int ts = (a1 + it) * kBN;
 #pragma unroll 1
         for (int cb = cb0; cb < cb1; ++cb) {
           float v[32];
@@ -331,11 +368,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         st[0] = m;
         st[1] = l;
       }
-    } else {
-      const int n = p.T - p.window;
+    }
+    if (MODE == 3) {
+      epi_grid_sync(p.gridbar);  // every chunk's statistics are in global memory
+      combine_stats();
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps));
+    }
+    if (kP2) {
       const int key = 32 * quad + lane;
-      for (int j = j0; j < j1; ++j) {
-        const int it = j - j0, buf = it & 1;
+      for (int i2 = 0; i2 < n2; ++i2) {
+        const int it = n1 + i2, buf = it & 1;
         mbar_wait(&sm.tfull[buf], (it >> 1) & 1);
         tc_fence_after();
         float acc = 0.f;
@@ -346,11 +388,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           const float4* b4 = reinterpret_cast<const float4*>(sm.bias + cb * 32);
 #pragma unroll
           for (int i = 0; i < 32; i += 4) {
-            const float4 b = b4[i / 4];  // broadcast: every lane reads the same columns
-            acc += fast_exp2(fmaf(v[i], p.scale_log2, -b.x));
-            acc += fast_exp2(fmaf(v[i + 1], p.scale_log2, -b.y));
-            acc += fast_exp2(fmaf(v[i + 2], p.scale_log2, -b.z));
-            acc += fast_exp2(fmaf(v[i + 3], p.scale_log2, -b.w));
+            const float4 bb = b4[i / 4];  // broadcast: every lane reads the same columns
+            acc += fast_exp2(fmaf(v[i], p.scale_log2, -bb.x));
+            acc += fast_exp2(fmaf(v[i + 1], p.scale_log2, -bb.y));
+            acc += fast_exp2(fmaf(v[i + 2], p.scale_log2, -bb.z));
+            acc += fast_exp2(fmaf(v[i + 3], p.scale_log2, -bb.w));
           }
         }
         tc_fence_before();
@@ -358,9 +400,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) mbar_arrive(&sm.tempty[buf]);
         sm.red[it & 1][half][key] = acc;
         asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps));
-        const int t = j * kBN + key;
+        const int t = (a2 + i2) * kBN + key;
         if (half == 0 && t < n)
           p.raw[static_cast<int64_t>(bh) * n + t] = acc + sm.red[it & 1][1][key];
+      }
+    }
+    if (MODE == 3) {
+      epi_grid_sync(p.gridbar);  // every raw column score is in global memory
+      const float* rr = p.raw + static_cast<int64_t>(bh) * n;
+      float* out = p.scores + static_cast<int64_t>(bh) * n;
+      const int t_end = min(e2 * kBN, n);
+      for (int t = a2 * kBN + threadIdx.x; t < t_end; t += 32 * kEpiWarps) {
+        float mx = __ldcg(rr + t);
+        const int lo = max(0, t - p.pool_r), hi = min(n - 1, t + p.pool_r);
+        for (int u = lo; u <= hi; ++u) mx = fmaxf(mx, __ldcg(rr + u));
+        out[t] = mx;
       }
     }
   }
@@ -441,25 +495,43 @@ namespace {
 
 template <int GW>
 int launch_score(const CUtensorMap& tq, const CUtensorMap& tk, const ScoreParams& p, int batch_heads,
-                 cudaStream_t st) {
+                 bool fused, cudaStream_t st) {
   const size_t smem = sizeof(ScoreSmem<GW>) + 1024;
   static bool configured = false;
   if (!configured) {
-    if (int rc = cuda_check(cudaFuncSetAttribute(score_kernel<1, GW>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-                            "score smem attribute"))
-      return rc;
-    if (int rc = cuda_check(cudaFuncSetAttribute(score_kernel<2, GW>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-                            "score smem attribute"))
-      return rc;
+    for (auto fn : {score_kernel<1, GW>, score_kernel<2, GW>, score_kernel<3, GW>})
+      if (int rc = cuda_check(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   smem),
+                              "score smem attribute"))
+        return rc;
     configured = true;
   }
   dim3 grid(p.n_chunks, batch_heads);
+  if (fused) {
+    // one cooperative launch: both passes and the pooling (grid <= #SMs, 1 CTA/SM)
+    if (int rc = cuda_check(cudaMemsetAsync(p.gridbar, 0, sizeof(GridBar), st), "gridbar reset"))
+      return rc;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cuda_check(cudaLaunchKernelEx(&cfg, score_kernel<3, GW>, tq, tk, p), "score fused launch");
+  }
   score_kernel<1, GW><<<grid, kThreads, smem, st>>>(tq, tk, p);
   if (int rc = cuda_check(cudaGetLastError(), "score pass 1 launch")) return rc;
   score_kernel<2, GW><<<grid, kThreads, smem, st>>>(tq, tk, p);
-  return cuda_check(cudaGetLastError(), "score pass 2 launch");
+  if (int rc = cuda_check(cudaGetLastError(), "score pass 2 launch")) return rc;
+  const int n = p.T - p.window;
+  const int64_t total = static_cast<int64_t>(batch_heads) * n;
+  pool_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(p.raw, p.scores, n,
+                                                                         p.pool_r, total);
+  return cuda_check(cudaGetLastError(), "score pool launch");
 }
 
 }  // namespace
@@ -501,14 +573,19 @@ extern "C" int fkv_snapkv_score(const void* q_win, const void* k, int32_t batch,
   if (int rc = make_map(&tk, k, static_cast<int64_t>(batch) * hkv * T, kBN)) return rc;
   float* stats = static_cast<float*>(workspace);
   float* raw = stats + static_cast<int64_t>(bh) * chunks * gw * 2;
+  auto* gridbar = reinterpret_cast<GridBar*>(
+      (reinterpret_cast<uintptr_t>(raw + static_cast<int64_t>(bh) * (T - window)) + 15) & ~uintptr_t(15));
   ScoreParams p{T, window, group, hkv, chunks, tiles_per_chunk, hq * window,
-                sm_scale * kLog2e, stats, raw};
+                sm_scale * kLog2e, stats, raw, scores, pool_k / 2, gridbar};
   auto st = static_cast<cudaStream_t>(stream);
-  int rc = gw == 128 ? launch_score<128>(tq, tk, p, bh, st) : launch_score<256>(tq, tk, p, bh, st);
-  if (rc) return rc;
-  const int n = T - window;
-  const int64_t total = static_cast<int64_t>(bh) * n;
-  pool_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(raw, scores, n, pool_k / 2,
-                                                                         total);
-  return cuda_check(cudaGetLastError(), "score pool launch");
+  // fused single launch whenever every CTA can be co-resident (1 CTA per SM)
+  int sms = 148;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const bool fused = static_cast<int64_t>(bh) * chunks <= sms;
+  return gw == 128 ? launch_score<128>(tq, tk, p, bh, fused, st)
+                   : launch_score<256>(tq, tk, p, bh, fused, st);
 }

@@ -230,6 +230,18 @@ def ada_select(scores: torch.Tensor, budget: int, window: int = 32, alpha: float
     return hb, offsets, idx[:bt * hkv * budget]
 
 
+def compact_into(cache: LayerCache, k: torch.Tensor, v: torch.Tensor, offsets: torch.Tensor,
+                 idx: torch.Tensor, seg_bh: torch.Tensor, seg_lo: torch.Tensor,
+                 seg_hi: torch.Tensor, max_tokens: int):
+    """K3 alone into an existing cache (device int32 segment tables; one launch)."""
+    _need_cuda(k, v, offsets, idx, seg_bh, seg_lo, seg_hi)
+    _native.check(_lib.fkv_compact(k.data_ptr(), v.data_ptr(), k.shape[2], int(seg_bh.shape[0]),
+                                   offsets.data_ptr(), idx.data_ptr(), seg_bh.data_ptr(),
+                                   seg_lo.data_ptr(), seg_hi.data_ptr(), cache.seg_row0.data_ptr(),
+                                   1, int(max_tokens), cache.k.data_ptr(), cache.v.data_ptr(),
+                                   _stream()))
+
+
 def compact(k: torch.Tensor, v: torch.Tensor, offsets: torch.Tensor, idx: torch.Tensor,
             seg_bh, seg_lo, seg_hi, seg_qrow, seg_out_row, group: int,
             chunk: int | None = None) -> LayerCache:
@@ -242,19 +254,15 @@ def compact(k: torch.Tensor, v: torch.Tensor, offsets: torch.Tensor, idx: torch.
     if k.dtype != torch.bfloat16 or k.shape != v.shape or k.shape[-1] != HEAD_DIM \
             or not (k.is_contiguous() and v.is_contiguous()):
         raise NativeError("k/v must be contiguous bf16 [Bt, Hkv, T, 128]")
-    T = k.shape[2]
     seg_lo = np.asarray(seg_lo, dtype=np.int64)
     seg_hi = np.asarray(seg_hi, dtype=np.int64)
     cache = LayerCache.allocate(seg_hi - seg_lo, seg_qrow, seg_out_row, group, k.device, chunk=chunk)
     dev = k.device
     i32 = lambda a: torch.as_tensor(np.ascontiguousarray(a, dtype=np.int32), device=dev)  # noqa: E731
-    sbh, slo, shi = i32(seg_bh), i32(seg_lo), i32(seg_hi)
-    _native.check(_lib.fkv_compact(k.data_ptr(), v.data_ptr(), T, len(seg_lo), offsets.data_ptr(),
-                                   idx.data_ptr(), sbh.data_ptr(), slo.data_ptr(), shi.data_ptr(),
-                                   cache.seg_row0.data_ptr(), 1,
-                                   int((seg_hi - seg_lo).max()) if len(seg_lo) else 0,
-                                   cache.k.data_ptr(), cache.v.data_ptr(), _stream()))
-    cache.host["compact_args"] = (sbh, slo, shi)  # keep alive until the stream consumes them
+    tabs = (i32(seg_bh), i32(seg_lo), i32(seg_hi))
+    compact_into(cache, k, v, offsets, idx, *tabs,
+                 int((seg_hi - seg_lo).max()) if len(seg_lo) else 0)
+    cache.host["compact_args"] = tabs  # keep alive until the stream consumes them
     return cache
 
 

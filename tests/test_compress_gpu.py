@@ -25,8 +25,11 @@ def _inputs(bt, hq, hkv, T, w, seed, dev, temp=1.0):
     return q.to(dev), k.to(dev), v.to(dev), q.double().numpy(), k.double().numpy(), v.double().numpy()
 
 
-@pytest.mark.parametrize("bt,hq,hkv,T", [(1, 32, 8, 4096), (2, 32, 8, 1000), (1, 64, 8, 2100), (2, 16, 4, 333)])
+@pytest.mark.parametrize("bt,hq,hkv,T", [(1, 32, 8, 4096), (2, 32, 8, 1000), (1, 64, 8, 2100), (2, 16, 4, 333),
+                                         (20, 32, 8, 300), (3, 64, 8, 20000)])
 def test_score_matches_oracle(cuda_device, bt, hq, hkv, T):
+    """Covers the fused cooperative launch (Bt*Hkv*chunks <= #SMs) and the
+    three-launch path (20 x 8 = 160 heads > 148 SMs)."""
     from paper_2502_15804_b200 import ops
     q, k, _, qn, kn, _ = _inputs(bt, hq, hkv, T, 32, 1, cuda_device, temp=2.0)
     s = ops.score(q, k).cpu().double().numpy()
