@@ -409,6 +409,7 @@ def emulate_tp(args, budgets, dev):
     q = torch.randn((L, bt, HQ, HEAD_DIM), device=dev).to(torch.bfloat16)
     model = fk.LatencyModel(0.0, 0.0, 1.0, 0.0)
     results = {}
+    samples = []  # (batch, per-request KV load of one GPU-layer, measured seconds)
     for tp in (2, 4, 8):
         row = {}
         modes = ["sha", "nodp", "dp"] + (["dp-free"] if tp == 8 else [])
@@ -439,6 +440,9 @@ def emulate_tp(args, budgets, dev):
             t = np.median(np.stack(span), axis=0)  # [L, tp]
             step = t.max(axis=1).sum()
             loads = rank_loads(plan, budgets, GROUP)
+            for l in range(L):
+                for g in range(tp):
+                    samples.append(fk.MeasurementSample(bt, float(loads[l, g]) / bt, float(t[l, g])))
             sim = fk.simulate(prof, plan, model, fk.SimulationConfig(1, 1, tp)).throughput
             row[mode] = {"tokens_per_s": bt / step, "stack_ms": step * 1e3,
                          "busy_rate": float(t.sum() / (step * tp)),
@@ -450,10 +454,54 @@ def emulate_tp(args, budgets, dev):
             row[mode]["gain_vs_sha"] = row[mode]["tokens_per_s"] / row["sha"]["tokens_per_s"]
             row[mode]["sim_gain_vs_sha"] = row[mode]["sim_throughput"] / row["sha"]["sim_throughput"]
         results[f"tp{tp}"] = row
+    results["calibration"] = calibrate_from(samples, budgets, args, dev, base, q)
     results["note"] = ("each rank's K4+K5 shard timed alone (CUDA-graph event nodes); layer span = "
                        "max over ranks; all-gather not included (single GPU); sim = reference simulator, "
                        "pure-cache latency model")
     return results
+
+
+def calibrate_from(samples, budgets, args, dev, base, q):
+    """feed measured per-(layer, GPU) decode latencies back into
+    the reference's latency law (latency.calibrate: c0 + c1*B + c2*C + c3*B*C)
+    and let the reference's simulator predict the SHA/AHA gains from it.
+    Batch-64 samples come from the emulation above; batch 16/32 samples time
+    whole TP=1 layers (the law needs two batch sizes)."""
+    import numpy as np
+    import torch
+    import paper_2502_15804_b200 as fk
+    from paper_2502_15804_b200 import ops
+    from paper_2502_15804_b200.cache import LayerCache
+    L, bt = budgets.shape[0], budgets.shape[1]
+    extra = []
+    for sub in (16, 32):
+        for l in range(0, L, 8):
+            lens = budgets[l, :sub].reshape(-1)
+            qrow = np.array([b * HQ + h * GROUP for b in range(sub) for h in range(HKV)])
+            c = LayerCache.view(base[l].k, base[l].v, base[l].host["seg_row0"][:sub * HKV], lens, qrow,
+                                qrow, GROUP)
+            qq = q[l, :sub].contiguous()
+            oo = torch.empty_like(qq)
+            ws = ops.DecodeWorkspace(c)
+            g = capture(lambda: ops.decode_into(qq, c, ws, out_bf16=oo))
+            tt = timed(g.replay, 5) / 5
+            extra.append(fk.MeasurementSample(sub, float(lens.sum()) / sub, tt))
+    try:
+        fit = fk.calibrate(samples + extra)
+    except fk.CalibrationError as exc:
+        return {"error": str(exc)}
+    m = fit.model
+    from paper_2502_15804_b200.sharding import budgets_profile
+    prof = budgets_profile(budgets, int(budgets.mean()))
+    pred = {}
+    for tp in (2, 4, 8):
+        ch = 8 if tp == 8 else args.ch
+        c = fk.compare(prof, tp, fk.EnumerationConfig(ch, 2, True, tp), m,
+                       fk.SimulationConfig(batch=bt, decode_steps=1, tp=tp), workers=8)
+        pred[f"tp{tp}"] = {r.name: r.throughput_gain for r in c.results}
+    return {"model": {"c0": m.c0, "c1": m.c1, "c2": m.c2, "c3": m.c3}, "residual_rms_s": fit.residual_rms,
+            "samples": fit.num_samples, "predicted_gain_vs_sha": pred,
+            "note": "kv_load = retained tokens per request on one GPU-layer; DP at TP8 = equal split CH=8"}
 
 
 def prefill_compress(peaks):
