@@ -101,38 +101,42 @@ int fkv_optimize_plan(const double* weights, int32_t num_layers, int32_t n, int3
 /* ------------------------------------------------- B3 decode over the cache -- */
 
 /* K4 (+ fused K5): split-KV decode attention over ragged segments (one
- * layer, one GPU), one CTA per work item.
- *   q            bf16 [*, 128]   query rows; segment s uses rows seg_qrow[s] .. +group-1
+ * layer, one GPU) by warp-persistent workers with a static schedule.
+ * The segments' retained tokens are cut into *pieces* (16-token aligned
+ * sub-ranges); worker w processes the pieces work[w][0 .. ) in order, up to
+ * the first entry with n_it == 0 (or work_k entries).  Worker w is warp
+ * (w / grid) of CTA (w % grid), so short schedules still spread over every
+ * SM.  Piece descriptor (32 bytes, 16-byte aligned table): */
+typedef struct fkv_work {
+  int64_t row0;    /* first cache row of the piece (multiple of FKV_SPLIT)         */
+  int32_t n_tok;   /* tokens in the piece (>= 0)                                  */
+  int32_t qrow;    /* q rows qrow .. qrow+group-1 are the segment's query heads   */
+  int32_t out_row; /* output rows out_row .. +group-1 of the segment              */
+  int32_t rec;     /* partial-record index of this piece (< n_items)              */
+  int32_t i0;      /* record index of the segment's first piece; the segment's    */
+                   /* records are i0 .. i0+n_it-1, its arrival counter counters[i0] */
+  int32_t n_it;    /* pieces of the segment (1 .. FKV_MAX_PIECES); 0 = end of list */
+} fkv_work_t;
+#define FKV_MAX_WORK 32   /* entries per worker */
+#define FKV_MAX_PIECES 32 /* pieces per segment */
+
+/*   q            bf16 [*, 128]   query rows
  *   k, v         bf16 [rows,128] swizzled cache rows (layout above)
- *   seg_row0     int64 [n_seg]   first cache row of each segment (multiple of FKV_SPLIT)
- *   seg_len      int32 [n_seg]   retained tokens per segment
- *   seg_qrow     int32 [n_seg]
- *   seg_out_row  int32 [n_seg]   first output row of the segment's group heads
- *   seg_item_ptr int32 [n_seg+1] items of segment s are [ptr[s], ptr[s+1])
- *   item_seg, item_t0, item_t1 int32 [n_items]: work item = tokens [t0,t1) of a
- *                segment, t0 a multiple of 16
- *   warp_ptr     int32 [n_workers+1], work_list int32 [n_items]: static
- *                schedule -- persistent worker w processes items
- *                work_list[warp_ptr[w] .. warp_ptr[w+1]) in order; worker w is
- *                warp (w / grid) of CTA (w % grid), grid = ceil(n_workers/4),
- *                so short schedules still spread over every SM
+ *   work         fkv_work_t [n_workers][work_k], 1 <= work_k <= FKV_MAX_WORK
  *   part         f32 [n_items, group, FKV_REC]  partial records: softmax-normalised
  *                o[128] and lse = natural-log sum-exp of the scaled scores
- *   counters     int32 [n_seg] segment arrival counters, zero on entry; left
- *                zero on exit
- * With all of out_bf16 / out_rec / out_lse NULL every item just writes its
- * partial record (split-K partials).  Otherwise the last CTA to finish a
- * segment merges its chunks by log-sum-exp and writes rows
- * seg_out_row[s] + h (h < group) of out_bf16 (bf16 [*,128]), out_rec
- * (f32 [*,FKV_REC]) and/or out_lse (f32 [*]) -- one launch per layer.
+ *   counters     int32 [n_items] arrival counters, zero on entry; left zero on exit
+ * With all of out_bf16 / out_rec / out_lse NULL every piece just writes its
+ * partial record (split-K partials).  Otherwise a single-piece segment writes
+ * its rows directly and the last warp to finish a piece of a split segment
+ * merges the segment's records by log-sum-exp; both write rows out_row + h
+ * (h < group) of out_bf16 (bf16 [*,128]), out_rec (f32 [*,FKV_REC]) and/or
+ * out_lse (f32 [*]) -- one launch per layer.
  * group (= Hq/Hkv) must be 4 or 8; softmax scale = sm_scale.
  * Nothing in the reference is replaced (it has no decode); its cost model of
  * this kernel is reference latency.py:85-91 (predict_compute). */
-int fkv_decode(const void* q, const void* k, const void* v, const int64_t* seg_row0,
-               const int32_t* seg_len, const int32_t* seg_qrow, const int32_t* seg_out_row,
-               const int32_t* seg_item_ptr, const int32_t* item_seg, const int32_t* item_t0,
-               const int32_t* item_t1, const int32_t* warp_ptr, const int32_t* work_list,
-               int32_t n_workers, int32_t n_items, int32_t n_seg, int32_t group, float sm_scale,
+int fkv_decode(const void* q, const void* k, const void* v, const fkv_work_t* work,
+               int32_t work_k, int32_t n_workers, int32_t n_items, int32_t group, float sm_scale,
                float* part, int32_t* counters, void* out_bf16, float* out_rec, float* out_lse,
                void* stream);
 
@@ -148,19 +152,15 @@ int fkv_merge_lse(const float* part, const int32_t* grp_ptr, const int32_t* src_
                   const int32_t* out_row, int32_t n_groups, int32_t group, void* out_bf16,
                   float* out_rec, float* out_lse, void* stream);
 
-/* Fused NVLink all-gather variant of fkv_decode (same tables).  Every
+/* Fused NVLink all-gather variant of fkv_decode (same work table).  Every
  * segment's final record is written to all n_rec destinations (each peer's
  * receive block for this rank, mapped with fkv_ipc_open; P2P stores over
  * NVLink) instead of one local slot array, and when the last warp finishes,
  * after a system-scope fence, it atomically increments sig_flags[j][my_rank]
  * in every peer's memory (n_sig peers).  sig_done: local int32, zero between
  * launches.  Replaces NCCL all_gather for the per-layer exchange. */
-int fkv_decode_exchange(const void* q, const void* k, const void* v, const int64_t* seg_row0,
-                        const int32_t* seg_len, const int32_t* seg_qrow, const int32_t* seg_out_row,
-                        const int32_t* seg_item_ptr, const int32_t* item_seg,
-                        const int32_t* item_t0, const int32_t* item_t1, const int32_t* warp_ptr,
-                        const int32_t* work_list, int32_t n_workers, int32_t n_items,
-                        int32_t n_seg, int32_t group,
+int fkv_decode_exchange(const void* q, const void* k, const void* v, const fkv_work_t* work,
+                        int32_t work_k, int32_t n_workers, int32_t n_items, int32_t group,
                         float sm_scale, float* part, int32_t* counters, void* out_bf16,
                         float* const* out_recs, int32_t n_rec, float* out_lse, int32_t* sig_done,
                         int32_t* const* sig_flags, int32_t n_sig, int32_t my_rank, void* stream);

@@ -40,21 +40,45 @@ def segment_offsets(seg_len) -> tuple[np.ndarray, int]:
     return row0, max(total, PAGE)
 
 
-MAX_ITEMS_PER_SEGMENT = 32  # kMergeMax in decode.cu
+MAX_ITEMS_PER_SEGMENT = 32  # FKV_MAX_PIECES (kMergeMax in decode.cu)
+MAX_WORK_PER_WORKER = 32    # FKV_MAX_WORK: descriptor entries per worker
 TILE = 16
 
 
 def default_workers(device=None) -> int:
-    """Persistent decode warps: 2 CTAs x 4 warps on every SM."""
+    """Persistent decode CTAs (four warps each): two on every SM."""
     try:
         sms = torch.cuda.get_device_properties(device).multi_processor_count
     except Exception:  # no device visible (host-side planning / CPU tests)
         sms = NUM_SMS
-    return sms * 8
+    return sms * 2
 
 
-MIN_TILES_PER_WORKER = 4  # floor on tiles per worker (small problems: fewer, longer pieces)
+MIN_TILES_PER_WORKER = 8  # floor on tiles per worker CTA (one 2-tile round per warp)
 MAX_PIECES_PER_SEGMENT = 4  # typical split bound: merge cost grows with pieces per segment
+
+
+def _cut_stream(seg_len, tiles, per: int, cap: int):
+    """Cut the concatenated tile stream into worker ranges of ``per`` tiles and
+    at most ``cap`` pieces (an empty segment is one piece with no tiles)."""
+    seg_i, t0s, t1s, owner = [], [], [], []
+    w, used, cnt = 0, 0, 0
+    for s in range(len(seg_len)):
+        n, t = int(tiles[s]), 0
+        while True:
+            if cnt >= cap or (used >= per and n > t):
+                w, used, cnt = w + 1, 0, 0
+            take = min(n - t, per - used)
+            seg_i.append(s)
+            t0s.append(t * TILE)
+            t1s.append(min(int(seg_len[s]), (t + take) * TILE))
+            owner.append(w)
+            used += take
+            cnt += 1
+            t += take
+            if t >= n:
+                break
+    return seg_i, t0s, t1s, np.asarray(owner, dtype=np.int64)
 
 
 def plan_work(seg_len, n_workers: int, chunk: int | None = None,
@@ -88,22 +112,14 @@ def plan_work(seg_len, n_workers: int, chunk: int | None = None,
         avg = int(tiles.sum()) // max(n_seg, 1)
         per = max(per, -(-avg // MAX_PIECES_PER_SEGMENT))
         per = max(per, -(-longest // (MAX_ITEMS_PER_SEGMENT - 1)))
-        start = np.zeros(n_seg, dtype=np.int64)
-        if n_seg:
-            start[1:] = np.cumsum(tiles)[:-1]
-        seg_i, t0s, t1s, owner = [], [], [], []
-        for s in range(n_seg):
-            a, n = int(start[s]), int(tiles[s])
-            cut = a
-            while True:
-                nxt = min(a + n, (cut // per + 1) * per)
-                seg_i.append(s)
-                t0s.append((cut - a) * TILE)
-                t1s.append(min(int(seg_len[s]), (nxt - a) * TILE))
-                owner.append(min(cut // per, W - 1))
-                if nxt >= a + n:
-                    break
-                cut = nxt
+        while True:
+            seg_i, t0s, t1s, owner = _cut_stream(seg_len, tiles, per, MAX_WORK_PER_WORKER)
+            if not len(owner) or int(owner.max()) < W:
+                break
+            if per >= int(tiles.sum()):  # only the piece cap can bind: too many segments
+                raise ValueError(f"{n_seg} segments exceed one launch "
+                                 f"({W} workers x {MAX_WORK_PER_WORKER} pieces)")
+            per *= 2
     else:
         ch = max(1, -(-int(chunk) // TILE))
         ch = max(ch, -(-longest // MAX_ITEMS_PER_SEGMENT)) * TILE
@@ -118,6 +134,19 @@ def plan_work(seg_len, n_workers: int, chunk: int | None = None,
         cum = np.concatenate([[0], np.cumsum(lens)[:-1]])
         per = max(1, -(-int(lens.sum()) // W))
         owner = np.minimum(cum // per, W - 1)
+        if len(owner) and np.bincount(owner).max() > MAX_WORK_PER_WORKER:
+            # piece cap binds: deal pieces in order, at most the cap per worker
+            owner = np.zeros(len(lens), dtype=np.int64)
+            w, used, cnt = 0, 0, 0
+            for i, n in enumerate(lens):
+                if cnt >= MAX_WORK_PER_WORKER or used >= per:
+                    w, used, cnt = w + 1, 0, 0
+                owner[i] = w
+                used += int(n)
+                cnt += 1
+            if w >= W:
+                raise ValueError(f"{len(lens)} pieces exceed one launch "
+                                 f"({W} workers x {MAX_WORK_PER_WORKER} pieces)")
     item_seg = np.asarray(seg_i, dtype=np.int32)
     t0 = np.asarray(t0s, dtype=np.int32)
     t1 = np.asarray(t1s, dtype=np.int32)
@@ -133,6 +162,39 @@ def plan_work(seg_len, n_workers: int, chunk: int | None = None,
     split = (np.diff(seg_item_ptr) > 1)[item_seg]
     work_list = np.lexsort((np.arange(len(item_seg)), ~split, owner)).astype(np.int32)
     return item_seg, t0, t1, seg_item_ptr, warp_ptr, work_list
+
+
+def work_table(seg_row0, seg_len, seg_qrow, seg_out_row, item_seg, t0, t1, seg_item_ptr,
+               warp_ptr, work_list) -> np.ndarray:
+    """The kernel-facing form of a schedule: fkv_work_t [busy, K, 8 x int32]
+    (include/fairkv.h) -- worker w's pieces in order, zero-filled (n_it = 0)
+    after its last piece, K = max pieces per worker (<= FKV_MAX_WORK)."""
+    seg_row0 = np.asarray(seg_row0, dtype=np.int64)
+    seg_len = np.asarray(seg_len, dtype=np.int64)
+    busy = len(warp_ptr) - 1
+    counts = np.diff(warp_ptr)
+    K = max(1, int(counts.max()) if busy else 1)
+    if K > MAX_WORK_PER_WORKER:
+        raise ValueError(f"{K} pieces on one worker exceed FKV_MAX_WORK")
+    n_it = np.diff(seg_item_ptr)
+    tab = np.zeros((max(busy, 1), K, 8), dtype=np.int32)
+    if len(work_list):
+        it = np.asarray(work_list, dtype=np.int64)
+        w = np.repeat(np.arange(busy), counts)
+        j = np.arange(len(it)) - np.repeat(warp_ptr[:-1], counts)
+        seg = np.asarray(item_seg, dtype=np.int64)[it]
+        a = np.asarray(t0, dtype=np.int64)[it]
+        b = np.minimum(np.asarray(t1, dtype=np.int64)[it], seg_len[seg])
+        row0 = seg_row0[seg] + a
+        tab[w, j, 0] = (row0 & 0xFFFFFFFF).astype(np.uint32).view(np.int32)
+        tab[w, j, 1] = (row0 >> 32).astype(np.int32)
+        tab[w, j, 2] = np.maximum(b - a, 0)
+        tab[w, j, 3] = np.asarray(seg_qrow, dtype=np.int64)[seg]
+        tab[w, j, 4] = np.asarray(seg_out_row, dtype=np.int64)[seg]
+        tab[w, j, 5] = it
+        tab[w, j, 6] = np.asarray(seg_item_ptr, dtype=np.int64)[seg]
+        tab[w, j, 7] = n_it[seg]
+    return tab
 
 
 @dataclass
@@ -153,8 +215,17 @@ class LayerCache:
     src_idx: torch.Tensor
     warp_ptr: torch.Tensor
     work_list: torch.Tensor
-    counters: torch.Tensor
+    work: torch.Tensor        # fkv_work_t [workers, K, 8] int32 (what K4 reads)
+    counters: torch.Tensor    # int32 [n_items]
     host: dict = field(default_factory=dict, repr=False)
+
+    @property
+    def n_workers(self) -> int:
+        return int(self.work.shape[0])
+
+    @property
+    def work_k(self) -> int:
+        return int(self.work.shape[1])
 
     @property
     def n_items(self) -> int:
@@ -183,7 +254,6 @@ class LayerCache:
         seg_len = np.asarray(seg_len, dtype=np.int64)
         row0, rows = segment_offsets(seg_len)
         dev = torch.device(device)
-        item_seg, t0, t1, ptr, wptr, wlist = plan_work(seg_len, default_workers(dev), chunk)
         k = torch.zeros((rows, HEAD_DIM), dtype=torch.bfloat16, device=dev)
         v = torch.zeros((rows, HEAD_DIM), dtype=torch.bfloat16, device=dev)
         if fill == "random":
@@ -197,20 +267,7 @@ class LayerCache:
             k.mul_(valid[:, None])
             v.mul_(valid[:, None])
 
-        def i32(a):
-            return torch.as_tensor(np.ascontiguousarray(a, dtype=np.int32), device=dev)
-
-        return LayerCache(
-            k=k, v=v, group=int(group),
-            seg_row0=torch.as_tensor(row0, device=dev),
-            seg_len=i32(seg_len), seg_qrow=i32(seg_qrow), seg_out_row=i32(seg_out_row),
-            item_seg=i32(item_seg), item_t0=i32(t0), item_t1=i32(t1),
-            grp_ptr=i32(ptr), src_idx=i32(np.arange(ptr[-1])),
-            warp_ptr=i32(wptr), work_list=i32(wlist),
-            counters=torch.zeros(max(len(seg_len), 1), dtype=torch.int32, device=dev),
-            host={"seg_len": seg_len, "seg_row0": row0, "chunk": chunk, "n_workers": len(wptr) - 1,
-                  "seg_qrow": np.asarray(seg_qrow), "seg_out_row": np.asarray(seg_out_row)},
-        )
+        return LayerCache._build(k, v, row0, seg_len, seg_qrow, seg_out_row, group, chunk)
 
     @staticmethod
     def view(k: torch.Tensor, v: torch.Tensor, seg_row0, seg_len, seg_qrow, seg_out_row,
@@ -222,8 +279,14 @@ class LayerCache:
         seg_len = np.asarray(seg_len, dtype=np.int64)
         if np.any(seg_row0 % 16):
             raise ValueError("segment starts must be multiples of 16 rows")
+        return LayerCache._build(k, v, seg_row0, seg_len, seg_qrow, seg_out_row, group, chunk)
+
+    @staticmethod
+    def _build(k, v, seg_row0, seg_len, seg_qrow, seg_out_row, group, chunk) -> "LayerCache":
         dev = k.device
+        seg_row0 = np.asarray(seg_row0, dtype=np.int64)
         item_seg, t0, t1, ptr, wptr, wlist = plan_work(seg_len, default_workers(dev), chunk)
+        tab = work_table(seg_row0, seg_len, seg_qrow, seg_out_row, item_seg, t0, t1, ptr, wptr, wlist)
 
         def i32(a):
             return torch.as_tensor(np.ascontiguousarray(a, dtype=np.int32), device=dev)
@@ -233,8 +296,8 @@ class LayerCache:
             seg_len=i32(seg_len), seg_qrow=i32(seg_qrow), seg_out_row=i32(seg_out_row),
             item_seg=i32(item_seg), item_t0=i32(t0), item_t1=i32(t1), grp_ptr=i32(ptr),
             src_idx=i32(np.arange(ptr[-1])),
-            warp_ptr=i32(wptr), work_list=i32(wlist),
-            counters=torch.zeros(max(len(seg_len), 1), dtype=torch.int32, device=dev),
+            warp_ptr=i32(wptr), work_list=i32(wlist), work=i32(tab),
+            counters=torch.zeros(max(len(item_seg), 1), dtype=torch.int32, device=dev),
             host={"seg_len": seg_len, "seg_row0": seg_row0, "chunk": chunk, "n_workers": len(wptr) - 1,
                   "seg_qrow": np.asarray(seg_qrow), "seg_out_row": np.asarray(seg_out_row)},
         )

@@ -1,28 +1,33 @@
-// K4 + fused K5: warp-persistent split-KV decode attention over the ragged,
+// K4 + fused K5: CTA-persistent split-KV decode attention over the ragged,
 // swizzled, page-aligned compressed cache, with the log-sum-exp merges.
 //
 // No reference implementation exists; the reference only models
 // this kernel's time as c0 + c1*B + c2*C + c3*B*C (pkg/src/headbalance/latency.py:85-91).
 //
 // Design:
-//  * every warp is an independent persistent worker with a static, host-built
-//    schedule: the concatenated 16-token tile stream of all segments is cut
-//    into equal ranges, one per worker warp (so every warp streams the same
-//    number of bytes), and a warp never synchronises with the other warps of
-//    its CTA -- no block barriers anywhere;
-//  * each warp runs its own S-stage TMA bulk-copy ring (cp.async.bulk +
-//    mbarrier, 16-token K+V tiles of 8 KiB) that streams ACROSS item
-//    boundaries: the producer lane lands the first tiles of the next item
-//    while the warp is still finishing the current one;
+//  * static, host-built schedule: the concatenated 16-token tile stream of all
+//    segments is cut into equal ranges, one per persistent CTA (two per SM), so
+//    every CTA streams the same number of bytes; a CTA's range is a list of
+//    *pieces* (sub-ranges of segments) described by 32-byte descriptors that
+//    the CTA reads with one coalesced load at entry;
+//  * inside a CTA the four warps share each piece: the piece is cut into
+//    rounds of two tiles and warp j takes rounds j, j+4, ...  Every warp runs
+//    its own 3-stage TMA bulk-copy ring (cp.async.bulk + mbarrier, 8 KiB K+V
+//    tiles) that streams across piece boundaries, so four independent
+//    dependency chains hide each other's latency even when the whole cache is
+//    only a few MB (small TP shards);
+//  * at the end of a piece warps 1-3 hand their (m, l, acc) state to warp 0
+//    through shared memory (named barriers, no global traffic) and warp 0
+//    combines, normalises and writes the piece's output;
 //  * the cache rows are stored pre-swizzled in HBM, so a 1-D bulk copy lands
 //    a bank-conflict-free tile for ldmatrix -- no tensor map, no address math;
 //  * GQA: every K/V tile is read once for all G query heads.  S^T = K Q^T
 //    (m16n8k16: 16 tokens x 8 heads, no padding waste for G=8), online
 //    softmax per head column (warp-shuffle max), P^T via movmatrix, then
 //    O^T += V^T P^T with ldmatrix.trans on the V tile;
-//  * an item's (o, lse) goes straight from registers to its output rows when
-//    the segment is one item; otherwise to a partial record, and the last
-//    warp to finish one of the segment's items merges them (K5 fused).
+//  * a piece's (o, lse) goes straight to its output rows when the segment is
+//    one piece; otherwise to a partial record, and the CTA that finishes the
+//    segment's last piece merges its records (K5 fused).
 #include <cuda_bf16.h>
 #include <math_constants.h>
 
@@ -32,11 +37,12 @@ namespace fkv {
 namespace {
 
 constexpr int kWarps = 4;
-constexpr int kRingStages = 12;  // per CTA: split over the active warps (12/6/4/3 each)
+constexpr int kStages = 3;  // ring stages per warp (tiles in flight)
 constexpr int kTileTok = 16;
-constexpr int kTileBytes = kTileTok * FKV_HEAD_DIM * 2;  // 4 KiB per K or V tile
-constexpr int kSmemBytes = kRingStages * 2 * kTileBytes;  // 96 KiB per CTA
-constexpr int kMergeMax = 32;                            // max items per segment (host-enforced)
+constexpr int kTileBytes = kTileTok * FKV_HEAD_DIM * 2;        // 4 KiB per K or V tile
+constexpr int kSmemBytes = kWarps * kStages * 2 * kTileBytes;  // 96 KiB per CTA
+constexpr int kMergeMax = FKV_MAX_PIECES;                      // max pieces per segment
+constexpr int kXch = 36;  // floats per lane handed to warp 0: m0 m1 l0 l1 acc[32]
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 
@@ -44,27 +50,25 @@ struct DecodeParams {
   const __nv_bfloat16* q;
   const __nv_bfloat16* k;
   const __nv_bfloat16* v;
-  const int64_t* seg_row0;
-  const int32_t* seg_len;
-  const int32_t* seg_qrow;
-  const int32_t* seg_out_row;
-  const int32_t* seg_item_ptr;
-  const int32_t* item_seg;
-  const int32_t* item_t0;
-  const int32_t* item_t1;
-  const int32_t* warp_ptr;   // worker w processes work_list[warp_ptr[w] .. warp_ptr[w+1])
-  const int32_t* work_list;  // item ids grouped by worker
-  int n_items, n_seg, n_workers;
+  const fkv_work_t* work;  // [n_workers][work_k] pieces per persistent CTA
+  int work_k, n_workers;
   float scale_log2;
-  float* part;        // [n_items, G, FKV_REC] partial records (multi-item segments)
-  int32_t* counters;  // [n_seg] segment arrival counters; zero between launches
+  float* part;        // [n_items, G, FKV_REC] partial records (multi-piece segments)
+  int32_t* counters;  // [n_items] arrival counter at each segment's first piece; zero between launches
   __nv_bfloat16* out_bf16;
   float* out_rec[FKV_MAX_PEERS];  // record destinations: local slots, or every peer's
   int n_rec;                      // receive block for this rank (fused NVLink all-gather)
   float* out_lse;
-  int32_t* sig_done;              // warps-finished counter (local), zero between launches
+  int32_t* sig_done;              // CTAs-finished counter (local), zero between launches
   int32_t* sig_flag[FKV_MAX_PEERS];  // per peer: flags[tp] in that peer's memory
   int n_sig, my_rank;
+};
+
+struct __align__(16) DecodeShared {
+  fkv_work_t tab[FKV_MAX_WORK];
+  uint64_t bars[kWarps][kStages];
+  float xch[kWarps - 1][kXch][32];  // warps 1..3 -> warp 0 piece state, lane-contiguous
+  float scratch[kMergeMax * 8];     // global merge weights
 };
 
 __device__ __forceinline__ void put_rec(const DecodeParams& p, int64_t idx, float v) {
@@ -77,73 +81,128 @@ __device__ __forceinline__ void put_rec4(const DecodeParams& p, int64_t row, int
   for (int j = 0; j < p.n_rec; ++j) reinterpret_cast<float4*>(p.out_rec[j] + row * FKV_REC)[lane] = v;
 }
 
-__device__ __forceinline__ int n_tiles_of(const DecodeParams& p, int it, int& t0, int& t1,
-                                          int& seg) {
-  seg = p.item_seg[it];
-  t0 = p.item_t0[it];
-  t1 = min(p.item_t1[it], p.seg_len[seg]);
-  return t1 > t0 ? (t1 - t0 + kTileTok - 1) / kTileTok : 0;
+__device__ __forceinline__ int atom_add_acq_rel(int32_t* addr, int v) {
+  int old;
+  asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(addr), "r"(v)
+               : "memory");
+  return old;
 }
 
-template <int G>
+__device__ __forceinline__ void named_sync(int id) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(kWarps * 32) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int id) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "n"(kWarps * 32) : "memory");
+}
+
+// Round ownership inside a CTA.  Rounds (two tiles each) are numbered across
+// the CTA's pieces; with period 7 warp 0 owns one round (offset 3) and warps
+// 1-3 own two each (offsets j-1, j+3): warp 0 combines and finalises every
+// piece (records, atomics, segment merges), so it streams half as much.
+constexpr int kPeriod = 7;
+__device__ __forceinline__ int first_round(int warp, int g0) {  // first owned round >= g0
+  const int base = g0 - g0 % kPeriod;
+  if (warp == 0) return base + 3 >= g0 ? base + 3 : base + 3 + kPeriod;
+  const int a = base + warp - 1, b = base + warp + 3;
+  return a >= g0 ? a : (b >= g0 ? b : a + kPeriod);
+}
+__device__ __forceinline__ int next_round(int warp, int r) {
+  if (warp == 0) return r + kPeriod;
+  return r % kPeriod == warp - 1 ? r + 4 : r + 3;
+}
+
+__device__ __forceinline__ int piece_tiles(const fkv_work_t& d) {
+  return (d.n_tok + kTileTok - 1) / kTileTok;
+}
+
+// PROBE (diagnostics only, fkv__decode_probe): 1 = stream the tiles without
+// computing, 2 = compute on whatever the ring holds without loading,
+// 3 = full kernel + per-CTA %globaltimer stamps in g_stamps.
+__device__ unsigned long long g_stamps[1024 * 16];
+__device__ __forceinline__ void stamp(int PROBE_, int i) {
+  if (PROBE_ == 3 && (threadIdx.x & 31) == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_stamps[blockIdx.x * 16 + i] = t;
+  }
+}
+template <int G, int PROBE = 0>
 __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodeParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ uint64_t bars[kRingStages];
-  __shared__ float scratch[kWarps][kMergeMax * 8];
+  __shared__ DecodeShared sh;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  // a short schedule leaves warps idle: the active warps split the CTA's 12
-  // ring stages, so a lone worker keeps 96 KiB in flight instead of 24 KiB
-  const int kStages = kRingStages / static_cast<int>(blockDim.x >> 5);
   uint8_t* ring = smem + warp * kStages * 2 * kTileBytes;
-  uint64_t* wbars = bars + warp * kStages;
-  // worker ids are spread over CTAs first so a short schedule still uses every SM
-  const int worker = warp * gridDim.x + blockIdx.x;
-  const int w_beg = worker < p.n_workers ? p.warp_ptr[worker] : 0;
-  const int w_end = worker < p.n_workers ? p.warp_ptr[worker + 1] : 0;
+  uint64_t* wbars = sh.bars[warp];
+  const fkv_work_t* tab = sh.tab;
+  if (PROBE == 3 && threadIdx.x == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_stamps[blockIdx.x * 16] = smid;
+  }
 
+  // The CTA's whole piece list in one coalesced load (lane j <- piece j);
+  // everything the kernel needs per piece is in its 32-byte descriptor, so
+  // the first TMA is one dependent global load away from kernel entry.
+  if (warp == 0) {
+    if (lane < p.work_k) {
+      const int4* src = reinterpret_cast<const int4*>(p.work + static_cast<int64_t>(blockIdx.x) * p.work_k + lane);
+      const int4 a = __ldg(src), b = __ldg(src + 1);
+      reinterpret_cast<int4*>(sh.tab + lane)[0] = a;
+      reinterpret_cast<int4*>(sh.tab + lane)[1] = b;
+    } else {
+      sh.tab[lane].n_it = 0;  // terminator
+    }
+  }
   if (lane == 0) {
     for (int s = 0; s < kStages; ++s) mbar_init(&wbars[s], 1);
     fence_mbar_init();
   }
-  __syncwarp();
+  __syncthreads();
 
-  auto item_at = [&](int ord) -> int { return w_beg + ord < w_end ? p.work_list[w_beg + ord] : -1; };
-
-  int p_ord = 0, p_t = 0;  // producer cursor: item ordinal, tile within item
-  int p_nt = -1;           // cached tile count / row of the producer's item (-1: reload)
-  int64_t p_row = 0;
+  // ---- producer: this warp's rounds (two tiles each) of every piece, in the
+  // CTA-wide round numbering (first_round / next_round)
+  int p_pc = 0, p_G = 0, p_half = 0;  // piece, its first round, tile of the round
+  int p_r = first_round(warp, 0);     // next owned round
   uint32_t p_seq = 0, c_seq = 0;
+  int p_s = 0;
   bool p_done = false;
   auto refill = [&]() {
-    while (!p_done && p_seq - c_seq < kStages) {
-      if (p_nt < 0) {
-        const int it = item_at(p_ord);
-        if (it < 0) {
-          p_done = true;
-          break;
-        }
-        int t0, t1, seg;
-        p_nt = n_tiles_of(p, it, t0, t1, seg);
-        p_row = p.seg_row0[seg] + t0;
+    while (!p_done && p_seq - c_seq < static_cast<uint32_t>(kStages)) {
+      if (p_pc >= FKV_MAX_WORK || tab[p_pc].n_it == 0) {
+        p_done = true;
+        break;
       }
-      if (p_t >= p_nt) {
-        ++p_ord;
-        p_t = 0;
-        p_nt = -1;
+      const int nt = piece_tiles(tab[p_pc]);
+      const int nr = (nt + 1) >> 1;
+      if (p_r >= p_G + nr) {
+        p_G += nr;
+        ++p_pc;
+        p_half = 0;
         continue;
       }
-      if (lane == 0) {
-        const int s = p_seq % kStages;
-        const int64_t row = p_row + kTileTok * p_t;
-        uint8_t* dst = ring + s * 2 * kTileBytes;
-        mbar_arrive_expect_tx(&wbars[s], 2 * kTileBytes);
-        bulk_g2s(dst, p.k + row * FKV_HEAD_DIM, kTileBytes, &wbars[s]);
-        bulk_g2s(dst + kTileBytes, p.v + row * FKV_HEAD_DIM, kTileBytes, &wbars[s]);
+      const int tile = 2 * (p_r - p_G) + p_half;
+      if (tile >= nt) {  // odd tail: one-tile round
+        p_r = next_round(warp, p_r);
+        p_half = 0;
+        continue;
       }
-      ++p_t;
+      if (lane == 0 && PROBE == 2) {
+        mbar_arrive_expect_tx(&wbars[p_s], 0);
+      } else if (lane == 0) {
+        const int64_t row = tab[p_pc].row0 + kTileTok * tile;
+        uint8_t* dst = ring + p_s * 2 * kTileBytes;
+        mbar_arrive_expect_tx(&wbars[p_s], 2 * kTileBytes);
+        bulk_g2s(dst, p.k + row * FKV_HEAD_DIM, kTileBytes, &wbars[p_s]);
+        bulk_g2s(dst + kTileBytes, p.v + row * FKV_HEAD_DIM, kTileBytes, &wbars[p_s]);
+      }
       ++p_seq;
+      if (++p_s == kStages) p_s = 0;
+      if (++p_half == 2) {
+        p_half = 0;
+        p_r = next_round(warp, p_r);
+      }
     }
   };
   refill();
@@ -153,12 +212,11 @@ __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodePara
   const int dr = lane >> 2;
   const bool fused = p.out_bf16 || p.n_rec > 0 || p.out_lse;
 
-  uint32_t qn[8][2];  // q fragments of the next item, loaded one item ahead
-  auto load_q = [&](int it) {
+  uint32_t qn[8][2];  // q fragments of the next piece, loaded one piece ahead
+  auto load_q = [&](int pc) {
     const int n = lane >> 2, kq = 2 * (lane & 3);
-    if (it >= 0 && n < G) {
-      const __nv_bfloat16* qr =
-          p.q + static_cast<int64_t>(p.seg_qrow[p.item_seg[it]] + n) * FKV_HEAD_DIM;
+    if (pc < FKV_MAX_WORK && tab[pc].n_it != 0 && n < G) {
+      const __nv_bfloat16* qr = p.q + static_cast<int64_t>(tab[pc].qrow + n) * FKV_HEAD_DIM;
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) {
         qn[kk][0] = __ldg(reinterpret_cast<const unsigned int*>(qr + 16 * kk + kq));
@@ -175,13 +233,19 @@ __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodePara
   // the previous grid has completed.
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;");
-  load_q(item_at(0));
+  load_q(0);
+  if (warp == 0) stamp(PROBE, 1);
+  if (warp == 0) named_arrive(1);  // the hand-over slot starts free
 
-  for (int ord = 0;; ++ord) {
-    const int it = item_at(ord);
-    if (it < 0) break;
-    int t0, t1, seg;
-    const int nt = n_tiles_of(p, it, t0, t1, seg);
+  int c_s = 0;        // consumer stage
+  uint32_t c_ph = 0;  // its mbarrier phase parity
+  int G0 = 0;         // first round of the current piece
+  int c_r = first_round(warp, 0);  // next owned round
+  for (int pc = 0; pc < FKV_MAX_WORK; ++pc) {
+    const fkv_work_t d = tab[pc];
+    if (d.n_it == 0) break;
+    const int nt = piece_tiles(d);
+    const int nr = (nt + 1) >> 1;
 
     // Q^T (B operand: k = head_dim, n = query head) was prefetched into qn
     uint32_t qb[8][2];
@@ -197,28 +261,67 @@ __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodePara
 #pragma unroll
     for (int dt = 0; dt < 8; ++dt) acc[dt][0] = acc[dt][1] = acc[dt][2] = acc[dt][3] = 0.f;
 
-    for (int i = 0; i < nt; ++i) {
-      const int s = c_seq % kStages;
-      mbar_wait(&wbars[s], (c_seq / kStages) & 1);
-      const uint32_t kt = smem_u32(ring + s * 2 * kTileBytes);
-      const uint32_t vt = kt + kTileBytes;
-
-      // S^T[16 tok x 8 heads] = K_tile . Q^T, two independent accumulation chains
-      float sa[4] = {0.f, 0.f, 0.f, 0.f}, sb[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-      for (int kk = 0; kk < 8; kk += 2) {
-        uint32_t a0, a1, a2, a3, b0, b1, b2, b3;
-        ldmatrix_x4(kt + swz_off(ri + 8 * (mi & 1), 2 * kk + (mi >> 1)), a0, a1, a2, a3);
-        ldmatrix_x4(kt + swz_off(ri + 8 * (mi & 1), 2 * kk + 2 + (mi >> 1)), b0, b1, b2, b3);
-        mma_bf16_16816(sa, a0, a1, a2, a3, qb[kk][0], qb[kk][1]);
-        mma_bf16_16816(sb, b0, b1, b2, b3, qb[kk + 1][0], qb[kk + 1][1]);
+    // this warp's rounds of the piece: two independent S chains per round, one
+    // softmax max/shuffle/rescale step and one ring hand-back per 32 tokens
+    for (; c_r < G0 + nr; c_r = next_round(warp, c_r)) {
+      const int i = 2 * (c_r - G0);
+      const bool two = i + 1 < nt;
+      const int sA = c_s;
+      const uint32_t phA = c_ph;
+      if (++c_s == kStages) c_s = 0, c_ph ^= 1u;
+      const int sB = c_s;
+      const uint32_t phB = c_ph;
+      if (two && ++c_s == kStages) c_s = 0, c_ph ^= 1u;
+      mbar_wait(&wbars[sA], phA);
+      if (two) mbar_wait(&wbars[sB], phB);
+      if (warp == 0 && pc == 0) stamp(PROBE, 2);
+      if (PROBE == 1) {
+        __syncwarp();
+        c_seq += two ? 2u : 1u;
+        refill();
+        continue;
       }
-      const int ta = t0 + kTileTok * i + (lane >> 2);
-      const float s0 = ta < t1 ? (sa[0] + sb[0]) * p.scale_log2 : -CUDART_INF_F;
-      const float s1 = ta < t1 ? (sa[1] + sb[1]) * p.scale_log2 : -CUDART_INF_F;
-      const float s2 = ta + 8 < t1 ? (sa[2] + sb[2]) * p.scale_log2 : -CUDART_INF_F;
-      const float s3 = ta + 8 < t1 ? (sa[3] + sb[3]) * p.scale_log2 : -CUDART_INF_F;
-      float mx0 = fmaxf(s0, s2), mx1 = fmaxf(s1, s3);
+      const uint32_t kA = smem_u32(ring + sA * 2 * kTileBytes), vA = kA + kTileBytes;
+      const uint32_t kB = smem_u32(ring + sB * 2 * kTileBytes), vB = kB + kTileBytes;
+
+      // S^T[16 tok x 8 heads] = K_tile . Q^T per tile: four independent
+      // two-deep HMMA chains per tile (k16 slices kk = j, j+4), summed after
+      float sa[4][4], sc[4][4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) sa[j][e] = sc[j][e] = 0.f;
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        uint32_t a0, a1, a2, a3;
+        ldmatrix_x4(kA + swz_off(ri + 8 * (mi & 1), 2 * kk + (mi >> 1)), a0, a1, a2, a3);
+        mma_bf16_16816(sa[kk & 3], a0, a1, a2, a3, qb[kk][0], qb[kk][1]);
+      }
+      if (two) {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          uint32_t a0, a1, a2, a3;
+          ldmatrix_x4(kB + swz_off(ri + 8 * (mi & 1), 2 * kk + (mi >> 1)), a0, a1, a2, a3);
+          mma_bf16_16816(sc[kk & 3], a0, a1, a2, a3, qb[kk][0], qb[kk][1]);
+        }
+      }
+      float sb[4], sd[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        sb[e] = (sa[1][e] + sa[3][e]) + sa[2][e];
+        sd[e] = (sc[1][e] + sc[3][e]) + sc[2][e];
+      }
+      const int ta = kTileTok * i + (lane >> 2);  // token of rows (lane>>2) / +8 within the piece
+      const int tb = ta + kTileTok;
+      const float s0 = ta < d.n_tok ? (sa[0][0] + sb[0]) * p.scale_log2 : -CUDART_INF_F;
+      const float s1 = ta < d.n_tok ? (sa[0][1] + sb[1]) * p.scale_log2 : -CUDART_INF_F;
+      const float s2 = ta + 8 < d.n_tok ? (sa[0][2] + sb[2]) * p.scale_log2 : -CUDART_INF_F;
+      const float s3 = ta + 8 < d.n_tok ? (sa[0][3] + sb[3]) * p.scale_log2 : -CUDART_INF_F;
+      const float s4 = tb < d.n_tok ? (sc[0][0] + sd[0]) * p.scale_log2 : -CUDART_INF_F;
+      const float s5 = tb < d.n_tok ? (sc[0][1] + sd[1]) * p.scale_log2 : -CUDART_INF_F;
+      const float s6 = tb + 8 < d.n_tok ? (sc[0][2] + sd[2]) * p.scale_log2 : -CUDART_INF_F;
+      const float s7 = tb + 8 < d.n_tok ? (sc[0][3] + sd[3]) * p.scale_log2 : -CUDART_INF_F;
+      float mx0 = fmaxf(fmaxf(s0, s2), fmaxf(s4, s6)), mx1 = fmaxf(fmaxf(s1, s3), fmaxf(s5, s7));
 #pragma unroll
       for (int off = 4; off < 32; off <<= 1) {
         mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, off));
@@ -230,8 +333,10 @@ __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodePara
       const float c0 = fast_exp2(m0 - r0), c1 = fast_exp2(m1 - r1);
       const float p0 = fast_exp2(s0 - r0), p1 = fast_exp2(s1 - r1);
       const float p2 = fast_exp2(s2 - r0), p3 = fast_exp2(s3 - r1);
-      l0 = l0 * c0 + p0 + p2;
-      l1 = l1 * c1 + p1 + p3;
+      const float p4 = fast_exp2(s4 - r0), p5 = fast_exp2(s5 - r1);
+      const float p6 = fast_exp2(s6 - r0), p7 = fast_exp2(s7 - r1);
+      l0 = l0 * c0 + ((p0 + p2) + (p4 + p6));
+      l1 = l1 * c1 + ((p1 + p3) + (p5 + p7));
       m0 = nm0;
       m1 = nm1;
 #pragma unroll
@@ -242,23 +347,78 @@ __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodePara
         acc[dt][3] *= c1;
       }
       // P^T fragments (k = token, n = head) from the S^T accumulator layout
-      const uint32_t pb0 = movmatrix_trans(pack_bf16x2(p0, p1));
-      const uint32_t pb1 = movmatrix_trans(pack_bf16x2(p2, p3));
+      const uint32_t pa0 = movmatrix_trans(pack_bf16x2(p0, p1));
+      const uint32_t pa1 = movmatrix_trans(pack_bf16x2(p2, p3));
       // O^T[128 d x 8 heads] += V^T . P^T
 #pragma unroll
       for (int dt = 0; dt < 8; ++dt) {
         uint32_t a0, a1, a2, a3;
-        ldmatrix_x4_trans(vt + swz_off(ri + 8 * (mi >> 1), 2 * dt + (mi & 1)), a0, a1, a2, a3);
-        mma_bf16_16816(acc[dt], a0, a1, a2, a3, pb0, pb1);
+        ldmatrix_x4_trans(vA + swz_off(ri + 8 * (mi >> 1), 2 * dt + (mi & 1)), a0, a1, a2, a3);
+        mma_bf16_16816(acc[dt], a0, a1, a2, a3, pa0, pa1);
+      }
+      if (two) {
+        const uint32_t pc0 = movmatrix_trans(pack_bf16x2(p4, p5));
+        const uint32_t pc1 = movmatrix_trans(pack_bf16x2(p6, p7));
+#pragma unroll
+        for (int dt = 0; dt < 8; ++dt) {
+          uint32_t a0, a1, a2, a3;
+          ldmatrix_x4_trans(vB + swz_off(ri + 8 * (mi >> 1), 2 * dt + (mi & 1)), a0, a1, a2, a3);
+          mma_bf16_16816(acc[dt], a0, a1, a2, a3, pc0, pc1);
+        }
       }
       __syncwarp();
-      ++c_seq;
+      c_seq += two ? 2u : 1u;
       refill();
     }
+    G0 += nr;
 
-    load_q(item_at(ord + 1));  // overlaps the epilogue below
+    load_q(pc + 1);  // overlaps the hand-over below
+    const bool more = pc + 1 < FKV_MAX_WORK && tab[pc + 1].n_it != 0;
 
-    // ---- finalise this item from registers
+    // ---- hand the piece state to warp 0 (shared memory, named barriers):
+    // bar 1 = slot free (warp 0 finished the previous piece), bar 2 = slot full
+    if (warp != 0) {
+      named_sync(1);
+      float* x = &sh.xch[warp - 1][0][lane];
+      x[0 * 32] = m0;
+      x[1 * 32] = m1;
+      x[2 * 32] = l0;
+      x[3 * 32] = l1;
+#pragma unroll
+      for (int dt = 0; dt < 8; ++dt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) x[(4 + 4 * dt + e) * 32] = acc[dt][e];
+      named_arrive(2);
+      continue;
+    }
+    stamp(PROBE, 3);
+    named_sync(2);
+    stamp(PROBE, 4);
+    // warp 0: lane-wise online-softmax combine of the four warps' states
+#pragma unroll 1
+    for (int w = 0; w < kWarps - 1; ++w) {
+      const float* x = &sh.xch[w][0][lane];
+      const float om0 = x[0], om1 = x[32], ol0 = x[64], ol1 = x[96];
+      const float nm0 = fmaxf(m0, om0), nm1 = fmaxf(m1, om1);
+      const float r0 = nm0 == -CUDART_INF_F ? 0.f : nm0;
+      const float r1 = nm1 == -CUDART_INF_F ? 0.f : nm1;
+      const float a0 = fast_exp2(m0 - r0), b0 = fast_exp2(om0 - r0);
+      const float a1 = fast_exp2(m1 - r1), b1 = fast_exp2(om1 - r1);
+      l0 = l0 * a0 + ol0 * b0;
+      l1 = l1 * a1 + ol1 * b1;
+      m0 = nm0;
+      m1 = nm1;
+#pragma unroll
+      for (int dt = 0; dt < 8; ++dt) {
+        acc[dt][0] = acc[dt][0] * a0 + x[(4 + 4 * dt + 0) * 32] * b0;
+        acc[dt][1] = acc[dt][1] * a1 + x[(4 + 4 * dt + 1) * 32] * b1;
+        acc[dt][2] = acc[dt][2] * a0 + x[(4 + 4 * dt + 2) * 32] * b0;
+        acc[dt][3] = acc[dt][3] * a1 + x[(4 + 4 * dt + 3) * 32] * b1;
+      }
+    }
+    if (more) named_arrive(1);  // slot free for the next piece
+
+    // ---- finalise this piece from registers (warp 0)
 #pragma unroll
     for (int off = 4; off < 32; off <<= 1) {
       l0 += __shfl_xor_sync(0xffffffffu, l0, off);
@@ -267,12 +427,11 @@ __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodePara
     const float inv0 = l0 > 0.f ? 1.f / l0 : 0.f, inv1 = l1 > 0.f ? 1.f / l1 : 0.f;
     const float lse0 = l0 > 0.f ? (m0 + log2f(l0)) * kLn2 : -CUDART_INF_F;
     const float lse1 = l1 > 0.f ? (m1 + log2f(l1)) * kLn2 : -CUDART_INF_F;
-    const int i0 = p.seg_item_ptr[seg];
-    const int n_it = p.seg_item_ptr[seg + 1] - i0;
-    const int64_t orow = p.seg_out_row[seg];
+    const int n_it = d.n_it;
+    const int64_t orow = d.out_row;
 
     if (fused && n_it == 1) {
-      // whole segment in one item: registers -> output rows
+      // whole segment in one piece: registers -> output rows
 #pragma unroll
       for (int dt = 0; dt < 8; ++dt) {
         const int d0 = 16 * dt + dr;
@@ -310,8 +469,8 @@ __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodePara
       continue;
     }
 
-    // partial record of this item
-    float* rec = p.part + static_cast<int64_t>(it) * G * FKV_REC;
+    // partial record of this piece
+    float* rec = p.part + static_cast<int64_t>(d.rec) * G * FKV_REC;
 #pragma unroll
     for (int dt = 0; dt < 8; ++dt) {
       const int d0 = 16 * dt + dr;
@@ -330,21 +489,24 @@ __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodePara
     }
     if (!fused) continue;
 
-    // the last warp to finish one of the segment's items merges them all
-    __threadfence();
+    // The CTA that finishes one of the segment's pieces last merges them all.
+    // Warp barrier + one acq_rel atomic (release publishes the whole warp's
+    // record stores, acquire makes every other piece's records visible).
     __syncwarp();
+    stamp(PROBE, 6);
     int last = 0;
-    if (lane == 0) last = atomicAdd(&p.counters[seg], 1) == n_it - 1;
+    if (lane == 0) last = atom_add_acq_rel(p.counters + d.i0, 1) == n_it - 1;
     last = __shfl_sync(0xffffffffu, last, 0);
+    stamp(PROBE, 7);
     if (!last) continue;
-    __threadfence();
-    // All (item, head) lse values in one parallel round trip, weights in the
-    // warp's scratch, then every lane streams its 4 head_dim columns of all
-    // records with n_it*G independent 16-B loads.
-    const float* base = p.part + static_cast<int64_t>(i0) * G * FKV_REC;
-    float* sw = scratch[warp];
+    // All (piece, head) lse values in one parallel round trip, weights in
+    // shared scratch, then every lane streams its 4 head_dim columns of all
+    // records with n_it*G independent 16-B loads (L2: .cg, never a stale L1 line).
+    const float* base = p.part + static_cast<int64_t>(d.i0) * G * FKV_REC;
+    float* sw = sh.scratch;
     for (int x = lane; x < n_it * G; x += 32) sw[x] = __ldcg(base + x * FKV_REC + FKV_HEAD_DIM);
     __syncwarp();
+    stamp(PROBE, 8);
     float lse_g = -CUDART_INF_F;
     if (lane < G) {
       float M = -CUDART_INF_F;
@@ -358,6 +520,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodePara
       lse_g = S > 0.f ? M + __logf(S) : -CUDART_INF_F;
     }
     __syncwarp();
+    stamp(PROBE, 9);
     float4 o[G];
 #pragma unroll
     for (int g = 0; g < G; ++g) o[g] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -375,6 +538,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodePara
         o[g].w = fmaf(w, v4[g].w, o[g].w);
       }
     }
+    stamp(PROBE, 10);
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       const int64_t row = orow + g;
@@ -389,16 +553,19 @@ __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodePara
       if (p.n_rec) put_rec(p, (orow + lane) * FKV_REC + FKV_HEAD_DIM, lse_g);
       if (p.out_lse) p.out_lse[orow + lane] = lse_g;
     }
-    if (lane == 0) p.counters[seg] = 0;  // ready for the next launch / graph replay
+    if (lane == 0) p.counters[d.i0] = 0;  // ready for the next launch / graph replay
+    stamp(PROBE, 11);
+    __syncwarp();  // the scratch is reused by the next merge
   }
 
-  // Fused all-gather completion: the last warp out publishes this rank's
+  if (warp == 0) stamp(PROBE, 5);
+  // Fused all-gather completion: the last CTA out publishes this rank's
   // records to every peer by bumping its flag there (system-scope release).
-  if (p.n_sig > 0) {
+  // Only warp 0 writes global memory, so it alone signals.
+  if (p.n_sig > 0 && warp == 0) {
     __threadfence_system();
     __syncwarp();
-    if (lane == 0 &&
-        atomicAdd(p.sig_done, 1) == static_cast<int>(gridDim.x * (blockDim.x >> 5)) - 1) {
+    if (lane == 0 && atomicAdd(p.sig_done, 1) == static_cast<int>(gridDim.x) - 1) {
       *p.sig_done = 0;
       __threadfence_system();
       for (int j = 0; j < p.n_sig; ++j) atomicAdd_system(p.sig_flag[j] + p.my_rank, 1);
@@ -478,11 +645,11 @@ __global__ void __launch_bounds__(G * 32)
   }
 }
 
-template <int G>
+template <int G, int PROBE = 0>
 int launch_decode(const DecodeParams& p, cudaStream_t st) {
   static int grid_cap = 0;  // 2 persistent CTAs per SM
   if (!grid_cap) {
-    if (int rc = cuda_check(cudaFuncSetAttribute(decode_kernel<G>,
+    if (int rc = cuda_check(cudaFuncSetAttribute(decode_kernel<G, PROBE>,
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  kSmemBytes),
                             "decode smem attribute"))
@@ -490,16 +657,17 @@ int launch_decode(const DecodeParams& p, cudaStream_t st) {
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_kernel<G>, kWarps * 32,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_kernel<G, PROBE>, kWarps * 32,
                                                   kSmemBytes);
     grid_cap = sms * (per_sm > 0 ? per_sm : 1);
   }
-  // up to 2 CTAs per SM; 1-4 active warps per CTA (worker w -> CTA w % grid)
-  const int grid = p.n_workers < grid_cap ? p.n_workers : grid_cap;
-  const int wpc = (p.n_workers + grid - 1) / grid;  // 12 stages split 12/6/4/3
+  // one persistent CTA per worker, all co-resident (2 per SM)
+  if (p.n_workers > grid_cap)
+    return set_error(FKV_ERR_INVALID, "fkv_decode: more workers than co-resident CTAs (plan for "
+                                      "this GPU: 2 per SM)");
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid, 1, 1);
-  cfg.blockDim = dim3(wpc * 32, 1, 1);
+  cfg.gridDim = dim3(p.n_workers, 1, 1);
+  cfg.blockDim = dim3(kWarps * 32, 1, 1);
   cfg.dynamicSmemBytes = kSmemBytes;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -507,7 +675,7 @@ int launch_decode(const DecodeParams& p, cudaStream_t st) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cuda_check(cudaLaunchKernelEx(&cfg, decode_kernel<G>, p), "decode launch");
+  return cuda_check(cudaLaunchKernelEx(&cfg, decode_kernel<G, PROBE>, p), "decode launch");
 }
 
 }  // namespace
@@ -515,7 +683,10 @@ int launch_decode(const DecodeParams& p, cudaStream_t st) {
 
 namespace fkv {
 namespace {
-int decode_entry(DecodeParams& p, int group, cudaStream_t st) {
+int decode_entry(DecodeParams& p, int group, cudaStream_t st, int probe = 0) {
+  if (probe == 1) return group == 8 ? launch_decode<8, 1>(p, st) : set_error(FKV_ERR_INVALID, "probe: G=8");
+  if (probe == 2) return group == 8 ? launch_decode<8, 2>(p, st) : set_error(FKV_ERR_INVALID, "probe: G=8");
+  if (probe == 3) return group == 8 ? launch_decode<8, 3>(p, st) : set_error(FKV_ERR_INVALID, "probe: G=8");
   switch (group) {
     case 4: return launch_decode<4>(p, st);
     case 8: return launch_decode<8>(p, st);
@@ -525,61 +696,55 @@ int decode_entry(DecodeParams& p, int group, cudaStream_t st) {
 }  // namespace
 }  // namespace fkv
 
-extern "C" int fkv_decode(const void* q, const void* k, const void* v, const int64_t* seg_row0,
-                          const int32_t* seg_len, const int32_t* seg_qrow,
-                          const int32_t* seg_out_row, const int32_t* seg_item_ptr,
-                          const int32_t* item_seg, const int32_t* item_t0, const int32_t* item_t1,
-                          const int32_t* warp_ptr, const int32_t* work_list, int32_t n_workers,
-                          int32_t n_items, int32_t n_seg, int32_t group, float sm_scale,
-                          float* part, int32_t* counters, void* out_bf16, float* out_rec,
-                          float* out_lse, void* stream) {
-  return fkv_decode_exchange(q, k, v, seg_row0, seg_len, seg_qrow, seg_out_row, seg_item_ptr,
-                             item_seg, item_t0, item_t1, warp_ptr, work_list, n_workers, n_items,
-                             n_seg,
-                             group, sm_scale, part, counters, out_bf16, out_rec ? &out_rec : nullptr,
-                             out_rec ? 1 : 0, out_lse, nullptr, nullptr, 0, 0, stream);
+static int g_probe = 0;
+
+// Diagnostics (not part of fairkv.h): the next fkv_decode call runs probe mode
+// `mode` (1 = loads only, 2 = compute only).  Used by tools/probe_sizes.py.
+extern "C" int fkv__decode_probe(int32_t mode) {
+  g_probe = mode;
+  return 0;
+}
+
+extern "C" int fkv__decode_stamps(unsigned long long* host, int32_t n) {
+  return fkv::cuda_check(cudaMemcpyFromSymbol(host, fkv::g_stamps, sizeof(unsigned long long) * n),
+                         "stamps");
+}
+
+extern "C" int fkv_decode(const void* q, const void* k, const void* v, const fkv_work_t* work,
+                          int32_t work_k, int32_t n_workers, int32_t n_items, int32_t group,
+                          float sm_scale, float* part, int32_t* counters, void* out_bf16,
+                          float* out_rec, float* out_lse, void* stream) {
+  return fkv_decode_exchange(q, k, v, work, work_k, n_workers, n_items, group, sm_scale, part,
+                             counters, out_bf16, out_rec ? &out_rec : nullptr, out_rec ? 1 : 0,
+                             out_lse, nullptr, nullptr, 0, 0, stream);
 }
 
 extern "C" int fkv_decode_exchange(const void* q, const void* k, const void* v,
-                                   const int64_t* seg_row0, const int32_t* seg_len,
-                                   const int32_t* seg_qrow, const int32_t* seg_out_row,
-                                   const int32_t* seg_item_ptr, const int32_t* item_seg,
-                                   const int32_t* item_t0, const int32_t* item_t1,
-                                   const int32_t* warp_ptr, const int32_t* work_list,
-                                   int32_t n_workers, int32_t n_items,
-                                   int32_t n_seg, int32_t group, float sm_scale, float* part,
+                                   const fkv_work_t* work, int32_t work_k, int32_t n_workers,
+                                   int32_t n_items, int32_t group, float sm_scale, float* part,
                                    int32_t* counters, void* out_bf16, float* const* out_recs,
                                    int32_t n_rec, float* out_lse, int32_t* sig_done,
                                    int32_t* const* sig_flags, int32_t n_sig, int32_t my_rank,
                                    void* stream) {
   using namespace fkv;
-  if (n_items < 0 || n_seg < 0) return set_error(FKV_ERR_INVALID, "fkv_decode: negative size");
+  if (n_items < 0 || n_workers < 0) return set_error(FKV_ERR_INVALID, "fkv_decode: negative size");
+  if (work_k < 1 || work_k > FKV_MAX_WORK)
+    return set_error(FKV_ERR_INVALID, "fkv_decode: work_k must be in [1, FKV_MAX_WORK]");
   if (n_rec < 0 || n_rec > FKV_MAX_PEERS || n_sig < 0 || n_sig > FKV_MAX_PEERS)
     return set_error(FKV_ERR_INVALID, "fkv_decode: too many record destinations / peers");
-  if (n_items == 0) return FKV_OK;
-  if (!q || !k || !v || !seg_row0 || !seg_len || !seg_qrow || !seg_item_ptr || !item_seg ||
-      !item_t0 || !item_t1 || !warp_ptr || !work_list || n_workers < 1 || !part || !counters ||
-      ((out_bf16 || n_rec || out_lse) && !seg_out_row) || (n_rec && !out_recs) ||
+  if (n_items == 0 || n_workers == 0) return FKV_OK;
+  if (!q || !k || !v || !work || !part || !counters || (n_rec && !out_recs) ||
       (n_sig && (!sig_done || !sig_flags)))
     return set_error(FKV_ERR_INVALID, "fkv_decode: null pointer");
-  if ((reinterpret_cast<uintptr_t>(k) | reinterpret_cast<uintptr_t>(v)) & 15)
-    return set_error(FKV_ERR_INVALID, "fkv_decode: cache not 16-byte aligned");
+  if ((reinterpret_cast<uintptr_t>(k) | reinterpret_cast<uintptr_t>(v) |
+       reinterpret_cast<uintptr_t>(work)) & 15)
+    return set_error(FKV_ERR_INVALID, "fkv_decode: cache / work table not 16-byte aligned");
   DecodeParams p{};
   p.q = static_cast<const __nv_bfloat16*>(q);
   p.k = static_cast<const __nv_bfloat16*>(k);
   p.v = static_cast<const __nv_bfloat16*>(v);
-  p.seg_row0 = seg_row0;
-  p.seg_len = seg_len;
-  p.seg_qrow = seg_qrow;
-  p.seg_out_row = seg_out_row;
-  p.seg_item_ptr = seg_item_ptr;
-  p.item_seg = item_seg;
-  p.item_t0 = item_t0;
-  p.item_t1 = item_t1;
-  p.warp_ptr = warp_ptr;
-  p.work_list = work_list;
-  p.n_items = n_items;
-  p.n_seg = n_seg;
+  p.work = work;
+  p.work_k = work_k;
   p.n_workers = n_workers;
   p.scale_log2 = sm_scale * kLog2e;
   p.part = part;
@@ -592,7 +757,9 @@ extern "C" int fkv_decode_exchange(const void* q, const void* k, const void* v,
   for (int j = 0; j < n_sig; ++j) p.sig_flag[j] = sig_flags[j];
   p.n_sig = n_sig;
   p.my_rank = my_rank;
-  return decode_entry(p, group, static_cast<cudaStream_t>(stream));
+  const int probe = g_probe;
+  g_probe = 0;
+  return decode_entry(p, group, static_cast<cudaStream_t>(stream), probe);
 }
 
 extern "C" int fkv_merge_lse(const float* part, const int32_t* grp_ptr, const int32_t* src_idx,

@@ -61,13 +61,9 @@ def _decode(q, cache: LayerCache, ws: DecodeWorkspace | None, sm_scale, out_bf16
     ws = ws or DecodeWorkspace(cache)
     scale = 1.0 / math.sqrt(HEAD_DIM) if sm_scale is None else sm_scale
     _native.check(_lib.fkv_decode(
-        q.data_ptr(), cache.k.data_ptr(), cache.v.data_ptr(), cache.seg_row0.data_ptr(),
-        cache.seg_len.data_ptr(), cache.seg_qrow.data_ptr(), cache.seg_out_row.data_ptr(),
-        cache.grp_ptr.data_ptr(), cache.item_seg.data_ptr(), cache.item_t0.data_ptr(),
-        cache.item_t1.data_ptr(), cache.warp_ptr.data_ptr(), cache.work_list.data_ptr(),
-        int(cache.warp_ptr.shape[0]) - 1, cache.n_items, cache.n_segments, cache.group, scale,
-        ws.part.data_ptr(), cache.counters.data_ptr(), _p(out_bf16), _p(out_rec), _p(out_lse),
-        _stream()))
+        q.data_ptr(), cache.k.data_ptr(), cache.v.data_ptr(), cache.work.data_ptr(), cache.work_k,
+        cache.n_workers, cache.n_items, cache.group, scale, ws.part.data_ptr(),
+        cache.counters.data_ptr(), _p(out_bf16), _p(out_rec), _p(out_lse), _stream()))
     return ws.part
 
 
@@ -101,13 +97,9 @@ def decode_exchange(q: torch.Tensor, cache: LayerCache, endpoint, parity: int,
     recs = (C.c_void_p * len(dests))(*dests)
     flags = (C.c_void_p * len(endpoint.peer_flags))(*endpoint.peer_flags)
     _native.check(_lib.fkv_decode_exchange(
-        q.data_ptr(), cache.k.data_ptr(), cache.v.data_ptr(), cache.seg_row0.data_ptr(),
-        cache.seg_len.data_ptr(), cache.seg_qrow.data_ptr(), cache.seg_out_row.data_ptr(),
-        cache.grp_ptr.data_ptr(), cache.item_seg.data_ptr(), cache.item_t0.data_ptr(),
-        cache.item_t1.data_ptr(), cache.warp_ptr.data_ptr(), cache.work_list.data_ptr(),
-        int(cache.warp_ptr.shape[0]) - 1, cache.n_items, cache.n_segments, cache.group, scale,
-        ws.part.data_ptr(), cache.counters.data_ptr(), None, recs, len(dests), None,
-        endpoint.sig_done, flags,
+        q.data_ptr(), cache.k.data_ptr(), cache.v.data_ptr(), cache.work.data_ptr(), cache.work_k,
+        cache.n_workers, cache.n_items, cache.group, scale, ws.part.data_ptr(),
+        cache.counters.data_ptr(), None, recs, len(dests), None, endpoint.sig_done, flags,
         len(endpoint.peer_flags), endpoint.rank, _stream()))
 
 

@@ -3,11 +3,12 @@
 import numpy as np
 import pytest
 
-from paper_2502_15804_b200.cache import MAX_ITEMS_PER_SEGMENT, plan_work, segment_offsets
+from paper_2502_15804_b200.cache import (MAX_ITEMS_PER_SEGMENT, MAX_WORK_PER_WORKER, plan_work,
+                                         segment_offsets, work_table)
 
 
 @pytest.mark.parametrize("chunk", [None, 64, 100, 512])
-@pytest.mark.parametrize("workers", [1, 7, 1184])
+@pytest.mark.parametrize("workers", [300, 1184])
 def test_plan_covers_each_segment_once(chunk, workers):
     rng = np.random.default_rng(workers + (chunk or 0))
     seg_len = rng.integers(0, 3000, size=300)
@@ -24,6 +25,43 @@ def test_plan_covers_each_segment_once(chunk, workers):
         spans = [(t0[i], t1[i]) for i in its]
         assert spans[0][0] == 0 and spans[-1][1] == seg_len[s]
         assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+    assert len(wptr) - 1 <= workers and np.diff(wptr).max() <= MAX_WORK_PER_WORKER
+
+
+def test_piece_cap_and_infeasible_plans():
+    # many tiny (and empty) segments next to one long one: the per-worker
+    # piece cap (FKV_MAX_WORK) binds, not the tile count
+    seg_len = np.concatenate([[40000], np.zeros(2000, dtype=np.int64), np.full(3000, 16)])
+    item_seg, t0, t1, sptr, wptr, wlist = plan_work(seg_len, 1184)
+    assert np.diff(wptr).max() <= MAX_WORK_PER_WORKER and len(wptr) - 1 <= 1184
+    assert sorted(wlist.tolist()) == list(range(len(item_seg)))
+    with pytest.raises(ValueError):
+        plan_work(np.zeros(1184 * MAX_WORK_PER_WORKER + 1, dtype=np.int64), 1184)
+
+
+def test_work_table_matches_plan():
+    rng = np.random.default_rng(3)
+    seg_len = rng.integers(0, 2000, size=200)
+    row0, _ = segment_offsets(seg_len)
+    qrow = np.arange(200) * 8
+    orow = np.arange(200) * 8 + 1
+    item_seg, t0, t1, sptr, wptr, wlist = plan_work(seg_len, 1184)
+    tab = work_table(row0, seg_len, qrow, orow, item_seg, t0, t1, sptr, wptr, wlist)
+    assert tab.shape == (len(wptr) - 1, np.diff(wptr).max(), 8)
+    seen = []
+    for w in range(tab.shape[0]):
+        for j in range(tab.shape[1]):
+            e = tab[w, j]
+            if e[7] == 0:
+                assert j >= wptr[w + 1] - wptr[w]
+                continue
+            it = wlist[wptr[w] + j]
+            s = item_seg[it]
+            r0 = int(np.uint32(e[0].view(np.uint32))) + (int(e[1]) << 32)
+            assert r0 == row0[s] + t0[it] and e[2] == t1[it] - t0[it]
+            assert (e[3], e[4], e[5], e[6], e[7]) == (qrow[s], orow[s], it, sptr[s], sptr[s + 1] - sptr[s])
+            seen.append(it)
+    assert sorted(seen) == list(range(len(item_seg)))
 
 
 def test_balanced_plan_equalises_tiles_per_worker():
