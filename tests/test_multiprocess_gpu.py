@@ -1,0 +1,86 @@
+"""The fused NVLink all-gather across real processes: two OS processes (one
+rank each, torch.distributed over gloo for the plumbing) share the single
+GPU of this environment, map each other's receive areas with CUDA IPC
+(exchange.P2PGroup.connect) and run StackDecoder with the P2P exchange.
+Every rank's o must equal the single-GPU decode of the same layers.  This is
+the multi-process path bench.py takes at N > 1 (IPC handles, cross-process
+system-scope flags), minus NVLink itself."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank: int, tp: int, port: int, mode: str, out_dir: str):
+    import torch.distributed as dist
+    import paper_2502_15804_b200 as fk
+    from paper_2502_15804_b200 import ops
+    from paper_2502_15804_b200.cache import LayerCache
+    from paper_2502_15804_b200.decoder import StackDecoder, rank_caches
+    from paper_2502_15804_b200.exchange import P2PGroup
+    from paper_2502_15804_b200.sharding import budgets_profile, plan_layouts, synthetic_budgets
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=tp)
+    dev = torch.device("cuda:0")
+    torch.cuda.set_device(dev)
+    L, bt, hkv, G, B = 3, 4, 8, 8, 256
+    hq = hkv * G
+    budgets = synthetic_budgets(L, bt, hkv, B, seed=11)
+    prof = budgets_profile(budgets, B)
+    plan = fk.sha_plan(prof, tp) if mode == "sha" else \
+        fk.optimize_plan(prof, tp, fk.EnumerationConfig(4, 2, True, tp))
+    shards, finals = plan_layouts(plan, budgets, G)
+    qrow = np.array([b * hq + h * G for b in range(bt) for h in range(hkv)])
+    gen = torch.Generator(device=dev).manual_seed(5)  # identical base cache in every process
+    base = [LayerCache.allocate(budgets[l].reshape(-1), qrow, qrow, G, dev, fill="random", generator=gen)
+            for l in range(L)]
+    caches = rank_caches([s[rank] for s in shards], bt, hq, G, tp, dev, base=base)
+    grp = P2PGroup.connect(rank, tp, finals[0].slots, G)
+    dec = StackDecoder(caches, finals, tp=tp, bt=bt, hq=hq, group=G, exchange="p2p",
+                       endpoint=grp.endpoints[0])
+    gq = torch.Generator(device=dev).manual_seed(9)
+    q = torch.randn((L, bt, hq, 128), generator=gq, device=dev).to(torch.bfloat16)
+    o = torch.zeros_like(q)
+    for _ in range(2):  # two steps: flags / counters / parity carry over
+        dec.step(q, o)
+    torch.cuda.synchronize()
+    ref = torch.stack([ops.decode(q[l], base[l])[0] for l in range(L)])
+    err = float((o.float() - ref.float()).abs().max())
+    ok = bool(torch.allclose(o.float(), ref.float(), rtol=2e-2, atol=1e-2))
+    with open(os.path.join(out_dir, f"rank{rank}.txt"), "w") as f:
+        f.write(f"{int(ok)} {err}\n")
+    dist.barrier()
+    grp.close()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("tp,mode", [(2, "sha"), (2, "dp")])
+def test_two_process_p2p_exchange(cuda_device, tmp_path, tp, mode):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, tp, port, mode, str(tmp_path))) for r in range(tp)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=240)
+    for p in procs:
+        if p.is_alive():
+            p.kill()
+            pytest.fail("multi-process exchange timed out")
+        assert p.exitcode == 0, f"rank exited with {p.exitcode}"
+    for r in range(tp):
+        ok, err = (tmp_path / f"rank{r}.txt").read_text().split()
+        assert ok == "1", f"rank {r}: max |o - ref| = {err}"
