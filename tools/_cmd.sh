@@ -1,4 +1,1 @@
-timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-python tools/probe_modes.py
-python tools/probe_sizes.py
-python tools/probe_shard.py 2>&1 | grep default
+for c in 2 3 4 6 8; do echo "== CTAs/SM $c"; FKV_CTAS_PER_SM=$c python tools/probe_shard.py 2>&1 | grep default; done
