@@ -540,8 +540,10 @@ def prefill_compress(peaks):
         hb, off, idx = ops.ada_select(sc, B, w)
         ops.score(q, k, workspace=ws)
         ops.ada_select(sc, B, w)
+        ops.score_select(q, k, B, w, workspace=ws)
         t_score = timed(lambda: ops.score(q, k, workspace=ws), 10) / 10
         t_sel = timed(lambda: ops.ada_select(sc, B, w), 10) / 10
+        t_fused = timed(lambda: ops.score_select(q, k, B, w, workspace=ws), 10) / 10
         cache, _, _ = ops.compress_layer(q, k, v, B, w)
         sbh, slo, shi = cache.host["compact_args"]
         mx = int(hb.max().item())
@@ -552,6 +554,7 @@ def prefill_compress(peaks):
         tf_peak = float(peaks.get("bf16_tflops", 1590.0))
         rows[name] = {
             "score_us": t_score * 1e6, "ada_select_us": t_sel * 1e6, "compact_us": t_cmp * 1e6,
+            "score_select_fused_us": t_fused * 1e6,
             "score_tflops": flops / t_score / 1e12, "score_tflops_frac": flops / t_score / 1e12 / tf_peak,
             "score_K_read_GBs_per_pass": kbytes / (t_score / 2) / 1e9,
             "roofline_us": max(flops / (tf_peak * 1e12), 2 * kbytes / (float(peaks.get("hbm_gbs", 6650.0)) * 1e9)) * 1e6,

@@ -49,7 +49,22 @@ struct ScoreParams {
   float* scores;       // pooled output (fused mode)
   int pool_r;          // pooling radius (pool_k / 2)
   struct GridBar* gridbar;  // fused mode: zeroed counter + generation
+  // MODE 4 (score + Ada split + top-k in one launch); workspace parts zeroed per launch
+  int budget, floor_k, rest_total;  // B, f = floor(alpha (B - w)), R = Hkv (B - w - f)
+  uint32_t* hist;      // [kSelPasses][Bt*Hkv][256] per-pass digit histograms (zeroed)
+  int32_t* active;     // [kSelPasses + 1] requests still searching, per pass (zeroed)
+  int32_t* need_floor; // [1] heads below their floor anywhere (zeroed)
+  uint64_t* ltau;      // [Bt*Hkv] head-local floor thresholds
+  int32_t* counts;     // [Bt*Hkv][n_chunks] int2 (chosen outright, ties at s*) per chunk
+  int32_t* budgets;    // out [Bt, Hkv]
+  int64_t* offsets;    // out [Bt*Hkv + 1]
+  int32_t* idx;        // out [Bt*Hkv*budget]
 };
+
+constexpr int kSelPasses = 4;            // 32-bit orderable scores, 8-bit digits (ties resolved by count)
+constexpr int kSelMaxKeys = kStages * kTileBytes / 4;  // pooled f32 keys staged in the (idle) K ring
+constexpr int kSelMaxHeads = 8;
+constexpr uint64_t kNoKey = ~0ull;
 
 // ------------------------------------------------------------ tcgen05 ----
 __device__ __forceinline__ void tc_fence_before() {
@@ -169,21 +184,352 @@ struct GridBar {
 
 // Grid-wide barrier among the epilogue warps of co-resident CTAs (cooperative
 // launch); the TMA and MMA warps keep streaming while the epilogue waits.
+// Monotonic counter (zeroed per launch): arrival k of every CTA lands in
+// [k*N, (k+1)*N), so the returned count names the barrier and its target.
 __device__ __forceinline__ void epi_grid_sync(GridBar* gb) {
   asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps));
   if (threadIdx.x == 0) {
-    const unsigned g = *reinterpret_cast<volatile unsigned*>(&gb->gen);
-    __threadfence();
-    if (atomicAdd(&gb->count, 1) == gridDim.x * gridDim.y - 1) {
-      gb->count = 0;
-      __threadfence();
-      atomicAdd(&gb->gen, 1);
-    } else {
-      while (*reinterpret_cast<volatile unsigned*>(&gb->gen) == g) __nanosleep(64);
+    const unsigned total = gridDim.x * gridDim.y;
+    unsigned old, v;
+    asm volatile("atom.add.release.gpu.u32 %0, [%1], 1;" : "=r"(old) : "l"(&gb->count) : "memory");
+    const unsigned target = (old / total + 1) * total;
+    while (true) {
+      asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(v) : "l"(&gb->count) : "memory");
+      if (v >= target) break;
+      __nanosleep(32);
     }
-    __threadfence();
   }
   asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps));
+}
+
+// diagnostics: %globaltimer stamps of CTA (0,0) through the fused select
+// (read with fkv__score_stamps; tools/probe_prefill_time.py)
+__device__ unsigned long long g_sstamps[64];
+__device__ __forceinline__ void sstamp(int i) {
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && i < 64) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_sstamps[i] = t;
+  }
+}
+
+__device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps)); }
+
+__device__ __forceinline__ uint32_t orderable(float f) {
+  const uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+// (score desc, index asc) as one unsigned order (select.cu uses the same key)
+__device__ __forceinline__ uint64_t compose(float sc, uint32_t index) {
+  return (static_cast<uint64_t>(orderable(sc)) << 32) | (0xffffffffu - index);
+}
+
+// Scratch of the selection phase, placed in the (idle) Q_win region.
+struct SelScratch {
+  int32_t suf[kSelMaxHeads][256];  // per-head suffix counts of the current digit
+  uint32_t hist[256];
+  int32_t above[kSelMaxHeads], n_at[kSelMaxHeads];
+  int32_t warp_tot[kEpiWarps];
+  int32_t dstar, exact;
+};
+
+// Inclusive suffix sum over d of one value per epilogue thread (d = tid).
+__device__ __forceinline__ int32_t epi_suffix_sum(int32_t v, SelScratch& x) {
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int32_t y = __shfl_down_sync(0xffffffffu, v, off);
+    if (lane + off < 32) v += y;
+  }
+  if (lane == 0) x.warp_tot[w] = v;
+  epi_sync();
+  for (int j = w + 1; j < kEpiWarps; ++j) v += x.warp_tot[j];
+  epi_sync();
+  return v;
+}
+
+__device__ __forceinline__ int32_t epi_count(bool pred, SelScratch& x) {
+  const int tid = threadIdx.x;
+  const uint32_t bal = __ballot_sync(0xffffffffu, pred);
+  if ((tid & 31) == 0) x.warp_tot[tid >> 5] = __popc(bal);
+  epi_sync();
+  int32_t c = 0;
+  for (int j = 0; j < kEpiWarps; ++j) c += x.warp_tot[j];
+  epi_sync();
+  return c;
+}
+
+// Warp-aggregated digit histogram of the keys matching (prefix, mask).
+template <class KeyOf>
+__device__ __forceinline__ void epi_histogram(KeyOf key_of, int nk, uint64_t prefix, uint64_t mask,
+                                              int shift, uint32_t* hist) {
+  const int lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < 256; i += 32 * kEpiWarps) hist[i] = 0;
+  epi_sync();
+  for (int base = 0; base < nk; base += 32 * kEpiWarps) {
+    const int i = base + threadIdx.x;
+    uint64_t key = 0;
+    const bool ok = i < nk && ((key = key_of(i)) & mask) == prefix;
+    const uint32_t d = ok ? static_cast<uint32_t>(key >> shift) & 255u : 256u;
+    const uint32_t peers = __match_any_sync(0xffffffffu, d);
+    if (ok && lane == __ffs(peers) - 1) atomicAdd(&hist[d], __popc(peers));
+  }
+  epi_sync();
+}
+
+// CTA-local (epilogue warps) threshold such that exactly k keys are >= it.
+template <class KeyOf>
+__device__ uint64_t epi_select_kth(KeyOf key_of, int nk, int k, SelScratch& x) {
+  uint64_t prefix = 0, mask = 0;
+  int need = k;
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    epi_histogram(key_of, nk, prefix, mask, shift, x.hist);
+    const int32_t sfx = epi_suffix_sum(static_cast<int32_t>(x.hist[threadIdx.x]), x);
+    const int32_t cnt = epi_count(sfx >= need, x);  // suffix is non-increasing in d
+    const int d = cnt - 1;
+    if (static_cast<int>(threadIdx.x) == d) {
+      x.dstar = d;
+      x.exact = sfx == need;
+      x.warp_tot[0] = sfx - static_cast<int32_t>(x.hist[d]);  // strictly above the bucket
+    }
+    epi_sync();
+    const int dd = x.dstar;
+    const bool exact = x.exact != 0;
+    need -= x.warp_tot[0];
+    prefix |= static_cast<uint64_t>(dd) << shift;
+    mask |= 255ull << shift;
+    epi_sync();
+    if (exact) break;
+  }
+  return prefix;
+}
+
+// ---------------------------------------------------------------------------
+// MODE 4, after pooling: Ada budget split + per-head top-k, grid-wide.  Same
+// result as select.cu's ada_select_kernel (one cluster per request there),
+// here spread over every CTA of the cooperative launch.
+//
+// Radix search over the 32-bit orderable score, MSB-first 8-bit digits: per
+// digit each CTA histograms its own pooled keys into the per-(request, head)
+// global histogram of that pass and, after a grid barrier, every CTA of the
+// request evaluates G(d) = sum_h max(0, N_h(d) - floor) from all heads'
+// histograms and takes the same d* = max{d : G(d) >= R} (the Ada split in
+// its floor-free form, see select.cu).  Four passes fix the threshold score
+// s*; keys with score > s* are chosen, and the tied keys at s* are taken in
+// the global tie order (head asc, token asc) until G reaches R exactly --
+// which needs only per-(head, chunk) tie counts, not four more radix passes
+// over the index bits.  Heads that end below their floor keep exactly their
+// own top-floor (CTA-local select).  One last barrier publishes per-chunk
+// counts so every CTA writes its chosen tokens at the right place of the
+// ascending index list.
+template <class Smem>
+__device__ void select_phase(const ScoreParams& p, Smem& sm, int b, int h, int bh, int chunk, int n,
+                             int t_beg, int nk, const float* sp) {
+  SelScratch& x = *reinterpret_cast<SelScratch*>(&sm.q[0][0][0]);
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int HK = p.hkv, BH = gridDim.y;
+  const int f = p.floor_k, R = p.rest_total;
+  sstamp(1);
+  if (tid < HK) x.above[tid] = 0, x.n_at[tid] = 0;
+  epi_sync();
+  uint32_t prefix = 0, mask = 0;
+  bool exact = R <= 0;
+  int dstar = 0;
+  for (int pass = 0, shift = 24; pass < 4; ++pass, shift -= 8) {
+    if (!exact) {  // add my keys' digit histogram to this pass's global one
+      epi_histogram([&](int i) { return static_cast<uint64_t>(orderable(sp[i])); }, nk, prefix, mask,
+                    shift, x.hist);
+      uint32_t* gh = p.hist + (static_cast<int64_t>(pass) * BH + bh) * 256;
+      if (x.hist[tid]) atomicAdd(gh + tid, x.hist[tid]);
+    }
+    sstamp(2 + 2 * pass);
+    epi_grid_sync(p.gridbar);  // fixed pass count: uniform across the grid
+    sstamp(3 + 2 * pass);
+    if (exact) continue;
+    // suffix counts of every head of this request (all heads' histograms
+    // loaded at once, one L2 round trip), then d* = max{d : G(d) >= R}
+    {
+      const uint32_t* gh = p.hist + (static_cast<int64_t>(pass) * BH + b * HK) * 256 + tid;
+      int32_t v[kSelMaxHeads];
+#pragma unroll
+      for (int hh = 0; hh < kSelMaxHeads; ++hh) v[hh] = hh < HK ? static_cast<int32_t>(__ldcg(gh + hh * 256)) : 0;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1)
+#pragma unroll
+        for (int hh = 0; hh < kSelMaxHeads; ++hh) {
+          const int32_t y = __shfl_down_sync(0xffffffffu, v[hh], off);
+          if (lane + off < 32) v[hh] += y;
+        }
+      if (lane == 0)
+#pragma unroll
+        for (int hh = 0; hh < kSelMaxHeads; ++hh) x.suf[hh][wid] = v[hh];  // warp totals (scratch)
+      epi_sync();
+      int32_t add[kSelMaxHeads];
+#pragma unroll
+      for (int hh = 0; hh < kSelMaxHeads; ++hh) {
+        add[hh] = x.above[hh];
+        for (int j = wid + 1; j < kEpiWarps; ++j) add[hh] += x.suf[hh][j];
+      }
+      epi_sync();
+#pragma unroll
+      for (int hh = 0; hh < kSelMaxHeads; ++hh)
+        if (hh < HK) x.suf[hh][tid] = v[hh] + add[hh];
+    }
+    epi_sync();
+    int32_t gd = 0;
+    for (int hh = 0; hh < HK; ++hh) gd += max(0, x.suf[hh][tid] - f);
+    const int32_t cnt = epi_count(gd >= R, x);
+    if (tid == cnt - 1) {
+      x.dstar = cnt - 1;
+      x.exact = gd == R;
+    }
+    epi_sync();
+    dstar = x.dstar;
+    exact = x.exact != 0;
+    // n_at: keys with the decided digits >= prefix.d*; above: strictly above d*
+    if (tid < HK) {
+      x.n_at[tid] = x.suf[tid][dstar];
+      x.above[tid] = dstar < 255 ? x.suf[tid][dstar + 1] : x.above[tid];
+    }
+    prefix |= static_cast<uint32_t>(dstar) << shift;
+    mask |= 255u << shift;
+    epi_sync();
+  }
+  sstamp(30);
+  const bool have_tau = R > 0;
+  // Final per-head counts.  exact: every key with orderable(score) >= prefix
+  // is in (N_h = n_at).  Otherwise s* = prefix is the full threshold score:
+  // base_h = #(score > s*) = above, tied_h = n_at - above; walk the ties in
+  // head order until G reaches R: heads before hstar take all their ties,
+  // hstar takes its first kstar, later heads none.
+  if (tid == 0) {
+    int hstar = HK, kstar = 0;
+    if (have_tau && !exact) {
+      int need = R;
+      for (int hh = 0; hh < HK; ++hh) need -= max(0, x.above[hh] - f);
+      for (int hh = 0; hh < HK && need > 0; ++hh) {
+        const int base = x.above[hh], tied = x.n_at[hh] - base;
+        const int gain = max(0, base + tied - f) - max(0, base - f);
+        if (gain >= need) {
+          hstar = hh;
+          kstar = max(0, f - base) + need;
+          need = 0;
+        } else {
+          need -= gain;
+        }
+      }
+      for (int hh = 0; hh < HK; ++hh)
+        x.n_at[hh] = hh < hstar ? x.n_at[hh] : (hh == hstar ? x.above[hh] + kstar : x.above[hh]);
+    }
+    x.dstar = hstar;
+    x.exact = kstar;
+  }
+  epi_sync();
+  const int hstar = x.dstar, kstar = x.exact;
+  const uint32_t sstar = prefix;
+  const bool below = !have_tau || x.n_at[h] < f;
+  auto budget_of = [&](int hh) {
+    const int c = have_tau ? max(0, x.n_at[hh] - f) : 0;
+    return p.window + f + c;
+  };
+
+  // heads that end below their floor keep exactly their own top-floor tokens
+  if (below && f > 0 && chunk == 0) {
+    const float* srow = p.scores + static_cast<int64_t>(bh) * n;
+    const uint64_t lt = epi_select_kth(
+        [&](int i) { return compose(__ldcg(srow + i), static_cast<uint32_t>(i)); }, n, f, x);
+    if (tid == 0) p.ltau[bh] = lt;
+  }
+  epi_grid_sync(p.gridbar);
+  const uint64_t ltau = below && f > 0 ? __ldcg(reinterpret_cast<const unsigned long long*>(p.ltau + bh))
+                                       : kNoKey;
+  // class of key i: 1 = chosen outright, 2 = tie at s* (hstar decides by tie rank)
+  auto klass = [&](int i) -> int {
+    if (below) return ltau != kNoKey && compose(sp[i], static_cast<uint32_t>(t_beg + i)) >= ltau;
+    if (!have_tau) return 0;
+    const uint32_t o = orderable(sp[i]);
+    if (exact) return (o & mask) >= prefix;
+    if (o > sstar) return 1;
+    return o == sstar ? (h < hstar ? 1 : (h == hstar ? 2 : 0)) : 0;
+  };
+  // publish (chosen outright, ties) of this chunk
+  int32_t c1 = 0, c2 = 0;
+  for (int i = tid; i < nk; i += 32 * kEpiWarps) {
+    const int k = klass(i);
+    c1 += k == 1;
+    c2 += k == 2;
+  }
+  c1 = __reduce_add_sync(0xffffffffu, c1);
+  c2 = __reduce_add_sync(0xffffffffu, c2);
+  if (lane == 0) x.suf[0][wid] = c1, x.suf[1][wid] = c2;
+  epi_sync();
+  if (tid == 0) {
+    int32_t a = 0, t2 = 0;
+    for (int j = 0; j < kEpiWarps; ++j) a += x.suf[0][j], t2 += x.suf[1][j];
+    int2* cc = reinterpret_cast<int2*>(p.counts) + static_cast<int64_t>(bh) * p.n_chunks + chunk;
+    *cc = make_int2(a, t2);
+  }
+  sstamp(31);
+  epi_grid_sync(p.gridbar);
+  sstamp(32);
+  // this chunk's position in the head's list, and its tie-rank origin
+  int64_t pos = 0;
+  int tie0 = 0;
+  for (int c = lane; c < chunk; c += 32) {
+    const int2 cc = __ldcg(reinterpret_cast<const int2*>(p.counts) + static_cast<int64_t>(bh) * p.n_chunks + c);
+    pos += cc.x;
+    tie0 += cc.y;
+  }
+  // tie counts of earlier chunks decide how many of their ties were taken
+  {
+    // warp 0 reduces (every warp computed the same partial sums per lane)
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      pos += __shfl_xor_sync(0xffffffffu, pos, off);
+      tie0 += __shfl_xor_sync(0xffffffffu, tie0, off);
+    }
+  }
+  if (h == hstar) pos += min(tie0, kstar);  // ties of earlier chunks that were taken
+  int64_t off = static_cast<int64_t>(b) * HK * p.budget;
+  for (int hh = 0; hh < h; ++hh) off += budget_of(hh);
+  const int bud = budget_of(h);
+  int32_t* out = p.idx + off;
+  int tie_run = tie0;  // tie rank of the next tie in token order
+  for (int base = 0; base < nk; base += 32 * kEpiWarps) {
+    const int i = base + tid;
+    const int k = i < nk ? klass(i) : 0;
+    const uint32_t bt = __ballot_sync(0xffffffffu, k == 2);
+    if (lane == 0) x.suf[1][wid] = __popc(bt);
+    epi_sync();
+    int tb = __popc(bt & ((1u << lane) - 1u));
+    int t_tot = 0;
+    for (int j = 0; j < kEpiWarps; ++j) {
+      if (j < wid) tb += x.suf[1][j];
+      t_tot += x.suf[1][j];
+    }
+    const bool take = k == 1 || (k == 2 && tie_run + tb < kstar);
+    const uint32_t bal = __ballot_sync(0xffffffffu, take);
+    if (lane == 0) x.suf[0][wid] = __popc(bal);
+    epi_sync();
+    int before = __popc(bal & ((1u << lane) - 1u)), total = 0;
+    for (int j = 0; j < kEpiWarps; ++j) {
+      if (j < wid) before += x.suf[0][j];
+      total += x.suf[0][j];
+    }
+    if (take) out[pos + before] = t_beg + i;
+    pos += total;
+    tie_run += t_tot;
+    epi_sync();
+  }
+  sstamp(33);
+  if (chunk == 0) {
+    for (int i = tid; i < p.window; i += 32 * kEpiWarps) out[bud - p.window + i] = n + i;
+    if (tid == 0) {
+      p.budgets[bh] = bud;
+      p.offsets[bh] = off;
+      if (bh == BH - 1) p.offsets[BH] = off + bud;
+    }
+  }
 }
 
 // MODE 1: pass 1 only; MODE 2: pass 2 only; MODE 3: both passes + pooling in
@@ -198,8 +544,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   constexpr uint32_t kCols = 2 * GW;  // two accumulator buffers of GW fp32 columns
   constexpr bool kP1 = MODE != 2, kP2 = MODE != 1;
+  constexpr bool kFused = MODE >= 3;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  sstamp(0);
   const int bh = blockIdx.y, chunk = blockIdx.x;
   const int b = bh / p.hkv, h = bh - b * p.hkv;
   const int n = p.T - p.window;
@@ -369,8 +717,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         st[1] = l;
       }
     }
-    if (MODE == 3) {
+    if (kFused) {
+      sstamp(40);
       epi_grid_sync(p.gridbar);  // every chunk's statistics are in global memory
+      sstamp(41);
       combine_stats();
       asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps));
     }
@@ -405,17 +755,24 @@ __global__ void __launch_bounds__(kThreads, 1)
           p.raw[static_cast<int64_t>(bh) * n + t] = acc + sm.red[it & 1][1][key];
       }
     }
-    if (MODE == 3) {
+    if (kFused) {
+      sstamp(42);
       epi_grid_sync(p.gridbar);  // every raw column score is in global memory
+      sstamp(43);
       const float* rr = p.raw + static_cast<int64_t>(bh) * n;
       float* out = p.scores + static_cast<int64_t>(bh) * n;
-      const int t_end = min(e2 * kBN, n);
-      for (int t = a2 * kBN + threadIdx.x; t < t_end; t += 32 * kEpiWarps) {
+      const int t_beg = a2 * kBN, t_end = min(e2 * kBN, n);
+      // MODE 4 stages this CTA's pooled scores in the K ring (idle: every tile
+      // was consumed before the epilogue reached the barrier above)
+      float* sp = reinterpret_cast<float*>(&sm.k[0][0][0][0]);
+      for (int t = t_beg + threadIdx.x; t < t_end; t += 32 * kEpiWarps) {
         float mx = __ldcg(rr + t);
         const int lo = max(0, t - p.pool_r), hi = min(n - 1, t + p.pool_r);
         for (int u = lo; u <= hi; ++u) mx = fmaxf(mx, __ldcg(rr + u));
         out[t] = mx;
+        if (MODE == 4) sp[t - t_beg] = mx;
       }
+      if (MODE == 4) select_phase(p, sm, b, h, bh, chunk, n, t_beg, max(t_end - t_beg, 0), sp);
     }
   }
   tc_fence_before();
@@ -495,11 +852,11 @@ namespace {
 
 template <int GW>
 int launch_score(const CUtensorMap& tq, const CUtensorMap& tk, const ScoreParams& p, int batch_heads,
-                 bool fused, cudaStream_t st) {
+                 int mode, cudaStream_t st) {
   const size_t smem = sizeof(ScoreSmem<GW>) + 1024;
   static bool configured = false;
   if (!configured) {
-    for (auto fn : {score_kernel<1, GW>, score_kernel<2, GW>, score_kernel<3, GW>})
+    for (auto fn : {score_kernel<1, GW>, score_kernel<2, GW>, score_kernel<3, GW>, score_kernel<4, GW>})
       if (int rc = cuda_check(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    smem),
                               "score smem attribute"))
@@ -507,8 +864,9 @@ int launch_score(const CUtensorMap& tq, const CUtensorMap& tk, const ScoreParams
     configured = true;
   }
   dim3 grid(p.n_chunks, batch_heads);
-  if (fused) {
+  if (mode >= 3) {
     // one cooperative launch: both passes and the pooling (grid <= #SMs, 1 CTA/SM)
+    // [+ MODE 4: the Ada split and top-k selection]
     if (int rc = cuda_check(cudaMemsetAsync(p.gridbar, 0, sizeof(GridBar), st), "gridbar reset"))
       return rc;
     cudaLaunchConfig_t cfg = {};
@@ -521,7 +879,9 @@ int launch_score(const CUtensorMap& tq, const CUtensorMap& tk, const ScoreParams
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cuda_check(cudaLaunchKernelEx(&cfg, score_kernel<3, GW>, tq, tk, p), "score fused launch");
+    return cuda_check(cudaLaunchKernelEx(&cfg, mode == 4 ? score_kernel<4, GW> : score_kernel<3, GW>, tq,
+                                         tk, p),
+                      "score fused launch");
   }
   score_kernel<1, GW><<<grid, kThreads, smem, st>>>(tq, tk, p);
   if (int rc = cuda_check(cudaGetLastError(), "score pass 1 launch")) return rc;
@@ -537,21 +897,43 @@ int launch_score(const CUtensorMap& tq, const CUtensorMap& tk, const ScoreParams
 }  // namespace
 }  // namespace fkv
 
-extern "C" int64_t fkv_score_workspace_bytes(int32_t batch, int32_t hkv, int32_t T, int32_t window,
-                                             int32_t group) {
+namespace fkv {
+namespace {
+struct ScoreLayout {
+  int chunks, tiles_per_chunk, bh;
+  int64_t stats, raw, gridbar, hist, active, ltau, counts, total;
+};
+
+ScoreLayout score_layout(int batch, int hkv, int T, int window, int group) {
+  ScoreLayout L{};
   const int gw = group * window;
-  const int n_tiles = (T + fkv::kBN - 1) / fkv::kBN;
-  const int bh = batch * hkv;
-  const int chunks = fkv::score_chunks(bh > 0 ? bh : 1, n_tiles);
-  const int64_t stats = static_cast<int64_t>(bh) * chunks * gw * 2 * 4;
-  const int64_t raw = static_cast<int64_t>(bh) * (T - window) * 4;
-  return stats + raw + 256;
+  const int n_tiles = (T + kBN - 1) / kBN;
+  L.bh = batch * hkv;
+  int chunks = score_chunks(L.bh > 0 ? L.bh : 1, n_tiles);
+  L.tiles_per_chunk = (n_tiles + chunks - 1) / chunks;
+  L.chunks = (n_tiles + L.tiles_per_chunk - 1) / L.tiles_per_chunk;
+  auto a16 = [](int64_t x) { return (x + 255) & ~int64_t(255); };
+  L.stats = 0;
+  L.raw = a16(L.stats + static_cast<int64_t>(L.bh) * L.chunks * gw * 2 * 4);
+  L.gridbar = a16(L.raw + static_cast<int64_t>(L.bh) * (T - window) * 4);
+  L.hist = a16(L.gridbar + 64);
+  L.active = a16(L.hist + static_cast<int64_t>(kSelPasses) * L.bh * 256 * 4);
+  L.ltau = a16(L.active + (kSelPasses + 2) * 4);
+  L.counts = a16(L.ltau + static_cast<int64_t>(L.bh) * 8);
+  L.total = a16(L.counts + static_cast<int64_t>(L.bh) * L.chunks * 8);
+  return L;
 }
 
-extern "C" int fkv_snapkv_score(const void* q_win, const void* k, int32_t batch, int32_t hq,
-                                int32_t hkv, int32_t T, int32_t window, int32_t pool_k,
-                                float sm_scale, float* scores, void* workspace, void* stream) {
-  using namespace fkv;
+int sms_count() {
+  int sms = 148, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms;
+}
+
+int score_common(const void* q_win, const void* k, int32_t batch, int32_t hq, int32_t hkv, int32_t T,
+                 int32_t window, int32_t pool_k, float sm_scale, float* scores, void* workspace,
+                 ScoreParams& p, ScoreLayout& L, CUtensorMap& tq, CUtensorMap& tk) {
   if (!q_win || !k || !scores || !workspace)
     return set_error(FKV_ERR_INVALID, "fkv_snapkv_score: null pointer");
   if (batch < 1 || hkv < 1 || hq % hkv || T <= window || window < 1 || pool_k < 1 || !(pool_k & 1))
@@ -562,30 +944,100 @@ extern "C" int fkv_snapkv_score(const void* q_win, const void* k, int32_t batch,
     return set_error(FKV_ERR_INVALID, "fkv_snapkv_score: group * window must be 128 or 256");
   if (static_cast<int64_t>(batch) * hkv * T >= 0x7fffffffLL)
     return set_error(FKV_ERR_INVALID, "fkv_snapkv_score: Bt * Hkv * T too large");
-  const int n_tiles = (T + kBN - 1) / kBN;
-  const int bh = batch * hkv;
-  int chunks = score_chunks(bh, n_tiles);
-  const int tiles_per_chunk = (n_tiles + chunks - 1) / chunks;
-  chunks = (n_tiles + tiles_per_chunk - 1) / tiles_per_chunk;
-
-  CUtensorMap tq, tk;
+  L = score_layout(batch, hkv, T, window, group);
   if (int rc = make_map(&tq, q_win, static_cast<int64_t>(batch) * hq * window, 128)) return rc;
   if (int rc = make_map(&tk, k, static_cast<int64_t>(batch) * hkv * T, kBN)) return rc;
-  float* stats = static_cast<float*>(workspace);
-  float* raw = stats + static_cast<int64_t>(bh) * chunks * gw * 2;
-  auto* gridbar = reinterpret_cast<GridBar*>(
-      (reinterpret_cast<uintptr_t>(raw + static_cast<int64_t>(bh) * (T - window)) + 15) & ~uintptr_t(15));
-  ScoreParams p{T, window, group, hkv, chunks, tiles_per_chunk, hq * window,
-                sm_scale * kLog2e, stats, raw, scores, pool_k / 2, gridbar};
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  p = ScoreParams{};
+  p.T = T;
+  p.window = window;
+  p.group = group;
+  p.hkv = hkv;
+  p.n_chunks = L.chunks;
+  p.tiles_per_chunk = L.tiles_per_chunk;
+  p.q_rows_per_req = hq * window;
+  p.scale_log2 = sm_scale * kLog2e;
+  p.stats = reinterpret_cast<float*>(ws + L.stats);
+  p.raw = reinterpret_cast<float*>(ws + L.raw);
+  p.scores = scores;
+  p.pool_r = pool_k / 2;
+  p.gridbar = reinterpret_cast<GridBar*>(ws + L.gridbar);
+  p.hist = reinterpret_cast<uint32_t*>(ws + L.hist);
+  p.active = reinterpret_cast<int32_t*>(ws + L.active);
+  p.need_floor = p.active + kSelPasses + 1;
+  p.ltau = reinterpret_cast<uint64_t*>(ws + L.ltau);
+  p.counts = reinterpret_cast<int32_t*>(ws + L.counts);
+  return FKV_OK;
+}
+}  // namespace
+}  // namespace fkv
+
+extern "C" int fkv__score_stamps(unsigned long long* host) {
+  return fkv::cuda_check(cudaMemcpyFromSymbol(host, fkv::g_sstamps, sizeof(unsigned long long) * 64),
+                         "score stamps");
+}
+
+extern "C" int64_t fkv_score_workspace_bytes(int32_t batch, int32_t hkv, int32_t T, int32_t window,
+                                             int32_t group) {
+  return fkv::score_layout(batch, hkv, T, window, group).total;
+}
+
+extern "C" int fkv_snapkv_score(const void* q_win, const void* k, int32_t batch, int32_t hq,
+                                int32_t hkv, int32_t T, int32_t window, int32_t pool_k,
+                                float sm_scale, float* scores, void* workspace, void* stream) {
+  using namespace fkv;
+  ScoreParams p;
+  ScoreLayout L;
+  CUtensorMap tq, tk;
+  if (int rc = score_common(q_win, k, batch, hq, hkv, T, window, pool_k, sm_scale, scores, workspace,
+                            p, L, tq, tk))
+    return rc;
   auto st = static_cast<cudaStream_t>(stream);
   // fused single launch whenever every CTA can be co-resident (1 CTA per SM)
-  int sms = 148;
-  {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int mode = static_cast<int64_t>(L.bh) * L.chunks <= sms_count() ? 3 : 1;
+  return p.group * window == 128 ? launch_score<128>(tq, tk, p, L.bh, mode, st)
+                                 : launch_score<256>(tq, tk, p, L.bh, mode, st);
+}
+
+extern "C" int fkv_ada_select(const float* scores, int32_t batch, int32_t hkv, int32_t n,
+                              int32_t budget, int32_t window, int32_t floor_k, int32_t* budgets,
+                              int64_t* offsets, int32_t* idx, void* stream);
+
+extern "C" int fkv_snapkv_select(const void* q_win, const void* k, int32_t batch, int32_t hq,
+                                 int32_t hkv, int32_t T, int32_t window, int32_t pool_k,
+                                 float sm_scale, int32_t budget, int32_t floor_k, float* scores,
+                                 int32_t* budgets, int64_t* offsets, int32_t* idx, void* workspace,
+                                 void* stream) {
+  using namespace fkv;
+  if (!budgets || !offsets || !idx) return set_error(FKV_ERR_INVALID, "fkv_snapkv_select: null pointer");
+  const int n = T - window, sel = budget - window;
+  if (sel < 0 || sel > n || floor_k < 0 || floor_k > sel)
+    return set_error(FKV_ERR_INVALID, "fkv_snapkv_select: need 0 <= floor <= budget-window <= T-window");
+  ScoreParams p;
+  ScoreLayout L;
+  CUtensorMap tq, tk;
+  if (int rc = score_common(q_win, k, batch, hq, hkv, T, window, pool_k, sm_scale, scores, workspace,
+                            p, L, tq, tk))
+    return rc;
+  auto st = static_cast<cudaStream_t>(stream);
+  const bool fused = static_cast<int64_t>(L.bh) * L.chunks <= sms_count() && hkv <= kSelMaxHeads &&
+                     L.tiles_per_chunk * kBN <= kSelMaxKeys;
+  if (!fused) {  // two launches: scoring, then the cluster split + select (select.cu)
+    const int mode = static_cast<int64_t>(L.bh) * L.chunks <= sms_count() ? 3 : 1;
+    if (int rc = p.group * window == 128 ? launch_score<128>(tq, tk, p, L.bh, mode, st)
+                                         : launch_score<256>(tq, tk, p, L.bh, mode, st))
+      return rc;
+    return fkv_ada_select(scores, batch, hkv, n, budget, window, floor_k, budgets, offsets, idx, stream);
   }
-  const bool fused = static_cast<int64_t>(bh) * chunks <= sms;
-  return gw == 128 ? launch_score<128>(tq, tk, p, bh, fused, st)
-                   : launch_score<256>(tq, tk, p, bh, fused, st);
+  p.budget = budget;
+  p.floor_k = floor_k;
+  p.rest_total = hkv * sel - hkv * floor_k;
+  p.budgets = budgets;
+  p.offsets = offsets;
+  p.idx = idx;
+  // zero the per-pass histograms, pass counters and the floor flag (one contiguous range)
+  if (int rc = cuda_check(cudaMemsetAsync(p.hist, 0, L.ltau - L.hist, st), "select workspace reset"))
+    return rc;
+  return p.group * window == 128 ? launch_score<128>(tq, tk, p, L.bh, 4, st)
+                                 : launch_score<256>(tq, tk, p, L.bh, 4, st);
 }

@@ -8,6 +8,7 @@ allocator) or take caller-provided buffers (``out=`` / ``ws=``) so the whole
 decode step can be captured in a CUDA graph.
 
     score(q_win, k, window, pool_k=7)   -> scores  f32 [Bt,Hkv,T-w]       (K1)
+    score_select(q_win, k, budget, ...) -> scores, budgets, offsets, idx  (K1+A18+K2, one launch)
     budgets(scores, budget, window, alpha=0.2) -> int32 [Bt,Hkv]          (A18)
     select(scores, budgets, window)     -> (offsets, idx)                 (K2)
     compact(k, v, offsets, idx, ...)    -> LayerCache                     (K3)
@@ -167,6 +168,39 @@ def score(q_win: torch.Tensor, k: torch.Tensor, window: int | None = None, pool_
     return out
 
 
+def score_select(q_win: torch.Tensor, k: torch.Tensor, budget: int, window: int | None = None,
+                 alpha: float = 0.2, pool_k: int = 7, sm_scale: float | None = None,
+                 workspace: torch.Tensor | None = None):
+    """K1 + A18 + K2 in one cooperative launch: Ada-SnapKV scores, the Ada
+    budget split and the per-head top-k (tcgen05 scoring, grid-wide radix
+    select).  -> (scores f32 [Bt,Hkv,T-w], budgets int32 [Bt,Hkv], offsets
+    int64 [Bt*Hkv+1], idx int32 [Bt*Hkv*budget]); identical to ``score``
+    followed by ``ada_select``.  Shapes whose grid cannot be co-resident fall
+    back to those two launches inside the library."""
+    _need_cuda(q_win, k)
+    if q_win.dtype != torch.bfloat16 or k.dtype != torch.bfloat16 or q_win.shape[-1] != HEAD_DIM \
+            or k.shape[-1] != HEAD_DIM or not (q_win.is_contiguous() and k.is_contiguous()):
+        raise NativeError("q_win / k must be contiguous bf16 [..., 128]")
+    bt, hq, w, _ = q_win.shape
+    _, hkv, T, _ = k.shape
+    if window is not None and window != w:
+        raise NativeError(f"window {window} != q_win.shape[2] {w}")
+    scale = 1.0 / math.sqrt(HEAD_DIM) if sm_scale is None else sm_scale
+    dev = k.device
+    sc = torch.empty((bt, hkv, T - w), dtype=torch.float32, device=dev)
+    hb = torch.empty((bt, hkv), dtype=torch.int32, device=dev)
+    offsets = torch.empty(bt * hkv + 1, dtype=torch.int64, device=dev)
+    idx = torch.empty(max(bt * hkv * budget, 1), dtype=torch.int32, device=dev)
+    need = int(_lib.fkv_score_workspace_bytes(bt, hkv, T, w, hq // hkv))
+    if workspace is None or workspace.numel() * workspace.element_size() < need:
+        workspace = torch.empty(need, dtype=torch.uint8, device=dev)
+    _native.check(_lib.fkv_snapkv_select(q_win.data_ptr(), k.data_ptr(), bt, hq, hkv, T, w, int(pool_k),
+                                         scale, int(budget), ada_floor(budget, w, alpha), sc.data_ptr(),
+                                         hb.data_ptr(), offsets.data_ptr(), idx.data_ptr(),
+                                         workspace.data_ptr(), _stream()))
+    return sc, hb, offsets, idx[:bt * hkv * budget]
+
+
 def ada_floor(budget: int, window: int, alpha: float) -> int:
     """Per-head Ada safeguard floor floor(alpha * (B - w))."""
     return int(math.floor(alpha * (budget - window)))
@@ -260,15 +294,14 @@ def compact(k: torch.Tensor, v: torch.Tensor, offsets: torch.Tensor, idx: torch.
 
 def compress_layer(q_win: torch.Tensor, k: torch.Tensor, v: torch.Tensor, budget: int,
                    window: int = 32, alpha: float = 0.2, pool_k: int = 7):
-    """Prefill of one layer on one GPU: K1 score -> A18+K2 (one cluster
-    launch) -> K3 compact (TP=1 layout).  Returns (cache, head_budgets, scores).
+    """Prefill of one layer on one GPU: K1 score + A18 budgets + K2 select
+    (one cooperative launch) -> K3 compact (TP=1 layout).  Returns (cache, head_budgets, scores).
     The host reads the budgets back once to lay out the ragged cache."""
     import numpy as np
     bt, hq = q_win.shape[0], q_win.shape[1]
     hkv = k.shape[1]
     group = hq // hkv
-    sc = score(q_win, k, window=window, pool_k=pool_k)
-    hb, offsets, idx = ada_select(sc, budget, window, alpha)
+    sc, hb, offsets, idx = score_select(q_win, k, budget, window, alpha, pool_k)
     hb_host = hb.cpu().numpy().reshape(-1)
     bh = np.arange(bt * hkv)
     qrow = (bh // hkv) * hq + (bh % hkv) * group

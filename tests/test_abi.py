@@ -19,7 +19,8 @@ def declared_symbols():
 def test_header_declares_the_abi():
     syms = declared_symbols()
     for name in ("fkv_solve_equal_split", "fkv_solve_free_split", "fkv_select_best",
-                 "fkv_optimize_plan", "fkv_decode", "fkv_merge_lse", "fkv_snapkv_score",
+                 "fkv_optimize_plan", "fkv_decode", "fkv_decode_exchange", "fkv_merge_lse",
+                 "fkv_merge_wait", "fkv_snapkv_score", "fkv_snapkv_select",
                  "fkv_ada_budgets", "fkv_topk_select", "fkv_compact", "fkv_last_error"):
         assert name in syms
 

@@ -159,3 +159,46 @@ def test_fused_ada_select_bit_exact(cuda_device, bt, T, budget, ties):
     ref_off, ref_idx = okv.topk_select(s64, ref_b, 32)
     np.testing.assert_array_equal(off.cpu().numpy(), ref_off)
     np.testing.assert_array_equal(idx.cpu().numpy(), ref_idx)
+
+
+@pytest.mark.parametrize("bt,hq,hkv,T,budget,temp,flat_head", [
+    (1, 32, 8, 4096, 128, 3.0, False),    # 8B shape, fused grid
+    (2, 64, 8, 6000, 256, 2.0, False),    # 70B shape (G*w = 256)
+    (1, 32, 8, 20000, 1024, 3.0, False),  # long context, several chunks per head
+    (2, 32, 8, 3000, 256, 2.0, True),     # a head whose window soaks up all attention: below its floor
+    (20, 32, 8, 600, 64, 2.0, False),     # 160 heads > 148 SMs: two-launch fallback
+])
+def test_fused_score_select_bit_exact(cuda_device, bt, hq, hkv, T, budget, temp, flat_head):
+    """K1 + A18 + K2 in one launch: scores within tolerance of the oracle;
+    budgets / offsets / indices bit-exact against the oracle fed the kernel's
+    own pooled scores (max-pooling makes exact ties common)."""
+    from paper_2502_15804_b200 import ops
+    q, k, _, qn, kn, _ = _inputs(bt, hq, hkv, T, 32, 13, cuda_device, temp=temp)
+    if flat_head:
+        # KV head 3: constant queries u, zero keys outside the window and window
+        # keys 20u -> the window takes all attention mass, every other score of
+        # the head ties at ~e^-57: the head keeps exactly its floor (lowest tokens)
+        G = hq // hkv
+        u = torch.full((128,), 0.5, dtype=torch.bfloat16, device=cuda_device)
+        q[:, 3 * G:4 * G] = u
+        k[:, 3] = 0
+        k[:, 3, T - 32:] = 20 * u
+        qn, kn = q.cpu().double().numpy(), k.cpu().double().numpy()
+    sc, hb, off, idx = ops.score_select(q, k, budget, 32)
+    torch.cuda.synchronize()
+    s64 = sc.cpu().double().numpy()
+    if T <= 6000:
+        ref_s = okv.snapkv_scores(qn, kn)
+        err = np.abs(s64 - ref_s).max(axis=-1) / np.abs(ref_s).max(axis=-1)
+        assert err.max() < 2e-2, err.max()
+    ref_b = okv.ada_budgets(s64, budget, 32, 0.2)
+    np.testing.assert_array_equal(hb.cpu().numpy(), ref_b)
+    if flat_head:
+        assert (ref_b[:, 3] == 32 + int(0.2 * (budget - 32))).all()  # kept exactly its floor
+    ref_off, ref_idx = okv.topk_select(s64, ref_b, 32)
+    np.testing.assert_array_equal(off.cpu().numpy(), ref_off)
+    np.testing.assert_array_equal(idx.cpu().numpy(), ref_idx)
+    # repeated launches reuse the workspace (counters / histograms re-zeroed)
+    sc2, hb2, off2, idx2 = ops.score_select(q, k, budget, 32)
+    torch.cuda.synchronize()
+    assert torch.equal(idx2, idx) and torch.equal(hb2, hb)

@@ -1,1 +1,2 @@
-for c in 2 3 4 6 8; do echo "== CTAs/SM $c"; FKV_CTAS_PER_SM=$c python tools/probe_shard.py 2>&1 | grep default; done
+timeout 900 python -m pytest tests/test_compress_gpu.py -x -q 2>&1 | tail -15
+python tools/probe_prefill_time.py
