@@ -37,10 +37,18 @@ namespace fkv {
 namespace {
 
 constexpr int kWarps = 4;
-constexpr int kStages = 3;  // ring stages per warp (tiles in flight)
+#ifndef FKV_K4_DEDICATED
+#define FKV_K4_DEDICATED 1
+#endif
+// FKV_K4_DEDICATED: warp 0 only combines / finalises (records, atomics,
+// segment merges) while warps 1-3 stream with 4-stage rings; otherwise all
+// four warps stream (3 stages) and warp 0 takes one round in seven.
+constexpr bool kDedicated = FKV_K4_DEDICATED != 0;
+constexpr int kStreamWarps = kDedicated ? kWarps - 1 : kWarps;
+constexpr int kStages = kDedicated ? 4 : 3;  // ring stages per streaming warp (tiles in flight)
 constexpr int kTileTok = 16;
-constexpr int kTileBytes = kTileTok * FKV_HEAD_DIM * 2;        // 4 KiB per K or V tile
-constexpr int kSmemBytes = kWarps * kStages * 2 * kTileBytes;  // 96 KiB per CTA
+constexpr int kTileBytes = kTileTok * FKV_HEAD_DIM * 2;              // 4 KiB per K or V tile
+constexpr int kSmemBytes = kStreamWarps * kStages * 2 * kTileBytes;  // 96 KiB per CTA
 constexpr int kMergeMax = FKV_MAX_PIECES;                      // max pieces per segment
 constexpr int kXch = 36;  // floats per lane handed to warp 0: m0 m1 l0 l1 acc[32]
 constexpr float kLog2e = 1.4426950408889634f;
@@ -69,6 +77,7 @@ struct __align__(16) DecodeShared {
   uint64_t bars[kWarps][kStages];
   float xch[kWarps - 1][kXch][32];  // warps 1..3 -> warp 0 piece state, lane-contiguous
   float scratch[kMergeMax * 8];     // global merge weights
+  int32_t fin_i0, fin_n_it, fin_orow;  // deferred merge of the CTA's last piece (n_it 0 = none)
 };
 
 __device__ __forceinline__ void put_rec(const DecodeParams& p, int64_t idx, float v) {
@@ -100,13 +109,19 @@ __device__ __forceinline__ void named_arrive(int id) {
 // 1-3 own two each (offsets j-1, j+3): warp 0 combines and finalises every
 // piece (records, atomics, segment merges), so it streams half as much.
 constexpr int kPeriod = 7;
+constexpr int kNoRound = 0x7fffffff;
 __device__ __forceinline__ int first_round(int warp, int g0) {  // first owned round >= g0
+  if (kDedicated) {  // warps 1-3 round robin, warp 0 none
+    if (warp == 0) return kNoRound;
+    return g0 + ((warp - 1 - g0 % 3) + 3) % 3;
+  }
   const int base = g0 - g0 % kPeriod;
   if (warp == 0) return base + 3 >= g0 ? base + 3 : base + 3 + kPeriod;
   const int a = base + warp - 1, b = base + warp + 3;
   return a >= g0 ? a : (b >= g0 ? b : a + kPeriod);
 }
 __device__ __forceinline__ int next_round(int warp, int r) {
+  if (kDedicated) return r + 3;
   if (warp == 0) return r + kPeriod;
   return r % kPeriod == warp - 1 ? r + 4 : r + 3;
 }
@@ -133,7 +148,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodePara
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  uint8_t* ring = smem + warp * kStages * 2 * kTileBytes;
+  uint8_t* ring = smem + (kDedicated ? (warp > 0 ? warp - 1 : 0) : warp) * kStages * 2 * kTileBytes;
   uint64_t* wbars = sh.bars[warp];
   const fkv_work_t* tab = sh.tab;
   if (PROBE == 3 && threadIdx.x == 0) {
@@ -159,6 +174,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodePara
     for (int s = 0; s < kStages; ++s) mbar_init(&wbars[s], 1);
     fence_mbar_init();
   }
+  if (threadIdx.x == 0) sh.fin_n_it = 0;
   __syncthreads();
 
   // ---- producer: this warp's rounds (two tiles each) of every piece, in the
@@ -167,7 +183,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodePara
   int p_r = first_round(warp, 0);     // next owned round
   uint32_t p_seq = 0, c_seq = 0;
   int p_s = 0;
-  bool p_done = false;
+  bool p_done = kDedicated && warp == 0;  // the combiner warp streams nothing
   auto refill = [&]() {
     while (!p_done && p_seq - c_seq < static_cast<uint32_t>(kStages)) {
       if (p_pc >= FKV_MAX_WORK || tab[p_pc].n_it == 0) {
@@ -498,6 +514,11 @@ __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodePara
     if (lane == 0) last = atom_add_acq_rel(p.counters + d.i0, 1) == n_it - 1;
     last = __shfl_sync(0xffffffffu, last, 0);
     stamp(PROBE, 7);
+    if (kDedicated && last && !more) {
+      // the CTA's last piece: warps 1-3 are idle, merge with all four (below)
+      if (lane == 0) sh.fin_i0 = d.i0, sh.fin_n_it = n_it, sh.fin_orow = static_cast<int32_t>(orow);
+      continue;
+    }
     if (!last) continue;
     // All (piece, head) lse values in one parallel round trip, weights in
     // shared scratch, then every lane streams its 4 head_dim columns of all
@@ -558,10 +579,75 @@ __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodePara
     __syncwarp();  // the scratch is reused by the next merge
   }
 
+  if (kDedicated) {
+    // Deferred merge of the segment the CTA's last piece completed: the four
+    // warps split the G heads, each lane loads its columns of every piece's
+    // record together with the lse values (one L2 round trip), weights by
+    // warp shuffles.
+    named_sync(3);
+    const int n_it = sh.fin_n_it;
+    if (n_it > 0) {
+      const float* base = p.part + static_cast<int64_t>(sh.fin_i0) * G * FKV_REC;
+      const int64_t orow = sh.fin_orow;
+      constexpr int kHpw = (G + kWarps - 1) / kWarps;  // heads per warp
+#pragma unroll
+      for (int hi = 0; hi < kHpw; ++hi) {
+        const int g = warp * kHpw + hi;
+        if (g >= G) break;
+        const float l = lane < n_it ? __ldcg(base + (lane * G + g) * FKV_REC + FKV_HEAD_DIM) : -CUDART_INF_F;
+        float4 v[8];
+        const int n0 = n_it < 8 ? n_it : 8;
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          v[i] = i < n0 ? __ldcg(reinterpret_cast<const float4*>(base + (i * G + g) * FKV_REC) + lane)
+                        : make_float4(0.f, 0.f, 0.f, 0.f);
+        float M = l;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+        const float e = M == -CUDART_INF_F || l == -CUDART_INF_F ? 0.f : __expf(l - M);
+        float S = e;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) S += __shfl_xor_sync(0xffffffffu, S, off);
+        const float wl = S > 0.f ? e / S : 0.f;
+        float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+        auto fma4 = [&](float wi, const float4& x) {
+          o.x = fmaf(wi, x.x, o.x);
+          o.y = fmaf(wi, x.y, o.y);
+          o.z = fmaf(wi, x.z, o.z);
+          o.w = fmaf(wi, x.w, o.w);
+        };
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float wi = __shfl_sync(0xffffffffu, wl, i);
+          if (i < n_it) fma4(wi, v[i]);
+        }
+        for (int i = 8; i < n_it; ++i)
+          fma4(__shfl_sync(0xffffffffu, wl, i),
+               __ldcg(reinterpret_cast<const float4*>(base + (i * G + g) * FKV_REC) + lane));
+        const float lse_g = S > 0.f ? M + __logf(S) : -CUDART_INF_F;
+        const int64_t row = orow + g;
+        if (p.out_bf16) {
+          __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(p.out_bf16 + row * FKV_HEAD_DIM) + 2 * lane;
+          ob[0] = __floats2bfloat162_rn(o.x, o.y);
+          ob[1] = __floats2bfloat162_rn(o.z, o.w);
+        }
+        if (p.n_rec) put_rec4(p, row, lane, o);
+        if (lane == 0) {
+          if (p.n_rec) put_rec(p, row * FKV_REC + FKV_HEAD_DIM, lse_g);
+          if (p.out_lse) p.out_lse[row] = lse_g;
+        }
+      }
+      if (threadIdx.x == 0) p.counters[sh.fin_i0] = 0;
+    }
+  }
+
   if (warp == 0) stamp(PROBE, 5);
   // Fused all-gather completion: the last CTA out publishes this rank's
   // records to every peer by bumping its flag there (system-scope release).
-  // Only warp 0 writes global memory, so it alone signals.
+  if (p.n_sig > 0 && kDedicated) {
+    __threadfence_system();  // every warp may have written peer records (merge above)
+    named_sync(3);
+  }
   if (p.n_sig > 0 && warp == 0) {
     __threadfence_system();
     __syncwarp();

@@ -48,7 +48,8 @@ for tp in (1, 8):
     nsplit = ((wk[:, :, 7] > 1)).sum(1)
     for k in sorted(set(npieces.tolist())):
         sel = npieces == k
-        print(f"   CTAs with {k} pieces: n={sel.sum():3d} mean done {np.nanmean(done[sel]):6.2f} exit {np.nanmean(st[sel,5]):6.2f}")
+        print(f"   CTAs with {k} pieces: n={sel.sum():3d} mean done {np.nanmean(done[sel]):6.2f} exit {np.nanmean(st[sel,5]):6.2f}  "
+              + " ".join(f"{names[i]}={np.nanmean(st[sel, i]):.2f}" for i in (1, 2, 4, 6, 7, 8, 9, 10, 11) if i < st.shape[1]))
     for k in sorted(set(nsplit.tolist())):
         sel = nsplit == k
         print(f"   CTAs with {k} split pieces: n={sel.sum():3d} mean done {np.nanmean(done[sel]):6.2f} exit {np.nanmean(st[sel,5]):6.2f}")
