@@ -119,6 +119,11 @@ typedef struct fkv_work {
 } fkv_work_t;
 #define FKV_MAX_WORK 32   /* entries per worker */
 #define FKV_MAX_PIECES 32 /* pieces per segment */
+/* flags: FKV_DECODE_SOLO = per-warp schedule for small caches.  Worker w is
+ * then one CTA whose four warps each stream their own pieces start to finish
+ * (piece owner warp = n_it >> 16, pieces per segment = n_it & 0xffff);
+ * without it the four warps share every piece of the CTA's list. */
+#define FKV_DECODE_SOLO 1
 
 /*   q            bf16 [*, 128]   query rows
  *   k, v         bf16 [rows,128] swizzled cache rows (layout above)
@@ -136,9 +141,9 @@ typedef struct fkv_work {
  * Nothing in the reference is replaced (it has no decode); its cost model of
  * this kernel is reference latency.py:85-91 (predict_compute). */
 int fkv_decode(const void* q, const void* k, const void* v, const fkv_work_t* work,
-               int32_t work_k, int32_t n_workers, int32_t n_items, int32_t group, float sm_scale,
-               float* part, int32_t* counters, void* out_bf16, float* out_rec, float* out_lse,
-               void* stream);
+               int32_t work_k, int32_t n_workers, int32_t n_items, int32_t group, int32_t flags,
+               float sm_scale, float* part, int32_t* counters, void* out_bf16, float* out_rec,
+               float* out_lse, void* stream);
 
 /* K5: log-sum-exp merge of partial records.  Output group g merges records
  * src_idx[grp_ptr[g] .. grp_ptr[g+1]) (each `group` heads of FKV_REC floats)
@@ -161,7 +166,7 @@ int fkv_merge_lse(const float* part, const int32_t* grp_ptr, const int32_t* src_
  * launches.  Replaces NCCL all_gather for the per-layer exchange. */
 int fkv_decode_exchange(const void* q, const void* k, const void* v, const fkv_work_t* work,
                         int32_t work_k, int32_t n_workers, int32_t n_items, int32_t group,
-                        float sm_scale, float* part, int32_t* counters, void* out_bf16,
+                        int32_t flags, float sm_scale, float* part, int32_t* counters, void* out_bf16,
                         float* const* out_recs, int32_t n_rec, float* out_lse, int32_t* sig_done,
                         int32_t* const* sig_flags, int32_t n_sig, int32_t my_rank, void* stream);
 

@@ -165,36 +165,76 @@ def plan_work(seg_len, n_workers: int, chunk: int | None = None,
 
 
 def work_table(seg_row0, seg_len, seg_qrow, seg_out_row, item_seg, t0, t1, seg_item_ptr,
-               warp_ptr, work_list) -> np.ndarray:
-    """The kernel-facing form of a schedule: fkv_work_t [busy, K, 8 x int32]
-    (include/fairkv.h) -- worker w's pieces in order, zero-filled (n_it = 0)
-    after its last piece, K = max pieces per worker (<= FKV_MAX_WORK)."""
+               warp_ptr, work_list, solo_ctas: int | None = None) -> np.ndarray:
+    """The kernel-facing form of a schedule: fkv_work_t [rows, K, 8 x int32]
+    (include/fairkv.h), zero-filled (n_it = 0) after each row's last piece,
+    K = max pieces per row (<= FKV_MAX_WORK).  Coop schedule: row = worker
+    = one CTA.  Solo schedule (``solo_ctas``): worker w is warp w // solo_ctas
+    of CTA w % solo_ctas, tagged in the high half of n_it."""
     seg_row0 = np.asarray(seg_row0, dtype=np.int64)
     seg_len = np.asarray(seg_len, dtype=np.int64)
     busy = len(warp_ptr) - 1
     counts = np.diff(warp_ptr)
-    K = max(1, int(counts.max()) if busy else 1)
-    if K > MAX_WORK_PER_WORKER:
-        raise ValueError(f"{K} pieces on one worker exceed FKV_MAX_WORK")
     n_it = np.diff(seg_item_ptr)
-    tab = np.zeros((max(busy, 1), K, 8), dtype=np.int32)
+    w = np.repeat(np.arange(busy), counts)
+    if solo_ctas:
+        rows = min(solo_ctas, max(busy, 1))
+        row_of, tag_of = w % rows, w // rows
+    else:
+        rows = max(busy, 1)
+        row_of, tag_of = w, np.zeros_like(w)
+    per_row = np.bincount(row_of, minlength=rows) if len(w) else np.zeros(rows, np.int64)
+    K = max(1, int(per_row.max()) if len(per_row) else 1)
+    if K > MAX_WORK_PER_WORKER:
+        raise ValueError(f"{K} pieces on one CTA exceed FKV_MAX_WORK")
+    tab = np.zeros((rows, K, 8), dtype=np.int32)
     if len(work_list):
         it = np.asarray(work_list, dtype=np.int64)
-        w = np.repeat(np.arange(busy), counts)
-        j = np.arange(len(it)) - np.repeat(warp_ptr[:-1], counts)
+        order = np.argsort(row_of, kind="stable")  # pieces of a row in worker order
+        j = np.empty(len(it), dtype=np.int64)
+        starts = np.concatenate([[0], np.cumsum(per_row)[:-1]])
+        j[order] = np.arange(len(it)) - np.repeat(starts, per_row)
         seg = np.asarray(item_seg, dtype=np.int64)[it]
         a = np.asarray(t0, dtype=np.int64)[it]
         b = np.minimum(np.asarray(t1, dtype=np.int64)[it], seg_len[seg])
         row0 = seg_row0[seg] + a
-        tab[w, j, 0] = (row0 & 0xFFFFFFFF).astype(np.uint32).view(np.int32)
-        tab[w, j, 1] = (row0 >> 32).astype(np.int32)
-        tab[w, j, 2] = np.maximum(b - a, 0)
-        tab[w, j, 3] = np.asarray(seg_qrow, dtype=np.int64)[seg]
-        tab[w, j, 4] = np.asarray(seg_out_row, dtype=np.int64)[seg]
-        tab[w, j, 5] = it
-        tab[w, j, 6] = np.asarray(seg_item_ptr, dtype=np.int64)[seg]
-        tab[w, j, 7] = n_it[seg]
+        tab[row_of, j, 0] = (row0 & 0xFFFFFFFF).astype(np.uint32).view(np.int32)
+        tab[row_of, j, 1] = (row0 >> 32).astype(np.int32)
+        tab[row_of, j, 2] = np.maximum(b - a, 0)
+        tab[row_of, j, 3] = np.asarray(seg_qrow, dtype=np.int64)[seg]
+        tab[row_of, j, 4] = np.asarray(seg_out_row, dtype=np.int64)[seg]
+        tab[row_of, j, 5] = it
+        tab[row_of, j, 6] = np.asarray(seg_item_ptr, dtype=np.int64)[seg]
+        tab[row_of, j, 7] = n_it[seg] | (tag_of << 16)
     return tab
+
+
+# K4 schedule choice: the per-warp ("solo") schedule when the cache is small
+# enough that the CTA-cooperative one would give each CTA few tiles
+# (FKV_K4_SCHEDULE = coop | solo | auto overrides, for measurements).
+SOLO_MAX_TILES_PER_CTA = 4  # measured crossover (tools/probe_sched.py): solo wins at <= 2-4 tiles per CTA
+SOLO_MIN_TILES = 2
+FKV_DECODE_SOLO = 1
+
+
+def plan_schedule(seg_len, seg_row0, seg_qrow, seg_out_row, device=None, chunk: int | None = None):
+    """-> (item_seg, t0, t1, seg_item_ptr, warp_ptr, work_list, table, flags)."""
+    import os
+    seg_len = np.asarray(seg_len, dtype=np.int64)
+    ctas = default_workers(device)
+    tiles = int(((seg_len + TILE - 1) // TILE).sum())
+    mode = os.environ.get("FKV_K4_SCHEDULE", "auto")
+    solo = mode == "solo" or (mode == "auto" and chunk is None and tiles <= SOLO_MAX_TILES_PER_CTA * ctas)
+    if solo:
+        try:
+            plan = plan_work(seg_len, 4 * ctas, chunk, min_tiles=SOLO_MIN_TILES)
+            tab = work_table(seg_row0, seg_len, seg_qrow, seg_out_row, *plan, solo_ctas=ctas)
+            return (*plan, tab, FKV_DECODE_SOLO)
+        except ValueError:
+            pass  # too many pieces for the per-CTA tables: cooperative schedule
+    plan = plan_work(seg_len, ctas, chunk)
+    tab = work_table(seg_row0, seg_len, seg_qrow, seg_out_row, *plan)
+    return (*plan, tab, 0)
 
 
 @dataclass
@@ -222,6 +262,10 @@ class LayerCache:
     @property
     def n_workers(self) -> int:
         return int(self.work.shape[0])
+
+    @property
+    def flags(self) -> int:
+        return int(self.host.get("flags", 0))
 
     @property
     def work_k(self) -> int:
@@ -285,8 +329,8 @@ class LayerCache:
     def _build(k, v, seg_row0, seg_len, seg_qrow, seg_out_row, group, chunk) -> "LayerCache":
         dev = k.device
         seg_row0 = np.asarray(seg_row0, dtype=np.int64)
-        item_seg, t0, t1, ptr, wptr, wlist = plan_work(seg_len, default_workers(dev), chunk)
-        tab = work_table(seg_row0, seg_len, seg_qrow, seg_out_row, item_seg, t0, t1, ptr, wptr, wlist)
+        item_seg, t0, t1, ptr, wptr, wlist, tab, flags = plan_schedule(seg_len, seg_row0, seg_qrow,
+                                                                       seg_out_row, dev, chunk)
 
         def i32(a):
             return torch.as_tensor(np.ascontiguousarray(a, dtype=np.int32), device=dev)
@@ -299,5 +343,6 @@ class LayerCache:
             warp_ptr=i32(wptr), work_list=i32(wlist), work=i32(tab),
             counters=torch.zeros(max(len(item_seg), 1), dtype=torch.int32, device=dev),
             host={"seg_len": seg_len, "seg_row0": seg_row0, "chunk": chunk, "n_workers": len(wptr) - 1,
-                  "seg_qrow": np.asarray(seg_qrow), "seg_out_row": np.asarray(seg_out_row)},
+                  "seg_qrow": np.asarray(seg_qrow), "seg_out_row": np.asarray(seg_out_row),
+                  "flags": flags},
         )

@@ -31,6 +31,8 @@
 #include <cuda_bf16.h>
 #include <math_constants.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace fkv {
@@ -141,14 +143,19 @@ __device__ __forceinline__ void stamp(int PROBE_, int i) {
     g_stamps[blockIdx.x * 16 + i] = t;
   }
 }
-template <int G, int PROBE = 0>
+// SOLO (small shards): every warp streams its own pieces start to finish and
+// finalises them itself -- no hand-over -- so a short schedule keeps four
+// independent tile streams per CTA; a piece's owner warp is n_it >> 16.
+template <int G, int PROBE = 0, bool SOLO = false>
 __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodeParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ DecodeShared sh;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  uint8_t* ring = smem + (kDedicated ? (warp > 0 ? warp - 1 : 0) : warp) * kStages * 2 * kTileBytes;
+  constexpr int NS = SOLO ? kSmemBytes / (kWarps * 2 * kTileBytes) : kStages;  // ring stages per warp
+  constexpr bool kCombiner = kDedicated && !SOLO;  // warp 0 only combines
+  uint8_t* ring = smem + (kCombiner ? (warp > 0 ? warp - 1 : 0) : warp) * NS * 2 * kTileBytes;
   uint64_t* wbars = sh.bars[warp];
   const fkv_work_t* tab = sh.tab;
   if (PROBE == 3 && threadIdx.x == 0) {
@@ -171,7 +178,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodePara
     }
   }
   if (lane == 0) {
-    for (int s = 0; s < kStages; ++s) mbar_init(&wbars[s], 1);
+    for (int s = 0; s < NS; ++s) mbar_init(&wbars[s], 1);
     fence_mbar_init();
   }
   if (threadIdx.x == 0) sh.fin_n_it = 0;
@@ -179,28 +186,39 @@ __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodePara
 
   // ---- producer: this warp's rounds (two tiles each) of every piece, in the
   // CTA-wide round numbering (first_round / next_round)
+  auto mine = [&](int pc) { return !SOLO || (tab[pc].n_it >> 16) == warp; };
   int p_pc = 0, p_G = 0, p_half = 0;  // piece, its first round, tile of the round
-  int p_r = first_round(warp, 0);     // next owned round
+  int p_r = SOLO ? 0 : first_round(warp, 0);  // next owned round (SOLO: round within the piece)
   uint32_t p_seq = 0, c_seq = 0;
   int p_s = 0;
-  bool p_done = kDedicated && warp == 0;  // the combiner warp streams nothing
+  bool p_done = kCombiner && warp == 0;  // the combiner warp streams nothing
   auto refill = [&]() {
-    while (!p_done && p_seq - c_seq < static_cast<uint32_t>(kStages)) {
+    while (!p_done && p_seq - c_seq < static_cast<uint32_t>(NS)) {
       if (p_pc >= FKV_MAX_WORK || tab[p_pc].n_it == 0) {
         p_done = true;
         break;
       }
+      if (SOLO && !mine(p_pc)) {
+        ++p_pc;
+        continue;
+      }
       const int nt = piece_tiles(tab[p_pc]);
       const int nr = (nt + 1) >> 1;
-      if (p_r >= p_G + nr) {
+      if (SOLO && p_r >= nr) {
+        ++p_pc;
+        p_r = 0;
+        p_half = 0;
+        continue;
+      }
+      if (!SOLO && p_r >= p_G + nr) {
         p_G += nr;
         ++p_pc;
         p_half = 0;
         continue;
       }
-      const int tile = 2 * (p_r - p_G) + p_half;
+      const int tile = 2 * (SOLO ? p_r : p_r - p_G) + p_half;
       if (tile >= nt) {  // odd tail: one-tile round
-        p_r = next_round(warp, p_r);
+        p_r = SOLO ? p_r + 1 : next_round(warp, p_r);
         p_half = 0;
         continue;
       }
@@ -214,10 +232,10 @@ __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodePara
         bulk_g2s(dst + kTileBytes, p.v + row * FKV_HEAD_DIM, kTileBytes, &wbars[p_s]);
       }
       ++p_seq;
-      if (++p_s == kStages) p_s = 0;
+      if (++p_s == NS) p_s = 0;
       if (++p_half == 2) {
         p_half = 0;
-        p_r = next_round(warp, p_r);
+        p_r = SOLO ? p_r + 1 : next_round(warp, p_r);
       }
     }
   };
@@ -229,8 +247,13 @@ __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodePara
   const bool fused = p.out_bf16 || p.n_rec > 0 || p.out_lse;
 
   uint32_t qn[8][2];  // q fragments of the next piece, loaded one piece ahead
+  auto next_mine = [&](int pc) {
+    while (SOLO && pc < FKV_MAX_WORK && tab[pc].n_it != 0 && !mine(pc)) ++pc;
+    return pc;
+  };
   auto load_q = [&](int pc) {
     const int n = lane >> 2, kq = 2 * (lane & 3);
+    pc = next_mine(pc);
     if (pc < FKV_MAX_WORK && tab[pc].n_it != 0 && n < G) {
       const __nv_bfloat16* qr = p.q + static_cast<int64_t>(tab[pc].qrow + n) * FKV_HEAD_DIM;
 #pragma unroll
@@ -251,17 +274,20 @@ __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodePara
   asm volatile("griddepcontrol.launch_dependents;");
   load_q(0);
   if (warp == 0) stamp(PROBE, 1);
-  if (warp == 0) named_arrive(1);  // the hand-over slot starts free
+  if (!SOLO && warp == 0) named_arrive(1);  // the hand-over slot starts free
 
   int c_s = 0;        // consumer stage
   uint32_t c_ph = 0;  // its mbarrier phase parity
   int G0 = 0;         // first round of the current piece
-  int c_r = first_round(warp, 0);  // next owned round
+  int c_r = SOLO ? 0 : first_round(warp, 0);  // next owned round
   for (int pc = 0; pc < FKV_MAX_WORK; ++pc) {
-    const fkv_work_t d = tab[pc];
+    fkv_work_t d = tab[pc];
     if (d.n_it == 0) break;
+    if (SOLO && !mine(pc)) continue;
+    d.n_it &= 0xffff;
     const int nt = piece_tiles(d);
     const int nr = (nt + 1) >> 1;
+    if (SOLO) c_r = G0;  // every round of an owned piece
 
     // Q^T (B operand: k = head_dim, n = query head) was prefetched into qn
     uint32_t qb[8][2];
@@ -279,15 +305,15 @@ __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodePara
 
     // this warp's rounds of the piece: two independent S chains per round, one
     // softmax max/shuffle/rescale step and one ring hand-back per 32 tokens
-    for (; c_r < G0 + nr; c_r = next_round(warp, c_r)) {
+    for (; c_r < G0 + nr; c_r = SOLO ? c_r + 1 : next_round(warp, c_r)) {
       const int i = 2 * (c_r - G0);
       const bool two = i + 1 < nt;
       const int sA = c_s;
       const uint32_t phA = c_ph;
-      if (++c_s == kStages) c_s = 0, c_ph ^= 1u;
+      if (++c_s == NS) c_s = 0, c_ph ^= 1u;
       const int sB = c_s;
       const uint32_t phB = c_ph;
-      if (two && ++c_s == kStages) c_s = 0, c_ph ^= 1u;
+      if (two && ++c_s == NS) c_s = 0, c_ph ^= 1u;
       mbar_wait(&wbars[sA], phA);
       if (two) mbar_wait(&wbars[sB], phB);
       if (warp == 0 && pc == 0) stamp(PROBE, 2);
@@ -393,7 +419,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodePara
 
     // ---- hand the piece state to warp 0 (shared memory, named barriers):
     // bar 1 = slot free (warp 0 finished the previous piece), bar 2 = slot full
-    if (warp != 0) {
+    if (!SOLO && warp != 0) {
       named_sync(1);
       float* x = &sh.xch[warp - 1][0][lane];
       x[0 * 32] = m0;
@@ -408,11 +434,11 @@ __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodePara
       continue;
     }
     stamp(PROBE, 3);
-    named_sync(2);
+    if (!SOLO) named_sync(2);
     stamp(PROBE, 4);
     // warp 0: lane-wise online-softmax combine of the four warps' states
 #pragma unroll 1
-    for (int w = 0; w < kWarps - 1; ++w) {
+    for (int w = 0; w < (SOLO ? 0 : kWarps - 1); ++w) {
       const float* x = &sh.xch[w][0][lane];
       const float om0 = x[0], om1 = x[32], ol0 = x[64], ol1 = x[96];
       const float nm0 = fmaxf(m0, om0), nm1 = fmaxf(m1, om1);
@@ -432,7 +458,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodePara
         acc[dt][3] = acc[dt][3] * a1 + x[(4 + 4 * dt + 3) * 32] * b1;
       }
     }
-    if (more) named_arrive(1);  // slot free for the next piece
+    if (!SOLO && more) named_arrive(1);  // slot free for the next piece
 
     // ---- finalise this piece from registers (warp 0)
 #pragma unroll
@@ -514,7 +540,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodePara
     if (lane == 0) last = atom_add_acq_rel(p.counters + d.i0, 1) == n_it - 1;
     last = __shfl_sync(0xffffffffu, last, 0);
     stamp(PROBE, 7);
-    if (kDedicated && last && !more) {
+    if (kCombiner && last && !more) {
       // the CTA's last piece: warps 1-3 are idle, merge with all four (below)
       if (lane == 0) sh.fin_i0 = d.i0, sh.fin_n_it = n_it, sh.fin_orow = static_cast<int32_t>(orow);
       continue;
@@ -524,7 +550,8 @@ __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodePara
     // shared scratch, then every lane streams its 4 head_dim columns of all
     // records with n_it*G independent 16-B loads (L2: .cg, never a stale L1 line).
     const float* base = p.part + static_cast<int64_t>(d.i0) * G * FKV_REC;
-    float* sw = sh.scratch;
+    // SOLO: any warp may merge -- per-warp weights in the (unused) hand-over area
+    float* sw = SOLO ? &sh.xch[0][0][0] + warp * kMergeMax * 8 : sh.scratch;
     for (int x = lane; x < n_it * G; x += 32) sw[x] = __ldcg(base + x * FKV_REC + FKV_HEAD_DIM);
     __syncwarp();
     stamp(PROBE, 8);
@@ -579,7 +606,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodePara
     __syncwarp();  // the scratch is reused by the next merge
   }
 
-  if (kDedicated) {
+  if (kCombiner) {
     // Deferred merge of the segment the CTA's last piece completed: the four
     // warps split the G heads, each lane loads its columns of every piece's
     // record together with the lse values (one L2 round trip), weights by
@@ -644,7 +671,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodePara
   if (warp == 0) stamp(PROBE, 5);
   // Fused all-gather completion: the last CTA out publishes this rank's
   // records to every peer by bumping its flag there (system-scope release).
-  if (p.n_sig > 0 && kDedicated) {
+  if (p.n_sig > 0 && (kCombiner || SOLO)) {
     __threadfence_system();  // every warp may have written peer records (merge above)
     named_sync(3);
   }
@@ -731,11 +758,11 @@ __global__ void __launch_bounds__(G * 32)
   }
 }
 
-template <int G, int PROBE = 0>
+template <int G, int PROBE = 0, bool SOLO = false>
 int launch_decode(const DecodeParams& p, cudaStream_t st) {
   static int grid_cap = 0;  // 2 persistent CTAs per SM
   if (!grid_cap) {
-    if (int rc = cuda_check(cudaFuncSetAttribute(decode_kernel<G, PROBE>,
+    if (int rc = cuda_check(cudaFuncSetAttribute(decode_kernel<G, PROBE, SOLO>,
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  kSmemBytes),
                             "decode smem attribute"))
@@ -743,7 +770,7 @@ int launch_decode(const DecodeParams& p, cudaStream_t st) {
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_kernel<G, PROBE>, kWarps * 32,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_kernel<G, PROBE, SOLO>, kWarps * 32,
                                                   kSmemBytes);
     grid_cap = sms * (per_sm > 0 ? per_sm : 1);
   }
@@ -759,9 +786,10 @@ int launch_decode(const DecodeParams& p, cudaStream_t st) {
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL (see kernel)
   attr[0].val.programmaticStreamSerializationAllowed = 1;
+  static const bool no_pdl = getenv("FKV_NO_PDL") != nullptr;  // diagnostics
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cuda_check(cudaLaunchKernelEx(&cfg, decode_kernel<G, PROBE>, p), "decode launch");
+  cfg.numAttrs = no_pdl ? 0 : 1;
+  return cuda_check(cudaLaunchKernelEx(&cfg, decode_kernel<G, PROBE, SOLO>, p), "decode launch");
 }
 
 }  // namespace
@@ -769,7 +797,14 @@ int launch_decode(const DecodeParams& p, cudaStream_t st) {
 
 namespace fkv {
 namespace {
-int decode_entry(DecodeParams& p, int group, cudaStream_t st, int probe = 0) {
+int decode_entry(DecodeParams& p, int group, cudaStream_t st, int probe = 0, bool solo = false) {
+  if (solo) {
+    switch (group) {
+      case 4: return launch_decode<4, 0, true>(p, st);
+      case 8: return probe == 3 ? launch_decode<8, 3, true>(p, st) : launch_decode<8, 0, true>(p, st);
+      default: return set_error(FKV_ERR_INVALID, "fkv_decode: group must be 4 or 8");
+    }
+  }
   if (probe == 1) return group == 8 ? launch_decode<8, 1>(p, st) : set_error(FKV_ERR_INVALID, "probe: G=8");
   if (probe == 2) return group == 8 ? launch_decode<8, 2>(p, st) : set_error(FKV_ERR_INVALID, "probe: G=8");
   if (probe == 3) return group == 8 ? launch_decode<8, 3>(p, st) : set_error(FKV_ERR_INVALID, "probe: G=8");
@@ -798,16 +833,17 @@ extern "C" int fkv__decode_stamps(unsigned long long* host, int32_t n) {
 
 extern "C" int fkv_decode(const void* q, const void* k, const void* v, const fkv_work_t* work,
                           int32_t work_k, int32_t n_workers, int32_t n_items, int32_t group,
-                          float sm_scale, float* part, int32_t* counters, void* out_bf16,
-                          float* out_rec, float* out_lse, void* stream) {
-  return fkv_decode_exchange(q, k, v, work, work_k, n_workers, n_items, group, sm_scale, part,
+                          int32_t flags, float sm_scale, float* part, int32_t* counters,
+                          void* out_bf16, float* out_rec, float* out_lse, void* stream) {
+  return fkv_decode_exchange(q, k, v, work, work_k, n_workers, n_items, group, flags, sm_scale, part,
                              counters, out_bf16, out_rec ? &out_rec : nullptr, out_rec ? 1 : 0,
                              out_lse, nullptr, nullptr, 0, 0, stream);
 }
 
 extern "C" int fkv_decode_exchange(const void* q, const void* k, const void* v,
                                    const fkv_work_t* work, int32_t work_k, int32_t n_workers,
-                                   int32_t n_items, int32_t group, float sm_scale, float* part,
+                                   int32_t n_items, int32_t group, int32_t flags, float sm_scale,
+                                   float* part,
                                    int32_t* counters, void* out_bf16, float* const* out_recs,
                                    int32_t n_rec, float* out_lse, int32_t* sig_done,
                                    int32_t* const* sig_flags, int32_t n_sig, int32_t my_rank,
@@ -845,7 +881,7 @@ extern "C" int fkv_decode_exchange(const void* q, const void* k, const void* v,
   p.my_rank = my_rank;
   const int probe = g_probe;
   g_probe = 0;
-  return decode_entry(p, group, static_cast<cudaStream_t>(stream), probe);
+  return decode_entry(p, group, static_cast<cudaStream_t>(stream), probe, (flags & FKV_DECODE_SOLO) != 0);
 }
 
 extern "C" int fkv_merge_lse(const float* part, const int32_t* grp_ptr, const int32_t* src_idx,

@@ -63,7 +63,7 @@ def _decode(q, cache: LayerCache, ws: DecodeWorkspace | None, sm_scale, out_bf16
     scale = 1.0 / math.sqrt(HEAD_DIM) if sm_scale is None else sm_scale
     _native.check(_lib.fkv_decode(
         q.data_ptr(), cache.k.data_ptr(), cache.v.data_ptr(), cache.work.data_ptr(), cache.work_k,
-        cache.n_workers, cache.n_items, cache.group, scale, ws.part.data_ptr(),
+        cache.n_workers, cache.n_items, cache.group, cache.flags, scale, ws.part.data_ptr(),
         cache.counters.data_ptr(), _p(out_bf16), _p(out_rec), _p(out_lse), _stream()))
     return ws.part
 
@@ -99,7 +99,7 @@ def decode_exchange(q: torch.Tensor, cache: LayerCache, endpoint, parity: int,
     flags = (C.c_void_p * len(endpoint.peer_flags))(*endpoint.peer_flags)
     _native.check(_lib.fkv_decode_exchange(
         q.data_ptr(), cache.k.data_ptr(), cache.v.data_ptr(), cache.work.data_ptr(), cache.work_k,
-        cache.n_workers, cache.n_items, cache.group, scale, ws.part.data_ptr(),
+        cache.n_workers, cache.n_items, cache.group, cache.flags, scale, ws.part.data_ptr(),
         cache.counters.data_ptr(), None, recs, len(dests), None, endpoint.sig_done, flags,
         len(endpoint.peer_flags), endpoint.rank, _stream()))
 

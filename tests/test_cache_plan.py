@@ -78,3 +78,29 @@ def test_balanced_plan_equalises_tiles_per_worker():
 def test_segment_offsets_page_aligned():
     row0, total = segment_offsets([0, 1, 64, 65])
     assert row0.tolist() == [0, 0, 64, 128] and total == 256
+
+
+def test_solo_work_table_tags_warps():
+    """Per-warp schedule: worker w -> warp w // ctas of CTA w % ctas, tagged
+    in the high half of n_it; every piece appears once."""
+    from paper_2502_15804_b200.cache import work_table
+    rng = np.random.default_rng(4)
+    seg_len = rng.integers(16, 300, size=64)
+    row0, _ = segment_offsets(seg_len)
+    qrow = np.arange(64) * 8
+    ctas = 296
+    item_seg, t0, t1, sptr, wptr, wlist = plan_work(seg_len, 4 * ctas, min_tiles=2)
+    tab = work_table(row0, seg_len, qrow, qrow, item_seg, t0, t1, sptr, wptr, wlist, solo_ctas=ctas)
+    busy = len(wptr) - 1
+    assert tab.shape[0] == min(ctas, busy)
+    seen = []
+    for c in range(tab.shape[0]):
+        for e in tab[c]:
+            if e[7] == 0:
+                continue
+            w = (e[7] >> 16) * tab.shape[0] + c
+            it = int(e[5])
+            assert wptr[w] <= list(wlist).index(it) < wptr[w + 1]
+            assert (e[7] & 0xffff) == sptr[item_seg[it] + 1] - sptr[item_seg[it]]
+            seen.append(it)
+    assert sorted(seen) == list(range(len(item_seg)))

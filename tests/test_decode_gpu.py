@@ -42,8 +42,12 @@ def build_cache(seg_lens, group, hkv, bt, device, seed=0, chunk=None):
 
 @pytest.mark.parametrize("group", [8, 4])
 @pytest.mark.parametrize("chunk", [None, 64, 128])
-def test_decode_matches_oracle(cuda_device, group, chunk):
+@pytest.mark.parametrize("schedule", ["auto", "coop", "solo"])
+def test_decode_matches_oracle(cuda_device, group, chunk, schedule, monkeypatch):
+    """Both K4 schedules (CTA-cooperative pieces / per-warp pieces) and the
+    host's automatic choice."""
     from paper_2502_15804_b200 import ops
+    monkeypatch.setenv("FKV_K4_SCHEDULE", schedule)
     rng = np.random.default_rng(group * 100 + (chunk or 0))
     hkv, bt = 8, 3
     seg_lens = rng.integers(1, 700, size=bt * hkv).tolist()
@@ -53,6 +57,26 @@ def test_decode_matches_oracle(cuda_device, group, chunk):
     seg_lens[3] = 64
     seg_lens[4] = 65
     cache, q, ks, vs = build_cache(seg_lens, group, hkv, bt, cuda_device, chunk=chunk)
+    if schedule != "auto" and chunk is None:
+        assert cache.flags == (1 if schedule == "solo" else 0)
+    o, lse = ops.decode(q.to(cuda_device), cache)
+    torch.cuda.synchronize()
+    o_ref, lse_ref = okv.decode_heads(q.float().numpy().astype(np.float64), ks, vs, group)
+    torch.testing.assert_close(o.float().cpu().double(), torch.from_numpy(o_ref), rtol=2e-2, atol=1e-2)
+    torch.testing.assert_close(lse.cpu().double(), torch.from_numpy(lse_ref), rtol=0, atol=2e-3)
+
+
+@pytest.mark.parametrize("schedule", ["coop", "solo"])
+def test_decode_many_segments_split(cuda_device, schedule, monkeypatch):
+    """Many long segments: pieces split across CTAs / warps, merged by the
+    fused K5 (several pieces per segment, the last CTA's cooperative merge)."""
+    from paper_2502_15804_b200 import ops
+    monkeypatch.setenv("FKV_K4_SCHEDULE", schedule)
+    rng = np.random.default_rng(11)
+    hkv, bt, group = 8, 8, 8
+    seg_lens = rng.integers(900, 2600, size=bt * hkv).tolist()
+    cache, q, ks, vs = build_cache(seg_lens, group, hkv, bt, cuda_device, seed=5)
+    assert int(np.diff(cache.grp_ptr.cpu().numpy()).max()) > 1  # some segments are split
     o, lse = ops.decode(q.to(cuda_device), cache)
     torch.cuda.synchronize()
     o_ref, lse_ref = okv.decode_heads(q.float().numpy().astype(np.float64), ks, vs, group)

@@ -1,3 +1,3 @@
-timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-python tools/probe_shard.py 2>&1 | grep default
-python tools/probe_timeline.py 2>&1 | grep -E "^tp|CTAs with"
+python tools/probe_floor.py
+echo "--- no PDL"; FKV_NO_PDL=1 python tools/probe_floor.py
+echo "--- coop"; FKV_K4_SCHEDULE=coop python tools/probe_floor.py
