@@ -314,8 +314,13 @@ def run_fairkv(args):
     qh.copy_(q)
     oh = torch.empty(o.shape, dtype=o.dtype, pin_memory=True)
     s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
-    cg = 8  # layers per copy (fewer, larger PCIe transfers; compute waits per group)
-    groups = [(a, min(a + cg, args.layers)) for a in range(0, args.layers, cg)]
+    # layers per copy: large groups in the middle (fewer, larger PCIe
+    # transfers), a single layer first and last so that only one layer's H2D
+    # and one layer's D2H are exposed outside the compute
+    cg = 8
+    cuts = sorted({0, min(1, args.layers), max(args.layers - 1, 0), args.layers,
+                   *range(1, args.layers - 1, cg)})
+    groups = [(a, b) for a, b in zip(cuts, cuts[1:]) if b > a]
     ev_in = [torch.cuda.Event() for _ in groups]
     ev_out = [torch.cuda.Event() for _ in groups]
 
