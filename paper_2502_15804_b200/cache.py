@@ -209,11 +209,61 @@ def work_table(seg_row0, seg_len, seg_qrow, seg_out_row, item_seg, t0, t1, seg_i
     return tab
 
 
+def plan_work_solo(seg_len, n_workers: int, piece_tiles: int = 16, whole_tiles: int = 24):
+    """Segment-aligned per-warp schedule for small caches: a segment of at
+    most ``whole_tiles`` tiles stays one piece (no LSE merge); longer ones are
+    cut into near-equal 16-token-aligned pieces of about
+    max(piece_tiles, total / n_workers) tiles; pieces go to workers one each
+    while they last, else largest-first onto the least-loaded worker.  Same
+    return convention as ``plan_work``."""
+    import heapq
+    seg_len = np.asarray(seg_len, dtype=np.int64)
+    n_seg = len(seg_len)
+    tiles = (seg_len + TILE - 1) // TILE
+    W = max(1, int(n_workers))
+    total = int(tiles.sum())
+    piece = max(int(piece_tiles), -(-total // W), 1)
+    seg_i, t0s, t1s = [], [], []
+    for s in range(n_seg):
+        n = int(tiles[s])
+        k = 1 if n <= whole_tiles else min(MAX_ITEMS_PER_SEGMENT, -(-n // piece))
+        cuts = [round(j * n / k) for j in range(k + 1)]
+        for j in range(k):
+            seg_i.append(s)
+            t0s.append(cuts[j] * TILE)
+            t1s.append(min(int(seg_len[s]), cuts[j + 1] * TILE))
+    item_seg = np.asarray(seg_i, dtype=np.int32)
+    t0 = np.asarray(t0s, dtype=np.int32)
+    t1 = np.asarray(t1s, dtype=np.int32)
+    n_items = len(item_seg)
+    if n_items <= W:
+        owner = np.arange(n_items, dtype=np.int64)
+    else:
+        size = np.maximum(t1.astype(np.int64) - t0, 0)
+        owner = np.empty(n_items, dtype=np.int64)
+        heap = [(0, w) for w in range(W)]
+        for i in np.lexsort((np.arange(n_items), -size)):
+            load, w = heapq.heappop(heap)
+            owner[i] = w
+            heapq.heappush(heap, (load + int(size[i]) + 1, w))
+        if np.bincount(owner, minlength=W).max() > MAX_WORK_PER_WORKER:
+            raise ValueError("too many pieces for the per-warp schedule")
+        # renumber workers by first piece so owners are 0..busy-1
+        _, owner = np.unique(owner, return_inverse=True)
+    seg_item_ptr = np.zeros(n_seg + 1, dtype=np.int32)
+    seg_item_ptr[1:] = np.cumsum(np.bincount(item_seg, minlength=n_seg))
+    busy = int(owner.max()) + 1 if n_items else 1
+    warp_ptr = np.zeros(busy + 1, dtype=np.int32)
+    warp_ptr[1:] = np.cumsum(np.bincount(owner, minlength=busy))
+    split = (np.diff(seg_item_ptr) > 1)[item_seg]
+    work_list = np.lexsort((np.arange(n_items), ~split, owner)).astype(np.int32)
+    return item_seg, t0, t1, seg_item_ptr, warp_ptr, work_list
+
+
 # K4 schedule choice: the per-warp ("solo") schedule when the cache is small
 # enough that the CTA-cooperative one would give each CTA few tiles
 # (FKV_K4_SCHEDULE = coop | solo | auto overrides, for measurements).
-SOLO_MAX_TILES_PER_CTA = 4  # measured crossover (tools/probe_sched.py): solo wins at <= 2-4 tiles per CTA
-SOLO_MIN_TILES = 2
+SOLO_MAX_TILES_PER_CTA = 19  # measured crossover (tools/probe_solo_params.py, probe_sched.py): ~5600 tiles per GPU-layer
 FKV_DECODE_SOLO = 1
 
 
@@ -226,8 +276,12 @@ def plan_schedule(seg_len, seg_row0, seg_qrow, seg_out_row, device=None, chunk: 
     mode = os.environ.get("FKV_K4_SCHEDULE", "auto")
     solo = mode == "solo" or (mode == "auto" and chunk is None and tiles <= SOLO_MAX_TILES_PER_CTA * ctas)
     if solo:
+        # piece / whole-segment thresholds grow with the cache: 4 tiles for a
+        # few hundred tiles per GPU-layer, 8 near the crossover (probe_solo_params)
+        pt = int(np.clip(round(1.5 * tiles / (4 * ctas)), 4, 8))
         try:
-            plan = plan_work(seg_len, 4 * ctas, chunk, min_tiles=SOLO_MIN_TILES)
+            plan = plan_work_solo(seg_len, 4 * ctas, int(os.environ.get("FKV_SOLO_PIECE", pt)),
+                                  int(os.environ.get("FKV_SOLO_WHOLE", pt)))
             tab = work_table(seg_row0, seg_len, seg_qrow, seg_out_row, *plan, solo_ctas=ctas)
             return (*plan, tab, FKV_DECODE_SOLO)
         except ValueError:

@@ -801,7 +801,13 @@ int decode_entry(DecodeParams& p, int group, cudaStream_t st, int probe = 0, boo
   if (solo) {
     switch (group) {
       case 4: return launch_decode<4, 0, true>(p, st);
-      case 8: return probe == 3 ? launch_decode<8, 3, true>(p, st) : launch_decode<8, 0, true>(p, st);
+      case 8:
+        switch (probe) {
+          case 1: return launch_decode<8, 1, true>(p, st);
+          case 2: return launch_decode<8, 2, true>(p, st);
+          case 3: return launch_decode<8, 3, true>(p, st);
+          default: return launch_decode<8, 0, true>(p, st);
+        }
       default: return set_error(FKV_ERR_INVALID, "fkv_decode: group must be 4 or 8");
     }
   }

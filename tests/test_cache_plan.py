@@ -80,6 +80,33 @@ def test_segment_offsets_page_aligned():
     assert row0.tolist() == [0, 0, 64, 128] and total == 256
 
 
+def _check_plan(seg_len, item_seg, t0, t1, sptr, wptr, wlist):
+    assert sorted(wlist.tolist()) == list(range(len(item_seg)))
+    assert (t0 % 16 == 0).all() and np.diff(wptr).max() <= MAX_WORK_PER_WORKER
+    for s in range(len(seg_len)):
+        its = range(sptr[s], sptr[s + 1])
+        assert 1 <= len(its) <= MAX_ITEMS_PER_SEGMENT and all(item_seg[i] == s for i in its)
+        spans = [(t0[i], t1[i]) for i in its]
+        assert spans[0][0] == 0 and spans[-1][1] == seg_len[s]
+        assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+
+
+@pytest.mark.parametrize("workers", [8, 64, 1184])
+def test_solo_plan_segment_aligned(workers):
+    """Per-warp planner: short segments stay whole (no merge), long ones are
+    cut into near-equal pieces; every piece on one worker."""
+    from paper_2502_15804_b200.cache import plan_work_solo
+    rng = np.random.default_rng(workers)
+    seg_len = np.concatenate([rng.integers(0, 384, size=200), rng.integers(2000, 9000, size=20)])
+    item_seg, t0, t1, sptr, wptr, wlist = plan_work_solo(seg_len, workers)
+    _check_plan(seg_len, item_seg, t0, t1, sptr, wptr, wlist)
+    n_pieces = np.diff(sptr)
+    assert (n_pieces[seg_len <= 24 * 16] == 1).all()
+    if workers == 1184:  # enough workers: long segments are spread
+        assert (n_pieces[seg_len >= 2000] > 1).all()
+    assert len(wptr) - 1 <= workers
+
+
 def test_solo_work_table_tags_warps():
     """Per-warp schedule: worker w -> warp w // ctas of CTA w % ctas, tagged
     in the high half of n_it; every piece appears once."""
@@ -90,6 +117,7 @@ def test_solo_work_table_tags_warps():
     qrow = np.arange(64) * 8
     ctas = 296
     item_seg, t0, t1, sptr, wptr, wlist = plan_work(seg_len, 4 * ctas, min_tiles=2)
+    _check_plan(seg_len, item_seg, t0, t1, sptr, wptr, wlist)
     tab = work_table(row0, seg_len, qrow, qrow, item_seg, t0, t1, sptr, wptr, wlist, solo_ctas=ctas)
     busy = len(wptr) - 1
     assert tab.shape[0] == min(ctas, busy)

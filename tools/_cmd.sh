@@ -1,3 +1,3 @@
-python tools/probe_floor.py
-echo "--- no PDL"; FKV_NO_PDL=1 python tools/probe_floor.py
-echo "--- coop"; FKV_K4_SCHEDULE=coop python tools/probe_floor.py
+FKV_K4_SCHEDULE=solo timeout 600 python -m pytest tests/test_decode_gpu.py tests/test_exchange_gpu.py -x -q 2>&1 | tail -2
+python tools/probe_small.py 2>&1 | grep solo
+python tools/probe_sched.py 512 1024
