@@ -399,6 +399,7 @@ def run_fairkv(args):
         del caches, dec
         torch.cuda.empty_cache()
         out["emulated_tp_budget_sweep"] = budget_sweep(args, dev)
+        out["cfg2_llama3.1-8b_b256_T16k"] = cfg2_sweep(args, dev, peak)
     if rank == 0 and world == 1 and not args.no_cpu:
         out["planner"] = planner_compare(budgets)
     if rank == 0 and world == 1 and not args.no_emulate:
@@ -499,6 +500,44 @@ def emulate_tp(args, budgets, dev, calibrate=True):
                        "GPU); tokens_per_s_bracketed = without the correction; sim = reference simulator, "
                        "pure-cache latency model")
     return results
+
+
+def cfg2_sweep(args, dev, peak):
+    """BASELINE configs[1]: Llama-3.1-8B shape (32 layers, 32Q/8KV heads, G=4),
+    Ada budget 256 (w=32, alpha=0.2, dirichlet skew), decode on one GPU,
+    batch sweep 1-256: tokens/s and K4 GB/s vs HBM peak."""
+    import numpy as np
+    import torch
+    from paper_2502_15804_b200 import ops
+    from paper_2502_15804_b200.cache import LayerCache
+    from paper_2502_15804_b200.sharding import synthetic_budgets
+    L, hq, hkv, G, B = 32, 32, 8, 4, 256
+    rows = {}
+    for bt in (1, 16, 64, 256):
+        budgets = synthetic_budgets(L, bt, hkv, B, window=WINDOW, alpha=ALPHA, seed=args.seed, context=16384)
+        qrow = np.array([b * hq + h * G for b in range(bt) for h in range(hkv)])
+        gen = torch.Generator(device=dev).manual_seed(11)
+        caches = [LayerCache.allocate(budgets[l].reshape(-1), qrow, qrow, G, dev, fill="random", generator=gen)
+                  for l in range(L)]
+        q = torch.randn((L, bt, hq, HEAD_DIM), device=dev).to(torch.bfloat16)
+        o = torch.empty_like(q)
+        wss = [ops.DecodeWorkspace(c) for c in caches]
+
+        def step():
+            for l in range(L):
+                ops.decode_into(q[l], caches[l], wss[l], out_bf16=o[l])
+        g = capture(step)
+        for _ in range(3):
+            g.replay()
+        t = timed(g.replay, 10) / 10
+        kv = sum(c.kv_bytes() for c in caches)
+        rows[f"batch{bt}"] = {"tokens_per_s": bt / t, "ms_per_step": t * 1e3,
+                              "kv_GBs": kv / t / 1e9, "hbm_frac": kv / t / 1e9 / peak,
+                              "kv_MB_per_step": kv / 1e6,
+                              "schedule": "solo" if caches[0].flags else "coop"}
+        del g, caches, wss
+        torch.cuda.empty_cache()
+    return rows
 
 
 def budget_sweep(args, dev):

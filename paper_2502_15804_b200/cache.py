@@ -268,20 +268,41 @@ FKV_DECODE_SOLO = 1
 
 
 def plan_schedule(seg_len, seg_row0, seg_qrow, seg_out_row, device=None, chunk: int | None = None):
-    """-> (item_seg, t0, t1, seg_item_ptr, warp_ptr, work_list, table, flags)."""
+    """Pick the K4 schedule for one cache and build its work table.
+
+    * small caches (<= SOLO_MAX_TILES_PER_CTA tiles per CTA): per-warp pieces
+      of 4-8 tiles (the launch floor and per-piece latency dominate; short
+      per-warp chains win);
+    * many short segments (>= 0.4 per warp, mean <= 24 tiles): per-warp,
+      segments up to max(16, 2 x the per-warp share) kept whole and packed
+      largest-first, longer ones split -- balanced with few LSE merges
+      (Llama-3.1-8B shape at batch 64-256: 93 % of HBM at batch 256);
+    * otherwise the CTA-cooperative schedule (few long segments: 70B shape).
+    FKV_K4_SCHEDULE = coop | solo | auto overrides (measurements).
+    -> (item_seg, t0, t1, seg_item_ptr, warp_ptr, work_list, table, flags)."""
     import os
     seg_len = np.asarray(seg_len, dtype=np.int64)
     ctas = default_workers(device)
-    tiles = int(((seg_len + TILE - 1) // TILE).sum())
+    seg_tiles = (seg_len + TILE - 1) // TILE
+    tiles = int(seg_tiles.sum())
+    n_seg = len(seg_len)
     mode = os.environ.get("FKV_K4_SCHEDULE", "auto")
-    solo = mode == "solo" or (mode == "auto" and chunk is None and tiles <= SOLO_MAX_TILES_PER_CTA * ctas)
+    small = tiles <= SOLO_MAX_TILES_PER_CTA * ctas
+    many_short = n_seg >= 0.4 * 4 * ctas and n_seg and tiles / n_seg <= 24
+    solo = mode == "solo" or (mode == "auto" and chunk is None and (small or many_short))
     if solo:
-        # piece / whole-segment thresholds grow with the cache: 4 tiles for a
-        # few hundred tiles per GPU-layer, 8 near the crossover (probe_solo_params)
-        pt = int(np.clip(round(1.5 * tiles / (4 * ctas)), 4, 8))
+        if small or mode == "solo" and not many_short:
+            # piece / whole-segment thresholds grow with the cache: 4 tiles for a
+            # few hundred tiles per GPU-layer, 8 near the crossover (probe_solo_params)
+            pt = wt = int(np.clip(round(1.5 * tiles / (4 * ctas)), 4, 8))
+        else:
+            # pieces of at least 16 tiles, at least twice the per-warp share:
+            # most segments stay whole, only the long tail is split
+            pt = wt = max(16, -(-2 * tiles // (4 * ctas)))
+        pt = int(os.environ.get("FKV_SOLO_PIECE", pt))
+        wt = int(os.environ.get("FKV_SOLO_WHOLE", wt))
         try:
-            plan = plan_work_solo(seg_len, 4 * ctas, int(os.environ.get("FKV_SOLO_PIECE", pt)),
-                                  int(os.environ.get("FKV_SOLO_WHOLE", pt)))
+            plan = plan_work_solo(seg_len, 4 * ctas, pt, wt)
             tab = work_table(seg_row0, seg_len, seg_qrow, seg_out_row, *plan, solo_ctas=ctas)
             return (*plan, tab, FKV_DECODE_SOLO)
         except ValueError:
