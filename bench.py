@@ -89,9 +89,14 @@ def make_plan(budgets, tp, ch, mode):
 
 
 def default_mode(tp):
-    # TP=8 with 8 KV heads: equal split with CH=4 degenerates to SHA,
-    # so the AHA-DP default there is the free split.
-    return "dp-free" if tp == 8 else "dp"
+    # AHA-DP with equal split everywhere; at TP=8 (8 KV heads) CH=4 degenerates
+    # to SHA, so TP=8 plans with CH=8 (plan_ch) -- the best of
+    # the emulated TP=8 variants (profiles/r01_bench_full.json emulated_tp).
+    return "dp"
+
+
+def plan_ch(tp, mode, ch):
+    return 8 if tp == 8 and mode == "dp" else ch
 
 
 # ------------------------------------------------------------- clocks -----
@@ -242,7 +247,7 @@ def run_fairkv(args):
     tp = world
     budgets, wname = workload(args)
     mode = "sha" if tp == 1 else default_mode(tp)
-    plan, prof = make_plan(budgets, tp, args.ch, mode)
+    plan, prof = make_plan(budgets, tp, plan_ch(tp, mode, args.ch), mode)
     shards, finals = plan_layouts(plan, budgets, GROUP)
     my = [s[rank] for s in shards]
     caches = rank_caches(my, args.batch, HQ, GROUP, tp, dev, fill="random", seed=args.seed + rank)
@@ -371,7 +376,7 @@ def run_fairkv(args):
             "layers": args.layers,
             "avg_budget": args.budget,
             "context": args.context,
-            "parallelism": f"tp{tp} ({'uniform head-sharded' if mode == 'sha' else 'AHA-' + mode + f' CH={args.ch}'})"
+            "parallelism": f"tp{tp} ({'uniform head-sharded' if mode == 'sha' else 'AHA-' + mode + f' CH={plan_ch(tp, mode, args.ch)}'})"
                            + (f", exchange {args.exchange}" if tp > 1 else ""),
             "l2": f"inputs larger than L2: {dec.kv_bytes() / 1e9:.1f} GB KV read per step per GPU",
             "graph": use_graph,

@@ -695,6 +695,13 @@ __global__ void __launch_bounds__(G * 32)
                      __nv_bfloat16* __restrict__ out_bf16, float* __restrict__ out_rec,
                      float* __restrict__ out_lse, const int32_t* flags, int tp,
                      int32_t* consumed) {
+  // Programmatic dependent launch (plain merges only, see fkv_merge_wait):
+  // the records are complete once the producer grid (NCCL all-gather, K4
+  // partials) is.
+  if (!flags) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;");
+  }
   // Fused all-gather consumer: wait until every peer has published this
   // layer's records (their flag reached consumed+1), read them from L2.
   __shared__ int s_target;
@@ -908,19 +915,23 @@ extern "C" int fkv_merge_wait(const float* part, const int32_t* grp_ptr, const i
   if (n_groups == 0) return FKV_OK;
   if (!part || !grp_ptr || !src_idx || !out_row || (!out_bf16 && !out_rec && !out_lse))
     return set_error(FKV_ERR_INVALID, "fkv_merge_lse: null pointer");
-  auto st = static_cast<cudaStream_t>(stream);
   auto ob = static_cast<__nv_bfloat16*>(out_bf16);
-  switch (group) {
-    case 4:
-      merge_lse_kernel<4><<<n_groups, 4 * 32, 0, st>>>(part, grp_ptr, src_idx, out_row, ob, out_rec,
-                                                       out_lse, flags, tp, consumed);
-      break;
-    case 8:
-      merge_lse_kernel<8><<<n_groups, 8 * 32, 0, st>>>(part, grp_ptr, src_idx, out_row, ob, out_rec,
-                                                       out_lse, flags, tp, consumed);
-      break;
-    default:
-      return set_error(FKV_ERR_INVALID, "fkv_merge_lse: group must be 4 or 8");
-  }
-  return cuda_check(cudaGetLastError(), "merge_lse launch");
+  if (group != 4 && group != 8) return set_error(FKV_ERR_INVALID, "fkv_merge_lse: group must be 4 or 8");
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(n_groups, 1, 1);
+  cfg.blockDim = dim3(group * 32, 1, 1);
+  cfg.stream = static_cast<cudaStream_t>(stream);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL (see kernel)
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  // A spinning consumer is never launched early: its CTAs would sit on SMs
+  // waiting for peers while grids queued behind it need them.
+  cfg.numAttrs = flags ? 0 : 1;
+  const cudaError_t e =
+      group == 4 ? cudaLaunchKernelEx(&cfg, merge_lse_kernel<4>, part, grp_ptr, src_idx, out_row, ob,
+                                      out_rec, out_lse, flags, tp, consumed)
+                 : cudaLaunchKernelEx(&cfg, merge_lse_kernel<8>, part, grp_ptr, src_idx, out_row, ob,
+                                      out_rec, out_lse, flags, tp, consumed);
+  return cuda_check(e, "merge_lse launch");
 }
