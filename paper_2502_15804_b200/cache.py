@@ -81,8 +81,35 @@ def _cut_stream(seg_len, tiles, per: int, cap: int):
     return seg_i, t0s, t1s, np.asarray(owner, dtype=np.int64)
 
 
+def _cut_stream_cost(seg_len, tiles, C: int, P: int, cap: int):
+    """Cut the tile stream into worker ranges of estimated cost <= C, a
+    worker's cost being sum over its pieces of (P + tiles): every piece pays
+    a fixed epilogue (hand-over, combine, output or record + merge)."""
+    seg_i, t0s, t1s, owner = [], [], [], []
+    w, cost, cnt = 0, 0, 0
+    for s in range(len(seg_len)):
+        n, t = int(tiles[s]), 0
+        while True:
+            if cnt >= cap or (cnt > 0 and (C - cost - P < 1 or (n == t and C - cost - P < 0))):
+                w, cost, cnt = w + 1, 0, 0
+            take = min(n - t, max(C - cost - P, 1))
+            seg_i.append(s)
+            t0s.append(t * TILE)
+            t1s.append(min(int(seg_len[s]), (t + take) * TILE))
+            owner.append(w)
+            cost += P + take
+            cnt += 1
+            t += take
+            if t >= n:
+                break
+    return seg_i, t0s, t1s, np.asarray(owner, dtype=np.int64)
+
+
+PIECE_COST_TILES = 48  # coop schedule: one piece's cost in tile-equivalents (plateau >= 32, probe_sched)
+
+
 def plan_work(seg_len, n_workers: int, chunk: int | None = None,
-              min_tiles: int = MIN_TILES_PER_WORKER):
+              min_tiles: int = MIN_TILES_PER_WORKER, piece_cost: int | None = None):
     """Static decode schedule for the warp-persistent K4 kernel.
 
     Default: the segments' 16-token tiles are laid end to end and the stream
@@ -112,14 +139,36 @@ def plan_work(seg_len, n_workers: int, chunk: int | None = None,
         avg = int(tiles.sum()) // max(n_seg, 1)
         per = max(per, -(-avg // MAX_PIECES_PER_SEGMENT))
         per = max(per, -(-longest // (MAX_ITEMS_PER_SEGMENT - 1)))
-        while True:
-            seg_i, t0s, t1s, owner = _cut_stream(seg_len, tiles, per, MAX_WORK_PER_WORKER)
-            if not len(owner) or int(owner.max()) < W:
-                break
-            if per >= int(tiles.sum()):  # only the piece cap can bind: too many segments
+        import os
+        P = int(os.environ.get("FKV_PIECE_COST", PIECE_COST_TILES)) if piece_cost is None else piece_cost
+        if P > 0 and n_seg:
+            # equal estimated time per worker (tiles + P per piece): smallest C
+            # whose greedy cut fits in W workers (binary search)
+            # C >= per + P: a worker still takes >= per tiles in one piece
+            # (min_tiles, and <= MAX_ITEMS_PER_SEGMENT pieces per segment)
+            lo = max(per + P, -(-(int(tiles.sum()) + P * n_seg) // W))
+            hi = max(lo, int(tiles.sum()) + P * (n_seg + 1))
+            best = None
+            while lo <= hi:
+                C = (lo + hi) // 2
+                cut = _cut_stream_cost(seg_len, tiles, C, P, MAX_WORK_PER_WORKER)
+                if int(cut[3].max()) < W:
+                    best, hi = cut, C - 1
+                else:
+                    lo = C + 1
+            if best is None:
                 raise ValueError(f"{n_seg} segments exceed one launch "
                                  f"({W} workers x {MAX_WORK_PER_WORKER} pieces)")
-            per *= 2
+            seg_i, t0s, t1s, owner = best
+        else:
+            while True:
+                seg_i, t0s, t1s, owner = _cut_stream(seg_len, tiles, per, MAX_WORK_PER_WORKER)
+                if not len(owner) or int(owner.max()) < W:
+                    break
+                if per >= int(tiles.sum()):  # only the piece cap can bind: too many segments
+                    raise ValueError(f"{n_seg} segments exceed one launch "
+                                     f"({W} workers x {MAX_WORK_PER_WORKER} pieces)")
+                per *= 2
     else:
         ch = max(1, -(-int(chunk) // TILE))
         ch = max(ch, -(-longest // MAX_ITEMS_PER_SEGMENT)) * TILE
@@ -270,14 +319,17 @@ FKV_DECODE_SOLO = 1
 def plan_schedule(seg_len, seg_row0, seg_qrow, seg_out_row, device=None, chunk: int | None = None):
     """Pick the K4 schedule for one cache and build its work table.
 
-    * small caches (<= SOLO_MAX_TILES_PER_CTA tiles per CTA): per-warp pieces
-      of 4-8 tiles (the launch floor and per-piece latency dominate; short
-      per-warp chains win);
-    * many short segments (>= 0.4 per warp, mean <= 24 tiles): per-warp,
+    * default: the CTA-cooperative schedule, stream cut to equal *estimated
+      time* per CTA (tiles + PIECE_COST_TILES per piece: a CTA with more,
+      shorter pieces gets fewer tiles, and ranges prefer segment boundaries);
+    * many short segments (at least one per warp and <= 24 tiles on average,
+      or 0.4 per warp and <= 12 tiles): the per-warp ("solo") schedule,
       segments up to max(16, 2 x the per-warp share) kept whole and packed
-      largest-first, longer ones split -- balanced with few LSE merges
-      (Llama-3.1-8B shape at batch 64-256: 93 % of HBM at batch 256);
-    * otherwise the CTA-cooperative schedule (few long segments: 70B shape).
+      largest-first -- balanced with few LSE merges (Llama-3.1-8B shape at
+      batch 256: 94 % of HBM);
+    * FKV_SOLO_SMALL=1 additionally sends small caches (<= 19 tiles per CTA)
+      to the solo schedule with 4-8-tile pieces (the choice before the
+      piece-cost planner).
     FKV_K4_SCHEDULE = coop | solo | auto overrides (measurements).
     -> (item_seg, t0, t1, seg_item_ptr, warp_ptr, work_list, table, flags)."""
     import os
@@ -287,8 +339,9 @@ def plan_schedule(seg_len, seg_row0, seg_qrow, seg_out_row, device=None, chunk: 
     tiles = int(seg_tiles.sum())
     n_seg = len(seg_len)
     mode = os.environ.get("FKV_K4_SCHEDULE", "auto")
-    small = tiles <= SOLO_MAX_TILES_PER_CTA * ctas
-    many_short = n_seg >= 0.4 * 4 * ctas and n_seg and tiles / n_seg <= 24
+    small = tiles <= SOLO_MAX_TILES_PER_CTA * ctas and os.environ.get("FKV_SOLO_SMALL") == "1"
+    mean = tiles / n_seg if n_seg else 0
+    many_short = (n_seg >= 4 * ctas and mean <= 24) or (n_seg >= 0.4 * 4 * ctas and mean <= 12)
     solo = mode == "solo" or (mode == "auto" and chunk is None and (small or many_short))
     if solo:
         if small or mode == "solo" and not many_short:

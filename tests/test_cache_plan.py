@@ -10,6 +10,20 @@ from paper_2502_15804_b200.cache import (MAX_ITEMS_PER_SEGMENT, MAX_WORK_PER_WOR
 @pytest.mark.parametrize("chunk", [None, 64, 100, 512])
 @pytest.mark.parametrize("workers", [300, 1184])
 def test_plan_covers_each_segment_once(chunk, workers):
+    _plan_covers(chunk, workers)
+
+
+def test_tiny_plan_respects_piece_caps():
+    # few tiles, many workers: pieces must not shrink below min_tiles / exceed
+    # MAX_ITEMS_PER_SEGMENT per segment (the kernel's merge scratch)
+    item_seg, t0, t1, sptr, wptr, wlist = plan_work([333, 1, 666], 296)
+    assert np.diff(sptr).max() <= MAX_ITEMS_PER_SEGMENT
+    for s in range(3):
+        its = list(range(sptr[s], sptr[s + 1]))
+        assert all(t1[i] - t0[i] >= 16 * 8 for i in its[:-1])  # only a segment's tail is short
+
+
+def _plan_covers(chunk, workers):
     rng = np.random.default_rng(workers + (chunk or 0))
     seg_len = rng.integers(0, 3000, size=300)
     seg_len[:3] = [0, 1, 16]
@@ -68,11 +82,31 @@ def test_balanced_plan_equalises_tiles_per_worker():
     rng = np.random.default_rng(0)
     seg_len = rng.integers(300, 3000, size=512)
     W = 1184
-    item_seg, t0, t1, sptr, wptr, wlist = plan_work(seg_len, W)
+    item_seg, t0, t1, sptr, wptr, wlist = plan_work(seg_len, W, piece_cost=0)
     tiles = -(-(t1 - t0) // 16)
     assert len(wptr) - 1 <= W
     per = np.array([tiles[wlist[wptr[w]:wptr[w + 1]]].sum() for w in range(len(wptr) - 1)])
     assert per.max() <= -(-tiles.sum() // W) + 1
+
+
+def test_piece_cost_plan_balances_estimated_time():
+    """Default coop planner: equal (tiles + P * pieces) per worker -- a worker
+    with more pieces gets fewer tiles; pieces prefer segment boundaries."""
+    from paper_2502_15804_b200.cache import PIECE_COST_TILES as P
+    rng = np.random.default_rng(1)
+    seg_len = rng.integers(100, 3000, size=512)
+    W = 296
+    item_seg, t0, t1, sptr, wptr, wlist = plan_work(seg_len, W)
+    tiles = -(-(t1 - t0) // 16)
+    busy = len(wptr) - 1
+    assert busy <= W and sorted(wlist.tolist()) == list(range(len(item_seg)))
+    cost = np.array([tiles[wlist[wptr[w]:wptr[w + 1]]].sum() + P * (wptr[w + 1] - wptr[w])
+                     for w in range(busy)])
+    ideal = (tiles.sum() + P * len(item_seg)) / busy
+    assert cost.max() <= 1.15 * ideal + P
+    # fewer split segments than the equal-tiles cut
+    eq = plan_work(seg_len, W, piece_cost=0)
+    assert (np.diff(sptr) > 1).sum() <= (np.diff(eq[3]) > 1).sum()
 
 
 def test_segment_offsets_page_aligned():
