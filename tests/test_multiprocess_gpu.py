@@ -84,3 +84,23 @@ def test_two_process_p2p_exchange(cuda_device, tmp_path, tp, mode):
     for r in range(tp):
         ok, err = (tmp_path / f"rank{r}.txt").read_text().split()
         assert ok == "1", f"rank {r}: max |o - ref| = {err}"
+
+
+def test_bench_two_ranks_shared_device():
+    """bench.py's N > 1 path end to end (torchrun, P2P exchange through CUDA
+    IPC, graph capture, max-over-ranks timing) with both ranks on the one GPU
+    (FKV_SHARED_DEVICE=1: gloo plumbing; timings meaningless)."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    env = dict(os.environ, FKV_SHARED_DEVICE="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", "2",
+           "--layers", "3", "--batch", "4", "--steps", "2", "--warmup", "3", "--no-emulate", "--no-cpu"]
+    r = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=280)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 2 and line["value"] > 0 and line["e2e"]["value"] > 0
+    assert "exchange p2p" in line["config"]["parallelism"]
