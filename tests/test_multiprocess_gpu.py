@@ -86,7 +86,7 @@ def test_two_process_p2p_exchange(cuda_device, tmp_path, tp, mode):
         assert ok == "1", f"rank {r}: max |o - ref| = {err}"
 
 
-def test_bench_two_ranks_shared_device():
+def test_bench_two_ranks_shared_device(cuda_device):
     """bench.py's N > 1 path end to end (torchrun, P2P exchange through CUDA
     IPC, graph capture, max-over-ranks timing) with both ranks on the one GPU
     (FKV_SHARED_DEVICE=1: gloo plumbing; timings meaningless)."""
