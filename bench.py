@@ -637,7 +637,8 @@ def prefill_compress(peaks):
     rows = {}
     for name, (bt, hq, hkv, T, B) in {"llama-3.1-8b_T16k_B256": (1, 32, 8, 16384, 256),
                                      "llama-3.1-8b_T16k_B256_batch4": (4, 32, 8, 16384, 256),
-                                     "llama-3.3-70b_T32k_B1024": (1, 64, 8, 32768, 1024)}.items():
+                                     "llama-3.3-70b_T32k_B1024": (1, 64, 8, 32768, 1024),
+                                     "llama-3.3-70b_T128k_B1024": (1, 64, 8, 131072, 1024)}.items():
         w = WINDOW
         g = torch.Generator(device=dev).manual_seed(5)
         q = torch.randn((bt, hq, w, HEAD_DIM), generator=g, device=dev).to(torch.bfloat16)

@@ -167,6 +167,7 @@ def test_fused_ada_select_bit_exact(cuda_device, bt, T, budget, ties):
     (1, 32, 8, 20000, 1024, 3.0, False),  # long context, several chunks per head
     (2, 32, 8, 3000, 256, 2.0, True),     # a head whose window soaks up all attention: below its floor
     (20, 32, 8, 600, 64, 2.0, False),     # 160 heads > 148 SMs: two-launch fallback
+    (1, 64, 8, 131072, 1024, 2.0, False),  # cfg5: 128k context, B=1024, 70B shape
 ])
 def test_fused_score_select_bit_exact(cuda_device, bt, hq, hkv, T, budget, temp, flat_head):
     """K1 + A18 + K2 in one launch: scores within tolerance of the oracle;
