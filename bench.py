@@ -405,6 +405,7 @@ def run_fairkv(args):
         torch.cuda.empty_cache()
         out["emulated_tp_budget_sweep"] = budget_sweep(args, dev)
         out["cfg2_llama3.1-8b_b256_T16k"] = cfg2_sweep(args, dev, peak)
+        out["full_layer"] = full_layer(args, budgets, dev)
     if rank == 0 and world == 1 and not args.no_cpu:
         out["planner"] = planner_compare(budgets)
     if rank == 0 and world == 1 and not args.no_emulate:
@@ -413,6 +414,94 @@ def run_fairkv(args):
         print(json.dumps(out))
     if world > 1:
         dist.destroy_process_group()
+
+
+def full_layer(args, budgets, dev):
+    """the decode layer with its weight GEMMs -- per layer and
+    rank: QKV projection x[Bt, 8192] @ W_qkv (the rank's q heads + K/V heads,
+    replicated rows for AHA-DP copies; cuBLAS bf16), K4 over the rank's shard,
+    o_proj o[Bt, 8192] @ W_o[:, rank's 1/tp of the columns] (column-parallel
+    after the all-gather).  Random-init weights; each rank's layers timed as
+    in emulate_tp (event-bracketed minus the back-to-back correction), span =
+    sum over layers of the max over ranks.  Shows how much of AHA's attention
+    gain survives once the weights (302 MB per layer at TP=1) are streamed too."""
+    import numpy as np
+    import torch
+    from paper_2502_15804_b200 import ops
+    from paper_2502_15804_b200.cache import LayerCache
+    from paper_2502_15804_b200.decoder import rank_caches
+    from paper_2502_15804_b200.sharding import plan_layouts
+    L, bt = budgets.shape[0], budgets.shape[1]
+    hidden = HQ * HEAD_DIM
+    qrow = np.array([b * HQ + h * GROUP for b in range(bt) for h in range(HKV)])
+    gen = torch.Generator(device=dev).manual_seed(17)
+    base = [LayerCache.allocate(budgets[l].reshape(-1), qrow, qrow, GROUP, dev, fill="random", generator=gen)
+            for l in range(L)]
+    w_qkv = [torch.randn((hidden, (HQ + 2 * HKV) * HEAD_DIM), device=dev, generator=gen).to(torch.bfloat16)
+             for _ in range(L)]
+    w_o = [torch.randn((hidden, hidden), device=dev, generator=gen).to(torch.bfloat16) for _ in range(L)]
+    x = torch.randn((bt, hidden), device=dev, generator=gen).to(torch.bfloat16)
+    q = torch.randn((L, bt, HQ, HEAD_DIM), device=dev, generator=gen).to(torch.bfloat16)
+    o_full = torch.randn((bt, hidden), device=dev, generator=gen).to(torch.bfloat16)
+    qkv_out = torch.empty((bt, (HQ + 2 * HKV) * HEAD_DIM), device=dev, dtype=torch.bfloat16)
+    y = torch.empty((bt, hidden), device=dev, dtype=torch.bfloat16)
+    results = {}
+    for tp, modes in ((1, ["sha"]), (2, ["sha", "nodp"]), (4, ["sha", "nodp", "dp"]), (8, ["sha", "dp"])):
+        row = {}
+        for mode in modes:
+            plan, _ = make_plan(budgets, tp, plan_ch(tp, mode, args.ch), mode)
+            shards, _ = plan_layouts(plan, budgets, GROUP)
+            t = np.zeros((L, tp))
+            attn = np.zeros((L, tp))
+            for g in range(tp):
+                caches = rank_caches([s[g] for s in shards], bt, HQ, GROUP, tp, dev, base=base)
+                sends = [torch.empty((max(c.n_segments, 1), GROUP, ops.REC), device=dev) for c in caches]
+                wss = [ops.DecodeWorkspace(c) for c in caches]
+                # the rank's QKV columns: G q heads + its own K and V per KV-head copy
+                cols = [len(plan.layers[l].groups[g]) * (GROUP + 2) * HEAD_DIM for l in range(L)]
+                ocols = hidden // tp
+                evs = [[torch.cuda.Event(enable_timing=True, external=True) for _ in range(4)] for _ in range(L)]
+
+                def layer(l, ev=None):
+                    if ev:
+                        ev[0].record()
+                    torch.mm(x, w_qkv[l][:, :cols[l]], out=qkv_out[:, :cols[l]])
+                    if ev:
+                        ev[1].record()
+                    ops.decode_into(q[l], caches[l], wss[l], out_rec=sends[l])
+                    if ev:
+                        ev[2].record()
+                    torch.mm(o_full, w_o[l][:, :ocols], out=y[:, :ocols])
+                    if ev:
+                        ev[3].record()
+
+                gb = capture(lambda: [layer(l, evs[l]) for l in range(L)])
+                gs = capture(lambda: [layer(l) for l in range(L)])
+                gb.replay()
+                gs.replay()
+                torch.cuda.synchronize()
+                tot = timed(gs.replay, 3) / 3
+                gb.replay()
+                torch.cuda.synchronize()
+                tb = np.array([evs[l][0].elapsed_time(evs[l][3]) for l in range(L)]) * 1e-3
+                ta = np.array([evs[l][1].elapsed_time(evs[l][2]) for l in range(L)]) * 1e-3
+                c_g = max(0.0, (tb.sum() - tot) / L)
+                t[:, g] = np.maximum(tb - c_g, 0.0)
+                attn[:, g] = ta
+                del gb, gs, caches, sends, wss
+            step = t.max(axis=1).sum()
+            row[mode] = {"tokens_per_s": bt / step, "ms_per_step": step * 1e3,
+                         "attention_share_bracketed": float(attn.sum() / t.sum()) if t.sum() else None}
+        for mode in modes[1:]:
+            row[mode]["gain_vs_sha"] = row[mode]["tokens_per_s"] / row["sha"]["tokens_per_s"]
+        results[f"tp{tp}"] = row
+    results["note"] = ("per layer: QKV GEMM + K4 + o_proj GEMM (cuBLAS bf16 for the GEMMs, random-init "
+                       "weights, 302 MB per layer at TP=1), all-gather excluded; "
+                       "attention_share_bracketed = K4 time (event-bracketed, uncorrected) / corrected "
+                       "layer time -- an upper bound")
+    del base, w_qkv, w_o
+    torch.cuda.empty_cache()
+    return results
 
 
 def emulate_tp(args, budgets, dev, calibrate=True):
