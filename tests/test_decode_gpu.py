@@ -134,3 +134,22 @@ def test_lse_merge_of_token_split_equals_whole(cuda_device):
     o_ref, lse_ref = okv.attend(q[0].float().cpu().numpy(), k.float().numpy(), v.float().numpy())
     torch.testing.assert_close(o[0].float().cpu().double(), torch.from_numpy(o_ref), rtol=2e-2, atol=1e-2)
     torch.testing.assert_close(lse[0].cpu().double(), torch.from_numpy(lse_ref), rtol=0, atol=2e-3)
+
+
+@pytest.mark.parametrize("schedule", ["coop", "solo"])
+def test_decode_empty_and_tiny_segments(cuda_device, schedule, monkeypatch):
+    """Zero-token segments (an AHA-DP copy can own no tokens) give o = 0 and
+    lse = -inf; 1..17-token segments exercise the masked tails."""
+    from paper_2502_15804_b200 import ops
+    monkeypatch.setenv("FKV_K4_SCHEDULE", schedule)
+    group, hkv, bt = 8, 8, 2
+    seg_lens = [0, 1, 2, 15, 16, 17, 0, 31, 33, 0, 5, 64, 65, 0, 7, 128]
+    cache, q, ks, vs = build_cache(seg_lens, group, hkv, bt, cuda_device, seed=9)
+    o, lse = ops.decode(q.to(cuda_device), cache)
+    torch.cuda.synchronize()
+    o_ref, lse_ref = okv.decode_heads(q.float().numpy().astype(np.float64), ks, vs, group)
+    torch.testing.assert_close(o.float().cpu().double(), torch.from_numpy(o_ref), rtol=2e-2, atol=1e-2)
+    lse_c = lse.cpu().double()
+    empty = torch.from_numpy(np.isneginf(lse_ref))
+    assert torch.isneginf(lse_c[empty]).all()
+    torch.testing.assert_close(lse_c[~empty], torch.from_numpy(lse_ref)[~empty], rtol=0, atol=2e-3)
