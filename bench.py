@@ -628,7 +628,7 @@ def cfg2_sweep(args, dev, peak):
         rows[f"batch{bt}"] = {"tokens_per_s": bt / t, "ms_per_step": t * 1e3,
                               "kv_GBs": kv / t / 1e9, "hbm_frac": kv / t / 1e9 / peak,
                               "kv_MB_per_step": kv / 1e6,
-                              "schedule": "solo" if caches[0].flags else "coop"}
+                              "schedule": {0: "coop", 1: "solo", 2: "wide"}[caches[0].flags]}
         del g, caches, wss
         torch.cuda.empty_cache()
     return rows

@@ -124,6 +124,9 @@ typedef struct fkv_work {
  * (piece owner warp = n_it >> 16, pieces per segment = n_it & 0xffff);
  * without it the four warps share every piece of the CTA's list. */
 #define FKV_DECODE_SOLO 1
+/* FKV_DECODE_WIDE = cooperative schedule with 8-warp CTAs (one per SM, seven
+ * streaming warps per piece) instead of 4-warp CTAs (two per SM). */
+#define FKV_DECODE_WIDE 2
 
 /*   q            bf16 [*, 128]   query rows
  *   k, v         bf16 [rows,128] swizzled cache rows (layout above)
@@ -140,6 +143,10 @@ typedef struct fkv_work {
  * group (= Hq/Hkv) must be 4 or 8; softmax scale = sm_scale.
  * Nothing in the reference is replaced (it has no decode); its cost model of
  * this kernel is reference latency.py:85-91 (predict_compute). */
+/* Persistent CTAs per SM of the schedule selected by `flags` (the planner
+ * sizes the work table with SMs x this many rows: one per co-resident CTA). */
+int fkv_decode_ctas_per_sm(int32_t flags);
+
 int fkv_decode(const void* q, const void* k, const void* v, const fkv_work_t* work,
                int32_t work_k, int32_t n_workers, int32_t n_items, int32_t group, int32_t flags,
                float sm_scale, float* part, int32_t* counters, void* out_bf16, float* out_rec,

@@ -37,6 +37,7 @@ _SIGS = {
                                   _vp, _vp, _vp, _vp, _vp]),
     "fkv_optimize_plan": (C.c_int, [_vp, _i32, _i32, _i32, _i32, _i32, _i32, _i64, _i64, _i32,
                                     _vp, _vp, _vp, _vp, _vp]),
+    "fkv_decode_ctas_per_sm": (C.c_int, [_i32]),
     "fkv_decode": (C.c_int, [_vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _f32, _vp, _vp,
                              _vp, _vp, _vp, _vp]),
     "fkv_merge_lse": (C.c_int, [_vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp]),

@@ -45,13 +45,16 @@ MAX_WORK_PER_WORKER = 32    # FKV_MAX_WORK: descriptor entries per worker
 TILE = 16
 
 
-def default_workers(device=None) -> int:
-    """Persistent decode CTAs (four warps each): two on every SM."""
+def default_workers(device=None, flags: int = 0) -> int:
+    """Persistent decode CTAs of a schedule (``flags``: FKV_DECODE_SOLO /
+    FKV_DECODE_WIDE / 0): SMs x its co-resident CTAs per SM (libfairkv: 1 for
+    the 8-warp cooperative CTA, 2 otherwise)."""
     try:
         sms = torch.cuda.get_device_properties(device).multi_processor_count
     except Exception:  # no device visible (host-side planning / CPU tests)
         sms = NUM_SMS
-    return sms * 2
+    from . import _native
+    return sms * int(_native.lib.fkv_decode_ctas_per_sm(int(flags)))
 
 
 MIN_TILES_PER_WORKER = 8  # floor on tiles per worker CTA (one 2-tile round per warp)
@@ -314,6 +317,8 @@ def plan_work_solo(seg_len, n_workers: int, piece_tiles: int = 16, whole_tiles: 
 # (FKV_K4_SCHEDULE = coop | solo | auto overrides, for measurements).
 SOLO_MAX_TILES_PER_CTA = 19  # measured crossover (tools/probe_solo_params.py, probe_sched.py): ~5600 tiles per GPU-layer
 FKV_DECODE_SOLO = 1
+FKV_DECODE_WIDE = 2
+WIDE_MAX_SEGMENTS = 128
 
 
 def plan_schedule(seg_len, seg_row0, seg_qrow, seg_out_row, device=None, chunk: int | None = None):
@@ -330,39 +335,47 @@ def plan_schedule(seg_len, seg_row0, seg_qrow, seg_out_row, device=None, chunk: 
     * FKV_SOLO_SMALL=1 additionally sends small caches (<= 19 tiles per CTA)
       to the solo schedule with 4-8-tile pieces (the choice before the
       piece-cost planner).
-    FKV_K4_SCHEDULE = coop | solo | auto overrides (measurements).
+    * few segments of at least 8 tiles (<= WIDE_MAX_SEGMENTS, e.g. a TP=4/8
+      rank's KV heads): the cooperative schedule with 8-warp CTAs (one per
+      SM, seven streaming warps per piece).
+    FKV_K4_SCHEDULE = coop | wide | solo | auto overrides (measurements).
     -> (item_seg, t0, t1, seg_item_ptr, warp_ptr, work_list, table, flags)."""
     import os
     seg_len = np.asarray(seg_len, dtype=np.int64)
-    ctas = default_workers(device)
+    solo_ctas = default_workers(device, FKV_DECODE_SOLO)
     seg_tiles = (seg_len + TILE - 1) // TILE
     tiles = int(seg_tiles.sum())
     n_seg = len(seg_len)
     mode = os.environ.get("FKV_K4_SCHEDULE", "auto")
-    small = tiles <= SOLO_MAX_TILES_PER_CTA * ctas and os.environ.get("FKV_SOLO_SMALL") == "1"
+    small = tiles <= SOLO_MAX_TILES_PER_CTA * solo_ctas and os.environ.get("FKV_SOLO_SMALL") == "1"
     mean = tiles / n_seg if n_seg else 0
-    many_short = (n_seg >= 4 * ctas and mean <= 24) or (n_seg >= 0.4 * 4 * ctas and mean <= 12)
+    warps = 4 * solo_ctas
+    many_short = (n_seg >= warps and mean <= 24) or (n_seg >= 0.4 * warps and mean <= 12)
     solo = mode == "solo" or (mode == "auto" and chunk is None and (small or many_short))
     if solo:
         if small or mode == "solo" and not many_short:
             # piece / whole-segment thresholds grow with the cache: 4 tiles for a
             # few hundred tiles per GPU-layer, 8 near the crossover (probe_solo_params)
-            pt = wt = int(np.clip(round(1.5 * tiles / (4 * ctas)), 4, 8))
+            pt = wt = int(np.clip(round(1.5 * tiles / warps), 4, 8))
         else:
             # pieces of at least 16 tiles, at least twice the per-warp share:
             # most segments stay whole, only the long tail is split
-            pt = wt = max(16, -(-2 * tiles // (4 * ctas)))
+            pt = wt = max(16, -(-2 * tiles // warps))
         pt = int(os.environ.get("FKV_SOLO_PIECE", pt))
         wt = int(os.environ.get("FKV_SOLO_WHOLE", wt))
         try:
-            plan = plan_work_solo(seg_len, 4 * ctas, pt, wt)
-            tab = work_table(seg_row0, seg_len, seg_qrow, seg_out_row, *plan, solo_ctas=ctas)
+            plan = plan_work_solo(seg_len, warps, pt, wt)
+            tab = work_table(seg_row0, seg_len, seg_qrow, seg_out_row, *plan, solo_ctas=solo_ctas)
             return (*plan, tab, FKV_DECODE_SOLO)
         except ValueError:
             pass  # too many pieces for the per-CTA tables: cooperative schedule
-    plan = plan_work(seg_len, ctas, chunk)
+    # few segments (a TP-sharded rank's cache): 8-warp CTAs, seven streams per
+    # piece; otherwise 4-warp CTAs, two per SM (tools/probe_sched.py)
+    wide = mode == "wide" or (mode != "coop" and n_seg <= WIDE_MAX_SEGMENTS and mean >= 8)
+    flags = FKV_DECODE_WIDE if wide else 0
+    plan = plan_work(seg_len, default_workers(device, flags), chunk)
     tab = work_table(seg_row0, seg_len, seg_qrow, seg_out_row, *plan)
-    return (*plan, tab, 0)
+    return (*plan, tab, flags)
 
 
 @dataclass

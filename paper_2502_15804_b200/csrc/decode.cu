@@ -38,19 +38,23 @@
 namespace fkv {
 namespace {
 
-constexpr int kWarps = 4;
-#ifndef FKV_K4_DEDICATED
-#define FKV_K4_DEDICATED 1
-#endif
-// FKV_K4_DEDICATED: warp 0 only combines / finalises (records, atomics,
-// segment merges) while warps 1-3 stream with 4-stage rings; otherwise all
-// four warps stream (3 stages) and warp 0 takes one round in seven.
-constexpr bool kDedicated = FKV_K4_DEDICATED != 0;
-constexpr int kStreamWarps = kDedicated ? kWarps - 1 : kWarps;
-constexpr int kStages = kDedicated ? 4 : 3;  // ring stages per streaming warp (tiles in flight)
+// CTA shapes (MODE).  Cooperative schedules: warp 0 only combines /
+// finalises (records, atomics, segment merges) while warps 1..W-1 stream:
+//   0 "coop"  W = 4, 4-stage rings, two CTAs per SM (96 KiB of ring each);
+//   2 "wide"  W = 8, 3-stage rings, one CTA per SM (168 KiB of ring) -- for
+//             caches with few segments (TP-sharded ranks), where 7 streams
+//             per piece beat 3.
+// 1 "solo": per-warp schedule, 4 warps all streaming, 3 stages, two per SM.
 constexpr int kTileTok = 16;
-constexpr int kTileBytes = kTileTok * FKV_HEAD_DIM * 2;              // 4 KiB per K or V tile
-constexpr int kSmemBytes = kStreamWarps * kStages * 2 * kTileBytes;  // 96 KiB per CTA
+constexpr int kTileBytes = kTileTok * FKV_HEAD_DIM * 2;  // 4 KiB per K or V tile
+template <int MODE>
+struct Shape {
+  static constexpr int W = MODE == 2 ? 8 : 4;                        // warps per CTA
+  static constexpr int S = MODE == 1 ? W : W - 1;                    // streaming warps
+  static constexpr int NS = MODE == 0 ? 4 : 3;                       // ring stages per streamer
+  static constexpr int kSmem = S * NS * 2 * kTileBytes;              // dynamic smem (ring)
+  static constexpr int kCtasPerSm = MODE == 2 ? 1 : 2;
+};
 constexpr int kMergeMax = FKV_MAX_PIECES;                      // max pieces per segment
 constexpr int kXch = 36;  // floats per lane handed to warp 0: m0 m1 l0 l1 acc[32]
 constexpr float kLog2e = 1.4426950408889634f;
@@ -74,10 +78,11 @@ struct DecodeParams {
   int n_sig, my_rank;
 };
 
+template <int W>
 struct __align__(16) DecodeShared {
   fkv_work_t tab[FKV_MAX_WORK];
-  uint64_t bars[kWarps][kStages];
-  float xch[kWarps - 1][kXch][32];  // warps 1..3 -> warp 0 piece state, lane-contiguous
+  uint64_t bars[W][4];
+  float xch[W - 1][kXch][32];  // warps 1..W-1 -> warp 0 piece state, lane-contiguous
   float scratch[kMergeMax * 8];     // global merge weights
   int32_t fin_i0, fin_n_it, fin_orow;  // deferred merge of the CTA's last piece (n_it 0 = none)
 };
@@ -99,33 +104,27 @@ __device__ __forceinline__ int atom_add_acq_rel(int32_t* addr, int v) {
   return old;
 }
 
+template <int W>
 __device__ __forceinline__ void named_sync(int id) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(kWarps * 32) : "memory");
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(W * 32) : "memory");
 }
+template <int W>
 __device__ __forceinline__ void named_arrive(int id) {
-  asm volatile("bar.arrive %0, %1;" ::"r"(id), "n"(kWarps * 32) : "memory");
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "n"(W * 32) : "memory");
 }
 
-// Round ownership inside a CTA.  Rounds (two tiles each) are numbered across
-// the CTA's pieces; with period 7 warp 0 owns one round (offset 3) and warps
-// 1-3 own two each (offsets j-1, j+3): warp 0 combines and finalises every
-// piece (records, atomics, segment merges), so it streams half as much.
-constexpr int kPeriod = 7;
+// Round ownership inside a CTA (cooperative schedule).  Rounds (two tiles
+// each) are numbered across the CTA's pieces and dealt round robin to the
+// streaming warps 1..W-1; warp 0 owns none.
 constexpr int kNoRound = 0x7fffffff;
+template <int W>
 __device__ __forceinline__ int first_round(int warp, int g0) {  // first owned round >= g0
-  if (kDedicated) {  // warps 1-3 round robin, warp 0 none
-    if (warp == 0) return kNoRound;
-    return g0 + ((warp - 1 - g0 % 3) + 3) % 3;
-  }
-  const int base = g0 - g0 % kPeriod;
-  if (warp == 0) return base + 3 >= g0 ? base + 3 : base + 3 + kPeriod;
-  const int a = base + warp - 1, b = base + warp + 3;
-  return a >= g0 ? a : (b >= g0 ? b : a + kPeriod);
+  if (warp == 0) return kNoRound;
+  return g0 + ((warp - 1 - g0 % (W - 1)) + (W - 1)) % (W - 1);
 }
-__device__ __forceinline__ int next_round(int warp, int r) {
-  if (kDedicated) return r + 3;
-  if (warp == 0) return r + kPeriod;
-  return r % kPeriod == warp - 1 ? r + 4 : r + 3;
+template <int W>
+__device__ __forceinline__ int next_round(int, int r) {
+  return r + (W - 1);
 }
 
 __device__ __forceinline__ int piece_tiles(const fkv_work_t& d) {
@@ -146,15 +145,18 @@ __device__ __forceinline__ void stamp(int PROBE_, int i) {
 // SOLO (small shards): every warp streams its own pieces start to finish and
 // finalises them itself -- no hand-over -- so a short schedule keeps four
 // independent tile streams per CTA; a piece's owner warp is n_it >> 16.
-template <int G, int PROBE = 0, bool SOLO = false>
-__global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodeParams p) {
+template <int G, int PROBE = 0, int MODE = 0>
+__global__ void __launch_bounds__(Shape<MODE>::W * 32, Shape<MODE>::kCtasPerSm)
+    decode_kernel(const DecodeParams p) {
+  constexpr bool SOLO = MODE == 1;
+  constexpr int W = Shape<MODE>::W;
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ DecodeShared sh;
+  __shared__ DecodeShared<W> sh;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  constexpr int NS = SOLO ? kSmemBytes / (kWarps * 2 * kTileBytes) : kStages;  // ring stages per warp
-  constexpr bool kCombiner = kDedicated && !SOLO;  // warp 0 only combines
+  constexpr int NS = Shape<MODE>::NS;   // ring stages per streaming warp
+  constexpr bool kCombiner = !SOLO;     // warp 0 only combines
   uint8_t* ring = smem + (kCombiner ? (warp > 0 ? warp - 1 : 0) : warp) * NS * 2 * kTileBytes;
   uint64_t* wbars = sh.bars[warp];
   const fkv_work_t* tab = sh.tab;
@@ -188,7 +190,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodePara
   // CTA-wide round numbering (first_round / next_round)
   auto mine = [&](int pc) { return !SOLO || (tab[pc].n_it >> 16) == warp; };
   int p_pc = 0, p_G = 0, p_half = 0;  // piece, its first round, tile of the round
-  int p_r = SOLO ? 0 : first_round(warp, 0);  // next owned round (SOLO: round within the piece)
+  int p_r = SOLO ? 0 : first_round<W>(warp, 0);  // next owned round (SOLO: round within the piece)
   uint32_t p_seq = 0, c_seq = 0;
   int p_s = 0;
   bool p_done = kCombiner && warp == 0;  // the combiner warp streams nothing
@@ -218,7 +220,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodePara
       }
       const int tile = 2 * (SOLO ? p_r : p_r - p_G) + p_half;
       if (tile >= nt) {  // odd tail: one-tile round
-        p_r = SOLO ? p_r + 1 : next_round(warp, p_r);
+        p_r = SOLO ? p_r + 1 : next_round<W>(warp, p_r);
         p_half = 0;
         continue;
       }
@@ -235,7 +237,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodePara
       if (++p_s == NS) p_s = 0;
       if (++p_half == 2) {
         p_half = 0;
-        p_r = SOLO ? p_r + 1 : next_round(warp, p_r);
+        p_r = SOLO ? p_r + 1 : next_round<W>(warp, p_r);
       }
     }
   };
@@ -274,12 +276,12 @@ __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodePara
   asm volatile("griddepcontrol.launch_dependents;");
   load_q(0);
   if (warp == 0) stamp(PROBE, 1);
-  if (!SOLO && warp == 0) named_arrive(1);  // the hand-over slot starts free
+  if (!SOLO && warp == 0) named_arrive<W>(1);  // the hand-over slot starts free
 
   int c_s = 0;        // consumer stage
   uint32_t c_ph = 0;  // its mbarrier phase parity
   int G0 = 0;         // first round of the current piece
-  int c_r = SOLO ? 0 : first_round(warp, 0);  // next owned round
+  int c_r = SOLO ? 0 : first_round<W>(warp, 0);  // next owned round
   for (int pc = 0; pc < FKV_MAX_WORK; ++pc) {
     fkv_work_t d = tab[pc];
     if (d.n_it == 0) break;
@@ -305,7 +307,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodePara
 
     // this warp's rounds of the piece: two independent S chains per round, one
     // softmax max/shuffle/rescale step and one ring hand-back per 32 tokens
-    for (; c_r < G0 + nr; c_r = SOLO ? c_r + 1 : next_round(warp, c_r)) {
+    for (; c_r < G0 + nr; c_r = SOLO ? c_r + 1 : next_round<W>(warp, c_r)) {
       const int i = 2 * (c_r - G0);
       const bool two = i + 1 < nt;
       const int sA = c_s;
@@ -420,7 +422,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodePara
     // ---- hand the piece state to warp 0 (shared memory, named barriers):
     // bar 1 = slot free (warp 0 finished the previous piece), bar 2 = slot full
     if (!SOLO && warp != 0) {
-      named_sync(1);
+      named_sync<W>(1);
       float* x = &sh.xch[warp - 1][0][lane];
       x[0 * 32] = m0;
       x[1 * 32] = m1;
@@ -430,15 +432,15 @@ __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodePara
       for (int dt = 0; dt < 8; ++dt)
 #pragma unroll
         for (int e = 0; e < 4; ++e) x[(4 + 4 * dt + e) * 32] = acc[dt][e];
-      named_arrive(2);
+      named_arrive<W>(2);
       continue;
     }
     stamp(PROBE, 3);
-    if (!SOLO) named_sync(2);
+    if (!SOLO) named_sync<W>(2);
     stamp(PROBE, 4);
     // warp 0: lane-wise online-softmax combine of the four warps' states
 #pragma unroll 1
-    for (int w = 0; w < (SOLO ? 0 : kWarps - 1); ++w) {
+    for (int w = 0; w < (SOLO ? 0 : W - 1); ++w) {
       const float* x = &sh.xch[w][0][lane];
       const float om0 = x[0], om1 = x[32], ol0 = x[64], ol1 = x[96];
       const float nm0 = fmaxf(m0, om0), nm1 = fmaxf(m1, om1);
@@ -458,7 +460,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodePara
         acc[dt][3] = acc[dt][3] * a1 + x[(4 + 4 * dt + 3) * 32] * b1;
       }
     }
-    if (!SOLO && more) named_arrive(1);  // slot free for the next piece
+    if (!SOLO && more) named_arrive<W>(1);  // slot free for the next piece
 
     // ---- finalise this piece from registers (warp 0)
 #pragma unroll
@@ -611,12 +613,12 @@ __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodePara
     // warps split the G heads, each lane loads its columns of every piece's
     // record together with the lse values (one L2 round trip), weights by
     // warp shuffles.
-    named_sync(3);
+    named_sync<W>(3);
     const int n_it = sh.fin_n_it;
     if (n_it > 0) {
       const float* base = p.part + static_cast<int64_t>(sh.fin_i0) * G * FKV_REC;
       const int64_t orow = sh.fin_orow;
-      constexpr int kHpw = (G + kWarps - 1) / kWarps;  // heads per warp
+      constexpr int kHpw = (G + W - 1) / W;  // heads per warp
 #pragma unroll
       for (int hi = 0; hi < kHpw; ++hi) {
         const int g = warp * kHpw + hi;
@@ -673,7 +675,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) decode_kernel(const DecodePara
   // records to every peer by bumping its flag there (system-scope release).
   if (p.n_sig > 0 && (kCombiner || SOLO)) {
     __threadfence_system();  // every warp may have written peer records (merge above)
-    named_sync(3);
+    named_sync<W>(3);
   }
   if (p.n_sig > 0 && warp == 0) {
     __threadfence_system();
@@ -765,20 +767,20 @@ __global__ void __launch_bounds__(G * 32)
   }
 }
 
-template <int G, int PROBE = 0, bool SOLO = false>
+template <int G, int PROBE = 0, int MODE = 0>
 int launch_decode(const DecodeParams& p, cudaStream_t st) {
   static int grid_cap = 0;  // 2 persistent CTAs per SM
   if (!grid_cap) {
-    if (int rc = cuda_check(cudaFuncSetAttribute(decode_kernel<G, PROBE, SOLO>,
+    if (int rc = cuda_check(cudaFuncSetAttribute(decode_kernel<G, PROBE, MODE>,
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 kSmemBytes),
+                                                 Shape<MODE>::kSmem),
                             "decode smem attribute"))
       return rc;
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_kernel<G, PROBE, SOLO>, kWarps * 32,
-                                                  kSmemBytes);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_kernel<G, PROBE, MODE>,
+                                                  Shape<MODE>::W * 32, Shape<MODE>::kSmem);
     grid_cap = sms * (per_sm > 0 ? per_sm : 1);
   }
   // one CTA per worker; nothing in the kernel waits on another CTA, so the
@@ -787,8 +789,8 @@ int launch_decode(const DecodeParams& p, cudaStream_t st) {
   (void)grid_cap;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(p.n_workers, 1, 1);
-  cfg.blockDim = dim3(kWarps * 32, 1, 1);
-  cfg.dynamicSmemBytes = kSmemBytes;
+  cfg.blockDim = dim3(Shape<MODE>::W * 32, 1, 1);
+  cfg.dynamicSmemBytes = Shape<MODE>::kSmem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL (see kernel)
@@ -796,7 +798,7 @@ int launch_decode(const DecodeParams& p, cudaStream_t st) {
   static const bool no_pdl = getenv("FKV_NO_PDL") != nullptr;  // diagnostics
   cfg.attrs = attr;
   cfg.numAttrs = no_pdl ? 0 : 1;
-  return cuda_check(cudaLaunchKernelEx(&cfg, decode_kernel<G, PROBE, SOLO>, p), "decode launch");
+  return cuda_check(cudaLaunchKernelEx(&cfg, decode_kernel<G, PROBE, MODE>, p), "decode launch");
 }
 
 }  // namespace
@@ -804,33 +806,33 @@ int launch_decode(const DecodeParams& p, cudaStream_t st) {
 
 namespace fkv {
 namespace {
-int decode_entry(DecodeParams& p, int group, cudaStream_t st, int probe = 0, bool solo = false) {
-  if (solo) {
-    switch (group) {
-      case 4: return launch_decode<4, 0, true>(p, st);
-      case 8:
-        switch (probe) {
-          case 1: return launch_decode<8, 1, true>(p, st);
-          case 2: return launch_decode<8, 2, true>(p, st);
-          case 3: return launch_decode<8, 3, true>(p, st);
-          default: return launch_decode<8, 0, true>(p, st);
-        }
-      default: return set_error(FKV_ERR_INVALID, "fkv_decode: group must be 4 or 8");
-    }
+template <int MODE>
+int launch_mode(DecodeParams& p, int group, cudaStream_t st, int probe) {
+  if (group == 4) return launch_decode<4, 0, MODE>(p, st);
+  if (group != 8) return set_error(FKV_ERR_INVALID, "fkv_decode: group must be 4 or 8");
+  switch (probe) {
+    case 1: return launch_decode<8, 1, MODE>(p, st);
+    case 2: return launch_decode<8, 2, MODE>(p, st);
+    case 3: return launch_decode<8, 3, MODE>(p, st);
+    default: return launch_decode<8, 0, MODE>(p, st);
   }
-  if (probe == 1) return group == 8 ? launch_decode<8, 1>(p, st) : set_error(FKV_ERR_INVALID, "probe: G=8");
-  if (probe == 2) return group == 8 ? launch_decode<8, 2>(p, st) : set_error(FKV_ERR_INVALID, "probe: G=8");
-  if (probe == 3) return group == 8 ? launch_decode<8, 3>(p, st) : set_error(FKV_ERR_INVALID, "probe: G=8");
-  switch (group) {
-    case 4: return launch_decode<4>(p, st);
-    case 8: return launch_decode<8>(p, st);
-    default: return set_error(FKV_ERR_INVALID, "fkv_decode: group must be 4 or 8");
-  }
+}
+
+int decode_entry(DecodeParams& p, int group, cudaStream_t st, int probe, int flags) {
+  if (flags & FKV_DECODE_SOLO) return launch_mode<1>(p, group, st, probe);
+  if (flags & FKV_DECODE_WIDE) return launch_mode<2>(p, group, st, probe);
+  return launch_mode<0>(p, group, st, probe);
 }
 }  // namespace
 }  // namespace fkv
 
 static int g_probe = 0;
+
+extern "C" int fkv_decode_ctas_per_sm(int32_t flags) {
+  if (flags & FKV_DECODE_SOLO) return fkv::Shape<1>::kCtasPerSm;
+  if (flags & FKV_DECODE_WIDE) return fkv::Shape<2>::kCtasPerSm;
+  return fkv::Shape<0>::kCtasPerSm;
+}
 
 // Diagnostics (not part of fairkv.h): the next fkv_decode call runs probe mode
 // `mode` (1 = loads only, 2 = compute only).  Used by tools/probe_sizes.py.
@@ -894,7 +896,7 @@ extern "C" int fkv_decode_exchange(const void* q, const void* k, const void* v,
   p.my_rank = my_rank;
   const int probe = g_probe;
   g_probe = 0;
-  return decode_entry(p, group, static_cast<cudaStream_t>(stream), probe, (flags & FKV_DECODE_SOLO) != 0);
+  return decode_entry(p, group, static_cast<cudaStream_t>(stream), probe, flags);
 }
 
 extern "C" int fkv_merge_lse(const float* part, const int32_t* grp_ptr, const int32_t* src_idx,

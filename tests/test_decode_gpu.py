@@ -42,7 +42,7 @@ def build_cache(seg_lens, group, hkv, bt, device, seed=0, chunk=None):
 
 @pytest.mark.parametrize("group", [8, 4])
 @pytest.mark.parametrize("chunk", [None, 64, 128])
-@pytest.mark.parametrize("schedule", ["auto", "coop", "solo"])
+@pytest.mark.parametrize("schedule", ["auto", "coop", "wide", "solo"])
 def test_decode_matches_oracle(cuda_device, group, chunk, schedule, monkeypatch):
     """Both K4 schedules (CTA-cooperative pieces / per-warp pieces) and the
     host's automatic choice."""
@@ -58,7 +58,7 @@ def test_decode_matches_oracle(cuda_device, group, chunk, schedule, monkeypatch)
     seg_lens[4] = 65
     cache, q, ks, vs = build_cache(seg_lens, group, hkv, bt, cuda_device, chunk=chunk)
     if schedule != "auto" and chunk is None:
-        assert cache.flags == (1 if schedule == "solo" else 0)
+        assert cache.flags == {"coop": 0, "solo": 1, "wide": 2}[schedule]
     o, lse = ops.decode(q.to(cuda_device), cache)
     torch.cuda.synchronize()
     o_ref, lse_ref = okv.decode_heads(q.float().numpy().astype(np.float64), ks, vs, group)
@@ -66,7 +66,7 @@ def test_decode_matches_oracle(cuda_device, group, chunk, schedule, monkeypatch)
     torch.testing.assert_close(lse.cpu().double(), torch.from_numpy(lse_ref), rtol=0, atol=2e-3)
 
 
-@pytest.mark.parametrize("schedule", ["coop", "solo"])
+@pytest.mark.parametrize("schedule", ["coop", "wide", "solo"])
 def test_decode_many_segments_split(cuda_device, schedule, monkeypatch):
     """Many long segments: pieces split across CTAs / warps, merged by the
     fused K5 (several pieces per segment, the last CTA's cooperative merge)."""
@@ -136,7 +136,7 @@ def test_lse_merge_of_token_split_equals_whole(cuda_device):
     torch.testing.assert_close(lse[0].cpu().double(), torch.from_numpy(lse_ref), rtol=0, atol=2e-3)
 
 
-@pytest.mark.parametrize("schedule", ["coop", "solo"])
+@pytest.mark.parametrize("schedule", ["coop", "wide", "solo"])
 def test_decode_empty_and_tiny_segments(cuda_device, schedule, monkeypatch):
     """Zero-token segments (an AHA-DP copy can own no tokens) give o = 0 and
     lse = -inf; 1..17-token segments exercise the masked tails."""

@@ -1,11 +1,10 @@
-python - <<'PY' 2>&1 | tail -12
-import sys, os, json, argparse, time
+timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+SCHEDS="coop wide auto" python tools/probe_sched.py 2>&1
+FKV_K4_SCHEDULE=auto python - <<'PY' 2>&1 | tail -2
+import sys, os, json, argparse
 sys.path.insert(0, '.')
 import torch, bench
-a = argparse.Namespace(seed=0, budget=1024, batch=64, layers=80, context=32768, ch=4)
-budgets, _ = bench.workload(a)
-t0 = time.time()
-r = bench.full_layer(a, budgets, torch.device('cuda'))
-print("elapsed", time.time() - t0)
-for k, v in r.items(): print(k, v if k == "note" else {m: {x: round(y, 3) for x, y in d.items() if y is not None} for m, d in v.items()})
+a = argparse.Namespace(seed=0)
+r = bench.cfg2_sweep(a, torch.device('cuda'), 6549.1)
+print(os.environ["FKV_K4_SCHEDULE"], {k: (round(v['ms_per_step']*1e3/32, 2), round(v['hbm_frac'], 3), v['schedule']) for k, v in r.items()})
 PY

@@ -22,7 +22,7 @@ for B in budgets_list:
         plan, prof = bench.make_plan(budgets, tp, 8 if tp == 8 else 4, mode)
         shards, _ = plan_layouts(plan, budgets, G)
         line = f"B={B:5d} tp{tp} {mode:4s}"
-        for sched in ("coop", "solo"):
+        for sched in os.environ.get("SCHEDS", "coop wide solo auto").split():
             os.environ["FKV_K4_SCHEDULE"] = sched
             worst = 0.0
             for g in range(tp):
@@ -36,8 +36,6 @@ for B in budgets_list:
                 gr.replay()
                 t = bench.timed(gr.replay, 3) / 3 / L
                 worst = max(worst, t)
-                if tp == 1 and sched == "solo" and caches[0].flags == 0:
-                    break
             line += f"  {sched} {worst*1e6:6.1f}us"
         print(line, flush=True)
     del base
