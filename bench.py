@@ -406,6 +406,7 @@ def run_fairkv(args):
         out["emulated_tp_budget_sweep"] = budget_sweep(args, dev)
         out["cfg2_llama3.1-8b_b256_T16k"] = cfg2_sweep(args, dev, peak)
         out["full_layer"] = full_layer(args, budgets, dev)
+        out["append"] = append_cost(args, budgets, dev)
     if rank == 0 and world == 1 and not args.no_cpu:
         out["planner"] = planner_compare(budgets)
     if rank == 0 and world == 1 and not args.no_emulate:
@@ -632,6 +633,25 @@ def cfg2_sweep(args, dev, peak):
         del g, caches, wss
         torch.cuda.empty_cache()
     return rows
+
+
+def append_cost(args, budgets, dev):
+    """Decode-time append (ops.append: the step's new K/V row into every
+    segment's headroom, work table grown on the device) on one 70B layer of
+    the workload: microseconds per layer-step, next to the layer's K4."""
+    import numpy as np
+    import torch
+    from paper_2502_15804_b200 import ops
+    from paper_2502_15804_b200.cache import LayerCache
+    bt = budgets.shape[1]
+    qrow = np.array([b * HQ + h * GROUP for b in range(bt) for h in range(HKV)])
+    c = LayerCache.allocate(budgets[0].reshape(-1), qrow, qrow, GROUP, dev, fill="random", reserve=64)
+    kn = torch.randn((bt, HKV, HEAD_DIM), device=dev).to(torch.bfloat16)
+    vn = torch.randn_like(kn)
+    ops.append(c, kn, vn)
+    t = timed(lambda: ops.append(c, kn, vn), 20) / 20
+    return {"us_per_layer_step": t * 1e6, "segments": c.n_segments,
+            "note": "one launch per layer and step; 64-row headroom per segment"}
 
 
 def budget_sweep(args, dev):

@@ -254,6 +254,17 @@ int fkv_compact(const void* k_src, const void* v_src, int32_t T, int32_t n_segme
                 const int32_t* seg_lo, const int32_t* seg_hi, const int64_t* seg_row0,
                 int32_t zero_pad, int32_t max_tokens, void* k_dst, void* v_dst, void* stream);
 
+/* Decode-time append: segment s with src_row[s] >= 0 (it owns the end of its
+ * head's token axis) receives row src_row[s] of k_new / v_new (bf16 [*,128])
+ * at cache row seg_row0[s] + seg_len[s] (swizzled); seg_len[s] and the n_tok
+ * of its last piece work[last_piece[s]] (flat fkv_work_t index) grow by one.
+ * Segments already at seg_cap[s] rows are skipped and counted in *overflow.
+ * One launch per layer and step; no host synchronisation. */
+int fkv_append(const void* k_new, const void* v_new, const int32_t* src_row,
+               const int64_t* seg_row0, int32_t* seg_len, const int32_t* seg_cap, void* work,
+               const int32_t* last_piece, int32_t n_segments, int32_t* overflow, void* k_dst,
+               void* v_dst, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

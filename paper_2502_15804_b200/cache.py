@@ -430,14 +430,18 @@ class LayerCache:
 
     @staticmethod
     def allocate(seg_len, seg_qrow, seg_out_row, group: int, device, chunk: int | None = None,
-                 fill: str = "zeros", generator: torch.Generator | None = None) -> "LayerCache":
+                 fill: str = "zeros", generator: torch.Generator | None = None,
+                 reserve: int = 0) -> "LayerCache":
         """Lay out segments and build the work plan.  ``fill='zeros'`` leaves
         the storage for the compaction kernel; ``fill='random'`` writes N(0,1)
         bf16 into every retained row (synthetic benchmark caches; the swizzle
         is a permutation, so random data needs no packing) and keeps padding
-        rows zero."""
+        rows zero.  ``reserve``: rows of headroom per segment for decode-time
+        appends (``ops.append``; segment s receives row s of the step's
+        [Bt, Hkv, 128] K/V)."""
         seg_len = np.asarray(seg_len, dtype=np.int64)
-        row0, rows = segment_offsets(seg_len)
+        cap = page_rows(seg_len + int(reserve))
+        row0, rows = segment_offsets(seg_len + int(reserve))
         dev = torch.device(device)
         k = torch.zeros((rows, HEAD_DIM), dtype=torch.bfloat16, device=dev)
         v = torch.zeros((rows, HEAD_DIM), dtype=torch.bfloat16, device=dev)
@@ -452,26 +456,39 @@ class LayerCache:
             k.mul_(valid[:, None])
             v.mul_(valid[:, None])
 
-        return LayerCache._build(k, v, row0, seg_len, seg_qrow, seg_out_row, group, chunk)
+        return LayerCache._build(k, v, row0, seg_len, seg_qrow, seg_out_row, group, chunk,
+                                 seg_cap=cap, append_src=np.arange(len(seg_len)))
 
     @staticmethod
     def view(k: torch.Tensor, v: torch.Tensor, seg_row0, seg_len, seg_qrow, seg_out_row,
-             group: int, chunk: int | None = None) -> "LayerCache":
+             group: int, chunk: int | None = None, seg_cap=None, append_src=None) -> "LayerCache":
         """A segment table over existing storage (e.g. the DP copies / shards
         of a base cache: each copy is a 16-aligned sub-range of its head's
-        rows).  No data moves."""
+        rows).  No data moves.  ``seg_cap`` / ``append_src``: append headroom
+        and the K/V row each segment receives per decode step (-1: none, e.g.
+        a DP copy that does not own the end of its head)."""
         seg_row0 = np.asarray(seg_row0, dtype=np.int64)
         seg_len = np.asarray(seg_len, dtype=np.int64)
         if np.any(seg_row0 % 16):
             raise ValueError("segment starts must be multiples of 16 rows")
-        return LayerCache._build(k, v, seg_row0, seg_len, seg_qrow, seg_out_row, group, chunk)
+        return LayerCache._build(k, v, seg_row0, seg_len, seg_qrow, seg_out_row, group, chunk,
+                                 seg_cap=seg_cap, append_src=append_src)
 
     @staticmethod
-    def _build(k, v, seg_row0, seg_len, seg_qrow, seg_out_row, group, chunk) -> "LayerCache":
+    def _build(k, v, seg_row0, seg_len, seg_qrow, seg_out_row, group, chunk, seg_cap=None,
+               append_src=None) -> "LayerCache":
         dev = k.device
         seg_row0 = np.asarray(seg_row0, dtype=np.int64)
+        seg_len = np.asarray(seg_len, dtype=np.int64)
         item_seg, t0, t1, ptr, wptr, wlist, tab, flags = plan_schedule(seg_len, seg_row0, seg_qrow,
                                                                        seg_out_row, dev, chunk)
+        # flat work-table index of every segment's last piece (append grows it)
+        valid = (tab[:, :, 7] & 0xFFFF) != 0
+        pos_of_item = np.zeros(max(len(item_seg), 1), dtype=np.int64)
+        pos_of_item[tab[:, :, 5][valid]] = np.flatnonzero(valid.reshape(-1))
+        last_piece = pos_of_item[np.asarray(ptr[1:], dtype=np.int64) - 1] if len(seg_len) else np.zeros(0)
+        seg_cap = seg_len if seg_cap is None else np.asarray(seg_cap, dtype=np.int64)
+        append_src = np.full(len(seg_len), -1) if append_src is None else np.asarray(append_src)
 
         def i32(a):
             return torch.as_tensor(np.ascontiguousarray(a, dtype=np.int32), device=dev)
@@ -485,5 +502,13 @@ class LayerCache:
             counters=torch.zeros(max(len(item_seg), 1), dtype=torch.int32, device=dev),
             host={"seg_len": seg_len, "seg_row0": seg_row0, "chunk": chunk, "n_workers": len(wptr) - 1,
                   "seg_qrow": np.asarray(seg_qrow), "seg_out_row": np.asarray(seg_out_row),
-                  "flags": flags},
+                  "flags": flags, "seg_cap": seg_cap,
+                  "seg_cap_t": i32(seg_cap), "append_src_t": i32(append_src),
+                  "last_piece_t": i32(last_piece),
+                  "overflow_t": torch.zeros(1, dtype=torch.int32, device=dev)},
         )
+
+    def sync_lengths(self) -> np.ndarray:
+        """Read the device segment lengths back (after appends) into host state."""
+        self.host["seg_len"] = self.seg_len.cpu().numpy().astype(np.int64)
+        return self.host["seg_len"]

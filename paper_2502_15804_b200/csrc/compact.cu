@@ -96,3 +96,65 @@ extern "C" int fkv_compact(const void* k_src, const void* v_src, int32_t T, int3
       seg_lo, seg_hi, seg_row0, zero_pad, static_cast<uint4*>(k_dst), static_cast<uint4*>(v_dst));
   return cuda_check(cudaGetLastError(), "compact launch");
 }
+
+// ---------------------------------------------------------------- append ----
+// Decode-time growth of the compressed cache: every segment that owns the end
+// of its head's token axis (a whole head, or the last AHA-DP copy) gets the
+// step's new K/V row.  One half-warp per segment: the 256-B row is stored
+// swizzled at cache row row0[s] + len[s] (the segment's reserved headroom),
+// then lane 0 bumps len[s] and the n_tok of the segment's last piece in the
+// decode work table, so the next fkv_decode sees the token with no host
+// round trip.  A segment at capacity is left unchanged and flagged in
+// *overflow (the host re-lays the cache out).
+namespace fkv {
+namespace {
+__global__ void __launch_bounds__(256)
+    append_kernel(const uint4* __restrict__ k_new, const uint4* __restrict__ v_new,
+                  const int32_t* __restrict__ src_row, const int64_t* __restrict__ seg_row0,
+                  int32_t* __restrict__ seg_len, const int32_t* __restrict__ seg_cap,
+                  int32_t* __restrict__ work_ntok, const int32_t* __restrict__ last_piece,
+                  int n_segments, int32_t* __restrict__ overflow, uint4* __restrict__ k_dst,
+                  uint4* __restrict__ v_dst) {
+  const int s = blockIdx.x * 16 + (threadIdx.x >> 4);
+  const int c = threadIdx.x & 15;
+  if (s >= n_segments) return;
+  const int src = src_row[s];
+  if (src < 0) return;  // this segment does not own the end of its head
+  const int len = seg_len[s];
+  if (len >= seg_cap[s]) {
+    if (c == 0) atomicAdd(overflow, 1);
+    return;
+  }
+  const uint4 kv = __ldg(k_new + static_cast<int64_t>(src) * 16 + c);
+  const uint4 vv = __ldg(v_new + static_cast<int64_t>(src) * 16 + c);
+  const int64_t dst = seg_row0[s] + len;
+  const int64_t o = dst * 16 + (c ^ static_cast<int>(dst & 7));
+  k_dst[o] = kv;
+  v_dst[o] = vv;
+  if (c == 0) {
+    seg_len[s] = len + 1;
+    work_ntok[static_cast<int64_t>(last_piece[s]) * 8] += 1;  // fkv_work_t.n_tok (int32 #2)
+  }
+}
+}  // namespace
+}  // namespace fkv
+
+extern "C" int fkv_append(const void* k_new, const void* v_new, const int32_t* src_row,
+                          const int64_t* seg_row0, int32_t* seg_len, const int32_t* seg_cap,
+                          void* work, const int32_t* last_piece, int32_t n_segments,
+                          int32_t* overflow, void* k_dst, void* v_dst, void* stream) {
+  using namespace fkv;
+  if (n_segments < 0) return set_error(FKV_ERR_INVALID, "fkv_append: bad sizes");
+  if (n_segments == 0) return FKV_OK;
+  if (!k_new || !v_new || !src_row || !seg_row0 || !seg_len || !seg_cap || !work || !last_piece ||
+      !overflow || !k_dst || !v_dst)
+    return set_error(FKV_ERR_INVALID, "fkv_append: null pointer");
+  if ((reinterpret_cast<uintptr_t>(k_new) | reinterpret_cast<uintptr_t>(v_new) |
+       reinterpret_cast<uintptr_t>(k_dst) | reinterpret_cast<uintptr_t>(v_dst)) & 15)
+    return set_error(FKV_ERR_INVALID, "fkv_append: buffers must be 16-byte aligned");
+  append_kernel<<<(n_segments + 15) / 16, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const uint4*>(k_new), static_cast<const uint4*>(v_new), src_row, seg_row0, seg_len,
+      seg_cap, static_cast<int32_t*>(work) + 2, last_piece, n_segments, overflow,
+      static_cast<uint4*>(k_dst), static_cast<uint4*>(v_dst));
+  return cuda_check(cudaGetLastError(), "append launch");
+}

@@ -21,11 +21,16 @@ from .sharding import FinalMerge, LayerShard
 
 def rank_caches(shards: list[LayerShard], bt: int, hq: int, group: int, tp: int, device,
                 *, base: list[LayerCache] | None = None, base_index=None, fill: str = "random",
-                seed: int = 0) -> list[LayerCache]:
+                seed: int = 0, reserve: int = 0, head_len=None) -> list[LayerCache]:
     """Per-layer caches of one rank.  With ``base`` (full per-head caches, one
     segment per (b, h) in b-major order) the rank's segments are views into
     it (DP copies = 16-aligned sub-ranges); otherwise fresh storage filled
-    with ``fill``."""
+    with ``fill`` and ``reserve`` rows of append headroom per segment.
+
+    Decode-time appends (``ops.append`` with the step's K/V [Bt, Hkv, 128]):
+    only the segment that owns the end of its head's token axis (a whole
+    head, or the last DP copy) takes the new token -- known from the base
+    cache's lengths, or from ``head_len`` [L][Bt, Hkv] for fresh storage."""
     hkv = hq // group
     out = []
     gen = torch.Generator(device=device).manual_seed(seed)
@@ -34,13 +39,25 @@ def rank_caches(shards: list[LayerShard], bt: int, hq: int, group: int, tp: int,
         # tp > 1: segment i's record rows are slot i's G heads; tp == 1: o rows
         out_row = np.arange(sh.n_segments) * group if tp > 1 else qrow
         lens = sh.seg_hi - sh.seg_lo
+        bh = sh.seg_b * hkv + sh.seg_h
         if base is not None:
             b0 = base[l].host["seg_row0"]
-            row0 = b0[sh.seg_b * hkv + sh.seg_h] + sh.seg_lo
-            out.append(LayerCache.view(base[l].k, base[l].v, row0, lens, qrow, out_row, group))
+            full = base[l].host["seg_len"][bh]
+            owns_end = sh.seg_hi >= full
+            cap = np.where(owns_end, base[l].host["seg_cap"][bh] - sh.seg_lo, lens)
+            src = np.where(owns_end, bh, -1)
+            row0 = b0[bh] + sh.seg_lo
+            out.append(LayerCache.view(base[l].k, base[l].v, row0, lens, qrow, out_row, group,
+                                       seg_cap=cap, append_src=src))
         else:
-            out.append(LayerCache.allocate(lens, qrow, out_row, group, device, fill=fill,
-                                           generator=gen))
+            c = LayerCache.allocate(lens, qrow, out_row, group, device, fill=fill, generator=gen,
+                                    reserve=reserve)
+            if head_len is not None:
+                owns_end = sh.seg_hi >= np.asarray(head_len[l]).reshape(-1)[bh]
+                c.host["append_src_t"].copy_(torch.as_tensor(np.where(owns_end, bh, -1).astype(np.int32)))
+            else:
+                c.host["append_src_t"].copy_(torch.as_tensor(bh.astype(np.int32)))
+            out.append(c)
     return out
 
 

@@ -141,6 +141,25 @@ def decode(q: torch.Tensor, cache: LayerCache, *, out: torch.Tensor | None = Non
     return out, out_lse
 
 
+def append(cache: LayerCache, k_new: torch.Tensor, v_new: torch.Tensor):
+    """Decode-time append of one token per (request, KV head): segment s takes
+    row ``append_src[s]`` of k_new / v_new (bf16 [Bt, Hkv, 128]) into its
+    reserved headroom; the work table's last piece grows on the device, so
+    the next ``decode`` includes it.  Segments at capacity are skipped and
+    counted in ``cache.host['overflow_t']`` (re-lay the cache out then)."""
+    _need_cuda(k_new, v_new, cache.k)
+    if k_new.dtype != torch.bfloat16 or k_new.shape != v_new.shape or k_new.shape[-1] != HEAD_DIM \
+            or not (k_new.is_contiguous() and v_new.is_contiguous()):
+        raise NativeError("k_new / v_new must be contiguous bf16 [..., 128] of one shape")
+    h = cache.host
+    _native.check(_lib.fkv_append(k_new.data_ptr(), v_new.data_ptr(), h["append_src_t"].data_ptr(),
+                                  cache.seg_row0.data_ptr(), cache.seg_len.data_ptr(),
+                                  h["seg_cap_t"].data_ptr(), cache.work.data_ptr(),
+                                  h["last_piece_t"].data_ptr(), cache.n_segments,
+                                  h["overflow_t"].data_ptr(), cache.k.data_ptr(), cache.v.data_ptr(),
+                                  _stream()))
+
+
 # ------------------------------------------------- compression (prefill) ----
 def score(q_win: torch.Tensor, k: torch.Tensor, window: int | None = None, pool_k: int = 7,
           sm_scale: float | None = None, workspace: torch.Tensor | None = None) -> torch.Tensor:

@@ -153,3 +153,54 @@ def test_decode_empty_and_tiny_segments(cuda_device, schedule, monkeypatch):
     empty = torch.from_numpy(np.isneginf(lse_ref))
     assert torch.isneginf(lse_c[empty]).all()
     torch.testing.assert_close(lse_c[~empty], torch.from_numpy(lse_ref)[~empty], rtol=0, atol=2e-3)
+
+
+@pytest.mark.parametrize("schedule", ["coop", "wide", "solo"])
+def test_append_then_decode(cuda_device, schedule, monkeypatch):
+    """Decode-time appends: each step writes the new token's K/V into every
+    segment's headroom (device-side length + work-table update); decode after
+    every step equals the oracle over the grown rows; capacity overflow is
+    counted, not written."""
+    from paper_2502_15804_b200 import ops
+    monkeypatch.setenv("FKV_K4_SCHEDULE", schedule)
+    from paper_2502_15804_b200.cache import LayerCache, segment_offsets
+    group, hkv, bt = 8, 8, 2
+    rng = np.random.default_rng(21)
+    seg_lens = rng.integers(1, 900, size=bt * hkv)
+    seg_lens[3] = 63  # one row short of a page: overflows after one append with reserve 0...
+    hq = hkv * group
+    qrow = [b * hq + h * group for b in range(bt) for h in range(hkv)]
+    reserve = 3
+    cache = LayerCache.allocate(seg_lens, qrow, qrow, group, cuda_device, reserve=reserve)
+    row0 = cache.host["seg_row0"]
+    g = torch.Generator().manual_seed(22)
+    ks = [torch.randn(int(n), 128, generator=g).to(torch.bfloat16) for n in seg_lens]
+    vs = [torch.randn(int(n), 128, generator=g).to(torch.bfloat16) for n in seg_lens]
+    kh = torch.zeros(cache.k.shape, dtype=torch.bfloat16)
+    vh = torch.zeros(cache.v.shape, dtype=torch.bfloat16)
+    for r0, k, v in zip(row0, ks, vs):
+        kh[r0:r0 + len(k)] = torch.from_numpy(okv.swizzle_rows(k.view(torch.int16).numpy(), r0)).view(torch.bfloat16)
+        vh[r0:r0 + len(v)] = torch.from_numpy(okv.swizzle_rows(v.view(torch.int16).numpy(), r0)).view(torch.bfloat16)
+    cache.k.copy_(kh)
+    cache.v.copy_(vh)
+    cap = cache.host["seg_cap"]
+    q = torch.randn(bt, hq, 128, generator=g).to(torch.bfloat16)
+    steps = int((cap - seg_lens).min()) + 2  # the tightest segment overflows twice
+    for step in range(steps):
+        kn = torch.randn(bt, hkv, 128, generator=g).to(torch.bfloat16)
+        vn = torch.randn(bt, hkv, 128, generator=g).to(torch.bfloat16)
+        ops.append(cache, kn.to(cuda_device), vn.to(cuda_device))
+        for s in range(bt * hkv):
+            if len(ks[s]) < cap[s]:
+                b, h = divmod(s, hkv)
+                ks[s] = torch.cat([ks[s], kn[b, h][None]])
+                vs[s] = torch.cat([vs[s], vn[b, h][None]])
+        o, lse = ops.decode(q.to(cuda_device), cache)
+        torch.cuda.synchronize()
+        kk = [x.float().numpy().astype(np.float64) for x in ks]
+        vv = [x.float().numpy().astype(np.float64) for x in vs]
+        o_ref, lse_ref = okv.decode_heads(q.float().numpy().astype(np.float64), kk, vv, group)
+        torch.testing.assert_close(o.float().cpu().double(), torch.from_numpy(o_ref), rtol=2e-2, atol=1e-2)
+        torch.testing.assert_close(lse.cpu().double(), torch.from_numpy(lse_ref), rtol=0, atol=2e-3)
+    assert np.array_equal(cache.sync_lengths(), np.array([len(x) for x in ks]))
+    assert int(cache.host["overflow_t"].item()) >= 2
