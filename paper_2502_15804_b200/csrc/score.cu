@@ -103,6 +103,28 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// 32 consecutive fp32 TMEM columns of this thread's lane, no wait (pair
+// with tmem_wait_ld: several loads in flight per wait).
+__device__ __forceinline__ void tmem_ld32_nw(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// Wait, then pin the loaded registers behind the wait: the register uses have
+// no data dependence on the wait otherwise and could be scheduled above it.
+__device__ __forceinline__ void tmem_wait_ld(uint32_t (&a)[32], uint32_t (&b)[32]) {
+  tmem_wait_ld();
+#pragma unroll
+  for (int i = 0; i < 32; ++i) asm volatile("" : "+r"(a[i]), "+r"(b[i]));
+}
+
 // 32 consecutive fp32 TMEM columns of this thread's lane.
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   uint32_t r[32];
@@ -665,30 +687,42 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&sm.tfull[buf], (it >> 1) & 1);
         tc_fence_after();
         const int ts = (a1 + it) * kBN;
+        // two 32-column chunks per TMEM wait, one running-max rescale per 64
+        // columns, four independent sum chains
 #pragma unroll 1
-        for (int cb = cb0; cb < cb1; ++cb) {
-          float v[32];
-          tmem_ld32(tmem + lane_base + buf * GW + mh * kBN + cb * 32, v);
+        for (int cb = cb0; cb < cb1; cb += 2) {
+          uint32_t ra[32], rb[32];
+          tmem_ld32_nw(tmem + lane_base + buf * GW + mh * kBN + cb * 32, ra);
+          tmem_ld32_nw(tmem + lane_base + buf * GW + mh * kBN + (cb + 1) * 32, rb);
+          tmem_wait_ld(ra, rb);
+          float v[64];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(ra[i]), v[32 + i] = __uint_as_float(rb[i]);
           const int c0 = ts + cb * 32;
           float bmax = -CUDART_INF_F;
-          if (c0 + 31 > limit) {  // only the window's tiles (and the tail) need masking
+          if (c0 + 63 > limit) {  // only the window's tiles (and the tail) need masking
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
+            for (int i = 0; i < 64; ++i) {
               v[i] = c0 + i <= limit ? v[i] : -CUDART_INF_F;
               bmax = fmaxf(bmax, v[i]);
             }
             if (bmax == -CUDART_INF_F) continue;
           } else {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) bmax = fmaxf(bmax, v[i]);
+            for (int i = 0; i < 64; ++i) bmax = fmaxf(bmax, v[i]);
           }
           // running max kept in raw-score units, exponents via one FFMA each
           const float nm = fmaxf(m, bmax);
           const float nms = nm * p.scale_log2;
-          float acc = 0.f;
+          float e0 = 0.f, e1 = 0.f, e2 = 0.f, e3 = 0.f;  // (a1/a2 name the tile starts)
 #pragma unroll
-          for (int i = 0; i < 32; ++i) acc += fast_exp2(fmaf(v[i], p.scale_log2, -nms));
-          l = l * fast_exp2((m - nm) * p.scale_log2) + acc;
+          for (int i = 0; i < 64; i += 4) {
+            e0 += fast_exp2(fmaf(v[i], p.scale_log2, -nms));
+            e1 += fast_exp2(fmaf(v[i + 1], p.scale_log2, -nms));
+            e2 += fast_exp2(fmaf(v[i + 2], p.scale_log2, -nms));
+            e3 += fast_exp2(fmaf(v[i + 3], p.scale_log2, -nms));
+          }
+          l = l * fast_exp2((m - nm) * p.scale_log2) + ((e0 + e1) + (e2 + e3));
           m = nm;
         }
         tc_fence_before();
