@@ -254,7 +254,19 @@ def run_fairkv(args):
     endpoint = None
     if tp > 1 and args.exchange == "p2p":
         from paper_2502_15804_b200.exchange import P2PGroup
-        endpoint = P2PGroup.connect(rank, tp, finals[0].slots, GROUP).endpoints[0]
+        try:
+            endpoint = P2PGroup.connect(rank, tp, finals[0].slots, GROUP).endpoints[0]
+            ok = 1
+        except Exception as exc:  # e.g. no CUDA IPC / peer access between these GPUs
+            print(f"rank {rank}: P2P exchange unavailable ({exc}); using NCCL all-gather",
+                  file=sys.stderr)
+            ok = 0
+        # every rank must take the same exchange path
+        flag = torch.tensor([ok], dtype=torch.int32,
+                            device="cpu" if dist.get_backend() == "gloo" else dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if int(flag.item()) == 0 and not shared:
+            args.exchange, endpoint = "nccl", None
     dec = StackDecoder(caches, finals if tp > 1 else None, tp=tp, bt=args.batch, hq=HQ, group=GROUP,
                        exchange=args.exchange, endpoint=endpoint)
     gq = torch.Generator(device=dev).manual_seed(123)
