@@ -334,7 +334,7 @@ def run_fairkv(args):
     # layers per copy: large groups in the middle (fewer, larger PCIe
     # transfers), a single layer first and last so that only one layer's H2D
     # and one layer's D2H are exposed outside the compute
-    cg = 8
+    cg = int(os.environ.get("FKV_E2E_GROUP", "4"))  # measured best of 1/2/4/8/16/40
     cuts = sorted({0, min(1, args.layers), max(args.layers - 1, 0), args.layers,
                    *range(1, args.layers - 1, cg)})
     groups = [(a, b) for a, b in zip(cuts, cuts[1:]) if b > a]
