@@ -543,7 +543,7 @@ def emulate_tp(args, budgets, dev, calibrate=True):
         for mode in modes:
             ch = args.ch if mode != "dp" or tp != 8 else 8  # equal split needs CH=8 at TP=8
             plan, prof = make_plan(budgets, tp, ch, mode)
-            shards, _ = plan_layouts(plan, budgets, GROUP)
+            shards, finals = plan_layouts(plan, budgets, GROUP)
             per_rank = [rank_caches([s[g] for s in shards], bt, HQ, GROUP, tp, dev, base=base)
                         for g in range(tp)]
             sends = [[torch.empty((max(c.n_segments, 1), GROUP, ops.REC), device=dev) for c in pr]
@@ -582,6 +582,20 @@ def emulate_tp(args, budgets, dev, calibrate=True):
                 del gg
             step = t.max(axis=1).sum()
             step_br = t_br.max(axis=1).sum()
+            # K5 after the all-gather (identical on every rank): LSE merge of
+            # the gathered records of each layer, 80 launches back to back
+            recv = torch.zeros((tp * finals[0].slots, GROUP, ops.REC), device=dev)
+            tabs5 = [tuple(torch.as_tensor(x, device=dev) for x in (f.grp_ptr, f.src_idx, f.out_row))
+                     for f in finals]
+            o5 = torch.empty((bt, HQ, HEAD_DIM), dtype=torch.bfloat16, device=dev)
+
+            def run_k5():
+                for l in range(L):
+                    ops.merge_lse(recv, *tabs5[l], GROUP, out_bf16=o5)
+            g5 = capture(run_k5)
+            g5.replay()
+            k5 = timed(g5.replay, 3) / 3
+            del g5, recv
             loads = rank_loads(plan, budgets, GROUP)
             for l in range(L):
                 for g in range(tp):
@@ -589,6 +603,7 @@ def emulate_tp(args, budgets, dev, calibrate=True):
             sim = fk.simulate(prof, plan, model, fk.SimulationConfig(1, 1, tp)).throughput
             row[mode] = {"tokens_per_s": bt / step, "stack_ms": step * 1e3,
                          "tokens_per_s_bracketed": bt / step_br,
+                         "tokens_per_s_with_k5": bt / (step + k5), "k5_us_per_layer": k5 / L * 1e6,
                          "busy_rate": float(t.sum() / (step * tp)),
                          "kv_max_over_mean": imbalance_ratio(loads),
                          "extra_copies": int(sum(len(gr) for la in plan.layers for gr in la.groups) - L * HKV),
@@ -604,7 +619,8 @@ def emulate_tp(args, budgets, dev, calibrate=True):
                        "(event nodes in one CUDA graph), minus the per-launch bracketing overhead measured by "
                        "timing the rank's 80 layers back to back; layer span = max over ranks (synchronous "
                        "per-layer barrier, reference simulate.py:118-136); all-gather not included (single "
-                       "GPU); tokens_per_s_bracketed = without the correction; sim = reference simulator, "
+                       "GPU); tokens_per_s_with_k5 adds the post-exchange LSE merge (K5) of every layer; "
+                       "tokens_per_s_bracketed = without the correction; sim = reference simulator, "
                        "pure-cache latency model")
     return results
 
