@@ -777,6 +777,7 @@ def prefill_compress(peaks):
     rows = {}
     for name, (bt, hq, hkv, T, B) in {"llama-3.1-8b_T16k_B256": (1, 32, 8, 16384, 256),
                                      "llama-3.1-8b_T16k_B256_batch4": (4, 32, 8, 16384, 256),
+                                     "llama-3.1-8b_T16k_B256_batch32": (32, 32, 8, 16384, 256),
                                      "llama-3.3-70b_T32k_B1024": (1, 64, 8, 32768, 1024),
                                      "llama-3.3-70b_T128k_B1024": (1, 64, 8, 131072, 1024)}.items():
         w = WINDOW
@@ -787,13 +788,15 @@ def prefill_compress(peaks):
         ws = torch.empty(int(ops._lib.fkv_score_workspace_bytes(bt, hkv, T, w, hq // hkv)),
                          dtype=torch.uint8, device=dev)
         sc = ops.score(q, k, workspace=ws)
-        hb, off, idx = ops.ada_select(sc, B, w)
+        wsel = torch.empty(int(ops._lib.fkv_ada_select_workspace_bytes(bt, hkv, T - w)), dtype=torch.uint8,
+                           device=dev)
+        hb, off, idx = ops.ada_select(sc, B, w, workspace=wsel)
         for _ in range(3):  # warm: first launches set attributes / encode tensor maps
             ops.score(q, k, workspace=ws)
-            ops.ada_select(sc, B, w)
+            ops.ada_select(sc, B, w, workspace=wsel)
             ops.score_select(q, k, B, w, workspace=ws)
         t_score = timed(lambda: ops.score(q, k, workspace=ws), 10) / 10
-        t_sel = timed(lambda: ops.ada_select(sc, B, w), 10) / 10
+        t_sel = timed(lambda: ops.ada_select(sc, B, w, workspace=wsel), 10) / 10
         t_fused = timed(lambda: ops.score_select(q, k, B, w, workspace=ws), 10) / 10
         cache, _, _ = ops.compress_layer(q, k, v, B, w)
         sbh, slo, shi = cache.host["compact_args"]
@@ -806,6 +809,8 @@ def prefill_compress(peaks):
         rows[name] = {
             "score_us": t_score * 1e6, "ada_select_us": t_sel * 1e6, "compact_us": t_cmp * 1e6,
             "score_select_fused_us": t_fused * 1e6,
+            "score_select_path": "one cooperative launch" if bt * hkv <= 148
+            else "score launches + grid-wide ada_select",
             "score_tflops": flops / t_score / 1e12, "score_tflops_frac": flops / t_score / 1e12 / tf_peak,
             "score_K_read_GBs_per_pass": kbytes / (t_score / 2) / 1e9,
             "roofline_us": max(flops / (tf_peak * 1e12), 2 * kbytes / (float(peaks.get("hbm_gbs", 6650.0)) * 1e9)) * 1e6,

@@ -236,13 +236,19 @@ int fkv_ada_budgets(const float* scores, int32_t batch, int32_t hkv, int32_t n, 
 int fkv_topk_select(const float* scores, const int32_t* budgets, int32_t batch, int32_t hkv,
                     int32_t n, int32_t window, int64_t* offsets, int32_t* idx, void* stream);
 
-/* A18 + K2 fused: one thread-block cluster per request (one CTA per KV head,
- * Hkv <= 8) computes the budgets, the offsets (request b starts at
- * b*hkv*budget) and the ascending index lists in a single launch; results are
- * identical to fkv_ada_budgets followed by fkv_topk_select. */
+/* A18 + K2 fused: one cooperative launch over every (request, head) -- the
+ * keys of each head are cut into chunks dealt out to persistent CTAs, a
+ * four-pass radix search over the 32-bit score finds every request's Ada
+ * threshold and every head's own floor threshold at once (grid barriers
+ * between passes), and each CTA writes its chunks' chosen tokens.  Budgets,
+ * offsets (request b starts at b*hkv*budget) and the ascending index lists
+ * are identical to fkv_ada_budgets followed by fkv_topk_select.  Hkv <= 16.
+ * workspace: device bytes >= fkv_ada_select_workspace_bytes(batch, hkv, n);
+ * no initial contents required (reset inside, stream-ordered). */
+int64_t fkv_ada_select_workspace_bytes(int32_t batch, int32_t hkv, int32_t n);
 int fkv_ada_select(const float* scores, int32_t batch, int32_t hkv, int32_t n, int32_t budget,
                    int32_t window, int32_t floor_k, int32_t* budgets, int64_t* offsets,
-                   int32_t* idx, void* stream);
+                   int32_t* idx, void* workspace, void* stream);
 
 /* K3: compaction.  For each destination segment s, rows j in [seg_lo, seg_hi)
  * of head seg_bh[s]'s selection are copied from k_src/v_src (bf16

@@ -328,8 +328,8 @@ __device__ uint64_t epi_select_kth(KeyOf key_of, int nk, int k, SelScratch& x) {
 
 // ---------------------------------------------------------------------------
 // MODE 4, after pooling: Ada budget split + per-head top-k, grid-wide.  Same
-// result as select.cu's ada_select_kernel (one cluster per request there),
-// here spread over every CTA of the cooperative launch.
+// result as select.cu's grid_select_kernel (the standalone launch over
+// pooled scores in HBM), here fused behind the scoring passes.
 //
 // Radix search over the 32-bit orderable score, MSB-first 8-bit digits: per
 // digit each CTA histograms its own pooled keys into the per-(request, head)
@@ -935,7 +935,7 @@ namespace fkv {
 namespace {
 struct ScoreLayout {
   int chunks, tiles_per_chunk, bh;
-  int64_t stats, raw, gridbar, hist, active, ltau, counts, total;
+  int64_t stats, raw, gridbar, hist, active, ltau, counts, sel, total;
 };
 
 ScoreLayout score_layout(int batch, int hkv, int T, int window, int group) {
@@ -954,7 +954,8 @@ ScoreLayout score_layout(int batch, int hkv, int T, int window, int group) {
   L.active = a16(L.hist + static_cast<int64_t>(kSelPasses) * L.bh * 256 * 4);
   L.ltau = a16(L.active + (kSelPasses + 2) * 4);
   L.counts = a16(L.ltau + static_cast<int64_t>(L.bh) * 8);
-  L.total = a16(L.counts + static_cast<int64_t>(L.bh) * L.chunks * 8);
+  L.sel = a16(L.counts + static_cast<int64_t>(L.bh) * L.chunks * 8);
+  L.total = a16(L.sel + fkv_ada_select_workspace_bytes(batch, hkv, T - window));
   return L;
 }
 
@@ -1033,9 +1034,6 @@ extern "C" int fkv_snapkv_score(const void* q_win, const void* k, int32_t batch,
                                  : launch_score<256>(tq, tk, p, L.bh, mode, st);
 }
 
-extern "C" int fkv_ada_select(const float* scores, int32_t batch, int32_t hkv, int32_t n,
-                              int32_t budget, int32_t window, int32_t floor_k, int32_t* budgets,
-                              int64_t* offsets, int32_t* idx, void* stream);
 
 extern "C" int fkv_snapkv_select(const void* q_win, const void* k, int32_t batch, int32_t hq,
                                  int32_t hkv, int32_t T, int32_t window, int32_t pool_k,
@@ -1061,7 +1059,8 @@ extern "C" int fkv_snapkv_select(const void* q_win, const void* k, int32_t batch
     if (int rc = p.group * window == 128 ? launch_score<128>(tq, tk, p, L.bh, mode, st)
                                          : launch_score<256>(tq, tk, p, L.bh, mode, st))
       return rc;
-    return fkv_ada_select(scores, batch, hkv, n, budget, window, floor_k, budgets, offsets, idx, stream);
+    return fkv_ada_select(scores, batch, hkv, n, budget, window, floor_k, budgets, offsets, idx,
+                          static_cast<uint8_t*>(workspace) + L.sel, stream);
   }
   p.budget = budget;
   p.floor_k = floor_k;

@@ -16,12 +16,9 @@
 // shared-memory histograms (__match_any_sync: the top digits of float keys
 // are nearly all equal, so naive per-thread atomics would serialise), early
 // exit when the threshold bucket is taken whole.
-#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include "common.cuh"
-
-namespace cg = cooperative_groups;
 
 namespace fkv {
 namespace {
@@ -231,151 +228,565 @@ __global__ void __launch_bounds__(kThreads)
   for (int i = threadIdx.x; i < window; i += blockDim.x) out[max(k, 0) + i] = n + i;
 }
 
-// ------------------------------------------------ A18 + K2, one cluster ----
-// One thread-block cluster per request, one CTA per KV head (cluster size =
-// Hkv <= 8).  Each CTA stages its head's scores in shared memory when they
-// fit; budgets, offsets (request b starts at b*Hkv*budget: every request
-// keeps exactly Hkv*budget tokens) and the ascending index lists are written
-// by the same launch.
-constexpr int kStageLimit = 40 * 1024;  // scores staged in smem up to 160 KiB
+// ------------------------------------------- A18 + K2, grid-wide search ----
+// One cooperative launch for every (request, head).  The keys of all heads,
+// laid end to end, are cut into equal contiguous ranges, one per persistent
+// CTA (a range covers the tail of one head, whole heads, the head of
+// another: its "pieces"), and an MSB-first radix search over the 32-bit
+// orderable score (8-bit digits, four passes) runs for all requests at once:
+// per pass every CTA adds its pieces' digit histograms into per-head global
+// histograms, one grid barrier, and every CTA re-derives the decisions of
+// the requests / heads it touches (identical on every CTA, no second
+// barrier).
+//
+// Two searches per head:
+//   global   the Ada split in its floor-free form: with N_h(tau) = #{keys of
+//            head h >= tau} the non-floor picks of head h are
+//            max(0, N_h - floor), so tau is the largest threshold with
+//            G(tau) = sum_h max(0, N_h(tau) - floor) >= R (R = Hkv (B - w - f));
+//   floor    the head's own f-th largest score, kept when it ends below its
+//            floor (N_h < f: exactly its top-f).
+// A head's global histogram is skipped once N_h < f is certain (it adds
+// nothing to G), its floor histogram once N_h >= f is certain, and the two
+// are one histogram while both searches share a prefix (always in pass 0).
+// Four passes fix the threshold score s*; ties at s* are resolved in the
+// global order (head asc, token asc) from per-piece tie counts, so no pass
+// over the index bits is needed.  Per-CTA (chosen, tied) counts of the last
+// piece meet after a fifth barrier and every CTA writes its chosen tokens in
+// ascending order.  Same results as ada_budgets_kernel + topk_select_kernel
+// (and the oracle).
+constexpr int kGThreads = 512, kGWarps = kGThreads / 32;
+constexpr int kGMaxHeads = 16;   // Hkv: one warp per head in the decisions
+constexpr int kGMaxPieces = 16;  // heads touched per CTA
+constexpr int kGBufs = 3;        // rotating per-pass histogram buffers
+constexpr int kGMinKeys = 2048;  // keys per CTA, at least
+constexpr int kGUnroll = 4;
 
-// Ada split without materialising the floors: with N_h(tau) = #{t : gkey_h(t)
-// >= tau}, the number of globally chosen (non-floor) elements of head h above
-// tau is max(0, N_h(tau) - floor) (a head's floor is its own top-floor in the
-// same order), so the global threshold is the largest tau with
-// G(tau) = sum_h max(0, N_h(tau) - floor) >= R.  A cluster-wide MSB-first radix
-// search finds it: per 8-bit digit every CTA (one head) builds its histogram,
-// turns it into suffix counts S_h[d] = N_h(prefix.d...) and publishes them in
-// shared memory; every CTA evaluates G[d] for all 256 digits from the
-// peers' S arrays (DSMEM) and takes d* = max{d : G[d] >= R}.  Only heads that
-// end below their floor (N_h(tau) < floor) need their own top-floor select.
-__global__ void __launch_bounds__(kThreads)
-    ada_select_kernel(const float* __restrict__ scores, int n, int window, int floor_k,
-                      int rest_total, int budget, int32_t* __restrict__ budgets,
-                      int64_t* __restrict__ offsets, int32_t* __restrict__ idx) {
-  extern __shared__ __align__(16) uint8_t dyn[];
-  __shared__ SelectSmem sm;
-  __shared__ int32_t suffix[256];
-  __shared__ int32_t s_budget;
-  cg::cluster_group cluster = cg::this_cluster();
-  const int hkv = static_cast<int>(cluster.num_blocks());
-  const int h = static_cast<int>(cluster.block_rank());
-  const int b = blockIdx.y;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const float* src = scores + (static_cast<int64_t>(b) * hkv + h) * n;
-  const bool staged = n <= kStageLimit;
-  float* sv = reinterpret_cast<float*>(dyn);
-  if (staged)
-    for (int t = threadIdx.x; t < n; t += blockDim.x) sv[t] = src[t];
+struct GSelParams {
+  const float* scores;  // [BH, n] of this launch
+  int hkv, n, window, f, R, budget;
+  int req0, bh_total;   // first request of this launch; Bt*Hkv over all launches
+  int64_t total;        // BH * n
+  uint32_t* hist;       // [kGBufs][BH][2][256] (buffers 0, 1 zeroed by the host)
+  int2* counts;         // [grid] (chosen outright, ties) of each CTA's last piece
+  unsigned* bar;        // grid barrier counter (zeroed by the host)
+  int32_t* budgets;     // [BH] of this launch
+  int64_t* offsets;     // [BH (+1)] of this launch
+  int32_t* idx;         // absolute
+};
+
+struct GReq {  // global search of one request
+  uint32_t prefix, mask;
+  int exact, hstar, kstar;
+  int above[kGMaxHeads], n_at[kGMaxHeads];
+};
+struct GHead {  // floor search of one head
+  uint32_t prefix, mask;
+  int exact, above, n_at;
+};
+struct GRule {  // final keep rule of one head: 0 = ties ranked, 1 = o >= prefix, 2 = none
+  uint32_t prefix;
+  int kind, ktie;
+};
+
+struct GSelSmem {
+  uint32_t hist[2][256];
+  int32_t suf[kGMaxHeads][256];
+  GReq req[kGMaxPieces];
+  GHead fl[kGMaxPieces];
+  GRule rule[kGMaxPieces];
+  uint8_t fact[kGMaxPieces];  // floor histogram built this pass
+  int2 pc[kGMaxPieces][kGWarps];  // (chosen outright, ties) per piece and warp segment
+  int32_t wt[2][kGWarps];
+  int32_t tmp;
+};
+
+// diagnostics: %globaltimer stamps of CTA 0 (fkv__select_stamps)
+__device__ unsigned long long g_gstamps[32];
+__device__ __forceinline__ void gstamp(int i) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_gstamps[i] = t;
+  }
+}
+
+__device__ __forceinline__ void grid_sync(unsigned* bar) {
   __syncthreads();
-  const float* s = staged ? sv : src;
-  const uint32_t gbase = static_cast<uint32_t>(h) * n;
-
-  // ---- cluster radix search for tau over the global keys of all heads
-  uint64_t prefix = 0, mask = 0;
-  int above = 0;          // this head's elements strictly above the current prefix range
-  int n_at_tau = 0;       // N_h(tau) once found
-  bool have_tau = rest_total > 0;
-  if (have_tau) {
-    for (int shift = 56; shift >= 0; shift -= 8) {
-      for (int i = threadIdx.x; i < 256; i += blockDim.x) sm.hist[i] = 0;
-      __syncthreads();
-      for (int base = 0; base < n; base += blockDim.x) {
-        const int t = base + threadIdx.x;
-        uint64_t key = t < n ? compose(s[t], gbase + t) : 0;
-        const bool ok = t < n && (key & mask) == prefix;
-        const uint32_t d = ok ? static_cast<uint32_t>(key >> shift) & 255u : 256u;
-        const uint32_t peers = __match_any_sync(0xffffffffu, d);
-        if (ok && lane == __ffs(peers) - 1) atomicAdd(&sm.hist[d], __popc(peers));
-      }
-      __syncthreads();
-      if (warp == 0) {  // suffix[d] = above + sum_{d' >= d} hist[d']
-        uint32_t loc[8], run = 0;
-#pragma unroll
-        for (int j = 7; j >= 0; --j) {
-          run += sm.hist[8 * lane + j];
-          loc[j] = run;
-        }
-        uint32_t incl = run;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-          const uint32_t v = __shfl_down_sync(0xffffffffu, incl, off);
-          if (lane + off < 32) incl += v;
-        }
-        const uint32_t higher = incl - run;  // bins owned by higher lanes
-#pragma unroll
-        for (int j = 0; j < 8; ++j) suffix[8 * lane + j] = above + static_cast<int>(higher + loc[j]);
-      }
-      cluster.sync();  // every head's suffix counts are published
-      bool ge = false;
-      int gd = 0;
-      if (threadIdx.x < 256) {
-        for (int r = 0; r < hkv; ++r) {
-          const int v = cluster.map_shared_rank(suffix, r)[threadIdx.x] - floor_k;
-          gd += v > 0 ? v : 0;
-        }
-        ge = gd >= rest_total;
-      }
-      // G is non-increasing in d: d* = (#digits with G >= R) - 1
-      const uint32_t cnt = block_sum(ge ? 1u : 0u, sm);
-      const int dstar = static_cast<int>(cnt) - 1;
-      if (threadIdx.x == dstar) {
-        sm.digit = dstar;
-        sm.above = gd == rest_total;  // exact: the whole bucket is taken
-      }
-      __syncthreads();
-      const int d = static_cast<int>(sm.digit);
-      const bool exact = sm.above != 0;
-      n_at_tau = suffix[d];
-      const int next_above = d < 255 ? suffix[d + 1] : above;
-      prefix |= static_cast<uint64_t>(d) << shift;
-      mask |= 255ull << shift;
-      cluster.sync();  // peers are done reading `suffix` before it is rewritten
-      if (exact) break;
-      above = next_above;
+  if (threadIdx.x == 0) {
+    const unsigned total = gridDim.x;
+    unsigned old, v;
+    asm volatile("atom.add.release.gpu.u32 %0, [%1], 1;" : "=r"(old) : "l"(bar) : "memory");
+    const unsigned target = (old / total + 1) * total;
+    while (true) {
+      asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+      if (v >= target) break;
+      __nanosleep(32);
     }
   }
-  const uint64_t tau = prefix;
-  const int c_h = have_tau ? (n_at_tau - floor_k > 0 ? n_at_tau - floor_k : 0) : 0;
-  const bool below_floor = !have_tau || n_at_tau < floor_k;
+  __syncthreads();
+}
 
-  // heads that end below their floor keep exactly their own top-floor tokens
-  uint64_t ltau = kNone;
-  if (below_floor && floor_k > 0)
-    ltau = cta_select_kth(
-        [&](int i, uint64_t& key) {
-          key = compose(s[i], static_cast<uint32_t>(i));
-          return true;
-        },
-        n, static_cast<uint32_t>(floor_k), sm);
-  auto chosen = [&](int t) -> bool {
-    if (!below_floor) return compose(s[t], gbase + t) >= tau;
-    return ltau != kNone && compose(s[t], static_cast<uint32_t>(t)) >= ltau;
+// Suffix counts of one 256-bin histogram (8 bins per lane): s[j] = base +
+// #keys in bins >= 8*lane + j; `up` = s of bin 8*lane + 8 (base past bin 255).
+__device__ __forceinline__ void warp_suffix(const uint32_t* gh, int base, int (&s)[8], int& up) {
+  const int lane = threadIdx.x & 31;
+  const uint4 x0 = __ldcg(reinterpret_cast<const uint4*>(gh + 8 * lane));
+  const uint4 x1 = __ldcg(reinterpret_cast<const uint4*>(gh + 8 * lane + 4));
+  const uint32_t h[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+  int run = 0;
+#pragma unroll
+  for (int j = 7; j >= 0; --j) {
+    run += static_cast<int>(h[j]);
+    s[j] = run;
+  }
+  int incl = run;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int v = __shfl_down_sync(0xffffffffu, incl, off);
+    if (lane + off < 32) incl += v;
+  }
+  const int higher = incl - run + base;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) s[j] += higher;
+  up = __shfl_down_sync(0xffffffffu, s[0], 1);
+  if (lane == 31) up = base;
+}
+
+__device__ __forceinline__ int rule_class(const GRule& r, uint32_t o) {
+  if (r.kind == 2) return 0;
+  if (r.kind == 1) return o >= r.prefix;
+  return o > r.prefix ? 1 : (o == r.prefix ? 2 : 0);
+}
+
+// Piece [lo, hi) of a head's keys s[]: the 16-B aligned body [a, b) and the
+// (at most 3 + 3) keys around it.
+__device__ __forceinline__ void split_aligned(const float* s, int lo, int hi, int& a, int& b) {
+  const int mis = static_cast<int>((reinterpret_cast<uintptr_t>(s + lo) >> 2) & 3);
+  a = min(hi, lo + ((4 - mis) & 3));
+  b = a + ((hi - a) & ~3);
+}
+
+// fn(valid, orderable key) over keys [lo, hi) by the whole CTA, every call
+// warp-uniform; the body in float4 loads, kGUnroll of them in flight per
+// thread.
+template <class Fn>
+__device__ __forceinline__ void for_keys(const float* s, int lo, int hi, Fn&& fn) {
+  const int tid = threadIdx.x;
+  int a, b;
+  split_aligned(s, lo, hi, a, b);
+  {
+    const int nh = a - lo;
+    const int i = tid < nh ? lo + tid : b + tid - nh;
+    const bool in = tid < nh + (hi - b);
+    fn(in, in ? orderable(__ldg(s + i)) : 0u);
+  }
+  const float4* v4 = reinterpret_cast<const float4*>(s + a);
+  const int nv = (b - a) >> 2;
+  for (int base = 0; base < nv; base += kGUnroll * kGThreads) {
+    float4 x[kGUnroll];
+#pragma unroll
+    for (int u = 0; u < kGUnroll; ++u) {
+      const int j = base + u * kGThreads + tid;
+      x[u] = j < nv ? __ldg(v4 + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < kGUnroll; ++u) {
+      const bool in = base + u * kGThreads + tid < nv;
+      fn(in, orderable(x[u].x));
+      fn(in, orderable(x[u].y));
+      fn(in, orderable(x[u].z));
+      fn(in, orderable(x[u].w));
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kGThreads) grid_select_kernel(const GSelParams p) {
+  __shared__ GSelSmem sm;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int HK = p.hkv, f = p.f, R = p.R, n = p.n;
+  const int64_t k0 = static_cast<int64_t>(blockIdx.x) * p.total / gridDim.x;
+  const int64_t k1 = static_cast<int64_t>(blockIdx.x + 1) * p.total / gridDim.x;
+  const int bh_lo = static_cast<int>(k0 / n), rq_lo = bh_lo / HK;
+  const int n_lh = k1 > k0 ? static_cast<int>((k1 - 1) / n) - bh_lo + 1 : 0;
+  const int n_lr = k1 > k0 ? static_cast<int>((k1 - 1) / n) / HK - rq_lo + 1 : 0;
+  const int64_t buf_words = p.total / n * 512;
+  // piece of local head lh: keys [lo, hi) of head bh_lo + lh
+  auto piece = [&](int lh, int& lo, int& hi) {
+    const int64_t h0 = static_cast<int64_t>(bh_lo + lh) * n;
+    lo = static_cast<int>(max(k0, h0) - h0);
+    hi = static_cast<int>(min(k1, h0 + n) - h0);
   };
 
-  // ---- budget, offsets within the request via DSMEM, ascending indices
-  if (threadIdx.x == 0) s_budget = window + floor_k + c_h;
-  cluster.sync();
-  int64_t off = static_cast<int64_t>(b) * hkv * budget;
-  for (int r = 0; r < h; ++r) off += *cluster.map_shared_rank(&s_budget, r);
-  const int bh = b * hkv + h;
-  if (threadIdx.x == 0) {
-    budgets[bh] = s_budget;
-    offsets[bh] = off;
-    if (b == static_cast<int>(gridDim.y) - 1 && h == hkv - 1) offsets[bh + 1] = off + s_budget;
+  for (int i = tid; i < n_lr * kGMaxHeads; i += kGThreads) {
+    sm.req[i / kGMaxHeads].above[i % kGMaxHeads] = 0;
+    sm.req[i / kGMaxHeads].n_at[i % kGMaxHeads] = R > 0 ? n : 0;
   }
-  int32_t* out = idx + off;
-  uint32_t written = 0;
-  for (int base = 0; base < n; base += blockDim.x) {
-    const int t = base + threadIdx.x;
-    const bool take = t < n && chosen(t);
-    uint32_t before;
-    const uint32_t got = block_flag_scan(take, before, sm);
-    if (take) out[written + before] = t;
-    written += got;
+  if (tid < n_lr) {
+    GReq& r = sm.req[tid];
+    r.prefix = r.mask = 0;
+    r.exact = R <= 0;
+    r.hstar = HK;
+    r.kstar = 0;
   }
-  for (int i = threadIdx.x; i < window; i += blockDim.x) out[s_budget - window + i] = n + i;
-  cluster.sync();  // keep this CTA's shared memory alive until every peer is done reading it
+  if (tid < n_lh) sm.fl[tid] = GHead{0u, 0u, f <= 0, 0, n};
+  gstamp(0);
+  __syncthreads();
+
+  for (int pass = 0, shift = 24; pass < 4; ++pass, shift -= 8) {
+    uint32_t* hb = p.hist + (pass % kGBufs) * buf_words;
+    // ---- my pieces' digit histograms into hb
+    for (int lh = 0; lh < n_lh; ++lh) {
+      const int bh = bh_lo + lh, h = bh % HK;
+      const GReq& rq = sm.req[bh / HK - rq_lo];
+      const GHead& fh = sm.fl[lh];
+      // global: N_h >= f still possible; floor: N_h < f still possible
+      const bool ga = !rq.exact && rq.n_at[h] >= f;
+      const bool fa = !fh.exact && (rq.exact ? rq.n_at[h] < f : rq.above[h] < f);
+      const bool same = ga && fa && rq.prefix == fh.prefix && rq.mask == fh.mask;
+      if (tid == 0) sm.fact[lh] = fa;
+      if (!ga && !fa) continue;
+      (&sm.hist[0][0])[tid] = 0;
+      __syncthreads();
+      int lo, hi;
+      piece(lh, lo, hi);
+      const float* s = p.scores + static_cast<int64_t>(bh) * n;
+      const uint32_t gp = rq.prefix, gm = rq.mask, fp = fh.prefix, fm = fh.mask;
+      auto add = [&](bool in, uint32_t o) {
+        const uint32_t dig = (o >> shift) & 255u;
+        const uint32_t dg = in && (o & gm) == gp ? dig : 256u;
+        const uint32_t df = in && (o & fm) == fp ? dig : 256u;
+        // plain shared atomics: measured on par with or faster than
+        // warp-aggregated adds (match.any), also on pooled Ada-SnapKV scores
+        // whose top byte takes few values
+        if (ga && dg < 256u) atomicAdd(&sm.hist[0][dg], 1u);
+        if (fa && !same && df < 256u) atomicAdd(&sm.hist[1][df], 1u);
+      };
+      for_keys(s, lo, hi, add);
+      __syncthreads();
+      uint32_t* gh = hb + static_cast<int64_t>(bh) * 512;
+      if (tid < 256) {
+        const uint32_t c = sm.hist[0][tid];
+        if (c) {
+          if (ga) atomicAdd(gh + tid, c);
+          if (same) atomicAdd(gh + 256 + tid, c);
+        }
+      } else if (fa && !same) {
+        const uint32_t c = sm.hist[1][tid - 256];
+        if (c) atomicAdd(gh + tid, c);
+      }
+      __syncthreads();
+    }
+    gstamp(1 + 3 * pass);
+    grid_sync(p.bar);
+    gstamp(2 + 3 * pass);
+    // the buffer of pass + 2 was last read by pass - 1's decisions (before
+    // this barrier) and is next written after the next one; the CTA holding
+    // a head's first key clears it
+    if (pass < 2) {
+      uint32_t* zb = p.hist + ((pass + 2) % kGBufs) * buf_words;
+      for (int lh = 0; lh < n_lh; ++lh) {
+        int lo, hi;
+        piece(lh, lo, hi);
+        if (lo == 0) (zb + static_cast<int64_t>(bh_lo + lh) * 512)[tid] = 0;
+      }
+    }
+    // ---- global decisions of my requests: d* = max{d : G(d) >= R}
+    for (int lr = 0; lr < n_lr; ++lr) {
+      GReq& rq = sm.req[lr];
+      if (rq.exact) continue;
+      const int b = rq_lo + lr;
+      if (wid < HK) {
+        int sv[8], up;
+        warp_suffix(hb + static_cast<int64_t>(b * HK + wid) * 512, rq.above[wid], sv, up);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) sm.suf[wid][8 * lane + j] = sv[j];
+      }
+      __syncthreads();
+      int gd = 0;
+      if (tid < 256)
+        for (int h = 0; h < HK; ++h) gd += max(0, sm.suf[h][tid] - f);
+      const int dstar = __syncthreads_count(tid < 256 && gd >= R) - 1;
+      if (tid == dstar) sm.tmp = gd == R;
+      __syncthreads();
+      if (tid < HK) {
+        rq.n_at[tid] = sm.suf[tid][dstar];
+        if (dstar < 255) rq.above[tid] = sm.suf[tid][dstar + 1];
+      }
+      if (tid == 0) {
+        rq.prefix |= static_cast<uint32_t>(dstar) << shift;
+        rq.mask |= 255u << shift;
+        rq.exact = sm.tmp;
+      }
+      __syncthreads();
+    }
+    gstamp(3 + 3 * pass);
+    // ---- floor decisions of my heads (one warp each): f-th largest
+    for (int lh = wid; lh < n_lh; lh += kGWarps) {
+      GHead& fh = sm.fl[lh];
+      if (!sm.fact[lh]) continue;
+      int sv[8], up;
+      warp_suffix(hb + static_cast<int64_t>(bh_lo + lh) * 512 + 256, fh.above, sv, up);
+      int c = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) c += sv[j] >= f;
+      const int dstar = __reduce_add_sync(0xffffffffu, c) - 1;
+      int at = 0, nxt = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (8 * lane + j == dstar) {
+          at = sv[j];
+          nxt = j < 7 ? sv[j + 1] : up;
+        }
+      at = __shfl_sync(0xffffffffu, at, dstar >> 3);
+      nxt = __shfl_sync(0xffffffffu, nxt, dstar >> 3);
+      if (lane == 0) {
+        fh.n_at = at;
+        fh.above = nxt;
+        fh.prefix |= static_cast<uint32_t>(dstar) << shift;
+        fh.mask |= 255u << shift;
+        fh.exact = at == f;
+      }
+    }
+    __syncthreads();
+  }
+
+  // ---- ties at s*: walk heads in order until G reaches R exactly
+  if (tid < n_lr) {
+    GReq& rq = sm.req[tid];
+    if (R > 0 && !rq.exact) {
+      int hstar = HK, kstar = 0, need = R;
+      for (int h = 0; h < HK; ++h) need -= max(0, rq.above[h] - f);
+      for (int h = 0; h < HK && need > 0; ++h) {
+        const int base = rq.above[h];
+        const int gain = max(0, rq.n_at[h] - f) - max(0, base - f);
+        if (gain >= need) {
+          hstar = h;
+          kstar = max(0, f - base) + need;
+          need = 0;
+        } else {
+          need -= gain;
+        }
+      }
+      for (int h = 0; h < HK; ++h)
+        rq.n_at[h] = h < hstar ? rq.n_at[h] : (h == hstar ? rq.above[h] + kstar : rq.above[h]);
+      rq.hstar = hstar;
+      rq.kstar = kstar;
+    }
+  }
+  __syncthreads();
+  if (tid < n_lh) {
+    const int bh = bh_lo + tid, h = bh % HK;
+    const GReq& rq = sm.req[bh / HK - rq_lo];
+    const GHead& fh = sm.fl[tid];
+    GRule r;
+    if (R <= 0 || rq.n_at[h] < f) {  // below the floor: own top-f
+      if (f <= 0) r = GRule{0u, 2, 0};
+      else if (fh.exact) r = GRule{fh.prefix, 1, 0};
+      else r = GRule{fh.prefix, 0, f - fh.above};
+    } else if (rq.exact) {
+      r = GRule{rq.prefix, 1, 0};
+    } else {
+      r = GRule{rq.prefix, 0, h < rq.hstar ? 0x7fffffff : (h == rq.hstar ? rq.kstar : 0)};
+    }
+    sm.rule[tid] = r;
+  }
+  __syncthreads();
+  auto budget_of = [&](const GReq& rq, int h) {
+    return p.window + f + (R > 0 ? max(0, rq.n_at[h] - f) : 0);
+  };
+  auto head_offset = [&](const GReq& rq, int bh) {
+    const int b = bh / HK, h = bh - b * HK;
+    int64_t off = static_cast<int64_t>(p.req0 + b) * HK * p.budget;
+    for (int hh = 0; hh < h; ++hh) off += budget_of(rq, hh);
+    return off;
+  };
+
+  // ---- per-warp-segment counts of every piece (warp w scans a contiguous
+  // 1/16 of the piece's aligned body; warp 0 also the keys before it, the
+  // last warp those after it); the last piece's total is published for the
+  // CTAs after me.  Budgets, offsets and window tokens by the CTA holding a
+  // head's first key.
+  struct Seg {
+    int lo, hi, a, b, v0, v1;
+  };
+  auto segment = [&](const float* s, int lo, int hi) {
+    Seg g;
+    g.lo = lo;
+    g.hi = hi;
+    split_aligned(s, lo, hi, g.a, g.b);
+    const int nv = (g.b - g.a) >> 2, per = (nv + kGWarps - 1) / kGWarps;
+    g.v0 = min(nv, wid * per);
+    g.v1 = min(nv, g.v0 + per);
+    return g;
+  };
+  for (int lh = 0; lh < n_lh; ++lh) {
+    const int bh = bh_lo + lh;
+    int lo, hi;
+    piece(lh, lo, hi);
+    const GRule r = sm.rule[lh];
+    const float* s = p.scores + static_cast<int64_t>(bh) * n;
+    int c1 = 0, c2 = 0;
+    if (r.kind != 2) {
+      const Seg g = segment(s, lo, hi);
+      auto count = [&](float x) {
+        const int k = rule_class(r, orderable(x));
+        c1 += k == 1;
+        c2 += k == 2;
+      };
+      if (wid == 0)
+        for (int i = g.lo + lane; i < g.a; i += 32) count(__ldg(s + i));
+      const float4* v4 = reinterpret_cast<const float4*>(s + g.a);
+#pragma unroll 4
+      for (int j = g.v0 + lane; j < g.v1; j += 32) {
+        const float4 x = __ldg(v4 + j);
+        count(x.x);
+        count(x.y);
+        count(x.z);
+        count(x.w);
+      }
+      if (wid == kGWarps - 1)
+        for (int i = g.b + lane; i < g.hi; i += 32) count(__ldg(s + i));
+    }
+    c1 = __reduce_add_sync(0xffffffffu, c1);
+    c2 = __reduce_add_sync(0xffffffffu, c2);
+    if (lane == 0) sm.pc[lh][wid] = make_int2(c1, c2);
+    if (lo == 0) {
+      const GReq& rq = sm.req[bh / HK - rq_lo];
+      const int bud = budget_of(rq, bh % HK);
+      const int64_t off = head_offset(rq, bh);
+      for (int i = tid; i < p.window; i += kGThreads) p.idx[off + bud - p.window + i] = n + i;
+      if (tid == 0) {
+        p.budgets[bh] = bud;
+        p.offsets[bh] = off;
+        if (p.req0 * HK + bh == p.bh_total - 1) p.offsets[bh + 1] = off + bud;
+      }
+    }
+  }
+  __syncthreads();
+  if (tid == 0 && n_lh > 0) {
+    int x = 0, y = 0;
+    for (int j = 0; j < kGWarps; ++j) x += sm.pc[n_lh - 1][j].x, y += sm.pc[n_lh - 1][j].y;
+    p.counts[blockIdx.x] = make_int2(x, y);
+  }
+  gstamp(20);
+  grid_sync(p.bar);
+  gstamp(21);
+
+  // ---- chosen tokens of my pieces, ascending, at their place in the list;
+  // each warp writes its own segment (no block barriers)
+  const uint32_t lt = (1u << lane) - 1u;
+  auto warp_excl = [&](int v, int& total) {  // exclusive prefix over lanes
+    int incl = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += y;
+    }
+    total = __shfl_sync(0xffffffffu, incl, 31);
+    return incl - v;
+  };
+  for (int lh = 0; lh < n_lh; ++lh) {
+    const int bh = bh_lo + lh;
+    const GRule r = sm.rule[lh];
+    if (r.kind == 2) continue;
+    const GReq& rq = sm.req[bh / HK - rq_lo];
+    int lo, hi;
+    piece(lh, lo, hi);
+    int pos = 0, tie0 = 0;
+    if (lo > 0) {  // earlier CTAs hold this head's keys [0, lo): their last pieces
+      const int64_t h0 = static_cast<int64_t>(bh) * n;
+      // first CTA c with c*total/grid <= h0 < (c+1)*total/grid
+      const int c_first = static_cast<int>(((h0 + 1) * gridDim.x + p.total - 1) / p.total) - 1;
+      for (int c = c_first + lane; c < static_cast<int>(blockIdx.x); c += 32) {
+        const int2 cc = __ldcg(p.counts + c);
+        pos += cc.x;
+        tie0 += cc.y;
+      }
+      pos = __reduce_add_sync(0xffffffffu, pos);
+      tie0 = __reduce_add_sync(0xffffffffu, tie0);
+      pos += min(tie0, r.ktie);
+    }
+    // this warp's segment: chosen outright and ties of the segments before it
+    int c1b = 0, tb = 0;
+    for (int j = 0; j < wid; ++j) c1b += sm.pc[lh][j].x, tb += sm.pc[lh][j].y;
+    int tie_run = tie0 + tb;
+    pos += c1b + min(tie_run, r.ktie) - min(tie0, r.ktie);
+    int32_t* out = p.idx + head_offset(rq, bh);
+    const float* s = p.scores + static_cast<int64_t>(bh) * n;
+    const Seg g = segment(s, lo, hi);
+    auto emit_scalar = [&](int i0, int i1) {
+      for (int base = i0; base < i1; base += 32) {
+        const int i = base + lane;
+        const int k = i < i1 ? rule_class(r, orderable(__ldg(s + i))) : 0;
+        const uint32_t ties = __ballot_sync(0xffffffffu, k == 2);
+        const bool take = k == 1 || (k == 2 && tie_run + __popc(ties & lt) < r.ktie);
+        const uint32_t bal = __ballot_sync(0xffffffffu, take);
+        if (take) out[pos + __popc(bal & lt)] = i;
+        pos += __popc(bal);
+        tie_run += __popc(ties);
+      }
+    };
+    if (wid == 0) emit_scalar(g.lo, g.a);
+    const float4* v4 = reinterpret_cast<const float4*>(s + g.a);
+    for (int jb = g.v0; jb < g.v1; jb += 32) {
+      const int j = jb + lane;
+      const float4 x = j < g.v1 ? __ldg(v4 + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+      int k[4] = {0, 0, 0, 0};
+      if (j < g.v1) {
+        k[0] = rule_class(r, orderable(x.x));
+        k[1] = rule_class(r, orderable(x.y));
+        k[2] = rule_class(r, orderable(x.z));
+        k[3] = rule_class(r, orderable(x.w));
+      }
+      int t_all, n_all;
+      int tr = tie_run + warp_excl((k[0] == 2) + (k[1] == 2) + (k[2] == 2) + (k[3] == 2), t_all);
+      bool tk[4];
+      int nt = 0;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        tk[c] = k[c] == 1;
+        if (k[c] == 2) tk[c] = tr++ < r.ktie;
+        nt += tk[c];
+      }
+      int q = pos + warp_excl(nt, n_all);
+      const int i0 = g.a + 4 * j;
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (tk[c]) out[q++] = i0 + c;
+      pos += n_all;
+      tie_run += t_all;
+    }
+    if (wid == kGWarps - 1) emit_scalar(g.b, g.hi);
+  }
+  gstamp(22);
+}
+
+int gsel_ctas() {
+  static int ctas = 0;
+  if (!ctas) {
+    int dev = 0, sms = 148, occ = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, grid_select_kernel, kGThreads, 0);
+    occ = occ < 1 ? 1 : (occ > 2 ? 2 : occ);
+    ctas = sms * occ;
+  }
+  return ctas;
+}
+
+// CTAs of a launch over `bh` heads of n keys.
+int gsel_grid(int bh, int n) {
+  const int64_t total = static_cast<int64_t>(bh) * n;
+  const int64_t want = (total + kGMinKeys - 1) / kGMinKeys;
+  const int ctas = gsel_ctas();
+  return want < 1 ? 1 : (want > ctas ? ctas : static_cast<int>(want));
+}
+
+// Requests per launch: a CTA's key range spans at most kGMaxPieces heads.
+int gsel_reqs_per_launch(int hkv) {
+  const int r = (kGMaxPieces - 2) * gsel_ctas() / hkv;
+  return r < 1 ? 1 : r;
 }
 
 }  // namespace
@@ -385,7 +796,7 @@ extern "C" int fkv_ada_budgets(const float* scores, int32_t batch, int32_t hkv, 
                                int32_t budget, int32_t window, int32_t floor_k, int32_t* budgets,
                                void* stream) {
   using namespace fkv;
-  if (!scores || !budgets) return set_error(FKV_ERR_INVALID, "fkv_ada_budgets: null pointer");
+  if ((!scores && n > 0) || !budgets) return set_error(FKV_ERR_INVALID, "fkv_ada_budgets: null pointer");
   if (batch < 0 || hkv < 1 || hkv > 64 || n < 0 || window < 0 || floor_k < 0)
     return set_error(FKV_ERR_INVALID, "fkv_ada_budgets: bad sizes");
   const int sel = budget - window;
@@ -404,7 +815,7 @@ extern "C" int fkv_topk_select(const float* scores, const int32_t* budgets, int3
                                int32_t hkv, int32_t n, int32_t window, int64_t* offsets,
                                int32_t* idx, void* stream) {
   using namespace fkv;
-  if (!scores || !budgets || !offsets || !idx)
+  if ((!scores && n > 0) || !budgets || !offsets || !idx)
     return set_error(FKV_ERR_INVALID, "fkv_topk_select: null pointer");
   if (batch < 0 || hkv < 1 || n < 0 || window < 0)
     return set_error(FKV_ERR_INVALID, "fkv_topk_select: bad sizes");
@@ -414,44 +825,76 @@ extern "C" int fkv_topk_select(const float* scores, const int32_t* budgets, int3
   return cuda_check(cudaGetLastError(), "topk_select launch");
 }
 
+extern "C" int fkv__select_stamps(unsigned long long* host) {
+  return fkv::cuda_check(cudaMemcpyFromSymbol(host, fkv::g_gstamps, sizeof(unsigned long long) * 32),
+                         "select stamps");
+}
+
+extern "C" int64_t fkv_ada_select_workspace_bytes(int32_t batch, int32_t hkv, int32_t n) {
+  using namespace fkv;
+  if (batch < 1 || hkv < 1) return 256;
+  const int reqs = batch < gsel_reqs_per_launch(hkv) ? batch : gsel_reqs_per_launch(hkv);
+  const int64_t hist = static_cast<int64_t>(kGBufs) * reqs * hkv * 512 * 4;
+  return 256 + hist + static_cast<int64_t>(gsel_ctas()) * 8;
+}
+
 extern "C" int fkv_ada_select(const float* scores, int32_t batch, int32_t hkv, int32_t n,
                               int32_t budget, int32_t window, int32_t floor_k, int32_t* budgets,
-                              int64_t* offsets, int32_t* idx, void* stream) {
+                              int64_t* offsets, int32_t* idx, void* workspace, void* stream) {
   using namespace fkv;
-  if (!scores || !budgets || !offsets || !idx)
+  if ((!scores && n > 0) || !budgets || !offsets || !idx || !workspace)
     return set_error(FKV_ERR_INVALID, "fkv_ada_select: null pointer");
-  if (batch < 0 || hkv < 1 || hkv > 8 || n < 0 || window < 0 || floor_k < 0)
-    return set_error(FKV_ERR_INVALID, "fkv_ada_select: bad sizes (Hkv must be 1..8)");
+  if (batch < 0 || hkv < 1 || hkv > kGMaxHeads || n < 0 || window < 0 || floor_k < 0)
+    return set_error(FKV_ERR_INVALID, "fkv_ada_select: bad sizes (Hkv must be 1..16)");
   const int sel = budget - window;
   if (sel < 0 || sel > n || floor_k > sel)
     return set_error(FKV_ERR_INVALID, "fkv_ada_select: need 0 <= floor <= budget-window <= n");
   if (static_cast<int64_t>(hkv) * n >= 0x7fffffffLL)
     return set_error(FKV_ERR_INVALID, "fkv_ada_select: Hkv * n too large");
   if (batch == 0) return FKV_OK;
-  const int rest = hkv * sel - hkv * floor_k;
-  const size_t smem = n <= kStageLimit ? static_cast<size_t>(n) * 4 : 16;
-  static size_t configured = 0;
-  if (smem > configured) {
-    if (int rc = cuda_check(cudaFuncSetAttribute(ada_select_kernel,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 static_cast<int>(smem)),
-                            "ada_select smem attribute"))
+  auto st = static_cast<cudaStream_t>(stream);
+  if (n == 0) {  // nothing to rank: every head keeps its window
+    if (int rc = fkv_ada_budgets(scores, batch, hkv, 0, budget, window, floor_k, budgets, stream))
       return rc;
-    configured = smem;
+    return fkv_topk_select(scores, budgets, batch, hkv, 0, window, offsets, idx, stream);
   }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(hkv, batch, 1);
-  cfg.blockDim = dim3(kThreads, 1, 1);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = static_cast<cudaStream_t>(stream);
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = hkv;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cuda_check(cudaLaunchKernelEx(&cfg, ada_select_kernel, scores, n, window, floor_k, rest,
-                                       budget, budgets, offsets, idx),
-                    "ada_select launch");
+  const int per = gsel_reqs_per_launch(hkv);
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  for (int r0 = 0; r0 < batch; r0 += per) {
+    const int reqs = batch - r0 < per ? batch - r0 : per;
+    const int bh = reqs * hkv;
+    GSelParams p{};
+    p.scores = scores + static_cast<int64_t>(r0) * hkv * n;
+    p.hkv = hkv;
+    p.n = n;
+    p.window = window;
+    p.f = floor_k;
+    p.R = hkv * sel - hkv * floor_k;
+    p.budget = budget;
+    p.req0 = r0;
+    p.bh_total = batch * hkv;
+    p.total = static_cast<int64_t>(bh) * n;
+    p.bar = reinterpret_cast<unsigned*>(ws);
+    p.hist = reinterpret_cast<uint32_t*>(ws + 256);
+    p.counts = reinterpret_cast<int2*>(ws + 256 + static_cast<int64_t>(kGBufs) * bh * 512 * 4);
+    p.budgets = budgets + static_cast<int64_t>(r0) * hkv;
+    p.offsets = offsets + static_cast<int64_t>(r0) * hkv;
+    p.idx = idx;
+    // barrier counter + the histogram buffers of passes 0 and 1
+    if (int rc = cuda_check(cudaMemsetAsync(ws, 0, 256 + static_cast<size_t>(2) * bh * 512 * 4, st),
+                            "ada_select workspace reset"))
+      return rc;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(gsel_grid(bh, n), 1, 1);
+    cfg.blockDim = dim3(kGThreads, 1, 1);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (int rc = cuda_check(cudaLaunchKernelEx(&cfg, grid_select_kernel, p), "ada_select launch"))
+      return rc;
+  }
+  return FKV_OK;
 }

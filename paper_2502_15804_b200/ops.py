@@ -257,10 +257,11 @@ def select(scores: torch.Tensor, head_budgets: torch.Tensor, window: int = 32,
     return offsets, idx[:total]
 
 
-def ada_select(scores: torch.Tensor, budget: int, window: int = 32, alpha: float = 0.2):
-    """A18 + K2 in one cluster launch: -> (budgets int32 [Bt, Hkv],
-    offsets int64 [Bt*Hkv+1], idx int32 [Bt*Hkv*budget]); identical to
-    ``budgets`` followed by ``select``."""
+def ada_select(scores: torch.Tensor, budget: int, window: int = 32, alpha: float = 0.2,
+               workspace: torch.Tensor | None = None):
+    """A18 + K2 in one cooperative grid-wide launch: -> (budgets int32
+    [Bt, Hkv], offsets int64 [Bt*Hkv+1], idx int32 [Bt*Hkv*budget]);
+    identical to ``budgets`` followed by ``select``."""
     _need_cuda(scores)
     if scores.dtype != torch.float32 or scores.dim() != 3 or not scores.is_contiguous():
         raise NativeError("scores must be contiguous f32 [Bt, Hkv, n]")
@@ -269,9 +270,13 @@ def ada_select(scores: torch.Tensor, budget: int, window: int = 32, alpha: float
     hb = torch.empty((bt, hkv), dtype=torch.int32, device=dev)
     offsets = torch.empty(bt * hkv + 1, dtype=torch.int64, device=dev)
     idx = torch.empty(max(bt * hkv * budget, 1), dtype=torch.int32, device=dev)
+    need = int(_lib.fkv_ada_select_workspace_bytes(bt, hkv, n))
+    if workspace is None or workspace.numel() * workspace.element_size() < need:
+        workspace = torch.empty(need, dtype=torch.uint8, device=dev)
     _native.check(_lib.fkv_ada_select(scores.data_ptr(), bt, hkv, n, int(budget), int(window),
                                       ada_floor(budget, window, alpha), hb.data_ptr(),
-                                      offsets.data_ptr(), idx.data_ptr(), _stream()))
+                                      offsets.data_ptr(), idx.data_ptr(), workspace.data_ptr(),
+                                      _stream()))
     return hb, offsets, idx[:bt * hkv * budget]
 
 

@@ -138,27 +138,43 @@ def test_selection_agreement_with_oracle_scores(cuda_device):
     assert agree >= 0.98
 
 
-@pytest.mark.parametrize("bt,T,budget,ties", [(3, 4096, 256, False), (2, 2048, 64, True),
-                                              (1, 65600, 1024, False), (2, 40000, 512, True),
-                                              (2, 3000, 256, "zero-head"), (1, 1000, 32, False)])
-def test_fused_ada_select_bit_exact(cuda_device, bt, T, budget, ties):
-    """The one-launch cluster kernel == oracle budgets + selection (also past
-    the shared-memory staging limit, n > 40960)."""
+@pytest.mark.parametrize("bt,T,budget,ties,hkv,alpha", [
+    (3, 4096, 256, False, 8, 0.2), (2, 2048, 64, True, 8, 0.2), (1, 65600, 1024, False, 8, 0.2),
+    (2, 40000, 512, True, 8, 0.2), (2, 3000, 256, "zero-head", 8, 0.2), (1, 1000, 32, False, 8, 0.2),
+    (1, 131104, 1024, False, 8, 0.2),      # cfg5 length: many chunks per head
+    (3, 5000, 300, "zero-head", 16, 0.2),  # 16 KV heads
+    (5, 3000, 200, True, 1, 0.2),          # one KV head: the floor is the whole story
+    (2, 3000, 256, True, 8, 1.0),          # floor = budget - window: no global picks
+    (2, 3000, 256, "zero-head", 8, 0.0),   # no floor
+    (600, 200, 64, False, 8, 0.2),         # 4800 heads: more than one launch
+    (64, 16384, 256, False, 8, 0.2),       # batch 64 at 16k: pieces across heads
+    (3, 32, 32, False, 8, 0.2),            # n = 0: the window only
+    (7, 300, 100, "zero-head", 8, 0.2),    # heads shorter than a CTA's key range
+])
+def test_fused_ada_select_bit_exact(cuda_device, bt, T, budget, ties, hkv, alpha):
+    """The one-launch grid-wide split + select == oracle budgets + selection."""
     from paper_2502_15804_b200 import ops
     g = torch.Generator().manual_seed(bt * 7 + T)
     n = T - 32
-    sc = torch.randint(0, 5, (bt, 8, n), generator=g).float() if ties is True else torch.rand(bt, 8, n, generator=g)
+    sc = torch.randint(0, 5, (bt, hkv, n), generator=g).float() if ties is True \
+        else torch.rand(bt, hkv, n, generator=g)
     if ties == "zero-head":  # a head that can only keep its floor
         sc[:, 2] = 0.0
         sc[:, 5] *= 1e-3
-    hb, off, idx = ops.ada_select(sc.to(cuda_device), budget, 32)
+    hb, off, idx = ops.ada_select(sc.to(cuda_device), budget, 32, alpha)
     torch.cuda.synchronize()
     s64 = sc.double().numpy()
-    ref_b = okv.ada_budgets(s64, budget, 32, 0.2)
+    ref_b = okv.ada_budgets(s64, budget, 32, alpha)
     np.testing.assert_array_equal(hb.cpu().numpy(), ref_b)
     ref_off, ref_idx = okv.topk_select(s64, ref_b, 32)
     np.testing.assert_array_equal(off.cpu().numpy(), ref_off)
     np.testing.assert_array_equal(idx.cpu().numpy(), ref_idx)
+    # the same workspace again (reset inside the call)
+    ws = torch.empty(int(ops._lib.fkv_ada_select_workspace_bytes(bt, hkv, n)), dtype=torch.uint8,
+                     device=cuda_device).fill_(0xAB)
+    for _ in range(2):
+        hb2, off2, idx2 = ops.ada_select(sc.to(cuda_device), budget, 32, alpha, workspace=ws)
+    assert torch.equal(hb2, hb) and torch.equal(off2, off) and torch.equal(idx2, idx)
 
 
 @pytest.mark.parametrize("bt,hq,hkv,T,budget,temp,flat_head", [

@@ -4,11 +4,11 @@ sys.path.insert(0, '.')
 import bench
 peaks = json.load(open('MEASURED_PEAKS.json')) if __import__('os').path.exists('MEASURED_PEAKS.json') else {}
 for k, v in bench.prefill_compress(peaks).items():
-    print(k, {a: round(b, 2) for a, b in v.items()})
+    print(k, {a: (round(b, 2) if isinstance(b, float) else b) for a, b in v.items()})
 
 import ctypes as C, numpy as np, torch
 from paper_2502_15804_b200 import ops, _native
-for (bt, hq, hkv, T, B) in [(1, 32, 8, 16384, 256), (1, 64, 8, 32768, 1024)]:
+for (bt, hq, hkv, T, B) in [(1, 32, 8, 16384, 256), (1, 64, 8, 32768, 1024), (1, 64, 8, 131072, 1024)]:
     dev = torch.device("cuda")
     q = torch.randn((bt, hq, 32, 128), device=dev).to(torch.bfloat16)
     k = torch.randn((bt, hkv, T, 128), device=dev).to(torch.bfloat16)
