@@ -416,6 +416,8 @@ def run_fairkv(args):
         del caches, dec
         torch.cuda.empty_cache()
         out["emulated_tp_budget_sweep"] = budget_sweep(args, dev)
+        out["cfg4_tp8_batch_sweep"] = cfg4_batch_sweep(args, budgets, dev)
+        out["cfg5_tp8_skew_B1024"] = cfg5_skew(args, dev)
         out["cfg2_llama3.1-8b_b256_T16k"] = cfg2_sweep(args, dev, peak)
         out["full_layer"] = full_layer(args, budgets, dev)
         out["append"] = append_cost(args, budgets, dev)
@@ -517,7 +519,7 @@ def full_layer(args, budgets, dev):
     return results
 
 
-def emulate_tp(args, budgets, dev, calibrate=True):
+def emulate_tp(args, budgets, dev, calibrate=True, tps=(2, 4, 8), modes_tp8=("sha", "nodp", "dp", "dp-free")):
     """AHA vs uniform TP at 2/4/8 GPUs, each rank's shard timed alone on this GPU."""
     import numpy as np
     import torch
@@ -537,9 +539,9 @@ def emulate_tp(args, budgets, dev, calibrate=True):
     model = fk.LatencyModel(0.0, 0.0, 1.0, 0.0)
     results = {}
     samples = []  # (batch, per-request KV load of one GPU-layer, measured seconds)
-    for tp in (2, 4, 8):
+    for tp in tps:
         row = {}
-        modes = ["sha", "nodp", "dp"] + (["dp-free"] if tp == 8 else [])
+        modes = list(modes_tp8) if tp == 8 else ["sha", "nodp", "dp"]
         for mode in modes:
             ch = args.ch if mode != "dp" or tp != 8 else 8  # equal split needs CH=8 at TP=8
             plan, prof = make_plan(budgets, tp, ch, mode)
@@ -702,6 +704,40 @@ def budget_sweep(args, dev):
                                   "kv_max_over_mean": round(v["kv_max_over_mean"], 4)}
                               for m, v in r.items()}
                          for tp, r in res.items() if tp.startswith("tp")}
+    return rows
+
+
+def cfg4_batch_sweep(args, budgets, dev):
+    """BASELINE configs[3]: 70B shape, AHA-DP copy heads CH=4 (free split; at
+    TP=8 the equal split needs CH=8, reported too), batch sweep 1-64 at 8 GPUs
+    (emulated as in emulate_tp: each rank's shard timed alone)."""
+    rows = {}
+    for bt in (1, 4, 16, 64):
+        res = emulate_tp(args, budgets[:, :bt].copy(), dev, calibrate=False, tps=(8,),
+                         modes_tp8=("sha", "nodp", "dp", "dp-free"))["tp8"]
+        rows[f"batch{bt}"] = {m: {"tokens_per_s": round(v["tokens_per_s"], 1),
+                                  "gain_vs_sha": round(v.get("gain_vs_sha", 1.0), 4),
+                                  "kv_max_over_mean": round(v["kv_max_over_mean"], 4)}
+                              for m, v in res.items()}
+    return rows
+
+
+def cfg5_skew(args, dev):
+    """BASELINE configs[4]: budget 1024 (128k context), strongly skewed
+    per-head budgets (dirichlet alpha=1, zipf s=1.2 -- the reference's
+    acceptance profile shape), AHA vs uniform TP at 8 GPUs (emulated)."""
+    from paper_2502_15804_b200.sharding import synthetic_budgets
+    rows = {}
+    for dist_, param in (("dirichlet", 1.0), ("zipf", 1.2)):
+        bud = synthetic_budgets(args.layers, args.batch, HKV, 1024, window=WINDOW, alpha=ALPHA,
+                                distribution=dist_, param=param, seed=7, context=131072)
+        res = emulate_tp(args, bud, dev, calibrate=False, tps=(8,),
+                         modes_tp8=("sha", "nodp", "dp", "dp-free"))["tp8"]
+        rows[f"{dist_}{param:g}"] = {m: {"tokens_per_s": round(v["tokens_per_s"], 1),
+                                        "gain_vs_sha": round(v.get("gain_vs_sha", 1.0), 4),
+                                        "kv_max_over_mean": round(v["kv_max_over_mean"], 4),
+                                        "busy_rate": round(v["busy_rate"], 4)}
+                                    for m, v in res.items()}
     return rows
 
 
