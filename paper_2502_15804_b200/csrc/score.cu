@@ -51,7 +51,7 @@ struct ScoreParams {
   struct GridBar* gridbar;  // fused mode: zeroed counter + generation
   // MODE 4 (score + Ada split + top-k in one launch); workspace parts zeroed per launch
   int budget, floor_k, rest_total;  // B, f = floor(alpha (B - w)), R = Hkv (B - w - f)
-  uint32_t* hist;      // [kSelPasses][Bt*Hkv][256] per-pass digit histograms (zeroed)
+  uint32_t* hist;      // [kSelPasses][Bt*Hkv][2][256] per-pass digit histograms, global + floor (zeroed)
   int32_t* active;     // [kSelPasses + 1] requests still searching, per pass (zeroed)
   int32_t* need_floor; // [1] heads below their floor anywhere (zeroed)
   uint64_t* ltau;      // [Bt*Hkv] head-local floor thresholds
@@ -249,10 +249,12 @@ __device__ __forceinline__ uint64_t compose(float sc, uint32_t index) {
 // Scratch of the selection phase, placed in the (idle) Q_win region.
 struct SelScratch {
   int32_t suf[kSelMaxHeads][256];  // per-head suffix counts of the current digit
-  uint32_t hist[256];
+  uint32_t hist[256], hist2[256];  // this chunk's digits: global search, floor search
   int32_t above[kSelMaxHeads], n_at[kSelMaxHeads];
   int32_t warp_tot[kEpiWarps];
   int32_t dstar, exact;
+  uint32_t fprefix, fmask;  // floor search of this CTA's head
+  int32_t fexact, fabove, f_at, f_next;
 };
 
 // Inclusive suffix sum over d of one value per epilogue thread (d = tid).
@@ -299,6 +301,23 @@ __device__ __forceinline__ void epi_histogram(KeyOf key_of, int nk, uint64_t pre
   epi_sync();
 }
 
+// Digit histograms of the pooled keys for the global search (keys matching
+// (gp, gm), into h0) and the floor search ((fp, fm), into h1) at once.
+__device__ __forceinline__ void epi_histogram2(const float* sp, int nk, bool ga, uint32_t gp, uint32_t gm,
+                                               bool fa, uint32_t fp, uint32_t fm, int shift, uint32_t* h0,
+                                               uint32_t* h1) {
+  h0[threadIdx.x] = 0;
+  h1[threadIdx.x] = 0;
+  epi_sync();
+  for (int i = threadIdx.x; i < nk; i += 32 * kEpiWarps) {
+    const uint32_t o = orderable(sp[i]);
+    const uint32_t d = (o >> shift) & 255u;
+    if (ga && (o & gm) == gp) atomicAdd(&h0[d], 1u);
+    if (fa && (o & fm) == fp) atomicAdd(&h1[d], 1u);
+  }
+  epi_sync();
+}
+
 // CTA-local (epilogue warps) threshold such that exactly k keys are >= it.
 template <class KeyOf>
 __device__ uint64_t epi_select_kth(KeyOf key_of, int nk, int k, SelScratch& x) {
@@ -333,17 +352,18 @@ __device__ uint64_t epi_select_kth(KeyOf key_of, int nk, int k, SelScratch& x) {
 //
 // Radix search over the 32-bit orderable score, MSB-first 8-bit digits: per
 // digit each CTA histograms its own pooled keys into the per-(request, head)
-// global histogram of that pass and, after a grid barrier, every CTA of the
+// global histograms of that pass and, after a grid barrier, every CTA of the
 // request evaluates G(d) = sum_h max(0, N_h(d) - floor) from all heads'
 // histograms and takes the same d* = max{d : G(d) >= R} (the Ada split in
-// its floor-free form, see select.cu).  Four passes fix the threshold score
-// s*; keys with score > s* are chosen, and the tied keys at s* are taken in
-// the global tie order (head asc, token asc) until G reaches R exactly --
-// which needs only per-(head, chunk) tie counts, not four more radix passes
-// over the index bits.  Heads that end below their floor keep exactly their
-// own top-floor (CTA-local select).  One last barrier publishes per-chunk
-// counts so every CTA writes its chosen tokens at the right place of the
-// ascending index list.
+// its floor-free form, see select.cu).  The same passes run each head's own
+// floor search (its f-th largest score), kept if the head ends below its
+// floor; a head's global histogram is skipped once N_h < f is certain, its
+// floor histogram once N_h >= f is, and one histogram serves both while
+// they share a prefix.  Four passes fix the threshold score; ties at it are
+// taken in the global tie order (head asc, token asc) -- or the head's token
+// order for the floor -- from per-chunk tie counts, with no passes over the
+// index bits.  One last barrier publishes per-chunk counts so every CTA
+// writes its chosen tokens at the right place of the ascending index list.
 template <class Smem>
 __device__ void select_phase(const ScoreParams& p, Smem& sm, int b, int h, int bh, int chunk, int n,
                              int t_beg, int nk, const float* sp) {
@@ -352,29 +372,58 @@ __device__ void select_phase(const ScoreParams& p, Smem& sm, int b, int h, int b
   const int HK = p.hkv, BH = gridDim.y;
   const int f = p.floor_k, R = p.rest_total;
   sstamp(1);
-  if (tid < HK) x.above[tid] = 0, x.n_at[tid] = 0;
+  if (tid < HK) x.above[tid] = 0, x.n_at[tid] = R > 0 ? n : 0;
+  if (tid == 0) {
+    x.fprefix = x.fmask = 0;
+    x.fexact = f <= 0;
+    x.fabove = 0;
+  }
   epi_sync();
   uint32_t prefix = 0, mask = 0;
   bool exact = R <= 0;
   int dstar = 0;
   for (int pass = 0, shift = 24; pass < 4; ++pass, shift -= 8) {
-    if (!exact) {  // add my keys' digit histogram to this pass's global one
-      epi_histogram([&](int i) { return static_cast<uint64_t>(orderable(sp[i])); }, nk, prefix, mask,
-                    shift, x.hist);
-      uint32_t* gh = p.hist + (static_cast<int64_t>(pass) * BH + bh) * 256;
-      if (x.hist[tid]) atomicAdd(gh + tid, x.hist[tid]);
+    // global: N_h >= f still possible; floor: N_h < f still possible
+    const bool ga = !exact && x.n_at[h] >= f;
+    const bool fa = !x.fexact && (exact ? x.n_at[h] < f : x.above[h] < f);
+    const bool same = ga && fa && prefix == x.fprefix && mask == x.fmask;
+    uint32_t* gh = p.hist + (static_cast<int64_t>(pass) * BH + bh) * 512;
+    if (ga || fa) {  // add my keys' digit histograms to this pass's global ones
+      epi_histogram2(sp, nk, ga, prefix, mask, fa && !same, x.fprefix, x.fmask, shift, x.hist, x.hist2);
+      if (ga && x.hist[tid]) atomicAdd(gh + tid, x.hist[tid]);
+      const uint32_t fc = same ? x.hist[tid] : (fa ? x.hist2[tid] : 0u);
+      if (fc) atomicAdd(gh + 256 + tid, fc);
     }
     sstamp(2 + 2 * pass);
     epi_grid_sync(p.gridbar);  // fixed pass count: uniform across the grid
     sstamp(3 + 2 * pass);
-    if (exact) continue;
+    if (fa) {  // my head's floor search: d* = max{d : S(d) >= f}
+      const int32_t v = static_cast<int32_t>(__ldcg(gh + 256 + tid));
+      const int32_t sfx = epi_suffix_sum(v, x) + x.fabove;
+      const int32_t cnt = epi_count(sfx >= f, x);
+      if (tid == cnt - 1) {
+        x.f_at = sfx;
+        x.f_next = sfx - v;
+      }
+      epi_sync();
+      if (tid == 0) {
+        x.fprefix |= static_cast<uint32_t>(cnt - 1) << shift;
+        x.fmask |= 255u << shift;
+        x.fabove = x.f_next;
+        x.fexact = x.f_at == f;
+      }
+    }
+    if (exact) {
+      epi_sync();
+      continue;
+    }
     // suffix counts of every head of this request (all heads' histograms
     // loaded at once, one L2 round trip), then d* = max{d : G(d) >= R}
     {
-      const uint32_t* gh = p.hist + (static_cast<int64_t>(pass) * BH + b * HK) * 256 + tid;
+      const uint32_t* gq = p.hist + (static_cast<int64_t>(pass) * BH + b * HK) * 512 + tid;
       int32_t v[kSelMaxHeads];
 #pragma unroll
-      for (int hh = 0; hh < kSelMaxHeads; ++hh) v[hh] = hh < HK ? static_cast<int32_t>(__ldcg(gh + hh * 256)) : 0;
+      for (int hh = 0; hh < kSelMaxHeads; ++hh) v[hh] = hh < HK ? static_cast<int32_t>(__ldcg(gq + hh * 512)) : 0;
 #pragma unroll
       for (int off = 1; off < 32; off <<= 1)
 #pragma unroll
@@ -448,31 +497,36 @@ __device__ void select_phase(const ScoreParams& p, Smem& sm, int b, int h, int b
   }
   epi_sync();
   const int hstar = x.dstar, kstar = x.exact;
-  const uint32_t sstar = prefix;
   const bool below = !have_tau || x.n_at[h] < f;
   auto budget_of = [&](int hh) {
     const int c = have_tau ? max(0, x.n_at[hh] - f) : 0;
     return p.window + f + c;
   };
-
-  // heads that end below their floor keep exactly their own top-floor tokens
-  if (below && f > 0 && chunk == 0) {
-    const float* srow = p.scores + static_cast<int64_t>(bh) * n;
-    const uint64_t lt = epi_select_kth(
-        [&](int i) { return compose(__ldcg(srow + i), static_cast<uint32_t>(i)); }, n, f, x);
-    if (tid == 0) p.ltau[bh] = lt;
+  // keep rule of my head: kind 0 = above thr + ranked ties at thr (the first
+  // ktie in order), 1 = o >= thr, 2 = nothing
+  int kind = 2, ktie = 0;
+  uint32_t thr = 0;
+  if (below) {  // exactly its own top-f
+    if (f > 0) {
+      thr = x.fprefix;
+      kind = x.fexact ? 1 : 0;
+      ktie = x.fexact ? 0 : f - x.fabove;
+    }
+  } else if (exact) {
+    thr = prefix;
+    kind = 1;
+  } else {
+    thr = prefix;
+    kind = 0;
+    ktie = h < hstar ? 0x7fffffff : (h == hstar ? kstar : 0);
   }
-  epi_grid_sync(p.gridbar);
-  const uint64_t ltau = below && f > 0 ? __ldcg(reinterpret_cast<const unsigned long long*>(p.ltau + bh))
-                                       : kNoKey;
-  // class of key i: 1 = chosen outright, 2 = tie at s* (hstar decides by tie rank)
+  // class of key i: 1 = chosen outright, 2 = tie at thr taken by tie rank
   auto klass = [&](int i) -> int {
-    if (below) return ltau != kNoKey && compose(sp[i], static_cast<uint32_t>(t_beg + i)) >= ltau;
-    if (!have_tau) return 0;
+    if (kind == 2) return 0;
     const uint32_t o = orderable(sp[i]);
-    if (exact) return (o & mask) >= prefix;
-    if (o > sstar) return 1;
-    return o == sstar ? (h < hstar ? 1 : (h == hstar ? 2 : 0)) : 0;
+    if (kind == 1) return o >= thr;
+    if (o != thr) return o > thr;
+    return ktie == 0x7fffffff ? 1 : (ktie > 0 ? 2 : 0);
   };
   // publish (chosen outright, ties) of this chunk
   int32_t c1 = 0, c2 = 0;
@@ -502,16 +556,15 @@ __device__ void select_phase(const ScoreParams& p, Smem& sm, int b, int h, int b
     pos += cc.x;
     tie0 += cc.y;
   }
-  // tie counts of earlier chunks decide how many of their ties were taken
   {
-    // warp 0 reduces (every warp computed the same partial sums per lane)
+    // every warp computed the same partial sums per lane
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
       pos += __shfl_xor_sync(0xffffffffu, pos, off);
       tie0 += __shfl_xor_sync(0xffffffffu, tie0, off);
     }
   }
-  if (h == hstar) pos += min(tie0, kstar);  // ties of earlier chunks that were taken
+  pos += min(tie0, ktie);  // ties of earlier chunks that were taken
   int64_t off = static_cast<int64_t>(b) * HK * p.budget;
   for (int hh = 0; hh < h; ++hh) off += budget_of(hh);
   const int bud = budget_of(h);
@@ -529,7 +582,7 @@ __device__ void select_phase(const ScoreParams& p, Smem& sm, int b, int h, int b
       if (j < wid) tb += x.suf[1][j];
       t_tot += x.suf[1][j];
     }
-    const bool take = k == 1 || (k == 2 && tie_run + tb < kstar);
+    const bool take = k == 1 || (k == 2 && tie_run + tb < ktie);
     const uint32_t bal = __ballot_sync(0xffffffffu, take);
     if (lane == 0) x.suf[0][wid] = __popc(bal);
     epi_sync();
@@ -951,7 +1004,7 @@ ScoreLayout score_layout(int batch, int hkv, int T, int window, int group) {
   L.raw = a16(L.stats + static_cast<int64_t>(L.bh) * L.chunks * gw * 2 * 4);
   L.gridbar = a16(L.raw + static_cast<int64_t>(L.bh) * (T - window) * 4);
   L.hist = a16(L.gridbar + 64);
-  L.active = a16(L.hist + static_cast<int64_t>(kSelPasses) * L.bh * 256 * 4);
+  L.active = a16(L.hist + static_cast<int64_t>(kSelPasses) * L.bh * 512 * 4);
   L.ltau = a16(L.active + (kSelPasses + 2) * 4);
   L.counts = a16(L.ltau + static_cast<int64_t>(L.bh) * 8);
   L.sel = a16(L.counts + static_cast<int64_t>(L.bh) * L.chunks * 8);

@@ -182,6 +182,7 @@ def test_fused_ada_select_bit_exact(cuda_device, bt, T, budget, ties, hkv, alpha
     (2, 64, 8, 6000, 256, 2.0, False),    # 70B shape (G*w = 256)
     (1, 32, 8, 20000, 1024, 3.0, False),  # long context, several chunks per head
     (2, 32, 8, 3000, 256, 2.0, True),     # a head whose window soaks up all attention: below its floor
+    (1, 32, 8, 40000, 1024, 3.0, True),   # the same over many chunks per head (joint floor search)
     (20, 32, 8, 600, 64, 2.0, False),     # 160 heads > 148 SMs: two-launch fallback
     (1, 64, 8, 131072, 1024, 2.0, False),  # cfg5: 128k context, B=1024, 70B shape
 ])
