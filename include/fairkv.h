@@ -226,15 +226,20 @@ int fkv_snapkv_select(const void* q_win, const void* k, int32_t batch, int32_t h
  * int32 [batch, hkv] = window + floor_k + (# of the head's tokens in the
  * global top-(hkv*(budget-window-floor_k)) of the non-floor scores), order
  * (score desc, head asc, token asc); floor = per-head top-floor_k by (score
- * desc, token asc).  Every row sums to hkv*budget. */
+ * desc, token asc).  Every row sums to hkv*budget.  Same grid-wide kernel
+ * as fkv_ada_select (budgets only); workspace as there.  Hkv <= 16. */
 int fkv_ada_budgets(const float* scores, int32_t batch, int32_t hkv, int32_t n, int32_t budget,
-                    int32_t window, int32_t floor_k, int32_t* budgets, void* stream);
+                    int32_t window, int32_t floor_k, int32_t* budgets, void* workspace,
+                    void* stream);
 
 /* K2: per-head top-(budgets - window) by (score desc, token asc), written
  * ascending at idx[offsets[bh]..], followed by the window tokens n..n+window-1;
- * offsets int64 [batch*hkv + 1] is the exclusive prefix sum of budgets. */
+ * offsets int64 [batch*hkv + 1] is the exclusive prefix sum of budgets (any
+ * budgets >= window).  Same grid-wide kernel as fkv_ada_select (each head's
+ * own radix search); workspace as there.  Hkv <= 16. */
 int fkv_topk_select(const float* scores, const int32_t* budgets, int32_t batch, int32_t hkv,
-                    int32_t n, int32_t window, int64_t* offsets, int32_t* idx, void* stream);
+                    int32_t n, int32_t window, int64_t* offsets, int32_t* idx, void* workspace,
+                    void* stream);
 
 /* A18 + K2 fused: one cooperative launch over every (request, head) -- the
  * keys of each head are cut into chunks dealt out to persistent CTAs, a

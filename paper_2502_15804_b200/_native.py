@@ -55,10 +55,10 @@ _SIGS = {
     "fkv_score_workspace_bytes": (C.c_int64, [_i32, _i32, _i32, _i32, _i32]),
     "fkv_snapkv_select": (C.c_int, [_vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _f32, _i32, _i32,
                                     _vp, _vp, _vp, _vp, _vp, _vp]),
-    "fkv_ada_budgets": (C.c_int, [_vp, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _vp]),
+    "fkv_ada_budgets": (C.c_int, [_vp, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp]),
     "fkv_ada_select_workspace_bytes": (C.c_int64, [_i32, _i32, _i32]),
     "fkv_ada_select": (C.c_int, [_vp, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp]),
-    "fkv_topk_select": (C.c_int, [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _vp]),
+    "fkv_topk_select": (C.c_int, [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp]),
     "fkv_append": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _vp]),
     "fkv_compact": (C.c_int, [_vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _vp,
                               _vp, _vp]),

@@ -5,17 +5,12 @@
 // "Algorithm definitions" and restated in oracle/kv.py:
 //   per-head order  (score desc, token asc)
 //   global order    (score desc, head asc, token asc)
-// Both are made total by a 64-bit composite key
-//   key64 = orderable(score) << 32 | (0xffffffff - index)
-// (index = token, or head * n + token for the global order), so a radix
-// select over key64 returns exactly k elements and results are exact
-// functions of the fp32 score tensor -- bit-exact against the oracle fed the
-// same scores.
-//
-// Radix select: one CTA, MSB-first 8-bit digits, warp-aggregated
-// shared-memory histograms (__match_any_sync: the top digits of float keys
-// are nearly all equal, so naive per-thread atomics would serialise), early
-// exit when the threshold bucket is taken whole.
+// One grid-wide kernel serves the three entry points (fkv_ada_select,
+// fkv_ada_budgets, fkv_topk_select): a radix search over the 32-bit
+// orderable score finds the threshold score, and the keys tied at it are
+// taken in the tie order above from per-range tie counts -- so results are
+// exact functions of the fp32 score tensor, bit-exact against the oracle fed
+// the same scores, without passes over the index bits.
 #include <cuda_runtime.h>
 
 #include "common.cuh"
@@ -23,209 +18,9 @@
 namespace fkv {
 namespace {
 
-constexpr int kThreads = 1024;
-constexpr uint64_t kNone = ~0ull;
-
 __device__ __forceinline__ uint32_t orderable(float f) {
   const uint32_t u = __float_as_uint(f);
   return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
-}
-
-__device__ __forceinline__ uint64_t compose(float s, uint32_t index) {
-  return (static_cast<uint64_t>(orderable(s)) << 32) | (0xffffffffu - index);
-}
-
-struct SelectSmem {
-  uint32_t hist[256];
-  uint32_t gh[256];  // cluster-summed histogram
-  uint32_t count;
-  uint32_t digit, above;
-  uint32_t warp_tot[32];
-  uint64_t tau_head[64];
-  uint32_t count_head[64];
-};
-
-// Threshold tau such that exactly k of the valid elements have key >= tau
-// (1 <= k <= #valid).  key_of(i, &key) -> valid.
-template <class KeyOf>
-__device__ uint64_t cta_select_kth(KeyOf key_of, int n, uint32_t k, SelectSmem& sm) {
-  uint64_t prefix = 0, mask = 0;
-  uint32_t need = k;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int shift = 56; shift >= 0; shift -= 8) {
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) sm.hist[i] = 0;
-    __syncthreads();
-    for (int base = 0; base < n; base += blockDim.x) {
-      const int i = base + threadIdx.x;
-      uint64_t key = 0;
-      const bool ok = i < n && key_of(i, key) && (key & mask) == prefix;
-      const uint32_t d = ok ? static_cast<uint32_t>(key >> shift) & 255u : 256u;
-      const uint32_t peers = __match_any_sync(0xffffffffu, d);
-      if (ok && lane == __ffs(peers) - 1) atomicAdd(&sm.hist[d], __popc(peers));
-    }
-    __syncthreads();
-    if (warp == 0) {
-      // lane L owns bins [8L, 8L+8); find the bin holding the need-th largest
-      uint32_t local = 0;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) local += sm.hist[8 * lane + j];
-      uint32_t incl = local;  // inclusive suffix sum over lanes >= this one
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const uint32_t v = __shfl_down_sync(0xffffffffu, incl, off);
-        if (lane + off < 32) incl += v;
-      }
-      const uint32_t suffix = incl - local;
-      if (suffix < need && suffix + local >= need) {
-        uint32_t acc = suffix;
-        for (int j = 7; j >= 0; --j) {
-          const uint32_t c = sm.hist[8 * lane + j];
-          if (acc + c >= need) {
-            sm.digit = 8 * lane + j;
-            sm.above = acc;
-            break;
-          }
-          acc += c;
-        }
-      }
-    }
-    __syncthreads();
-    const uint32_t d = sm.digit;
-    need -= sm.above;
-    prefix |= static_cast<uint64_t>(d) << shift;
-    mask |= 255ull << shift;
-    const bool whole = sm.hist[d] == need;
-    __syncthreads();
-    if (whole) return prefix;
-  }
-  return prefix;
-}
-
-// Exclusive block scan of a 0/1 flag (one per thread), returns the total.
-__device__ uint32_t block_flag_scan(bool flag, uint32_t& before, SelectSmem& sm) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t ballot = __ballot_sync(0xffffffffu, flag);
-  const uint32_t in_warp = __popc(ballot & ((1u << lane) - 1u));
-  if (lane == 0) sm.warp_tot[warp] = __popc(ballot);
-  __syncthreads();
-  uint32_t warp_base = 0, total = 0;
-  const int nw = blockDim.x >> 5;
-  for (int w = 0; w < nw; ++w) {
-    const uint32_t t = sm.warp_tot[w];
-    if (w < warp) warp_base += t;
-    total += t;
-  }
-  __syncthreads();
-  before = warp_base + in_warp;
-  return total;
-}
-
-__device__ uint32_t block_sum(uint32_t v, SelectSmem& sm) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-  if (lane == 0) sm.warp_tot[warp] = v;
-  __syncthreads();
-  uint32_t total = 0;
-  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) total += sm.warp_tot[w];
-  __syncthreads();
-  return total;
-}
-
-// ---------------------------------------------------------------- A18 ----
-// grid = Bt, one CTA per request.  scores f32 [Bt, Hkv, n] (pooled).
-__global__ void __launch_bounds__(kThreads)
-    ada_budgets_kernel(const float* __restrict__ scores, int hkv, int n, int window, int floor_k,
-                       int rest_total, int32_t* __restrict__ budgets) {
-  __shared__ SelectSmem sm;
-  const int b = blockIdx.x;
-  const float* s = scores + static_cast<int64_t>(b) * hkv * n;
-  // phase 1: per-head floors (top floor_k by (score desc, token asc))
-  for (int h = 0; h < hkv; ++h) {
-    uint64_t tau = kNone;
-    if (floor_k > 0) {
-      const float* sh = s + static_cast<int64_t>(h) * n;
-      tau = cta_select_kth(
-          [&](int i, uint64_t& key) {
-            key = compose(sh[i], static_cast<uint32_t>(i));
-            return true;
-          },
-          n, static_cast<uint32_t>(floor_k), sm);
-    }
-    if (threadIdx.x == 0) sm.tau_head[h] = tau;
-    __syncthreads();
-  }
-  auto in_floor = [&](int h, int t) -> bool {
-    const uint64_t tau = sm.tau_head[h];
-    return tau != kNone && compose(s[static_cast<int64_t>(h) * n + t], static_cast<uint32_t>(t)) >= tau;
-  };
-  // phase 2: global top rest_total over the non-floor elements
-  const int total = hkv * n;
-  uint64_t gtau = kNone;
-  if (rest_total > 0) {
-    gtau = cta_select_kth(
-        [&](int i, uint64_t& key) {
-          const int h = i / n, t = i - h * n;
-          if (in_floor(h, t)) return false;
-          key = compose(s[i], static_cast<uint32_t>(i));
-          return true;
-        },
-        total, static_cast<uint32_t>(rest_total), sm);
-  }
-  // phase 3: per-head counts of globally chosen elements
-  for (int h = 0; h < hkv; ++h) {
-    uint32_t c = 0;
-    if (gtau != kNone) {
-      for (int t = threadIdx.x; t < n; t += blockDim.x) {
-        const int i = h * n + t;
-        if (!in_floor(h, t) && compose(s[i], static_cast<uint32_t>(i)) >= gtau) ++c;
-      }
-    }
-    const uint32_t tot = block_sum(c, sm);
-    if (threadIdx.x == 0) budgets[b * hkv + h] = window + floor_k + static_cast<int32_t>(tot);
-  }
-}
-
-// ----------------------------------------------------------------- K2 ----
-// grid = Bt * Hkv.  Writes offsets[bh] (exclusive prefix of budgets) and the
-// selected tokens of head (b,h) ascending, then the window tokens n..n+w-1.
-__global__ void __launch_bounds__(kThreads)
-    topk_select_kernel(const float* __restrict__ scores, const int32_t* __restrict__ budgets,
-                       int n, int window, int64_t* __restrict__ offsets,
-                       int32_t* __restrict__ idx) {
-  __shared__ SelectSmem sm;
-  const int bh = blockIdx.x;
-  // offset = sum of budgets before this head
-  uint32_t part = 0;
-  for (int j = threadIdx.x; j < bh; j += blockDim.x) part += static_cast<uint32_t>(budgets[j]);
-  const int64_t off = block_sum(part, sm);
-  if (threadIdx.x == 0) {
-    offsets[bh] = off;
-    if (bh == gridDim.x - 1) offsets[bh + 1] = off + budgets[bh];
-  }
-  const int k = budgets[bh] - window;
-  const float* s = scores + static_cast<int64_t>(bh) * n;
-  int32_t* out = idx + off;
-  if (k > 0) {
-    const uint64_t tau =
-        k >= n ? 0ull
-               : cta_select_kth(
-                     [&](int i, uint64_t& key) {
-                       key = compose(s[i], static_cast<uint32_t>(i));
-                       return true;
-                     },
-                     n, static_cast<uint32_t>(k), sm);
-    uint32_t written = 0;
-    for (int base = 0; base < n; base += blockDim.x) {
-      const int t = base + threadIdx.x;
-      const bool take = t < n && compose(s[t], static_cast<uint32_t>(t)) >= tau;
-      uint32_t before;
-      const uint32_t tot = block_flag_scan(take, before, sm);
-      if (take) out[written + before] = t;
-      written += tot;
-    }
-  }
-  for (int i = threadIdx.x; i < window; i += blockDim.x) out[max(k, 0) + i] = n + i;
 }
 
 // ------------------------------------------- A18 + K2, grid-wide search ----
@@ -265,6 +60,9 @@ constexpr int kGUnroll = 4;
 struct GSelParams {
   const float* scores;  // [BH, n] of this launch
   int hkv, n, window, f, R, budget;
+  const int32_t* head_k;       // top-k mode: per-head budgets of this launch (incl. window); null = Ada
+  const int32_t* budgets_all;  // top-k mode: all budgets (offsets are their exclusive prefix)
+  int select;                  // 0: budgets only (Ada mode)
   int req0, bh_total;   // first request of this launch; Bt*Hkv over all launches
   int64_t total;        // BH * n
   uint32_t* hist;       // [kGBufs][BH][2][256] (buffers 0, 1 zeroed by the host)
@@ -280,9 +78,9 @@ struct GReq {  // global search of one request
   int exact, hstar, kstar;
   int above[kGMaxHeads], n_at[kGMaxHeads];
 };
-struct GHead {  // floor search of one head
+struct GHead {  // floor search of one head (its own top-f; top-k mode: f = k)
   uint32_t prefix, mask;
-  int exact, above, n_at;
+  int exact, above, n_at, f;
 };
 struct GRule {  // final keep rule of one head: 0 = ties ranked, 1 = o >= prefix, 2 = none
   uint32_t prefix;
@@ -297,6 +95,9 @@ struct GSelSmem {
   GRule rule[kGMaxPieces];
   uint8_t fact[kGMaxPieces];  // floor histogram built this pass
   int2 pc[kGMaxPieces][kGWarps];  // (chosen outright, ties) per piece and warp segment
+  int64_t off[kGMaxPieces];       // index-list offset of each local head
+  int32_t bud[kGMaxPieces];       // budget of each local head
+  long long red[kGWarps];
   int32_t wt[2][kGWarps];
   int32_t tmp;
 };
@@ -429,7 +230,12 @@ __global__ void __launch_bounds__(kGThreads) grid_select_kernel(const GSelParams
     r.hstar = HK;
     r.kstar = 0;
   }
-  if (tid < n_lh) sm.fl[tid] = GHead{0u, 0u, f <= 0, 0, n};
+  if (tid < n_lh) {
+    int fh = f;
+    if (p.head_k) fh = min(max(p.head_k[bh_lo + tid] - p.window, 0), n);
+    // no floor search: none to keep, all kept (prefix 0 takes every key), or budgets only
+    sm.fl[tid] = GHead{0u, 0u, fh <= 0 || fh >= n || !p.select, 0, n, fh};
+  }
   gstamp(0);
   __syncthreads();
 
@@ -442,7 +248,7 @@ __global__ void __launch_bounds__(kGThreads) grid_select_kernel(const GSelParams
       const GHead& fh = sm.fl[lh];
       // global: N_h >= f still possible; floor: N_h < f still possible
       const bool ga = !rq.exact && rq.n_at[h] >= f;
-      const bool fa = !fh.exact && (rq.exact ? rq.n_at[h] < f : rq.above[h] < f);
+      const bool fa = !fh.exact && (rq.exact ? rq.n_at[h] < fh.f : rq.above[h] < fh.f);
       const bool same = ga && fa && rq.prefix == fh.prefix && rq.mask == fh.mask;
       if (tid == 0) sm.fact[lh] = fa;
       if (!ga && !fa) continue;
@@ -529,7 +335,7 @@ __global__ void __launch_bounds__(kGThreads) grid_select_kernel(const GSelParams
       warp_suffix(hb + static_cast<int64_t>(bh_lo + lh) * 512 + 256, fh.above, sv, up);
       int c = 0;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) c += sv[j] >= f;
+      for (int j = 0; j < 8; ++j) c += sv[j] >= fh.f;
       const int dstar = __reduce_add_sync(0xffffffffu, c) - 1;
       int at = 0, nxt = 0;
 #pragma unroll
@@ -545,7 +351,7 @@ __global__ void __launch_bounds__(kGThreads) grid_select_kernel(const GSelParams
         fh.above = nxt;
         fh.prefix |= static_cast<uint32_t>(dstar) << shift;
         fh.mask |= 255u << shift;
-        fh.exact = at == f;
+        fh.exact = at == fh.f;
       }
     }
     __syncthreads();
@@ -580,10 +386,10 @@ __global__ void __launch_bounds__(kGThreads) grid_select_kernel(const GSelParams
     const GReq& rq = sm.req[bh / HK - rq_lo];
     const GHead& fh = sm.fl[tid];
     GRule r;
-    if (R <= 0 || rq.n_at[h] < f) {  // below the floor: own top-f
-      if (f <= 0) r = GRule{0u, 2, 0};
+    if (R <= 0 || rq.n_at[h] < f) {  // below the floor (or top-k mode): own top-f
+      if (fh.f <= 0) r = GRule{0u, 2, 0};
       else if (fh.exact) r = GRule{fh.prefix, 1, 0};
-      else r = GRule{fh.prefix, 0, f - fh.above};
+      else r = GRule{fh.prefix, 0, fh.f - fh.above};
     } else if (rq.exact) {
       r = GRule{rq.prefix, 1, 0};
     } else {
@@ -592,15 +398,42 @@ __global__ void __launch_bounds__(kGThreads) grid_select_kernel(const GSelParams
     sm.rule[tid] = r;
   }
   __syncthreads();
-  auto budget_of = [&](const GReq& rq, int h) {
-    return p.window + f + (R > 0 ? max(0, rq.n_at[h] - f) : 0);
-  };
-  auto head_offset = [&](const GReq& rq, int bh) {
-    const int b = bh / HK, h = bh - b * HK;
+  // budgets and index-list offsets of my heads
+  if (p.head_k) {  // top-k mode: exclusive prefix of the given budgets
+    const int first = p.req0 * HK + bh_lo;
+    long long part = 0;
+    for (int i = tid; i < first; i += kGThreads) part += p.budgets_all[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    if (lane == 0) sm.red[wid] = part;
+    __syncthreads();
+    if (tid == 0) {
+      long long off = 0;
+      for (int j = 0; j < kGWarps; ++j) off += sm.red[j];
+      for (int lh = 0; lh < n_lh; ++lh) {
+        sm.off[lh] = off;
+        sm.bud[lh] = p.head_k[bh_lo + lh];
+        off += sm.bud[lh];
+      }
+    }
+  } else if (tid < n_lh) {  // Ada mode: request b starts at b * Hkv * budget
+    const int bh = bh_lo + tid, b = bh / HK, h = bh - b * HK;
+    const GReq& rq = sm.req[b - rq_lo];
+    auto budget_of = [&](int hh) { return p.window + f + (R > 0 ? max(0, rq.n_at[hh] - f) : 0); };
     int64_t off = static_cast<int64_t>(p.req0 + b) * HK * p.budget;
-    for (int hh = 0; hh < h; ++hh) off += budget_of(rq, hh);
-    return off;
-  };
+    for (int hh = 0; hh < h; ++hh) off += budget_of(hh);
+    sm.off[tid] = off;
+    sm.bud[tid] = budget_of(h);
+  }
+  __syncthreads();
+  if (!p.select) {  // budgets only (uniform: no barrier follows)
+    for (int lh = tid; lh < n_lh; lh += kGThreads) {
+      int lo, hi;
+      piece(lh, lo, hi);
+      if (lo == 0) p.budgets[bh_lo + lh] = sm.bud[lh];
+    }
+    return;
+  }
 
   // ---- per-warp-segment counts of every piece (warp w scans a contiguous
   // 1/16 of the piece's aligned body; warp 0 also the keys before it, the
@@ -651,13 +484,13 @@ __global__ void __launch_bounds__(kGThreads) grid_select_kernel(const GSelParams
     c1 = __reduce_add_sync(0xffffffffu, c1);
     c2 = __reduce_add_sync(0xffffffffu, c2);
     if (lane == 0) sm.pc[lh][wid] = make_int2(c1, c2);
-    if (lo == 0) {
-      const GReq& rq = sm.req[bh / HK - rq_lo];
-      const int bud = budget_of(rq, bh % HK);
-      const int64_t off = head_offset(rq, bh);
-      for (int i = tid; i < p.window; i += kGThreads) p.idx[off + bud - p.window + i] = n + i;
+    if (lo == 0) {  // window tokens after the head's selected ones
+      const int bud = sm.bud[lh];
+      const int64_t off = sm.off[lh];
+      const int kept = p.head_k ? sm.fl[lh].f : bud - p.window;
+      for (int i = tid; i < p.window; i += kGThreads) p.idx[off + kept + i] = n + i;
       if (tid == 0) {
-        p.budgets[bh] = bud;
+        if (!p.head_k) p.budgets[bh] = bud;
         p.offsets[bh] = off;
         if (p.req0 * HK + bh == p.bh_total - 1) p.offsets[bh + 1] = off + bud;
       }
@@ -690,7 +523,6 @@ __global__ void __launch_bounds__(kGThreads) grid_select_kernel(const GSelParams
     const int bh = bh_lo + lh;
     const GRule r = sm.rule[lh];
     if (r.kind == 2) continue;
-    const GReq& rq = sm.req[bh / HK - rq_lo];
     int lo, hi;
     piece(lh, lo, hi);
     int pos = 0, tie0 = 0;
@@ -712,7 +544,7 @@ __global__ void __launch_bounds__(kGThreads) grid_select_kernel(const GSelParams
     for (int j = 0; j < wid; ++j) c1b += sm.pc[lh][j].x, tb += sm.pc[lh][j].y;
     int tie_run = tie0 + tb;
     pos += c1b + min(tie_run, r.ktie) - min(tie0, r.ktie);
-    int32_t* out = p.idx + head_offset(rq, bh);
+    int32_t* out = p.idx + sm.off[lh];
     const float* s = p.scores + static_cast<int64_t>(bh) * n;
     const Seg g = segment(s, lo, hi);
     auto emit_scalar = [&](int i0, int i1) {
@@ -792,38 +624,84 @@ int gsel_reqs_per_launch(int hkv) {
 }  // namespace
 }  // namespace fkv
 
-extern "C" int fkv_ada_budgets(const float* scores, int32_t batch, int32_t hkv, int32_t n,
-                               int32_t budget, int32_t window, int32_t floor_k, int32_t* budgets,
-                               void* stream) {
-  using namespace fkv;
-  if ((!scores && n > 0) || !budgets) return set_error(FKV_ERR_INVALID, "fkv_ada_budgets: null pointer");
-  if (batch < 0 || hkv < 1 || hkv > 64 || n < 0 || window < 0 || floor_k < 0)
-    return set_error(FKV_ERR_INVALID, "fkv_ada_budgets: bad sizes");
-  const int sel = budget - window;
-  if (sel < 0 || sel > n || floor_k > sel)
-    return set_error(FKV_ERR_INVALID, "fkv_ada_budgets: need 0 <= floor <= budget-window <= n");
-  if (static_cast<int64_t>(hkv) * n >= 0x7fffffffLL)
-    return set_error(FKV_ERR_INVALID, "fkv_ada_budgets: Hkv * n too large");
-  if (batch == 0) return FKV_OK;
-  const int rest = hkv * sel - hkv * floor_k;
-  ada_budgets_kernel<<<batch, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
-      scores, hkv, n, window, floor_k, rest, budgets);
-  return cuda_check(cudaGetLastError(), "ada_budgets launch");
+namespace fkv {
+namespace {
+
+// n == 0: nothing to rank -- every head keeps its window only.
+__global__ void window_only_kernel(int bh_total, int window, const int32_t* head_k, int32_t* budgets,
+                                   int64_t* offsets, int32_t* idx) {
+  int64_t off = 0;
+  for (int bh = 0; bh < bh_total; ++bh) {
+    const int bud = head_k ? head_k[bh] : window;
+    if (threadIdx.x == 0) {
+      if (!head_k && budgets) budgets[bh] = bud;
+      if (offsets) offsets[bh] = off;
+    }
+    if (idx)
+      for (int i = threadIdx.x; i < window; i += blockDim.x) idx[off + i] = i;
+    off += bud;
+  }
+  if (threadIdx.x == 0 && offsets) offsets[bh_total] = off;
 }
 
-extern "C" int fkv_topk_select(const float* scores, const int32_t* budgets, int32_t batch,
-                               int32_t hkv, int32_t n, int32_t window, int64_t* offsets,
-                               int32_t* idx, void* stream) {
-  using namespace fkv;
-  if ((!scores && n > 0) || !budgets || !offsets || !idx)
-    return set_error(FKV_ERR_INVALID, "fkv_topk_select: null pointer");
-  if (batch < 0 || hkv < 1 || n < 0 || window < 0)
-    return set_error(FKV_ERR_INVALID, "fkv_topk_select: bad sizes");
+// The three entry points: Ada split + selection (head_k null, select 1),
+// Ada budgets only (select 0), per-head top-k of given budgets (head_k).
+int grid_select(const float* scores, int batch, int hkv, int n, int budget, int window, int floor_k,
+                const int32_t* head_k, int select, int32_t* budgets, int64_t* offsets, int32_t* idx,
+                void* workspace, cudaStream_t st) {
   if (batch == 0) return FKV_OK;
-  topk_select_kernel<<<batch * hkv, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
-      scores, budgets, n, window, offsets, idx);
-  return cuda_check(cudaGetLastError(), "topk_select launch");
+  if (n == 0) {
+    window_only_kernel<<<1, 32, 0, st>>>(batch * hkv, window, head_k, budgets, select ? offsets : nullptr,
+                                         select ? idx : nullptr);
+    return cuda_check(cudaGetLastError(), "window-only launch");
+  }
+  const int per = gsel_reqs_per_launch(hkv);
+  const int sel = budget - window;
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  for (int r0 = 0; r0 < batch; r0 += per) {
+    const int reqs = batch - r0 < per ? batch - r0 : per;
+    const int bh = reqs * hkv;
+    GSelParams p{};
+    p.scores = scores + static_cast<int64_t>(r0) * hkv * n;
+    p.hkv = hkv;
+    p.n = n;
+    p.window = window;
+    p.f = head_k ? 0 : floor_k;
+    p.R = head_k ? 0 : hkv * sel - hkv * floor_k;
+    p.budget = budget;
+    p.head_k = head_k ? head_k + static_cast<int64_t>(r0) * hkv : nullptr;
+    p.budgets_all = head_k;
+    p.select = select;
+    p.req0 = r0;
+    p.bh_total = batch * hkv;
+    p.total = static_cast<int64_t>(bh) * n;
+    p.bar = reinterpret_cast<unsigned*>(ws);
+    p.hist = reinterpret_cast<uint32_t*>(ws + 256);
+    p.counts = reinterpret_cast<int2*>(ws + 256 + static_cast<int64_t>(kGBufs) * bh * 512 * 4);
+    p.budgets = head_k ? nullptr : budgets + static_cast<int64_t>(r0) * hkv;
+    p.offsets = offsets ? offsets + static_cast<int64_t>(r0) * hkv : nullptr;
+    p.idx = idx;
+    // barrier counter + the histogram buffers of passes 0 and 1
+    if (int rc = cuda_check(cudaMemsetAsync(ws, 0, 256 + static_cast<size_t>(2) * bh * 512 * 4, st),
+                            "select workspace reset"))
+      return rc;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(gsel_grid(bh, n), 1, 1);
+    cfg.blockDim = dim3(kGThreads, 1, 1);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (int rc = cuda_check(cudaLaunchKernelEx(&cfg, grid_select_kernel, p), "grid select launch"))
+      return rc;
+  }
+  return FKV_OK;
 }
+
+}  // namespace
+}  // namespace fkv
 
 extern "C" int fkv__select_stamps(unsigned long long* host) {
   return fkv::cuda_check(cudaMemcpyFromSymbol(host, fkv::g_gstamps, sizeof(unsigned long long) * 32),
@@ -838,63 +716,53 @@ extern "C" int64_t fkv_ada_select_workspace_bytes(int32_t batch, int32_t hkv, in
   return 256 + hist + static_cast<int64_t>(gsel_ctas()) * 8;
 }
 
+namespace {
+int check_sizes(const char* fn, const float* scores, int batch, int hkv, int n, int window, void* workspace) {
+  using namespace fkv;
+  if ((!scores && n > 0) || !workspace) return set_error(FKV_ERR_INVALID, std::string(fn) + ": null pointer");
+  if (batch < 0 || hkv < 1 || hkv > kGMaxHeads || n < 0 || window < 0)
+    return set_error(FKV_ERR_INVALID, std::string(fn) + ": bad sizes (Hkv must be 1..16)");
+  if (static_cast<int64_t>(hkv) * n >= 0x7fffffffLL)
+    return set_error(FKV_ERR_INVALID, std::string(fn) + ": Hkv * n too large");
+  return FKV_OK;
+}
+int check_ada(const char* fn, int n, int budget, int window, int floor_k) {
+  using namespace fkv;
+  const int sel = budget - window;
+  if (floor_k < 0 || sel < 0 || sel > n || floor_k > sel)
+    return set_error(FKV_ERR_INVALID, std::string(fn) + ": need 0 <= floor <= budget-window <= n");
+  return FKV_OK;
+}
+}  // namespace
+
+extern "C" int fkv_ada_budgets(const float* scores, int32_t batch, int32_t hkv, int32_t n,
+                               int32_t budget, int32_t window, int32_t floor_k, int32_t* budgets,
+                               void* workspace, void* stream) {
+  using namespace fkv;
+  if (!budgets) return set_error(FKV_ERR_INVALID, "fkv_ada_budgets: null pointer");
+  if (int rc = check_sizes("fkv_ada_budgets", scores, batch, hkv, n, window, workspace)) return rc;
+  if (int rc = check_ada("fkv_ada_budgets", n, budget, window, floor_k)) return rc;
+  return grid_select(scores, batch, hkv, n, budget, window, floor_k, nullptr, 0, budgets, nullptr, nullptr,
+                     workspace, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int fkv_topk_select(const float* scores, const int32_t* budgets, int32_t batch,
+                               int32_t hkv, int32_t n, int32_t window, int64_t* offsets,
+                               int32_t* idx, void* workspace, void* stream) {
+  using namespace fkv;
+  if (!budgets || !offsets || !idx) return set_error(FKV_ERR_INVALID, "fkv_topk_select: null pointer");
+  if (int rc = check_sizes("fkv_topk_select", scores, batch, hkv, n, window, workspace)) return rc;
+  return grid_select(scores, batch, hkv, n, 0, window, 0, budgets, 1, nullptr, offsets, idx, workspace,
+                     static_cast<cudaStream_t>(stream));
+}
+
 extern "C" int fkv_ada_select(const float* scores, int32_t batch, int32_t hkv, int32_t n,
                               int32_t budget, int32_t window, int32_t floor_k, int32_t* budgets,
                               int64_t* offsets, int32_t* idx, void* workspace, void* stream) {
   using namespace fkv;
-  if ((!scores && n > 0) || !budgets || !offsets || !idx || !workspace)
-    return set_error(FKV_ERR_INVALID, "fkv_ada_select: null pointer");
-  if (batch < 0 || hkv < 1 || hkv > kGMaxHeads || n < 0 || window < 0 || floor_k < 0)
-    return set_error(FKV_ERR_INVALID, "fkv_ada_select: bad sizes (Hkv must be 1..16)");
-  const int sel = budget - window;
-  if (sel < 0 || sel > n || floor_k > sel)
-    return set_error(FKV_ERR_INVALID, "fkv_ada_select: need 0 <= floor <= budget-window <= n");
-  if (static_cast<int64_t>(hkv) * n >= 0x7fffffffLL)
-    return set_error(FKV_ERR_INVALID, "fkv_ada_select: Hkv * n too large");
-  if (batch == 0) return FKV_OK;
-  auto st = static_cast<cudaStream_t>(stream);
-  if (n == 0) {  // nothing to rank: every head keeps its window
-    if (int rc = fkv_ada_budgets(scores, batch, hkv, 0, budget, window, floor_k, budgets, stream))
-      return rc;
-    return fkv_topk_select(scores, budgets, batch, hkv, 0, window, offsets, idx, stream);
-  }
-  const int per = gsel_reqs_per_launch(hkv);
-  uint8_t* ws = static_cast<uint8_t*>(workspace);
-  for (int r0 = 0; r0 < batch; r0 += per) {
-    const int reqs = batch - r0 < per ? batch - r0 : per;
-    const int bh = reqs * hkv;
-    GSelParams p{};
-    p.scores = scores + static_cast<int64_t>(r0) * hkv * n;
-    p.hkv = hkv;
-    p.n = n;
-    p.window = window;
-    p.f = floor_k;
-    p.R = hkv * sel - hkv * floor_k;
-    p.budget = budget;
-    p.req0 = r0;
-    p.bh_total = batch * hkv;
-    p.total = static_cast<int64_t>(bh) * n;
-    p.bar = reinterpret_cast<unsigned*>(ws);
-    p.hist = reinterpret_cast<uint32_t*>(ws + 256);
-    p.counts = reinterpret_cast<int2*>(ws + 256 + static_cast<int64_t>(kGBufs) * bh * 512 * 4);
-    p.budgets = budgets + static_cast<int64_t>(r0) * hkv;
-    p.offsets = offsets + static_cast<int64_t>(r0) * hkv;
-    p.idx = idx;
-    // barrier counter + the histogram buffers of passes 0 and 1
-    if (int rc = cuda_check(cudaMemsetAsync(ws, 0, 256 + static_cast<size_t>(2) * bh * 512 * 4, st),
-                            "ada_select workspace reset"))
-      return rc;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(gsel_grid(bh, n), 1, 1);
-    cfg.blockDim = dim3(kGThreads, 1, 1);
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeCooperative;
-    attr[0].val.cooperative = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    if (int rc = cuda_check(cudaLaunchKernelEx(&cfg, grid_select_kernel, p), "ada_select launch"))
-      return rc;
-  }
-  return FKV_OK;
+  if (!budgets || !offsets || !idx) return set_error(FKV_ERR_INVALID, "fkv_ada_select: null pointer");
+  if (int rc = check_sizes("fkv_ada_select", scores, batch, hkv, n, window, workspace)) return rc;
+  if (int rc = check_ada("fkv_ada_select", n, budget, window, floor_k)) return rc;
+  return grid_select(scores, batch, hkv, n, budget, window, floor_k, nullptr, 1, budgets, offsets, idx,
+                     workspace, static_cast<cudaStream_t>(stream));
 }

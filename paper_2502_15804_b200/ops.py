@@ -225,7 +225,15 @@ def ada_floor(budget: int, window: int, alpha: float) -> int:
     return int(math.floor(alpha * (budget - window)))
 
 
-def budgets(scores: torch.Tensor, budget: int, window: int = 32, alpha: float = 0.2) -> torch.Tensor:
+def _select_workspace(bt: int, hkv: int, n: int, dev, workspace: torch.Tensor | None) -> torch.Tensor:
+    need = int(_lib.fkv_ada_select_workspace_bytes(bt, hkv, n))
+    if workspace is None or workspace.numel() * workspace.element_size() < need:
+        workspace = torch.empty(need, dtype=torch.uint8, device=dev)
+    return workspace
+
+
+def budgets(scores: torch.Tensor, budget: int, window: int = 32, alpha: float = 0.2,
+            workspace: torch.Tensor | None = None) -> torch.Tensor:
     """A18: Ada cross-head split of Hkv*budget retained tokens per request.
 
     scores f32 [Bt, Hkv, T-w] (pooled Ada-SnapKV scores) -> int32 [Bt, Hkv],
@@ -235,13 +243,15 @@ def budgets(scores: torch.Tensor, budget: int, window: int = 32, alpha: float = 
         raise NativeError("scores must be contiguous f32 [Bt, Hkv, n]")
     bt, hkv, n = scores.shape
     out = torch.empty((bt, hkv), dtype=torch.int32, device=scores.device)
+    ws = _select_workspace(bt, hkv, n, scores.device, workspace)
     _native.check(_lib.fkv_ada_budgets(scores.data_ptr(), bt, hkv, n, int(budget), int(window),
-                                       ada_floor(budget, window, alpha), out.data_ptr(), _stream()))
+                                       ada_floor(budget, window, alpha), out.data_ptr(), ws.data_ptr(),
+                                       _stream()))
     return out
 
 
 def select(scores: torch.Tensor, head_budgets: torch.Tensor, window: int = 32,
-           total: int | None = None):
+           total: int | None = None, workspace: torch.Tensor | None = None):
     """K2: per-head top-(b_h - w) tokens by (score desc, token asc), ascending,
     then the window tokens.  Returns (offsets int64 [Bt*Hkv+1], idx int32).
     ``total`` = sum of budgets (Hkv*budget*Bt when they come from
@@ -252,8 +262,10 @@ def select(scores: torch.Tensor, head_budgets: torch.Tensor, window: int = 32,
         total = int(head_budgets.sum().item())
     offsets = torch.empty(bt * hkv + 1, dtype=torch.int64, device=scores.device)
     idx = torch.empty(max(total, 1), dtype=torch.int32, device=scores.device)
+    ws = _select_workspace(bt, hkv, n, scores.device, workspace)
     _native.check(_lib.fkv_topk_select(scores.data_ptr(), head_budgets.data_ptr(), bt, hkv, n,
-                                       int(window), offsets.data_ptr(), idx.data_ptr(), _stream()))
+                                       int(window), offsets.data_ptr(), idx.data_ptr(), ws.data_ptr(),
+                                       _stream()))
     return offsets, idx[:total]
 
 
@@ -270,9 +282,7 @@ def ada_select(scores: torch.Tensor, budget: int, window: int = 32, alpha: float
     hb = torch.empty((bt, hkv), dtype=torch.int32, device=dev)
     offsets = torch.empty(bt * hkv + 1, dtype=torch.int64, device=dev)
     idx = torch.empty(max(bt * hkv * budget, 1), dtype=torch.int32, device=dev)
-    need = int(_lib.fkv_ada_select_workspace_bytes(bt, hkv, n))
-    if workspace is None or workspace.numel() * workspace.element_size() < need:
-        workspace = torch.empty(need, dtype=torch.uint8, device=dev)
+    workspace = _select_workspace(bt, hkv, n, dev, workspace)
     _native.check(_lib.fkv_ada_select(scores.data_ptr(), bt, hkv, n, int(budget), int(window),
                                       ada_floor(budget, window, alpha), hb.data_ptr(),
                                       offsets.data_ptr(), idx.data_ptr(), workspace.data_ptr(),

@@ -64,6 +64,27 @@ def test_budgets_and_select_bit_exact(cuda_device, budget):
     np.testing.assert_array_equal(idx, ref_idx)
 
 
+@pytest.mark.parametrize("bt,hkv,n,ties", [(3, 8, 5000, False), (2, 16, 3000, True), (600, 8, 168, False),
+                                           (1, 8, 70000, True), (4, 4, 0, False)])
+def test_topk_select_any_budgets(cuda_device, bt, hkv, n, ties):
+    """K2 with budgets that are not an Ada split (window-only heads, whole-head
+    heads, random sizes): per-head top-k == the oracle's."""
+    from paper_2502_15804_b200 import ops
+    g = torch.Generator().manual_seed(bt + hkv + n)
+    sc = torch.randint(0, 6, (bt, hkv, n), generator=g).float() if ties else torch.rand(bt, hkv, n, generator=g)
+    hb = torch.randint(32, 32 + n + 1, (bt, hkv), generator=g, dtype=torch.int32)
+    hb[0, 0] = 32           # window only
+    hb[-1, -1] = 32 + n     # every token
+    off, idx = ops.select(sc.to(cuda_device), hb.to(cuda_device), 32)
+    torch.cuda.synchronize()
+    ref_off, ref_idx = okv.topk_select(sc.double().numpy(), hb.numpy(), 32)
+    np.testing.assert_array_equal(off.cpu().numpy(), ref_off)
+    np.testing.assert_array_equal(idx.cpu().numpy(), ref_idx)
+    if n:
+        rb = okv.ada_budgets(sc.double().numpy(), 32 + n // 2, 32, 0.2)
+        np.testing.assert_array_equal(ops.budgets(sc.to(cuda_device), 32 + n // 2, 32).cpu().numpy(), rb)
+
+
 def test_select_with_exact_ties(cuda_device):
     """Integer-valued scores: massive exact ties exercise both tie rules."""
     from paper_2502_15804_b200 import ops
