@@ -52,9 +52,6 @@ struct ScoreParams {
   // MODE 4 (score + Ada split + top-k in one launch); workspace parts zeroed per launch
   int budget, floor_k, rest_total;  // B, f = floor(alpha (B - w)), R = Hkv (B - w - f)
   uint32_t* hist;      // [kSelPasses][Bt*Hkv][2][256] per-pass digit histograms, global + floor (zeroed)
-  int32_t* active;     // [kSelPasses + 1] requests still searching, per pass (zeroed)
-  int32_t* need_floor; // [1] heads below their floor anywhere (zeroed)
-  uint64_t* ltau;      // [Bt*Hkv] head-local floor thresholds
   int32_t* counts;     // [Bt*Hkv][n_chunks] int2 (chosen outright, ties at s*) per chunk
   int32_t* budgets;    // out [Bt, Hkv]
   int64_t* offsets;    // out [Bt*Hkv + 1]
@@ -64,7 +61,6 @@ struct ScoreParams {
 constexpr int kSelPasses = 4;            // 32-bit orderable scores, 8-bit digits (ties resolved by count)
 constexpr int kSelMaxKeys = kStages * kTileBytes / 4;  // pooled f32 keys staged in the (idle) K ring
 constexpr int kSelMaxHeads = 8;
-constexpr uint64_t kNoKey = ~0ull;
 
 // ------------------------------------------------------------ tcgen05 ----
 __device__ __forceinline__ void tc_fence_before() {
@@ -241,10 +237,6 @@ __device__ __forceinline__ uint32_t orderable(float f) {
   const uint32_t u = __float_as_uint(f);
   return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
-// (score desc, index asc) as one unsigned order (select.cu uses the same key)
-__device__ __forceinline__ uint64_t compose(float sc, uint32_t index) {
-  return (static_cast<uint64_t>(orderable(sc)) << 32) | (0xffffffffu - index);
-}
 
 // Scratch of the selection phase, placed in the (idle) Q_win region.
 struct SelScratch {
@@ -318,34 +310,6 @@ __device__ __forceinline__ void epi_histogram2(const float* sp, int nk, bool ga,
   epi_sync();
 }
 
-// CTA-local (epilogue warps) threshold such that exactly k keys are >= it.
-template <class KeyOf>
-__device__ uint64_t epi_select_kth(KeyOf key_of, int nk, int k, SelScratch& x) {
-  uint64_t prefix = 0, mask = 0;
-  int need = k;
-  for (int shift = 56; shift >= 0; shift -= 8) {
-    epi_histogram(key_of, nk, prefix, mask, shift, x.hist);
-    const int32_t sfx = epi_suffix_sum(static_cast<int32_t>(x.hist[threadIdx.x]), x);
-    const int32_t cnt = epi_count(sfx >= need, x);  // suffix is non-increasing in d
-    const int d = cnt - 1;
-    if (static_cast<int>(threadIdx.x) == d) {
-      x.dstar = d;
-      x.exact = sfx == need;
-      x.warp_tot[0] = sfx - static_cast<int32_t>(x.hist[d]);  // strictly above the bucket
-    }
-    epi_sync();
-    const int dd = x.dstar;
-    const bool exact = x.exact != 0;
-    need -= x.warp_tot[0];
-    prefix |= static_cast<uint64_t>(dd) << shift;
-    mask |= 255ull << shift;
-    epi_sync();
-    if (exact) break;
-  }
-  return prefix;
-}
-
-// ---------------------------------------------------------------------------
 // MODE 4, after pooling: Ada budget split + per-head top-k, grid-wide.  Same
 // result as select.cu's grid_select_kernel (the standalone launch over
 // pooled scores in HBM), here fused behind the scoring passes.
@@ -988,7 +952,7 @@ namespace fkv {
 namespace {
 struct ScoreLayout {
   int chunks, tiles_per_chunk, bh;
-  int64_t stats, raw, gridbar, hist, active, ltau, counts, sel, total;
+  int64_t stats, raw, gridbar, hist, counts, sel, total;
 };
 
 ScoreLayout score_layout(int batch, int hkv, int T, int window, int group) {
@@ -1004,9 +968,7 @@ ScoreLayout score_layout(int batch, int hkv, int T, int window, int group) {
   L.raw = a16(L.stats + static_cast<int64_t>(L.bh) * L.chunks * gw * 2 * 4);
   L.gridbar = a16(L.raw + static_cast<int64_t>(L.bh) * (T - window) * 4);
   L.hist = a16(L.gridbar + 64);
-  L.active = a16(L.hist + static_cast<int64_t>(kSelPasses) * L.bh * 512 * 4);
-  L.ltau = a16(L.active + (kSelPasses + 2) * 4);
-  L.counts = a16(L.ltau + static_cast<int64_t>(L.bh) * 8);
+  L.counts = a16(L.hist + static_cast<int64_t>(kSelPasses) * L.bh * 512 * 4);
   L.sel = a16(L.counts + static_cast<int64_t>(L.bh) * L.chunks * 8);
   L.total = a16(L.sel + fkv_ada_select_workspace_bytes(batch, hkv, T - window));
   return L;
@@ -1051,9 +1013,6 @@ int score_common(const void* q_win, const void* k, int32_t batch, int32_t hq, in
   p.pool_r = pool_k / 2;
   p.gridbar = reinterpret_cast<GridBar*>(ws + L.gridbar);
   p.hist = reinterpret_cast<uint32_t*>(ws + L.hist);
-  p.active = reinterpret_cast<int32_t*>(ws + L.active);
-  p.need_floor = p.active + kSelPasses + 1;
-  p.ltau = reinterpret_cast<uint64_t*>(ws + L.ltau);
   p.counts = reinterpret_cast<int32_t*>(ws + L.counts);
   return FKV_OK;
 }
@@ -1121,8 +1080,8 @@ extern "C" int fkv_snapkv_select(const void* q_win, const void* k, int32_t batch
   p.budgets = budgets;
   p.offsets = offsets;
   p.idx = idx;
-  // zero the per-pass histograms, pass counters and the floor flag (one contiguous range)
-  if (int rc = cuda_check(cudaMemsetAsync(p.hist, 0, L.ltau - L.hist, st), "select workspace reset"))
+  // zero the per-pass histograms
+  if (int rc = cuda_check(cudaMemsetAsync(p.hist, 0, L.counts - L.hist, st), "select workspace reset"))
     return rc;
   return p.group * window == 128 ? launch_score<128>(tq, tk, p, L.bh, 4, st)
                                  : launch_score<256>(tq, tk, p, L.bh, 4, st);
