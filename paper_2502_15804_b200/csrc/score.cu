@@ -895,7 +895,20 @@ int score_chunks(int bh, int n_tiles) {
       sms = 148;
   }
   int c = sms / bh;
-  if (c < 1) c = 1;
+  if (c < 1) {
+    // more heads than SMs (the multi-launch path, one CTA per SM at a time):
+    // the fewest chunks per head whose CTAs fill the last wave to >= 90 %,
+    // keeping >= 16 tiles per chunk
+    c = 1;
+    for (int t = 1; t <= 8 && n_tiles / t >= 16; ++t) {
+      const long long ctas = static_cast<long long>(bh) * t;
+      const long long waves = (ctas + sms - 1) / sms;
+      if (ctas * 10 >= waves * sms * 9) {
+        c = t;
+        break;
+      }
+    }
+  }
   return c > n_tiles ? n_tiles : c;
 }
 
