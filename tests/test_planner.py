@@ -298,3 +298,34 @@ def test_calibration_roundtrip():
         assert x == pytest.approx(y, rel=1e-6)
     with pytest.raises(fk.CalibrationError, match="at least 4"):
         fk.calibrate(s[:3])
+
+
+def test_live_reference_solvers_random():
+    """Randomised B1 parity against the live reference kernel (pattern of the
+    reference's test_kernel_backends.py:42-77): canonical copy lists of random
+    schemes, with and without a hint, tight and loose cutoffs -- identical
+    (spread, rgs) and node counts from both solvers."""
+    hb = reference_headbalance()
+    if hb is None:
+        pytest.skip("reference package not available here")
+    from headbalance._kernel import reference as ref_kernel
+    rng = random.Random(4242)
+    checked = 0
+    for _ in range(120):
+        tp = rng.choice([2, 3, 4])
+        n = rng.randint(tp, 9)
+        r = [rng.choice([1, 1, 2]) if tp > 1 else 1 for _ in range(n)]
+        copies = sorted(((rng.uniform(0.5, 50.0) / ri, h) for h in range(n) for ri in [r[h]] for _ in range(ri)),
+                        key=lambda x: (-x[0], x[1]))
+        w = [c[0] for c in copies]
+        heads = [c[1] for c in copies]
+        free = rng.random() < 0.4
+        if not free and len(w) % tp:
+            continue
+        cutoff = rng.choice([math.inf, 1e9, sum(w) / tp * 0.2])
+        budget = rng.choice([50, 2000, 200000])
+        ours = (native.solve_free_split if free else native.solve_equal_split)(w, heads, tp, cutoff, budget)
+        theirs = (ref_kernel.solve_free_split if free else ref_kernel.solve_equal_split)(w, heads, tp, cutoff, budget)
+        assert _res(ours[0]) == _res(theirs[0]) and ours[1] == theirs[1], (w, heads, tp, cutoff, budget, free)
+        checked += 1
+    assert checked > 60
