@@ -111,8 +111,40 @@ def _cut_stream_cost(seg_len, tiles, C: int, P: int, cap: int):
 PIECE_COST_TILES = 48  # coop schedule: one piece's cost in tile-equivalents (plateau >= 32, probe_sched)
 
 
+PAIR_PIECE_TILES = 12  # SM pairing: measured per-piece cost (~2.4 us vs ~0.21 us per tile per CTA)
+
+
+def _pair_on_sms(owner, t0s, t1s, sms: int):
+    """Relabel workers so that the two CTAs sharing an SM (CTA j and j + sms:
+    the block scheduler places a fresh grid round robin over the SMs, second
+    slots in the same order) carry similar work.  The per-CTA cut equalises
+    tiles + P x pieces, so tile counts vary inversely with piece counts; two
+    piece-heavy CTAs on one SM would leave it idle early while another SM
+    streams two tile-heavy ones.  Heaviest CTAs (by tiles) get an SM to
+    themselves when the grid has fewer than 2 x sms CTAs; the rest are paired
+    heaviest with lightest."""
+    owner = np.asarray(owner, dtype=np.int64)
+    busy = int(owner.max()) + 1 if len(owner) else 0
+    k = busy - sms  # number of SMs running two CTAs
+    if k <= 0:
+        return owner
+    import os
+    pw = float(os.environ.get("FKV_PAIR_PIECE", PAIR_PIECE_TILES))
+    w_tiles = np.bincount(owner, weights=(np.asarray(t1s) - np.asarray(t0s) + TILE - 1) // TILE + pw,
+                          minlength=busy)
+    order = np.argsort(-w_tiles, kind="stable")
+    new_id = np.empty(busy, dtype=np.int64)
+    solo, paired = order[:sms - k], order[sms - k:]
+    new_id[solo] = np.arange(k, sms)
+    for j in range(k):  # heaviest remaining with lightest remaining
+        new_id[paired[j]] = j
+        new_id[paired[2 * k - 1 - j]] = j + sms
+    return new_id[owner]
+
+
 def plan_work(seg_len, n_workers: int, chunk: int | None = None,
-              min_tiles: int = MIN_TILES_PER_WORKER, piece_cost: int | None = None):
+              min_tiles: int = MIN_TILES_PER_WORKER, piece_cost: int | None = None,
+              sms: int | None = None):
     """Static decode schedule for the warp-persistent K4 kernel.
 
     Default: the segments' 16-token tiles are laid end to end and the stream
@@ -199,13 +231,16 @@ def plan_work(seg_len, n_workers: int, chunk: int | None = None,
             if w >= W:
                 raise ValueError(f"{len(lens)} pieces exceed one launch "
                                  f"({W} workers x {MAX_WORK_PER_WORKER} pieces)")
+    import os
+    if sms and os.environ.get("FKV_SM_PAIRING", "1") == "1":
+        owner = _pair_on_sms(owner, t0s, t1s, int(sms))
     item_seg = np.asarray(seg_i, dtype=np.int32)
     t0 = np.asarray(t0s, dtype=np.int32)
     t1 = np.asarray(t1s, dtype=np.int32)
     owner = np.asarray(owner, dtype=np.int64)
     seg_item_ptr = np.zeros(n_seg + 1, dtype=np.int32)
     seg_item_ptr[1:] = np.cumsum(np.bincount(item_seg, minlength=n_seg))
-    busy = int(owner.max()) + 1 if len(owner) else 1  # owners are 0..busy-1, non-decreasing
+    busy = int(owner.max()) + 1 if len(owner) else 1  # owners are 0..busy-1
     warp_ptr = np.zeros(busy + 1, dtype=np.int32)
     warp_ptr[1:] = np.cumsum(np.bincount(owner, minlength=busy))
     # Within a worker, pieces of split segments go first: their LSE merges
@@ -373,7 +408,9 @@ def plan_schedule(seg_len, seg_row0, seg_qrow, seg_out_row, device=None, chunk: 
     # piece; otherwise 4-warp CTAs, two per SM (tools/probe_sched.py)
     wide = mode == "wide" or (mode != "coop" and n_seg <= WIDE_MAX_SEGMENTS and mean >= 8)
     flags = FKV_DECODE_WIDE if wide else 0
-    plan = plan_work(seg_len, default_workers(device, flags), chunk)
+    workers = default_workers(device, flags)
+    ctas_sm = max(1, workers // default_workers(device, FKV_DECODE_WIDE))
+    plan = plan_work(seg_len, workers, chunk, sms=workers // ctas_sm if ctas_sm > 1 else None)
     tab = work_table(seg_row0, seg_len, seg_qrow, seg_out_row, *plan)
     return (*plan, tab, flags)
 

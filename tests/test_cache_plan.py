@@ -166,3 +166,24 @@ def test_solo_work_table_tags_warps():
             assert (e[7] & 0xffff) == sptr[item_seg[it] + 1] - sptr[item_seg[it]]
             seen.append(it)
     assert sorted(seen) == list(range(len(item_seg)))
+
+
+def test_sm_pairing_is_a_permutation_that_balances_sms():
+    """_pair_on_sms relabels workers (every piece kept, ids 0..busy-1) so the
+    two CTAs sharing an SM (j, j + sms) carry similar work."""
+    from paper_2502_15804_b200.cache import plan_work
+    rng = np.random.default_rng(3)
+    seg = rng.integers(200, 2000, 512)
+    a = plan_work(seg, 296)
+    b = plan_work(seg, 296, sms=148)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2])
+    assert len(b[4]) == len(a[4])
+    def per_worker_tiles(plan):
+        item_seg, t0, t1, _, wp, wl = plan
+        return np.array([((t1[wl[wp[w]:wp[w + 1]]] - t0[wl[wp[w]:wp[w + 1]]] + 15) // 16).sum()
+                         for w in range(len(wp) - 1)])
+    ta, tb = per_worker_tiles(a), per_worker_tiles(b)
+    assert sorted(ta) == sorted(tb)
+    sm_a = ta[:148] + np.append(ta[148:], np.zeros(296 - len(ta)))[:148]
+    sm_b = tb[:148] + np.append(tb[148:], np.zeros(296 - len(tb)))[:148]
+    assert sm_b.max() - sm_b.min() <= sm_a.max() - sm_a.min()

@@ -68,3 +68,22 @@ for tp in (1, 8):
     late = np.argsort(-st[:, 5])[:5]
     for c in late:
         print("   late CTA", c, np.round(st[c], 2).tolist())
+    # per-CTA cost model: exit time vs (tiles, pieces, split pieces); per-SM totals
+    tiles = ((np.maximum(wk[:, :, 2], 0) + 15) // 16).sum(1)
+    A = np.stack([tiles, npieces, nsplit, np.ones(n)], 1).astype(float)
+    ex = st[:, 5]
+    ok = ~np.isnan(ex)
+    coef, *_ = np.linalg.lstsq(A[ok], ex[ok], rcond=None)
+    print(f"   exit ~ {coef[0]*1e3:.1f} ns/tile + {coef[1]:.2f} us/piece + {coef[2]:.2f} us/split + {coef[3]:.2f}"
+          f"  (resid rms {np.sqrt(np.mean((A[ok] @ coef - ex[ok])**2)):.2f} us)")
+    sm_t = {}
+    for c in range(n):
+        sm_t.setdefault(int(smid[c]), []).append((tiles[c], ex[c]))
+    tot = np.array([sum(t for t, _ in v) for v in sm_t.values()])
+    last = np.array([max(e for _, e in v) for v in sm_t.values()])
+    print(f"   per-SM tiles min/mean/max {tot.min()}/{tot.mean():.1f}/{tot.max()}  per-SM last exit p0/p50/max "
+          f"{np.percentile(last,0):.1f}/{np.percentile(last,50):.1f}/{last.max():.1f}")
+    print(f"   corr(per-SM tiles, last exit) = {np.corrcoef(tot, last)[0,1]:.2f}")
+    if n > 148:
+        same = np.mean([smid[i] == smid[i + 148] for i in range(n - 148)])
+        print(f"   CTA i and i+148 on the same SM: {same:.2f};  smid[:8] {smid[:8].astype(int).tolist()} smid[148:156] {smid[148:156].astype(int).tolist()}")
