@@ -8,6 +8,8 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv \
 ncu --set full --clock-control none --import-source on -k regex:decode_kernel -s 85 -c 1 \
     -o gpurun_out/prof_k4 python bench.py --steps 1 --warmup 1 --no-emulate --no-cpu \
     > gpurun_out/ncu_k4.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:"score_kernel|ada_select|compact_kernel|pool_kernel" -c 6 \
+ncu --set full --clock-control none --import-source on -k regex:"score_kernel|compact_kernel|pool_kernel" -c 6 \
     -o gpurun_out/prof_prefill python tools/probe_one_prefill.py > gpurun_out/ncu_prefill.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:grid_select -c 2 \
+    -o gpurun_out/prof_select python tools/probe_one_select.py > gpurun_out/ncu_select.log 2>&1
 ls -la gpurun_out
