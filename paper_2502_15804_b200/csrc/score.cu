@@ -246,7 +246,7 @@ struct SelScratch {
   int32_t warp_tot[kEpiWarps];
   int32_t dstar, exact;
   uint32_t fprefix, fmask;  // floor search of this CTA's head
-  int32_t fexact, fabove, f_at, f_next;
+  int32_t fexact, fabove;
 };
 
 // Inclusive suffix sum over d of one value per epilogue thread (d = tid).
@@ -291,6 +291,33 @@ __device__ __forceinline__ void epi_histogram(KeyOf key_of, int nk, uint64_t pre
     if (ok && lane == __ffs(peers) - 1) atomicAdd(&hist[d], __popc(peers));
   }
   epi_sync();
+}
+
+// Suffix counts of one global 256-bin histogram by one warp (8 bins per
+// lane): s[j] = base + #keys in bins >= 8*lane + j; `up` = the count past the
+// lane's last bin (base past bin 255).
+__device__ __forceinline__ void warp_suffix8(const uint32_t* gh, int base, int (&s)[8], int& up) {
+  const int lane = threadIdx.x & 31;
+  const uint4 x0 = __ldcg(reinterpret_cast<const uint4*>(gh + 8 * lane));
+  const uint4 x1 = __ldcg(reinterpret_cast<const uint4*>(gh + 8 * lane + 4));
+  const uint32_t h[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+  int run = 0;
+#pragma unroll
+  for (int j = 7; j >= 0; --j) {
+    run += static_cast<int>(h[j]);
+    s[j] = run;
+  }
+  int incl = run;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int v = __shfl_down_sync(0xffffffffu, incl, off);
+    if (lane + off < 32) incl += v;
+  }
+  const int higher = incl - run + base;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) s[j] += higher;
+  up = __shfl_down_sync(0xffffffffu, s[0], 1);
+  if (lane == 31) up = base;
 }
 
 // Digit histograms of the pooled keys for the global search (keys matching
@@ -361,56 +388,43 @@ __device__ void select_phase(const ScoreParams& p, Smem& sm, int b, int h, int b
     sstamp(2 + 2 * pass);
     epi_grid_sync(p.gridbar);  // fixed pass count: uniform across the grid
     sstamp(3 + 2 * pass);
-    if (fa) {  // my head's floor search: d* = max{d : S(d) >= f}
-      const int32_t v = static_cast<int32_t>(__ldcg(gh + 256 + tid));
-      const int32_t sfx = epi_suffix_sum(v, x) + x.fabove;
-      const int32_t cnt = epi_count(sfx >= f, x);
-      if (tid == cnt - 1) {
-        x.f_at = sfx;
-        x.f_next = sfx - v;
-      }
-      epi_sync();
-      if (tid == 0) {
-        x.fprefix |= static_cast<uint32_t>(cnt - 1) << shift;
-        x.fmask |= 255u << shift;
-        x.fabove = x.f_next;
-        x.fexact = x.f_at == f;
-      }
+    // decisions, one warp per histogram (8 bins per lane, no block-wide
+    // scans): warp w -> suffix counts of head w's global histogram; warp 0
+    // also runs my head's floor search (its floor histogram is the global one
+    // while the two searches share a prefix)
+    const uint32_t* gq = p.hist + (static_cast<int64_t>(pass) * BH + b * HK) * 512;
+    if (!exact && wid < HK) {
+      int sv[8], up;
+      warp_suffix8(gq + wid * 512, x.above[wid], sv, up);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) x.suf[wid][8 * lane + j] = sv[j];
     }
-    if (exact) {
-      epi_sync();
-      continue;
-    }
-    // suffix counts of every head of this request (all heads' histograms
-    // loaded at once, one L2 round trip), then d* = max{d : G(d) >= R}
-    {
-      const uint32_t* gq = p.hist + (static_cast<int64_t>(pass) * BH + b * HK) * 512 + tid;
-      int32_t v[kSelMaxHeads];
+    if (fa && wid == 0) {  // my head's floor search: d* = max{d : S(d) >= f}
+      int sv[8], up;
+      warp_suffix8(same ? gh : gh + 256, x.fabove, sv, up);
+      int c = 0;
 #pragma unroll
-      for (int hh = 0; hh < kSelMaxHeads; ++hh) v[hh] = hh < HK ? static_cast<int32_t>(__ldcg(gq + hh * 512)) : 0;
+      for (int j = 0; j < 8; ++j) c += sv[j] >= f;
+      const int ds = __reduce_add_sync(0xffffffffu, c) - 1;
+      int at = 0, nxt = 0;
 #pragma unroll
-      for (int off = 1; off < 32; off <<= 1)
-#pragma unroll
-        for (int hh = 0; hh < kSelMaxHeads; ++hh) {
-          const int32_t y = __shfl_down_sync(0xffffffffu, v[hh], off);
-          if (lane + off < 32) v[hh] += y;
+      for (int j = 0; j < 8; ++j)
+        if (8 * lane + j == ds) {
+          at = sv[j];
+          nxt = j < 7 ? sv[j + 1] : up;
         }
-      if (lane == 0)
-#pragma unroll
-        for (int hh = 0; hh < kSelMaxHeads; ++hh) x.suf[hh][wid] = v[hh];  // warp totals (scratch)
-      epi_sync();
-      int32_t add[kSelMaxHeads];
-#pragma unroll
-      for (int hh = 0; hh < kSelMaxHeads; ++hh) {
-        add[hh] = x.above[hh];
-        for (int j = wid + 1; j < kEpiWarps; ++j) add[hh] += x.suf[hh][j];
+      at = __shfl_sync(0xffffffffu, at, ds >> 3);
+      nxt = __shfl_sync(0xffffffffu, nxt, ds >> 3);
+      if (lane == 0) {
+        x.fprefix |= static_cast<uint32_t>(ds) << shift;
+        x.fmask |= 255u << shift;
+        x.fabove = nxt;
+        x.fexact = at == f;
       }
-      epi_sync();
-#pragma unroll
-      for (int hh = 0; hh < kSelMaxHeads; ++hh)
-        if (hh < HK) x.suf[hh][tid] = v[hh] + add[hh];
     }
     epi_sync();
+    sstamp(12 + 3 * pass);
+    if (exact) continue;
     int32_t gd = 0;
     for (int hh = 0; hh < HK; ++hh) gd += max(0, x.suf[hh][tid] - f);
     const int32_t cnt = epi_count(gd >= R, x);
@@ -429,6 +443,7 @@ __device__ void select_phase(const ScoreParams& p, Smem& sm, int b, int h, int b
     prefix |= static_cast<uint32_t>(dstar) << shift;
     mask |= 255u << shift;
     epi_sync();
+    sstamp(13 + 3 * pass);
   }
   sstamp(30);
   const bool have_tau = R > 0;

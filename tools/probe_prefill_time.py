@@ -24,6 +24,7 @@ for (bt, hq, hkv, T, B) in [(1, 32, 8, 16384, 256), (1, 64, 8, 32768, 1024), (1,
     t0 = st[0]
     names = {0: "start", 40: "pre-stats-bar", 41: "post-stats-bar", 42: "pre-raw-bar", 43: "post-raw-bar", 1: "select-start",
              30: "search-done", 31: "pre-count-bar", 32: "post-count-bar", 33: "written"}
-    for p in range(9):
+    for p in range(4):
         names[2 + 2 * p] = f"pass{p}-pre-bar"; names[3 + 2 * p] = f"pass{p}-post-bar"
+        names[12 + 3 * p] = f"p{p}-floor-done"; names[13 + 3 * p] = f"p{p}-global-done"
     print(f"T={T} B={B}:", ", ".join(f"{names[i]} {(st[i]-t0)/1e3:.1f}" for i in sorted(names) if st[i] >= t0 and st[i] - t0 < 1e7))
