@@ -831,12 +831,36 @@ __global__ void __launch_bounds__(kThreads, 1)
       // MODE 4 stages this CTA's pooled scores in the K ring (idle: every tile
       // was consumed before the epilogue reached the barrier above)
       float* sp = reinterpret_cast<float*>(&sm.k[0][0][0][0]);
-      for (int t = t_beg + threadIdx.x; t < t_end; t += 32 * kEpiWarps) {
-        float mx = __ldcg(rr + t);
-        const int lo = max(0, t - p.pool_r), hi = min(n - 1, t + p.pool_r);
-        for (int u = lo; u <= hi; ++u) mx = fmaxf(mx, __ldcg(rr + u));
-        out[t] = mx;
-        if (MODE == 4) sp[t - t_beg] = mx;
+      if (p.pool_r == 3) {  // the default 7-wide pool: 4 keys x 7 taps in flight per thread
+        constexpr int kU = 4, kE = 32 * kEpiWarps;
+        for (int t0 = t_beg + threadIdx.x; t0 < t_end; t0 += kU * kE) {
+          float w[kU][7];
+#pragma unroll
+          for (int u = 0; u < kU; ++u)
+#pragma unroll
+            for (int j = 0; j < 7; ++j) {
+              const int t = t0 + u * kE, xj = t + j - 3;
+              w[u][j] = t < t_end && xj >= 0 && xj < n ? __ldcg(rr + xj) : -CUDART_INF_F;
+            }
+#pragma unroll
+          for (int u = 0; u < kU; ++u) {
+            const int t = t0 + u * kE;
+            if (t >= t_end) break;
+            float mx = w[u][0];
+#pragma unroll
+            for (int j = 1; j < 7; ++j) mx = fmaxf(mx, w[u][j]);
+            out[t] = mx;
+            if (MODE == 4) sp[t - t_beg] = mx;
+          }
+        }
+      } else {
+        for (int t = t_beg + threadIdx.x; t < t_end; t += 32 * kEpiWarps) {
+          float mx = __ldcg(rr + t);
+          const int lo = max(0, t - p.pool_r), hi = min(n - 1, t + p.pool_r);
+          for (int u = lo; u <= hi; ++u) mx = fmaxf(mx, __ldcg(rr + u));
+          out[t] = mx;
+          if (MODE == 4) sp[t - t_beg] = mx;
+        }
       }
       if (MODE == 4) select_phase(p, sm, b, h, bh, chunk, n, t_beg, max(t_end - t_beg, 0), sp);
     }
