@@ -955,7 +955,7 @@ namespace {
 
 template <int GW>
 int launch_score(const CUtensorMap& tq, const CUtensorMap& tk, const ScoreParams& p, int batch_heads,
-                 int mode, cudaStream_t st) {
+                 int mode, cudaStream_t st, size_t reset_bytes = sizeof(GridBar)) {
   const size_t smem = sizeof(ScoreSmem<GW>) + 1024;
   static bool configured = false;
   if (!configured) {
@@ -970,7 +970,8 @@ int launch_score(const CUtensorMap& tq, const CUtensorMap& tk, const ScoreParams
   if (mode >= 3) {
     // one cooperative launch: both passes and the pooling (grid <= #SMs, 1 CTA/SM)
     // [+ MODE 4: the Ada split and top-k selection]
-    if (int rc = cuda_check(cudaMemsetAsync(p.gridbar, 0, sizeof(GridBar), st), "gridbar reset"))
+    // grid barrier counter (+ MODE 4: the per-pass histograms right after it)
+    if (int rc = cuda_check(cudaMemsetAsync(p.gridbar, 0, reset_bytes, st), "gridbar reset"))
       return rc;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
@@ -1132,9 +1133,8 @@ extern "C" int fkv_snapkv_select(const void* q_win, const void* k, int32_t batch
   p.budgets = budgets;
   p.offsets = offsets;
   p.idx = idx;
-  // zero the per-pass histograms
-  if (int rc = cuda_check(cudaMemsetAsync(p.hist, 0, L.counts - L.hist, st), "select workspace reset"))
-    return rc;
-  return p.group * window == 128 ? launch_score<128>(tq, tk, p, L.bh, 4, st)
-                                 : launch_score<256>(tq, tk, p, L.bh, 4, st);
+  // the barrier counter and the per-pass histograms are one contiguous range
+  const size_t reset = static_cast<size_t>(L.counts - L.gridbar);
+  return p.group * window == 128 ? launch_score<128>(tq, tk, p, L.bh, 4, st, reset)
+                                 : launch_score<256>(tq, tk, p, L.bh, 4, st, reset);
 }
