@@ -813,6 +813,8 @@ def prefill_compress(peaks):
     from paper_2502_15804_b200 import ops
     dev = torch.device("cuda")
     rows = {}
+    mufu_path = ROOT / "profiles" / "mufu_peak.json"
+    mufu_rate = json.loads(mufu_path.read_text())["ex2_per_s"] if mufu_path.exists() else 4.62e12
     for name, (bt, hq, hkv, T, B) in {"llama-3.1-8b_T16k_B256": (1, 32, 8, 16384, 256),
                                      "llama-3.1-8b_T16k_B256_batch4": (4, 32, 8, 16384, 256),
                                      "llama-3.1-8b_T16k_B256_batch32": (32, 32, 8, 16384, 256),
@@ -853,6 +855,7 @@ def prefill_compress(peaks):
                   "score_select_us": graph_us(lambda: ops.score_select(q, k, B, w, workspace=ws)),
                   "compact_us": graph_us(lambda: ops.compact_into(cache, k, v, off, idx, sbh, slo, shi, mx))}
         flops = 2 * 2.0 * bt * hq * w * T * HEAD_DIM  # two passes of Q_win.K^T
+        exps = 2.0 * bt * hq * w * T  # one ex2 per score per pass (MUFU)
         kbytes = bt * hkv * T * HEAD_DIM * 2
         tf_peak = float(peaks.get("bf16_tflops", 1590.0))
         rows[name] = {
@@ -864,6 +867,10 @@ def prefill_compress(peaks):
             "score_K_read_GBs_per_pass": kbytes / (t_score / 2) / 1e9,
             "roofline_us": max(flops / (tf_peak * 1e12), 2 * kbytes / (float(peaks.get("hbm_gbs", 6650.0)) * 1e9)) * 1e6,
             "graph_replay": dev_us,
+            # K1 is bound by the special-function unit, not the tensor cores:
+            # two exponentials per (query row, key), at the measured ex2 rate
+            "mufu_bound_us": exps / mufu_rate * 1e6,
+            "score_mufu_frac": exps / mufu_rate / (dev_us["score_us"] * 1e-6),
         }
     return rows
 
