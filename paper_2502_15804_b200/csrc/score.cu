@@ -45,7 +45,7 @@ struct ScoreParams {
   int q_rows_per_req;  // Hq * w
   float scale_log2;    // log2(e) / sqrt(d)
   float* stats;        // [Bt*Hkv, n_chunks, GW, 2] (max, sum) in log2 units
-  float* raw;          // [Bt*Hkv, T - w]
+  float* raw;          // [2 row halves][Bt*Hkv, T - w] partial column sums
   float* scores;       // pooled output (fused mode)
   int pool_r;          // pooling radius (pool_k / 2)
   struct GridBar* gridbar;  // fused mode: zeroed counter + generation
@@ -121,6 +121,12 @@ __device__ __forceinline__ void tmem_wait_ld(uint32_t (&a)[32], uint32_t (&b)[32
   for (int i = 0; i < 32; ++i) asm volatile("" : "+r"(a[i]), "+r"(b[i]));
 }
 
+__device__ __forceinline__ void tmem_wait_ld(uint32_t (&a)[32]) {
+  tmem_wait_ld();
+#pragma unroll
+  for (int i = 0; i < 32; ++i) asm volatile("" : "+r"(a[i]));
+}
+
 // 32 consecutive fp32 TMEM columns of this thread's lane.
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   uint32_t r[32];
@@ -192,7 +198,6 @@ struct __align__(1024) ScoreSmem {
   uint64_t full[kStages], empty[kStages], tfull[2], tempty[2], qbar;
   uint32_t tmem_base;
   alignas(16) float bias[GW];  // pass 2: per query row, m_r + log2(G * l_r) (log2 units)
-  float red[2][2][kBN];      // pass 2: [tile parity][column half][key] partial sums
   float ml[kBN][2];          // pass 1, GW=128: second column half's (max, sum) per row
 };
 
@@ -727,6 +732,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_ld32_nw(tmem + lane_base + buf * GW + mh * kBN + cb * 32, ra);
           tmem_ld32_nw(tmem + lane_base + buf * GW + mh * kBN + (cb + 1) * 32, rb);
           tmem_wait_ld(ra, rb);
+          if (cb + 2 >= cb1) {  // the tile's last columns are in registers: hand the
+            tc_fence_before();  // TMEM buffer back to the MMA warp before the math
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sm.tempty[buf]);
+          }
           float v[64];
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(ra[i]), v[32 + i] = __uint_as_float(rb[i]);
@@ -757,9 +767,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           l = l * fast_exp2((m - nm) * p.scale_log2) + ((e0 + e1) + (e2 + e3));
           m = nm;
         }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.tempty[buf]);
       }
       m = m == -CUDART_INF_F ? m : m * p.scale_log2;  // to log2 units
       if (MH == 1) {
@@ -796,36 +803,54 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int it = n1 + i2, buf = it & 1;
         mbar_wait(&sm.tfull[buf], (it >> 1) & 1);
         tc_fence_after();
+        constexpr int NC = GW / 64;  // 32-column chunks of this warp's row half
         float acc = 0.f;
-#pragma unroll 1
-        for (int cb = half * (GW / 64); cb < (half + 1) * (GW / 64); ++cb) {
-          float v[32];
-          tmem_ld32(tmem + lane_base + buf * GW + cb * 32, v);
-          const float4* b4 = reinterpret_cast<const float4*>(sm.bias + cb * 32);
+        auto chunk_sum = [&](const uint32_t (&r)[32], int c) {
+          const float4* b4 = reinterpret_cast<const float4*>(sm.bias + (half * NC + c) * 32);
 #pragma unroll
           for (int i = 0; i < 32; i += 4) {
             const float4 bb = b4[i / 4];  // broadcast: every lane reads the same columns
-            acc += fast_exp2(fmaf(v[i], p.scale_log2, -bb.x));
-            acc += fast_exp2(fmaf(v[i + 1], p.scale_log2, -bb.y));
-            acc += fast_exp2(fmaf(v[i + 2], p.scale_log2, -bb.z));
-            acc += fast_exp2(fmaf(v[i + 3], p.scale_log2, -bb.w));
+            acc += fast_exp2(fmaf(__uint_as_float(r[i]), p.scale_log2, -bb.x));
+            acc += fast_exp2(fmaf(__uint_as_float(r[i + 1]), p.scale_log2, -bb.y));
+            acc += fast_exp2(fmaf(__uint_as_float(r[i + 2]), p.scale_log2, -bb.z));
+            acc += fast_exp2(fmaf(__uint_as_float(r[i + 3]), p.scale_log2, -bb.w));
           }
+        };
+        if constexpr (NC == 2) {
+          // both chunks in registers, the buffer back to the MMA warp, then the math
+          uint32_t ra[32], rb[32];
+          tmem_ld32_nw(tmem + lane_base + buf * GW + (half * NC) * 32, ra);
+          tmem_ld32_nw(tmem + lane_base + buf * GW + (half * NC + 1) * 32, rb);
+          tmem_wait_ld(ra, rb);
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&sm.tempty[buf]);
+          chunk_sum(ra, 0);
+          chunk_sum(rb, 1);
+        } else {
+          // GW = 256: four chunks would cost 128 registers; one at a time
+#pragma unroll 1
+          for (int c = 0; c < NC; ++c) {
+            uint32_t ra[32];
+            tmem_ld32_nw(tmem + lane_base + buf * GW + (half * NC + c) * 32, ra);
+            tmem_wait_ld(ra);
+            chunk_sum(ra, c);
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&sm.tempty[buf]);
         }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.tempty[buf]);
-        sm.red[it & 1][half][key] = acc;
-        asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps));
+        // this row half's partial column sum; the pooling adds the two halves
         const int t = (a2 + i2) * kBN + key;
-        if (half == 0 && t < n)
-          p.raw[static_cast<int64_t>(bh) * n + t] = acc + sm.red[it & 1][1][key];
+        if (t < n) p.raw[(static_cast<int64_t>(half) * gridDim.y + bh) * n + t] = acc;
       }
     }
     if (kFused) {
       sstamp(42);
       epi_grid_sync(p.gridbar);  // every raw column score is in global memory
       sstamp(43);
-      const float* rr = p.raw + static_cast<int64_t>(bh) * n;
+      const float* rr = p.raw + static_cast<int64_t>(bh) * n;                 // row half 0
+      const float* rr1 = p.raw + (static_cast<int64_t>(gridDim.y) + bh) * n;  // row half 1
       float* out = p.scores + static_cast<int64_t>(bh) * n;
       const int t_beg = a2 * kBN, t_end = min(e2 * kBN, n);
       // MODE 4 stages this CTA's pooled scores in the K ring (idle: every tile
@@ -840,7 +865,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int j = 0; j < 7; ++j) {
               const int t = t0 + u * kE, xj = t + j - 3;
-              w[u][j] = t < t_end && xj >= 0 && xj < n ? __ldcg(rr + xj) : -CUDART_INF_F;
+              w[u][j] = t < t_end && xj >= 0 && xj < n ? __ldcg(rr + xj) + __ldcg(rr1 + xj) : -CUDART_INF_F;
             }
 #pragma unroll
           for (int u = 0; u < kU; ++u) {
@@ -855,9 +880,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       } else {
         for (int t = t_beg + threadIdx.x; t < t_end; t += 32 * kEpiWarps) {
-          float mx = __ldcg(rr + t);
+          float mx = __ldcg(rr + t) + __ldcg(rr1 + t);
           const int lo = max(0, t - p.pool_r), hi = min(n - 1, t + p.pool_r);
-          for (int u = lo; u <= hi; ++u) mx = fmaxf(mx, __ldcg(rr + u));
+          for (int u = lo; u <= hi; ++u) mx = fmaxf(mx, __ldcg(rr + u) + __ldcg(rr1 + u));
           out[t] = mx;
           if (MODE == 4) sp[t - t_beg] = mx;
         }
@@ -880,10 +905,11 @@ __global__ void pool_kernel(const float* __restrict__ raw, float* __restrict__ o
   if (i >= total) return;
   const int64_t row = i / n;
   const int t = static_cast<int>(i - row * n);
-  const float* r = raw + row * n;
-  float m = r[t];
+  const float* r = raw + row * n;          // row half 0 of the column sums
+  const float* r1 = raw + total + row * n;  // row half 1
+  float m = r[t] + r1[t];
   const int lo = max(0, t - radius), hi = min(n - 1, t + radius);
-  for (int u = lo; u <= hi; ++u) m = fmaxf(m, r[u]);
+  for (int u = lo; u <= hi; ++u) m = fmaxf(m, r[u] + r1[u]);
   out[i] = m;
 }
 
@@ -1019,7 +1045,7 @@ ScoreLayout score_layout(int batch, int hkv, int T, int window, int group) {
   auto a16 = [](int64_t x) { return (x + 255) & ~int64_t(255); };
   L.stats = 0;
   L.raw = a16(L.stats + static_cast<int64_t>(L.bh) * L.chunks * gw * 2 * 4);
-  L.gridbar = a16(L.raw + static_cast<int64_t>(L.bh) * (T - window) * 4);
+  L.gridbar = a16(L.raw + static_cast<int64_t>(L.bh) * (T - window) * 4 * 2);  // two row halves
   L.hist = a16(L.gridbar + 64);
   L.counts = a16(L.hist + static_cast<int64_t>(kSelPasses) * L.bh * 512 * 4);
   L.sel = a16(L.counts + static_cast<int64_t>(L.bh) * L.chunks * 8);
