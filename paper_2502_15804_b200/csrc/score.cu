@@ -195,7 +195,7 @@ template <int GW>
 struct __align__(1024) ScoreSmem {
   __nv_bfloat16 q[2][GW][64];                 // [d-half][row][64], 128-B swizzled by TMA
   __nv_bfloat16 k[kStages][2][kBN][64];
-  uint64_t full[kStages], empty[kStages], tfull[2], tempty[2], qbar;
+  uint64_t full[kStages], empty[kStages], tfull[512 / GW], tempty[512 / GW], qbar;
   uint32_t tmem_base;
   alignas(16) float bias[GW];  // pass 2: per query row, m_r + log2(G * l_r) (log2 units)
   float ml[kBN][2];          // pass 1, GW=128: second column half's (max, sum) per row
@@ -601,7 +601,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   ScoreSmem<GW>& sm = *reinterpret_cast<ScoreSmem<GW>*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-  constexpr uint32_t kCols = 2 * GW;  // two accumulator buffers of GW fp32 columns
+  constexpr int NB = 512 / GW;           // accumulator buffers: all 512 TMEM columns
+  constexpr uint32_t kCols = NB * GW;
   constexpr bool kP1 = MODE != 2, kP2 = MODE != 1;
   constexpr bool kFused = MODE >= 3;
 
@@ -624,7 +625,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&sm.full[s], 1);
       mbar_init(&sm.empty[s], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NB; ++i) {
       mbar_init(&sm.tfull[i], 1);
       mbar_init(&sm.tempty[i], kEpiWarps);
     }
@@ -682,9 +683,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr uint32_t kIdesc2 = idesc_bf16(128, GW);
       const uint32_t q_base = smem_u32(&sm.q[0][0][0]);
       for (int it = 0; it < n1 + n2; ++it) {
-        const int s = it % kStages, buf = it & 1;
+        const int s = it % kStages, buf = it % NB;
         mbar_wait(&sm.full[s], (it / kStages) & 1);
-        mbar_wait(&sm.tempty[buf], ((it >> 1) & 1) ^ 1);
+        mbar_wait(&sm.tempty[buf], ((it / NB) & 1) ^ 1);
         tc_fence_after();
         const uint32_t k_base = smem_u32(&sm.k[s][0][0][0]);
         const uint32_t d_buf = tmem + buf * GW;
@@ -720,8 +721,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int limit = min(p.T - 1, p.T - p.window + (r % p.window));  // last visible key
       float m = -CUDART_INF_F, l = 0.f;
       for (int it = 0; it < n1; ++it) {
-        const int buf = it & 1;
-        mbar_wait(&sm.tfull[buf], (it >> 1) & 1);
+        const int buf = it % NB;
+        mbar_wait(&sm.tfull[buf], (it / NB) & 1);
         tc_fence_after();
         const int ts = (a1 + it) * kBN;
         // two 32-column chunks per TMEM wait, one running-max rescale per 64
@@ -800,8 +801,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (kP2) {
       const int key = 32 * quad + lane;
       for (int i2 = 0; i2 < n2; ++i2) {
-        const int it = n1 + i2, buf = it & 1;
-        mbar_wait(&sm.tfull[buf], (it >> 1) & 1);
+        const int it = n1 + i2, buf = it % NB;
+        mbar_wait(&sm.tfull[buf], (it / NB) & 1);
         tc_fence_after();
         constexpr int NC = GW / 64;  // 32-column chunks of this warp's row half
         float acc = 0.f;
