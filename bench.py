@@ -519,6 +519,9 @@ def full_layer(args, budgets, dev):
     return results
 
 
+EMU_REPLAYS = 7  # replays per emulated timing (median of the bracketed spans, min of back-to-back)
+
+
 def emulate_tp(args, budgets, dev, calibrate=True, tps=(2, 4, 8), modes_tp8=("sha", "nodp", "dp", "dp-free")):
     """AHA vs uniform TP at 2/4/8 GPUs, each rank's shard timed alone on this GPU."""
     import numpy as np
@@ -561,7 +564,7 @@ def emulate_tp(args, budgets, dev, calibrate=True, tps=(2, 4, 8), modes_tp8=("sh
                     evs[l][tp].record()
             gph = capture(body)
             span = []
-            for _ in range(3):
+            for _ in range(EMU_REPLAYS):
                 gph.replay()
                 torch.cuda.synchronize()
                 t = np.array([[evs[l][g].elapsed_time(evs[l][g + 1]) for g in range(tp)] for l in range(L)]) * 1e-3
@@ -578,7 +581,7 @@ def emulate_tp(args, budgets, dev, calibrate=True, tps=(2, 4, 8), modes_tp8=("sh
                         ops.decode_into(q[l], per_rank[g][l], wss[g][l], out_rec=sends[g][l])
                 gg = capture(run_g)
                 gg.replay()
-                tot = timed(gg.replay, 3) / 3
+                tot = min(timed(gg.replay, 1) for _ in range(EMU_REPLAYS))
                 c_g = max(0.0, (t_br[:, g].sum() - tot) / L)
                 t[:, g] = np.maximum(t_br[:, g] - c_g, 0.0)
                 del gg
