@@ -354,6 +354,7 @@ SOLO_MAX_TILES_PER_CTA = 19  # measured crossover (tools/probe_solo_params.py, p
 FKV_DECODE_SOLO = 1
 FKV_DECODE_WIDE = 2
 WIDE_MAX_SEGMENTS = 128
+WIDE_MIN_MEAN_TILES = 6  # probe_sched: wide wins from ~6 tiles per segment (TP=8 B=128 SHA), coop below (its AHA-DP copies, ~4)
 
 
 def plan_schedule(seg_len, seg_row0, seg_qrow, seg_out_row, device=None, chunk: int | None = None):
@@ -406,7 +407,7 @@ def plan_schedule(seg_len, seg_row0, seg_qrow, seg_out_row, device=None, chunk: 
             pass  # too many pieces for the per-CTA tables: cooperative schedule
     # few segments (a TP-sharded rank's cache): 8-warp CTAs, seven streams per
     # piece; otherwise 4-warp CTAs, two per SM (tools/probe_sched.py)
-    wide = mode == "wide" or (mode != "coop" and n_seg <= WIDE_MAX_SEGMENTS and mean >= 8)
+    wide = mode == "wide" or (mode != "coop" and n_seg <= WIDE_MAX_SEGMENTS and mean >= WIDE_MIN_MEAN_TILES)
     flags = FKV_DECODE_WIDE if wide else 0
     workers = default_workers(device, flags)
     ctas_sm = max(1, workers // default_workers(device, FKV_DECODE_WIDE))
