@@ -610,7 +610,12 @@ int gsel_ctas() {
 // CTAs of a launch over `bh` heads of n keys.
 int gsel_grid(int bh, int n) {
   const int64_t total = static_cast<int64_t>(bh) * n;
-  const int64_t want = (total + kGMinKeys - 1) / kGMinKeys;
+  int64_t want = (total + kGMinKeys - 1) / kGMinKeys;
+  // short heads: enough CTAs that no key range spans more than kGMaxPieces
+  // heads (ranges of <= (kGMaxPieces - 2) * n keys); gsel_reqs_per_launch
+  // keeps this within the co-resident grid
+  const int64_t span = (bh + kGMaxPieces - 3) / (kGMaxPieces - 2);
+  want = want > span ? want : span;
   const int ctas = gsel_ctas();
   return want < 1 ? 1 : (want > ctas ? ctas : static_cast<int>(want));
 }

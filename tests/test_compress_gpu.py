@@ -65,7 +65,7 @@ def test_budgets_and_select_bit_exact(cuda_device, budget):
 
 
 @pytest.mark.parametrize("bt,hkv,n,ties", [(3, 8, 5000, False), (2, 16, 3000, True), (600, 8, 168, False),
-                                           (1, 8, 70000, True), (4, 4, 0, False)])
+                                           (1, 8, 70000, True), (4, 4, 0, False), (50, 8, 3, True)])
 def test_topk_select_any_budgets(cuda_device, bt, hkv, n, ties):
     """K2 with budgets that are not an Ada split (window-only heads, whole-head
     heads, random sizes): per-head top-k == the oracle's."""
@@ -171,6 +171,7 @@ def test_selection_agreement_with_oracle_scores(cuda_device):
     (64, 16384, 256, False, 8, 0.2),       # batch 64 at 16k: pieces across heads
     (3, 32, 32, False, 8, 0.2),            # n = 0: the window only
     (7, 300, 100, "zero-head", 8, 0.2),    # heads shorter than a CTA's key range
+    (40, 40, 36, True, 8, 0.2),            # 8 keys per head: many heads per CTA range
 ])
 def test_fused_ada_select_bit_exact(cuda_device, bt, T, budget, ties, hkv, alpha):
     """The one-launch grid-wide split + select == oracle budgets + selection."""
