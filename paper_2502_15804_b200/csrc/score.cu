@@ -961,19 +961,22 @@ int score_chunks(int bh, int n_tiles) {
       sms = 148;
   }
   int c = sms / bh;
-  if (c < 1) {
-    // more heads than SMs (the multi-launch path, one CTA per SM at a time):
-    // the fewest chunks per head whose CTAs fill the last wave to >= 90 %,
-    // keeping >= 16 tiles per chunk
-    c = 1;
-    for (int t = 1; t <= 8 && n_tiles / t >= 16; ++t) {
+  // one co-resident wave (the fused cooperative launch) when it keeps >= 80 %
+  // of the SMs busy; otherwise several waves of CTAs (the multi-launch path):
+  // the fewest chunks per head whose last wave is >= 90 % full, keeping >= 16
+  // tiles per chunk (tools/probe_prefill_batch.py: 80-144 heads of 16k keys
+  // at one chunk each left up to half the SMs idle)
+  if (c < 1 || static_cast<long long>(bh) * c * 100 < 80LL * sms) {
+    int best = c < 1 ? 1 : c;
+    double best_fill = 0.0;
+    for (int t = 1; t <= 16 && n_tiles / t >= 16; ++t) {
       const long long ctas = static_cast<long long>(bh) * t;
       const long long waves = (ctas + sms - 1) / sms;
-      if (ctas * 10 >= waves * sms * 9) {
-        c = t;
-        break;
-      }
+      const double fill = static_cast<double>(ctas) / static_cast<double>(waves * sms);
+      if (fill > best_fill + 1e-9) best_fill = fill, best = t;
+      if (fill >= 0.9) break;
     }
+    c = best;
   }
   return c > n_tiles ? n_tiles : c;
 }
