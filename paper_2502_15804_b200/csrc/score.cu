@@ -11,15 +11,19 @@
 //   pass 1  D[GW rows x 128 keys]   = Q_win . K_tile^T  -> per-row online max
 //           and sum-exp with rows in TMEM lanes (thread-local reductions);
 //   pass 2  D^T[128 keys x GW rows] = K_tile . Q_win^T  -> per-key column
-//           sums of exp(s - m_r)/l_r with keys in TMEM lanes (thread-local).
+//           sums of exp(s - m_r)/l_r with keys in TMEM lanes (thread-local);
+//           the two row halves (warps 0-3 / 4-7) store separate partial
+//           sums, added by the pooling (no block barrier per tile).
 // Q_win (GW = G*w = 128 or 256 rows) is TMA-loaded once per CTA and stays in
 // shared memory; K tiles (128 keys x 128 d, 32 KiB) stream through a 3-stage
 // TMA ring with 128-B swizzle; one elected thread issues
-// tcgen05.mma.cta_group::1.kind::f16 (M=128, N=128 or GW, K=16) into a
-// double-buffered fp32 TMEM accumulator; eight epilogue warps drain it with
-// tcgen05.ld (warp e reads TMEM lanes 32*(e%4) and half e/4 of the columns).
+// tcgen05.mma.cta_group::1.kind::f16 (M=128, N=128 or GW, K=16) into fp32
+// TMEM accumulators (512 / GW buffers: all 512 columns); eight epilogue warps
+// drain them with tcgen05.ld (warp e reads TMEM lanes 32*(e%4) and half e/4
+// of the columns) and hand each buffer back as soon as it is in registers.
 // Warp roles: 0-7 epilogue, 8 TMA producer, 9 MMA issuer.  Grid: one wave
-// of one CTA per SM ((Bt*Hkv) x chunks <= #SMs when possible).
+// of one CTA per SM ((Bt*Hkv) x chunks <= #SMs) when that keeps >= 80 % of
+// the SMs busy, else wave-filled chunks over several launches (score_chunks).
 // The second pass re-reads K mostly from L2 (a layer's K for one request is
 // 32 MiB at 16k context, well inside the 126 MB L2).
 #include <cuda.h>
