@@ -371,7 +371,7 @@ def plan_schedule(seg_len, seg_row0, seg_qrow, seg_out_row, device=None, chunk: 
     * FKV_SOLO_SMALL=1 additionally sends small caches (<= 19 tiles per CTA)
       to the solo schedule with 4-8-tile pieces (the choice before the
       piece-cost planner).
-    * few segments of at least 8 tiles (<= WIDE_MAX_SEGMENTS, e.g. a TP=4/8
+    * few segments of >= WIDE_MIN_MEAN_TILES tiles on average (<= WIDE_MAX_SEGMENTS, e.g. a TP=4/8
       rank's KV heads): the cooperative schedule with 8-warp CTAs (one per
       SM, seven streaming warps per piece).
     FKV_K4_SCHEDULE = coop | wide | solo | auto overrides (measurements).
