@@ -34,3 +34,20 @@ def test_planner_compare_runs_here():
         assert row["native_s"] > 0
         if "identical" in row:
             assert row["identical"]
+
+
+def test_committed_bench_line_has_the_contract_keys():
+    """profiles/r01_bench_full.json (the last GPU bench run) carries every key
+    of the driver's contract, incl. roofline / cpu_baseline / e2e / clocks."""
+    d = json.loads((ROOT / "profiles" / "r01_bench_full.json").read_text())
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+                "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e",
+                "clocks", "gpu_launches"):
+        assert key in d, key
+    r = d["roofline"]
+    assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0 < r["frac"] <= 1
+    assert abs(r["achieved"] / r["peak"] - r["frac"]) < 1e-6 and r["traffic"] > 0
+    assert {"value", "unit", "cores", "kind", "sample"} <= set(d["cpu_baseline"])
+    assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
+    assert d["warmup"] >= 3 and d["gpu_launches"] > 0 and "workload" in d["config"]
+    assert not set(d["clocks"]["reasons"]) & {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
