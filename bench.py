@@ -286,11 +286,20 @@ def run_fairkv(args):
     if world > 1:
         dist.barrier()
     with ClockSampler(local) as clk:
-        # hold the clocks under load for ~1 s before the timed region (extra warm-up)
-        t_load = time.time()
-        while time.time() - t_load < 1.0:
+        # hold the clocks under load for ~1 s before the timed region (extra
+        # warm-up).  The replay count must be the same on every rank: the
+        # exchange's flags are counters, so a rank that ran one replay more
+        # than its peers would wait for flags that never come.
+        t_one = max(timed(run, 1), 1e-6)
+        n_load = max(1, int(1.0 / t_one))
+        if world > 1:
+            cnt = torch.tensor([n_load], dtype=torch.int64,
+                               device="cpu" if dist.get_backend() == "gloo" else dev)
+            dist.all_reduce(cnt, op=dist.ReduceOp.MIN)
+            n_load = int(cnt.item())
+        for _ in range(n_load):
             run()
-            torch.cuda.synchronize()
+        torch.cuda.synchronize()
         t = timed(run, args.steps)
     t = max_over_ranks(t, world)
     if world > 1:

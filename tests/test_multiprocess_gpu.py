@@ -86,10 +86,6 @@ def test_two_process_p2p_exchange(cuda_device, tmp_path, tp, mode):
         assert ok == "1", f"rank {r}: max |o - ref| = {err}"
 
 
-@pytest.mark.skipif(os.environ.get("FKV_SHARED_BENCH_TEST") != "1",
-                    reason="opt-in: two graph-replaying ranks time-sliced on one GPU intermittently stall "
-                           "(>280 s) in the spinning cross-process wait; the protocol itself is covered by "
-                           "test_two_process_p2p_exchange")
 def test_bench_two_ranks_shared_device(cuda_device):
     """bench.py's N > 1 path end to end (torchrun, P2P exchange through CUDA
     IPC, graph capture, max-over-ranks timing) with both ranks on the one GPU
