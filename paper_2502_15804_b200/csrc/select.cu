@@ -56,6 +56,7 @@ constexpr int kGMaxPieces = 16;  // heads touched per CTA
 constexpr int kGBufs = 3;        // rotating per-pass histogram buffers
 constexpr int kGMinKeys = 2048;  // keys per CTA, at least
 constexpr int kGUnroll = 4;
+constexpr int kGCacheBytes = 84 * 1024;  // key cache per CTA (two CTAs per SM still fit)
 
 struct GSelParams {
   const float* scores;  // [BH, n] of this launch
@@ -63,6 +64,7 @@ struct GSelParams {
   const int32_t* head_k;       // top-k mode: per-head budgets of this launch (incl. window); null = Ada
   const int32_t* budgets_all;  // top-k mode: all budgets (offsets are their exclusive prefix)
   int select;                  // 0: budgets only (Ada mode)
+  int cache;                   // 1: the CTA's keys stay in shared memory after pass 0
   int req0, bh_total;   // first request of this launch; Bt*Hkv over all launches
   int64_t total;        // BH * n
   uint32_t* hist;       // [kGBufs][BH][2][256] (buffers 0, 1 zeroed by the host)
@@ -180,7 +182,7 @@ __device__ __forceinline__ void for_keys(const float* s, int lo, int hi, Fn&& fn
     const int nh = a - lo;
     const int i = tid < nh ? lo + tid : b + tid - nh;
     const bool in = tid < nh + (hi - b);
-    fn(in, in ? orderable(__ldg(s + i)) : 0u);
+    fn(in, in ? orderable(__ldg(s + i)) : 0u, i);
   }
   const float4* v4 = reinterpret_cast<const float4*>(s + a);
   const int nv = (b - a) >> 2;
@@ -193,17 +195,19 @@ __device__ __forceinline__ void for_keys(const float* s, int lo, int hi, Fn&& fn
     }
 #pragma unroll
     for (int u = 0; u < kGUnroll; ++u) {
-      const bool in = base + u * kGThreads + tid < nv;
-      fn(in, orderable(x[u].x));
-      fn(in, orderable(x[u].y));
-      fn(in, orderable(x[u].z));
-      fn(in, orderable(x[u].w));
+      const int j = base + u * kGThreads + tid;
+      const bool in = j < nv;
+      fn(in, orderable(x[u].x), a + 4 * j);
+      fn(in, orderable(x[u].y), a + 4 * j + 1);
+      fn(in, orderable(x[u].z), a + 4 * j + 2);
+      fn(in, orderable(x[u].w), a + 4 * j + 3);
     }
   }
 }
 
 __global__ void __launch_bounds__(kGThreads) grid_select_kernel(const GSelParams p) {
   __shared__ GSelSmem sm;
+  extern __shared__ uint32_t skeys[];  // p.cache: orderable keys of [k0, k1)
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int HK = p.hkv, f = p.f, R = p.R, n = p.n;
   const int64_t k0 = static_cast<int64_t>(blockIdx.x) * p.total / gridDim.x;
@@ -258,7 +262,9 @@ __global__ void __launch_bounds__(kGThreads) grid_select_kernel(const GSelParams
       piece(lh, lo, hi);
       const float* s = p.scores + static_cast<int64_t>(bh) * n;
       const uint32_t gp = rq.prefix, gm = rq.mask, fp = fh.prefix, fm = fh.mask;
-      auto add = [&](bool in, uint32_t o) {
+      uint32_t* skh = skeys + (static_cast<int64_t>(bh) * n - k0);  // this head's keys (p.cache)
+      auto add = [&](bool in, uint32_t o, int i) {
+        if (p.cache && pass == 0 && in) skh[i] = o;
         const uint32_t dig = (o >> shift) & 255u;
         const uint32_t dg = in && (o & gm) == gp ? dig : 256u;
         const uint32_t df = in && (o & fm) == fp ? dig : 256u;
@@ -268,7 +274,15 @@ __global__ void __launch_bounds__(kGThreads) grid_select_kernel(const GSelParams
         if (ga && dg < 256u) atomicAdd(&sm.hist[0][dg], 1u);
         if (fa && !same && df < 256u) atomicAdd(&sm.hist[1][df], 1u);
       };
-      for_keys(s, lo, hi, add);
+      if (p.cache && pass > 0) {  // keys from the shared-memory cache
+        for (int base = lo; base < hi; base += kGThreads) {
+          const int i = base + tid;
+          const bool in = i < hi;
+          add(in, in ? skh[i] : 0u, i);
+        }
+      } else {
+        for_keys(s, lo, hi, add);
+      }
       __syncthreads();
       uint32_t* gh = hb + static_cast<int64_t>(bh) * 512;
       if (tid < 256) {
@@ -462,24 +476,34 @@ __global__ void __launch_bounds__(kGThreads) grid_select_kernel(const GSelParams
     int c1 = 0, c2 = 0;
     if (r.kind != 2) {
       const Seg g = segment(s, lo, hi);
-      auto count = [&](float x) {
-        const int k = rule_class(r, orderable(x));
+      auto count = [&](uint32_t o) {
+        const int k = rule_class(r, o);
         c1 += k == 1;
         c2 += k == 2;
       };
+      const uint32_t* skh = skeys + (static_cast<int64_t>(bh) * n - k0);
+      auto key = [&](int i) { return p.cache ? skh[i] : orderable(__ldg(s + i)); };
       if (wid == 0)
-        for (int i = g.lo + lane; i < g.a; i += 32) count(__ldg(s + i));
+        for (int i = g.lo + lane; i < g.a; i += 32) count(key(i));
       const float4* v4 = reinterpret_cast<const float4*>(s + g.a);
 #pragma unroll 4
       for (int j = g.v0 + lane; j < g.v1; j += 32) {
-        const float4 x = __ldg(v4 + j);
-        count(x.x);
-        count(x.y);
-        count(x.z);
-        count(x.w);
+        if (p.cache) {
+          const int i = g.a + 4 * j;
+          count(skh[i]);
+          count(skh[i + 1]);
+          count(skh[i + 2]);
+          count(skh[i + 3]);
+        } else {
+          const float4 x = __ldg(v4 + j);
+          count(orderable(x.x));
+          count(orderable(x.y));
+          count(orderable(x.z));
+          count(orderable(x.w));
+        }
       }
       if (wid == kGWarps - 1)
-        for (int i = g.b + lane; i < g.hi; i += 32) count(__ldg(s + i));
+        for (int i = g.b + lane; i < g.hi; i += 32) count(key(i));
     }
     c1 = __reduce_add_sync(0xffffffffu, c1);
     c2 = __reduce_add_sync(0xffffffffu, c2);
@@ -547,10 +571,11 @@ __global__ void __launch_bounds__(kGThreads) grid_select_kernel(const GSelParams
     int32_t* out = p.idx + sm.off[lh];
     const float* s = p.scores + static_cast<int64_t>(bh) * n;
     const Seg g = segment(s, lo, hi);
+    const uint32_t* skh = skeys + (static_cast<int64_t>(bh) * n - k0);
     auto emit_scalar = [&](int i0, int i1) {
       for (int base = i0; base < i1; base += 32) {
         const int i = base + lane;
-        const int k = i < i1 ? rule_class(r, orderable(__ldg(s + i))) : 0;
+        const int k = i < i1 ? rule_class(r, p.cache ? skh[i] : orderable(__ldg(s + i))) : 0;
         const uint32_t ties = __ballot_sync(0xffffffffu, k == 2);
         const bool take = k == 1 || (k == 2 && tie_run + __popc(ties & lt) < r.ktie);
         const uint32_t bal = __ballot_sync(0xffffffffu, take);
@@ -563,13 +588,21 @@ __global__ void __launch_bounds__(kGThreads) grid_select_kernel(const GSelParams
     const float4* v4 = reinterpret_cast<const float4*>(s + g.a);
     for (int jb = g.v0; jb < g.v1; jb += 32) {
       const int j = jb + lane;
-      const float4 x = j < g.v1 ? __ldg(v4 + j) : make_float4(0.f, 0.f, 0.f, 0.f);
       int k[4] = {0, 0, 0, 0};
       if (j < g.v1) {
-        k[0] = rule_class(r, orderable(x.x));
-        k[1] = rule_class(r, orderable(x.y));
-        k[2] = rule_class(r, orderable(x.z));
-        k[3] = rule_class(r, orderable(x.w));
+        if (p.cache) {
+          const int i = g.a + 4 * j;
+          k[0] = rule_class(r, skh[i]);
+          k[1] = rule_class(r, skh[i + 1]);
+          k[2] = rule_class(r, skh[i + 2]);
+          k[3] = rule_class(r, skh[i + 3]);
+        } else {
+          const float4 x = __ldg(v4 + j);
+          k[0] = rule_class(r, orderable(x.x));
+          k[1] = rule_class(r, orderable(x.y));
+          k[2] = rule_class(r, orderable(x.z));
+          k[3] = rule_class(r, orderable(x.w));
+        }
       }
       int t_all, n_all;
       int tr = tie_run + warp_excl((k[0] == 2) + (k[1] == 2) + (k[2] == 2) + (k[3] == 2), t_all);
@@ -690,9 +723,21 @@ int grid_select(const float* scores, int batch, int hkv, int n, int budget, int 
     if (int rc = cuda_check(cudaMemsetAsync(ws, 0, 256 + static_cast<size_t>(2) * bh * 512 * 4, st),
                             "select workspace reset"))
       return rc;
+    const int grid = gsel_grid(bh, n);
+    const int64_t span_keys = (p.total + grid - 1) / grid + 1;
+    p.cache = span_keys * 4 <= kGCacheBytes;
+    static bool configured = false;
+    if (!configured) {
+      if (int rc = cuda_check(cudaFuncSetAttribute(grid_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   kGCacheBytes),
+                              "grid select smem attribute"))
+        return rc;
+      configured = true;
+    }
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(gsel_grid(bh, n), 1, 1);
+    cfg.gridDim = dim3(grid, 1, 1);
     cfg.blockDim = dim3(kGThreads, 1, 1);
+    cfg.dynamicSmemBytes = p.cache ? static_cast<size_t>(span_keys) * 4 : 0;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeCooperative;
