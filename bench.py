@@ -528,7 +528,8 @@ def full_layer(args, budgets, dev):
     return results
 
 
-EMU_REPLAYS = 7  # replays per emulated timing (median of the bracketed spans, min of back-to-back)
+EMU_REPLAYS = 3  # replays per emulated timing (median of the bracketed spans, min of back-to-back)
+EMU_ROUNDS = 3   # interleaved rounds over the modes; the median round is reported
 
 
 def emulate_tp(args, budgets, dev, calibrate=True, tps=(2, 4, 8), modes_tp8=("sha", "nodp", "dp", "dp-free")):
@@ -554,6 +555,11 @@ def emulate_tp(args, budgets, dev, calibrate=True, tps=(2, 4, 8), modes_tp8=("sh
     for tp in tps:
         row = {}
         modes = list(modes_tp8) if tp == 8 else ["sha", "nodp", "dp"]
+        # Build every mode first, then time them in interleaved rounds (the
+        # median round per mode): a few-µs layer drifts with clocks / power
+        # state by several percent, which sequential per-mode timing would
+        # fold into the AHA-vs-uniform ratios.
+        st = {}
         for mode in modes:
             ch = args.ch if mode != "dp" or tp != 8 else 8  # equal split needs CH=8 at TP=8
             plan, prof = make_plan(budgets, tp, ch, mode)
@@ -565,35 +571,51 @@ def emulate_tp(args, budgets, dev, calibrate=True, tps=(2, 4, 8), modes_tp8=("sh
             wss = [[ops.DecodeWorkspace(c) for c in pr] for pr in per_rank]
             evs = [[torch.cuda.Event(enable_timing=True, external=True) for _ in range(tp + 1)] for _ in range(L)]
 
-            def body():
+            def body(per_rank=per_rank, wss=wss, sends=sends, evs=evs):
                 for l in range(L):
                     for g in range(tp):
                         evs[l][g].record()
                         ops.decode_into(q[l], per_rank[g][l], wss[g][l], out_rec=sends[g][l])
                     evs[l][tp].record()
             gph = capture(body)
+            # Event nodes between launches cost every kernel a full launch and
+            # ramp (no programmatic overlap), which a real rank -- 80 layers back
+            # to back -- does not pay.  Each rank's layers are also timed back
+            # to back to remove the per-launch bracketing overhead c_g.
+            ggs = []
+            for g in range(tp):
+                def run_g(g=g, per_rank=per_rank, wss=wss, sends=sends):
+                    for l in range(L):
+                        ops.decode_into(q[l], per_rank[g][l], wss[g][l], out_rec=sends[g][l])
+                ggs.append(capture(run_g))
+            st[mode] = dict(plan=plan, prof=prof, finals=finals, keep=(per_rank, sends, wss), evs=evs,
+                            gph=gph, ggs=ggs, rounds=[])
+
+        def measure(m):
+            gph, evs, ggs = m["gph"], m["evs"], m["ggs"]
             span = []
             for _ in range(EMU_REPLAYS):
                 gph.replay()
                 torch.cuda.synchronize()
-                t = np.array([[evs[l][g].elapsed_time(evs[l][g + 1]) for g in range(tp)] for l in range(L)]) * 1e-3
-                span.append(t)
+                span.append(np.array([[evs[l][g].elapsed_time(evs[l][g + 1]) for g in range(tp)]
+                                      for l in range(L)]) * 1e-3)
             t_br = np.median(np.stack(span), axis=0)  # [L, tp], each launch event-bracketed
-            # Event nodes between launches cost every kernel a full launch and
-            # ramp (no programmatic overlap), which a real rank -- 80 layers back
-            # to back -- does not pay.  Time each rank's layers back to back too
-            # and remove the per-launch bracketing overhead c_g it reveals.
             t = np.empty_like(t_br)
             for g in range(tp):
-                def run_g(g=g):
-                    for l in range(L):
-                        ops.decode_into(q[l], per_rank[g][l], wss[g][l], out_rec=sends[g][l])
-                gg = capture(run_g)
-                gg.replay()
-                tot = min(timed(gg.replay, 1) for _ in range(EMU_REPLAYS))
+                ggs[g].replay()
+                tot = min(timed(ggs[g].replay, 1) for _ in range(EMU_REPLAYS))
                 c_g = max(0.0, (t_br[:, g].sum() - tot) / L)
                 t[:, g] = np.maximum(t_br[:, g] - c_g, 0.0)
-                del gg
+            return t, t_br
+
+        for _ in range(EMU_ROUNDS):
+            for mode in modes:
+                st[mode]["rounds"].append(measure(st[mode]))
+        for mode in modes:
+            m = st[mode]
+            steps = [r[0].max(axis=1).sum() for r in m["rounds"]]
+            t, t_br = m["rounds"][int(np.argsort(steps)[len(steps) // 2])]
+            plan, prof, finals = m["plan"], m["prof"], m["finals"]
             step = t.max(axis=1).sum()
             step_br = t_br.max(axis=1).sum()
             # K5 after the all-gather (identical on every rank): LSE merge of
@@ -621,8 +643,9 @@ def emulate_tp(args, budgets, dev, calibrate=True, tps=(2, 4, 8), modes_tp8=("sh
                          "busy_rate": float(t.sum() / (step * tp)),
                          "kv_max_over_mean": imbalance_ratio(loads),
                          "extra_copies": int(sum(len(gr) for la in plan.layers for gr in la.groups) - L * HKV),
-                         "sim_throughput": sim}
-            del gph, per_rank, sends, wss
+                         "sim_throughput": sim,
+                         "rounds_tokens_per_s": [round(bt / x, 1) for x in steps]}
+        del st
         for mode in modes[1:]:
             row[mode]["gain_vs_sha"] = row[mode]["tokens_per_s"] / row["sha"]["tokens_per_s"]
             row[mode]["sim_gain_vs_sha"] = row[mode]["sim_throughput"] / row["sha"]["sim_throughput"]
@@ -631,7 +654,8 @@ def emulate_tp(args, budgets, dev, calibrate=True, tps=(2, 4, 8), modes_tp8=("sh
         results["calibration"] = calibrate_from(samples, budgets, args, dev, base, q)
     results["note"] = ("each rank's K4 (+ fused segment merge) shard of every layer timed alone on this GPU "
                        "(event nodes in one CUDA graph), minus the per-launch bracketing overhead measured by "
-                       "timing the rank's 80 layers back to back; layer span = max over ranks (synchronous "
+                       "timing the rank's 80 layers back to back; modes timed in 3 interleaved rounds, median "
+                       "round reported (rounds_tokens_per_s); layer span = max over ranks (synchronous "
                        "per-layer barrier, reference simulate.py:118-136); all-gather not included (single "
                        "GPU); tokens_per_s_with_k5 adds the post-exchange LSE merge (K5) of every layer; "
                        "tokens_per_s_bracketed = without the correction; sim = reference simulator, "
