@@ -58,6 +58,10 @@ extern "C" {
 
 const char* fkv_last_error(void);
 int fkv_version(void);
+/* SHA-256 (hex) of the sources, headers and flags the library was built
+ * from (csrc/build.py); the Python binding refuses a library whose hash
+ * does not match the sources next to it. */
+const char* fkv_source_hash(void);
 
 /* ------------------------------------------------------------ B1 planner -- */
 
@@ -127,6 +131,13 @@ typedef struct fkv_work {
 /* FKV_DECODE_WIDE = cooperative schedule with 8-warp CTAs (one per SM, seven
  * streaming warps per piece) instead of 4-warp CTAs (two per SM). */
 #define FKV_DECODE_WIDE 2
+/* FKV_DECODE_AFTER_WAIT: the cache or its work table was just written on
+ * this stream (fkv_append / fkv_compact).  The kernel is launched with
+ * programmatic dependent launch; by default it reads the work table and
+ * starts its first K/V copies before waiting for the preceding grid (they
+ * are static between steps).  With this flag every global read comes after
+ * the wait. */
+#define FKV_DECODE_AFTER_WAIT 4
 
 /*   q            bf16 [*, 128]   query rows
  *   k, v         bf16 [rows,128] swizzled cache rows (layout above)

@@ -1,6 +1,7 @@
 """Search-kernel plugin registry (drop-in for pkg/src/headbalance/_kernel/__init__.py:1-57).
 
-One backend: ``"native"``, the C++ planner inside libfairkv.so.  The
+One backend, reported as ``"compiled"`` like the reference's compiled
+kernel: the C++ planner inside libfairkv.so.  The
 reference's pure-Python kernel is not part of this product; its CPU
 restatement lives in ``oracle/`` and is used only by the tests as the
 checker.  ``HEADBALANCE_KERNEL`` keeps the reference's spelling: unset /
@@ -29,13 +30,17 @@ if _choice not in _NATIVE_NAMES:
 
 
 def backend() -> str:
-    """Name of the active kernel backend."""
-    return "native"
+    """Name of the active kernel backend: "compiled", as the reference names
+    its compiled kernel (_kernel/__init__.py:32-34) -- this one is the C++
+    planner in libfairkv.so."""
+    return "compiled"
 
 
 def implementations() -> dict:
-    """All kernel implementations shipped, for parity tests and benchmarks."""
-    return {"native": native}
+    """All kernel implementations shipped, for parity tests and benchmarks
+    (reference _kernel/__init__.py:37-46; the pure-Python kernel is not
+    shipped -- tests bring it as the checker)."""
+    return {"compiled": native}
 
 
 def solve_equal_split(weights, heads, tp, cutoff, node_budget=DEFAULT_NODE_BUDGET, hint=None):

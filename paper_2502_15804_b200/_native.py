@@ -23,6 +23,24 @@ if not LIB_PATH.exists():
         "(or __graft_entry__.build()); this package has no fallback path"
     )
 
+def _check_fresh() -> None:
+    """Refuse a library built from other sources than the ones next to it
+    (a stale prebuilt binary in a snapshot): its embedded source hash must
+    equal the hash of csrc/ + include/ (csrc/build.py).  Skipped when the
+    sources are not shipped, or FAIRKV_LIB points elsewhere on purpose."""
+    if "FAIRKV_LIB" in os.environ:
+        return
+    from .csrc import build as _build
+    if not all((_build.CSRC / n).exists() for n in _build.CU_SOURCES + _build.CXX_SOURCES):
+        return
+    have, want = _build.embedded_hash(LIB_PATH), _build.source_hash()
+    if have != want:
+        raise ImportError(
+            f"{LIB_PATH} was built from different sources (embedded hash {have}, sources {want}); "
+            "rebuild with `python -m paper_2502_15804_b200.csrc.build` (or __graft_entry__.build())")
+
+
+_check_fresh()
 lib = C.CDLL(str(LIB_PATH))  # CDLL releases the GIL for the duration of each call
 
 _i32, _i64, _f32, _f64, _vp = C.c_int32, C.c_int64, C.c_float, C.c_double, C.c_void_p
@@ -31,6 +49,7 @@ _pi32, _pi64, _pf64 = C.POINTER(_i32), C.POINTER(_i64), C.POINTER(_f64)
 _SIGS = {
     "fkv_last_error": (C.c_char_p, []),
     "fkv_version": (C.c_int, []),
+    "fkv_source_hash": (C.c_char_p, []),
     "fkv_solve_equal_split": (C.c_int, [_vp, _vp, _i32, _i32, _f64, _i64, _vp, _vp, _vp, _vp, _vp]),
     "fkv_solve_free_split": (C.c_int, [_vp, _vp, _i32, _i32, _f64, _i64, _vp, _vp, _vp, _vp, _vp]),
     "fkv_select_best": (C.c_int, [_vp, _i32, _i32, _i32, _i32, _i32, _i64, _i64,

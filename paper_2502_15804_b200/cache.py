@@ -353,6 +353,7 @@ def plan_work_solo(seg_len, n_workers: int, piece_tiles: int = 16, whole_tiles: 
 SOLO_MAX_TILES_PER_CTA = 19  # measured crossover (tools/probe_solo_params.py, probe_sched.py): ~5600 tiles per GPU-layer
 FKV_DECODE_SOLO = 1
 FKV_DECODE_WIDE = 2
+FKV_DECODE_AFTER_WAIT = 4
 WIDE_MAX_SEGMENTS = 128
 WIDE_MIN_MEAN_TILES = 6  # probe_sched: wide wins from ~6 tiles per segment (TP=8 B=128 SHA), coop below (its AHA-DP copies, ~4)
 
@@ -445,6 +446,13 @@ class LayerCache:
     @property
     def flags(self) -> int:
         return int(self.host.get("flags", 0))
+
+    @property
+    def launch_flags(self) -> int:
+        """Schedule flags plus FKV_DECODE_AFTER_WAIT once the cache has been
+        written on the device (compaction, decode-time appends): the decode
+        kernel then reads nothing before its programmatic-launch wait."""
+        return self.flags | (FKV_DECODE_AFTER_WAIT if self.host.get("written") else 0)
 
     @property
     def work_k(self) -> int:

@@ -4,11 +4,38 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <string>
 
 #include "fairkv.h"
 
 namespace fkv {
+
+// One-time, per-device host setup (function attributes, SM counts and
+// occupancy belong to a device: a process that launches on a second GPU must
+// redo them there).  `init` returns a positive value or a negative error
+// code; racing threads may both run it (it is idempotent), the first
+// positive result sticks.  Devices beyond kMaxDevices recompute every call.
+constexpr int kMaxDevices = 64;
+template <typename F>
+int per_device(std::atomic<int> (&slot)[kMaxDevices], F&& init) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) dev = -1;
+  if (dev >= 0 && dev < kMaxDevices) {
+    const int v = slot[dev].load(std::memory_order_acquire);
+    if (v > 0) return v;
+  }
+  const int v = init(dev < 0 ? 0 : dev);
+  if (v > 0 && dev >= 0 && dev < kMaxDevices) slot[dev].store(v, std::memory_order_release);
+  return v;
+}
+
+inline int sm_count(int dev) {
+  int sms = 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0)
+    sms = 148;
+  return sms;
+}
 
 int set_error(int code, const std::string& msg);
 

@@ -76,6 +76,7 @@ struct DecodeParams {
   int32_t* sig_done;              // CTAs-finished counter (local), zero between launches
   int32_t* sig_flag[FKV_MAX_PEERS];  // per peer: flags[tp] in that peer's memory
   int n_sig, my_rank;
+  int after_wait;  // FKV_DECODE_AFTER_WAIT: no global read before griddepcontrol.wait
 };
 
 template <int W>
@@ -166,6 +167,9 @@ __global__ void __launch_bounds__(Shape<MODE>::W * 32, Shape<MODE>::kCtasPerSm)
     g_stamps[blockIdx.x * 16] = smid;
   }
 
+  // A cache written by the preceding kernel (append / compact): its rows and
+  // work table are only guaranteed visible after the wait.
+  if (p.after_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
   // The CTA's whole piece list in one coalesced load (lane j <- piece j);
   // everything the kernel needs per piece is in its 32-byte descriptor, so
   // the first TMA is one dependent global load away from kernel entry.
@@ -269,9 +273,10 @@ __global__ void __launch_bounds__(Shape<MODE>::W * 32, Shape<MODE>::kCtasPerSm)
     }
   };
   // Programmatic dependent launch: everything above (barrier init, schedule
-  // reads, the first K/V tiles in flight) touches only the static cache and
-  // overlaps the previous kernel's tail; q and every global write come after
-  // the previous grid has completed.
+  // reads, the first K/V tiles in flight) touches only the cache, static
+  // between steps unless FKV_DECODE_AFTER_WAIT, and overlaps the previous
+  // kernel's tail; q and every global write come after the previous grid has
+  // completed.
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;");
   load_q(0);
@@ -769,24 +774,18 @@ __global__ void __launch_bounds__(G * 32)
 
 template <int G, int PROBE = 0, int MODE = 0>
 int launch_decode(const DecodeParams& p, cudaStream_t st) {
-  static int grid_cap = 0;  // 2 persistent CTAs per SM
-  if (!grid_cap) {
-    if (int rc = cuda_check(cudaFuncSetAttribute(decode_kernel<G, PROBE, MODE>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 Shape<MODE>::kSmem),
-                            "decode smem attribute"))
-      return rc;
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_kernel<G, PROBE, MODE>,
-                                                  Shape<MODE>::W * 32, Shape<MODE>::kSmem);
-    grid_cap = sms * (per_sm > 0 ? per_sm : 1);
-  }
+  static std::atomic<int> ready[kMaxDevices];  // smem attribute set on this device
+  const int rc = per_device(ready, [](int) {
+    const int e = cuda_check(cudaFuncSetAttribute(decode_kernel<G, PROBE, MODE>,
+                                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  Shape<MODE>::kSmem),
+                             "decode smem attribute");
+    return e < 0 ? e : 1;
+  });
+  if (rc < 0) return rc;
   // one CTA per worker; nothing in the kernel waits on another CTA, so the
-  // grid may exceed the co-resident limit (grid_cap) -- later CTAs start as
-  // earlier ones retire
-  (void)grid_cap;
+  // grid may exceed the co-resident limit -- later CTAs start as earlier
+  // ones retire
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(p.n_workers, 1, 1);
   cfg.blockDim = dim3(Shape<MODE>::W * 32, 1, 1);
@@ -894,6 +893,7 @@ extern "C" int fkv_decode_exchange(const void* q, const void* k, const void* v,
   for (int j = 0; j < n_sig; ++j) p.sig_flag[j] = sig_flags[j];
   p.n_sig = n_sig;
   p.my_rank = my_rank;
+  p.after_wait = (flags & FKV_DECODE_AFTER_WAIT) != 0;
   const int probe = g_probe;
   g_probe = 0;
   return decode_entry(p, group, static_cast<cudaStream_t>(stream), probe, flags);

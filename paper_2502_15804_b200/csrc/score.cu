@@ -925,15 +925,16 @@ using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, 
                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 EncodeTiled encoder() {
-  static EncodeTiled fn = nullptr;
-  if (!fn) {
+  // a driver entry point: the same for every device, resolved once
+  static const EncodeTiled fn = []() -> EncodeTiled {
     void* ptr = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
             cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeTiled>(ptr);
-  }
+      return reinterpret_cast<EncodeTiled>(ptr);
+    return nullptr;
+  }();
   return fn;
 }
 
@@ -957,13 +958,8 @@ int make_map(CUtensorMap* map, const void* base, int64_t rows, int box_rows) {
 // Key chunks per (request, KV head): one wave of one CTA per SM when the
 // heads alone do not fill the GPU; never more chunks than tiles.
 int score_chunks(int bh, int n_tiles) {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0)
-      sms = 148;
-  }
+  static std::atomic<int> sms_of[kMaxDevices];
+  const int sms = per_device(sms_of, sm_count);
   int c = sms / bh;
   // one co-resident wave (the fused cooperative launch) when it keeps >= 80 %
   // of the SMs busy; otherwise several waves of CTAs (the multi-launch path):
@@ -991,15 +987,16 @@ template <int GW>
 int launch_score(const CUtensorMap& tq, const CUtensorMap& tk, const ScoreParams& p, int batch_heads,
                  int mode, cudaStream_t st, size_t reset_bytes = sizeof(GridBar)) {
   const size_t smem = sizeof(ScoreSmem<GW>) + 1024;
-  static bool configured = false;
-  if (!configured) {
+  static std::atomic<int> ready[kMaxDevices];  // smem attributes set on this device
+  const int rc0 = per_device(ready, [smem](int) {
     for (auto fn : {score_kernel<1, GW>, score_kernel<2, GW>, score_kernel<3, GW>, score_kernel<4, GW>})
       if (int rc = cuda_check(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    smem),
                               "score smem attribute"))
         return rc;
-    configured = true;
-  }
+    return 1;
+  });
+  if (rc0 < 0) return rc0;
   dim3 grid(p.n_chunks, batch_heads);
   if (mode >= 3) {
     // one cooperative launch: both passes and the pooling (grid <= #SMs, 1 CTA/SM)

@@ -628,16 +628,13 @@ __global__ void __launch_bounds__(kGThreads) grid_select_kernel(const GSelParams
 }
 
 int gsel_ctas() {
-  static int ctas = 0;
-  if (!ctas) {
-    int dev = 0, sms = 148, occ = 1;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  static std::atomic<int> ctas[kMaxDevices];
+  return per_device(ctas, [](int dev) {
+    int occ = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, grid_select_kernel, kGThreads, 0);
     occ = occ < 1 ? 1 : (occ > 2 ? 2 : occ);
-    ctas = sms * occ;
-  }
-  return ctas;
+    return sm_count(dev) * occ;
+  });
 }
 
 // CTAs of a launch over `bh` heads of n keys.
@@ -726,14 +723,15 @@ int grid_select(const float* scores, int batch, int hkv, int n, int budget, int 
     const int grid = gsel_grid(bh, n);
     const int64_t span_keys = (p.total + grid - 1) / grid + 1;
     p.cache = span_keys * 4 <= kGCacheBytes;
-    static bool configured = false;
-    if (!configured) {
-      if (int rc = cuda_check(cudaFuncSetAttribute(grid_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   kGCacheBytes),
-                              "grid select smem attribute"))
-        return rc;
-      configured = true;
-    }
+    static std::atomic<int> ready[kMaxDevices];  // smem attribute set on this device
+    const int rc0 = per_device(ready, [](int) {
+      const int e = cuda_check(cudaFuncSetAttribute(grid_select_kernel,
+                                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                    kGCacheBytes),
+                               "grid select smem attribute");
+      return e < 0 ? e : 1;
+    });
+    if (rc0 < 0) return rc0;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid, 1, 1);
     cfg.blockDim = dim3(kGThreads, 1, 1);

@@ -16,6 +16,7 @@ import torch
 
 from . import ops
 from .cache import LayerCache
+from .exchange import exchange_buffer
 from .sharding import FinalMerge, LayerShard
 
 
@@ -93,8 +94,9 @@ class StackDecoder:
             return
         if self.exchange_mode == "p2p":
             ptr, src, row = self.final[l]
-            ops.decode_exchange(q, c, self.endpoint, l & 1, self.ws[l])
-            ops.merge_wait(self.endpoint, l & 1, ptr, src, row, self.group, out_bf16=out,
+            buf = exchange_buffer(l, len(self.caches))
+            ops.decode_exchange(q, c, self.endpoint, buf, self.ws[l])
+            ops.merge_wait(self.endpoint, buf, ptr, src, row, self.group, out_bf16=out,
                            out_lse=out_lse)
             return
         ops.decode_into(q, c, self.ws[l], out_rec=self.send[l])

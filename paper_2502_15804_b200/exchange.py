@@ -8,10 +8,14 @@ rank (P2P stores over NVLink, ``fkv_decode_exchange``); its last warp then
 bumps ``flags[r]`` on every rank (system-scope atomics after a system
 fence).  The merge kernel on each rank waits until all ``flags`` reached
 this layer's count, merges the DP copies and writes o (``fkv_merge_wait``).
-Layer parity double-buffers ``recv``: a rank can run at most one layer
-ahead of any peer (layer l+1's merge needs every peer's layer l+1 decode,
-which follows that peer's layer l merge in stream order), so the buffer a
-fast rank writes is never the one a slow rank is still reading.
+Receive areas rotate per layer (``exchange_buffer``): a rank can run at
+most one layer ahead of any peer (its merge of layer s needs every peer's
+decode of s, which follows that peer's merge of s-1 in stream order), so it
+suffices that consecutive layers of the running sequence -- including the
+wrap from the last layer of one step to layer 0 of the next -- use different
+buffers.  Parity alone does that for an even layer count; an odd count
+gives its last layer a third buffer.  The assignment is static, so the whole
+step can be captured once in a CUDA graph and replayed.
 
 ``P2PGroup.connect`` maps peers via torch.distributed (one process per GPU);
 ``P2PGroup.loopback`` builds tp virtual ranks inside one process on one GPU
@@ -28,6 +32,19 @@ import torch
 from . import _native
 
 REC = 132
+NBUF = 3  # receive areas per rank (see exchange_buffer)
+
+
+def exchange_buffer(layer: int, num_layers: int) -> int:
+    """Receive area of ``layer`` in a step of ``num_layers`` layers: layer
+    parity, except the last layer of an odd-length step (its successor is
+    layer 0 of the next step, also parity 0), which takes area 2."""
+    if num_layers < 2:
+        raise ValueError("the fused exchange needs >= 2 layers per step: consecutive steps of a "
+                         "1-layer stack would reuse one receive area while a peer still reads it")
+    if not 0 <= layer < num_layers:
+        raise ValueError(f"layer {layer} outside 0..{num_layers - 1}")
+    return 2 if num_layers % 2 and layer == num_layers - 1 else layer & 1
 
 
 class _Buf:
@@ -61,10 +78,10 @@ class RankEndpoint:
     def __init__(self, rank: int, tp: int, slots: int, group: int):
         self.rank, self.tp, self.slots, self.group = rank, tp, slots, group
         self.block = slots * group * REC * 4          # bytes of one rank's block
-        self.recv = [_Buf(tp * self.block), _Buf(tp * self.block)]  # layer parity
+        self.recv = [_Buf(tp * self.block) for _ in range(NBUF)]  # exchange_buffer()
         self.flags = _Buf(4 * max(tp, 2))
         self.ctr = _Buf(16)                            # [0] sig_done, [2:4] consumed
-        self.peer_recv: list[list[int]] = [[], []]    # [parity][peer] base address
+        self.peer_recv: list[list[int]] = [[] for _ in range(NBUF)]  # [buffer][peer] base
         self.peer_flags: list[int] = []
 
     # -- pointers handed to the kernels
@@ -106,7 +123,7 @@ class P2PGroup:
     def loopback(tp: int, slots: int, group: int) -> "P2PGroup":
         eps = [RankEndpoint(r, tp, slots, group) for r in range(tp)]
         for ep in eps:
-            ep.peer_recv = [[e.recv[par].ptr for e in eps] for par in (0, 1)]
+            ep.peer_recv = [[e.recv[par].ptr for e in eps] for par in range(NBUF)]
             ep.peer_flags = [e.flags.ptr for e in eps]
         return P2PGroup(eps)
 
@@ -114,11 +131,11 @@ class P2PGroup:
     def connect(rank: int, tp: int, slots: int, group: int, process_group=None) -> "P2PGroup":
         import torch.distributed as dist
         ep = RankEndpoint(rank, tp, slots, group)
-        mine = {"recv": [ep.recv[0].handle(), ep.recv[1].handle()], "flags": ep.flags.handle()}
+        mine = {"recv": [b.handle() for b in ep.recv], "flags": ep.flags.handle()}
         allh = [None] * tp
         dist.all_gather_object(allh, mine, group=process_group)
         opened = []
-        for par in (0, 1):
+        for par in range(NBUF):
             row = []
             for r, h in enumerate(allh):
                 if r == rank:

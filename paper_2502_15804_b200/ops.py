@@ -63,7 +63,7 @@ def _decode(q, cache: LayerCache, ws: DecodeWorkspace | None, sm_scale, out_bf16
     scale = 1.0 / math.sqrt(HEAD_DIM) if sm_scale is None else sm_scale
     _native.check(_lib.fkv_decode(
         q.data_ptr(), cache.k.data_ptr(), cache.v.data_ptr(), cache.work.data_ptr(), cache.work_k,
-        cache.n_workers, cache.n_items, cache.group, cache.flags, scale, ws.part.data_ptr(),
+        cache.n_workers, cache.n_items, cache.group, cache.launch_flags, scale, ws.part.data_ptr(),
         cache.counters.data_ptr(), _p(out_bf16), _p(out_rec), _p(out_lse), _stream()))
     return ws.part
 
@@ -99,7 +99,7 @@ def decode_exchange(q: torch.Tensor, cache: LayerCache, endpoint, parity: int,
     flags = (C.c_void_p * len(endpoint.peer_flags))(*endpoint.peer_flags)
     _native.check(_lib.fkv_decode_exchange(
         q.data_ptr(), cache.k.data_ptr(), cache.v.data_ptr(), cache.work.data_ptr(), cache.work_k,
-        cache.n_workers, cache.n_items, cache.group, cache.flags, scale, ws.part.data_ptr(),
+        cache.n_workers, cache.n_items, cache.group, cache.launch_flags, scale, ws.part.data_ptr(),
         cache.counters.data_ptr(), None, recs, len(dests), None, endpoint.sig_done, flags,
         len(endpoint.peer_flags), endpoint.rank, _stream()))
 
@@ -152,6 +152,7 @@ def append(cache: LayerCache, k_new: torch.Tensor, v_new: torch.Tensor):
             or not (k_new.is_contiguous() and v_new.is_contiguous()):
         raise NativeError("k_new / v_new must be contiguous bf16 [..., 128] of one shape")
     h = cache.host
+    h["written"] = True
     _native.check(_lib.fkv_append(k_new.data_ptr(), v_new.data_ptr(), h["append_src_t"].data_ptr(),
                                   cache.seg_row0.data_ptr(), cache.seg_len.data_ptr(),
                                   h["seg_cap_t"].data_ptr(), cache.work.data_ptr(),
@@ -295,6 +296,7 @@ def compact_into(cache: LayerCache, k: torch.Tensor, v: torch.Tensor, offsets: t
                  seg_hi: torch.Tensor, max_tokens: int):
     """K3 alone into an existing cache (device int32 segment tables; one launch)."""
     _need_cuda(k, v, offsets, idx, seg_bh, seg_lo, seg_hi)
+    cache.host["written"] = True
     _native.check(_lib.fkv_compact(k.data_ptr(), v.data_ptr(), k.shape[2], int(seg_bh.shape[0]),
                                    offsets.data_ptr(), idx.data_ptr(), seg_bh.data_ptr(),
                                    seg_lo.data_ptr(), seg_hi.data_ptr(), cache.seg_row0.data_ptr(),

@@ -1,11 +1,16 @@
 """Compression path parity on the GPU (K1 score, A18 budgets, K2 select, K3
 compact) against the float64 oracle (oracle/kv.py).
 
-Tolerances: scores (fp32 from bf16 operands, tcgen05 fp32 accumulation,
-ex2.approx) within rtol 2e-2 of the oracle, measured against the row maximum.
+Tolerances: scores are fp32 (bf16 operands, tcgen05 fp32 accumulation,
+ex2.approx): elementwise |s - ref| <= 1e-4 |ref| + 1e-6 max_t |ref| (north_star
+fp32 rtol 1e-4; the atol floor is for scores many orders below their row's
+peak, where the flush-to-zero exponential underflows).  Long contexts (32k,
+128k) are checked on sampled heads against the float64 oracle.
 Budgets, offsets, selected indices and compacted rows are BIT-EXACT functions
 of the score tensor: the oracle is fed the GPU's own fp32 scores (exact in
-float64), so any mismatch is a selection/tie-rule bug, not rounding.
+float64), so any mismatch is a selection/tie-rule bug, not rounding; and
+end to end (GPU scores vs oracle scores) on inputs whose every selection
+boundary is separated by more than the score tolerance.
 """
 
 import numpy as np
@@ -15,6 +20,26 @@ import torch
 from oracle import kv as okv
 
 pytestmark = pytest.mark.gpu
+
+S_RTOL, S_ATOL_ROW = 1e-4, 1e-6
+
+
+def check_scores(s, ref):
+    """Elementwise score tolerance; returns the worst |err| / allowed."""
+    s, ref = np.asarray(s, np.float64), np.asarray(ref, np.float64)
+    assert s.shape == ref.shape
+    allowed = S_RTOL * np.abs(ref) + S_ATOL_ROW * np.abs(ref).max(axis=-1, keepdims=True)
+    worst = float((np.abs(s - ref) / allowed).max())
+    assert worst <= 1.0, f"score error {worst:.3g} x the tolerance"
+    return worst
+
+
+def sampled_head_scores(qn, kn, heads):
+    """float64 oracle scores of the listed (b, h) only: [len(heads), T-w]."""
+    hq, hkv = qn.shape[1], kn.shape[1]
+    G = hq // hkv
+    return np.stack([okv.snapkv_scores(qn[b:b + 1, h * G:(h + 1) * G], kn[b:b + 1, h:h + 1])[0, 0]
+                     for b, h in heads])
 
 
 def _inputs(bt, hq, hkv, T, w, seed, dev, temp=1.0):
@@ -33,12 +58,27 @@ def test_score_matches_oracle(cuda_device, bt, hq, hkv, T):
     from paper_2502_15804_b200 import ops
     q, k, _, qn, kn, _ = _inputs(bt, hq, hkv, T, 32, 1, cuda_device, temp=2.0)
     s = ops.score(q, k).cpu().double().numpy()
-    ref = okv.snapkv_scores(qn, kn)
-    assert s.shape == ref.shape
-    err = np.abs(s - ref).max(axis=-1) / np.abs(ref).max(axis=-1)
-    assert err.max() < 2e-2, err.max()
-    rel = np.abs(s - ref) / np.maximum(np.abs(ref), 1e-3 * np.abs(ref).max(axis=-1, keepdims=True))
-    assert np.median(rel) < 5e-3
+    print(f"score error {check_scores(s, okv.snapkv_scores(qn, kn)):.3g} x tolerance")
+
+
+@pytest.mark.parametrize("bt,hq,T,fused", [(1, 64, 32768, True), (1, 64, 131072, True), (2, 64, 32768, False),
+                                           (1, 32, 131072, False)])
+def test_score_long_context_sampled(cuda_device, bt, hq, T, fused):
+    """cfg4 (32k) and cfg5 (128k): many key chunks per head and the
+    multi-chunk softmax-statistics combine, checked elementwise on sampled
+    heads against the float64 oracle (both the score-only and the fused
+    score+select launch)."""
+    from paper_2502_15804_b200 import ops
+    q, k, _, qn, kn, _ = _inputs(bt, hq, 8, T, 32, 17, cuda_device, temp=2.0)
+    if fused:
+        s = ops.score_select(q, k, 1024, 32)[0]
+    else:
+        s = ops.score(q, k)
+    s = s.cpu().double().numpy()
+    heads = [(0, 0), (bt - 1, 5)]
+    ref = sampled_head_scores(qn, kn, heads)
+    got = np.stack([s[b, h] for b, h in heads])
+    print(f"T={T}: score error {check_scores(got, ref):.3g} x tolerance")
 
 
 def _gpu_select(sc, budget, w, alpha=0.2):
@@ -138,8 +178,8 @@ def test_compress_then_decode_end_to_end(cuda_device):
     ks = [kn[b, h, idx[off[b * hkv + h]:off[b * hkv + h + 1]]] for b in range(bt) for h in range(hkv)]
     vs = [vn[b, h, idx[off[b * hkv + h]:off[b * hkv + h + 1]]] for b in range(bt) for h in range(hkv)]
     o_ref, lse_ref = okv.decode_heads(qd.double().numpy(), ks, vs, G)
-    torch.testing.assert_close(o.float().cpu().double(), torch.from_numpy(o_ref), rtol=2e-2, atol=1e-2)
-    torch.testing.assert_close(lse.cpu().double(), torch.from_numpy(lse_ref), rtol=0, atol=2e-3)
+    torch.testing.assert_close(o.float().cpu().double(), torch.from_numpy(o_ref), rtol=2e-2, atol=1e-3)
+    torch.testing.assert_close(lse.cpu().double(), torch.from_numpy(lse_ref), rtol=1e-4, atol=1e-5)
 
 
 def test_selection_agreement_with_oracle_scores(cuda_device):
@@ -228,9 +268,10 @@ def test_fused_score_select_bit_exact(cuda_device, bt, hq, hkv, T, budget, temp,
     torch.cuda.synchronize()
     s64 = sc.cpu().double().numpy()
     if T <= 6000:
-        ref_s = okv.snapkv_scores(qn, kn)
-        err = np.abs(s64 - ref_s).max(axis=-1) / np.abs(ref_s).max(axis=-1)
-        assert err.max() < 2e-2, err.max()
+        check_scores(s64, okv.snapkv_scores(qn, kn))
+    else:
+        heads = [(0, 0), (bt - 1, 3 if flat_head else 6)]
+        check_scores(np.stack([s64[b, h] for b, h in heads]), sampled_head_scores(qn, kn, heads))
     ref_b = okv.ada_budgets(s64, budget, 32, 0.2)
     np.testing.assert_array_equal(hb.cpu().numpy(), ref_b)
     if flat_head:

@@ -36,7 +36,7 @@ def _setup(tp, mode, dev, L=3, bt=4, B=256):
 @pytest.mark.parametrize("tp,mode", [(2, "sha"), (2, "dp"), (4, "dp"), (8, "free")])
 def test_loopback_exchange_matches_single_gpu(cuda_device, tp, mode):
     from paper_2502_15804_b200 import ops
-    from paper_2502_15804_b200.exchange import P2PGroup
+    from paper_2502_15804_b200.exchange import P2PGroup, exchange_buffer
     base, per_rank, finals, bt, hq, G = _setup(tp, mode, cuda_device)
     L = len(base)
     slots = max(f.slots for f in finals)
@@ -49,10 +49,10 @@ def test_loopback_exchange_matches_single_gpu(cuda_device, tp, mode):
     def step():
         for l in range(L):
             for r in range(tp):
-                ops.decode_exchange(q[l], per_rank[r][l], grp.endpoints[r], l & 1)
+                ops.decode_exchange(q[l], per_rank[r][l], grp.endpoints[r], exchange_buffer(l, L))
             for r in range(tp):
                 ptr, src, row = tabs[l]
-                ops.merge_wait(grp.endpoints[r], l & 1, ptr, src, row, G, out_bf16=outs[r, l])
+                ops.merge_wait(grp.endpoints[r], exchange_buffer(l, L), ptr, src, row, G, out_bf16=outs[r, l])
 
     step()
     torch.cuda.synchronize()
@@ -88,7 +88,7 @@ def test_sharded_append_then_exchange(cuda_device, tp, mode):
     from paper_2502_15804_b200 import ops
     from paper_2502_15804_b200.cache import LayerCache
     from paper_2502_15804_b200.decoder import rank_caches
-    from paper_2502_15804_b200.exchange import P2PGroup
+    from paper_2502_15804_b200.exchange import P2PGroup, exchange_buffer
     from paper_2502_15804_b200.sharding import budgets_profile, plan_layouts, synthetic_budgets
     G, hkv, L, bt, B = 8, 8, 2, 4, 256
     hq = G * hkv
@@ -114,10 +114,10 @@ def test_sharded_append_then_exchange(cuda_device, tp, mode):
                 ops.append(per_rank[r][l], kn, vn)  # owning copies only
             ops.append(base[l], kn, vn)  # writes the same rows again; grows the TP=1 view
             for r in range(tp):
-                ops.decode_exchange(q[l], per_rank[r][l], grp.endpoints[r], l & 1)
+                ops.decode_exchange(q[l], per_rank[r][l], grp.endpoints[r], exchange_buffer(l, L))
             for r in range(tp):
                 ptr, src, row = tabs[l]
-                ops.merge_wait(grp.endpoints[r], l & 1, ptr, src, row, G, out_bf16=out[r, l])
+                ops.merge_wait(grp.endpoints[r], exchange_buffer(l, L), ptr, src, row, G, out_bf16=out[r, l])
         torch.cuda.synchronize()
         ref = torch.stack([ops.decode(q[l], base[l])[0] for l in range(L)])
         for r in range(tp):
