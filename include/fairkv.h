@@ -139,18 +139,29 @@ typedef struct fkv_work {
  * the wait. */
 #define FKV_DECODE_AFTER_WAIT 4
 
+/* Exchange records (the per-layer all-gather payload; "XREC"): a block of
+ * `slots` rows of `group` heads =
+ *     bf16 o[slots * group][128]   (256 bytes per head row)
+ *     f32  lse[slots * group]
+ * FKV_XREC_BYTES(slots, group) bytes.  Segment s of a rank writes rows
+ * out_row .. out_row + group - 1 (out_row = s * group) of its block; in a
+ * receive area rank r's block starts at r * FKV_XREC_BYTES. */
+#define FKV_XREC_BYTES(slots, group) ((int64_t)(slots) * (group) * (FKV_HEAD_DIM * 2 + 4))
+
 /*   q            bf16 [*, 128]   query rows
  *   k, v         bf16 [rows,128] swizzled cache rows (layout above)
  *   work         fkv_work_t [n_workers][work_k], 1 <= work_k <= FKV_MAX_WORK
- *   part         f32 [n_items, group, FKV_REC]  partial records: softmax-normalised
- *                o[128] and lse = natural-log sum-exp of the scaled scores
+ *   part         f32 [n_items, group, FKV_REC]  partial records of split
+ *                segments: softmax-normalised o[128] and lse = natural-log
+ *                sum-exp of the scaled scores
  *   counters     int32 [n_items] arrival counters, zero on entry; left zero on exit
- * With all of out_bf16 / out_rec / out_lse NULL every piece just writes its
+ * With all of out_bf16 / out_xrec / out_lse NULL every piece just writes its
  * partial record (split-K partials).  Otherwise a single-piece segment writes
  * its rows directly and the last warp to finish a piece of a split segment
  * merges the segment's records by log-sum-exp; both write rows out_row + h
- * (h < group) of out_bf16 (bf16 [*,128]), out_rec (f32 [*,FKV_REC]) and/or
- * out_lse (f32 [*]) -- one launch per layer.
+ * (h < group) of out_bf16 (bf16 [*,128]), the exchange block out_xrec
+ * (XREC layout, xrec_slots rows of `group` heads) and/or out_lse (f32 [*]),
+ * with 16-byte stores -- one launch per layer.  Outputs 16-byte aligned.
  * group (= Hq/Hkv) must be 4 or 8; softmax scale = sm_scale.
  * Nothing in the reference is replaced (it has no decode); its cost model of
  * this kernel is reference latency.py:85-91 (predict_compute). */
@@ -160,41 +171,43 @@ int fkv_decode_ctas_per_sm(int32_t flags);
 
 int fkv_decode(const void* q, const void* k, const void* v, const fkv_work_t* work,
                int32_t work_k, int32_t n_workers, int32_t n_items, int32_t group, int32_t flags,
-               float sm_scale, float* part, int32_t* counters, void* out_bf16, float* out_rec,
-               float* out_lse, void* stream);
+               float sm_scale, float* part, int32_t* counters, void* out_bf16, void* out_xrec,
+               int32_t xrec_slots, float* out_lse, void* stream);
 
-/* K5: log-sum-exp merge of partial records.  Output group g merges records
- * src_idx[grp_ptr[g] .. grp_ptr[g+1]) (each `group` heads of FKV_REC floats)
- * and writes, for heads h < group, row out_row[g] + h of any of:
- *   out_bf16 bf16 [*,128] normalised o;  out_rec f32 [*,FKV_REC] record;
- *   out_lse f32 [*] merged lse.
- * Used for chunk->segment, segment->send-slot, and (after the all-gather)
- * DP-copy->head merges.  The all-gather itself stands in for the reference's
- * modeled allreduce (reference latency.py:94-101, simulate.py:132-133). */
-int fkv_merge_lse(const float* part, const int32_t* grp_ptr, const int32_t* src_idx,
-                  const int32_t* out_row, int32_t n_groups, int32_t group, void* out_bf16,
-                  float* out_rec, float* out_lse, void* stream);
+/* K5: log-sum-exp merge of exchange records.  xrec = blocks of xrec_slots
+ * rows (block r at r * FKV_XREC_BYTES(xrec_slots, group)); record index
+ * i = r * xrec_slots + slot.  Output group g merges the records
+ * src_idx[grp_ptr[g] .. grp_ptr[g+1]) and writes, for heads h < group, row
+ * out_row[g] + h of out_bf16 (bf16 [*,128]) and/or out_lse (f32 [*]).
+ * This is the DP-copy -> head merge after the all-gather; the all-gather
+ * stands in for the reference's modeled allreduce (reference
+ * latency.py:94-101, simulate.py:132-133). */
+int fkv_merge_lse(const void* xrec, int32_t xrec_slots, const int32_t* grp_ptr,
+                  const int32_t* src_idx, const int32_t* out_row, int32_t n_groups, int32_t group,
+                  void* out_bf16, float* out_lse, void* stream);
 
 /* Fused NVLink all-gather variant of fkv_decode (same work table).  Every
  * segment's final record is written to all n_rec destinations (each peer's
- * receive block for this rank, mapped with fkv_ipc_open; P2P stores over
- * NVLink) instead of one local slot array, and when the last warp finishes,
- * after a system-scope fence, it atomically increments sig_flags[j][my_rank]
- * in every peer's memory (n_sig peers).  sig_done: local int32, zero between
- * launches.  Replaces NCCL all_gather for the per-layer exchange. */
+ * receive block for this rank, mapped with fkv_ipc_open; 16-byte P2P stores
+ * over NVLink, bf16 o + f32 lse) instead of one local block, and when the
+ * last CTA finishes, after a system-scope fence, it atomically increments
+ * sig_flags[j][my_rank] in every peer's memory (n_sig peers).  sig_done:
+ * local int32, zero between launches.  Replaces NCCL all_gather for the
+ * per-layer exchange. */
 int fkv_decode_exchange(const void* q, const void* k, const void* v, const fkv_work_t* work,
                         int32_t work_k, int32_t n_workers, int32_t n_items, int32_t group,
                         int32_t flags, float sm_scale, float* part, int32_t* counters, void* out_bf16,
-                        float* const* out_recs, int32_t n_rec, float* out_lse, int32_t* sig_done,
-                        int32_t* const* sig_flags, int32_t n_sig, int32_t my_rank, void* stream);
+                        void* const* out_xrecs, int32_t n_rec, int32_t xrec_slots, float* out_lse,
+                        int32_t* sig_done, int32_t* const* sig_flags, int32_t n_sig, int32_t my_rank,
+                        void* stream);
 
 /* fkv_merge_lse preceded by the consumer side of the fused all-gather: every
  * CTA waits (acquire, system scope) until flags[r] >= consumed[0] + 1 for all
  * r < tp, merges, and the last CTA advances consumed[0] (consumed[1] is its
  * arrival counter, zero between launches).  flags == NULL: plain merge. */
-int fkv_merge_wait(const float* part, const int32_t* grp_ptr, const int32_t* src_idx,
-                   const int32_t* out_row, int32_t n_groups, int32_t group, void* out_bf16,
-                   float* out_rec, float* out_lse, const int32_t* flags, int32_t tp,
+int fkv_merge_wait(const void* xrec, int32_t xrec_slots, const int32_t* grp_ptr,
+                   const int32_t* src_idx, const int32_t* out_row, int32_t n_groups, int32_t group,
+                   void* out_bf16, float* out_lse, const int32_t* flags, int32_t tp,
                    int32_t* consumed, void* stream);
 
 /* Device memory that can be shared with the other GPUs of the node. */

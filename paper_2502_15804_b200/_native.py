@@ -58,11 +58,11 @@ _SIGS = {
                                     _vp, _vp, _vp, _vp, _vp]),
     "fkv_decode_ctas_per_sm": (C.c_int, [_i32]),
     "fkv_decode": (C.c_int, [_vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _f32, _vp, _vp,
-                             _vp, _vp, _vp, _vp]),
-    "fkv_merge_lse": (C.c_int, [_vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp]),
+                             _vp, _vp, _i32, _vp, _vp]),
+    "fkv_merge_lse": (C.c_int, [_vp, _i32, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp]),
     "fkv_decode_exchange": (C.c_int, [_vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _f32,
-                                      _vp, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _i32, _i32, _vp]),
-    "fkv_merge_wait": (C.c_int, [_vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _i32, _vp,
+                                      _vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _i32, _i32, _vp]),
+    "fkv_merge_wait": (C.c_int, [_vp, _i32, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _i32, _vp,
                                  _vp]),
     "fkv_dev_alloc": (C.c_int, [_i64, _vp]),
     "fkv_dev_free": (C.c_int, [_vp]),

@@ -70,8 +70,11 @@ struct DecodeParams {
   float* part;        // [n_items, G, FKV_REC] partial records (multi-piece segments)
   int32_t* counters;  // [n_items] arrival counter at each segment's first piece; zero between launches
   __nv_bfloat16* out_bf16;
-  float* out_rec[FKV_MAX_PEERS];  // record destinations: local slots, or every peer's
-  int n_rec;                      // receive block for this rank (fused NVLink all-gather)
+  // exchange-record destinations (FKV_XREC layout): a local send block, or
+  // this rank's block in every peer's receive area (fused NVLink all-gather)
+  uint8_t* out_rec[FKV_MAX_PEERS];
+  int n_rec;
+  int64_t rec_lse_off;  // bytes from a block's start to its lse array
   float* out_lse;
   int32_t* sig_done;              // CTAs-finished counter (local), zero between launches
   int32_t* sig_flag[FKV_MAX_PEERS];  // per peer: flags[tp] in that peer's memory
@@ -88,14 +91,79 @@ struct __align__(16) DecodeShared {
   int32_t fin_i0, fin_n_it, fin_orow;  // deferred merge of the CTA's last piece (n_it 0 = none)
 };
 
-__device__ __forceinline__ void put_rec(const DecodeParams& p, int64_t idx, float v) {
+// ---- segment outputs: o rows (bf16, 16-byte stores) and lse, to the local
+// outputs and every exchange-record destination.  Row r of a record block is
+// at r * 256 bytes, its lse at rec_lse_off + 4 r (include/fairkv.h FKV_XREC).
+__device__ __forceinline__ void store_o16(const DecodeParams& p, int64_t row, int col, int4 v) {
+  if (p.out_bf16) *reinterpret_cast<int4*>(p.out_bf16 + row * FKV_HEAD_DIM + col) = v;
 #pragma unroll 1
-  for (int j = 0; j < p.n_rec; ++j) p.out_rec[j][idx] = v;
+  for (int j = 0; j < p.n_rec; ++j)
+    *reinterpret_cast<int4*>(p.out_rec[j] + (row * FKV_HEAD_DIM + col) * 2) = v;
+}
+__device__ __forceinline__ void store_lse1(const DecodeParams& p, int64_t row, float l) {
+  if (p.out_lse) p.out_lse[row] = l;
+#pragma unroll 1
+  for (int j = 0; j < p.n_rec; ++j) reinterpret_cast<float*>(p.out_rec[j] + p.rec_lse_off)[row] = l;
+}
+__device__ __forceinline__ void store_lse4(const DecodeParams& p, int64_t row, float4 l) {
+  if (p.out_lse) *reinterpret_cast<float4*>(p.out_lse + row) = l;
+#pragma unroll 1
+  for (int j = 0; j < p.n_rec; ++j)
+    *reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out_rec[j] + p.rec_lse_off) + row) = l;
 }
 
-__device__ __forceinline__ void put_rec4(const DecodeParams& p, int64_t row, int lane, float4 v) {
-#pragma unroll 1
-  for (int j = 0; j < p.n_rec; ++j) reinterpret_cast<float4*>(p.out_rec[j] + row * FKV_REC)[lane] = v;
+__device__ __forceinline__ uint2 pack_bf16x4(float4 v) {
+  return make_uint2(pack_bf16x2(v.x, v.y), pack_bf16x2(v.z, v.w));
+}
+
+// One head row held as a float4 of columns 4*lane .. +3 by every lane:
+// neighbouring lanes pair up so even lanes store 16 bytes (8 columns).
+__device__ __forceinline__ void emit_row_lanes(const DecodeParams& p, int64_t row, float4 o, int lane) {
+  const uint2 w = pack_bf16x4(o);
+  const uint32_t hx = __shfl_down_sync(0xffffffffu, w.x, 1), hy = __shfl_down_sync(0xffffffffu, w.y, 1);
+  if ((lane & 1) == 0) store_o16(p, row, 4 * lane, make_int4(w.x, w.y, hx, hy));
+}
+
+// lse of heads 0..G-1 held by lanes 0..G-1 -> float4 stores by lanes 0 (and 1).
+template <int G>
+__device__ __forceinline__ void emit_lse_lanes(const DecodeParams& p, int64_t row, float l, int lane) {
+  const int b = 4 * (lane & 1);
+  const float a0 = __shfl_sync(0xffffffffu, l, b), a1 = __shfl_sync(0xffffffffu, l, b + 1);
+  const float a2 = __shfl_sync(0xffffffffu, l, b + 2), a3 = __shfl_sync(0xffffffffu, l, b + 3);
+  if (lane < G / 4) store_lse4(p, row + b, make_float4(a0, a1, a2, a3));
+}
+
+// The finalised o of one whole segment, in the mma accumulator layout
+// (acc[dt][e]: column 16 dt + (lane >> 2) (+8 for e >= 2) of head
+// 2 (lane & 3) (+1 for odd e); inv = 1 / softmax denominator per head) ->
+// G rows of bf16 with 16-byte stores.  movmatrix turns each 8-column block
+// into "lane L holds 2 columns of head L >> 2"; a 4x4 word transpose among
+// the 4 lanes of a head then gives every lane 8 consecutive columns.
+template <int G>
+__device__ __forceinline__ void emit_acc(const DecodeParams& p, int64_t orow, const float (&acc)[8][4],
+                                         float inv0, float inv1, int lane) {
+  uint32_t t[16];  // t[c]: this lane's word of 8-column chunk c of head lane >> 2
+#pragma unroll
+  for (int dt = 0; dt < 8; ++dt) {
+    t[2 * dt] = movmatrix_trans(pack_bf16x2(acc[dt][0] * inv0, acc[dt][1] * inv1));
+    t[2 * dt + 1] = movmatrix_trans(pack_bf16x2(acc[dt][2] * inv0, acc[dt][3] * inv1));
+  }
+  const int j = lane & 3, h = lane >> 2;
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {  // chunks 4m .. 4m+3: lane j collects chunk 4m + j
+    uint32_t w[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int si = (j - r) & 3;  // send my word of chunk 4m + si to lane (j - r) & 3
+      const uint32_t send = si == 0 ? t[4 * m] : si == 1 ? t[4 * m + 1] : si == 2 ? t[4 * m + 2] : t[4 * m + 3];
+      const uint32_t got = __shfl_sync(0xffffffffu, send, (lane & ~3) | ((j + r) & 3));
+      const int k = (j + r) & 3;  // ... and receive word k (= source lane) of chunk 4m + j
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+        if (k == x) w[x] = got;
+    }
+    if (h < G) store_o16(p, orow + h, 8 * (4 * m + j), make_int4(w[0], w[1], w[2], w[3]));
+  }
 }
 
 __device__ __forceinline__ int atom_add_acq_rel(int32_t* addr, int v) {
@@ -480,41 +548,12 @@ __global__ void __launch_bounds__(Shape<MODE>::W * 32, Shape<MODE>::kCtasPerSm)
     const int64_t orow = d.out_row;
 
     if (fused && n_it == 1) {
-      // whole segment in one piece: registers -> output rows
-#pragma unroll
-      for (int dt = 0; dt < 8; ++dt) {
-        const int d0 = 16 * dt + dr;
-        if (h0 < G) {
-          if (p.out_bf16) {
-            p.out_bf16[(orow + h0) * FKV_HEAD_DIM + d0] = __float2bfloat16_rn(acc[dt][0] * inv0);
-            p.out_bf16[(orow + h0) * FKV_HEAD_DIM + d0 + 8] = __float2bfloat16_rn(acc[dt][2] * inv0);
-          }
-          if (p.n_rec) {
-            put_rec(p, (orow + h0) * FKV_REC + d0, acc[dt][0] * inv0);
-            put_rec(p, (orow + h0) * FKV_REC + d0 + 8, acc[dt][2] * inv0);
-          }
-        }
-        if (h1 < G) {
-          if (p.out_bf16) {
-            p.out_bf16[(orow + h1) * FKV_HEAD_DIM + d0] = __float2bfloat16_rn(acc[dt][1] * inv1);
-            p.out_bf16[(orow + h1) * FKV_HEAD_DIM + d0 + 8] = __float2bfloat16_rn(acc[dt][3] * inv1);
-          }
-          if (p.n_rec) {
-            put_rec(p, (orow + h1) * FKV_REC + d0, acc[dt][1] * inv1);
-            put_rec(p, (orow + h1) * FKV_REC + d0 + 8, acc[dt][3] * inv1);
-          }
-        }
-      }
-      if (lane < 4) {
-        if (h0 < G) {
-          if (p.n_rec) put_rec(p, (orow + h0) * FKV_REC + FKV_HEAD_DIM, lse0);
-          if (p.out_lse) p.out_lse[orow + h0] = lse0;
-        }
-        if (h1 < G) {
-          if (p.n_rec) put_rec(p, (orow + h1) * FKV_REC + FKV_HEAD_DIM, lse1);
-          if (p.out_lse) p.out_lse[orow + h1] = lse1;
-        }
-      }
+      // whole segment in one piece: registers -> output rows (16-byte stores)
+      emit_acc<G>(p, orow, acc, inv0, inv1, lane);
+      // lse of head g is lse0 / lse1 of lane g >> 1 (lanes 0..3)
+      const float la = __shfl_sync(0xffffffffu, lse0, (lane >> 1) & 3);
+      const float lb = __shfl_sync(0xffffffffu, lse1, (lane >> 1) & 3);
+      emit_lse_lanes<G>(p, orow, (lane & 1) ? lb : la, lane);
       continue;
     }
 
@@ -595,19 +634,8 @@ __global__ void __launch_bounds__(Shape<MODE>::W * 32, Shape<MODE>::kCtasPerSm)
     }
     stamp(PROBE, 10);
 #pragma unroll
-    for (int g = 0; g < G; ++g) {
-      const int64_t row = orow + g;
-      if (p.out_bf16) {
-        __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(p.out_bf16 + row * FKV_HEAD_DIM) + 2 * lane;
-        ob[0] = __floats2bfloat162_rn(o[g].x, o[g].y);
-        ob[1] = __floats2bfloat162_rn(o[g].z, o[g].w);
-      }
-      if (p.n_rec) put_rec4(p, row, lane, o[g]);
-    }
-    if (lane < G) {
-      if (p.n_rec) put_rec(p, (orow + lane) * FKV_REC + FKV_HEAD_DIM, lse_g);
-      if (p.out_lse) p.out_lse[orow + lane] = lse_g;
-    }
+    for (int g = 0; g < G; ++g) emit_row_lanes(p, orow + g, o[g], lane);
+    emit_lse_lanes<G>(p, orow, lse_g, lane);
     if (lane == 0) p.counters[d.i0] = 0;  // ready for the next launch / graph replay
     stamp(PROBE, 11);
     __syncwarp();  // the scratch is reused by the next merge
@@ -660,16 +688,8 @@ __global__ void __launch_bounds__(Shape<MODE>::W * 32, Shape<MODE>::kCtasPerSm)
                __ldcg(reinterpret_cast<const float4*>(base + (i * G + g) * FKV_REC) + lane));
         const float lse_g = S > 0.f ? M + __logf(S) : -CUDART_INF_F;
         const int64_t row = orow + g;
-        if (p.out_bf16) {
-          __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(p.out_bf16 + row * FKV_HEAD_DIM) + 2 * lane;
-          ob[0] = __floats2bfloat162_rn(o.x, o.y);
-          ob[1] = __floats2bfloat162_rn(o.z, o.w);
-        }
-        if (p.n_rec) put_rec4(p, row, lane, o);
-        if (lane == 0) {
-          if (p.n_rec) put_rec(p, row * FKV_REC + FKV_HEAD_DIM, lse_g);
-          if (p.out_lse) p.out_lse[row] = lse_g;
-        }
+        emit_row_lanes(p, row, o, lane);
+        if (lane == 0) store_lse1(p, row, lse_g);
       }
       if (threadIdx.x == 0) p.counters[sh.fin_i0] = 0;
     }
@@ -694,17 +714,18 @@ __global__ void __launch_bounds__(Shape<MODE>::W * 32, Shape<MODE>::kCtasPerSm)
 }
 
 // K5 standalone (after the all-gather): warp g of the CTA merges head g of
-// one output group in a single online-LSE pass; lane = 4 head_dim columns.
+// one output group in a single online-LSE pass over exchange records
+// (FKV_XREC blocks of `slots` rows, block r at r * block_bytes); lane = 4
+// head_dim columns.
 template <int G>
 __global__ void __launch_bounds__(G * 32)
-    merge_lse_kernel(const float* __restrict__ part, const int32_t* __restrict__ grp_ptr,
-                     const int32_t* __restrict__ src_idx, const int32_t* __restrict__ out_row,
-                     __nv_bfloat16* __restrict__ out_bf16, float* __restrict__ out_rec,
-                     float* __restrict__ out_lse, const int32_t* flags, int tp,
-                     int32_t* consumed) {
+    merge_lse_kernel(const uint8_t* __restrict__ xrec, int slots, int64_t block_bytes,
+                     const int32_t* __restrict__ grp_ptr, const int32_t* __restrict__ src_idx,
+                     const int32_t* __restrict__ out_row, __nv_bfloat16* __restrict__ out_bf16,
+                     float* __restrict__ out_lse, const int32_t* flags, int tp, int32_t* consumed) {
   // Programmatic dependent launch (plain merges only, see fkv_merge_wait):
   // the records are complete once the producer grid (NCCL all-gather, K4
-  // partials) is.
+  // records) is.
   if (!flags) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;");
@@ -730,20 +751,25 @@ __global__ void __launch_bounds__(G * 32)
   const int grp = blockIdx.x;
   const int g = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int i0 = grp_ptr[grp], i1 = grp_ptr[grp + 1];
+  const int64_t lse_off = static_cast<int64_t>(slots) * G * FKV_HEAD_DIM * 2;
   float m = -CUDART_INF_F, S = 0.f;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int i = i0; i < i1; ++i) {
-    const float* rec = part + (static_cast<int64_t>(src_idx[i]) * G + g) * FKV_REC;
-    const float l = rec[FKV_HEAD_DIM];
+    const int src = src_idx[i];
+    const uint8_t* blk = xrec + static_cast<int64_t>(src / slots) * block_bytes;
+    const int64_t row = static_cast<int64_t>(src % slots) * G + g;
+    const float l = __ldcg(reinterpret_cast<const float*>(blk + lse_off) + row);
     if (l == -CUDART_INF_F) continue;
-    const float4 o = reinterpret_cast<const float4*>(rec)[lane];
+    const uint2 w = __ldcg(reinterpret_cast<const uint2*>(blk + row * FKV_HEAD_DIM * 2) + lane);
+    const float2 o01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w.x));
+    const float2 o23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w.y));
     const float nm = fmaxf(m, l);
     const float a = __expf(m - nm), b = __expf(l - nm);
     S = S * a + b;
-    acc.x = acc.x * a + o.x * b;
-    acc.y = acc.y * a + o.y * b;
-    acc.z = acc.z * a + o.z * b;
-    acc.w = acc.w * a + o.w * b;
+    acc.x = acc.x * a + o01.x * b;
+    acc.y = acc.y * a + o01.y * b;
+    acc.z = acc.z * a + o23.x * b;
+    acc.w = acc.w * a + o23.y * b;
     m = nm;
   }
   const float inv = S > 0.f ? 1.f / S : 0.f;
@@ -757,10 +783,6 @@ __global__ void __launch_bounds__(G * 32)
     __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(out_bf16 + row * FKV_HEAD_DIM) + 2 * lane;
     ob[0] = __floats2bfloat162_rn(acc.x, acc.y);
     ob[1] = __floats2bfloat162_rn(acc.z, acc.w);
-  }
-  if (out_rec) {
-    reinterpret_cast<float4*>(out_rec + row * FKV_REC)[lane] = acc;
-    if (lane == 0) out_rec[row * FKV_REC + FKV_HEAD_DIM] = lse;
   }
   if (out_lse && lane == 0) out_lse[row] = lse;
   if (flags) {
@@ -848,33 +870,38 @@ extern "C" int fkv__decode_stamps(unsigned long long* host, int32_t n) {
 extern "C" int fkv_decode(const void* q, const void* k, const void* v, const fkv_work_t* work,
                           int32_t work_k, int32_t n_workers, int32_t n_items, int32_t group,
                           int32_t flags, float sm_scale, float* part, int32_t* counters,
-                          void* out_bf16, float* out_rec, float* out_lse, void* stream) {
+                          void* out_bf16, void* out_xrec, int32_t xrec_slots, float* out_lse,
+                          void* stream) {
   return fkv_decode_exchange(q, k, v, work, work_k, n_workers, n_items, group, flags, sm_scale, part,
-                             counters, out_bf16, out_rec ? &out_rec : nullptr, out_rec ? 1 : 0,
-                             out_lse, nullptr, nullptr, 0, 0, stream);
+                             counters, out_bf16, out_xrec ? &out_xrec : nullptr, out_xrec ? 1 : 0,
+                             xrec_slots, out_lse, nullptr, nullptr, 0, 0, stream);
 }
 
 extern "C" int fkv_decode_exchange(const void* q, const void* k, const void* v,
                                    const fkv_work_t* work, int32_t work_k, int32_t n_workers,
                                    int32_t n_items, int32_t group, int32_t flags, float sm_scale,
-                                   float* part,
-                                   int32_t* counters, void* out_bf16, float* const* out_recs,
-                                   int32_t n_rec, float* out_lse, int32_t* sig_done,
-                                   int32_t* const* sig_flags, int32_t n_sig, int32_t my_rank,
-                                   void* stream) {
+                                   float* part, int32_t* counters, void* out_bf16,
+                                   void* const* out_xrecs, int32_t n_rec, int32_t xrec_slots,
+                                   float* out_lse, int32_t* sig_done, int32_t* const* sig_flags,
+                                   int32_t n_sig, int32_t my_rank, void* stream) {
   using namespace fkv;
   if (n_items < 0 || n_workers < 0) return set_error(FKV_ERR_INVALID, "fkv_decode: negative size");
   if (work_k < 1 || work_k > FKV_MAX_WORK)
     return set_error(FKV_ERR_INVALID, "fkv_decode: work_k must be in [1, FKV_MAX_WORK]");
   if (n_rec < 0 || n_rec > FKV_MAX_PEERS || n_sig < 0 || n_sig > FKV_MAX_PEERS)
     return set_error(FKV_ERR_INVALID, "fkv_decode: too many record destinations / peers");
+  if (n_rec > 0 && xrec_slots < 1)
+    return set_error(FKV_ERR_INVALID, "fkv_decode: exchange records need xrec_slots >= 1");
   if (n_items == 0 || n_workers == 0) return FKV_OK;
-  if (!q || !k || !v || !work || !part || !counters || (n_rec && !out_recs) ||
+  if (!q || !k || !v || !work || !part || !counters || (n_rec && !out_xrecs) ||
       (n_sig && (!sig_done || !sig_flags)))
     return set_error(FKV_ERR_INVALID, "fkv_decode: null pointer");
-  if ((reinterpret_cast<uintptr_t>(k) | reinterpret_cast<uintptr_t>(v) |
-       reinterpret_cast<uintptr_t>(work)) & 15)
-    return set_error(FKV_ERR_INVALID, "fkv_decode: cache / work table not 16-byte aligned");
+  uintptr_t align = reinterpret_cast<uintptr_t>(k) | reinterpret_cast<uintptr_t>(v) |
+                    reinterpret_cast<uintptr_t>(work) | reinterpret_cast<uintptr_t>(out_bf16) |
+                    reinterpret_cast<uintptr_t>(out_lse);
+  for (int j = 0; j < n_rec; ++j) align |= reinterpret_cast<uintptr_t>(out_xrecs[j]);
+  if (align & 15)
+    return set_error(FKV_ERR_INVALID, "fkv_decode: cache / work table / outputs not 16-byte aligned");
   DecodeParams p{};
   p.q = static_cast<const __nv_bfloat16*>(q);
   p.k = static_cast<const __nv_bfloat16*>(k);
@@ -886,8 +913,9 @@ extern "C" int fkv_decode_exchange(const void* q, const void* k, const void* v,
   p.part = part;
   p.counters = counters;
   p.out_bf16 = static_cast<__nv_bfloat16*>(out_bf16);
-  for (int j = 0; j < n_rec; ++j) p.out_rec[j] = out_recs[j];
+  for (int j = 0; j < n_rec; ++j) p.out_rec[j] = static_cast<uint8_t*>(out_xrecs[j]);
   p.n_rec = n_rec;
+  p.rec_lse_off = static_cast<int64_t>(xrec_slots) * group * FKV_HEAD_DIM * 2;
   p.out_lse = out_lse;
   p.sig_done = sig_done;
   for (int j = 0; j < n_sig; ++j) p.sig_flag[j] = sig_flags[j];
@@ -899,26 +927,30 @@ extern "C" int fkv_decode_exchange(const void* q, const void* k, const void* v,
   return decode_entry(p, group, static_cast<cudaStream_t>(stream), probe, flags);
 }
 
-extern "C" int fkv_merge_lse(const float* part, const int32_t* grp_ptr, const int32_t* src_idx,
-                             const int32_t* out_row, int32_t n_groups, int32_t group,
-                             void* out_bf16, float* out_rec, float* out_lse, void* stream) {
-  return fkv_merge_wait(part, grp_ptr, src_idx, out_row, n_groups, group, out_bf16, out_rec,
+extern "C" int fkv_merge_lse(const void* xrec, int32_t xrec_slots, const int32_t* grp_ptr,
+                             const int32_t* src_idx, const int32_t* out_row, int32_t n_groups,
+                             int32_t group, void* out_bf16, float* out_lse, void* stream) {
+  return fkv_merge_wait(xrec, xrec_slots, grp_ptr, src_idx, out_row, n_groups, group, out_bf16,
                         out_lse, nullptr, 0, nullptr, stream);
 }
 
-extern "C" int fkv_merge_wait(const float* part, const int32_t* grp_ptr, const int32_t* src_idx,
-                              const int32_t* out_row, int32_t n_groups, int32_t group,
-                              void* out_bf16, float* out_rec, float* out_lse,
-                              const int32_t* flags, int32_t tp, int32_t* consumed, void* stream) {
+extern "C" int fkv_merge_wait(const void* xrec, int32_t xrec_slots, const int32_t* grp_ptr,
+                              const int32_t* src_idx, const int32_t* out_row, int32_t n_groups,
+                              int32_t group, void* out_bf16, float* out_lse, const int32_t* flags,
+                              int32_t tp, int32_t* consumed, void* stream) {
   using namespace fkv;
   if (flags && (!consumed || tp < 1 || tp > FKV_MAX_PEERS))
     return set_error(FKV_ERR_INVALID, "fkv_merge_wait: bad flags / consumed / tp");
-  if (n_groups < 0) return set_error(FKV_ERR_INVALID, "n_groups < 0");
+  if (n_groups < 0 || xrec_slots < 1) return set_error(FKV_ERR_INVALID, "fkv_merge_lse: bad sizes");
   if (n_groups == 0) return FKV_OK;
-  if (!part || !grp_ptr || !src_idx || !out_row || (!out_bf16 && !out_rec && !out_lse))
+  if (!xrec || !grp_ptr || !src_idx || !out_row || (!out_bf16 && !out_lse))
     return set_error(FKV_ERR_INVALID, "fkv_merge_lse: null pointer");
+  if (reinterpret_cast<uintptr_t>(xrec) & 15)
+    return set_error(FKV_ERR_INVALID, "fkv_merge_lse: records not 16-byte aligned");
   auto ob = static_cast<__nv_bfloat16*>(out_bf16);
+  auto xr = static_cast<const uint8_t*>(xrec);
   if (group != 4 && group != 8) return set_error(FKV_ERR_INVALID, "fkv_merge_lse: group must be 4 or 8");
+  const int64_t block = FKV_XREC_BYTES(xrec_slots, group);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(n_groups, 1, 1);
   cfg.blockDim = dim3(group * 32, 1, 1);
@@ -931,9 +963,9 @@ extern "C" int fkv_merge_wait(const float* part, const int32_t* grp_ptr, const i
   // waiting for peers while grids queued behind it need them.
   cfg.numAttrs = flags ? 0 : 1;
   const cudaError_t e =
-      group == 4 ? cudaLaunchKernelEx(&cfg, merge_lse_kernel<4>, part, grp_ptr, src_idx, out_row, ob,
-                                      out_rec, out_lse, flags, tp, consumed)
-                 : cudaLaunchKernelEx(&cfg, merge_lse_kernel<8>, part, grp_ptr, src_idx, out_row, ob,
-                                      out_rec, out_lse, flags, tp, consumed);
+      group == 4 ? cudaLaunchKernelEx(&cfg, merge_lse_kernel<4>, xr, xrec_slots, block, grp_ptr, src_idx,
+                                      out_row, ob, out_lse, flags, tp, consumed)
+                 : cudaLaunchKernelEx(&cfg, merge_lse_kernel<8>, xr, xrec_slots, block, grp_ptr, src_idx,
+                                      out_row, ob, out_lse, flags, tp, consumed);
   return cuda_check(e, "merge_lse launch");
 }

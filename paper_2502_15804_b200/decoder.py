@@ -82,8 +82,9 @@ class StackDecoder:
         self.send, self.recv, self.final = [], [], []
         if tp > 1:
             for c, f in zip(caches, finals):
-                self.send.append(torch.zeros((f.slots, group, ops.REC), dtype=torch.float32, device=dev))
-                self.recv.append(torch.zeros((tp * f.slots, group, ops.REC), dtype=torch.float32, device=dev))
+                if exchange != "p2p":  # NCCL: exchange-record send block + gathered blocks
+                    self.send.append(ops.xrec_empty(f.slots, group, dev)[0])
+                    self.recv.append(ops.xrec_empty(f.slots, group, dev, ranks=tp))
                 self.final.append(tuple(torch.as_tensor(x, device=dev) for x in (f.grp_ptr, f.src_idx, f.out_row)))
         self.kernel_launches_per_step = len(caches) * (2 if tp > 1 else 1)
 
@@ -99,14 +100,25 @@ class StackDecoder:
             ops.merge_wait(self.endpoint, buf, ptr, src, row, self.group, out_bf16=out,
                            out_lse=out_lse)
             return
-        ops.decode_into(q, c, self.ws[l], out_rec=self.send[l])
+        self.produce(l, q)
         self.exchange(l)
-        ptr, src, row = self.final[l]
-        ops.merge_lse(self.recv[l], ptr, src, row, self.group, out_bf16=out, out_lse=out_lse)
+        self.consume(l, out, out_lse)
+
+    # The NCCL path in its three stream-ordered parts (tests drive them in
+    # lockstep for several virtual ranks with a loopback all-gather).
+    def produce(self, l: int, q: torch.Tensor):
+        """K4 + fused segment merge -> this rank's exchange-record block."""
+        ops.decode_into(q, self.caches[l], self.ws[l], out_rec=self.send[l])
 
     def exchange(self, l: int):
+        """All-gather of the blocks: recv[l][r] = rank r's send block."""
         import torch.distributed as dist
-        dist.all_gather_into_tensor(self.recv[l], self.send[l], group=self.pg)
+        dist.all_gather_into_tensor(self.recv[l].view(-1), self.send[l], group=self.pg)
+
+    def consume(self, l: int, out: torch.Tensor, out_lse: torch.Tensor | None = None):
+        """K5: LSE merge of each head's DP copies -> o [Bt, Hq, 128]."""
+        ptr, src, row = self.final[l]
+        ops.merge_lse(self.recv[l], ptr, src, row, self.group, out_bf16=out, out_lse=out_lse)
 
     def step(self, q_layers: torch.Tensor, out_layers: torch.Tensor):
         """q_layers / out_layers: [L, Bt, Hq, 128] bf16."""

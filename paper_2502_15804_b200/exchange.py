@@ -1,10 +1,12 @@
 """Fused NVLink all-gather for the sharded decode (replaces NCCL all_gather).
 
 Each rank owns, in memory it allocated with ``fkv_dev_alloc`` and exported
-with CUDA IPC, a receive area ``recv[parity][tp, slots, G, 132]`` and a flag
+with CUDA IPC, receive areas ``recv[buf]`` of tp exchange-record blocks
+(FKV_XREC: bf16 o [slots*G, 128] + f32 lse [slots*G] per rank) and a flag
 array ``flags[tp]``.  Per layer the decode kernel of rank r writes every
-segment's final (o, lse) record straight into ``recv[parity][r]`` of *every*
-rank (P2P stores over NVLink, ``fkv_decode_exchange``); its last warp then
+segment's final (o, lse) record straight into block r of ``recv[buf]`` of
+*every* rank (16-byte P2P stores over NVLink, ``fkv_decode_exchange``); its
+last CTA then
 bumps ``flags[r]`` on every rank (system-scope atomics after a system
 fence).  The merge kernel on each rank waits until all ``flags`` reached
 this layer's count, merges the DP copies and writes o (``fkv_merge_wait``).
@@ -31,7 +33,6 @@ import torch
 
 from . import _native
 
-REC = 132
 NBUF = 3  # receive areas per rank (see exchange_buffer)
 
 
@@ -77,7 +78,7 @@ class RankEndpoint:
 
     def __init__(self, rank: int, tp: int, slots: int, group: int):
         self.rank, self.tp, self.slots, self.group = rank, tp, slots, group
-        self.block = slots * group * REC * 4          # bytes of one rank's block
+        self.block = slots * group * (2 * 128 + 4)   # FKV_XREC_BYTES: one rank's block
         self.recv = [_Buf(tp * self.block) for _ in range(NBUF)]  # exchange_buffer()
         self.flags = _Buf(4 * max(tp, 2))
         self.ctr = _Buf(16)                            # [0] sig_done, [2:4] consumed
@@ -89,9 +90,9 @@ class RankEndpoint:
         """Where this rank's records go: its block in every peer's receive area."""
         return [base + self.rank * self.block for base in self.peer_recv[parity]]
 
-    def recv_tensor(self, parity: int) -> torch.Tensor:
-        return _as_tensor(self.recv[parity].ptr, self.tp * self.slots * self.group * REC,
-                          (self.tp * self.slots, self.group, REC))
+    def recv_tensor(self, buf: int) -> torch.Tensor:
+        """uint8 [tp, block] view of receive area ``buf`` (ops.xrec_view decodes it)."""
+        return _as_tensor(self.recv[buf].ptr, self.tp * self.block).view(self.tp, self.block)
 
     @property
     def sig_done(self) -> int:
@@ -106,12 +107,12 @@ class RankEndpoint:
             b.free()
 
 
-def _as_tensor(ptr: int, numel: int, shape) -> torch.Tensor:
-    """Zero-copy float32 CUDA tensor over library-owned device memory."""
+def _as_tensor(ptr: int, nbytes: int) -> torch.Tensor:
+    """Zero-copy uint8 CUDA tensor over library-owned device memory."""
     class _Ifc:
-        __cuda_array_interface__ = {"shape": (numel,), "typestr": "<f4", "data": (ptr, False),
+        __cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False),
                                     "version": 3, "strides": None}
-    return torch.as_tensor(_Ifc(), device="cuda").view(*shape)
+    return torch.as_tensor(_Ifc(), device="cuda")
 
 
 class P2PGroup:

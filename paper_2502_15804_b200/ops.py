@@ -44,7 +44,36 @@ def _p(t):
 
 
 # -------------------------------------------------------------- decode ----
-REC = 132  # floats per partial record (FKV_REC): o[128], lse, pad
+REC = 132  # floats per partial record of a split segment (FKV_REC): o[128], lse, pad
+XREC_ROW = HEAD_DIM * 2 + 4  # bytes per head of an exchange record: bf16 o[128] + f32 lse
+
+
+def xrec_bytes(slots: int, group: int) -> int:
+    """FKV_XREC_BYTES: one block of exchange records (``slots`` segments of
+    ``group`` heads): bf16 o [slots*group, 128] then f32 lse [slots*group]."""
+    return int(slots) * int(group) * XREC_ROW
+
+
+def xrec_empty(slots: int, group: int, device, ranks: int = 1) -> torch.Tensor:
+    """uint8 [ranks, xrec_bytes]: a send block (ranks=1) or a receive area."""
+    return torch.zeros((ranks, xrec_bytes(slots, group)), dtype=torch.uint8, device=device)
+
+
+def xrec_view(buf: torch.Tensor, group: int):
+    """(o bf16 [ranks, slots*group, 128], lse f32 [ranks, slots*group]) views
+    of exchange-record blocks ``buf`` (uint8 [ranks, block])."""
+    buf = buf.reshape(-1, buf.shape[-1])
+    n = buf.shape[-1] // XREC_ROW  # rows = slots * group
+    o = buf[:, :n * HEAD_DIM * 2].view(torch.bfloat16).view(-1, n, HEAD_DIM)
+    lse = buf[:, n * HEAD_DIM * 2:].view(torch.float32)
+    return o, lse
+
+
+def _xrec_slots(buf: torch.Tensor, group: int) -> int:
+    row = group * XREC_ROW
+    if buf.dtype != torch.uint8 or buf.shape[-1] % row:
+        raise NativeError(f"exchange records must be uint8 [..., slots * {row}]")
+    return buf.shape[-1] // row
 
 
 class DecodeWorkspace:
@@ -61,10 +90,11 @@ def _decode(q, cache: LayerCache, ws: DecodeWorkspace | None, sm_scale, out_bf16
         raise NativeError("q must be contiguous bf16 [..., 128]")
     ws = ws or DecodeWorkspace(cache)
     scale = 1.0 / math.sqrt(HEAD_DIM) if sm_scale is None else sm_scale
+    slots = _xrec_slots(out_rec, cache.group) if out_rec is not None else 0
     _native.check(_lib.fkv_decode(
         q.data_ptr(), cache.k.data_ptr(), cache.v.data_ptr(), cache.work.data_ptr(), cache.work_k,
         cache.n_workers, cache.n_items, cache.group, cache.launch_flags, scale, ws.part.data_ptr(),
-        cache.counters.data_ptr(), _p(out_bf16), _p(out_rec), _p(out_lse), _stream()))
+        cache.counters.data_ptr(), _p(out_bf16), _p(out_rec), slots, _p(out_lse), _stream()))
     return ws.part
 
 
@@ -77,7 +107,9 @@ def decode_partial(q: torch.Tensor, cache: LayerCache, ws: DecodeWorkspace | Non
 def decode_into(q: torch.Tensor, cache: LayerCache, ws: DecodeWorkspace | None = None, *,
                 out_bf16=None, out_rec=None, out_lse=None, sm_scale: float | None = None):
     """K4 with the fused per-segment LSE merge: segment s writes rows
-    seg_out_row[s] .. + G - 1 of the given outputs (one launch)."""
+    seg_out_row[s] .. + G - 1 of the given outputs (one launch): ``out_bf16``
+    bf16 [*, 128], ``out_lse`` f32 [*], ``out_rec`` one exchange-record block
+    (``xrec_empty(slots, G, dev)``; the NCCL all-gather's send buffer)."""
     if out_bf16 is None and out_rec is None and out_lse is None:
         raise NativeError("decode_into needs at least one output")
     _decode(q, cache, ws, sm_scale, out_bf16, out_rec, out_lse)
@@ -100,8 +132,8 @@ def decode_exchange(q: torch.Tensor, cache: LayerCache, endpoint, parity: int,
     _native.check(_lib.fkv_decode_exchange(
         q.data_ptr(), cache.k.data_ptr(), cache.v.data_ptr(), cache.work.data_ptr(), cache.work_k,
         cache.n_workers, cache.n_items, cache.group, cache.launch_flags, scale, ws.part.data_ptr(),
-        cache.counters.data_ptr(), None, recs, len(dests), None, endpoint.sig_done, flags,
-        len(endpoint.peer_flags), endpoint.rank, _stream()))
+        cache.counters.data_ptr(), None, recs, len(dests), endpoint.slots, None, endpoint.sig_done,
+        flags, len(endpoint.peer_flags), endpoint.rank, _stream()))
 
 
 def merge_wait(endpoint, parity: int, grp_ptr, src_idx, out_row, group: int, *, out_bf16=None,
@@ -111,20 +143,22 @@ def merge_wait(endpoint, parity: int, grp_ptr, src_idx, out_row, group: int, *, 
     _need_cuda(grp_ptr, src_idx, out_row)
     n_groups = int(out_row.shape[0])
     _native.check(_lib.fkv_merge_wait(
-        endpoint.recv[parity].ptr, grp_ptr.data_ptr(), src_idx.data_ptr(), out_row.data_ptr(),
-        n_groups, int(group), _p(out_bf16), None, _p(out_lse), endpoint.flags.ptr, endpoint.tp,
-        endpoint.consumed, _stream()))
+        endpoint.recv[parity].ptr, endpoint.slots, grp_ptr.data_ptr(), src_idx.data_ptr(),
+        out_row.data_ptr(), n_groups, int(group), _p(out_bf16), _p(out_lse), endpoint.flags.ptr,
+        endpoint.tp, endpoint.consumed, _stream()))
 
 
-def merge_lse(part, grp_ptr, src_idx, out_row, group: int, *, out_bf16=None, out_rec=None,
-              out_lse=None):
-    """K5: rows out_row[g] .. +group-1 <- LSE merge of the records
-    src_idx[grp_ptr[g]:grp_ptr[g+1]] of ``part`` ([*, group, REC] f32)."""
-    _need_cuda(part, grp_ptr, src_idx, out_row)
+def merge_lse(xrec, grp_ptr, src_idx, out_row, group: int, *, out_bf16=None, out_lse=None):
+    """K5: rows out_row[g] .. +group-1 <- LSE merge of the exchange records
+    src_idx[grp_ptr[g]:grp_ptr[g+1]] of ``xrec`` (uint8 [ranks, block]; record
+    i = rank * slots + slot)."""
+    _need_cuda(xrec, grp_ptr, src_idx, out_row)
+    if out_bf16 is None and out_lse is None:
+        raise NativeError("merge_lse needs at least one output")
     n_groups = int(out_row.shape[0])
     _native.check(_lib.fkv_merge_lse(
-        part.data_ptr(), grp_ptr.data_ptr(), src_idx.data_ptr(), out_row.data_ptr(), n_groups,
-        int(group), _p(out_bf16), _p(out_rec), _p(out_lse), _stream()))
+        xrec.data_ptr(), _xrec_slots(xrec, group), grp_ptr.data_ptr(), src_idx.data_ptr(),
+        out_row.data_ptr(), n_groups, int(group), _p(out_bf16), _p(out_lse), _stream()))
 
 
 def decode(q: torch.Tensor, cache: LayerCache, *, out: torch.Tensor | None = None,

@@ -25,6 +25,37 @@ def test_reference_arm_json_line():
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["value"] > 0
 
 
+def test_reference_arm_never_loads_the_product():
+    """--impl reference runs the reference's own generate_profile + the oracle
+    decode; neither the package nor libfairkv.so may be loaded."""
+    code = ("import runpy, sys; sys.argv = ['bench.py', '--impl', 'reference', '--steps', '1', "
+            "'--warmup', '0', '--layers', '2', '--batch', '2', '--budget', '128']; "
+            "runpy.run_path('bench.py', run_name='__main__'); "
+            "bad = [m for m in sys.modules if m.startswith('paper_2502_15804_b200')]; "
+            "maps = open('/proc/self/maps').read(); "
+            "assert not bad and 'libfairkv' not in maps, (bad, 'libfairkv' in maps); print('clean')")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert r.returncode == 0 and r.stdout.strip().endswith("clean"), r.stderr[-2000:]
+
+
+def test_reference_arm_budgets_match_the_product():
+    """oracle/workload.py over the reference's generate_profile reproduces the
+    product's synthetic_budgets bit for bit (same workload in both arms)."""
+    import numpy as np
+    sys.path.insert(0, str(ROOT))
+    import bench
+    from oracle import workload
+    from paper_2502_15804_b200.sharding import synthetic_budgets
+    hb = bench.ref_headbalance()
+    if hb is None:
+        import pytest
+        pytest.skip("reference not installed")
+    for dist_, param, seed in (("dirichlet", 8.0, 0), ("zipf", 1.2, 7), ("dirichlet", 1.0, 3)):
+        a = workload.synthetic_budgets(hb, 80, 16, 8, 1024, distribution=dist_, param=param, seed=seed)
+        b = synthetic_budgets(80, 16, 8, 1024, distribution=dist_, param=param, seed=seed)
+        assert np.array_equal(a, b)
+
+
 def test_planner_compare_runs_here():
     sys.path.insert(0, str(ROOT))
     import bench

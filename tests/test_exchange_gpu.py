@@ -58,7 +58,7 @@ def test_loopback_exchange_matches_single_gpu(cuda_device, tp, mode):
     torch.cuda.synchronize()
     ref = torch.stack([ops.decode(q[l], base[l])[0] for l in range(L)])
     for r in range(tp):
-        torch.testing.assert_close(outs[r].float(), ref.float(), rtol=2e-2, atol=1e-2)
+        torch.testing.assert_close(outs[r].float(), ref.float(), rtol=2e-2, atol=4e-3)
     # graph replay: flags and counters are monotonic / self-resetting
     g = torch.cuda.CUDAGraph()
     s = torch.cuda.Stream()
@@ -74,7 +74,7 @@ def test_loopback_exchange_matches_single_gpu(cuda_device, tp, mode):
         g.replay()
     torch.cuda.synchronize()
     for r in range(tp):
-        torch.testing.assert_close(outs[r].float(), ref.float(), rtol=2e-2, atol=1e-2)
+        torch.testing.assert_close(outs[r].float(), ref.float(), rtol=2e-2, atol=4e-3)
     grp.close()
 
 
@@ -121,7 +121,82 @@ def test_sharded_append_then_exchange(cuda_device, tp, mode):
         torch.cuda.synchronize()
         ref = torch.stack([ops.decode(q[l], base[l])[0] for l in range(L)])
         for r in range(tp):
-            torch.testing.assert_close(out[r].float(), ref.float(), rtol=2e-2, atol=1e-2)
+            torch.testing.assert_close(out[r].float(), ref.float(), rtol=2e-2, atol=4e-3)
     grown = sum(int(c.sync_lengths().sum()) for pr in per_rank for c in pr)
     assert grown == sum(int(c.sync_lengths().sum()) for c in base)
     grp.close()
+
+
+@pytest.mark.parametrize("tp,mode", [(2, "dp"), (4, "dp"), (8, "free")])
+def test_nccl_path_loopback_allgather(cuda_device, tp, mode):
+    """The NCCL fallback of StackDecoder (K4 -> exchange-record send block ->
+    all_gather_into_tensor -> K5) with tp virtual ranks on this GPU: each
+    layer every rank produces, a loopback all-gather stacks the send blocks
+    into every rank's receive area exactly as NCCL's all_gather_into_tensor
+    lays them out (rank r's block at r * block), every rank consumes.  Each
+    rank's o equals the single-GPU decode; a CUDA graph replays it."""
+    from paper_2502_15804_b200 import ops
+    from paper_2502_15804_b200.decoder import StackDecoder
+    base, per_rank, finals, bt, hq, G = _setup(tp, mode, cuda_device, L=4)
+    L = len(base)
+    decs = [StackDecoder(per_rank[r], finals, tp=tp, bt=bt, hq=hq, group=G, exchange="nccl")
+            for r in range(tp)]
+    q = torch.randn(L, bt, hq, 128, device=cuda_device).to(torch.bfloat16)
+    outs = torch.zeros(tp, L, bt, hq, 128, dtype=torch.bfloat16, device=cuda_device)
+
+    def step():
+        for l in range(L):
+            for r in range(tp):
+                decs[r].produce(l, q[l])
+            gathered = torch.stack([decs[r].send[l] for r in range(tp)])
+            for r in range(tp):
+                decs[r].recv[l].copy_(gathered)
+            for r in range(tp):
+                decs[r].consume(l, outs[r, l])
+
+    step()
+    torch.cuda.synchronize()
+    ref = torch.stack([ops.decode(q[l], base[l])[0] for l in range(L)])
+    for r in range(tp):
+        torch.testing.assert_close(outs[r].float(), ref.float(), rtol=2e-2, atol=4e-3)
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.graph(g, stream=s):
+        step()
+    outs.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    for r in range(tp):
+        torch.testing.assert_close(outs[r].float(), ref.float(), rtol=2e-2, atol=4e-3)
+
+
+def test_nccl_allgather_of_exchange_blocks(cuda_device, tmp_path):
+    """The real NCCL call on the exchange-record blocks (world size 1 in a
+    subprocess: one GPU here): all_gather_into_tensor of a uint8 send block
+    into the [tp, block] receive area the K5 merge reads."""
+    import subprocess
+    import sys
+    from pathlib import Path
+    code = r'''
+import os, torch, torch.distributed as dist
+os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=os.environ["PORT"])
+dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda:0"))
+from paper_2502_15804_b200 import ops
+send = ops.xrec_empty(3, 8, "cuda")[0].random_(0, 255)
+recv = ops.xrec_empty(3, 8, "cuda", ranks=1)
+dist.all_gather_into_tensor(recv.view(-1), send)
+torch.cuda.synchronize()
+assert torch.equal(recv[0], send)
+dist.destroy_process_group()
+print("ok")
+'''
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    import os
+    root = Path(__file__).resolve().parent.parent
+    env = dict(os.environ, PORT=str(port), PYTHONPATH=str(root))
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=240)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]

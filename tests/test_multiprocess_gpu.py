@@ -65,7 +65,7 @@ def _worker(rank: int, tp: int, port: int, mode: str, out_dir: str):
         torch.cuda.synchronize()
         ref_s = torch.stack([ops.decode(q_s[l], base[l])[0] for l in range(L)])
         err = max(err, float((o.float() - ref_s.float()).abs().max()))
-        ok = ok and bool(torch.allclose(o.float(), ref_s.float(), rtol=2e-2, atol=1e-2))
+        ok = ok and bool(torch.allclose(o.float(), ref_s.float(), rtol=2e-2, atol=4e-3))
     del ref
     with open(os.path.join(out_dir, f"rank{rank}.txt"), "w") as f:
         f.write(f"{int(ok)} {err}\n")
@@ -111,4 +111,7 @@ def test_bench_two_ranks_shared_device(cuda_device):
     assert r.returncode == 0, r.stderr[-2000:]
     line = json.loads(r.stdout.strip().splitlines()[-1])
     assert line["n_gpus"] == 2 and line["value"] > 0 and line["e2e"]["value"] > 0
-    assert "exchange p2p" in line["config"]["parallelism"]
+    assert "exchange p2p" in line["placement"]
+    # every placement was checked against a local decode before timing
+    assert set(line["check"]) == set(line["modes"]) == {"sha", "nodp", "dp", "dp-free"}
+    assert all(c["ok"] for c in line["check"].values())

@@ -27,7 +27,7 @@ from oracle import kv as okv
 pytestmark = pytest.mark.gpu
 
 S_RTOL, S_ATOL_ROW = 1e-4, 1e-6
-O_TOL = dict(rtol=2e-2, atol=1e-3)
+O_TOL = dict(rtol=2e-2, atol=4e-3)  # bf16; atol: half a bf16 ulp at the unit scale of V
 LSE_TOL = dict(rtol=1e-4, atol=1e-5)
 
 
@@ -79,7 +79,15 @@ def test_cfg1_end_to_end_tp2(cuda_device):
 
     bt, hq, hkv, T, w, B, tp = 1, 32, 8, 4096, 32, 128, 2
     G = hq // hkv
-    q, k, v, s_ref, _ = separated_inputs(bt, hq, hkv, T, B, seed0=0)
+    cfg = fk.EnumerationConfig(4, 2, True, tp)
+    # a draw whose selection boundaries are separated *and* whose AHA-DP plan
+    # replicates a head (so the token-split copies and their merge run)
+    for seed0 in range(0, 400, 40):
+        q, k, v, s_ref, _ = separated_inputs(bt, hq, hkv, T, B, seed0=seed0)
+        b0 = okv.ada_budgets(s_ref, B, w, 0.2)
+        p0 = fk.optimize_plan(fk.profile_from_budgets(b0[None], B), tp, cfg)
+        if any(c.replica_count > 1 for g in p0.layers[0].groups for c in g):
+            break
     dev = cuda_device
     kd, vd = k.to(dev), v.to(dev)
 
@@ -94,7 +102,6 @@ def test_cfg1_end_to_end_tp2(cuda_device):
 
     # ---- placement: profile -> AHA plan, identical to the reference's
     prof = fk.profile_from_budgets(budgets[None], B)
-    cfg = fk.EnumerationConfig(4, 2, True, tp)
     plan = fk.optimize_plan(prof, tp, cfg)
     la = plan.layers[0]
     ref = reference_headbalance()

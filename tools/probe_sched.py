@@ -19,7 +19,7 @@ for B in budgets_list:
     base = [LayerCache.allocate(budgets.reshape(L, -1)[l], qrow, qrow, G, dev, fill="random") for l in range(L)]
     q = torch.randn((L, bt, HQ, 128), device=dev).to(torch.bfloat16)
     for tp, mode in [(1, "sha"), (2, "sha"), (4, "sha"), (8, "sha"), (8, "dp")]:
-        plan, prof = bench.make_plan(budgets, tp, 8 if tp == 8 else 4, mode)
+        plan, prof = bench.make_plan(budgets, tp, mode)
         shards, _ = plan_layouts(plan, budgets, G)
         line = f"B={B:5d} tp{tp} {mode:4s}"
         for sched in os.environ.get("SCHEDS", "coop wide solo auto").split():
@@ -27,7 +27,7 @@ for B in budgets_list:
             worst = 0.0
             for g in range(tp):
                 caches = rank_caches([s[g] for s in shards], bt, HQ, G, tp, dev, base=base)
-                sends = [torch.empty((max(c.n_segments, 1), G, ops.REC), device=dev) for c in caches]
+                sends = [ops.xrec_empty(max(c.n_segments, 1), G, dev)[0] for c in caches]
                 wss = [ops.DecodeWorkspace(c) for c in caches]
                 def body():
                     for l in range(L):

@@ -18,11 +18,11 @@ q = torch.randn((bt, HQ, 128), device=dev).to(torch.bfloat16)
 o = torch.empty_like(q)
 names = ["entry", "pdl-wait", "first-data", "rounds-done(last piece)", "combine-start", "exit", "pre-atomic", "post-atomic", "merge:lse-loaded", "merge:weights", "merge:records-loaded", "merge:stored"]
 for tp in (1, 8):
-    plan, prof = bench.make_plan(budgets, tp, 4, "sha")
+    plan, prof = bench.make_plan(budgets, tp, "sha")
     shards, _ = plan_layouts(plan, budgets, G)
     cache = rank_caches([s[0] for s in shards], bt, HQ, G, tp, dev, base=base)[0]
     ws = ops.DecodeWorkspace(cache)
-    send = torch.empty((max(cache.n_segments, 1), G, ops.REC), device=dev)
+    send = ops.xrec_empty(max(cache.n_segments, 1), G, dev)[0]
     for _ in range(3):
         ops.decode_into(q, cache, ws, out_rec=send)
     torch.cuda.synchronize()
