@@ -547,7 +547,7 @@ def _alloc_base(budgets, dev, seed=7):
 def emulate_tp(args, budgets, dev, base, q, tps=(2, 4, 8), modes=("sha",) + AHA_MODES):
     """AHA vs uniform TP at 2/4/8 GPUs on this GPU.  Per placement and rank
     g: K4 with the fused exchange (``decode_exchange`` into loopback
-    endpoints: every record stored to all tp receive areas, the flag bumps)
+    endpoints: every record stored to all tp receive areas as epoch-tagged XLL units)
     over the rank's shard of every layer, timed alone (event nodes in one
     CUDA graph) and corrected by the rank's 80 layers back to back; then the
     K5 merge of the gathered records.  Layer span = max_g t(l, g) + K5(l)."""
@@ -585,17 +585,26 @@ def emulate_tp(args, budgets, dev, base, q, tps=(2, 4, 8), modes=("sha",) + AHA_
                     for l in range(L):
                         ops.decode_exchange(q[l], per_rank[g][l], grp.endpoints[g], bufs[l], wss[g][l])
                 ggs.append(capture(run_g))
-            # K5 (identical work on every rank): plain LSE merge of the gathered
-            # records of each layer from rank 0's receive areas
+            # K5: the marginal cost of every rank's merge_wait (polls its XLL
+            # records, merges, advances the epoch) -- all ranks' K4 + K5 per
+            # layer minus the same K4 sequence alone, per (layer, rank)
             tabs = [tuple(torch.as_tensor(x, device=dev) for x in (f.grp_ptr, f.src_idx, f.out_row))
                     for f in finals]
             o5 = torch.empty((bt, HQ, HEAD_DIM), dtype=torch.bfloat16, device=dev)
-            ep0 = grp.endpoints[0]
 
-            def run_k5(tabs=tabs, ep0=ep0, o5=o5, bufs=bufs):
+            def run_k4(per_rank=per_rank, wss=wss, grp=grp, bufs=bufs):
                 for l in range(L):
-                    ops.merge_lse(ep0.recv_tensor(bufs[l]), *tabs[l], GROUP, out_bf16=o5)
-            g5 = capture(run_k5)
+                    for g in range(tp):
+                        ops.decode_exchange(q[l], per_rank[g][l], grp.endpoints[g], bufs[l], wss[g][l])
+
+            def run_k45(per_rank=per_rank, wss=wss, grp=grp, bufs=bufs, tabs=tabs, o5=o5):
+                for l in range(L):
+                    for g in range(tp):
+                        ops.decode_exchange(q[l], per_rank[g][l], grp.endpoints[g], bufs[l], wss[g][l])
+                    for g in range(tp):
+                        ops.merge_wait(grp.endpoints[g], bufs[l], *tabs[l], GROUP, out_bf16=o5)
+            g4, g45 = capture(run_k4), capture(run_k45)
+            g5 = (g4, g45)
             st[mode] = dict(plan=plan, prof=prof, keep=(per_rank, wss, grp, tabs, o5), evs=evs, gph=gph,
                             ggs=ggs, g5=g5, rounds=[])
 
@@ -614,8 +623,11 @@ def emulate_tp(args, budgets, dev, base, q, tps=(2, 4, 8), modes=("sha",) + AHA_
                 tot = min(timed(ggs[g].replay, 1) for _ in range(EMU_REPLAYS))
                 c_g = max(0.0, (t_br[:, g].sum() - tot) / L)
                 t[:, g] = np.maximum(t_br[:, g] - c_g, 0.0)
-            m["g5"].replay()
-            k5 = min(timed(m["g5"].replay, 1) for _ in range(EMU_REPLAYS)) / L
+            g4, g45 = m["g5"]
+            g45.replay()
+            t4 = min(timed(g4.replay, 1) for _ in range(EMU_REPLAYS))
+            t45 = min(timed(g45.replay, 1) for _ in range(EMU_REPLAYS))
+            k5 = max(0.0, t45 - t4) / (L * tp)
             return t, t_br, k5
 
         for _ in range(EMU_ROUNDS):
@@ -650,10 +662,11 @@ def emulate_tp(args, budgets, dev, base, q, tps=(2, 4, 8), modes=("sha",) + AHA_
         row["best_aha"] = {"placement": aha, "gain_vs_sha": row[aha]["gain_vs_sha"]}
         results[f"tp{tp}"] = row
     results["note"] = ("per placement and rank: K4 with the fused exchange stores into loopback endpoints "
-                       "(decode_exchange: records to all tp receive areas + flag bumps) of every layer timed "
-                       "alone on this GPU (event nodes in one CUDA graph) minus the per-launch bracketing "
-                       "overhead (each rank's 80 layers back to back); layer span = max over ranks + the K5 "
-                       "merge of the gathered records (synchronous per-layer barrier, reference "
+                       "(decode_exchange: XLL records tagged with the layer's epoch to all tp receive areas) "
+                       "of every layer timed alone on this GPU (event nodes in one CUDA graph) minus the "
+                       "per-launch bracketing overhead (each rank's 80 layers back to back); layer span = max "
+                       "over ranks + K5 (merge_wait: polls the records, merges, advances the epoch; its "
+                       "marginal cost per launch) (synchronous per-layer barrier, reference "
                        "simulate.py:118-136); NVLink latency not included (one GPU); placements timed in 3 "
                        "interleaved rounds, median round; sim = reference simulator, pure-cache latency law")
     return results

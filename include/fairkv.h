@@ -186,29 +186,39 @@ int fkv_merge_lse(const void* xrec, int32_t xrec_slots, const int32_t* grp_ptr,
                   const int32_t* src_idx, const int32_t* out_row, int32_t n_groups, int32_t group,
                   void* out_bf16, float* out_lse, void* stream);
 
+/* Fused NVLink all-gather records ("XLL", a low-latency format in the style
+ * of NCCL's LL protocol): the rows of an XREC block, but every 16-byte unit
+ * carries 8 payload bytes and the exchange epoch twice, {w0, epoch, w1, epoch},
+ * written with one 16-byte store.  A reader that sees both epoch words of a
+ * unit equal to the expected epoch has that unit's payload -- no fence, no
+ * completion flag, no system-scope release (a MEMBAR.SYS costs ~10 us per
+ * launch on B200).  Head row = 32 units of o (4 bf16 columns each) + one unit
+ * {lse, epoch, 0, epoch} = FKV_XLL_ROW_BYTES; block = slots * group rows. */
+#define FKV_XLL_ROW_BYTES 528
+#define FKV_XLL_BYTES(slots, group) ((int64_t)(slots) * (group) * FKV_XLL_ROW_BYTES)
+
 /* Fused NVLink all-gather variant of fkv_decode (same work table).  Every
- * segment's final record is written to all n_rec destinations (each peer's
- * receive block for this rank, mapped with fkv_ipc_open; 16-byte P2P stores
- * over NVLink, bf16 o + f32 lse) instead of one local block, and when the
- * last CTA finishes, after a system-scope fence, it atomically increments
- * sig_flags[j][my_rank] in every peer's memory (n_sig peers).  sig_done:
- * local int32, zero between launches.  Replaces NCCL all_gather for the
- * per-layer exchange. */
+ * segment's final record is written in XLL format to all n_rec destinations
+ * (this rank's block of each peer's receive area, mapped with fkv_ipc_open;
+ * 16-byte P2P stores over NVLink) instead of one local block, tagged with
+ * epoch = epoch_ctr[0] + 1 (read after the preceding grid completes: the
+ * previous layer's fkv_merge_wait advanced it).  Replaces NCCL all_gather
+ * for the per-layer exchange; the reference models this step as an
+ * allreduce (reference latency.py:94-101). */
 int fkv_decode_exchange(const void* q, const void* k, const void* v, const fkv_work_t* work,
                         int32_t work_k, int32_t n_workers, int32_t n_items, int32_t group,
                         int32_t flags, float sm_scale, float* part, int32_t* counters, void* out_bf16,
                         void* const* out_xrecs, int32_t n_rec, int32_t xrec_slots, float* out_lse,
-                        int32_t* sig_done, int32_t* const* sig_flags, int32_t n_sig, int32_t my_rank,
-                        void* stream);
+                        const int32_t* epoch_ctr, void* stream);
 
-/* fkv_merge_lse preceded by the consumer side of the fused all-gather: every
- * CTA waits (acquire, system scope) until flags[r] >= consumed[0] + 1 for all
- * r < tp, merges, and the last CTA advances consumed[0] (consumed[1] is its
- * arrival counter, zero between launches).  flags == NULL: plain merge. */
+/* fkv_merge_lse over a receive area of XLL blocks (block r at
+ * r * FKV_XLL_BYTES) with the consumer side of the fused all-gather: each
+ * warp polls its records' units until they carry epoch_ctr[0] + 1, merges,
+ * and the last CTA advances epoch_ctr[0] (epoch_ctr[1] is its arrival
+ * counter, zero between launches).  epoch_ctr == NULL: fkv_merge_lse. */
 int fkv_merge_wait(const void* xrec, int32_t xrec_slots, const int32_t* grp_ptr,
                    const int32_t* src_idx, const int32_t* out_row, int32_t n_groups, int32_t group,
-                   void* out_bf16, float* out_lse, const int32_t* flags, int32_t tp,
-                   int32_t* consumed, void* stream);
+                   void* out_bf16, float* out_lse, int32_t* epoch_ctr, void* stream);
 
 /* Device memory that can be shared with the other GPUs of the node. */
 int fkv_dev_alloc(int64_t bytes, void** out_ptr);

@@ -19,7 +19,7 @@ LIB_PATH = Path(os.environ.get("FAIRKV_LIB", Path(__file__).resolve().parent / "
 
 if not LIB_PATH.exists():
     raise ImportError(
-        f"{LIB_PATH} is missing: build it with `python -m paper_2502_15804_b200.csrc.build` "
+        f"{LIB_PATH} is missing: build it with `python paper_2502_15804_b200/csrc/build.py` "
         "(or __graft_entry__.build()); this package has no fallback path"
     )
 
@@ -37,7 +37,7 @@ def _check_fresh() -> None:
     if have != want:
         raise ImportError(
             f"{LIB_PATH} was built from different sources (embedded hash {have}, sources {want}); "
-            "rebuild with `python -m paper_2502_15804_b200.csrc.build` (or __graft_entry__.build())")
+            "rebuild with `python paper_2502_15804_b200/csrc/build.py` (or __graft_entry__.build())")
 
 
 _check_fresh()
@@ -61,9 +61,8 @@ _SIGS = {
                              _vp, _vp, _i32, _vp, _vp]),
     "fkv_merge_lse": (C.c_int, [_vp, _i32, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp]),
     "fkv_decode_exchange": (C.c_int, [_vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _f32,
-                                      _vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _i32, _i32, _vp]),
-    "fkv_merge_wait": (C.c_int, [_vp, _i32, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _i32, _vp,
-                                 _vp]),
+                                      _vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp]),
+    "fkv_merge_wait": (C.c_int, [_vp, _i32, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp]),
     "fkv_dev_alloc": (C.c_int, [_i64, _vp]),
     "fkv_dev_free": (C.c_int, [_vp]),
     "fkv_ipc_get": (C.c_int, [_vp, _vp]),

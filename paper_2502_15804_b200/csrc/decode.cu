@@ -76,9 +76,7 @@ struct DecodeParams {
   int n_rec;
   int64_t rec_lse_off;  // bytes from a block's start to its lse array
   float* out_lse;
-  int32_t* sig_done;              // CTAs-finished counter (local), zero between launches
-  int32_t* sig_flag[FKV_MAX_PEERS];  // per peer: flags[tp] in that peer's memory
-  int n_sig, my_rank;
+  const int32_t* epoch_ctr;  // non-null: out_rec are XLL blocks tagged epoch_ctr[0] + 1
   int after_wait;  // FKV_DECODE_AFTER_WAIT: no global read before griddepcontrol.wait
 };
 
@@ -92,24 +90,52 @@ struct __align__(16) DecodeShared {
 };
 
 // ---- segment outputs: o rows (bf16, 16-byte stores) and lse, to the local
-// outputs and every exchange-record destination.  Row r of a record block is
-// at r * 256 bytes, its lse at rec_lse_off + 4 r (include/fairkv.h FKV_XREC).
-__device__ __forceinline__ void store_o16(const DecodeParams& p, int64_t row, int col, int4 v) {
+// outputs and every exchange-record destination.  Plain XREC blocks: row r
+// at r * 256 bytes, its lse at rec_lse_off + 4 r; XLL blocks (fused
+// exchange, ep != 0): row r at r * FKV_XLL_ROW_BYTES, 16-byte units
+// {w0, ep, w1, ep} -- one P2P store per 8 payload bytes (include/fairkv.h).
+__device__ __forceinline__ void st_ll(uint8_t* a, uint32_t w0, uint32_t w1, uint32_t ep) {
+  asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(a), "r"(w0), "r"(ep), "r"(w1),
+               "r"(ep)
+               : "memory");
+}
+__device__ __forceinline__ void store_o16(const DecodeParams& p, uint32_t ep, int64_t row, int col, int4 v) {
   if (p.out_bf16) *reinterpret_cast<int4*>(p.out_bf16 + row * FKV_HEAD_DIM + col) = v;
 #pragma unroll 1
-  for (int j = 0; j < p.n_rec; ++j)
-    *reinterpret_cast<int4*>(p.out_rec[j] + (row * FKV_HEAD_DIM + col) * 2) = v;
+  for (int j = 0; j < p.n_rec; ++j) {
+    if (ep) {
+      uint8_t* u = p.out_rec[j] + row * FKV_XLL_ROW_BYTES + col * 4;  // unit col / 4
+      st_ll(u, v.x, v.y, ep);
+      st_ll(u + 16, v.z, v.w, ep);
+    } else {
+      *reinterpret_cast<int4*>(p.out_rec[j] + (row * FKV_HEAD_DIM + col) * 2) = v;
+    }
+  }
 }
-__device__ __forceinline__ void store_lse1(const DecodeParams& p, int64_t row, float l) {
+__device__ __forceinline__ void store_lse1(const DecodeParams& p, uint32_t ep, int64_t row, float l) {
   if (p.out_lse) p.out_lse[row] = l;
 #pragma unroll 1
-  for (int j = 0; j < p.n_rec; ++j) reinterpret_cast<float*>(p.out_rec[j] + p.rec_lse_off)[row] = l;
+  for (int j = 0; j < p.n_rec; ++j) {
+    if (ep)
+      st_ll(p.out_rec[j] + row * FKV_XLL_ROW_BYTES + 32 * 16, __float_as_uint(l), 0u, ep);
+    else
+      reinterpret_cast<float*>(p.out_rec[j] + p.rec_lse_off)[row] = l;
+  }
 }
-__device__ __forceinline__ void store_lse4(const DecodeParams& p, int64_t row, float4 l) {
+__device__ __forceinline__ void store_lse4(const DecodeParams& p, uint32_t ep, int64_t row, float4 l) {
   if (p.out_lse) *reinterpret_cast<float4*>(p.out_lse + row) = l;
 #pragma unroll 1
-  for (int j = 0; j < p.n_rec; ++j)
-    *reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out_rec[j] + p.rec_lse_off) + row) = l;
+  for (int j = 0; j < p.n_rec; ++j) {
+    if (ep) {
+      uint8_t* u = p.out_rec[j] + row * FKV_XLL_ROW_BYTES + 32 * 16;
+      st_ll(u, __float_as_uint(l.x), 0u, ep);
+      st_ll(u + FKV_XLL_ROW_BYTES, __float_as_uint(l.y), 0u, ep);
+      st_ll(u + 2 * FKV_XLL_ROW_BYTES, __float_as_uint(l.z), 0u, ep);
+      st_ll(u + 3 * FKV_XLL_ROW_BYTES, __float_as_uint(l.w), 0u, ep);
+    } else {
+      *reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out_rec[j] + p.rec_lse_off) + row) = l;
+    }
+  }
 }
 
 __device__ __forceinline__ uint2 pack_bf16x4(float4 v) {
@@ -118,19 +144,21 @@ __device__ __forceinline__ uint2 pack_bf16x4(float4 v) {
 
 // One head row held as a float4 of columns 4*lane .. +3 by every lane:
 // neighbouring lanes pair up so even lanes store 16 bytes (8 columns).
-__device__ __forceinline__ void emit_row_lanes(const DecodeParams& p, int64_t row, float4 o, int lane) {
+__device__ __forceinline__ void emit_row_lanes(const DecodeParams& p, uint32_t ep, int64_t row, float4 o,
+                                               int lane) {
   const uint2 w = pack_bf16x4(o);
   const uint32_t hx = __shfl_down_sync(0xffffffffu, w.x, 1), hy = __shfl_down_sync(0xffffffffu, w.y, 1);
-  if ((lane & 1) == 0) store_o16(p, row, 4 * lane, make_int4(w.x, w.y, hx, hy));
+  if ((lane & 1) == 0) store_o16(p, ep, row, 4 * lane, make_int4(w.x, w.y, hx, hy));
 }
 
 // lse of heads 0..G-1 held by lanes 0..G-1 -> float4 stores by lanes 0 (and 1).
 template <int G>
-__device__ __forceinline__ void emit_lse_lanes(const DecodeParams& p, int64_t row, float l, int lane) {
+__device__ __forceinline__ void emit_lse_lanes(const DecodeParams& p, uint32_t ep, int64_t row, float l,
+                                               int lane) {
   const int b = 4 * (lane & 1);
   const float a0 = __shfl_sync(0xffffffffu, l, b), a1 = __shfl_sync(0xffffffffu, l, b + 1);
   const float a2 = __shfl_sync(0xffffffffu, l, b + 2), a3 = __shfl_sync(0xffffffffu, l, b + 3);
-  if (lane < G / 4) store_lse4(p, row + b, make_float4(a0, a1, a2, a3));
+  if (lane < G / 4) store_lse4(p, ep, row + b, make_float4(a0, a1, a2, a3));
 }
 
 // The finalised o of one whole segment, in the mma accumulator layout
@@ -140,8 +168,8 @@ __device__ __forceinline__ void emit_lse_lanes(const DecodeParams& p, int64_t ro
 // into "lane L holds 2 columns of head L >> 2"; a 4x4 word transpose among
 // the 4 lanes of a head then gives every lane 8 consecutive columns.
 template <int G>
-__device__ __forceinline__ void emit_acc(const DecodeParams& p, int64_t orow, const float (&acc)[8][4],
-                                         float inv0, float inv1, int lane) {
+__device__ __forceinline__ void emit_acc(const DecodeParams& p, uint32_t ep, int64_t orow,
+                                         const float (&acc)[8][4], float inv0, float inv1, int lane) {
   uint32_t t[16];  // t[c]: this lane's word of 8-column chunk c of head lane >> 2
 #pragma unroll
   for (int dt = 0; dt < 8; ++dt) {
@@ -162,7 +190,7 @@ __device__ __forceinline__ void emit_acc(const DecodeParams& p, int64_t orow, co
       for (int x = 0; x < 4; ++x)
         if (k == x) w[x] = got;
     }
-    if (h < G) store_o16(p, orow + h, 8 * (4 * m + j), make_int4(w[0], w[1], w[2], w[3]));
+    if (h < G) store_o16(p, ep, orow + h, 8 * (4 * m + j), make_int4(w[0], w[1], w[2], w[3]));
   }
 }
 
@@ -347,6 +375,8 @@ __global__ void __launch_bounds__(Shape<MODE>::W * 32, Shape<MODE>::kCtasPerSm)
   // completed.
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;");
+  // exchange epoch of this layer: the previous merge_wait advanced the counter
+  const uint32_t ep = p.epoch_ctr ? static_cast<uint32_t>(*reinterpret_cast<const volatile int32_t*>(p.epoch_ctr)) + 1u : 0u;
   load_q(0);
   if (warp == 0) stamp(PROBE, 1);
   if (!SOLO && warp == 0) named_arrive<W>(1);  // the hand-over slot starts free
@@ -549,11 +579,11 @@ __global__ void __launch_bounds__(Shape<MODE>::W * 32, Shape<MODE>::kCtasPerSm)
 
     if (fused && n_it == 1) {
       // whole segment in one piece: registers -> output rows (16-byte stores)
-      emit_acc<G>(p, orow, acc, inv0, inv1, lane);
+      emit_acc<G>(p, ep, orow, acc, inv0, inv1, lane);
       // lse of head g is lse0 / lse1 of lane g >> 1 (lanes 0..3)
       const float la = __shfl_sync(0xffffffffu, lse0, (lane >> 1) & 3);
       const float lb = __shfl_sync(0xffffffffu, lse1, (lane >> 1) & 3);
-      emit_lse_lanes<G>(p, orow, (lane & 1) ? lb : la, lane);
+      emit_lse_lanes<G>(p, ep, orow, (lane & 1) ? lb : la, lane);
       continue;
     }
 
@@ -634,8 +664,8 @@ __global__ void __launch_bounds__(Shape<MODE>::W * 32, Shape<MODE>::kCtasPerSm)
     }
     stamp(PROBE, 10);
 #pragma unroll
-    for (int g = 0; g < G; ++g) emit_row_lanes(p, orow + g, o[g], lane);
-    emit_lse_lanes<G>(p, orow, lse_g, lane);
+    for (int g = 0; g < G; ++g) emit_row_lanes(p, ep, orow + g, o[g], lane);
+    emit_lse_lanes<G>(p, ep, orow, lse_g, lane);
     if (lane == 0) p.counters[d.i0] = 0;  // ready for the next launch / graph replay
     stamp(PROBE, 11);
     __syncwarp();  // the scratch is reused by the next merge
@@ -688,66 +718,56 @@ __global__ void __launch_bounds__(Shape<MODE>::W * 32, Shape<MODE>::kCtasPerSm)
                __ldcg(reinterpret_cast<const float4*>(base + (i * G + g) * FKV_REC) + lane));
         const float lse_g = S > 0.f ? M + __logf(S) : -CUDART_INF_F;
         const int64_t row = orow + g;
-        emit_row_lanes(p, row, o, lane);
-        if (lane == 0) store_lse1(p, row, lse_g);
+        emit_row_lanes(p, ep, row, o, lane);
+        if (lane == 0) store_lse1(p, ep, row, lse_g);
       }
       if (threadIdx.x == 0) p.counters[sh.fin_i0] = 0;
     }
   }
 
   if (warp == 0) stamp(PROBE, 5);
-  // Fused all-gather completion: the last CTA out publishes this rank's
-  // records to every peer by bumping its flag there (system-scope release).
-  if (p.n_sig > 0 && (kCombiner || SOLO)) {
-    __threadfence_system();  // every warp may have written peer records (merge above)
-    named_sync<W>(3);
-  }
-  if (p.n_sig > 0 && warp == 0) {
-    __threadfence_system();
-    __syncwarp();
-    if (lane == 0 && atomicAdd(p.sig_done, 1) == static_cast<int>(gridDim.x) - 1) {
-      *p.sig_done = 0;
-      __threadfence_system();
-      for (int j = 0; j < p.n_sig; ++j) atomicAdd_system(p.sig_flag[j] + p.my_rank, 1);
-    }
-  }
 }
 
 // K5 standalone (after the all-gather): warp g of the CTA merges head g of
-// one output group in a single online-LSE pass over exchange records
-// (FKV_XREC blocks of `slots` rows, block r at r * block_bytes); lane = 4
-// head_dim columns.
-template <int G>
+// one output group in a single online-LSE pass over exchange records (block
+// r at r * block_bytes, `slots` rows per block); lane = 4 head_dim columns.
+// LL: XLL blocks written by peers' fkv_decode_exchange -- every lane polls
+// its own 16-byte unit (and the row's lse unit) until both epoch words match,
+// so each merge starts as soon as its own records have landed.
+__device__ __forceinline__ int4 ld_ll(const uint8_t* a) {
+  int4 v;
+  asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(a)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ int4 wait_ll(const uint8_t* a, int ep) {
+  int4 v = ld_ll(a);
+  while (v.y != ep || v.w != ep) {
+    __nanosleep(20);
+    v = ld_ll(a);
+  }
+  return v;
+}
+
+template <int G, bool LL>
 __global__ void __launch_bounds__(G * 32)
     merge_lse_kernel(const uint8_t* __restrict__ xrec, int slots, int64_t block_bytes,
                      const int32_t* __restrict__ grp_ptr, const int32_t* __restrict__ src_idx,
                      const int32_t* __restrict__ out_row, __nv_bfloat16* __restrict__ out_bf16,
-                     float* __restrict__ out_lse, const int32_t* flags, int tp, int32_t* consumed) {
-  // Programmatic dependent launch (plain merges only, see fkv_merge_wait):
-  // the records are complete once the producer grid (NCCL all-gather, K4
-  // records) is.
-  if (!flags) {
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    asm volatile("griddepcontrol.launch_dependents;");
-  }
-  // Fused all-gather consumer: wait until every peer has published this
-  // layer's records (their flag reached consumed+1), read them from L2.
-  __shared__ int s_target;
-  if (flags) {
-    if (threadIdx.x == 0) {
-      const int target = *reinterpret_cast<volatile int32_t*>(consumed) + 1;
-      for (int r = 0; r < tp; ++r) {
-        int v;
-        do {
-          asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(flags + r) : "memory");
-          if (v < target) __nanosleep(32);
-        } while (v < target);
-      }
-      s_target = target;
-    }
-    __syncthreads();
-    __threadfence_system();
-  }
+                     float* __restrict__ out_lse, int32_t* epoch_ctr) {
+  // Programmatic dependent launch.  Plain records are complete once the
+  // producer grid (NCCL all-gather, K4 records) is.  XLL records validate
+  // themselves, so the LL merge starts polling while the producer K4 still
+  // runs and does not wait for it: it starts only after that K4 triggered,
+  // i.e. passed its own wait on the previous merge, so the epoch the previous
+  // merge advanced is final; the next K4 reads the epoch only after its wait
+  // on this grid.
+  int ep = 0;
+  if (LL) ep = *reinterpret_cast<volatile int32_t*>(epoch_ctr) + 1;
+  else asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
   const int grp = blockIdx.x;
   const int g = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int i0 = grp_ptr[grp], i1 = grp_ptr[grp + 1];
@@ -758,9 +778,18 @@ __global__ void __launch_bounds__(G * 32)
     const int src = src_idx[i];
     const uint8_t* blk = xrec + static_cast<int64_t>(src / slots) * block_bytes;
     const int64_t row = static_cast<int64_t>(src % slots) * G + g;
-    const float l = __ldcg(reinterpret_cast<const float*>(blk + lse_off) + row);
+    float l;
+    uint2 w;
+    if (LL) {
+      const uint8_t* r = blk + row * FKV_XLL_ROW_BYTES;
+      const int4 u = wait_ll(r + 16 * lane, ep);
+      l = __int_as_float(wait_ll(r + 32 * 16, ep).x);
+      w = make_uint2(u.x, u.z);
+    } else {
+      l = __ldcg(reinterpret_cast<const float*>(blk + lse_off) + row);
+      if (l != -CUDART_INF_F) w = __ldcg(reinterpret_cast<const uint2*>(blk + row * FKV_HEAD_DIM * 2) + lane);
+    }
     if (l == -CUDART_INF_F) continue;
-    const uint2 w = __ldcg(reinterpret_cast<const uint2*>(blk + row * FKV_HEAD_DIM * 2) + lane);
     const float2 o01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w.x));
     const float2 o23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w.y));
     const float nm = fmaxf(m, l);
@@ -785,11 +814,12 @@ __global__ void __launch_bounds__(G * 32)
     ob[1] = __floats2bfloat162_rn(acc.z, acc.w);
   }
   if (out_lse && lane == 0) out_lse[row] = lse;
-  if (flags) {
+  if (LL) {
+    // the last CTA out advances the epoch (every CTA read it at entry)
     __syncthreads();
-    if (threadIdx.x == 0 && atomicAdd(consumed + 1, 1) == static_cast<int>(gridDim.x) - 1) {
-      consumed[1] = 0;
-      atomicExch(consumed, s_target);  // this layer consumed: next wait targets +1
+    if (threadIdx.x == 0 && atomicAdd(epoch_ctr + 1, 1) == static_cast<int>(gridDim.x) - 1) {
+      epoch_ctr[1] = 0;
+      atomicExch(epoch_ctr, ep);
     }
   }
 }
@@ -874,7 +904,7 @@ extern "C" int fkv_decode(const void* q, const void* k, const void* v, const fkv
                           void* stream) {
   return fkv_decode_exchange(q, k, v, work, work_k, n_workers, n_items, group, flags, sm_scale, part,
                              counters, out_bf16, out_xrec ? &out_xrec : nullptr, out_xrec ? 1 : 0,
-                             xrec_slots, out_lse, nullptr, nullptr, 0, 0, stream);
+                             xrec_slots, out_lse, nullptr, stream);
 }
 
 extern "C" int fkv_decode_exchange(const void* q, const void* k, const void* v,
@@ -882,19 +912,17 @@ extern "C" int fkv_decode_exchange(const void* q, const void* k, const void* v,
                                    int32_t n_items, int32_t group, int32_t flags, float sm_scale,
                                    float* part, int32_t* counters, void* out_bf16,
                                    void* const* out_xrecs, int32_t n_rec, int32_t xrec_slots,
-                                   float* out_lse, int32_t* sig_done, int32_t* const* sig_flags,
-                                   int32_t n_sig, int32_t my_rank, void* stream) {
+                                   float* out_lse, const int32_t* epoch_ctr, void* stream) {
   using namespace fkv;
   if (n_items < 0 || n_workers < 0) return set_error(FKV_ERR_INVALID, "fkv_decode: negative size");
   if (work_k < 1 || work_k > FKV_MAX_WORK)
     return set_error(FKV_ERR_INVALID, "fkv_decode: work_k must be in [1, FKV_MAX_WORK]");
-  if (n_rec < 0 || n_rec > FKV_MAX_PEERS || n_sig < 0 || n_sig > FKV_MAX_PEERS)
-    return set_error(FKV_ERR_INVALID, "fkv_decode: too many record destinations / peers");
+  if (n_rec < 0 || n_rec > FKV_MAX_PEERS)
+    return set_error(FKV_ERR_INVALID, "fkv_decode: too many record destinations");
   if (n_rec > 0 && xrec_slots < 1)
     return set_error(FKV_ERR_INVALID, "fkv_decode: exchange records need xrec_slots >= 1");
   if (n_items == 0 || n_workers == 0) return FKV_OK;
-  if (!q || !k || !v || !work || !part || !counters || (n_rec && !out_xrecs) ||
-      (n_sig && (!sig_done || !sig_flags)))
+  if (!q || !k || !v || !work || !part || !counters || (n_rec && !out_xrecs))
     return set_error(FKV_ERR_INVALID, "fkv_decode: null pointer");
   uintptr_t align = reinterpret_cast<uintptr_t>(k) | reinterpret_cast<uintptr_t>(v) |
                     reinterpret_cast<uintptr_t>(work) | reinterpret_cast<uintptr_t>(out_bf16) |
@@ -917,10 +945,7 @@ extern "C" int fkv_decode_exchange(const void* q, const void* k, const void* v,
   p.n_rec = n_rec;
   p.rec_lse_off = static_cast<int64_t>(xrec_slots) * group * FKV_HEAD_DIM * 2;
   p.out_lse = out_lse;
-  p.sig_done = sig_done;
-  for (int j = 0; j < n_sig; ++j) p.sig_flag[j] = sig_flags[j];
-  p.n_sig = n_sig;
-  p.my_rank = my_rank;
+  p.epoch_ctr = epoch_ctr;
   p.after_wait = (flags & FKV_DECODE_AFTER_WAIT) != 0;
   const int probe = g_probe;
   g_probe = 0;
@@ -931,26 +956,25 @@ extern "C" int fkv_merge_lse(const void* xrec, int32_t xrec_slots, const int32_t
                              const int32_t* src_idx, const int32_t* out_row, int32_t n_groups,
                              int32_t group, void* out_bf16, float* out_lse, void* stream) {
   return fkv_merge_wait(xrec, xrec_slots, grp_ptr, src_idx, out_row, n_groups, group, out_bf16,
-                        out_lse, nullptr, 0, nullptr, stream);
+                        out_lse, nullptr, stream);
 }
 
 extern "C" int fkv_merge_wait(const void* xrec, int32_t xrec_slots, const int32_t* grp_ptr,
                               const int32_t* src_idx, const int32_t* out_row, int32_t n_groups,
-                              int32_t group, void* out_bf16, float* out_lse, const int32_t* flags,
-                              int32_t tp, int32_t* consumed, void* stream) {
+                              int32_t group, void* out_bf16, float* out_lse, int32_t* epoch_ctr,
+                              void* stream) {
   using namespace fkv;
-  if (flags && (!consumed || tp < 1 || tp > FKV_MAX_PEERS))
-    return set_error(FKV_ERR_INVALID, "fkv_merge_wait: bad flags / consumed / tp");
   if (n_groups < 0 || xrec_slots < 1) return set_error(FKV_ERR_INVALID, "fkv_merge_lse: bad sizes");
   if (n_groups == 0) return FKV_OK;
   if (!xrec || !grp_ptr || !src_idx || !out_row || (!out_bf16 && !out_lse))
     return set_error(FKV_ERR_INVALID, "fkv_merge_lse: null pointer");
   if (reinterpret_cast<uintptr_t>(xrec) & 15)
     return set_error(FKV_ERR_INVALID, "fkv_merge_lse: records not 16-byte aligned");
+  if (group != 4 && group != 8) return set_error(FKV_ERR_INVALID, "fkv_merge_lse: group must be 4 or 8");
   auto ob = static_cast<__nv_bfloat16*>(out_bf16);
   auto xr = static_cast<const uint8_t*>(xrec);
-  if (group != 4 && group != 8) return set_error(FKV_ERR_INVALID, "fkv_merge_lse: group must be 4 or 8");
-  const int64_t block = FKV_XREC_BYTES(xrec_slots, group);
+  const bool ll = epoch_ctr != nullptr;
+  const int64_t block = ll ? FKV_XLL_BYTES(xrec_slots, group) : FKV_XREC_BYTES(xrec_slots, group);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(n_groups, 1, 1);
   cfg.blockDim = dim3(group * 32, 1, 1);
@@ -959,13 +983,17 @@ extern "C" int fkv_merge_wait(const void* xrec, int32_t xrec_slots, const int32_
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL (see kernel)
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  // A spinning consumer is never launched early: its CTAs would sit on SMs
-  // waiting for peers while grids queued behind it need them.
-  cfg.numAttrs = flags ? 0 : 1;
-  const cudaError_t e =
-      group == 4 ? cudaLaunchKernelEx(&cfg, merge_lse_kernel<4>, xr, xrec_slots, block, grp_ptr, src_idx,
-                                      out_row, ob, out_lse, flags, tp, consumed)
-                 : cudaLaunchKernelEx(&cfg, merge_lse_kernel<8>, xr, xrec_slots, block, grp_ptr, src_idx,
-                                      out_row, ob, out_lse, flags, tp, consumed);
+  cfg.numAttrs = getenv("FKV_K5_NO_PDL") && ll ? 0 : 1;  // env: diagnostics
+  cudaError_t e;
+  if (group == 4)
+    e = ll ? cudaLaunchKernelEx(&cfg, merge_lse_kernel<4, true>, xr, xrec_slots, block, grp_ptr, src_idx,
+                                out_row, ob, out_lse, epoch_ctr)
+           : cudaLaunchKernelEx(&cfg, merge_lse_kernel<4, false>, xr, xrec_slots, block, grp_ptr, src_idx,
+                                out_row, ob, out_lse, epoch_ctr);
+  else
+    e = ll ? cudaLaunchKernelEx(&cfg, merge_lse_kernel<8, true>, xr, xrec_slots, block, grp_ptr, src_idx,
+                                out_row, ob, out_lse, epoch_ctr)
+           : cudaLaunchKernelEx(&cfg, merge_lse_kernel<8, false>, xr, xrec_slots, block, grp_ptr, src_idx,
+                                out_row, ob, out_lse, epoch_ctr);
   return cuda_check(e, "merge_lse launch");
 }

@@ -1,15 +1,20 @@
 """Fused NVLink all-gather for the sharded decode (replaces NCCL all_gather).
 
 Each rank owns, in memory it allocated with ``fkv_dev_alloc`` and exported
-with CUDA IPC, receive areas ``recv[buf]`` of tp exchange-record blocks
-(FKV_XREC: bf16 o [slots*G, 128] + f32 lse [slots*G] per rank) and a flag
-array ``flags[tp]``.  Per layer the decode kernel of rank r writes every
-segment's final (o, lse) record straight into block r of ``recv[buf]`` of
-*every* rank (16-byte P2P stores over NVLink, ``fkv_decode_exchange``); its
-last CTA then
-bumps ``flags[r]`` on every rank (system-scope atomics after a system
-fence).  The merge kernel on each rank waits until all ``flags`` reached
-this layer's count, merges the DP copies and writes o (``fkv_merge_wait``).
+with CUDA IPC, receive areas ``recv[buf]`` of tp exchange-record blocks in
+the XLL format (include/fairkv.h: per head row 32 units {4 o bytes, epoch,
+4 o bytes, epoch} + one {lse, epoch, 0, epoch} unit) and an epoch counter.
+Per layer the decode kernel of rank r writes every segment's final (o, lse)
+record straight into block r of ``recv[buf]`` of *every* rank (16-byte P2P
+stores over NVLink, ``fkv_decode_exchange``), each unit tagged with the
+layer's epoch (the rank's counter + 1).  The merge kernel on each rank
+polls exactly the units it merges until they carry that epoch, merges the
+DP copies and writes o (``fkv_merge_wait``); its last CTA advances the
+counter.  The data carries its own completion flag (NCCL's LL idea), so
+the producer needs no fence and no flag write: a system-scope release
+(MEMBAR.SYS) measured ~10 us per launch on B200, as much as a TP=8 rank's
+whole decode.  Epochs grow monotonically and every rank runs the same
+layer sequence, so all ranks agree on them without communicating.
 Receive areas rotate per layer (``exchange_buffer``): a rank can run at
 most one layer ahead of any peer (its merge of layer s needs every peer's
 decode of s, which follows that peer's merge of s-1 in stream order), so it
@@ -78,12 +83,10 @@ class RankEndpoint:
 
     def __init__(self, rank: int, tp: int, slots: int, group: int):
         self.rank, self.tp, self.slots, self.group = rank, tp, slots, group
-        self.block = slots * group * (2 * 128 + 4)   # FKV_XREC_BYTES: one rank's block
+        self.block = slots * group * 528              # FKV_XLL_BYTES: one rank's block
         self.recv = [_Buf(tp * self.block) for _ in range(NBUF)]  # exchange_buffer()
-        self.flags = _Buf(4 * max(tp, 2))
-        self.ctr = _Buf(16)                            # [0] sig_done, [2:4] consumed
+        self.ctr = _Buf(16)                            # [0] epoch, [1] merge arrival counter
         self.peer_recv: list[list[int]] = [[] for _ in range(NBUF)]  # [buffer][peer] base
-        self.peer_flags: list[int] = []
 
     # -- pointers handed to the kernels
     def dest_records(self, parity: int) -> list[int]:
@@ -91,19 +94,16 @@ class RankEndpoint:
         return [base + self.rank * self.block for base in self.peer_recv[parity]]
 
     def recv_tensor(self, buf: int) -> torch.Tensor:
-        """uint8 [tp, block] view of receive area ``buf`` (ops.xrec_view decodes it)."""
+        """uint8 [tp, block] view of receive area ``buf`` (XLL blocks)."""
         return _as_tensor(self.recv[buf].ptr, self.tp * self.block).view(self.tp, self.block)
 
     @property
-    def sig_done(self) -> int:
+    def epoch(self) -> int:
+        """Device address of the epoch counter (int32[2])."""
         return self.ctr.ptr
 
-    @property
-    def consumed(self) -> int:
-        return self.ctr.ptr + 8
-
     def free(self):
-        for b in (*self.recv, self.flags, self.ctr):
+        for b in (*self.recv, self.ctr):
             b.free()
 
 
@@ -125,14 +125,13 @@ class P2PGroup:
         eps = [RankEndpoint(r, tp, slots, group) for r in range(tp)]
         for ep in eps:
             ep.peer_recv = [[e.recv[par].ptr for e in eps] for par in range(NBUF)]
-            ep.peer_flags = [e.flags.ptr for e in eps]
         return P2PGroup(eps)
 
     @staticmethod
     def connect(rank: int, tp: int, slots: int, group: int, process_group=None) -> "P2PGroup":
         import torch.distributed as dist
         ep = RankEndpoint(rank, tp, slots, group)
-        mine = {"recv": [b.handle() for b in ep.recv], "flags": ep.flags.handle()}
+        mine = {"recv": [b.handle() for b in ep.recv]}
         allh = [None] * tp
         dist.all_gather_object(allh, mine, group=process_group)
         opened = []
@@ -145,12 +144,6 @@ class P2PGroup:
                     row.append(_open(h["recv"][par]))
                     opened.append(row[-1])
             ep.peer_recv[par] = row
-        for r, h in enumerate(allh):
-            if r == rank:
-                ep.peer_flags.append(ep.flags.ptr)
-            else:
-                ep.peer_flags.append(_open(h["flags"]))
-                opened.append(ep.peer_flags[-1])
         return P2PGroup([ep], opened)
 
     def close(self):

@@ -46,6 +46,7 @@ def _p(t):
 # -------------------------------------------------------------- decode ----
 REC = 132  # floats per partial record of a split segment (FKV_REC): o[128], lse, pad
 XREC_ROW = HEAD_DIM * 2 + 4  # bytes per head of an exchange record: bf16 o[128] + f32 lse
+XLL_ROW = 528  # FKV_XLL_ROW_BYTES: the same head row in the fused exchange's LL format
 
 
 def xrec_bytes(slots: int, group: int) -> int:
@@ -118,8 +119,9 @@ def decode_into(q: torch.Tensor, cache: LayerCache, ws: DecodeWorkspace | None =
 def decode_exchange(q: torch.Tensor, cache: LayerCache, endpoint, parity: int,
                     ws: DecodeWorkspace | None = None, sm_scale: float | None = None):
     """K4 with the fused NVLink all-gather: every segment's final record goes
-    to this rank's block of every peer's receive area (P2P stores), then the
-    last warp signals all peers (``exchange.RankEndpoint``)."""
+    to this rank's block of every peer's receive area ``parity`` as XLL units
+    tagged with this layer's exchange epoch (16-byte P2P stores; no fence, no
+    completion flag -- ``exchange.RankEndpoint``)."""
     import ctypes as C
     _need_cuda(q, cache.k)
     if q.dtype != torch.bfloat16 or q.shape[-1] != HEAD_DIM or not q.is_contiguous():
@@ -128,24 +130,24 @@ def decode_exchange(q: torch.Tensor, cache: LayerCache, endpoint, parity: int,
     scale = 1.0 / math.sqrt(HEAD_DIM) if sm_scale is None else sm_scale
     dests = endpoint.dest_records(parity)
     recs = (C.c_void_p * len(dests))(*dests)
-    flags = (C.c_void_p * len(endpoint.peer_flags))(*endpoint.peer_flags)
     _native.check(_lib.fkv_decode_exchange(
         q.data_ptr(), cache.k.data_ptr(), cache.v.data_ptr(), cache.work.data_ptr(), cache.work_k,
         cache.n_workers, cache.n_items, cache.group, cache.launch_flags, scale, ws.part.data_ptr(),
-        cache.counters.data_ptr(), None, recs, len(dests), endpoint.slots, None, endpoint.sig_done,
-        flags, len(endpoint.peer_flags), endpoint.rank, _stream()))
+        cache.counters.data_ptr(), None, recs, len(dests), endpoint.slots, None, endpoint.epoch,
+        _stream()))
 
 
 def merge_wait(endpoint, parity: int, grp_ptr, src_idx, out_row, group: int, *, out_bf16=None,
                out_lse=None):
-    """K5 after the fused all-gather: wait for every peer's flag, then merge
-    the DP copies of each head from this rank's receive area."""
+    """K5 after the fused all-gather: every warp polls its records in
+    receive area ``parity`` until they carry this layer's epoch, merges the
+    DP copies of each head by LSE, and the last CTA advances the epoch."""
     _need_cuda(grp_ptr, src_idx, out_row)
     n_groups = int(out_row.shape[0])
     _native.check(_lib.fkv_merge_wait(
         endpoint.recv[parity].ptr, endpoint.slots, grp_ptr.data_ptr(), src_idx.data_ptr(),
-        out_row.data_ptr(), n_groups, int(group), _p(out_bf16), _p(out_lse), endpoint.flags.ptr,
-        endpoint.tp, endpoint.consumed, _stream()))
+        out_row.data_ptr(), n_groups, int(group), _p(out_bf16), _p(out_lse), endpoint.epoch,
+        _stream()))
 
 
 def merge_lse(xrec, grp_ptr, src_idx, out_row, group: int, *, out_bf16=None, out_lse=None):

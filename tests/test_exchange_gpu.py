@@ -1,6 +1,6 @@
 """Fused NVLink all-gather protocol (fkv_decode_exchange + fkv_merge_wait),
 exercised with tp virtual ranks on one GPU ("loopback": every peer pointer
-is local memory, same kernels, same flags/parity protocol).  Every rank's
+is local memory, same kernels, same epoch/buffer-rotation protocol).  Every rank's
 o must equal the single-GPU (TP=1) decode, layer after layer, including DP
 copies split along the token axis and a CUDA-graph replay."""
 
@@ -59,7 +59,7 @@ def test_loopback_exchange_matches_single_gpu(cuda_device, tp, mode):
     ref = torch.stack([ops.decode(q[l], base[l])[0] for l in range(L)])
     for r in range(tp):
         torch.testing.assert_close(outs[r].float(), ref.float(), rtol=2e-2, atol=4e-3)
-    # graph replay: flags and counters are monotonic / self-resetting
+    # graph replay: epochs are monotonic, arrival counters self-resetting
     g = torch.cuda.CUDAGraph()
     s = torch.cuda.Stream()
     s.wait_stream(torch.cuda.current_stream())

@@ -4,7 +4,7 @@ GPU of this environment, map each other's receive areas with CUDA IPC
 (exchange.P2PGroup.connect) and run StackDecoder with the P2P exchange.
 Every rank's o must equal the single-GPU decode of the same layers.  This is
 the multi-process path bench.py takes at N > 1 (IPC handles, cross-process
-system-scope flags), minus NVLink itself."""
+epoch-tagged XLL records polled across processes), minus NVLink itself."""
 
 import os
 import socket
