@@ -78,6 +78,7 @@ struct DecodeParams {
   float* out_lse;
   const int32_t* epoch_ctr;  // non-null: out_rec are XLL blocks tagged epoch_ctr[0] + 1
   int after_wait;  // FKV_DECODE_AFTER_WAIT: no global read before griddepcontrol.wait
+  int stamp_slot;  // PROBE 3: stamp block of this launch (0..3)
 };
 
 template <int W>
@@ -231,12 +232,12 @@ __device__ __forceinline__ int piece_tiles(const fkv_work_t& d) {
 // PROBE (diagnostics only, fkv__decode_probe): 1 = stream the tiles without
 // computing, 2 = compute on whatever the ring holds without loading,
 // 3 = full kernel + per-CTA %globaltimer stamps in g_stamps.
-__device__ unsigned long long g_stamps[1024 * 16];
-__device__ __forceinline__ void stamp(int PROBE_, int i) {
+__device__ unsigned long long g_stamps[4 * 1024 * 16];  // [slot][CTA][16]
+__device__ __forceinline__ void stamp(int PROBE_, int slot, int i) {
   if (PROBE_ == 3 && (threadIdx.x & 31) == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    g_stamps[blockIdx.x * 16 + i] = t;
+    g_stamps[(slot * 1024 + blockIdx.x) * 16 + i] = t;
   }
 }
 // SOLO (small shards): every warp streams its own pieces start to finish and
@@ -257,10 +258,11 @@ __global__ void __launch_bounds__(Shape<MODE>::W * 32, Shape<MODE>::kCtasPerSm)
   uint8_t* ring = smem + (kCombiner ? (warp > 0 ? warp - 1 : 0) : warp) * NS * 2 * kTileBytes;
   uint64_t* wbars = sh.bars[warp];
   const fkv_work_t* tab = sh.tab;
+  if (warp == 0) stamp(PROBE, p.stamp_slot, 12);  // entry
   if (PROBE == 3 && threadIdx.x == 0) {
     unsigned smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-    g_stamps[blockIdx.x * 16] = smid;
+    g_stamps[(p.stamp_slot * 1024 + blockIdx.x) * 16] = smid;
   }
 
   // A cache written by the preceding kernel (append / compact): its rows and
@@ -378,7 +380,7 @@ __global__ void __launch_bounds__(Shape<MODE>::W * 32, Shape<MODE>::kCtasPerSm)
   // exchange epoch of this layer: the previous merge_wait advanced the counter
   const uint32_t ep = p.epoch_ctr ? static_cast<uint32_t>(*reinterpret_cast<const volatile int32_t*>(p.epoch_ctr)) + 1u : 0u;
   load_q(0);
-  if (warp == 0) stamp(PROBE, 1);
+  if (warp == 0) stamp(PROBE, p.stamp_slot, 1);
   if (!SOLO && warp == 0) named_arrive<W>(1);  // the hand-over slot starts free
 
   int c_s = 0;        // consumer stage
@@ -421,7 +423,7 @@ __global__ void __launch_bounds__(Shape<MODE>::W * 32, Shape<MODE>::kCtasPerSm)
       if (two && ++c_s == NS) c_s = 0, c_ph ^= 1u;
       mbar_wait(&wbars[sA], phA);
       if (two) mbar_wait(&wbars[sB], phB);
-      if (warp == 0 && pc == 0) stamp(PROBE, 2);
+      if (warp == 0 && pc == 0) stamp(PROBE, p.stamp_slot, 2);
       if (PROBE == 1) {
         __syncwarp();
         c_seq += two ? 2u : 1u;
@@ -538,9 +540,9 @@ __global__ void __launch_bounds__(Shape<MODE>::W * 32, Shape<MODE>::kCtasPerSm)
       named_arrive<W>(2);
       continue;
     }
-    stamp(PROBE, 3);
+    stamp(PROBE, p.stamp_slot, 3);
     if (!SOLO) named_sync<W>(2);
-    stamp(PROBE, 4);
+    stamp(PROBE, p.stamp_slot, 4);
     // warp 0: lane-wise online-softmax combine of the four warps' states
 #pragma unroll 1
     for (int w = 0; w < (SOLO ? 0 : W - 1); ++w) {
@@ -611,11 +613,11 @@ __global__ void __launch_bounds__(Shape<MODE>::W * 32, Shape<MODE>::kCtasPerSm)
     // Warp barrier + one acq_rel atomic (release publishes the whole warp's
     // record stores, acquire makes every other piece's records visible).
     __syncwarp();
-    stamp(PROBE, 6);
+    stamp(PROBE, p.stamp_slot, 6);
     int last = 0;
     if (lane == 0) last = atom_add_acq_rel(p.counters + d.i0, 1) == n_it - 1;
     last = __shfl_sync(0xffffffffu, last, 0);
-    stamp(PROBE, 7);
+    stamp(PROBE, p.stamp_slot, 7);
     if (kCombiner && last && !more) {
       // the CTA's last piece: warps 1-3 are idle, merge with all four (below)
       if (lane == 0) sh.fin_i0 = d.i0, sh.fin_n_it = n_it, sh.fin_orow = static_cast<int32_t>(orow);
@@ -630,7 +632,7 @@ __global__ void __launch_bounds__(Shape<MODE>::W * 32, Shape<MODE>::kCtasPerSm)
     float* sw = SOLO ? &sh.xch[0][0][0] + warp * kMergeMax * 8 : sh.scratch;
     for (int x = lane; x < n_it * G; x += 32) sw[x] = __ldcg(base + x * FKV_REC + FKV_HEAD_DIM);
     __syncwarp();
-    stamp(PROBE, 8);
+    stamp(PROBE, p.stamp_slot, 8);
     float lse_g = -CUDART_INF_F;
     if (lane < G) {
       float M = -CUDART_INF_F;
@@ -644,7 +646,7 @@ __global__ void __launch_bounds__(Shape<MODE>::W * 32, Shape<MODE>::kCtasPerSm)
       lse_g = S > 0.f ? M + __logf(S) : -CUDART_INF_F;
     }
     __syncwarp();
-    stamp(PROBE, 9);
+    stamp(PROBE, p.stamp_slot, 9);
     float4 o[G];
 #pragma unroll
     for (int g = 0; g < G; ++g) o[g] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -662,12 +664,12 @@ __global__ void __launch_bounds__(Shape<MODE>::W * 32, Shape<MODE>::kCtasPerSm)
         o[g].w = fmaf(w, v4[g].w, o[g].w);
       }
     }
-    stamp(PROBE, 10);
+    stamp(PROBE, p.stamp_slot, 10);
 #pragma unroll
     for (int g = 0; g < G; ++g) emit_row_lanes(p, ep, orow + g, o[g], lane);
     emit_lse_lanes<G>(p, ep, orow, lse_g, lane);
     if (lane == 0) p.counters[d.i0] = 0;  // ready for the next launch / graph replay
-    stamp(PROBE, 11);
+    stamp(PROBE, p.stamp_slot, 11);
     __syncwarp();  // the scratch is reused by the next merge
   }
 
@@ -725,7 +727,7 @@ __global__ void __launch_bounds__(Shape<MODE>::W * 32, Shape<MODE>::kCtasPerSm)
     }
   }
 
-  if (warp == 0) stamp(PROBE, 5);
+  if (warp == 0) stamp(PROBE, p.stamp_slot, 5);
 }
 
 // K5 standalone (after the all-gather): warp g of the CTA merges head g of
@@ -886,7 +888,8 @@ extern "C" int fkv_decode_ctas_per_sm(int32_t flags) {
 }
 
 // Diagnostics (not part of fairkv.h): the next fkv_decode call runs probe mode
-// `mode` (1 = loads only, 2 = compute only).  Used by tools/probe_sizes.py.
+// `mode & 15` (1 = loads only, 2 = compute only, 3 = timestamps into stamp
+// block mode >> 4).  Used by tools/probe_*.py.
 extern "C" int fkv__decode_probe(int32_t mode) {
   g_probe = mode;
   return 0;
@@ -947,7 +950,8 @@ extern "C" int fkv_decode_exchange(const void* q, const void* k, const void* v,
   p.out_lse = out_lse;
   p.epoch_ctr = epoch_ctr;
   p.after_wait = (flags & FKV_DECODE_AFTER_WAIT) != 0;
-  const int probe = g_probe;
+  const int probe = g_probe & 15;
+  p.stamp_slot = (g_probe >> 4) & 3;
   g_probe = 0;
   return decode_entry(p, group, static_cast<cudaStream_t>(stream), probe, flags);
 }
