@@ -680,6 +680,7 @@ __global__ void __launch_bounds__(Shape<MODE>::W * 32, Shape<MODE>::kCtasPerSm)
     // warp shuffles.
     named_sync<W>(3);
     const int n_it = sh.fin_n_it;
+    if (warp == 0) stamp(PROBE, p.stamp_slot, 13);
     if (n_it > 0) {
       const float* base = p.part + static_cast<int64_t>(sh.fin_i0) * G * FKV_REC;
       const int64_t orow = sh.fin_orow;
@@ -725,6 +726,7 @@ __global__ void __launch_bounds__(Shape<MODE>::W * 32, Shape<MODE>::kCtasPerSm)
       }
       if (threadIdx.x == 0) p.counters[sh.fin_i0] = 0;
     }
+    if (warp == 0) stamp(PROBE, p.stamp_slot, 14);
   }
 
   if (warp == 0) stamp(PROBE, p.stamp_slot, 5);

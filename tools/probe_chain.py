@@ -19,7 +19,7 @@ tp = int(sys.argv[1]) if len(sys.argv) > 1 else 8
 mode = sys.argv[2] if len(sys.argv) > 2 else "sha"
 B = int(sys.argv[3]) if len(sys.argv) > 3 else 1024
 xchg = len(sys.argv) > 4 and sys.argv[4] == "xchg"
-L, bt, HQ, G, N = 4, 64, 64, 8, 4
+L, bt, HQ, G, N = 16, 64, 64, 8, 4  # 16 chained layers; timestamps of the first N launches
 budgets = synthetic_budgets(L, bt, 8, B, window=32, alpha=0.2, seed=0, context=32768)
 qrow = np.array([b * HQ + h * G for b in range(bt) for h in range(8)])
 base = [LayerCache.allocate(budgets.reshape(L, -1)[l], qrow, qrow, G, dev, fill="random") for l in range(L)]
@@ -36,7 +36,7 @@ o5 = torch.empty((bt, HQ, 128), device=dev, dtype=torch.bfloat16)
 
 def body(probe):
     for l in range(L):
-        if probe:
+        if probe and l < N:
             _native.lib.fkv__decode_probe(3 + 16 * l)
         if xchg:  # this rank's K4 + exchange, then its merge (other ranks' records pre-filled below)
             ops.decode_exchange(q[l], caches[l], grp.endpoints[0], exchange_buffer(l, L), wss[l])
@@ -44,7 +44,20 @@ def body(probe):
             ops.decode_into(q[l], caches[l], wss[l], out_rec=sends[l])
 
 
+def body_mode(mode):
+    for l in range(L):
+        _native.lib.fkv__decode_probe(mode)
+        ops.decode_into(q[l], caches[l], wss[l], out_rec=sends[l])
+
+
 g_plain = bench.capture(lambda: body(False))
+gp = bench.capture(lambda: [ops.decode_partial(q[l], caches[l], wss[l]) for l in range(L)])
+gp.replay()
+print(f"  chained partial records only (no split merges): {min(bench.timed(gp.replay, 1) for _ in range(5)) / L * 1e6:.2f} us/layer")
+for mode, nm in ((1, "loads only"), (2, "compute only")):
+    gm = bench.capture(lambda: body_mode(mode))
+    gm.replay()
+    print(f"  chained {nm}: {min(bench.timed(gm.replay, 1) for _ in range(5)) / L * 1e6:.2f} us/layer")
 g_probe = bench.capture(lambda: body(True))
 for _ in range(3):
     g_probe.replay()
@@ -53,15 +66,16 @@ t_plain = min(bench.timed(g_plain.replay, 1) for _ in range(5)) / L
 n = caches[0].n_workers
 buf = (C.c_ulonglong * (4 * 1024 * 16))()
 _native.lib.fkv__decode_stamps(buf, 4 * 1024 * 16)
-st = np.array(buf, dtype=np.float64).reshape(4, 1024, 16)[:, :n, :]
+st = np.array(buf, dtype=np.float64).reshape(4, 1024, 16)[:, :n, :]  # launches 0..N-1
 times = st[:, :, 1:].copy()
 times[times == 0] = np.nan
 t0 = np.nanmin(times[0, :, 11])  # entry stamp (index 12 -> 11 here)
 rel = (times - t0) / 1e3
 print(f"tp{tp} {mode} B={B} {'xchg' if xchg else 'rec'}: workers {n}, kv {caches[0].kv_bytes()/1e6:.1f} MB/layer, "
       f"flags {caches[0].flags}, chained graph {t_plain*1e6:.2f} us/layer (no probe)")
-cols = {"entry": 11, "pdl-wait": 0, "first-data": 1, "rounds-done": 2, "exit": 4}
-for l in range(L):
+cols = {"entry": 11, "pdl-wait": 0, "combine": 2, "pre-atomic": 5, "post-atomic": 6, "merge0": 12, "merge1": 13,
+        "exit": 4}
+for l in range(N):
     line = f"  launch {l}:"
     for nm, i in cols.items():
         x = rel[l, :, i]
