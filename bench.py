@@ -527,7 +527,12 @@ def run_fairkv(args):
 
 
 # ------------------------------------------------- emulated TP (N = 1) -----
-EMU_REPLAYS = 3  # replays per emulated timing (median of the bracketed spans, min of back-to-back)
+EMU_REPLAYS = 3  # replays per back-to-back emulated timing (min)
+# replays of the event-bracketed graph: CUDA event timestamps are quantised
+# (~0.5 us), so a per-(layer, rank) median of a few replays is a multiple of
+# the quantum and the max over similar ranks picks whichever rounded up; the
+# mean over many replays resolves below the quantum (natural jitter dithers)
+EMU_SPAN_REPLAYS = 16
 EMU_ROUNDS = 3   # interleaved rounds over the placements; the median round is reported
 
 
@@ -611,12 +616,12 @@ def emulate_tp(args, budgets, dev, base, q, tps=(2, 4, 8), modes=("sha",) + AHA_
         def measure(m):
             gph, evs, ggs = m["gph"], m["evs"], m["ggs"]
             span = []
-            for _ in range(EMU_REPLAYS):
+            for _ in range(EMU_SPAN_REPLAYS):
                 gph.replay()
                 torch.cuda.synchronize()
                 span.append(np.array([[evs[l][g].elapsed_time(evs[l][g + 1]) for g in range(tp)]
                                       for l in range(L)]) * 1e-3)
-            t_br = np.median(np.stack(span), axis=0)  # [L, tp], each launch event-bracketed
+            t_br = np.mean(np.stack(span), axis=0)  # [L, tp], each launch event-bracketed
             t = np.empty_like(t_br)
             for g in range(tp):
                 ggs[g].replay()

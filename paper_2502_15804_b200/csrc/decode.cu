@@ -524,6 +524,119 @@ __global__ void __launch_bounds__(Shape<MODE>::W * 32, Shape<MODE>::kCtasPerSm)
     load_q(pc + 1);  // overlaps the hand-over below
     const bool more = pc + 1 < FKV_MAX_WORK && tab[pc + 1].n_it != 0;
 
+    if (kCombiner && !more) {
+      // ---- the CTA's final piece: every warp is idle once it is streamed,
+      // so all W warps combine it, each over its own column blocks (dt),
+      // instead of warp 0 alone -- this combine sits on the launch's
+      // critical path (small TP shards: one piece per CTA)
+      if (warp != 0) {
+        named_sync<W>(1);  // hand-over slot free
+        float* x = &sh.xch[warp - 1][0][lane];
+        x[0 * 32] = m0;
+        x[1 * 32] = m1;
+        x[2 * 32] = l0;
+        x[3 * 32] = l1;
+#pragma unroll
+        for (int dt = 0; dt < 8; ++dt)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) x[(4 + 4 * dt + e) * 32] = acc[dt][e];
+      }
+      named_sync<W>(2);  // every state in shared memory
+      stamp(PROBE, p.stamp_slot, 4);
+      constexpr int kDt = 8 / W;  // column blocks per warp
+      float fm0 = -CUDART_INF_F, fm1 = -CUDART_INF_F, fl0 = 0.f, fl1 = 0.f;
+      float fa[kDt][4];
+#pragma unroll
+      for (int k = 0; k < kDt; ++k) fa[k][0] = fa[k][1] = fa[k][2] = fa[k][3] = 0.f;
+#pragma unroll 1
+      for (int s = 0; s < W - 1; ++s) {
+        const float* x = &sh.xch[s][0][lane];
+        const float om0 = x[0], om1 = x[32], ol0 = x[64], ol1 = x[96];
+        const float nm0 = fmaxf(fm0, om0), nm1 = fmaxf(fm1, om1);
+        const float r0 = nm0 == -CUDART_INF_F ? 0.f : nm0;
+        const float r1 = nm1 == -CUDART_INF_F ? 0.f : nm1;
+        const float a0 = fast_exp2(fm0 - r0), b0 = fast_exp2(om0 - r0);
+        const float a1 = fast_exp2(fm1 - r1), b1 = fast_exp2(om1 - r1);
+        fl0 = fl0 * a0 + ol0 * b0;
+        fl1 = fl1 * a1 + ol1 * b1;
+        fm0 = nm0;
+        fm1 = nm1;
+#pragma unroll
+        for (int k = 0; k < kDt; ++k) {
+          const int dt = warp + k * W;
+          fa[k][0] = fa[k][0] * a0 + x[(4 + 4 * dt + 0) * 32] * b0;
+          fa[k][1] = fa[k][1] * a1 + x[(4 + 4 * dt + 1) * 32] * b1;
+          fa[k][2] = fa[k][2] * a0 + x[(4 + 4 * dt + 2) * 32] * b0;
+          fa[k][3] = fa[k][3] * a1 + x[(4 + 4 * dt + 3) * 32] * b1;
+        }
+      }
+#pragma unroll
+      for (int off = 4; off < 32; off <<= 1) {
+        fl0 += __shfl_xor_sync(0xffffffffu, fl0, off);
+        fl1 += __shfl_xor_sync(0xffffffffu, fl1, off);
+      }
+      const float inv0 = fl0 > 0.f ? 1.f / fl0 : 0.f, inv1 = fl1 > 0.f ? 1.f / fl1 : 0.f;
+      const float lse0 = fl0 > 0.f ? (fm0 + log2f(fl0)) * kLn2 : -CUDART_INF_F;
+      const float lse1 = fl1 > 0.f ? (fm1 + log2f(fl1)) * kLn2 : -CUDART_INF_F;
+      const int n_it = d.n_it;
+      const int64_t orow = d.out_row;
+      if (fused && n_it == 1) {
+        // whole segment: bf16 rows staged in shared memory (the rings: every
+        // copy issued was consumed, streaming is over), then 16-byte stores
+        auto ostage = reinterpret_cast<__nv_bfloat16(*)[FKV_HEAD_DIM]>(smem);
+#pragma unroll
+        for (int k = 0; k < kDt; ++k) {
+          const int d0 = 16 * (warp + k * W) + dr;
+          if (h0 < G) {
+            ostage[h0][d0] = __float2bfloat16_rn(fa[k][0] * inv0);
+            ostage[h0][d0 + 8] = __float2bfloat16_rn(fa[k][2] * inv0);
+          }
+          if (h1 < G) {
+            ostage[h1][d0] = __float2bfloat16_rn(fa[k][1] * inv1);
+            ostage[h1][d0 + 8] = __float2bfloat16_rn(fa[k][3] * inv1);
+          }
+        }
+        named_sync<W>(2);
+        for (int c = threadIdx.x; c < G * 16; c += W * 32)
+          store_o16(p, ep, orow + (c >> 4), 8 * (c & 15),
+                    *reinterpret_cast<const int4*>(&ostage[c >> 4][8 * (c & 15)]));
+        if (warp == 0) {
+          const float la = __shfl_sync(0xffffffffu, lse0, (lane >> 1) & 3);
+          const float lb = __shfl_sync(0xffffffffu, lse1, (lane >> 1) & 3);
+          emit_lse_lanes<G>(p, ep, orow, (lane & 1) ? lb : la, lane);
+        }
+        break;
+      }
+      // split segment: this warp's columns of the piece's partial record
+      float* rec = p.part + static_cast<int64_t>(d.rec) * G * FKV_REC;
+#pragma unroll
+      for (int k = 0; k < kDt; ++k) {
+        const int d0 = 16 * (warp + k * W) + dr;
+        if (h0 < G) {
+          rec[h0 * FKV_REC + d0] = fa[k][0] * inv0;
+          rec[h0 * FKV_REC + d0 + 8] = fa[k][2] * inv0;
+        }
+        if (h1 < G) {
+          rec[h1 * FKV_REC + d0] = fa[k][1] * inv1;
+          rec[h1 * FKV_REC + d0 + 8] = fa[k][3] * inv1;
+        }
+      }
+      if (warp == 0 && lane < 4) {
+        if (h0 < G) rec[h0 * FKV_REC + FKV_HEAD_DIM] = lse0;
+        if (h1 < G) rec[h1 * FKV_REC + FKV_HEAD_DIM] = lse1;
+      }
+      if (!fused) break;
+      // the barrier orders every warp's record stores before thread 0's
+      // acq_rel arrival (cumulative release); the CTA finishing the segment's
+      // last piece merges it after the loop, with all warps
+      named_sync<W>(2);
+      stamp(PROBE, p.stamp_slot, 6);
+      if (threadIdx.x == 0 && atom_add_acq_rel(p.counters + d.i0, 1) == n_it - 1)
+        sh.fin_i0 = d.i0, sh.fin_n_it = n_it, sh.fin_orow = static_cast<int32_t>(orow);
+      stamp(PROBE, p.stamp_slot, 7);
+      break;
+    }
+
     // ---- hand the piece state to warp 0 (shared memory, named barriers):
     // bar 1 = slot free (warp 0 finished the previous piece), bar 2 = slot full
     if (!SOLO && warp != 0) {
