@@ -358,6 +358,68 @@ WIDE_MAX_SEGMENTS = 128
 WIDE_MIN_MEAN_TILES = 6  # probe_sched: wide wins from ~6 tiles per segment (TP=8 B=128 SHA), coop below (its AHA-DP copies, ~4)
 
 
+# Whole-segment schedule (one segment per CTA, no splits) vs the equal-cost
+# split cut, by a linear model of the per-layer K4 time fitted on
+# tools/probe_whole.py (the heaviest rank of TP=4/8 shards of the 70B
+# workload, SHA / AHA-DP, B = 128..1024, 16 chained layers, profiles/):
+#   split ~ S0 + 0.165 us per MB of the cache   (S0: launch, PDL release and
+#           the split-segment merge tail -- record, acq_rel counter, L2 round
+#           trips; larger for the 2-CTA-per-SM shape, more pieces)
+#   whole ~ W0 + per-tile cost x the longest segment (one CTA streams it
+#           alone: 7 streaming warps ~0.1 us per 16-token tile, 3 ~0.285 us)
+#                        S0    W0   us per tile
+WHOLE_MODEL = {"wide": (5.6, 3.5, 0.100), "coop": (7.6, 2.6, 0.285)}
+SPLIT_US_PER_MB = 0.165
+
+
+def whole_segments_win(seg_tiles, workers: int, wide: bool) -> bool:
+    """One segment per CTA beats the split schedule (model above)."""
+    seg_tiles = np.asarray(seg_tiles, dtype=np.int64)
+    n = len(seg_tiles)
+    if not n or n > workers:
+        return False
+    s0, w0, per_tile = WHOLE_MODEL["wide" if wide else "coop"]
+    mb = float(seg_tiles.sum()) * TILE * HEAD_DIM * 4 / 1e6
+    return w0 + per_tile * int(seg_tiles.max()) <= s0 + SPLIT_US_PER_MB * mb
+
+
+def _whole_owners(seg_tiles, sms: int) -> np.ndarray:
+    """CTA id of each segment in the whole-segment schedule: with more
+    segments than SMs, k = n - sms SMs run two CTAs (CTA j and j + sms share
+    an SM, see _pair_on_sms); the longest segments get an SM to themselves and
+    the rest pair longest with shortest."""
+    seg_tiles = np.asarray(seg_tiles, dtype=np.int64)
+    n = len(seg_tiles)
+    k = n - sms
+    if k <= 0:
+        return np.arange(n, dtype=np.int64)
+    order = np.argsort(-seg_tiles, kind="stable")
+    owner = np.empty(n, dtype=np.int64)
+    owner[order[:sms - k]] = np.arange(k, sms)
+    rest = order[sms - k:]
+    for j in range(k):
+        owner[rest[j]] = j
+        owner[rest[2 * k - 1 - j]] = j + sms
+    return owner
+
+
+def plan_work_whole(seg_len, sms: int):
+    """Whole-segment schedule: segment s is the only piece of CTA
+    _whole_owners(...)[s].  Same return convention as ``plan_work``."""
+    seg_len = np.asarray(seg_len, dtype=np.int64)
+    n = len(seg_len)
+    owner = _whole_owners((seg_len + TILE - 1) // TILE, sms)
+    busy = int(owner.max()) + 1
+    item_seg = np.arange(n, dtype=np.int32)
+    t0 = np.zeros(n, dtype=np.int32)
+    t1 = seg_len.astype(np.int32)
+    seg_item_ptr = np.arange(n + 1, dtype=np.int32)
+    warp_ptr = np.zeros(busy + 1, dtype=np.int32)
+    warp_ptr[1:] = np.cumsum(np.bincount(owner, minlength=busy))
+    work_list = np.argsort(owner, kind="stable").astype(np.int32)
+    return item_seg, t0, t1, seg_item_ptr, warp_ptr, work_list
+
+
 def plan_schedule(seg_len, seg_row0, seg_qrow, seg_out_row, device=None, chunk: int | None = None):
     """Pick the K4 schedule for one cache and build its work table.
 
@@ -375,7 +437,11 @@ def plan_schedule(seg_len, seg_row0, seg_qrow, seg_out_row, device=None, chunk: 
     * few segments of >= WIDE_MIN_MEAN_TILES tiles on average (<= WIDE_MAX_SEGMENTS, e.g. a TP=4/8
       rank's KV heads): the cooperative schedule with 8-warp CTAs (one per
       SM, seven streaming warps per piece).
-    FKV_K4_SCHEDULE = coop | wide | solo | auto overrides (measurements).
+    * cooperative schedules: one whole segment per CTA instead of the split
+      cut when the model in ``whole_segments_win`` says the saved merge tail
+      outweighs the longer critical segment (small TP shards).
+    FKV_K4_SCHEDULE = coop | wide | solo | auto and FKV_K4_WHOLE = 0 | 1
+    override (measurements).
     -> (item_seg, t0, t1, seg_item_ptr, warp_ptr, work_list, table, flags)."""
     import os
     seg_len = np.asarray(seg_len, dtype=np.int64)
@@ -412,6 +478,14 @@ def plan_schedule(seg_len, seg_row0, seg_qrow, seg_out_row, device=None, chunk: 
     flags = FKV_DECODE_WIDE if wide else 0
     workers = default_workers(device, flags)
     ctas_sm = max(1, workers // default_workers(device, FKV_DECODE_WIDE))
+    whole = os.environ.get("FKV_K4_WHOLE")
+    if chunk is None and 0 < n_seg <= workers and (
+            whole == "1" or (whole is None and whole_segments_win(seg_tiles, workers, wide))):
+        # one whole segment per CTA: no split-segment LSE merges (their
+        # record -> acq_rel counter -> L2 round trips sit in the launch's tail)
+        plan = plan_work_whole(seg_len, workers // ctas_sm)
+        tab = work_table(seg_row0, seg_len, seg_qrow, seg_out_row, *plan)
+        return (*plan, tab, flags)
     plan = plan_work(seg_len, workers, chunk, sms=workers // ctas_sm if ctas_sm > 1 else None)
     tab = work_table(seg_row0, seg_len, seg_qrow, seg_out_row, *plan)
     return (*plan, tab, flags)

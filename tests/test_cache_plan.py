@@ -187,3 +187,33 @@ def test_sm_pairing_is_a_permutation_that_balances_sms():
     sm_a = ta[:148] + np.append(ta[148:], np.zeros(296 - len(ta)))[:148]
     sm_b = tb[:148] + np.append(tb[148:], np.zeros(296 - len(tb)))[:148]
     assert sm_b.max() - sm_b.min() <= sm_a.max() - sm_a.min()
+
+
+def test_whole_segment_plan_and_choice():
+    """plan_work_whole: every segment is exactly one piece on its own CTA;
+    with more segments than SMs the longest run alone and the rest pair
+    longest-with-shortest (CTA j and j + sms share an SM).  The choice model
+    picks it for small TP shards and keeps the split cut for a TP=1 layer."""
+    from paper_2502_15804_b200.cache import (_whole_owners, plan_work_whole, whole_segments_win,
+                                             work_table)
+    rng = np.random.default_rng(4)
+    seg_len = rng.integers(0, 2000, size=200)
+    sms = 148
+    item_seg, t0, t1, ptr, warp_ptr, work_list = plan_work_whole(seg_len, sms)
+    assert np.array_equal(item_seg, np.arange(200)) and (t0 == 0).all() and np.array_equal(t1, seg_len)
+    assert np.array_equal(ptr, np.arange(201)) and np.array_equal(np.diff(warp_ptr), np.ones(200))
+    tiles = (seg_len + 15) // 16
+    own = _whole_owners(tiles, sms)
+    per_sm = np.bincount(own % sms, weights=tiles, minlength=sms)
+    k = 200 - sms
+    paired = np.bincount(own % sms, minlength=sms) == 2
+    assert paired.sum() == k
+    assert per_sm[~paired].min() >= np.sort(tiles)[::-1][sms - k - 1] - 0  # longest alone
+    tab = work_table(np.arange(200) * 2048, seg_len, np.arange(200) * 8, np.arange(200) * 8,
+                     item_seg, t0, t1, ptr, warp_ptr, work_list)
+    assert tab.shape[:2] == (200, 1) and (tab[:, 0, 7] == 1).all()
+    assert sorted(tab[:, 0, 5].tolist()) == list(range(200))
+    # TP=8 rank at B=256 (64 segments of ~18 tiles): whole; a TP=1 layer: split
+    assert whole_segments_win(np.full(64, 18), 148, True)
+    assert not whole_segments_win(np.full(512, 64), 296, False)   # more segments than CTAs
+    assert not whole_segments_win(np.r_[np.full(63, 40), 200], 148, True)  # one long segment: split it

@@ -94,6 +94,34 @@ def test_decode_many_segments_split(cuda_device, schedule, monkeypatch):
     check_o_lse(o, lse, o_ref, lse_ref)
 
 
+@pytest.mark.parametrize("schedule,bt", [("wide", 8), ("coop", 8), ("coop", 24)])
+def test_decode_whole_segment_schedule(cuda_device, schedule, bt, monkeypatch):
+    """One whole segment per CTA (no split-segment merges; every CTA's only
+    piece is combined by all its warps); bt=24 under coop puts 192 segments on
+    148 SMs: the longest get an SM alone, the rest pair longest with shortest."""
+    from paper_2502_15804_b200 import ops
+    from paper_2502_15804_b200.cache import NUM_SMS, _whole_owners
+    monkeypatch.setenv("FKV_K4_SCHEDULE", schedule)
+    monkeypatch.setenv("FKV_K4_WHOLE", "1")
+    rng = np.random.default_rng(bt)
+    hkv, group = 8, 8
+    seg_lens = rng.integers(0, 900, size=bt * hkv).tolist()
+    seg_lens[:4] = [0, 1, 16, 17]
+    cache, q, ks, vs = build_cache(seg_lens, group, hkv, bt, cuda_device, seed=bt)
+    assert int(np.diff(cache.grp_ptr.cpu().numpy()).max()) == 1  # no segment is split
+    assert cache.flags == {"coop": 0, "wide": 2}[schedule]
+    o, lse = ops.decode(q.to(cuda_device), cache)
+    torch.cuda.synchronize()
+    o_ref, lse_ref = okv.decode_heads(q.float().numpy().astype(np.float64), ks, vs, group)
+    check_o_lse(o, lse, o_ref, lse_ref)
+    if bt == 24:  # SM pairing of the whole-segment schedule
+        tiles = (np.asarray(seg_lens) + 15) // 16
+        own = _whole_owners(tiles, NUM_SMS)
+        assert sorted(own.tolist()) == list(range(len(seg_lens)))
+        alone = own[(own >= len(seg_lens) - NUM_SMS) & (own < NUM_SMS)]
+        assert tiles[np.isin(own, alone)].min() >= tiles[~np.isin(own, alone)].max()
+
+
 def test_decode_large_scores_stable(cuda_device):
     """Large-magnitude logits must not overflow the online softmax."""
     from paper_2502_15804_b200 import ops
