@@ -683,7 +683,11 @@ def calibrate_reference(args, budgets, dev, base, q):
     tokens per request on one GPU-layer) -> the reference's compare()
     predicting the AHA gains at TP 2/4/8.  Samples: whole TP1 layers over the
     first `nh` KV heads of the first `sub` requests, batch 1/4/16/64 x
-    1/2/4/8 heads (batch and load vary independently, as the law needs)."""
+    1/2/4/8 heads (batch and load vary independently, as the law needs),
+    plus the same batches over all 8 heads cut to their first 16 / 64
+    retained tokens: small per-request loads expose the per-request cost
+    (q, o, one segment per head) that the c1 term models -- without them the
+    OLS has nothing to pin c1 and returns it slightly negative (rejected)."""
     import numpy as np
     import torch
     from paper_2502_15804_b200 import ops
@@ -700,6 +704,20 @@ def calibrate_reference(args, budgets, dev, base, q):
             heads = [b * HKV + h for b in range(sub) for h in range(nh)]
             lens = budgets[l].reshape(-1)[heads]
             qrow = np.array([b * HQ + h * GROUP for b in range(sub) for h in range(nh)])
+            c = LayerCache.view(base[l].k, base[l].v, base[l].host["seg_row0"][heads], lens, qrow, qrow, GROUP)
+            qq = q[l, :sub].contiguous()
+            oo = torch.empty_like(qq)
+            ws = ops.DecodeWorkspace(c)
+            g = capture(lambda: [ops.decode_into(qq, c, ws, out_bf16=oo) for _ in range(10)])
+            g.replay()
+            tt = min(timed(g.replay, 1) for _ in range(3)) / 10
+            samples.append(hb.MeasurementSample(sub, float(lens.sum()) / sub, tt))
+    for i, sub in enumerate((1, 4, 16, 64)):
+        for cap in (16, 64):
+            l = (5 * i + cap) % L
+            heads = [b * HKV + h for b in range(sub) for h in range(HKV)]
+            lens = np.minimum(budgets[l].reshape(-1)[heads], cap)
+            qrow = np.array([b * HQ + h * GROUP for b in range(sub) for h in range(HKV)])
             c = LayerCache.view(base[l].k, base[l].v, base[l].host["seg_row0"][heads], lens, qrow, qrow, GROUP)
             qq = q[l, :sub].contiguous()
             oo = torch.empty_like(qq)

@@ -127,3 +127,89 @@ class StackDecoder:
 
     def kv_bytes(self) -> int:
         return sum(c.kv_bytes() for c in self.caches)
+
+
+class DecodeLayer:
+    """One decode layer of the sharded model on one rank, with its weight
+    GEMMs: for x [Bt, Hq*128] bf16 (the layer input, the
+    same on every rank)
+
+      qkv  = x @ W_qkv[:, this rank's heads]    cuBLAS bf16: q of every local
+             KV-head copy's G query heads, k and v of its KV head (AHA-DP
+             copies replicate these columns on every GPU holding the head)
+      append the new k / v to the copies that own their head's token tail
+             (ops.append: a DP copy's earlier token range does not grow)
+      o    = K4 over the local copies + fused NVLink all-gather + K5 LSE merge
+             (ops.decode_exchange / merge_wait; TP = 1: ops.decode_into)
+             -> o [Bt, Hq, 128] on every rank
+      y_g  = o @ W_o[:, g-th 1/tp of the columns]   cuBLAS bf16
+
+    and returns y_g [Bt, Hq*128 / tp] (column-parallel o_proj: the caller
+    all-gathers the y_g into the next layer's x).  The QKV and o_proj GEMMs
+    are plain library GEMMs; the attention between them is this package's
+    kernels.  ``w_qkv`` [Hq*128, (Hq + 2 Hkv)*128] in the usual
+    [q heads | k heads | v heads] column order, ``w_o`` [Hq*128, Hq*128]."""
+
+    def __init__(self, w_qkv: torch.Tensor, w_o: torch.Tensor, cache: LayerCache, shard: LayerShard,
+                 final: FinalMerge | None, *, tp: int, rank: int, bt: int, hq: int, group: int,
+                 endpoint=None, buf: int = 0):
+        d = 128
+        hkv = hq // group
+        hidden = hq * d
+        if w_qkv.shape != (hidden, (hq + 2 * hkv) * d) or w_o.shape != (hidden, hidden):
+            raise ValueError("w_qkv must be [Hq*128, (Hq+2Hkv)*128] and w_o [Hq*128, Hq*128]")
+        if hidden % tp:
+            raise ValueError("Hq*128 must divide by tp (column-parallel o_proj)")
+        if tp > 1 and (endpoint is None or final is None):
+            raise ValueError("tp > 1 needs the exchange endpoint and the final merge tables")
+        heads = np.unique(np.asarray(shard.seg_h, dtype=np.int64))
+        qcols = [np.arange(h * group * d, (h + 1) * group * d) for h in heads]
+        kcols = [hq * d + np.arange(h * d, (h + 1) * d) for h in heads]
+        vcols = [(hq + hkv) * d + np.arange(h * d, (h + 1) * d) for h in heads]
+        cols = np.concatenate(qcols + kcols + vcols) if len(heads) else np.zeros(0, np.int64)
+        dev = cache.k.device
+        self.w_qkv = w_qkv[:, torch.as_tensor(cols, device=w_qkv.device)].contiguous()
+        oc = hidden // tp
+        self.w_o = w_o[:, rank * oc:(rank + 1) * oc].contiguous()
+        self.cache, self.tp, self.rank, self.endpoint, self.buf = cache, tp, rank, endpoint, buf
+        self.bt, self.hq, self.hkv, self.group, self.nh = bt, hq, hkv, group, len(heads)
+        self.heads = torch.as_tensor(heads, device=dev)
+        self.ws = ops.DecodeWorkspace(cache)
+        self.q = torch.zeros((bt, hkv, group, d), dtype=torch.bfloat16, device=dev)
+        self.k_new = torch.zeros((bt, hkv, d), dtype=torch.bfloat16, device=dev)
+        self.v_new = torch.zeros((bt, hkv, d), dtype=torch.bfloat16, device=dev)
+        self.o = torch.empty((bt, hq, d), dtype=torch.bfloat16, device=dev)
+        self.qkv = torch.empty((bt, self.w_qkv.shape[1]), dtype=torch.bfloat16, device=dev)
+        self.y = torch.empty((bt, oc), dtype=torch.bfloat16, device=dev)
+        self.final = None if final is None else tuple(
+            torch.as_tensor(x, device=dev) for x in (final.grp_ptr, final.src_idx, final.out_row))
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        """One decode step of this layer on this rank -> y_g (a view of a
+        buffer reused by the next call)."""
+        self.produce(x)
+        return self.consume()
+
+    # forward() in its two stream-ordered halves: virtual ranks sharing one
+    # GPU (loopback tests) must issue every rank's produce() before any
+    # consume() polls for the peers' records.
+    def produce(self, x: torch.Tensor):
+        """QKV GEMM, append, K4 (+ the fused exchange stores at tp > 1)."""
+        d, G, nh = 128, self.group, self.nh
+        torch.mm(x, self.w_qkv, out=self.qkv)
+        self.q.index_copy_(1, self.heads, self.qkv[:, :nh * G * d].view(self.bt, nh, G, d))
+        self.k_new.index_copy_(1, self.heads, self.qkv[:, nh * G * d:nh * (G + 1) * d].view(self.bt, nh, d))
+        self.v_new.index_copy_(1, self.heads, self.qkv[:, nh * (G + 1) * d:].view(self.bt, nh, d))
+        ops.append(self.cache, self.k_new, self.v_new)
+        q = self.q.view(self.bt, self.hq, d)
+        if self.tp == 1:
+            ops.decode_into(q, self.cache, self.ws, out_bf16=self.o)
+        else:
+            ops.decode_exchange(q, self.cache, self.endpoint, self.buf, self.ws)
+
+    def consume(self) -> torch.Tensor:
+        """K5 merge of the gathered records (tp > 1) and the o_proj GEMM."""
+        if self.tp > 1:
+            ops.merge_wait(self.endpoint, self.buf, *self.final, self.group, out_bf16=self.o)
+        torch.mm(self.o.view(self.bt, self.hq * 128), self.w_o, out=self.y)
+        return self.y
