@@ -212,14 +212,15 @@ struct GridBar {
 // Grid-wide barrier among the epilogue warps of co-resident CTAs (cooperative
 // launch); the TMA and MMA warps keep streaming while the epilogue waits.
 // Monotonic counter (zeroed per launch): arrival k of every CTA lands in
-// [k*N, (k+1)*N), so the returned count names the barrier and its target.
-__device__ __forceinline__ void epi_grid_sync(GridBar* gb) {
+// [k*N, (k+1)*N), so the k-th barrier's target is known up front and the
+// arrival is a fire-and-forget release reduction (the poll is the only
+// round trip).  `k` counts this CTA's barriers (thread 0's copy matters).
+__device__ __forceinline__ void epi_grid_sync(GridBar* gb, unsigned& k) {
   asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps));
   if (threadIdx.x == 0) {
-    const unsigned total = gridDim.x * gridDim.y;
-    unsigned old, v;
-    asm volatile("atom.add.release.gpu.u32 %0, [%1], 1;" : "=r"(old) : "l"(&gb->count) : "memory");
-    const unsigned target = (old / total + 1) * total;
+    const unsigned target = ++k * (gridDim.x * gridDim.y);
+    unsigned v;
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&gb->count) : "memory");
     while (true) {
       asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(v) : "l"(&gb->count) : "memory");
       if (v >= target) break;
@@ -305,10 +306,8 @@ __device__ __forceinline__ void epi_histogram(KeyOf key_of, int nk, uint64_t pre
 // Suffix counts of one global 256-bin histogram by one warp (8 bins per
 // lane): s[j] = base + #keys in bins >= 8*lane + j; `up` = the count past the
 // lane's last bin (base past bin 255).
-__device__ __forceinline__ void warp_suffix8(const uint32_t* gh, int base, int (&s)[8], int& up) {
+__device__ __forceinline__ void warp_suffix8_of(const uint4 x0, const uint4 x1, int base, int (&s)[8], int& up) {
   const int lane = threadIdx.x & 31;
-  const uint4 x0 = __ldcg(reinterpret_cast<const uint4*>(gh + 8 * lane));
-  const uint4 x1 = __ldcg(reinterpret_cast<const uint4*>(gh + 8 * lane + 4));
   const uint32_t h[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
   int run = 0;
 #pragma unroll
@@ -327,6 +326,11 @@ __device__ __forceinline__ void warp_suffix8(const uint32_t* gh, int base, int (
   for (int j = 0; j < 8; ++j) s[j] += higher;
   up = __shfl_down_sync(0xffffffffu, s[0], 1);
   if (lane == 31) up = base;
+}
+__device__ __forceinline__ void warp_suffix8(const uint32_t* gh, int base, int (&s)[8], int& up) {
+  const int lane = threadIdx.x & 31;
+  warp_suffix8_of(__ldcg(reinterpret_cast<const uint4*>(gh + 8 * lane)),
+                  __ldcg(reinterpret_cast<const uint4*>(gh + 8 * lane + 4)), base, s, up);
 }
 
 // Digit histograms of the pooled keys for the global search (keys matching
@@ -366,7 +370,7 @@ __device__ __forceinline__ void epi_histogram2(const float* sp, int nk, bool ga,
 // writes its chosen tokens at the right place of the ascending index list.
 template <class Smem>
 __device__ void select_phase(const ScoreParams& p, Smem& sm, int b, int h, int bh, int chunk, int n,
-                             int t_beg, int nk, const float* sp) {
+                             int t_beg, int nk, const float* sp, unsigned& n_bar) {
   SelScratch& x = *reinterpret_cast<SelScratch*>(&sm.q[0][0][0]);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int HK = p.hkv, BH = gridDim.y;
@@ -395,13 +399,21 @@ __device__ void select_phase(const ScoreParams& p, Smem& sm, int b, int h, int b
       if (fc) atomicAdd(gh + 256 + tid, fc);
     }
     sstamp(2 + 2 * pass);
-    epi_grid_sync(p.gridbar);  // fixed pass count: uniform across the grid
+    epi_grid_sync(p.gridbar, n_bar);  // fixed pass count: uniform across the grid
     sstamp(3 + 2 * pass);
     // decisions, one warp per histogram (8 bins per lane, no block-wide
     // scans): warp w -> suffix counts of head w's global histogram; warp 0
     // also runs my head's floor search (its floor histogram is the global one
     // while the two searches share a prefix)
     const uint32_t* gq = p.hist + (static_cast<int64_t>(pass) * BH + b * HK) * 512;
+    // warp 0 loads my head's floor histogram together with its global one
+    // (one L2 round trip for both)
+    uint4 fx0 = make_uint4(0, 0, 0, 0), fx1 = fx0;
+    if (fa && wid == 0) {
+      const uint32_t* fg = same ? gh : gh + 256;
+      fx0 = __ldcg(reinterpret_cast<const uint4*>(fg + 8 * lane));
+      fx1 = __ldcg(reinterpret_cast<const uint4*>(fg + 8 * lane + 4));
+    }
     if (!exact && wid < HK) {
       int sv[8], up;
       warp_suffix8(gq + wid * 512, x.above[wid], sv, up);
@@ -410,7 +422,7 @@ __device__ void select_phase(const ScoreParams& p, Smem& sm, int b, int h, int b
     }
     if (fa && wid == 0) {  // my head's floor search: d* = max{d : S(d) >= f}
       int sv[8], up;
-      warp_suffix8(same ? gh : gh + 256, x.fabove, sv, up);
+      warp_suffix8_of(fx0, fx1, x.fabove, sv, up);
       int c = 0;
 #pragma unroll
       for (int j = 0; j < 8; ++j) c += sv[j] >= f;
@@ -534,7 +546,7 @@ __device__ void select_phase(const ScoreParams& p, Smem& sm, int b, int h, int b
     *cc = make_int2(a, t2);
   }
   sstamp(31);
-  epi_grid_sync(p.gridbar);
+  epi_grid_sync(p.gridbar, n_bar);
   sstamp(32);
   // this chunk's position in the head's list, and its tie-rank origin
   int64_t pos = 0;
@@ -612,6 +624,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   sstamp(0);
+  unsigned n_bar = 0;  // grid barriers passed (epilogue thread 0)
   const int bh = blockIdx.y, chunk = blockIdx.x;
   const int b = bh / p.hkv, h = bh - b * p.hkv;
   const int n = p.T - p.window;
@@ -797,7 +810,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     if (kFused) {
       sstamp(40);
-      epi_grid_sync(p.gridbar);  // every chunk's statistics are in global memory
+      epi_grid_sync(p.gridbar, n_bar);  // every chunk's statistics are in global memory
       sstamp(41);
       combine_stats();
       asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps));
@@ -852,7 +865,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     if (kFused) {
       sstamp(42);
-      epi_grid_sync(p.gridbar);  // every raw column score is in global memory
+      epi_grid_sync(p.gridbar, n_bar);  // every raw column score is in global memory
       sstamp(43);
       const float* rr = p.raw + static_cast<int64_t>(bh) * n;                 // row half 0
       const float* rr1 = p.raw + (static_cast<int64_t>(gridDim.y) + bh) * n;  // row half 1
@@ -892,7 +905,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (MODE == 4) sp[t - t_beg] = mx;
         }
       }
-      if (MODE == 4) select_phase(p, sm, b, h, bh, chunk, n, t_beg, max(t_end - t_beg, 0), sp);
+      if (MODE == 4) select_phase(p, sm, b, h, bh, chunk, n, t_beg, max(t_end - t_beg, 0), sp, n_bar);
     }
   }
   tc_fence_before();

@@ -13,6 +13,8 @@
 // the same scores, without passes over the index bits.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace fkv {
@@ -114,13 +116,16 @@ __device__ __forceinline__ void gstamp(int i) {
   }
 }
 
-__device__ __forceinline__ void grid_sync(unsigned* bar) {
+// Grid barrier over a counter zeroed per launch: arrival k of every CTA
+// lands in [k*N, (k+1)*N), so the k-th barrier's target is known up front
+// and the arrival is a fire-and-forget release reduction -- the poll that
+// follows it is the only round trip (a returning atomic costs one more).
+__device__ __forceinline__ void grid_sync(unsigned* bar, unsigned& k) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    const unsigned total = gridDim.x;
-    unsigned old, v;
-    asm volatile("atom.add.release.gpu.u32 %0, [%1], 1;" : "=r"(old) : "l"(bar) : "memory");
-    const unsigned target = (old / total + 1) * total;
+    const unsigned target = ++k * gridDim.x;
+    unsigned v;
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
     while (true) {
       asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
       if (v >= target) break;
@@ -132,10 +137,8 @@ __device__ __forceinline__ void grid_sync(unsigned* bar) {
 
 // Suffix counts of one 256-bin histogram (8 bins per lane): s[j] = base +
 // #keys in bins >= 8*lane + j; `up` = s of bin 8*lane + 8 (base past bin 255).
-__device__ __forceinline__ void warp_suffix(const uint32_t* gh, int base, int (&s)[8], int& up) {
+__device__ __forceinline__ void warp_suffix_of(const uint4 x0, const uint4 x1, int base, int (&s)[8], int& up) {
   const int lane = threadIdx.x & 31;
-  const uint4 x0 = __ldcg(reinterpret_cast<const uint4*>(gh + 8 * lane));
-  const uint4 x1 = __ldcg(reinterpret_cast<const uint4*>(gh + 8 * lane + 4));
   const uint32_t h[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
   int run = 0;
 #pragma unroll
@@ -154,6 +157,11 @@ __device__ __forceinline__ void warp_suffix(const uint32_t* gh, int base, int (&
   for (int j = 0; j < 8; ++j) s[j] += higher;
   up = __shfl_down_sync(0xffffffffu, s[0], 1);
   if (lane == 31) up = base;
+}
+__device__ __forceinline__ void warp_suffix(const uint32_t* gh, int base, int (&s)[8], int& up) {
+  const int lane = threadIdx.x & 31;
+  warp_suffix_of(__ldcg(reinterpret_cast<const uint4*>(gh + 8 * lane)),
+                 __ldcg(reinterpret_cast<const uint4*>(gh + 8 * lane + 4)), base, s, up);
 }
 
 __device__ __forceinline__ int rule_class(const GRule& r, uint32_t o) {
@@ -242,9 +250,11 @@ __global__ void __launch_bounds__(kGThreads) grid_select_kernel(const GSelParams
   }
   gstamp(0);
   __syncthreads();
+  unsigned n_bar = 0;  // grid barriers passed (thread 0)
 
   for (int pass = 0, shift = 24; pass < 4; ++pass, shift -= 8) {
     uint32_t* hb = p.hist + (pass % kGBufs) * buf_words;
+    gstamp(23 + 2 * pass);
     // ---- my pieces' digit histograms into hb
     for (int lh = 0; lh < n_lh; ++lh) {
       const int bh = bh_lo + lh, h = bh % HK;
@@ -284,6 +294,7 @@ __global__ void __launch_bounds__(kGThreads) grid_select_kernel(const GSelParams
         for_keys(s, lo, hi, add);
       }
       __syncthreads();
+      if (lh == 0) gstamp(24 + 2 * pass);
       uint32_t* gh = hb + static_cast<int64_t>(bh) * 512;
       if (tid < 256) {
         const uint32_t c = sm.hist[0][tid];
@@ -298,7 +309,7 @@ __global__ void __launch_bounds__(kGThreads) grid_select_kernel(const GSelParams
       __syncthreads();
     }
     gstamp(1 + 3 * pass);
-    grid_sync(p.bar);
+    grid_sync(p.bar, n_bar);
     gstamp(2 + 3 * pass);
     // the buffer of pass + 2 was last read by pass - 1's decisions (before
     // this barrier) and is next written after the next one; the CTA holding
@@ -310,6 +321,16 @@ __global__ void __launch_bounds__(kGThreads) grid_select_kernel(const GSelParams
         piece(lh, lo, hi);
         if (lo == 0) (zb + static_cast<int64_t>(bh_lo + lh) * 512)[tid] = 0;
       }
+    }
+    // my heads' floor histograms (one warp per local head), loaded now so the
+    // round trip overlaps the global decisions' (both are L2 reads of this
+    // pass's histograms)
+    const bool fjob = wid < n_lh && sm.fact[wid];
+    uint4 fx0 = make_uint4(0, 0, 0, 0), fx1 = fx0;
+    if (fjob) {
+      const uint32_t* fg = hb + static_cast<int64_t>(bh_lo + wid) * 512 + 256;
+      fx0 = __ldcg(reinterpret_cast<const uint4*>(fg + 8 * lane));
+      fx1 = __ldcg(reinterpret_cast<const uint4*>(fg + 8 * lane + 4));
     }
     // ---- global decisions of my requests: d* = max{d : G(d) >= R}
     for (int lr = 0; lr < n_lr; ++lr) {
@@ -342,11 +363,11 @@ __global__ void __launch_bounds__(kGThreads) grid_select_kernel(const GSelParams
     }
     gstamp(3 + 3 * pass);
     // ---- floor decisions of my heads (one warp each): f-th largest
-    for (int lh = wid; lh < n_lh; lh += kGWarps) {
+    for (int lh = wid; lh < n_lh; lh += kGWarps) {  // n_lh <= kGMaxPieces == kGWarps: one pass
       GHead& fh = sm.fl[lh];
       if (!sm.fact[lh]) continue;
       int sv[8], up;
-      warp_suffix(hb + static_cast<int64_t>(bh_lo + lh) * 512 + 256, fh.above, sv, up);
+      warp_suffix_of(fx0, fx1, fh.above, sv, up);
       int c = 0;
 #pragma unroll
       for (int j = 0; j < 8; ++j) c += sv[j] >= fh.f;
@@ -527,7 +548,7 @@ __global__ void __launch_bounds__(kGThreads) grid_select_kernel(const GSelParams
     p.counts[blockIdx.x] = make_int2(x, y);
   }
   gstamp(20);
-  grid_sync(p.bar);
+  grid_sync(p.bar, n_bar);
   gstamp(21);
 
   // ---- chosen tokens of my pieces, ascending, at their place in the list;
@@ -640,7 +661,11 @@ int gsel_ctas() {
 // CTAs of a launch over `bh` heads of n keys.
 int gsel_grid(int bh, int n) {
   const int64_t total = static_cast<int64_t>(bh) * n;
-  int64_t want = (total + kGMinKeys - 1) / kGMinKeys;
+  static const int min_keys = [] {
+    const char* e = getenv("FKV_GSEL_MIN_KEYS");  // tuning experiments
+    return e ? atoi(e) : kGMinKeys;
+  }();
+  int64_t want = (total + min_keys - 1) / min_keys;
   // short heads: enough CTAs that no key range spans more than kGMaxPieces
   // heads (ranges of <= (kGMaxPieces - 2) * n keys); gsel_reqs_per_launch
   // keeps this within the co-resident grid

@@ -10,7 +10,7 @@ import torch
 from paper_2502_15804_b200 import ops, _native
 import bench
 dev = torch.device("cuda:0")
-for bt, n, B in ((1, 16384 - 32, 256), (4, 16384 - 32, 256), (1, 32768 - 32, 1024), (1, 131072 - 32, 1024)):
+for bt, n, B in ((1, 16384 - 32, 256), (1, 131072 - 32, 1024)):
     s = torch.rand(bt, 8, n, generator=torch.Generator().manual_seed(0)).to(dev)
     ws = torch.empty(int(_native.lib.fkv_ada_select_workspace_bytes(bt, 8, n)), dtype=torch.uint8, device=dev)
     ops.ada_select(s, B, workspace=ws)
@@ -26,6 +26,8 @@ for bt, n, B in ((1, 16384 - 32, 256), (4, 16384 - 32, 256), (1, 32768 - 32, 102
     rel = lambda i: (st[i] - t0) / 1e3 if st[i] else float("nan")  # noqa: E731
     phases = []
     for p in range(4):
-        phases.append(f"p{p}: hist {rel(1 + 3 * p):5.2f} bar {rel(2 + 3 * p):5.2f} dec {rel(3 + 3 * p):5.2f}")
+        phases.append(f"p{p}: start {rel(23 + 2 * p):5.2f} keys {rel(24 + 2 * p):5.2f} hist {rel(1 + 3 * p):5.2f} "
+                      f"bar {rel(2 + 3 * p):5.2f} dec {rel(3 + 3 * p):5.2f}")
     print(f"bt={bt} n={n + 32} B={B}: graph replay {t * 1e6:6.2f} us; CTA0 (us from its start): "
           + " | ".join(phases) + f" | counts {rel(20):5.2f} bar {rel(21):5.2f} end {rel(22):5.2f}", flush=True)
+
