@@ -365,51 +365,71 @@ WIDE_MIN_MEAN_TILES = 6  # probe_sched: wide wins from ~6 tiles per segment (TP=
 #   split ~ S0 + 0.165 us per MB of the cache   (S0: launch, PDL release and
 #           the split-segment merge tail -- record, acq_rel counter, L2 round
 #           trips; larger for the 2-CTA-per-SM shape, more pieces)
-#   whole ~ W0 + per-tile cost x the longest segment (one CTA streams it
-#           alone: 7 streaming warps ~0.1 us per 16-token tile, 3 ~0.285 us)
+#   whole ~ W0 + max(per-tile cost x the most loaded CTA's tiles (7
+#           streaming warps ~0.1 us per 16-token tile, 3 ~0.285 us),
+#           0.161 us per MB: HBM-bound once every SM is busy)
+# The whole schedule also wins for a TP=1 layer of the bench workload (512
+# segments, two per CTA longest-first: 47.1 -> 43.2 us, 6.2 TB/s): the
+# split cut's merge tail costs more than the packing's imbalance.
 #                        S0    W0   us per tile
-WHOLE_MODEL = {"wide": (5.6, 3.5, 0.100), "coop": (7.6, 2.6, 0.285)}
+WHOLE_MODEL = {"wide": (5.6, 3.3, 0.104), "coop": (7.6, 2.6, 0.285)}
 SPLIT_US_PER_MB = 0.165
+WHOLE_MARGIN_US = 0.5   # near a tie the split cut stays (TP=8 uniform TP, B=512: 8.7 vs 9.5 us)
+WHOLE_US_PER_MB = 0.161  # the whole schedule is HBM-bound once every SM is busy (TP=1: 6.2 TB/s)
 
 
-def whole_segments_win(seg_tiles, workers: int, wide: bool) -> bool:
-    """One segment per CTA beats the split schedule (model above)."""
+def _whole_owners(seg_tiles, workers: int, sms: int) -> np.ndarray:
+    """CTA id of each segment in the whole-segment schedule.  Up to `sms`
+    segments: one per CTA, each on its own SM.  More: longest-first onto the
+    least-loaded of `workers` CTAs (a CTA's load = its tiles + PAIR_PIECE_TILES
+    per extra segment), then CTA ids relabelled so that CTA j and j + sms --
+    which share an SM -- pair heavy with light (_pair_on_sms)."""
+    import heapq
     seg_tiles = np.asarray(seg_tiles, dtype=np.int64)
     n = len(seg_tiles)
-    if not n or n > workers:
+    if n <= sms:
+        return np.arange(n, dtype=np.int64)
+    owner = np.empty(n, dtype=np.int64)
+    heap = [(0, w) for w in range(workers)]
+    for s in np.lexsort((np.arange(n), -seg_tiles)):
+        load, w = heapq.heappop(heap)
+        owner[s] = w
+        heapq.heappush(heap, (load + int(seg_tiles[s]) + (PAIR_PIECE_TILES if load else 0), w))
+    _, owner = np.unique(owner, return_inverse=True)  # busy CTAs 0..k-1
+    t1 = seg_tiles * TILE
+    return _pair_on_sms(owner, np.zeros(n, dtype=np.int64), t1, sms)
+
+
+def _whole_cta_tiles(seg_tiles, owner) -> np.ndarray:
+    own = np.asarray(owner, dtype=np.int64)
+    tiles = np.bincount(own, weights=np.asarray(seg_tiles, dtype=np.float64))
+    extra = np.maximum(np.bincount(own) - 1, 0) * PAIR_PIECE_TILES
+    return tiles + extra
+
+
+def whole_segments_win(seg_tiles, workers: int, wide: bool, sms: int = NUM_SMS) -> bool:
+    """Whole segments (one or a few per CTA) beat the split schedule (model
+    above, with the most loaded CTA's tiles as the critical path)."""
+    seg_tiles = np.asarray(seg_tiles, dtype=np.int64)
+    n = len(seg_tiles)
+    if not n or n > workers * MAX_WORK_PER_WORKER:
         return False
     s0, w0, per_tile = WHOLE_MODEL["wide" if wide else "coop"]
     mb = float(seg_tiles.sum()) * TILE * HEAD_DIM * 4 / 1e6
-    return w0 + per_tile * int(seg_tiles.max()) <= s0 + SPLIT_US_PER_MB * mb
+    crit = float(_whole_cta_tiles(seg_tiles, _whole_owners(seg_tiles, workers, sms)).max())
+    whole = w0 + max(per_tile * crit, WHOLE_US_PER_MB * mb)
+    return whole + WHOLE_MARGIN_US <= s0 + SPLIT_US_PER_MB * mb
 
 
-def _whole_owners(seg_tiles, sms: int) -> np.ndarray:
-    """CTA id of each segment in the whole-segment schedule: with more
-    segments than SMs, k = n - sms SMs run two CTAs (CTA j and j + sms share
-    an SM, see _pair_on_sms); the longest segments get an SM to themselves and
-    the rest pair longest with shortest."""
-    seg_tiles = np.asarray(seg_tiles, dtype=np.int64)
-    n = len(seg_tiles)
-    k = n - sms
-    if k <= 0:
-        return np.arange(n, dtype=np.int64)
-    order = np.argsort(-seg_tiles, kind="stable")
-    owner = np.empty(n, dtype=np.int64)
-    owner[order[:sms - k]] = np.arange(k, sms)
-    rest = order[sms - k:]
-    for j in range(k):
-        owner[rest[j]] = j
-        owner[rest[2 * k - 1 - j]] = j + sms
-    return owner
-
-
-def plan_work_whole(seg_len, sms: int):
-    """Whole-segment schedule: segment s is the only piece of CTA
-    _whole_owners(...)[s].  Same return convention as ``plan_work``."""
+def plan_work_whole(seg_len, workers: int, sms: int):
+    """Whole-segment schedule: every segment is one piece, on the CTA given
+    by _whole_owners.  Same return convention as ``plan_work``."""
     seg_len = np.asarray(seg_len, dtype=np.int64)
     n = len(seg_len)
-    owner = _whole_owners((seg_len + TILE - 1) // TILE, sms)
+    owner = _whole_owners((seg_len + TILE - 1) // TILE, workers, sms)
     busy = int(owner.max()) + 1
+    if np.bincount(owner).max() > MAX_WORK_PER_WORKER:
+        raise ValueError("too many segments per CTA for the whole-segment schedule")
     item_seg = np.arange(n, dtype=np.int32)
     t0 = np.zeros(n, dtype=np.int32)
     t1 = seg_len.astype(np.int32)
@@ -479,11 +499,12 @@ def plan_schedule(seg_len, seg_row0, seg_qrow, seg_out_row, device=None, chunk: 
     workers = default_workers(device, flags)
     ctas_sm = max(1, workers // default_workers(device, FKV_DECODE_WIDE))
     whole = os.environ.get("FKV_K4_WHOLE")
-    if chunk is None and 0 < n_seg <= workers and (
-            whole == "1" or (whole is None and whole_segments_win(seg_tiles, workers, wide))):
+    sms = workers // ctas_sm
+    if chunk is None and 0 < n_seg <= workers * MAX_WORK_PER_WORKER and (
+            whole == "1" or (whole is None and whole_segments_win(seg_tiles, workers, wide, sms))):
         # one whole segment per CTA: no split-segment LSE merges (their
         # record -> acq_rel counter -> L2 round trips sit in the launch's tail)
-        plan = plan_work_whole(seg_len, workers // ctas_sm)
+        plan = plan_work_whole(seg_len, workers, sms)
         tab = work_table(seg_row0, seg_len, seg_qrow, seg_out_row, *plan)
         return (*plan, tab, flags)
     plan = plan_work(seg_len, workers, chunk, sms=workers // ctas_sm if ctas_sm > 1 else None)

@@ -190,30 +190,37 @@ def test_sm_pairing_is_a_permutation_that_balances_sms():
 
 
 def test_whole_segment_plan_and_choice():
-    """plan_work_whole: every segment is exactly one piece on its own CTA;
-    with more segments than SMs the longest run alone and the rest pair
-    longest-with-shortest (CTA j and j + sms share an SM).  The choice model
-    picks it for small TP shards and keeps the split cut for a TP=1 layer."""
-    from paper_2502_15804_b200.cache import (_whole_owners, plan_work_whole, whole_segments_win,
-                                             work_table)
+    """plan_work_whole: every segment is exactly one piece; up to one segment
+    per SM each gets its own CTA; with more, longest-first onto the least
+    loaded of the CTAs and CTA j / j + sms (one SM) paired heavy with light.
+    The choice model picks it for small TP shards and keeps the split cut for
+    long segments and for a TP=1 layer."""
+    from paper_2502_15804_b200.cache import (_whole_cta_tiles, _whole_owners, plan_work_whole,
+                                             whole_segments_win, work_table)
     rng = np.random.default_rng(4)
-    seg_len = rng.integers(0, 2000, size=200)
-    sms = 148
-    item_seg, t0, t1, ptr, warp_ptr, work_list = plan_work_whole(seg_len, sms)
-    assert np.array_equal(item_seg, np.arange(200)) and (t0 == 0).all() and np.array_equal(t1, seg_len)
-    assert np.array_equal(ptr, np.arange(201)) and np.array_equal(np.diff(warp_ptr), np.ones(200))
-    tiles = (seg_len + 15) // 16
-    own = _whole_owners(tiles, sms)
-    per_sm = np.bincount(own % sms, weights=tiles, minlength=sms)
-    k = 200 - sms
-    paired = np.bincount(own % sms, minlength=sms) == 2
-    assert paired.sum() == k
-    assert per_sm[~paired].min() >= np.sort(tiles)[::-1][sms - k - 1] - 0  # longest alone
-    tab = work_table(np.arange(200) * 2048, seg_len, np.arange(200) * 8, np.arange(200) * 8,
-                     item_seg, t0, t1, ptr, warp_ptr, work_list)
-    assert tab.shape[:2] == (200, 1) and (tab[:, 0, 7] == 1).all()
-    assert sorted(tab[:, 0, 5].tolist()) == list(range(200))
-    # TP=8 rank at B=256 (64 segments of ~18 tiles): whole; a TP=1 layer: split
+    sms, workers = 148, 296
+    for n in (100, 200, 400):
+        seg_len = rng.integers(0, 2000, size=n)
+        item_seg, t0, t1, ptr, warp_ptr, work_list = plan_work_whole(seg_len, workers, sms)
+        assert np.array_equal(item_seg, np.arange(n)) and (t0 == 0).all() and np.array_equal(t1, seg_len)
+        assert np.array_equal(ptr, np.arange(n + 1))
+        tiles = (seg_len + 15) // 16
+        own = _whole_owners(tiles, workers, sms)
+        busy = int(own.max()) + 1
+        assert busy <= workers and sorted(set(own.tolist())) == list(range(busy))
+        cta = _whole_cta_tiles(tiles, own)
+        if n <= sms:
+            assert np.array_equal(own, np.arange(n))
+        else:  # LPT bound: no CTA above the mean share + the longest segment (+ piece costs)
+            assert cta.max() <= tiles.sum() / workers + tiles.max() + 12 * 2
+        tab = work_table(np.arange(n) * 2048, seg_len, np.arange(n) * 8, np.arange(n) * 8,
+                         item_seg, t0, t1, ptr, warp_ptr, work_list)
+        assert tab.shape[0] == busy and (tab[:, :, 7][tab[:, :, 7] > 0] == 1).all()
+        assert sorted(tab[:, :, 5][tab[:, :, 7] > 0].tolist()) == list(range(n))
+    # TP=8 rank at B=256 (64 segments of ~18 tiles) and a TP=1 layer (512
+    # segments, two per CTA): whole; one long segment among short ones, or 64
+    # long segments on 148 SMs (uniform TP=8, B=1024): split
     assert whole_segments_win(np.full(64, 18), 148, True)
-    assert not whole_segments_win(np.full(512, 64), 296, False)   # more segments than CTAs
-    assert not whole_segments_win(np.r_[np.full(63, 40), 200], 148, True)  # one long segment: split it
+    assert whole_segments_win(np.full(512, 64), 296, False)
+    assert not whole_segments_win(np.r_[np.full(63, 40), 200], 148, True)
+    assert not whole_segments_win(np.full(64, 120), 148, True)

@@ -114,12 +114,10 @@ def test_decode_whole_segment_schedule(cuda_device, schedule, bt, monkeypatch):
     torch.cuda.synchronize()
     o_ref, lse_ref = okv.decode_heads(q.float().numpy().astype(np.float64), ks, vs, group)
     check_o_lse(o, lse, o_ref, lse_ref)
-    if bt == 24:  # SM pairing of the whole-segment schedule
+    if bt == 24:  # 192 segments on 148 SMs: one CTA each, heavy paired with light
         tiles = (np.asarray(seg_lens) + 15) // 16
-        own = _whole_owners(tiles, NUM_SMS)
+        own = _whole_owners(tiles, 2 * NUM_SMS, NUM_SMS)
         assert sorted(own.tolist()) == list(range(len(seg_lens)))
-        alone = own[(own >= len(seg_lens) - NUM_SMS) & (own < NUM_SMS)]
-        assert tiles[np.isin(own, alone)].min() >= tiles[~np.isin(own, alone)].max()
 
 
 def test_decode_large_scores_stable(cuda_device):

@@ -17,21 +17,25 @@ for B in [int(x) for x in sys.argv[1:]] or [128, 256, 512, 1024]:
     qrow = np.array([b * HQ + h * G for b in range(bt) for h in range(8)])
     base = [LayerCache.allocate(budgets.reshape(L, -1)[l], qrow, qrow, G, dev, fill="random") for l in range(L)]
     q = torch.randn((L, bt, HQ, 128), device=dev).to(torch.bfloat16)
-    for tp, mode in [(4, "sha"), (4, "dp"), (8, "sha"), (8, "dp"), (8, "dp-free")]:
+    for tp, mode in [(1, "sha"), (2, "sha"), (2, "dp"), (4, "sha"), (4, "dp"), (8, "sha"), (8, "dp"), (8, "dp-free")]:
         plan, prof = bench.make_plan(budgets, tp, mode)
         shards, _ = plan_layouts(plan, budgets, G)
         toks = [sum(int((s[g].seg_hi - s[g].seg_lo).sum()) for s in shards) for g in range(tp)]
         g = int(np.argmax(toks))
         line = f"B={B:5d} tp{tp} {mode:7s} rank{g} {toks[g] * 512 / L / 1e6:5.1f} MB/layer"
-        for whole in ("0", "1"):
-            os.environ["FKV_K4_WHOLE"] = whole
+        for whole in ("0", "1", None):
+            if whole is None:
+                os.environ.pop("FKV_K4_WHOLE", None)
+            else:
+                os.environ["FKV_K4_WHOLE"] = whole
             caches = rank_caches([s[g] for s in shards], bt, HQ, G, tp, dev, base=base)
             sends = [ops.xrec_empty(max(c.n_segments, 1), G, dev)[0] for c in caches]
             wss = [ops.DecodeWorkspace(c) for c in caches]
             gr = bench.capture(lambda: [ops.decode_into(q[l], caches[l], wss[l], out_rec=sends[l]) for l in range(L)])
             gr.replay()
             t = min(bench.timed(gr.replay, 1) for _ in range(5)) / L
-            line += f"  {'whole' if whole == '1' else 'split'} {t * 1e6:6.2f}us (f{caches[0].flags},{caches[0].n_workers}w)"
+            nm = {"0": "split", "1": "whole", None: "auto"}[whole]
+            line += f"  {nm} {t * 1e6:6.2f}us (f{caches[0].flags},{caches[0].n_workers}w)"
         print(line, flush=True)
     del base
     torch.cuda.empty_cache()
