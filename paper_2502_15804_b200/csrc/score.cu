@@ -9,19 +9,20 @@
 //
 // Two tcgen05 passes over K, each CTA owning (request, KV head, key chunk):
 //   pass 1  D[GW rows x 128 keys]   = Q_win . K_tile^T  -> per-row online max
-//           and sum-exp with rows in TMEM lanes (thread-local reductions);
+//           and sum-exp with rows in TMEM lanes (thread-local reductions,
+//           one partial per column group, combined once per chunk);
 //   pass 2  D^T[128 keys x GW rows] = K_tile . Q_win^T  -> per-key column
 //           sums of exp(s - m_r)/l_r with keys in TMEM lanes (thread-local);
-//           the two row halves (warps 0-3 / 4-7) store separate partial
+//           the four column groups (warps 4c..4c+3) store separate partial
 //           sums, added by the pooling (no block barrier per tile).
 // Q_win (GW = G*w = 128 or 256 rows) is TMA-loaded once per CTA and stays in
 // shared memory; K tiles (128 keys x 128 d, 32 KiB) stream through a 3-stage
 // TMA ring with 128-B swizzle; one elected thread issues
 // tcgen05.mma.cta_group::1.kind::f16 (M=128, N=128 or GW, K=16) into fp32
-// TMEM accumulators (512 / GW buffers: all 512 columns); eight epilogue warps
-// drain them with tcgen05.ld (warp e reads TMEM lanes 32*(e%4) and half e/4
-// of the columns) and hand each buffer back as soon as it is in registers.
-// Warp roles: 0-7 epilogue, 8 TMA producer, 9 MMA issuer.  Grid: one wave
+// TMEM accumulators (512 / GW buffers: all 512 columns); sixteen epilogue
+// warps drain them with tcgen05.ld (warp e reads TMEM lanes 32*(e%4) and
+// column group e/4) and hand each buffer back as soon as it is in registers.
+// Warp roles: 0-15 epilogue, 16 TMA producer, 17 MMA issuer.  Grid: one wave
 // of one CTA per SM ((Bt*Hkv) x chunks <= #SMs) when that keeps >= 80 % of
 // the SMs busy, else wave-filled chunks over several launches (score_chunks).
 // The second pass re-reads K mostly from L2 (a layer's K for one request is
@@ -39,9 +40,14 @@ namespace {
 constexpr int kBN = 128;                 // keys per tile
 constexpr int kStages = 3;
 constexpr int kTileBytes = kBN * 256;    // 128 keys x 128 d x bf16
-constexpr int kEpiWarps = 8;
+// 16 epilogue warps: four per SM sub-partition, so one warp's TMEM-load wait
+// is covered by the others' exponentials (the MUFU pipe is the bound)
+constexpr int kEpiWarps = 16;
 constexpr int kTmaWarp = kEpiWarps, kMmaWarp = kEpiWarps + 1;
 constexpr int kThreads = 32 * (kEpiWarps + 2);
+constexpr int kRawParts = 4;  // column partial sums per key written by pass 2 (one per column quarter)
+// the selection phase runs on epilogue warps 0-7 (named barrier 2)
+constexpr int kSelWarps = 8, kSelThreads = 32 * kSelWarps;
 constexpr float kLog2e = 1.4426950408889634f;
 
 struct ScoreParams {
@@ -202,7 +208,7 @@ struct __align__(1024) ScoreSmem {
   uint64_t full[kStages], empty[kStages], tfull[512 / GW], tempty[512 / GW], qbar;
   uint32_t tmem_base;
   alignas(16) float bias[GW];  // pass 2: per query row, m_r + log2(G * l_r) (log2 units)
-  float ml[kBN][2];          // pass 1, GW=128: second column half's (max, sum) per row
+  float ml[4 * 128 * 2];     // pass 1: per-row (max, sum) partials of column groups 1..3 -> group 0
 };
 
 struct GridBar {
@@ -215,8 +221,9 @@ struct GridBar {
 // [k*N, (k+1)*N), so the k-th barrier's target is known up front and the
 // arrival is a fire-and-forget release reduction (the poll is the only
 // round trip).  `k` counts this CTA's barriers (thread 0's copy matters).
+template <int BAR = 1, int NT = 32 * kEpiWarps>
 __device__ __forceinline__ void epi_grid_sync(GridBar* gb, unsigned& k) {
-  asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps));
+  asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(NT));
   if (threadIdx.x == 0) {
     const unsigned target = ++k * (gridDim.x * gridDim.y);
     unsigned v;
@@ -227,7 +234,7 @@ __device__ __forceinline__ void epi_grid_sync(GridBar* gb, unsigned& k) {
       __nanosleep(32);
     }
   }
-  asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps));
+  asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(NT));
 }
 
 // diagnostics: %globaltimer stamps of CTA (0,0) through the fused select
@@ -242,6 +249,7 @@ __device__ __forceinline__ void sstamp(int i) {
 }
 
 __device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps)); }
+__device__ __forceinline__ void sel_sync() { asm volatile("bar.sync 2, %0;" ::"n"(kSelThreads)); }
 
 __device__ __forceinline__ uint32_t orderable(float f) {
   const uint32_t u = __float_as_uint(f);
@@ -253,54 +261,21 @@ struct SelScratch {
   int32_t suf[kSelMaxHeads][256];  // per-head suffix counts of the current digit
   uint32_t hist[256], hist2[256];  // this chunk's digits: global search, floor search
   int32_t above[kSelMaxHeads], n_at[kSelMaxHeads];
-  int32_t warp_tot[kEpiWarps];
+  int32_t warp_tot[kSelWarps];
   int32_t dstar, exact;
   uint32_t fprefix, fmask;  // floor search of this CTA's head
   int32_t fexact, fabove;
 };
 
-// Inclusive suffix sum over d of one value per epilogue thread (d = tid).
-__device__ __forceinline__ int32_t epi_suffix_sum(int32_t v, SelScratch& x) {
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const int32_t y = __shfl_down_sync(0xffffffffu, v, off);
-    if (lane + off < 32) v += y;
-  }
-  if (lane == 0) x.warp_tot[w] = v;
-  epi_sync();
-  for (int j = w + 1; j < kEpiWarps; ++j) v += x.warp_tot[j];
-  epi_sync();
-  return v;
-}
-
 __device__ __forceinline__ int32_t epi_count(bool pred, SelScratch& x) {
   const int tid = threadIdx.x;
   const uint32_t bal = __ballot_sync(0xffffffffu, pred);
   if ((tid & 31) == 0) x.warp_tot[tid >> 5] = __popc(bal);
-  epi_sync();
+  sel_sync();
   int32_t c = 0;
-  for (int j = 0; j < kEpiWarps; ++j) c += x.warp_tot[j];
-  epi_sync();
+  for (int j = 0; j < kSelWarps; ++j) c += x.warp_tot[j];
+  sel_sync();
   return c;
-}
-
-// Warp-aggregated digit histogram of the keys matching (prefix, mask).
-template <class KeyOf>
-__device__ __forceinline__ void epi_histogram(KeyOf key_of, int nk, uint64_t prefix, uint64_t mask,
-                                              int shift, uint32_t* hist) {
-  const int lane = threadIdx.x & 31;
-  for (int i = threadIdx.x; i < 256; i += 32 * kEpiWarps) hist[i] = 0;
-  epi_sync();
-  for (int base = 0; base < nk; base += 32 * kEpiWarps) {
-    const int i = base + threadIdx.x;
-    uint64_t key = 0;
-    const bool ok = i < nk && ((key = key_of(i)) & mask) == prefix;
-    const uint32_t d = ok ? static_cast<uint32_t>(key >> shift) & 255u : 256u;
-    const uint32_t peers = __match_any_sync(0xffffffffu, d);
-    if (ok && lane == __ffs(peers) - 1) atomicAdd(&hist[d], __popc(peers));
-  }
-  epi_sync();
 }
 
 // Suffix counts of one global 256-bin histogram by one warp (8 bins per
@@ -340,14 +315,15 @@ __device__ __forceinline__ void epi_histogram2(const float* sp, int nk, bool ga,
                                                uint32_t* h1) {
   h0[threadIdx.x] = 0;
   h1[threadIdx.x] = 0;
-  epi_sync();
-  for (int i = threadIdx.x; i < nk; i += 32 * kEpiWarps) {
+  sel_sync();
+#pragma unroll 4
+  for (int i = threadIdx.x; i < nk; i += kSelThreads) {
     const uint32_t o = orderable(sp[i]);
     const uint32_t d = (o >> shift) & 255u;
     if (ga && (o & gm) == gp) atomicAdd(&h0[d], 1u);
     if (fa && (o & fm) == fp) atomicAdd(&h1[d], 1u);
   }
-  epi_sync();
+  sel_sync();
 }
 
 // MODE 4, after pooling: Ada budget split + per-head top-k, grid-wide.  Same
@@ -382,7 +358,7 @@ __device__ void select_phase(const ScoreParams& p, Smem& sm, int b, int h, int b
     x.fexact = f <= 0;
     x.fabove = 0;
   }
-  epi_sync();
+  sel_sync();
   uint32_t prefix = 0, mask = 0;
   bool exact = R <= 0;
   int dstar = 0;
@@ -399,7 +375,7 @@ __device__ void select_phase(const ScoreParams& p, Smem& sm, int b, int h, int b
       if (fc) atomicAdd(gh + 256 + tid, fc);
     }
     sstamp(2 + 2 * pass);
-    epi_grid_sync(p.gridbar, n_bar);  // fixed pass count: uniform across the grid
+    epi_grid_sync<2, kSelThreads>(p.gridbar, n_bar);  // fixed pass count: uniform across the grid
     sstamp(3 + 2 * pass);
     // decisions, one warp per histogram (8 bins per lane, no block-wide
     // scans): warp w -> suffix counts of head w's global histogram; warp 0
@@ -443,7 +419,7 @@ __device__ void select_phase(const ScoreParams& p, Smem& sm, int b, int h, int b
         x.fexact = at == f;
       }
     }
-    epi_sync();
+    sel_sync();
     sstamp(12 + 3 * pass);
     if (exact) continue;
     int32_t gd = 0;
@@ -453,7 +429,7 @@ __device__ void select_phase(const ScoreParams& p, Smem& sm, int b, int h, int b
       x.dstar = cnt - 1;
       x.exact = gd == R;
     }
-    epi_sync();
+    sel_sync();
     dstar = x.dstar;
     exact = x.exact != 0;
     // n_at: keys with the decided digits >= prefix.d*; above: strictly above d*
@@ -463,7 +439,7 @@ __device__ void select_phase(const ScoreParams& p, Smem& sm, int b, int h, int b
     }
     prefix |= static_cast<uint32_t>(dstar) << shift;
     mask |= 255u << shift;
-    epi_sync();
+    sel_sync();
     sstamp(13 + 3 * pass);
   }
   sstamp(30);
@@ -495,7 +471,7 @@ __device__ void select_phase(const ScoreParams& p, Smem& sm, int b, int h, int b
     x.dstar = hstar;
     x.exact = kstar;
   }
-  epi_sync();
+  sel_sync();
   const int hstar = x.dstar, kstar = x.exact;
   const bool below = !have_tau || x.n_at[h] < f;
   auto budget_of = [&](int hh) {
@@ -528,9 +504,14 @@ __device__ void select_phase(const ScoreParams& p, Smem& sm, int b, int h, int b
     if (o != thr) return o > thr;
     return ktie == 0x7fffffff ? 1 : (ktie > 0 ? 2 : 0);
   };
-  // publish (chosen outright, ties) of this chunk
+  // per-warp (chosen outright, ties) counts of contiguous key segments, kept
+  // in x.suf for the writes; the chunk's totals are published for the CTAs
+  // after it
+  const int seg = ((nk + kSelWarps - 1) / kSelWarps + 31) & ~31;
+  const int s0 = min(nk, wid * seg), s1 = min(nk, s0 + seg);
   int32_t c1 = 0, c2 = 0;
-  for (int i = tid; i < nk; i += 32 * kEpiWarps) {
+#pragma unroll 4
+  for (int i = s0 + lane; i < s1; i += 32) {
     const int k = klass(i);
     c1 += k == 1;
     c2 += k == 2;
@@ -538,15 +519,15 @@ __device__ void select_phase(const ScoreParams& p, Smem& sm, int b, int h, int b
   c1 = __reduce_add_sync(0xffffffffu, c1);
   c2 = __reduce_add_sync(0xffffffffu, c2);
   if (lane == 0) x.suf[0][wid] = c1, x.suf[1][wid] = c2;
-  epi_sync();
+  sel_sync();
   if (tid == 0) {
     int32_t a = 0, t2 = 0;
-    for (int j = 0; j < kEpiWarps; ++j) a += x.suf[0][j], t2 += x.suf[1][j];
+    for (int j = 0; j < kSelWarps; ++j) a += x.suf[0][j], t2 += x.suf[1][j];
     int2* cc = reinterpret_cast<int2*>(p.counts) + static_cast<int64_t>(bh) * p.n_chunks + chunk;
     *cc = make_int2(a, t2);
   }
   sstamp(31);
-  epi_grid_sync(p.gridbar, n_bar);
+  epi_grid_sync<2, kSelThreads>(p.gridbar, n_bar);
   sstamp(32);
   // this chunk's position in the head's list, and its tie-rank origin
   int64_t pos = 0;
@@ -559,46 +540,35 @@ __device__ void select_phase(const ScoreParams& p, Smem& sm, int b, int h, int b
   {
     // every warp computed the same partial sums per lane
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      pos += __shfl_xor_sync(0xffffffffu, pos, off);
-      tie0 += __shfl_xor_sync(0xffffffffu, tie0, off);
+    for (int o = 16; o > 0; o >>= 1) {
+      pos += __shfl_xor_sync(0xffffffffu, pos, o);
+      tie0 += __shfl_xor_sync(0xffffffffu, tie0, o);
     }
   }
-  pos += min(tie0, ktie);  // ties of earlier chunks that were taken
   int64_t off = static_cast<int64_t>(b) * HK * p.budget;
   for (int hh = 0; hh < h; ++hh) off += budget_of(hh);
   const int bud = budget_of(h);
   int32_t* out = p.idx + off;
-  int tie_run = tie0;  // tie rank of the next tie in token order
-  for (int base = 0; base < nk; base += 32 * kEpiWarps) {
-    const int i = base + tid;
-    const int k = i < nk ? klass(i) : 0;
-    const uint32_t bt = __ballot_sync(0xffffffffu, k == 2);
-    if (lane == 0) x.suf[1][wid] = __popc(bt);
-    epi_sync();
-    int tb = __popc(bt & ((1u << lane) - 1u));
-    int t_tot = 0;
-    for (int j = 0; j < kEpiWarps; ++j) {
-      if (j < wid) tb += x.suf[1][j];
-      t_tot += x.suf[1][j];
-    }
-    const bool take = k == 1 || (k == 2 && tie_run + tb < ktie);
+  // this warp's segment: chosen outright and ties of the segments before it
+  int c1b = 0, tb = 0;
+  for (int j = 0; j < wid; ++j) c1b += x.suf[0][j], tb += x.suf[1][j];
+  int tie_run = tie0 + tb;  // tie rank of the warp's next tie in token order
+  pos += c1b + min(tie_run, ktie);
+  const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll 4
+  for (int base = s0; base < s1; base += 32) {  // no block barriers: each warp writes its own segment
+    const int i = base + lane;
+    const int k = i < s1 ? klass(i) : 0;
+    const uint32_t ties = __ballot_sync(0xffffffffu, k == 2);
+    const bool take = k == 1 || (k == 2 && tie_run + __popc(ties & lt) < ktie);
     const uint32_t bal = __ballot_sync(0xffffffffu, take);
-    if (lane == 0) x.suf[0][wid] = __popc(bal);
-    epi_sync();
-    int before = __popc(bal & ((1u << lane) - 1u)), total = 0;
-    for (int j = 0; j < kEpiWarps; ++j) {
-      if (j < wid) before += x.suf[0][j];
-      total += x.suf[0][j];
-    }
-    if (take) out[pos + before] = t_beg + i;
-    pos += total;
-    tie_run += t_tot;
-    epi_sync();
+    if (take) out[pos + __popc(bal & lt)] = t_beg + i;
+    pos += __popc(bal);
+    tie_run += __popc(ties);
   }
   sstamp(33);
   if (chunk == 0) {
-    for (int i = tid; i < p.window; i += 32 * kEpiWarps) out[bud - p.window + i] = n + i;
+    for (int i = tid; i < p.window; i += kSelThreads) out[bud - p.window + i] = n + i;
     if (tid == 0) {
       p.budgets[bh] = bud;
       p.offsets[bh] = off;
@@ -726,14 +696,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ---------------------------------------------------- epilogue ----
-    const int quad = warp & 3, half = warp >> 2;
+    // warp w reads TMEM lanes 32*(w%4) (its lane quarter) and column group
+    // cs = w/4 of every accumulator buffer
+    const int quad = warp & 3, cs = warp >> 2;
     const uint32_t lane_base = static_cast<uint32_t>(32 * quad) << 16;
     if (kP1) {
-      // GW=256: warp half = row half (one whole row per thread);
-      // GW=128: warp half = column half (per-row partials, combined at the end)
-      constexpr int MH = GW / 128;
-      const int mh = MH == 2 ? half : 0;
-      const int cb0 = MH == 2 ? 0 : 2 * half, cb1 = MH == 2 ? 4 : 2 * half + 2;
+      // rows in TMEM lanes: GW=128 -> one M=128 tile, each row's 128 keys in
+      // four column groups of 32; GW=256 -> two M=128 tiles (row halves), each
+      // row's keys in two column groups of 64.  Per-row partial (max, sum) of
+      // each column group, combined by group 0 at the end.
+      constexpr int MH = GW / 128, CG = 4 / MH, NCH = kBN / CG / 32;
+      const int mh = MH == 2 ? cs >> 1 : 0, cg = MH == 2 ? cs & 1 : cs;
       const int r = mh * 128 + 32 * quad + lane;
       const int limit = min(p.T - 1, p.T - p.window + (r % p.window));  // last visible key
       float m = -CUDART_INF_F, l = 0.f;
@@ -741,68 +714,69 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int buf = it % NB;
         mbar_wait(&sm.tfull[buf], (it / NB) & 1);
         tc_fence_after();
-        const int ts = (a1 + it) * kBN;
-        // two 32-column chunks per TMEM wait, one running-max rescale per 64
-        // columns, four independent sum chains
-#pragma unroll 1
-        for (int cb = cb0; cb < cb1; cb += 2) {
-          uint32_t ra[32], rb[32];
-          tmem_ld32_nw(tmem + lane_base + buf * GW + mh * kBN + cb * 32, ra);
-          tmem_ld32_nw(tmem + lane_base + buf * GW + mh * kBN + (cb + 1) * 32, rb);
+        const uint32_t col = buf * GW + mh * kBN + cg * (NCH * 32);
+        uint32_t ra[32], rb[32];
+        tmem_ld32_nw(tmem + lane_base + col, ra);
+        if constexpr (NCH == 2) {
+          tmem_ld32_nw(tmem + lane_base + col + 32, rb);
           tmem_wait_ld(ra, rb);
-          if (cb + 2 >= cb1) {  // the tile's last columns are in registers: hand the
-            tc_fence_before();  // TMEM buffer back to the MMA warp before the math
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&sm.tempty[buf]);
-          }
-          float v[64];
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(ra[i]), v[32 + i] = __uint_as_float(rb[i]);
-          const int c0 = ts + cb * 32;
-          float bmax = -CUDART_INF_F;
-          if (c0 + 63 > limit) {  // only the window's tiles (and the tail) need masking
-#pragma unroll
-            for (int i = 0; i < 64; ++i) {
-              v[i] = c0 + i <= limit ? v[i] : -CUDART_INF_F;
-              bmax = fmaxf(bmax, v[i]);
-            }
-            if (bmax == -CUDART_INF_F) continue;
-          } else {
-#pragma unroll
-            for (int i = 0; i < 64; ++i) bmax = fmaxf(bmax, v[i]);
-          }
-          // running max kept in raw-score units, exponents via one FFMA each
-          const float nm = fmaxf(m, bmax);
-          const float nms = nm * p.scale_log2;
-          float e0 = 0.f, e1 = 0.f, e2 = 0.f, e3 = 0.f;  // (a1/a2 name the tile starts)
-#pragma unroll
-          for (int i = 0; i < 64; i += 4) {
-            e0 += fast_exp2(fmaf(v[i], p.scale_log2, -nms));
-            e1 += fast_exp2(fmaf(v[i + 1], p.scale_log2, -nms));
-            e2 += fast_exp2(fmaf(v[i + 2], p.scale_log2, -nms));
-            e3 += fast_exp2(fmaf(v[i + 3], p.scale_log2, -nms));
-          }
-          l = l * fast_exp2((m - nm) * p.scale_log2) + ((e0 + e1) + (e2 + e3));
-          m = nm;
+        } else {
+          tmem_wait_ld(ra);
         }
+        tc_fence_before();  // the columns are in registers: the buffer goes back
+        __syncwarp();       // to the MMA warp before the math
+        if (lane == 0) mbar_arrive(&sm.tempty[buf]);
+        constexpr int NV = NCH * 32;
+        float v[NV];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(ra[i]);
+        if constexpr (NCH == 2) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[32 + i] = __uint_as_float(rb[i]);
+        }
+        const int c0 = (a1 + it) * kBN + cg * NV;
+        float bmax = -CUDART_INF_F;
+        if (c0 + NV - 1 > limit) {  // only the window's tiles (and the tail) need masking
+#pragma unroll
+          for (int i = 0; i < NV; ++i) {
+            v[i] = c0 + i <= limit ? v[i] : -CUDART_INF_F;
+            bmax = fmaxf(bmax, v[i]);
+          }
+          if (bmax == -CUDART_INF_F) continue;
+        } else {
+#pragma unroll
+          for (int i = 0; i < NV; ++i) bmax = fmaxf(bmax, v[i]);
+        }
+        // running max kept in raw-score units, exponents via one FFMA each,
+        // four independent sum chains
+        const float nm = fmaxf(m, bmax);
+        const float nms = nm * p.scale_log2;
+        float e0 = 0.f, e1 = 0.f, e2 = 0.f, e3 = 0.f;
+#pragma unroll
+        for (int i = 0; i < NV; i += 4) {
+          e0 += fast_exp2(fmaf(v[i], p.scale_log2, -nms));
+          e1 += fast_exp2(fmaf(v[i + 1], p.scale_log2, -nms));
+          e2 += fast_exp2(fmaf(v[i + 2], p.scale_log2, -nms));
+          e3 += fast_exp2(fmaf(v[i + 3], p.scale_log2, -nms));
+        }
+        l = l * fast_exp2((m - nm) * p.scale_log2) + ((e0 + e1) + (e2 + e3));
+        m = nm;
       }
       m = m == -CUDART_INF_F ? m : m * p.scale_log2;  // to log2 units
-      if (MH == 1) {
-        if (half == 1) {
-          sm.ml[32 * quad + lane][0] = m;
-          sm.ml[32 * quad + lane][1] = l;
-        }
-        asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps));
-        if (half == 0) {
-          const float m1 = sm.ml[32 * quad + lane][0], l1 = sm.ml[32 * quad + lane][1];
+      if (cg > 0) {
+        sm.ml[(cg * GW + r) * 2] = m;
+        sm.ml[(cg * GW + r) * 2 + 1] = l;
+      }
+      epi_sync();
+      if (cg == 0) {
+        for (int g = 1; g < CG; ++g) {
+          const float m1 = sm.ml[(g * GW + r) * 2], l1 = sm.ml[(g * GW + r) * 2 + 1];
           const float nm = fmaxf(m, m1);
           if (nm != -CUDART_INF_F) {
             l = l * exp2f(m - nm) + l1 * exp2f(m1 - nm);
             m = nm;
           }
         }
-      }
-      if (MH == 2 || half == 0) {
         float* st = p.stats + ((static_cast<int64_t>(bh) * p.n_chunks + chunk) * GW + r) * 2;
         st[0] = m;
         st[1] = l;
@@ -813,99 +787,90 @@ __global__ void __launch_bounds__(kThreads, 1)
       epi_grid_sync(p.gridbar, n_bar);  // every chunk's statistics are in global memory
       sstamp(41);
       combine_stats();
-      asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps));
+      epi_sync();
     }
     if (kP2) {
+      // keys in TMEM lanes, query rows in columns: warp (quad, cs) sums the
+      // exponentials of rows [cs*GW/4, (cs+1)*GW/4) for its 32 keys; the four
+      // column-group partials are added by the pooling
+      constexpr int NC = GW / 128;  // 32-column chunks per warp
       const int key = 32 * quad + lane;
       for (int i2 = 0; i2 < n2; ++i2) {
         const int it = n1 + i2, buf = it % NB;
         mbar_wait(&sm.tfull[buf], (it / NB) & 1);
         tc_fence_after();
-        constexpr int NC = GW / 64;  // 32-column chunks of this warp's row half
         float acc = 0.f;
-        auto chunk_sum = [&](const uint32_t (&r)[32], int c) {
-          const float4* b4 = reinterpret_cast<const float4*>(sm.bias + (half * NC + c) * 32);
+        auto chunk_sum = [&](const uint32_t (&rr)[32], int c) {
+          const float4* b4 = reinterpret_cast<const float4*>(sm.bias + cs * (GW / 4) + c * 32);
 #pragma unroll
           for (int i = 0; i < 32; i += 4) {
             const float4 bb = b4[i / 4];  // broadcast: every lane reads the same columns
-            acc += fast_exp2(fmaf(__uint_as_float(r[i]), p.scale_log2, -bb.x));
-            acc += fast_exp2(fmaf(__uint_as_float(r[i + 1]), p.scale_log2, -bb.y));
-            acc += fast_exp2(fmaf(__uint_as_float(r[i + 2]), p.scale_log2, -bb.z));
-            acc += fast_exp2(fmaf(__uint_as_float(r[i + 3]), p.scale_log2, -bb.w));
+            acc += fast_exp2(fmaf(__uint_as_float(rr[i]), p.scale_log2, -bb.x));
+            acc += fast_exp2(fmaf(__uint_as_float(rr[i + 1]), p.scale_log2, -bb.y));
+            acc += fast_exp2(fmaf(__uint_as_float(rr[i + 2]), p.scale_log2, -bb.z));
+            acc += fast_exp2(fmaf(__uint_as_float(rr[i + 3]), p.scale_log2, -bb.w));
           }
         };
+        uint32_t ra[32], rb[32];
+        const uint32_t col = buf * GW + cs * (GW / 4);
+        tmem_ld32_nw(tmem + lane_base + col, ra);
         if constexpr (NC == 2) {
-          // both chunks in registers, the buffer back to the MMA warp, then the math
-          uint32_t ra[32], rb[32];
-          tmem_ld32_nw(tmem + lane_base + buf * GW + (half * NC) * 32, ra);
-          tmem_ld32_nw(tmem + lane_base + buf * GW + (half * NC + 1) * 32, rb);
+          tmem_ld32_nw(tmem + lane_base + col + 32, rb);
           tmem_wait_ld(ra, rb);
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&sm.tempty[buf]);
-          chunk_sum(ra, 0);
-          chunk_sum(rb, 1);
         } else {
-          // GW = 256: four chunks would cost 128 registers; one at a time
-#pragma unroll 1
-          for (int c = 0; c < NC; ++c) {
-            uint32_t ra[32];
-            tmem_ld32_nw(tmem + lane_base + buf * GW + (half * NC + c) * 32, ra);
-            tmem_wait_ld(ra);
-            chunk_sum(ra, c);
-          }
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&sm.tempty[buf]);
+          tmem_wait_ld(ra);
         }
-        // this row half's partial column sum; the pooling adds the two halves
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.tempty[buf]);
+        chunk_sum(ra, 0);
+        if constexpr (NC == 2) chunk_sum(rb, 1);
         const int t = (a2 + i2) * kBN + key;
-        if (t < n) p.raw[(static_cast<int64_t>(half) * gridDim.y + bh) * n + t] = acc;
+        if (t < n) p.raw[(static_cast<int64_t>(cs) * gridDim.y + bh) * n + t] = acc;
       }
     }
     if (kFused) {
       sstamp(42);
       epi_grid_sync(p.gridbar, n_bar);  // every raw column score is in global memory
       sstamp(43);
-      const float* rr = p.raw + static_cast<int64_t>(bh) * n;                 // row half 0
-      const float* rr1 = p.raw + (static_cast<int64_t>(gridDim.y) + bh) * n;  // row half 1
       float* out = p.scores + static_cast<int64_t>(bh) * n;
       const int t_beg = a2 * kBN, t_end = min(e2 * kBN, n);
       // MODE 4 stages this CTA's pooled scores in the K ring (idle: every tile
       // was consumed before the epilogue reached the barrier above)
       float* sp = reinterpret_cast<float*>(&sm.k[0][0][0][0]);
-      if (p.pool_r == 3) {  // the default 7-wide pool: 4 keys x 7 taps in flight per thread
-        constexpr int kU = 4, kE = 32 * kEpiWarps;
-        for (int t0 = t_beg + threadIdx.x; t0 < t_end; t0 += kU * kE) {
-          float w[kU][7];
-#pragma unroll
-          for (int u = 0; u < kU; ++u)
-#pragma unroll
-            for (int j = 0; j < 7; ++j) {
-              const int t = t0 + u * kE, xj = t + j - 3;
-              w[u][j] = t < t_end && xj >= 0 && xj < n ? __ldcg(rr + xj) + __ldcg(rr1 + xj) : -CUDART_INF_F;
-            }
-#pragma unroll
-          for (int u = 0; u < kU; ++u) {
-            const int t = t0 + u * kE;
-            if (t >= t_end) break;
-            float mx = w[u][0];
-#pragma unroll
-            for (int j = 1; j < 7; ++j) mx = fmaxf(mx, w[u][j]);
-            out[t] = mx;
-            if (MODE == 4) sp[t - t_beg] = mx;
+      // the raw column sums (four partials added) of a block of keys and its
+      // pooling halo, staged in the (idle) Q_win region, then max-pooled
+      float* stg = reinterpret_cast<float*>(&sm.q[0][0][0]);
+      constexpr int kStg = GW * 256 / 4;
+      const int R = p.pool_r, blk = kStg - 2 * R;
+      const int64_t part = static_cast<int64_t>(gridDim.y) * n;
+      const float* rw = p.raw + static_cast<int64_t>(bh) * n;
+      for (int b0 = t_beg; b0 < t_end; b0 += blk) {
+        const int b1 = min(b0 + blk, t_end);
+        const int lo = b0 - R, cnt = b1 - b0 + 2 * R;
+#pragma unroll 4
+        for (int j = threadIdx.x; j < cnt; j += 32 * kEpiWarps) {
+          const int x = lo + j;
+          float v = -CUDART_INF_F;
+          if (x >= 0 && x < n) {
+            const float q0 = __ldcg(rw + x), q1 = __ldcg(rw + part + x);
+            const float q2 = __ldcg(rw + 2 * part + x), q3 = __ldcg(rw + 3 * part + x);
+            v = (q0 + q1) + (q2 + q3);
           }
+          stg[j] = v;
         }
-      } else {
-        for (int t = t_beg + threadIdx.x; t < t_end; t += 32 * kEpiWarps) {
-          float mx = __ldcg(rr + t) + __ldcg(rr1 + t);
-          const int lo = max(0, t - p.pool_r), hi = min(n - 1, t + p.pool_r);
-          for (int u = lo; u <= hi; ++u) mx = fmaxf(mx, __ldcg(rr + u) + __ldcg(rr1 + u));
+        epi_sync();
+        for (int t = b0 + threadIdx.x; t < b1; t += 32 * kEpiWarps) {
+          const float* w = stg + (t - b0);  // taps t-R .. t+R
+          float mx = w[R];
+          for (int j = 0; j <= 2 * R; ++j) mx = fmaxf(mx, w[j]);
           out[t] = mx;
           if (MODE == 4) sp[t - t_beg] = mx;
         }
+        epi_sync();
       }
-      if (MODE == 4) select_phase(p, sm, b, h, bh, chunk, n, t_beg, max(t_end - t_beg, 0), sp, n_bar);
+      if (MODE == 4 && warp < kSelWarps)
+        select_phase(p, sm, b, h, bh, chunk, n, t_beg, max(t_end - t_beg, 0), sp, n_bar);
     }
   }
   tc_fence_before();
@@ -923,11 +888,12 @@ __global__ void pool_kernel(const float* __restrict__ raw, float* __restrict__ o
   if (i >= total) return;
   const int64_t row = i / n;
   const int t = static_cast<int>(i - row * n);
-  const float* r = raw + row * n;          // row half 0 of the column sums
-  const float* r1 = raw + total + row * n;  // row half 1
-  float m = r[t] + r1[t];
+  const float* r = raw + row * n;  // column partial 0; partial c at + c * total
+  // the four column-group partials, added in the fused kernel's order
+  auto col = [&](int u) { return (r[u] + r[total + u]) + (r[2 * total + u] + r[3 * total + u]); };
+  float m = col(t);
   const int lo = max(0, t - radius), hi = min(n - 1, t + radius);
-  for (int u = lo; u <= hi; ++u) m = fmaxf(m, r[u] + r1[u]);
+  for (int u = lo; u <= hi; ++u) m = fmaxf(m, col(u));
   out[i] = m;
 }
 
@@ -1063,7 +1029,7 @@ ScoreLayout score_layout(int batch, int hkv, int T, int window, int group) {
   auto a16 = [](int64_t x) { return (x + 255) & ~int64_t(255); };
   L.stats = 0;
   L.raw = a16(L.stats + static_cast<int64_t>(L.bh) * L.chunks * gw * 2 * 4);
-  L.gridbar = a16(L.raw + static_cast<int64_t>(L.bh) * (T - window) * 4 * 2);  // two row halves
+  L.gridbar = a16(L.raw + static_cast<int64_t>(L.bh) * (T - window) * 4 * kRawParts);  // column partials
   L.hist = a16(L.gridbar + 64);
   L.counts = a16(L.hist + static_cast<int64_t>(kSelPasses) * L.bh * 512 * 4);
   L.sel = a16(L.counts + static_cast<int64_t>(L.bh) * L.chunks * 8);
