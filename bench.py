@@ -1016,8 +1016,9 @@ def prefill_compress(peaks):
         rows[name] = {
             "score_us": t_score * 1e6, "ada_select_us": t_sel * 1e6, "compact_us": t_cmp * 1e6,
             "score_select_fused_us": t_fused * 1e6,
-            "score_select_path": "one cooperative launch" if bt * hkv <= 148
-            else "score launches + grid-wide ada_select",
+            "score_select_path": ("one persistent cooperative launch (per-chunk select)"
+                                  if bt * hkv <= 148 else
+                                  "one persistent cooperative launch (items dealt round robin, grid-wide select)"),
             "score_tflops": flops / t_score / 1e12, "score_tflops_frac": flops / t_score / 1e12 / tf_peak,
             "score_K_read_GBs_per_pass": kbytes / (t_score / 2) / 1e9,
             "roofline_us": max(flops / (tf_peak * 1e12), 2 * kbytes / (float(peaks.get("hbm_gbs", 6650.0)) * 1e9)) * 1e6,

@@ -7,7 +7,7 @@
 //   raw[t]  = (1/G) sum_r P[r,t]              t < T - w
 //   s[t]    = max(raw[t-3 .. t+3])            (pooling kernel below)
 //
-// Two tcgen05 passes over K, each CTA owning (request, KV head, key chunk):
+// Two tcgen05 passes over K per work item (request, KV head, key chunk):
 //   pass 1  D[GW rows x 128 keys]   = Q_win . K_tile^T  -> per-row online max
 //           and sum-exp with rows in TMEM lanes (thread-local reductions,
 //           one partial per column group, combined once per chunk);
@@ -15,24 +15,33 @@
 //           sums of exp(s - m_r)/l_r with keys in TMEM lanes (thread-local);
 //           the four column groups (warps 4c..4c+3) store separate partial
 //           sums, added by the pooling (no block barrier per tile).
-// Q_win (GW = G*w = 128 or 256 rows) is TMA-loaded once per CTA and stays in
+// Q_win (GW = G*w = 128 or 256 rows) is TMA-loaded per item and stays in
 // shared memory; K tiles (128 keys x 128 d, 32 KiB) stream through a 3-stage
 // TMA ring with 128-B swizzle; one elected thread issues
 // tcgen05.mma.cta_group::1.kind::f16 (M=128, N=128 or GW, K=16) into fp32
 // TMEM accumulators (512 / GW buffers: all 512 columns); sixteen epilogue
 // warps drain them with tcgen05.ld (warp e reads TMEM lanes 32*(e%4) and
 // column group e/4) and hand each buffer back as soon as it is in registers.
-// Warp roles: 0-15 epilogue, 16 TMA producer, 17 MMA issuer.  Grid: one wave
-// of one CTA per SM ((Bt*Hkv) x chunks <= #SMs) when that keeps >= 80 % of
-// the SMs busy, else wave-filled chunks over several launches (score_chunks).
-// The second pass re-reads K mostly from L2 (a layer's K for one request is
-// 32 MiB at 16k context, well inside the 126 MB L2).
+// Warp roles: 0-15 epilogue, 16 TMA producer, 17 MMA issuer.
+// One persistent cooperative launch at any batch (one CTA per SM): the
+// Bt*Hkv*chunks items are dealt round robin (score_waves); pass 1 of every
+// item, one grid barrier, pass 2 of every item, a second barrier, pooling,
+// then the Ada split + top-k in the same launch (per chunk when every CTA
+// holds one item, else the grid-wide search of gsel.cuh).  With one item
+// per CTA the second pass re-reads K mostly from L2 (a layer's K for one
+// request is 32 MiB at 16k context).
 #include <cuda.h>
+
+#include <algorithm>
+#include <cstddef>
+#include <cstdlib>
+#include <type_traits>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
 #include "common.cuh"
+#include "gsel.cuh"
 
 namespace fkv {
 namespace {
@@ -51,21 +60,24 @@ constexpr int kSelWarps = 8, kSelThreads = 32 * kSelWarps;
 constexpr float kLog2e = 1.4426950408889634f;
 
 struct ScoreParams {
-  int T, window, group, hkv, n_chunks, tiles_per_chunk;
+  int T, window, group, hkv, n_chunks;  // key chunks per (request, KV head)
+  int n_waves, bh_total;  // persistent schedule (score_waves): items per CTA, heads
   int q_rows_per_req;  // Hq * w
   float scale_log2;    // log2(e) / sqrt(d)
   float* stats;        // [Bt*Hkv, n_chunks, GW, 2] (max, sum) in log2 units
-  float* raw;          // [2 row halves][Bt*Hkv, T - w] partial column sums
-  float* scores;       // pooled output (fused mode)
+  float* raw;          // [kRawParts][Bt*Hkv, T - w] partial column sums
+  float* scores;       // pooled output
   int pool_r;          // pooling radius (pool_k / 2)
-  struct GridBar* gridbar;  // fused mode: zeroed counter + generation
-  // MODE 4 (score + Ada split + top-k in one launch); workspace parts zeroed per launch
+  struct GridBar* gridbar;  // zeroed counter
+  // selection after the scoring (fkv_snapkv_select); workspace parts zeroed per launch
+  int sel_mode;        // 0 none, 1 per-chunk (one wave: select_phase), 2 grid search over the pooled scores
   int budget, floor_k, rest_total;  // B, f = floor(alpha (B - w)), R = Hkv (B - w - f)
-  uint32_t* hist;      // [kSelPasses][Bt*Hkv][2][256] per-pass digit histograms, global + floor (zeroed)
-  int32_t* counts;     // [Bt*Hkv][n_chunks] int2 (chosen outright, ties at s*) per chunk
+  uint32_t* hist;      // sel_mode 1: [kSelPasses][Bt*Hkv][2][256] per-pass digit histograms (zeroed)
+  int32_t* counts;     // sel_mode 1: [Bt*Hkv][n_chunks] int2 (chosen outright, ties at s*) per chunk
   int32_t* budgets;    // out [Bt, Hkv]
   int64_t* offsets;    // out [Bt*Hkv + 1]
   int32_t* idx;        // out [Bt*Hkv*budget]
+  GSelParams gs;       // sel_mode 2
 };
 
 constexpr int kSelPasses = 4;            // 32-bit orderable scores, 8-bit digits (ties resolved by count)
@@ -205,11 +217,14 @@ template <int GW>
 struct __align__(1024) ScoreSmem {
   __nv_bfloat16 q[2][GW][64];                 // [d-half][row][64], 128-B swizzled by TMA
   __nv_bfloat16 k[kStages][2][kBN][64];
-  uint64_t full[kStages], empty[kStages], tfull[512 / GW], tempty[512 / GW], qbar;
+  uint64_t full[kStages], empty[kStages], tfull[512 / GW], tempty[512 / GW], qbar, qempty;
   uint32_t tmem_base;
   alignas(16) float bias[GW];  // pass 2: per query row, m_r + log2(G * l_r) (log2 units)
   float ml[4 * 128 * 2];     // pass 1: per-row (max, sum) partials of column groups 1..3 -> group 0
 };
+static_assert(offsetof(ScoreSmem<128>, k) == sizeof(ScoreSmem<128>::q) &&
+                  offsetof(ScoreSmem<256>, k) == sizeof(ScoreSmem<256>::q),
+              "Q_win and the K ring are contiguous (the grid select's key cache spans both)");
 
 struct GridBar {
   unsigned count, gen;
@@ -251,10 +266,6 @@ __device__ __forceinline__ void sstamp(int i) {
 __device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps)); }
 __device__ __forceinline__ void sel_sync() { asm volatile("bar.sync 2, %0;" ::"n"(kSelThreads)); }
 
-__device__ __forceinline__ uint32_t orderable(float f) {
-  const uint32_t u = __float_as_uint(f);
-  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
-}
 
 // Scratch of the selection phase, placed in the (idle) Q_win region.
 struct SelScratch {
@@ -349,7 +360,7 @@ __device__ void select_phase(const ScoreParams& p, Smem& sm, int b, int h, int b
                              int t_beg, int nk, const float* sp, unsigned& n_bar) {
   SelScratch& x = *reinterpret_cast<SelScratch*>(&sm.q[0][0][0]);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int HK = p.hkv, BH = gridDim.y;
+  const int HK = p.hkv, BH = p.bh_total;
   const int f = p.floor_k, R = p.rest_total;
   sstamp(1);
   if (tid < HK) x.above[tid] = 0, x.n_at[tid] = R > 0 ? n : 0;
@@ -577,10 +588,63 @@ __device__ void select_phase(const ScoreParams& p, Smem& sm, int b, int h, int b
   }
 }
 
-// MODE 1: pass 1 only; MODE 2: pass 2 only; MODE 3: both passes + pooling in
-// one cooperative launch (stats combined after a grid barrier, K re-read from
-// L2, raw scores pooled after a second barrier).
-template <int MODE, int GW>
+// The epilogue warps as the 512 threads of the grid-wide select (gsel.cuh):
+// named barrier 1 instead of __syncthreads.
+struct EpiCx {
+  int cta, ncta;
+  __device__ void sync() const { epi_sync(); }
+  __device__ int count(bool pred) const {
+    int r;
+    asm volatile("{\n.reg .pred q;\nsetp.ne.u32 q, %1, 0;\nbar.red.popc.u32 %0, 1, %2, q;\n}"
+                 : "=r"(r)
+                 : "r"(static_cast<int>(pred)), "n"(32 * kEpiWarps)
+                 : "memory");
+    return r;
+  }
+  __device__ void grid(unsigned* bar, unsigned& k) const { grid_sync_n(bar, k, ncta, [] { epi_sync(); }); }
+};
+
+// Grid-select state (sel_mode 2) at the start of the idle Q_win region, its
+// key cache right after it through the (idle, contiguous) K ring.
+__host__ __device__ constexpr int gsel_cache_off() { return (static_cast<int>(sizeof(GSelSmem)) + 15) & ~15; }
+template <int GW>
+__host__ __device__ constexpr int gsel_cache_keys() {
+  return (GW * 256 + kStages * kTileBytes - gsel_cache_off()) / 4;
+}
+
+// One work item = key chunk `chunk` of (request, KV head) `bh`: tiles
+// [a, e1) of pass 1 (all T keys) and [a, e2) of pass 2 (the T - w scored
+// keys); chunks split a head's tiles as evenly as possible.  Items are dealt
+// round robin: item w * grid + cta is the CTA's w-th.
+struct Item {
+  int bh, chunk, a, e1, e2;
+  bool valid;
+};
+__device__ __forceinline__ Item score_item(const ScoreParams& p, int w) {
+  Item it{};
+  // 32-bit arithmetic: items < 2^31 and chunk * tiles < 2^31 (Bt*Hkv*T < 2^31 is checked on the host)
+  const int i = (w * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+  it.bh = i / p.n_chunks;
+  it.chunk = i - it.bh * p.n_chunks;
+  it.valid = it.bh < p.bh_total;
+  const int nt1 = (p.T + kBN - 1) / kBN, nt2 = (p.T - p.window + kBN - 1) / kBN;
+  it.a = it.chunk * nt1 / p.n_chunks;
+  it.e1 = (it.chunk + 1) * nt1 / p.n_chunks;
+  it.e2 = min(it.e1, nt2);
+  if (!it.valid) it.e1 = it.e2 = it.a;
+  return it;
+}
+
+// Persistent cooperative launch (one CTA per SM): every CTA runs pass 1 of
+// each of its items, then one grid barrier (every chunk's row statistics are
+// in global memory), then pass 2 of each item, a second barrier, the pooling
+// of each item and (MODE 4) the Ada split + top-k -- per chunk in place
+// (sel_mode 1: one item per CTA) or the grid-wide search over the pooled
+// scores (sel_mode 2, gsel.cuh).  The TMA and MMA warps run ahead across
+// items and passes; the Q_win tile is reloaded whenever the item changes,
+// once the MMA warp has released it.  MODE 3: scores only; MODE 4: scores +
+// selection.
+template <int MODE, int GW, bool MULTI>
 __global__ void __launch_bounds__(kThreads, 1)
     score_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                  const ScoreParams p) {
@@ -589,21 +653,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   constexpr int NB = 512 / GW;           // accumulator buffers: all 512 TMEM columns
   constexpr uint32_t kCols = NB * GW;
-  constexpr bool kP1 = MODE != 2, kP2 = MODE != 1;
-  constexpr bool kFused = MODE >= 3;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   sstamp(0);
   unsigned n_bar = 0;  // grid barriers passed (epilogue thread 0)
-  const int bh = blockIdx.y, chunk = blockIdx.x;
-  const int b = bh / p.hkv, h = bh - b * p.hkv;
   const int n = p.T - p.window;
-  const int nt1 = (p.T + kBN - 1) / kBN, nt2 = (n + kBN - 1) / kBN;
-  const int a1 = chunk * p.tiles_per_chunk, e1 = kP1 ? min(a1 + p.tiles_per_chunk, nt1) : a1;
-  const int a2 = chunk * p.tiles_per_chunk, e2 = kP2 ? min(a2 + p.tiles_per_chunk, nt2) : a2;
-  const int n1 = max(e1 - a1, 0), n2 = max(e2 - a2, 0);  // tiles of each pass; iterations continue
-  const int krow0 = bh * p.T;
-  const int qrow0 = b * p.q_rows_per_req + h * GW;
+  const int W = MULTI ? p.n_waves : 1;  // items per CTA (compile-time 1: straight-line passes)
 
   if (warp == kTmaWarp && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_q)) : "memory");
@@ -617,27 +672,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&sm.tempty[i], kEpiWarps);
     }
     mbar_init(&sm.qbar, 1);
+    mbar_init(&sm.qempty, 1);
     fence_mbar_init();
   }
   if (warp == kMmaWarp) tmem_alloc(&sm.tmem_base, kCols);
-
-  // combine every chunk's pass-1 statistics (log2 domain) into per-row biases
-  auto combine_stats = [&]() {
-    for (int r = threadIdx.x; r < GW; r += 32 * kEpiWarps) {
-      float M = -CUDART_INF_F, L = 0.f;
-      const float* st = p.stats + (static_cast<int64_t>(bh) * p.n_chunks) * GW * 2;
-      for (int c = 0; c < p.n_chunks; ++c) {
-        const float m = __ldcg(st + (c * GW + r) * 2), l = __ldcg(st + (c * GW + r) * 2 + 1);
-        if (l <= 0.f) continue;
-        const float nm = fmaxf(M, m);
-        L = L * exp2f(M - nm) + l * exp2f(m - nm);
-        M = nm;
-      }
-      // exp2(s*c - m) / (G*l) == exp2(s*c - bias): one FFMA + one MUFU per score
-      sm.bias[r] = L > 0.f ? M + log2f(L * static_cast<float>(p.group)) : CUDART_INF_F;
-    }
-  };
-  if (MODE == 2 && warp < kEpiWarps) combine_stats();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -645,53 +683,98 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == kTmaWarp) {
     // ------------------------------------------------ TMA producer ----
-    if (lane == 0 && n1 + n2 > 0) {
-      mbar_arrive_expect_tx(&sm.qbar, GW * 256);
-      for (int c = 0; c < 2; ++c)
-        for (int rh = 0; rh < GW / 128; ++rh)
-          tma_load_2d(&sm.q[c][rh * 128][0], &tm_q, 64 * c, qrow0 + 128 * rh, &sm.qbar);
+    if (lane == 0) {
       const uint64_t keep = l2_policy(true), stream = l2_policy(false);
-      for (int it = 0; it < n1 + n2; ++it) {
-        const bool p1 = it < n1;
-        const int j = p1 ? a1 + it : a2 + (it - n1);
-        const int s = it % kStages;
-        mbar_wait(&sm.empty[s], ((it / kStages) & 1) ^ 1);
-        mbar_arrive_expect_tx(&sm.full[s], kTileBytes);
-        for (int c = 0; c < 2; ++c)
-          tma_load_2d_hint(&sm.k[s][c][0][0], &tm_k, 64 * c, krow0 + j * kBN, &sm.full[s],
-                           p1 ? keep : stream);
+      int g = 0, nq = 0;  // K tiles and Q_win loads issued
+      int cur = -1;       // item whose Q_win is in shared memory
+      for (int seg = 0; seg < 2 * W; ++seg) {  // pass 1 of every item, then pass 2
+        const bool p1 = seg < W;
+        const int w = p1 ? seg : seg - W;
+        const Item itm = score_item(p, w);
+        const int nt = p1 ? itm.e1 - itm.a : itm.e2 - itm.a;
+        if (nt == 0) continue;
+        if (cur != w) {
+          const int b = itm.bh / p.hkv, h = itm.bh - b * p.hkv;
+          const int qrow0 = b * p.q_rows_per_req + h * GW;
+          if (nq > 0) mbar_wait(&sm.qempty, (nq - 1) & 1);  // the MMA warp is done with the last Q_win
+          mbar_arrive_expect_tx(&sm.qbar, GW * 256);
+          for (int c = 0; c < 2; ++c)
+            for (int rh = 0; rh < GW / 128; ++rh)
+              tma_load_2d(&sm.q[c][rh * 128][0], &tm_q, 64 * c, qrow0 + 128 * rh, &sm.qbar);
+          ++nq;
+          cur = w;
+        }
+        const int krow0 = itm.bh * p.T;
+        for (int it = 0; it < nt; ++it, ++g) {
+          const int s = g % kStages;
+          mbar_wait(&sm.empty[s], ((g / kStages) & 1) ^ 1);
+          mbar_arrive_expect_tx(&sm.full[s], kTileBytes);
+          for (int c = 0; c < 2; ++c)
+            tma_load_2d_hint(&sm.k[s][c][0][0], &tm_k, 64 * c, krow0 + (itm.a + it) * kBN, &sm.full[s],
+                             p1 ? keep : stream);
+        }
       }
     }
   } else if (warp == kMmaWarp) {
     // -------------------------------------------------- MMA issuer ----
-    if (lane == 0 && n1 + n2 > 0) {
-      mbar_wait(&sm.qbar, 0);
+    if (lane == 0) {
       constexpr uint32_t kIdesc1 = idesc_bf16(128, kBN);
       constexpr uint32_t kIdesc2 = idesc_bf16(128, GW);
       const uint32_t q_base = smem_u32(&sm.q[0][0][0]);
-      for (int it = 0; it < n1 + n2; ++it) {
-        const int s = it % kStages, buf = it % NB;
-        mbar_wait(&sm.full[s], (it / kStages) & 1);
-        mbar_wait(&sm.tempty[buf], ((it / NB) & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t k_base = smem_u32(&sm.k[s][0][0][0]);
-        const uint32_t d_buf = tmem + buf * GW;
-        const bool p1 = it < n1;
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const uint32_t koff = (kk >> 2) * (kBN * 128) + (kk & 3) * 32;
-          const uint32_t qoff = (kk >> 2) * (GW * 128) + (kk & 3) * 32;
-          if (p1) {
-#pragma unroll
-            for (int mh = 0; mh < GW / 128; ++mh)
-              umma_bf16(d_buf + mh * kBN, sw128_desc(q_base + qoff + mh * 128 * 128),
-                        sw128_desc(k_base + koff), kIdesc1, kk > 0);
-          } else {
-            umma_bf16(d_buf, sw128_desc(k_base + koff), sw128_desc(q_base + qoff), kIdesc2, kk > 0);
-          }
+      int g = 0, nq = 0, cur = -1;
+      // the same (pass, item) sequence as the producer; the Q_win tile is
+      // released (qempty) before every change of item
+      auto next_item = [&](int seg) {  // item of the next non-empty segment after seg, or -1
+        for (int s2 = seg + 1; s2 < 2 * W; ++s2) {
+          const int w2 = s2 < W ? s2 : s2 - W;
+          const Item i2 = score_item(p, w2);
+          if ((s2 < W ? i2.e1 : i2.e2) > i2.a) return w2;
         }
-        umma_commit(&sm.empty[s]);
-        umma_commit(&sm.tfull[buf]);
+        return -1;
+      };
+      for (int seg = 0; seg < 2 * W; ++seg) {
+        const bool p1 = seg < W;
+        const int w = p1 ? seg : seg - W;
+        const Item itm = score_item(p, w);
+        const int nt = p1 ? itm.e1 - itm.a : itm.e2 - itm.a;
+        if (nt == 0) continue;
+        if (cur != w) {
+          mbar_wait(&sm.qbar, nq & 1);
+          ++nq;
+          cur = w;
+        }
+        // one tile: wait for its K stage and a free accumulator buffer, issue
+        // the 8 K=16 steps (pass 1: D = Q K^T per row half; pass 2: D^T = K Q^T)
+        auto tile = [&](auto pass1) {
+          const int s = g % kStages, buf = g % NB;
+          mbar_wait(&sm.full[s], (g / kStages) & 1);
+          mbar_wait(&sm.tempty[buf], ((g / NB) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t k_base = smem_u32(&sm.k[s][0][0][0]);
+          const uint32_t d_buf = tmem + buf * GW;
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            const uint32_t koff = (kk >> 2) * (kBN * 128) + (kk & 3) * 32;
+            const uint32_t qoff = (kk >> 2) * (GW * 128) + (kk & 3) * 32;
+            if constexpr (decltype(pass1)::value) {
+#pragma unroll
+              for (int mh = 0; mh < GW / 128; ++mh)
+                umma_bf16(d_buf + mh * kBN, sw128_desc(q_base + qoff + mh * 128 * 128),
+                          sw128_desc(k_base + koff), kIdesc1, kk > 0);
+            } else {
+              umma_bf16(d_buf, sw128_desc(k_base + koff), sw128_desc(q_base + qoff), kIdesc2, kk > 0);
+            }
+          }
+          umma_commit(&sm.empty[s]);
+          umma_commit(&sm.tfull[buf]);
+          ++g;
+        };
+        if (p1)
+          for (int it = 0; it < nt; ++it) tile(std::true_type{});
+        else
+          for (int it = 0; it < nt; ++it) tile(std::false_type{});
+        const int nx = next_item(seg);
+        if (nx >= 0 && nx != w) umma_commit(&sm.qempty);  // Q_win may be reloaded once these MMAs are done
       }
     }
   } else {
@@ -700,151 +783,177 @@ __global__ void __launch_bounds__(kThreads, 1)
     // cs = w/4 of every accumulator buffer
     const int quad = warp & 3, cs = warp >> 2;
     const uint32_t lane_base = static_cast<uint32_t>(32 * quad) << 16;
-    if (kP1) {
-      // rows in TMEM lanes: GW=128 -> one M=128 tile, each row's 128 keys in
-      // four column groups of 32; GW=256 -> two M=128 tiles (row halves), each
-      // row's keys in two column groups of 64.  Per-row partial (max, sum) of
-      // each column group, combined by group 0 at the end.
-      constexpr int MH = GW / 128, CG = 4 / MH, NCH = kBN / CG / 32;
-      const int mh = MH == 2 ? cs >> 1 : 0, cg = MH == 2 ? cs & 1 : cs;
-      const int r = mh * 128 + 32 * quad + lane;
-      const int limit = min(p.T - 1, p.T - p.window + (r % p.window));  // last visible key
-      float m = -CUDART_INF_F, l = 0.f;
-      for (int it = 0; it < n1; ++it) {
-        const int buf = it % NB;
-        mbar_wait(&sm.tfull[buf], (it / NB) & 1);
-        tc_fence_after();
-        const uint32_t col = buf * GW + mh * kBN + cg * (NCH * 32);
-        uint32_t ra[32], rb[32];
-        tmem_ld32_nw(tmem + lane_base + col, ra);
-        if constexpr (NCH == 2) {
-          tmem_ld32_nw(tmem + lane_base + col + 32, rb);
-          tmem_wait_ld(ra, rb);
-        } else {
-          tmem_wait_ld(ra);
-        }
-        tc_fence_before();  // the columns are in registers: the buffer goes back
-        __syncwarp();       // to the MMA warp before the math
-        if (lane == 0) mbar_arrive(&sm.tempty[buf]);
-        constexpr int NV = NCH * 32;
-        float v[NV];
-#pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(ra[i]);
-        if constexpr (NCH == 2) {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[32 + i] = __uint_as_float(rb[i]);
-        }
-        const int c0 = (a1 + it) * kBN + cg * NV;
-        float bmax = -CUDART_INF_F;
-        if (c0 + NV - 1 > limit) {  // only the window's tiles (and the tail) need masking
-#pragma unroll
-          for (int i = 0; i < NV; ++i) {
-            v[i] = c0 + i <= limit ? v[i] : -CUDART_INF_F;
-            bmax = fmaxf(bmax, v[i]);
+    int g = 0;  // accumulator tiles consumed
+    for (int w = 0; w < W; ++w) {
+      const Item itm = score_item(p, w);
+      const int bh = itm.bh, n1 = itm.e1 - itm.a;
+      if (n1 > 0) {
+        // rows in TMEM lanes: GW=128 -> one M=128 tile, each row's 128 keys in
+        // four column groups of 32; GW=256 -> two M=128 tiles (row halves), each
+        // row's keys in two column groups of 64.  Per-row partial (max, sum) of
+        // each column group, combined by group 0 at the end.
+        constexpr int MH = GW / 128, CG = 4 / MH, NCH = kBN / CG / 32;
+        const int mh = MH == 2 ? cs >> 1 : 0, cg = MH == 2 ? cs & 1 : cs;
+        const int r = mh * 128 + 32 * quad + lane;
+        const int limit = min(p.T - 1, p.T - p.window + (r % p.window));  // last visible key
+        float m = -CUDART_INF_F, l = 0.f;
+        for (int it = 0; it < n1; ++it, ++g) {
+          const int buf = g % NB;
+          mbar_wait(&sm.tfull[buf], (g / NB) & 1);
+          tc_fence_after();
+          const uint32_t col = buf * GW + mh * kBN + cg * (NCH * 32);
+          uint32_t ra[32], rb[32];
+          tmem_ld32_nw(tmem + lane_base + col, ra);
+          if constexpr (NCH == 2) {
+            tmem_ld32_nw(tmem + lane_base + col + 32, rb);
+            tmem_wait_ld(ra, rb);
+          } else {
+            tmem_wait_ld(ra);
           }
-          if (bmax == -CUDART_INF_F) continue;
-        } else {
+          tc_fence_before();  // the columns are in registers: the buffer goes back
+          __syncwarp();       // to the MMA warp before the math
+          if (lane == 0) mbar_arrive(&sm.tempty[buf]);
+          constexpr int NV = NCH * 32;
+          float v[NV];
 #pragma unroll
-          for (int i = 0; i < NV; ++i) bmax = fmaxf(bmax, v[i]);
-        }
-        // running max kept in raw-score units, exponents via one FFMA each,
-        // four independent sum chains
-        const float nm = fmaxf(m, bmax);
-        const float nms = nm * p.scale_log2;
-        float e0 = 0.f, e1 = 0.f, e2 = 0.f, e3 = 0.f;
+          for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(ra[i]);
+          if constexpr (NCH == 2) {
 #pragma unroll
-        for (int i = 0; i < NV; i += 4) {
-          e0 += fast_exp2(fmaf(v[i], p.scale_log2, -nms));
-          e1 += fast_exp2(fmaf(v[i + 1], p.scale_log2, -nms));
-          e2 += fast_exp2(fmaf(v[i + 2], p.scale_log2, -nms));
-          e3 += fast_exp2(fmaf(v[i + 3], p.scale_log2, -nms));
-        }
-        l = l * fast_exp2((m - nm) * p.scale_log2) + ((e0 + e1) + (e2 + e3));
-        m = nm;
-      }
-      m = m == -CUDART_INF_F ? m : m * p.scale_log2;  // to log2 units
-      if (cg > 0) {
-        sm.ml[(cg * GW + r) * 2] = m;
-        sm.ml[(cg * GW + r) * 2 + 1] = l;
-      }
-      epi_sync();
-      if (cg == 0) {
-        for (int g = 1; g < CG; ++g) {
-          const float m1 = sm.ml[(g * GW + r) * 2], l1 = sm.ml[(g * GW + r) * 2 + 1];
-          const float nm = fmaxf(m, m1);
-          if (nm != -CUDART_INF_F) {
-            l = l * exp2f(m - nm) + l1 * exp2f(m1 - nm);
-            m = nm;
+            for (int i = 0; i < 32; ++i) v[32 + i] = __uint_as_float(rb[i]);
           }
+          const int c0 = (itm.a + it) * kBN + cg * NV;
+          float bmax = -CUDART_INF_F;
+          if (c0 + NV - 1 > limit) {  // only the window's tiles (and the tail) need masking
+#pragma unroll
+            for (int i = 0; i < NV; ++i) {
+              v[i] = c0 + i <= limit ? v[i] : -CUDART_INF_F;
+              bmax = fmaxf(bmax, v[i]);
+            }
+            if (bmax == -CUDART_INF_F) continue;
+          } else {
+#pragma unroll
+            for (int i = 0; i < NV; ++i) bmax = fmaxf(bmax, v[i]);
+          }
+          // running max kept in raw-score units, exponents via one FFMA each,
+          // four independent sum chains
+          const float nm = fmaxf(m, bmax);
+          const float nms = nm * p.scale_log2;
+          float e0 = 0.f, e1 = 0.f, e2 = 0.f, e3 = 0.f;
+#pragma unroll
+          for (int i = 0; i < NV; i += 4) {
+            e0 += fast_exp2(fmaf(v[i], p.scale_log2, -nms));
+            e1 += fast_exp2(fmaf(v[i + 1], p.scale_log2, -nms));
+            e2 += fast_exp2(fmaf(v[i + 2], p.scale_log2, -nms));
+            e3 += fast_exp2(fmaf(v[i + 3], p.scale_log2, -nms));
+          }
+          l = l * fast_exp2((m - nm) * p.scale_log2) + ((e0 + e1) + (e2 + e3));
+          m = nm;
         }
-        float* st = p.stats + ((static_cast<int64_t>(bh) * p.n_chunks + chunk) * GW + r) * 2;
-        st[0] = m;
-        st[1] = l;
+        m = m == -CUDART_INF_F ? m : m * p.scale_log2;  // to log2 units
+        if (cg > 0) {
+          sm.ml[(cg * GW + r) * 2] = m;
+          sm.ml[(cg * GW + r) * 2 + 1] = l;
+        }
+        epi_sync();
+        if (cg == 0) {
+          for (int gg = 1; gg < CG; ++gg) {
+            const float m1 = sm.ml[(gg * GW + r) * 2], l1 = sm.ml[(gg * GW + r) * 2 + 1];
+            const float nm = fmaxf(m, m1);
+            if (nm != -CUDART_INF_F) {
+              l = l * exp2f(m - nm) + l1 * exp2f(m1 - nm);
+              m = nm;
+            }
+          }
+          float* st = p.stats + ((static_cast<int64_t>(bh) * p.n_chunks + itm.chunk) * GW + r) * 2;
+          st[0] = m;
+          st[1] = l;
+        }
+        if constexpr (MULTI) epi_sync();  // sm.ml is free for the next item
       }
     }
-    if (kFused) {
-      sstamp(40);
-      epi_grid_sync(p.gridbar, n_bar);  // every chunk's statistics are in global memory
-      sstamp(41);
-      combine_stats();
-      epi_sync();
-    }
-    if (kP2) {
-      // keys in TMEM lanes, query rows in columns: warp (quad, cs) sums the
-      // exponentials of rows [cs*GW/4, (cs+1)*GW/4) for its 32 keys; the four
-      // column-group partials are added by the pooling
-      constexpr int NC = GW / 128;  // 32-column chunks per warp
-      const int key = 32 * quad + lane;
-      for (int i2 = 0; i2 < n2; ++i2) {
-        const int it = n1 + i2, buf = it % NB;
-        mbar_wait(&sm.tfull[buf], (it / NB) & 1);
-        tc_fence_after();
-        float acc = 0.f;
-        auto chunk_sum = [&](const uint32_t (&rr)[32], int c) {
-          const float4* b4 = reinterpret_cast<const float4*>(sm.bias + cs * (GW / 4) + c * 32);
-#pragma unroll
-          for (int i = 0; i < 32; i += 4) {
-            const float4 bb = b4[i / 4];  // broadcast: every lane reads the same columns
-            acc += fast_exp2(fmaf(__uint_as_float(rr[i]), p.scale_log2, -bb.x));
-            acc += fast_exp2(fmaf(__uint_as_float(rr[i + 1]), p.scale_log2, -bb.y));
-            acc += fast_exp2(fmaf(__uint_as_float(rr[i + 2]), p.scale_log2, -bb.z));
-            acc += fast_exp2(fmaf(__uint_as_float(rr[i + 3]), p.scale_log2, -bb.w));
+    sstamp(40);
+    epi_grid_sync(p.gridbar, n_bar);  // every chunk's statistics are in global memory
+    sstamp(41);
+    for (int w = 0; w < W; ++w) {
+      const Item itm = score_item(p, w);
+      const int bh = itm.bh, n2 = itm.e2 - itm.a;
+      if (n2 > 0) {
+        // combine the head's chunk statistics (log2 domain) into per-row biases:
+        // exp2(s*c - m) / (G*l) == exp2(s*c - bias), one FFMA + one MUFU per score
+        for (int r = threadIdx.x; r < GW; r += 32 * kEpiWarps) {
+          float M = -CUDART_INF_F, L = 0.f;
+          const float* st = p.stats + (static_cast<int64_t>(bh) * p.n_chunks) * GW * 2;
+          for (int c = 0; c < p.n_chunks; ++c) {
+            const float mc = __ldcg(st + (c * GW + r) * 2), lc = __ldcg(st + (c * GW + r) * 2 + 1);
+            if (lc <= 0.f) continue;
+            const float nm = fmaxf(M, mc);
+            L = L * exp2f(M - nm) + lc * exp2f(mc - nm);
+            M = nm;
           }
-        };
-        uint32_t ra[32], rb[32];
-        const uint32_t col = buf * GW + cs * (GW / 4);
-        tmem_ld32_nw(tmem + lane_base + col, ra);
-        if constexpr (NC == 2) {
-          tmem_ld32_nw(tmem + lane_base + col + 32, rb);
-          tmem_wait_ld(ra, rb);
-        } else {
-          tmem_wait_ld(ra);
+          sm.bias[r] = L > 0.f ? M + log2f(L * static_cast<float>(p.group)) : CUDART_INF_F;
         }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.tempty[buf]);
-        chunk_sum(ra, 0);
-        if constexpr (NC == 2) chunk_sum(rb, 1);
-        const int t = (a2 + i2) * kBN + key;
-        if (t < n) p.raw[(static_cast<int64_t>(cs) * gridDim.y + bh) * n + t] = acc;
+        epi_sync();
+        // keys in TMEM lanes, query rows in columns: warp (quad, cs) sums the
+        // exponentials of rows [cs*GW/4, (cs+1)*GW/4) for its 32 keys; the four
+        // column-group partials are added by the pooling
+        constexpr int NC = GW / 128;  // 32-column chunks per warp
+        const int key = 32 * quad + lane;
+        for (int i2 = 0; i2 < n2; ++i2, ++g) {
+          const int buf = g % NB;
+          mbar_wait(&sm.tfull[buf], (g / NB) & 1);
+          tc_fence_after();
+          float acc = 0.f;
+          auto chunk_sum = [&](const uint32_t (&rr)[32], int c) {
+            const float4* b4 = reinterpret_cast<const float4*>(sm.bias + cs * (GW / 4) + c * 32);
+#pragma unroll
+            for (int i = 0; i < 32; i += 4) {
+              const float4 bb = b4[i / 4];  // broadcast: every lane reads the same columns
+              acc += fast_exp2(fmaf(__uint_as_float(rr[i]), p.scale_log2, -bb.x));
+              acc += fast_exp2(fmaf(__uint_as_float(rr[i + 1]), p.scale_log2, -bb.y));
+              acc += fast_exp2(fmaf(__uint_as_float(rr[i + 2]), p.scale_log2, -bb.z));
+              acc += fast_exp2(fmaf(__uint_as_float(rr[i + 3]), p.scale_log2, -bb.w));
+            }
+          };
+          uint32_t ra[32], rb[32];
+          const uint32_t col = buf * GW + cs * (GW / 4);
+          tmem_ld32_nw(tmem + lane_base + col, ra);
+          if constexpr (NC == 2) {
+            tmem_ld32_nw(tmem + lane_base + col + 32, rb);
+            tmem_wait_ld(ra, rb);
+          } else {
+            tmem_wait_ld(ra);
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&sm.tempty[buf]);
+          chunk_sum(ra, 0);
+          if constexpr (NC == 2) chunk_sum(rb, 1);
+          const int t = (itm.a + i2) * kBN + key;
+          if (t < n) p.raw[(static_cast<int64_t>(cs) * p.bh_total + bh) * n + t] = acc;
+        }
+        epi_sync();  // sm.bias is free for the next item
       }
     }
-    if (kFused) {
-      sstamp(42);
-      epi_grid_sync(p.gridbar, n_bar);  // every raw column score is in global memory
-      sstamp(43);
+    sstamp(42);
+    epi_grid_sync(p.gridbar, n_bar);  // every raw column score is in global memory
+    sstamp(43);
+    // pooling of every item: the raw column sums (four partials added) of a
+    // block of keys and its halo, staged in the (idle) Q_win region, then
+    // max-pooled; one wave + per-chunk selection also stages the pooled keys
+    // in the (idle) K ring
+    float* sp = reinterpret_cast<float*>(&sm.k[0][0][0][0]);
+    float* stg = reinterpret_cast<float*>(&sm.q[0][0][0]);
+    constexpr int kStg = GW * 256 / 4;
+    const int R = p.pool_r, blk = kStg - 2 * R;
+    const int64_t part = static_cast<int64_t>(p.bh_total) * n;
+    Item mine{};
+    for (int w = 0; w < W; ++w) {
+      const Item itm = score_item(p, w);
+      if (itm.e2 <= itm.a) continue;
+      const int bh = itm.bh;
       float* out = p.scores + static_cast<int64_t>(bh) * n;
-      const int t_beg = a2 * kBN, t_end = min(e2 * kBN, n);
-      // MODE 4 stages this CTA's pooled scores in the K ring (idle: every tile
-      // was consumed before the epilogue reached the barrier above)
-      float* sp = reinterpret_cast<float*>(&sm.k[0][0][0][0]);
-      // the raw column sums (four partials added) of a block of keys and its
-      // pooling halo, staged in the (idle) Q_win region, then max-pooled
-      float* stg = reinterpret_cast<float*>(&sm.q[0][0][0]);
-      constexpr int kStg = GW * 256 / 4;
-      const int R = p.pool_r, blk = kStg - 2 * R;
-      const int64_t part = static_cast<int64_t>(gridDim.y) * n;
       const float* rw = p.raw + static_cast<int64_t>(bh) * n;
+      const int t_beg = itm.a * kBN, t_end = min(itm.e2 * kBN, n);
       for (int b0 = t_beg; b0 < t_end; b0 += blk) {
         const int b1 = min(b0 + blk, t_end);
         const int lo = b0 - R, cnt = b1 - b0 + 2 * R;
@@ -861,16 +970,32 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         epi_sync();
         for (int t = b0 + threadIdx.x; t < b1; t += 32 * kEpiWarps) {
-          const float* w = stg + (t - b0);  // taps t-R .. t+R
-          float mx = w[R];
-          for (int j = 0; j <= 2 * R; ++j) mx = fmaxf(mx, w[j]);
+          const float* wv = stg + (t - b0);  // taps t-R .. t+R
+          float mx = wv[R];
+          for (int j = 0; j <= 2 * R; ++j) mx = fmaxf(mx, wv[j]);
           out[t] = mx;
-          if (MODE == 4) sp[t - t_beg] = mx;
+          if (MODE == 4 && p.sel_mode == 1) sp[t - t_beg] = mx;
         }
         epi_sync();
       }
-      if (MODE == 4 && warp < kSelWarps)
-        select_phase(p, sm, b, h, bh, chunk, n, t_beg, max(t_end - t_beg, 0), sp, n_bar);
+    }
+    if (MODE == 4 && p.sel_mode == 1) {
+      // one wave, every CTA holds one chunk (possibly without scored keys) and
+      // takes part in the selection's grid barriers
+      mine = score_item(p, 0);
+      if (warp < kSelWarps) {
+        const int b = mine.bh / p.hkv, h = mine.bh - b * p.hkv;
+        const int t_beg = mine.a * kBN, t_end = min(mine.e2 * kBN, n);
+        select_phase(p, sm, b, h, mine.bh, mine.chunk, n, t_beg, max(t_end - t_beg, 0), sp, n_bar);
+      }
+    } else if (MODE == 4 && p.sel_mode == 2) {
+      // every pooled score is in global memory: the grid-wide search over them,
+      // its state in the Q_win region and its key cache in the K ring
+      epi_grid_sync(p.gridbar, n_bar);
+      static_assert(sizeof(GSelSmem) <= sizeof(sm.q), "grid-select state must fit in the Q_win region");
+      uint8_t* base = reinterpret_cast<uint8_t*>(&sm.q[0][0][0]);
+      gsel_body(p.gs, *reinterpret_cast<GSelSmem*>(base), reinterpret_cast<uint32_t*>(base + gsel_cache_off()),
+                EpiCx{static_cast<int>(blockIdx.y * gridDim.x + blockIdx.x), static_cast<int>(gridDim.x * gridDim.y)});
     }
   }
   tc_fence_before();
@@ -879,22 +1004,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     tmem_dealloc(tmem, kCols);
   }
-}
-
-// Max-pool (kernel pool_k, stride 1, -inf padding) of the raw column scores.
-__global__ void pool_kernel(const float* __restrict__ raw, float* __restrict__ out, int n,
-                            int radius, int64_t total) {
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= total) return;
-  const int64_t row = i / n;
-  const int t = static_cast<int>(i - row * n);
-  const float* r = raw + row * n;  // column partial 0; partial c at + c * total
-  // the four column-group partials, added in the fused kernel's order
-  auto col = [&](int u) { return (r[u] + r[total + u]) + (r[2 * total + u] + r[3 * total + u]); };
-  float m = col(t);
-  const int lo = max(0, t - radius), hi = min(n - 1, t + radius);
-  for (int u = lo; u <= hi; ++u) m = fmaxf(m, col(u));
-  out[i] = m;
 }
 
 // ------------------------------------------------------- host helpers ----
@@ -934,41 +1043,55 @@ int make_map(CUtensorMap* map, const void* base, int64_t rows, int box_rows) {
 
 }  // namespace
 
-// Key chunks per (request, KV head): one wave of one CTA per SM when the
-// heads alone do not fill the GPU; never more chunks than tiles.
-int score_chunks(int bh, int n_tiles) {
+// Persistent schedule of one scoring launch (one CTA per SM): each KV head
+// cut into `chunks` key chunks, the bh * chunks items dealt round robin over
+// `grid` CTAs, `waves` items per CTA at most.  The chunk count minimises the
+// busiest CTA's tiles plus a per-item cost (Q_win reload, pipeline restart
+// ~ 1.5 tiles), fewer chunks on ties; heads that fit one wave keep one item
+// per CTA: batch 1 at 16k -> 16 chunks per head, batch 1 at 128k -> 18,
+// batch 4 at 16k -> 4, batch 32 at 16k -> 4 (seven items per CTA).
+struct Waves {
+  int chunks, waves, grid;
+};
+Waves score_waves(int bh, int T) {
   static std::atomic<int> sms_of[kMaxDevices];
   const int sms = per_device(sms_of, sm_count);
-  int c = sms / bh;
-  // one co-resident wave (the fused cooperative launch) when it keeps >= 80 %
-  // of the SMs busy; otherwise several waves of CTAs (the multi-launch path):
-  // the fewest chunks per head whose last wave is >= 90 % full, keeping >= 16
-  // tiles per chunk (tools/probe_prefill_batch.py: 80-144 heads of 16k keys
-  // at one chunk each left up to half the SMs idle)
-  if (c < 1 || static_cast<long long>(bh) * c * 100 < 80LL * sms) {
-    int best = c < 1 ? 1 : c;
-    double best_fill = 0.0;
-    for (int t = 1; t <= 16 && n_tiles / t >= 16; ++t) {
-      const long long ctas = static_cast<long long>(bh) * t;
-      const long long waves = (ctas + sms - 1) / sms;
-      const double fill = static_cast<double>(ctas) / static_cast<double>(waves * sms);
-      if (fill > best_fill + 1e-9) best_fill = fill, best = t;
-      if (fill >= 0.9) break;
+  const int n_tiles = (T + kBN - 1) / kBN;
+  static const int force_chunks = [] {  // tuning experiments: FKV_SCORE_CHUNKS
+    const char* e = getenv("FKV_SCORE_CHUNKS");
+    return e ? atoi(e) : 0;
+  }();
+  Waves best{1, 1, 1};
+  double best_cost = 1e300;
+  // heads that fit one wave stay in one (one item per CTA: the per-chunk
+  // selection and no Q_win reloads): the most chunks that still fit
+  const int one_wave = bh <= sms ? sms / bh : 0;
+  for (int c = 1; c <= n_tiles && c <= 256; ++c) {
+    if (force_chunks > 0 && c != force_chunks) continue;
+    if (force_chunks == 0 && one_wave > 0 && c > one_wave) break;
+    const int64_t items = static_cast<int64_t>(bh) * c;
+    const int64_t waves = (items + sms - 1) / sms;
+    const double cost = static_cast<double>(waves) * ((n_tiles + c - 1) / c + 1.5);
+    if (cost < best_cost - 1e-9) {
+      best_cost = cost;
+      best.chunks = c;
+      best.waves = static_cast<int>(waves);
+      best.grid = static_cast<int>(items < sms ? items : sms);
     }
-    c = best;
   }
-  return c > n_tiles ? n_tiles : c;
+  return best;
 }
 
 namespace {
 
 template <int GW>
-int launch_score(const CUtensorMap& tq, const CUtensorMap& tk, const ScoreParams& p, int batch_heads,
-                 int mode, cudaStream_t st, size_t reset_bytes = sizeof(GridBar)) {
+int launch_score(const CUtensorMap& tq, const CUtensorMap& tk, const ScoreParams& p, int grid, int mode,
+                 cudaStream_t st, size_t reset_bytes) {
   const size_t smem = sizeof(ScoreSmem<GW>) + 1024;
   static std::atomic<int> ready[kMaxDevices];  // smem attributes set on this device
   const int rc0 = per_device(ready, [smem](int) {
-    for (auto fn : {score_kernel<1, GW>, score_kernel<2, GW>, score_kernel<3, GW>, score_kernel<4, GW>})
+    for (auto fn : {score_kernel<3, GW, false>, score_kernel<4, GW, false>, score_kernel<3, GW, true>,
+                    score_kernel<4, GW, true>})
       if (int rc = cuda_check(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    smem),
                               "score smem attribute"))
@@ -976,72 +1099,55 @@ int launch_score(const CUtensorMap& tq, const CUtensorMap& tk, const ScoreParams
     return 1;
   });
   if (rc0 < 0) return rc0;
-  dim3 grid(p.n_chunks, batch_heads);
-  if (mode >= 3) {
-    // one cooperative launch: both passes and the pooling (grid <= #SMs, 1 CTA/SM)
-    // [+ MODE 4: the Ada split and top-k selection]
-    // grid barrier counter (+ MODE 4: the per-pass histograms right after it)
-    if (int rc = cuda_check(cudaMemsetAsync(p.gridbar, 0, reset_bytes, st), "gridbar reset"))
-      return rc;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = grid;
-    cfg.blockDim = dim3(kThreads, 1, 1);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeCooperative;
-    attr[0].val.cooperative = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return cuda_check(cudaLaunchKernelEx(&cfg, mode == 4 ? score_kernel<4, GW> : score_kernel<3, GW>, tq,
-                                         tk, p),
-                      "score fused launch");
-  }
-  score_kernel<1, GW><<<grid, kThreads, smem, st>>>(tq, tk, p);
-  if (int rc = cuda_check(cudaGetLastError(), "score pass 1 launch")) return rc;
-  score_kernel<2, GW><<<grid, kThreads, smem, st>>>(tq, tk, p);
-  if (int rc = cuda_check(cudaGetLastError(), "score pass 2 launch")) return rc;
-  const int n = p.T - p.window;
-  const int64_t total = static_cast<int64_t>(batch_heads) * n;
-  pool_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(p.raw, p.scores, n,
-                                                                         p.pool_r, total);
-  return cuda_check(cudaGetLastError(), "score pool launch");
+  // grid barrier counters (+ the selection's zeroed histograms right after them)
+  if (int rc = cuda_check(cudaMemsetAsync(p.gridbar, 0, reset_bytes, st), "score workspace reset")) return rc;
+  cudaLaunchConfig_t cfg = {};
+  // one wave: a (chunks, heads) grid (measured: the same CTAs as a 1-D grid
+  // stream K ~30 % faster -- block placement over the two dies)
+  cfg.gridDim = p.n_waves == 1 && getenv("FKV_SCORE_1D") == nullptr ? dim3(p.n_chunks, p.bh_total, 1)
+                                                                    : dim3(grid, 1, 1);
+  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // grid barriers: every CTA co-resident (one per SM)
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const bool multi = p.n_waves > 1;
+  auto fn = mode == 4 ? (multi ? score_kernel<4, GW, true> : score_kernel<4, GW, false>)
+                      : (multi ? score_kernel<3, GW, true> : score_kernel<3, GW, false>);
+  return cuda_check(cudaLaunchKernelEx(&cfg, fn, tq, tk, p), "score launch");
 }
 
-}  // namespace
-}  // namespace fkv
-
-namespace fkv {
-namespace {
+// Workspace: stats | raw | gridbar | zeroed selection state | per-chunk counts | standalone select
 struct ScoreLayout {
-  int chunks, tiles_per_chunk, bh;
-  int64_t stats, raw, gridbar, hist, counts, sel, total;
+  Waves wv;
+  int bh;
+  int64_t stats, raw, gridbar, zero, zero_bytes1, zero_bytes2, counts, sel, total;
 };
 
 ScoreLayout score_layout(int batch, int hkv, int T, int window, int group) {
   ScoreLayout L{};
   const int gw = group * window;
-  const int n_tiles = (T + kBN - 1) / kBN;
   L.bh = batch * hkv;
-  int chunks = score_chunks(L.bh > 0 ? L.bh : 1, n_tiles);
-  L.tiles_per_chunk = (n_tiles + chunks - 1) / chunks;
-  L.chunks = (n_tiles + L.tiles_per_chunk - 1) / L.tiles_per_chunk;
+  L.wv = score_waves(L.bh > 0 ? L.bh : 1, T);
   auto a16 = [](int64_t x) { return (x + 255) & ~int64_t(255); };
+  const int64_t n = T - window;
   L.stats = 0;
-  L.raw = a16(L.stats + static_cast<int64_t>(L.bh) * L.chunks * gw * 2 * 4);
-  L.gridbar = a16(L.raw + static_cast<int64_t>(L.bh) * (T - window) * 4 * kRawParts);  // column partials
-  L.hist = a16(L.gridbar + 64);
-  L.counts = a16(L.hist + static_cast<int64_t>(kSelPasses) * L.bh * 512 * 4);
-  L.sel = a16(L.counts + static_cast<int64_t>(L.bh) * L.chunks * 8);
+  L.raw = a16(L.stats + static_cast<int64_t>(L.bh) * L.wv.chunks * gw * 2 * 4);
+  L.gridbar = a16(L.raw + static_cast<int64_t>(L.bh) * n * 4 * kRawParts);  // column partials
+  L.zero = L.gridbar + 256;
+  // sel_mode 1: per-pass per-head digit histograms; sel_mode 2: the grid
+  // search's barrier (256 B), three histogram buffers (two zeroed) and counts
+  L.zero_bytes1 = static_cast<int64_t>(kSelPasses) * L.bh * 512 * 4;
+  L.zero_bytes2 = 256 + static_cast<int64_t>(2) * L.bh * 512 * 4;
+  const int64_t zone = std::max(L.zero_bytes1, 256 + static_cast<int64_t>(kGBufs) * L.bh * 512 * 4 +
+                                                   static_cast<int64_t>(L.wv.grid) * 8);
+  L.counts = a16(L.zero + zone);
+  L.sel = a16(L.counts + static_cast<int64_t>(L.bh) * L.wv.chunks * 8);
   L.total = a16(L.sel + fkv_ada_select_workspace_bytes(batch, hkv, T - window));
   return L;
-}
-
-int sms_count() {
-  int sms = 148, dev = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  return sms;
 }
 
 int score_common(const void* q_win, const void* k, int32_t batch, int32_t hq, int32_t hkv, int32_t T,
@@ -1066,8 +1172,9 @@ int score_common(const void* q_win, const void* k, int32_t batch, int32_t hq, in
   p.window = window;
   p.group = group;
   p.hkv = hkv;
-  p.n_chunks = L.chunks;
-  p.tiles_per_chunk = L.tiles_per_chunk;
+  p.n_chunks = L.wv.chunks;
+  p.n_waves = L.wv.waves;
+  p.bh_total = L.bh;
   p.q_rows_per_req = hq * window;
   p.scale_log2 = sm_scale * kLog2e;
   p.stats = reinterpret_cast<float*>(ws + L.stats);
@@ -1075,7 +1182,7 @@ int score_common(const void* q_win, const void* k, int32_t batch, int32_t hq, in
   p.scores = scores;
   p.pool_r = pool_k / 2;
   p.gridbar = reinterpret_cast<GridBar*>(ws + L.gridbar);
-  p.hist = reinterpret_cast<uint32_t*>(ws + L.hist);
+  p.hist = reinterpret_cast<uint32_t*>(ws + L.zero);
   p.counts = reinterpret_cast<int32_t*>(ws + L.counts);
   return FKV_OK;
 }
@@ -1103,12 +1210,9 @@ extern "C" int fkv_snapkv_score(const void* q_win, const void* k, int32_t batch,
                             p, L, tq, tk))
     return rc;
   auto st = static_cast<cudaStream_t>(stream);
-  // fused single launch whenever every CTA can be co-resident (1 CTA per SM)
-  const int mode = static_cast<int64_t>(L.bh) * L.chunks <= sms_count() ? 3 : 1;
-  return p.group * window == 128 ? launch_score<128>(tq, tk, p, L.bh, mode, st)
-                                 : launch_score<256>(tq, tk, p, L.bh, mode, st);
+  return p.group * window == 128 ? launch_score<128>(tq, tk, p, L.wv.grid, 3, st, 256)
+                                 : launch_score<256>(tq, tk, p, L.wv.grid, 3, st, 256);
 }
-
 
 extern "C" int fkv_snapkv_select(const void* q_win, const void* k, int32_t batch, int32_t hq,
                                  int32_t hkv, int32_t T, int32_t window, int32_t pool_k,
@@ -1127,15 +1231,18 @@ extern "C" int fkv_snapkv_select(const void* q_win, const void* k, int32_t batch
                             p, L, tq, tk))
     return rc;
   auto st = static_cast<cudaStream_t>(stream);
-  const bool fused = static_cast<int64_t>(L.bh) * L.chunks <= sms_count() && hkv <= kSelMaxHeads &&
-                     L.tiles_per_chunk * kBN <= kSelMaxKeys;
-  if (!fused) {  // two launches: scoring, then the cluster split + select (select.cu)
-    const int mode = static_cast<int64_t>(L.bh) * L.chunks <= sms_count() ? 3 : 1;
-    if (int rc = p.group * window == 128 ? launch_score<128>(tq, tk, p, L.bh, mode, st)
-                                         : launch_score<256>(tq, tk, p, L.bh, mode, st))
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  const int max_chunk_keys = ((T + kBN - 1) / kBN + L.wv.chunks - 1) / L.wv.chunks * kBN;
+  if (L.wv.waves == 1 && hkv <= kSelMaxHeads && max_chunk_keys <= kSelMaxKeys) {
+    p.sel_mode = 1;  // every CTA selects within its own chunk
+  } else if (hkv <= kGMaxHeads && L.bh <= (kGMaxPieces - 2) * L.wv.grid) {
+    p.sel_mode = 2;  // grid-wide search over the pooled scores, same launch
+  } else {           // two launches: scoring, then the standalone grid select (select.cu)
+    if (int rc = p.group * window == 128 ? launch_score<128>(tq, tk, p, L.wv.grid, 3, st, 256)
+                                         : launch_score<256>(tq, tk, p, L.wv.grid, 3, st, 256))
       return rc;
-    return fkv_ada_select(scores, batch, hkv, n, budget, window, floor_k, budgets, offsets, idx,
-                          static_cast<uint8_t*>(workspace) + L.sel, stream);
+    return fkv_ada_select(scores, batch, hkv, n, budget, window, floor_k, budgets, offsets, idx, ws + L.sel,
+                          stream);
   }
   p.budget = budget;
   p.floor_k = floor_k;
@@ -1143,8 +1250,30 @@ extern "C" int fkv_snapkv_select(const void* q_win, const void* k, int32_t batch
   p.budgets = budgets;
   p.offsets = offsets;
   p.idx = idx;
-  // the barrier counter and the per-pass histograms are one contiguous range
-  const size_t reset = static_cast<size_t>(L.counts - L.gridbar);
-  return p.group * window == 128 ? launch_score<128>(tq, tk, p, L.bh, 4, st, reset)
-                                 : launch_score<256>(tq, tk, p, L.bh, 4, st, reset);
+  size_t reset = 256 + static_cast<size_t>(p.sel_mode == 1 ? L.zero_bytes1 : L.zero_bytes2);
+  if (p.sel_mode == 2) {
+    GSelParams& g = p.gs;
+    g.scores = scores;
+    g.hkv = hkv;
+    g.n = n;
+    g.window = window;
+    g.f = floor_k;
+    g.R = p.rest_total;
+    g.budget = budget;
+    g.select = 1;
+    g.req0 = 0;
+    g.bh_total = L.bh;
+    g.total = static_cast<int64_t>(L.bh) * n;
+    g.bar = reinterpret_cast<unsigned*>(ws + L.zero);
+    g.hist = reinterpret_cast<uint32_t*>(ws + L.zero + 256);
+    g.counts = reinterpret_cast<int2*>(ws + L.zero + 256 + static_cast<int64_t>(kGBufs) * L.bh * 512 * 4);
+    g.budgets = budgets;
+    g.offsets = offsets;
+    g.idx = idx;
+    const int64_t span_keys = (g.total + L.wv.grid - 1) / L.wv.grid + 1;
+    // the CTA's keys fit in the (idle) Q_win + K ring after the select state
+    g.cache = span_keys <= (p.group * window == 128 ? gsel_cache_keys<128>() : gsel_cache_keys<256>());
+  }
+  return p.group * window == 128 ? launch_score<128>(tq, tk, p, L.wv.grid, 4, st, reset)
+                                 : launch_score<256>(tq, tk, p, L.wv.grid, 4, st, reset);
 }

@@ -245,11 +245,14 @@ def test_fused_ada_select_bit_exact(cuda_device, bt, T, budget, ties, hkv, alpha
     (1, 32, 8, 20000, 1024, 3.0, False),  # long context, several chunks per head
     (2, 32, 8, 3000, 256, 2.0, True),     # a head whose window soaks up all attention: below its floor
     (1, 32, 8, 40000, 1024, 3.0, True),   # the same over many chunks per head (joint floor search)
-    (20, 32, 8, 600, 64, 2.0, False),     # 160 heads > 148 SMs: two-launch fallback
-    (1, 64, 8, 131072, 1024, 2.0, False),  # cfg5: 128k context, B=1024, 70B shape
+    (20, 32, 8, 600, 64, 2.0, False),     # 160 heads > 148 SMs: two waves, grid-wide select in the launch
+    (1, 64, 8, 131072, 1024, 2.0, False),  # cfg5: 128k context, B=1024, 70B shape (four L2 waves)
+    (32, 32, 8, 16384, 256, 3.0, False),  # batch 32 at 16k: 16 waves of 16 heads, one launch
 ])
 def test_fused_score_select_bit_exact(cuda_device, bt, hq, hkv, T, budget, temp, flat_head):
-    """K1 + A18 + K2 in one launch: scores within tolerance of the oracle;
+    """K1 + A18 + K2 in one persistent launch at any batch (one wave with the
+    per-chunk selection, or several L2-sized waves with the grid-wide search):
+    scores within tolerance of the oracle;
     budgets / offsets / indices bit-exact against the oracle fed the kernel's
     own pooled scores (max-pooling makes exact ties common)."""
     from paper_2502_15804_b200 import ops
