@@ -242,15 +242,15 @@ int fkv_snapkv_score(const void* q_win, const void* k, int32_t batch, int32_t hq
                      int32_t T, int32_t window, int32_t pool_k, float sm_scale, float* scores,
                      void* workspace, void* stream);
 
-/* K1 + A18 + K2 in one cooperative launch: the scores above, then the Ada
- * budget split and the per-head top-k selection by a grid-wide radix search
- * over the pooled scores (every CTA histograms its own key range; per-pass
- * digit histograms meet in the workspace between grid barriers).  Outputs
- * are identical to fkv_snapkv_score followed by fkv_ada_select (budgets
- * int32 [batch, hkv], offsets int64 [batch*hkv + 1] with request b starting
- * at b*hkv*budget, idx int32 [batch*hkv*budget]).  Same workspace size as
- * fkv_snapkv_score.  Shapes whose grid cannot be co-resident (or Hkv > 16)
- * run as those two launches. */
+/* K1 + A18 + K2 in one persistent cooperative launch at any batch: the
+ * scores above, then the Ada budget split and the per-head top-k selection
+ * by a grid-wide radix search over the pooled scores (every CTA histograms
+ * its own key range; per-pass digit histograms meet in the workspace between
+ * grid barriers).  Outputs are identical to fkv_snapkv_score followed by
+ * fkv_ada_select (budgets int32 [batch, hkv], offsets int64 [batch*hkv + 1]
+ * with request b starting at b*hkv*budget, idx int32 [batch*hkv*budget]).
+ * Same workspace size as fkv_snapkv_score.  Hkv > 16, or more than 14 heads
+ * per SM, run as those two launches. */
 int fkv_snapkv_select(const void* q_win, const void* k, int32_t batch, int32_t hq, int32_t hkv,
                       int32_t T, int32_t window, int32_t pool_k, float sm_scale, int32_t budget,
                       int32_t floor_k, float* scores, int32_t* budgets, int64_t* offsets,

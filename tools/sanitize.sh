@@ -5,7 +5,7 @@
 OUT=gpurun_out/sanitize
 mkdir -p $OUT
 CS=/usr/local/cuda/bin/compute-sanitizer
-PARTS="score_fused score_multi select compress_decode decode_coop decode_wide decode_solo exchange"
+PARTS="score_fused score_multi score_fused256 score_multi256 select compress_decode decode_coop decode_wide decode_solo exchange"
 : > $OUT/summary.txt
 for tool in memcheck racecheck synccheck initcheck; do
   for part in $PARTS; do

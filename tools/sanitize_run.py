@@ -6,7 +6,7 @@ the summaries to ``gpurun_out/sanitize/``.  Each part also checks its result
 against the float64 oracle, so a run that "passes" the sanitizer with wrong
 numbers is caught too.
 
-  python tools/sanitize_run.py {score_fused,score_multi,select,compact,
+  python tools/sanitize_run.py {score_fused,score_multi,score_fused256,score_multi256,select,compact,
                                 decode_coop,decode_wide,decode_solo,exchange,append}
 """
 
@@ -170,7 +170,9 @@ def exchange():
 
 PARTS = {
     "score_fused": lambda: score(1, 32, 8, 2048),
-    "score_multi": lambda: score(20, 32, 8, 300),
+    "score_multi": lambda: score(20, 32, 8, 300),  # 160 heads: several items per CTA, grid-wide select
+    "score_fused256": lambda: score(1, 64, 8, 2048),  # G*w = 256 (70B shape)
+    "score_multi256": lambda: score(20, 64, 8, 300),
     "select": select,
     "compress_decode": compress_decode,
     "decode_coop": lambda: decode_sched("coop"),
