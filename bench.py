@@ -653,6 +653,10 @@ def emulate_tp(args, budgets, dev, base, q, tps=(2, 4, 8), modes=("sha",) + AHA_
                  "extra_copies": int(sum(len(g) for la in m["plan"].layers for g in la.groups) - L * HKV),
                  "rounds_tokens_per_s": [round(bt / x, 1) for x in steps],
                  "placement": mode_label(tp, mode, args.ch)}
+            # the reference's load efficiency of the plan (allocate.py:418-424: mean
+            # per-GPU load / bottleneck load), beside the measured busy rate
+            import paper_2502_15804_b200 as fk
+            r["efficiency"] = float((hb or fk).efficiency(m["plan"], m["prof"]))
             if hb is not None:  # the reference simulator's prediction (pure-cache latency law)
                 model = hb.LatencyModel(0.0, 0.0, 1.0, 0.0)
                 r["sim_throughput"] = hb.simulate(m["prof"], m["plan"], model, hb.SimulationConfig(1, 1, tp)).throughput
