@@ -859,14 +859,6 @@ __device__ __forceinline__ int4 ld_ll(const uint8_t* a) {
                : "memory");
   return v;
 }
-__device__ __forceinline__ int4 wait_ll(const uint8_t* a, int ep) {
-  int4 v = ld_ll(a);
-  while (v.y != ep || v.w != ep) {
-    __nanosleep(20);
-    v = ld_ll(a);
-  }
-  return v;
-}
 
 template <int G, bool LL>
 __global__ void __launch_bounds__(G * 32)
@@ -898,9 +890,19 @@ __global__ void __launch_bounds__(G * 32)
     float l;
     uint2 w;
     if (LL) {
+      // both units' loads in flight together, then each polled until it
+      // carries the epoch (one round trip on the critical path, not two)
       const uint8_t* r = blk + row * FKV_XLL_ROW_BYTES;
-      const int4 u = wait_ll(r + 16 * lane, ep);
-      l = __int_as_float(wait_ll(r + 32 * 16, ep).x);
+      int4 u = ld_ll(r + 16 * lane), ul = ld_ll(r + 32 * 16);
+      while (u.y != ep || u.w != ep) {
+        __nanosleep(20);
+        u = ld_ll(r + 16 * lane);
+      }
+      while (ul.y != ep || ul.w != ep) {
+        __nanosleep(20);
+        ul = ld_ll(r + 32 * 16);
+      }
+      l = __int_as_float(ul.x);
       w = make_uint2(u.x, u.z);
     } else {
       l = __ldcg(reinterpret_cast<const float*>(blk + lse_off) + row);
