@@ -247,7 +247,8 @@ def test_fused_ada_select_bit_exact(cuda_device, bt, T, budget, ties, hkv, alpha
     (1, 32, 8, 40000, 1024, 3.0, True),   # the same over many chunks per head (joint floor search)
     (20, 32, 8, 600, 64, 2.0, False),     # 160 heads > 148 SMs: two waves, grid-wide select in the launch
     (1, 64, 8, 131072, 1024, 2.0, False),  # cfg5: 128k context, B=1024, 70B shape (four L2 waves)
-    (32, 32, 8, 16384, 256, 3.0, False),  # batch 32 at 16k: 16 waves of 16 heads, one launch
+    (32, 32, 8, 16384, 256, 3.0, False),  # batch 32 at 16k: several items per CTA, one launch
+    (20, 64, 8, 900, 128, 2.0, True),     # G*w = 256 with several items per CTA (Q_win reloads), a flat head
 ])
 def test_fused_score_select_bit_exact(cuda_device, bt, hq, hkv, T, budget, temp, flat_head):
     """K1 + A18 + K2 in one persistent launch at any batch (one wave with the
