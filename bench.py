@@ -1013,6 +1013,24 @@ def prefill_compress(peaks):
                   "ada_select_us": graph_us(lambda: ops.ada_select(sc, B, w, workspace=wsel)),
                   "score_select_us": graph_us(lambda: ops.score_select(q, k, B, w, workspace=ws)),
                   "compact_us": graph_us(lambda: ops.compact_into(cache, k, v, off, idx, sbh, slo, shi, mx))}
+        # a whole layer stack's compression (8 layers, host-visible wall time):
+        # per layer compress_layer (one host round trip per layer) vs
+        # compress_stack (all fused launches queued, one round trip, then
+        # every compaction)
+        Ls = 8
+
+        def per_layer():
+            for _ in range(Ls):
+                ops.compress_layer(q, k, v, B, w)
+            torch.cuda.synchronize()
+
+        def stacked():
+            ops.compress_stack([q] * Ls, [k] * Ls, [v] * Ls, B, w)
+            torch.cuda.synchronize()
+        per_layer()
+        stacked()
+        t_pl = min(timed(per_layer, 1) for _ in range(3)) / Ls
+        t_st = min(timed(stacked, 1) for _ in range(3)) / Ls
         flops = 2 * 2.0 * bt * hq * w * T * HEAD_DIM  # two passes of Q_win.K^T
         exps = 2.0 * bt * hq * w * T  # one ex2 per score per pass (MUFU)
         kbytes = bt * hkv * T * HEAD_DIM * 2
@@ -1027,6 +1045,8 @@ def prefill_compress(peaks):
             "score_K_read_GBs_per_pass": kbytes / (t_score / 2) / 1e9,
             "roofline_us": max(flops / (tf_peak * 1e12), 2 * kbytes / (float(peaks.get("hbm_gbs", 6650.0)) * 1e9)) * 1e6,
             "graph_replay": dev_us,
+            "stack8_compress_layer_us_per_layer": t_pl * 1e6,
+            "stack8_compress_stack_us_per_layer": t_st * 1e6,
             # K1 is bound by the special-function unit, not the tensor cores:
             # two exponentials per (query row, key), at the measured ex2 rate
             "mufu_bound_us": exps / mufu_rate * 1e6,

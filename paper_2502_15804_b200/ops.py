@@ -379,3 +379,31 @@ def compress_layer(q_win: torch.Tensor, k: torch.Tensor, v: torch.Tensor, budget
     qrow = (bh // hkv) * hq + (bh % hkv) * group
     cache = compact(k, v, offsets, idx, bh, np.zeros_like(bh), hb_host, qrow, qrow, group)
     return cache, hb, sc
+
+
+def compress_stack(q_wins, ks, vs, budget: int, window: int = 32, alpha: float = 0.2, pool_k: int = 7):
+    """Prefill compression of a whole layer stack on one GPU with ONE host
+    round trip: every layer's fused K1 + A18 + K2 launch is queued first
+    (workspace reused, stream ordered), the budgets of all layers come back
+    in one copy, then every layer's K3 compaction is queued.  compress_layer
+    per layer instead stalls the stream once per layer (the host must know a
+    layer's budgets to lay out its ragged cache).  q_wins / ks / vs: one
+    tensor per layer, shapes as compress_layer.  Returns ([cache], budgets
+    int32 [L, Bt, Hkv] on the device, [scores])."""
+    import numpy as np
+    if not (len(q_wins) == len(ks) == len(vs)) or not ks:
+        raise NativeError("compress_stack needs the same number (>= 1) of q_win, k and v tensors")
+    bt, hq, w = q_wins[0].shape[0], q_wins[0].shape[1], q_wins[0].shape[2]
+    hkv, T = ks[0].shape[1], ks[0].shape[2]
+    group = hq // hkv
+    dev = ks[0].device
+    need = int(_lib.fkv_score_workspace_bytes(bt, hkv, T, w, group))
+    ws = torch.empty(need, dtype=torch.uint8, device=dev)
+    sel = [score_select(q, k, budget, window, alpha, pool_k, workspace=ws) for q, k in zip(q_wins, ks)]
+    hbs = torch.stack([x[1] for x in sel])
+    hb_host = hbs.cpu().numpy()  # the one host round trip
+    bh = np.arange(bt * hkv)
+    qrow = (bh // hkv) * hq + (bh % hkv) * group
+    caches = [compact(k, v, x[2], x[3], bh, np.zeros_like(bh), hb_host[l].reshape(-1), qrow, qrow, group)
+              for l, (k, v, x) in enumerate(zip(ks, vs, sel))]
+    return caches, hbs, [x[0] for x in sel]

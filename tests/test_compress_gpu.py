@@ -182,6 +182,24 @@ def test_compress_then_decode_end_to_end(cuda_device):
     torch.testing.assert_close(lse.cpu().double(), torch.from_numpy(lse_ref), rtol=1e-4, atol=1e-5)
 
 
+def test_compress_stack_matches_per_layer(cuda_device):
+    """compress_stack (all layers' fused launches queued, one host round trip,
+    then every compaction) builds the same caches as compress_layer per layer:
+    budgets, scores and the compacted K/V bytes bit for bit."""
+    from paper_2502_15804_b200 import ops
+    L, bt, hq, hkv, T, B = 3, 2, 32, 8, 2500, 256
+    layers = [_inputs(bt, hq, hkv, T, 32, 40 + l, cuda_device, temp=2.0)[:3] for l in range(L)]
+    caches, hbs, scs = ops.compress_stack([x[0] for x in layers], [x[1] for x in layers],
+                                          [x[2] for x in layers], B)
+    torch.cuda.synchronize()
+    for l, (q, k, v) in enumerate(layers):
+        cache, hb, sc = ops.compress_layer(q, k, v, B)
+        torch.cuda.synchronize()
+        assert torch.equal(hbs[l], hb) and torch.equal(scs[l], sc)
+        assert torch.equal(caches[l].k, cache.k) and torch.equal(caches[l].v, cache.v)
+        assert torch.equal(caches[l].work, cache.work)
+
+
 def test_selection_agreement_with_oracle_scores(cuda_device):
     """Unconstrained inputs: index sets chosen from GPU scores vs from the
     float64 oracle scores agree except at near-ties (reported, >= 98%)."""
