@@ -139,6 +139,34 @@ typedef struct fkv_work {
  * the wait. */
 #define FKV_DECODE_AFTER_WAIT 4
 
+/* Host-side K4 schedule planner (csrc/schedule.cpp; the Python form is
+ * cache.plan_schedule, kept as its checker).  Picks the CTA shape of one
+ * cache (FKV_DECODE_SOLO / FKV_DECODE_WIDE / cooperative; split or
+ * whole-segment pieces) and builds its work table.  Device parameters: SM
+ * count and fkv_decode_ctas_per_sm() of each shape; the remaining fields are
+ * the planner's tuning knobs (cache.py: FKV_K4_SCHEDULE, FKV_K4_WHOLE,
+ * FKV_SOLO_SMALL, FKV_SOLO_PIECE, FKV_SOLO_WHOLE, FKV_PIECE_COST,
+ * FKV_PAIR_PIECE, FKV_SM_PAIRING; chunk <= 0: none). */
+typedef struct {
+  int32_t sms, ctas_coop, ctas_wide, ctas_solo;
+  int32_t mode;                  /* 0 auto, 1 coop, 2 wide, 3 solo */
+  int32_t whole;                 /* -1 auto, 0 never, 1 always */
+  int32_t solo_small, solo_piece, solo_whole;  /* solo_piece / solo_whole: -1 = default */
+  int32_t piece_cost, sm_pairing, chunk;
+  double pair_piece;
+} fkv_sched_params;
+
+/* Outputs (int32): item_seg / item_t0 / item_t1 / work_list [n_items],
+ * seg_item_ptr [n_seg + 1], warp_ptr [busy + 1], table [rows * K * 8]
+ * (fkv_work_t rows); out_sizes = {n_items, busy, rows, K, flags}.  Buffers
+ * hold item_cap items, worker_cap workers and table_cap table ints; too
+ * small: FKV_ERR_INVALID with the needed sizes in out_sizes. */
+int fkv_plan_schedule(const int64_t* seg_len, const int64_t* seg_row0, const int64_t* seg_qrow,
+                      const int64_t* seg_out_row, int32_t n_seg, const fkv_sched_params* prm,
+                      int32_t item_cap, int32_t worker_cap, int32_t table_cap, int32_t* item_seg,
+                      int32_t* item_t0, int32_t* item_t1, int32_t* seg_item_ptr, int32_t* warp_ptr,
+                      int32_t* work_list, int32_t* table, int32_t* out_sizes);
+
 /* Exchange records (the per-layer all-gather payload; "XREC"): a block of
  * `slots` rows of `group` heads =
  *     bf16 o[slots * group][128]   (256 bytes per head row)

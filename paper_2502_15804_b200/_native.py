@@ -44,6 +44,13 @@ _check_fresh()
 lib = C.CDLL(str(LIB_PATH))  # CDLL releases the GIL for the duration of each call
 
 _i32, _i64, _f32, _f64, _vp = C.c_int32, C.c_int64, C.c_float, C.c_double, C.c_void_p
+
+
+class SchedParams(C.Structure):
+    """fkv_sched_params (include/fairkv.h)."""
+    _fields_ = [(n, C.c_int32) for n in ("sms", "ctas_coop", "ctas_wide", "ctas_solo", "mode", "whole",
+                                         "solo_small", "solo_piece", "solo_whole", "piece_cost",
+                                         "sm_pairing", "chunk")] + [("pair_piece", C.c_double)]
 _pi32, _pi64, _pf64 = C.POINTER(_i32), C.POINTER(_i64), C.POINTER(_f64)
 
 _SIGS = {
@@ -57,6 +64,8 @@ _SIGS = {
     "fkv_optimize_plan": (C.c_int, [_vp, _i32, _i32, _i32, _i32, _i32, _i32, _i64, _i64, _i32,
                                     _vp, _vp, _vp, _vp, _vp]),
     "fkv_decode_ctas_per_sm": (C.c_int, [_i32]),
+    "fkv_plan_schedule": (C.c_int, [_vp, _vp, _vp, _vp, _i32, _vp, _i32, _i32, _i32,
+                                    _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "fkv_decode": (C.c_int, [_vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _f32, _vp, _vp,
                              _vp, _vp, _i32, _vp, _vp]),
     "fkv_merge_lse": (C.c_int, [_vp, _i32, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp]),

@@ -17,6 +17,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass, field
 
+import os
+
 import numpy as np
 import torch
 
@@ -440,7 +442,65 @@ def plan_work_whole(seg_len, workers: int, sms: int):
     return item_seg, t0, t1, seg_item_ptr, warp_ptr, work_list
 
 
+def _sched_params(device, chunk):
+    """fkv_sched_params of the native planner: the device and the planner's
+    environment knobs, as plan_schedule_py reads them."""
+    import ctypes as C
+    from . import _native
+    try:
+        sms = torch.cuda.get_device_properties(device).multi_processor_count
+    except Exception:  # no device visible (host-side planning / CPU tests)
+        sms = NUM_SMS
+    mode = {"auto": 0, "coop": 1, "wide": 2, "solo": 3}.get(os.environ.get("FKV_K4_SCHEDULE", "auto"), 0)
+    whole = os.environ.get("FKV_K4_WHOLE")
+    prm = _native.SchedParams(
+        sms=sms, ctas_coop=_native.lib.fkv_decode_ctas_per_sm(0),
+        ctas_wide=_native.lib.fkv_decode_ctas_per_sm(FKV_DECODE_WIDE),
+        ctas_solo=_native.lib.fkv_decode_ctas_per_sm(FKV_DECODE_SOLO), mode=mode,
+        whole=-1 if whole is None else (1 if whole == "1" else 0),
+        solo_small=int(os.environ.get("FKV_SOLO_SMALL") == "1"),
+        solo_piece=int(os.environ.get("FKV_SOLO_PIECE", -1)), solo_whole=int(os.environ.get("FKV_SOLO_WHOLE", -1)),
+        piece_cost=int(os.environ.get("FKV_PIECE_COST", PIECE_COST_TILES)),
+        sm_pairing=int(os.environ.get("FKV_SM_PAIRING", "1") == "1"),
+        chunk=-1 if chunk is None else int(chunk),
+        pair_piece=float(os.environ.get("FKV_PAIR_PIECE", PAIR_PIECE_TILES)))
+    return C.byref(prm), sms
+
+
 def plan_schedule(seg_len, seg_row0, seg_qrow, seg_out_row, device=None, chunk: int | None = None):
+    """Pick the K4 schedule for one cache and build its work table: the
+    native planner (csrc/schedule.cpp, fkv_plan_schedule), bit-identical to
+    ``plan_schedule_py`` below (tests/test_schedule_native.py), which
+    FKV_PY_SCHEDULE=1 selects.  Same return value."""
+    if os.environ.get("FKV_PY_SCHEDULE") == "1":
+        return plan_schedule_py(seg_len, seg_row0, seg_qrow, seg_out_row, device, chunk)
+    from . import _native
+    i64 = lambda a: np.ascontiguousarray(a, dtype=np.int64)  # noqa: E731
+    seg_len, seg_row0 = i64(seg_len), i64(seg_row0)
+    seg_qrow, seg_out_row = i64(seg_qrow), i64(seg_out_row)
+    n = len(seg_len)
+    prm, sms = _sched_params(device, chunk)
+    cap_items = max(1, n * MAX_ITEMS_PER_SEGMENT)
+    cap_workers = max(1, 8 * sms)
+    cap_table = cap_workers * MAX_WORK_PER_WORKER * 8
+    out = [np.empty(cap_items, np.int32) for _ in range(3)]
+    sptr = np.empty(n + 1, np.int32)
+    wptr = np.empty(cap_workers + 1, np.int32)
+    wlist = np.empty(cap_items, np.int32)
+    tab = np.empty(cap_table, np.int32)
+    sizes = np.zeros(5, np.int32)
+    p = lambda a: a.ctypes.data  # noqa: E731
+    rc = _native.lib.fkv_plan_schedule(
+        p(seg_len), p(seg_row0), p(seg_qrow), p(seg_out_row), n, prm, cap_items, cap_workers, cap_table,
+        p(out[0]), p(out[1]), p(out[2]), p(sptr), p(wptr), p(wlist), p(tab), p(sizes))
+    if rc < 0:  # the same exception as the Python planner (e.g. too many segments for one launch)
+        raise ValueError(_native.last_error())
+    n_items, busy, rows, K, flags = (int(x) for x in sizes)
+    return (out[0][:n_items], out[1][:n_items], out[2][:n_items], sptr, wptr[:busy + 1], wlist[:n_items],
+            tab[:rows * K * 8].reshape(rows, K, 8), flags)
+
+
+def plan_schedule_py(seg_len, seg_row0, seg_qrow, seg_out_row, device=None, chunk: int | None = None):
     """Pick the K4 schedule for one cache and build its work table.
 
     * default: the CTA-cooperative schedule, stream cut to equal *estimated
@@ -631,22 +691,33 @@ class LayerCache:
         seg_cap = seg_len if seg_cap is None else np.asarray(seg_cap, dtype=np.int64)
         append_src = np.full(len(seg_len), -1) if append_src is None else np.asarray(append_src)
 
-        def i32(a):
-            return torch.as_tensor(np.ascontiguousarray(a, dtype=np.int32), device=dev)
+        # every int32 table in one host buffer and one host-to-device copy
+        # (16-byte aligned pieces: the work table is read with int4 loads);
+        # fifteen small copies cost more than the planning itself
+        parts = [np.ascontiguousarray(a, dtype=np.int32).reshape(-1) for a in (
+            seg_len, seg_qrow, seg_out_row, item_seg, t0, t1, ptr, np.arange(ptr[-1]), wptr, wlist, tab,
+            seg_cap, append_src, last_piece, np.zeros(max(len(item_seg), 1)), np.zeros(1),
+            np.ascontiguousarray(seg_row0, dtype=np.int64).view(np.int32))]
+        offs = np.cumsum([0] + [-(-len(a) // 4) * 4 for a in parts])
+        host_buf = np.zeros(int(offs[-1]), dtype=np.int32)
+        for a, o in zip(parts, offs[:-1]):
+            host_buf[o:o + len(a)] = a
+        buf = torch.from_numpy(host_buf).to(dev)
+        view = [buf[int(o):int(o) + len(a)] for a, o in zip(parts, offs[:-1])]
+        (seg_len_t, qrow_t, orow_t, iseg_t, t0_t, t1_t, ptr_t, src_t, wptr_t, wlist_t, tab_t, cap_t, asrc_t,
+         lp_t, ctr_t, ovf_t, row0_t) = view
 
         return LayerCache(
-            k=k, v=v, group=int(group), seg_row0=torch.as_tensor(seg_row0, device=dev),
-            seg_len=i32(seg_len), seg_qrow=i32(seg_qrow), seg_out_row=i32(seg_out_row),
-            item_seg=i32(item_seg), item_t0=i32(t0), item_t1=i32(t1), grp_ptr=i32(ptr),
-            src_idx=i32(np.arange(ptr[-1])),
-            warp_ptr=i32(wptr), work_list=i32(wlist), work=i32(tab),
-            counters=torch.zeros(max(len(item_seg), 1), dtype=torch.int32, device=dev),
+            k=k, v=v, group=int(group), seg_row0=row0_t.view(torch.int64),
+            seg_len=seg_len_t, seg_qrow=qrow_t, seg_out_row=orow_t,
+            item_seg=iseg_t, item_t0=t0_t, item_t1=t1_t, grp_ptr=ptr_t, src_idx=src_t,
+            warp_ptr=wptr_t, work_list=wlist_t, work=tab_t.view(tab.shape),
+            counters=ctr_t,
             host={"seg_len": seg_len, "seg_row0": seg_row0, "chunk": chunk, "n_workers": len(wptr) - 1,
                   "seg_qrow": np.asarray(seg_qrow), "seg_out_row": np.asarray(seg_out_row),
                   "flags": flags, "seg_cap": seg_cap,
-                  "seg_cap_t": i32(seg_cap), "append_src_t": i32(append_src),
-                  "last_piece_t": i32(last_piece),
-                  "overflow_t": torch.zeros(1, dtype=torch.int32, device=dev)},
+                  "seg_cap_t": cap_t, "append_src_t": asrc_t, "last_piece_t": lp_t,
+                  "overflow_t": ovf_t, "table_buf": buf},
         )
 
     def sync_lengths(self) -> np.ndarray:

@@ -1,0 +1,85 @@
+"""The native K4 schedule planner (csrc/schedule.cpp, fkv_plan_schedule)
+against its Python form (cache.plan_schedule_py): every output -- pieces,
+pointers, work list, the fkv_work_t table and the chosen CTA shape -- equal,
+on random caches across the size range (a TP=8 rank's few heads to a TP=1
+batch-64 layer), skewed and empty segments, every schedule override and the
+chunked path.  CPU only."""
+
+import numpy as np
+import pytest
+
+from paper_2502_15804_b200 import cache as C
+
+
+def _segments(rng, n, mean):
+    kind = rng.integers(3)
+    if kind == 0:
+        lens = rng.integers(0, 2 * mean + 1, n)
+    elif kind == 1:  # dirichlet-skewed, like Ada budgets
+        lens = np.round(rng.dirichlet(np.full(n, 2.0)) * mean * n).astype(np.int64)
+    else:  # a few very long segments among short ones
+        lens = rng.integers(0, mean // 4 + 1, n)
+        lens[rng.integers(0, n, max(1, n // 10))] = rng.integers(mean, 8 * mean + 1)
+    return lens.astype(np.int64)
+
+
+def _check(lens, chunk=None):
+    row0, _ = C.segment_offsets(lens)
+    qrow = np.arange(len(lens), dtype=np.int64) * 8
+    orow = qrow[::-1].copy()
+    got = C.plan_schedule(lens, row0, qrow, orow, None, chunk)
+    want = C.plan_schedule_py(lens, row0, qrow, orow, None, chunk)
+    names = ("item_seg", "t0", "t1", "seg_item_ptr", "warp_ptr", "work_list", "table")
+    for nm, a, b in zip(names, got[:7], want[:7]):
+        np.testing.assert_array_equal(np.asarray(a), np.asarray(b), err_msg=nm)
+    assert got[7] == want[7], "flags"
+    return got[7]
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_native_matches_python_random(seed):
+    rng = np.random.default_rng(seed)
+    seen = set()
+    for n, mean in ((8, 1024), (16, 300), (64, 1024), (130, 700), (512, 1024), (1100, 120), (2048, 40),
+                    (5, 3), (300, 2000)):
+        seen.add(_check(_segments(rng, n, mean)))
+    assert len(seen) >= 2  # several CTA shapes exercised
+
+
+@pytest.mark.parametrize("env", [{"FKV_K4_SCHEDULE": "coop"}, {"FKV_K4_SCHEDULE": "wide"},
+                                 {"FKV_K4_SCHEDULE": "solo"}, {"FKV_K4_WHOLE": "1"}, {"FKV_K4_WHOLE": "0"},
+                                 {"FKV_SOLO_SMALL": "1"}, {"FKV_PIECE_COST": "0"}, {"FKV_SM_PAIRING": "0"},
+                                 {"FKV_PAIR_PIECE": "7.5"}, {"FKV_SOLO_PIECE": "6", "FKV_SOLO_WHOLE": "9"}])
+def test_native_matches_python_overrides(monkeypatch, env):
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    rng = np.random.default_rng(99)
+    for n, mean in ((8, 1024), (64, 500), (512, 1024), (1500, 60), (200, 5)):
+        _check(_segments(rng, n, mean))
+
+
+@pytest.mark.parametrize("chunk", [16, 100, 512, 4096])
+def test_native_matches_python_chunked(chunk):
+    rng = np.random.default_rng(chunk)
+    for n, mean in ((8, 1024), (64, 3000), (300, 200)):
+        _check(_segments(rng, n, mean), chunk)
+
+
+def test_native_edge_cases():
+    _check(np.zeros(0, dtype=np.int64))
+    _check(np.zeros(7, dtype=np.int64))
+    _check(np.array([1], dtype=np.int64))
+    _check(np.array([100000], dtype=np.int64))  # one very long segment: many pieces
+    _check(np.full(296 * 32, 1, dtype=np.int64))  # at the piece cap of a launch
+
+
+def test_native_errors_match():
+    # more segments than one launch can hold: both planners refuse
+    lens = np.ones(148 * 8 * 32 + 5000, dtype=np.int64)
+    row0, _ = C.segment_offsets(lens)
+    q = np.zeros(len(lens), dtype=np.int64)
+    with pytest.raises(ValueError):
+        C.plan_schedule_py(lens, row0, q, q)
+    from paper_2502_15804_b200.errors import NativeError
+    with pytest.raises((ValueError, NativeError)):
+        C.plan_schedule(lens, row0, q, q)
