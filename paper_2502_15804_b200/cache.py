@@ -442,21 +442,37 @@ def plan_work_whole(seg_len, workers: int, sms: int):
     return item_seg, t0, t1, seg_item_ptr, warp_ptr, work_list
 
 
+_DEVICE_SHAPES: dict = {}  # device index -> (SMs, CTAs per SM of coop / wide / solo)
+_PLAN_SCRATCH: dict = {}   # output buffers of fkv_plan_schedule, reused across calls
+
+
+def _device_shapes(device):
+    from . import _native
+    try:
+        idx = torch.device(device).index if device is not None else torch.cuda.current_device()
+        idx = torch.cuda.current_device() if idx is None else idx
+    except Exception:  # no device visible (host-side planning / CPU tests)
+        idx = -1
+    if idx not in _DEVICE_SHAPES:
+        try:
+            sms = torch.cuda.get_device_properties(idx).multi_processor_count
+        except Exception:
+            sms = NUM_SMS
+        _DEVICE_SHAPES[idx] = (sms, *(int(_native.lib.fkv_decode_ctas_per_sm(f))
+                                     for f in (0, FKV_DECODE_WIDE, FKV_DECODE_SOLO)))
+    return _DEVICE_SHAPES[idx]
+
+
 def _sched_params(device, chunk):
     """fkv_sched_params of the native planner: the device and the planner's
     environment knobs, as plan_schedule_py reads them."""
     import ctypes as C
     from . import _native
-    try:
-        sms = torch.cuda.get_device_properties(device).multi_processor_count
-    except Exception:  # no device visible (host-side planning / CPU tests)
-        sms = NUM_SMS
+    sms, c_coop, c_wide, c_solo = _device_shapes(device)
     mode = {"auto": 0, "coop": 1, "wide": 2, "solo": 3}.get(os.environ.get("FKV_K4_SCHEDULE", "auto"), 0)
     whole = os.environ.get("FKV_K4_WHOLE")
     prm = _native.SchedParams(
-        sms=sms, ctas_coop=_native.lib.fkv_decode_ctas_per_sm(0),
-        ctas_wide=_native.lib.fkv_decode_ctas_per_sm(FKV_DECODE_WIDE),
-        ctas_solo=_native.lib.fkv_decode_ctas_per_sm(FKV_DECODE_SOLO), mode=mode,
+        sms=sms, ctas_coop=c_coop, ctas_wide=c_wide, ctas_solo=c_solo, mode=mode,
         whole=-1 if whole is None else (1 if whole == "1" else 0),
         solo_small=int(os.environ.get("FKV_SOLO_SMALL") == "1"),
         solo_piece=int(os.environ.get("FKV_SOLO_PIECE", -1)), solo_whole=int(os.environ.get("FKV_SOLO_WHOLE", -1)),
@@ -483,11 +499,14 @@ def plan_schedule(seg_len, seg_row0, seg_qrow, seg_out_row, device=None, chunk: 
     cap_items = max(1, n * MAX_ITEMS_PER_SEGMENT)
     cap_workers = max(1, 8 * sms)
     cap_table = cap_workers * MAX_WORK_PER_WORKER * 8
-    out = [np.empty(cap_items, np.int32) for _ in range(3)]
+    sc = _PLAN_SCRATCH  # single-threaded host planning: one scratch per process
+    if sc.get("items", 0) < cap_items or sc.get("workers", 0) < cap_workers:
+        sc.update(items=cap_items, workers=cap_workers,
+                  out=[np.empty(cap_items, np.int32) for _ in range(4)],
+                  wptr=np.empty(cap_workers + 1, np.int32), tab=np.empty(cap_table, np.int32))
+    out, wptr, tab = sc["out"], sc["wptr"], sc["tab"]
+    wlist = out[3]
     sptr = np.empty(n + 1, np.int32)
-    wptr = np.empty(cap_workers + 1, np.int32)
-    wlist = np.empty(cap_items, np.int32)
-    tab = np.empty(cap_table, np.int32)
     sizes = np.zeros(5, np.int32)
     p = lambda a: a.ctypes.data  # noqa: E731
     rc = _native.lib.fkv_plan_schedule(
@@ -496,8 +515,8 @@ def plan_schedule(seg_len, seg_row0, seg_qrow, seg_out_row, device=None, chunk: 
     if rc < 0:  # the same exception as the Python planner (e.g. too many segments for one launch)
         raise ValueError(_native.last_error())
     n_items, busy, rows, K, flags = (int(x) for x in sizes)
-    return (out[0][:n_items], out[1][:n_items], out[2][:n_items], sptr, wptr[:busy + 1], wlist[:n_items],
-            tab[:rows * K * 8].reshape(rows, K, 8), flags)
+    return (out[0][:n_items].copy(), out[1][:n_items].copy(), out[2][:n_items].copy(), sptr,
+            wptr[:busy + 1].copy(), wlist[:n_items].copy(), tab[:rows * K * 8].reshape(rows, K, 8).copy(), flags)
 
 
 def plan_schedule_py(seg_len, seg_row0, seg_qrow, seg_out_row, device=None, chunk: int | None = None):

@@ -16,7 +16,6 @@
 #include <cmath>
 #include <cstdint>
 #include <numeric>
-#include <queue>
 #include <string>
 #include <utility>
 #include <vector>
@@ -65,6 +64,30 @@ std::vector<i64> stable_order(i64 n, Key&& less) {
   std::stable_sort(o.begin(), o.end(), less);
   return o;
 }
+
+// heapq of (load, worker) tuples: the least load, then the lowest worker id.
+// Packed into one int64 key (load << 16 | worker; workers < 65536) so the
+// heap compares one integer.
+class MinHeap {
+ public:
+  explicit MinHeap(i64 workers) {
+    h_.reserve(workers);
+    for (i64 w = 0; w < workers; ++w) h_.push_back(w);  // load 0: already a heap in id order
+  }
+  std::pair<i64, i64> pop() {
+    std::pop_heap(h_.begin(), h_.end(), std::greater<i64>());
+    const i64 k = h_.back();
+    h_.pop_back();
+    return {k >> 16, k & 0xffff};
+  }
+  void push(i64 load, i64 w) {
+    h_.push_back((load << 16) | w);
+    std::push_heap(h_.begin(), h_.end(), std::greater<i64>());
+  }
+
+ private:
+  std::vector<i64> h_;
+};
 
 // ---- cut of the concatenated tile stream (cache.py _cut_stream / _cut_stream_cost)
 struct Cut {
@@ -323,16 +346,13 @@ Plan plan_work_solo(const V& seg_len, i64 n_workers, i64 piece_tiles, i64 whole_
     for (i64 i = 0; i < n_items; ++i) size[i] = std::max<i64>(t1s[i] - t0s[i], 0);
     // np.lexsort((arange, -size)): size descending, index ascending
     auto order = stable_order(n_items, [&](i64 a, i64 b) { return size[a] > size[b]; });
-    using E = std::pair<i64, i64>;  // (load, worker): heapq order
-    std::priority_queue<E, std::vector<E>, std::greater<E>> heap;
-    for (i64 w = 0; w < W; ++w) heap.push({0, w});
+    MinHeap heap(W);
     std::vector<i64> cnt(W, 0);
     for (i64 i : order) {
-      E top = heap.top();
-      heap.pop();
-      owner[i] = top.second;
-      cnt[top.second] += 1;
-      heap.push({top.first + size[i] + 1, top.second});
+      const auto [load, w] = heap.pop();
+      owner[i] = w;
+      cnt[w] += 1;
+      heap.push(load + size[i] + 1, w);
     }
     if (*std::max_element(cnt.begin(), cnt.end()) > kMaxWork)
       throw PlanError{"too many pieces for the per-warp schedule"};
@@ -355,16 +375,13 @@ V whole_owners(const V& seg_tiles, i64 workers, i64 sms, double pair_piece) {
     return owner;
   }
   auto order = stable_order(n, [&](i64 a, i64 b) { return seg_tiles[a] > seg_tiles[b]; });
-  using E = std::pair<i64, i64>;
-  std::priority_queue<E, std::vector<E>, std::greater<E>> heap;
-  for (i64 w = 0; w < workers; ++w) heap.push({0, w});
+  MinHeap heap(workers);
   std::vector<char> used(workers, 0);
   for (i64 s : order) {
-    E top = heap.top();
-    heap.pop();
-    owner[s] = top.second;
-    used[top.second] = 1;
-    heap.push({top.first + seg_tiles[s] + (top.first ? kPairPieceTilesWhole : 0), top.second});
+    const auto [load, w] = heap.pop();
+    owner[s] = w;
+    used[w] = 1;
+    heap.push(load + seg_tiles[s] + (load ? kPairPieceTilesWhole : 0), w);
   }
   std::vector<i64> rank(workers, -1);
   i64 r = 0;
