@@ -1031,6 +1031,7 @@ def prefill_compress(peaks):
         stacked()
         t_pl = min(timed(per_layer, 1) for _ in range(3)) / Ls
         t_st = min(timed(stacked, 1) for _ in range(3)) / Ls
+        hbm_bps = float(peaks.get("hbm_gbs", 6650.0)) * 1e9
         flops = 2 * 2.0 * bt * hq * w * T * HEAD_DIM  # two passes of Q_win.K^T
         exps = 2.0 * bt * hq * w * T  # one ex2 per score per pass (MUFU)
         kbytes = bt * hkv * T * HEAD_DIM * 2
@@ -1051,7 +1052,14 @@ def prefill_compress(peaks):
             # two exponentials per (query row, key), at the measured ex2 rate
             "mufu_bound_us": exps / mufu_rate * 1e6,
             "score_mufu_frac": exps / mufu_rate / (dev_us["score_us"] * 1e-6),
+            # the two passes in sequence (pass 2 needs every chunk's pass-1
+            # statistics): pass 1 streams K from HBM and exponentiates, pass 2
+            # exponentiates again over K re-read from L2 when it fits (the one-
+            # item-per-CTA schedule keeps it there), else from HBM
+            "two_pass_bound_us": (max(kbytes / hbm_bps, exps / 2 / mufu_rate)
+                                  + max(kbytes / hbm_bps if kbytes > 96e6 else 0.0, exps / 2 / mufu_rate)) * 1e6,
         }
+        rows[name]["score_two_pass_frac"] = rows[name]["two_pass_bound_us"] / dev_us["score_us"]
     return rows
 
 
