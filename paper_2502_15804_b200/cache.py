@@ -443,7 +443,7 @@ def plan_work_whole(seg_len, workers: int, sms: int):
 
 
 _DEVICE_SHAPES: dict = {}  # device index -> (SMs, CTAs per SM of coop / wide / solo)
-_PLAN_SCRATCH: dict = {}   # output buffers of fkv_plan_schedule, reused across calls
+_PLAN_SCRATCH = __import__("threading").local()  # output buffers of fkv_plan_schedule, per thread
 
 
 def _device_shapes(device):
@@ -499,7 +499,7 @@ def plan_schedule(seg_len, seg_row0, seg_qrow, seg_out_row, device=None, chunk: 
     cap_items = max(1, n * MAX_ITEMS_PER_SEGMENT)
     cap_workers = max(1, 8 * sms)
     cap_table = cap_workers * MAX_WORK_PER_WORKER * 8
-    sc = _PLAN_SCRATCH  # single-threaded host planning: one scratch per process
+    sc = _PLAN_SCRATCH.__dict__  # reused across calls, one set per thread
     if sc.get("items", 0) < cap_items or sc.get("workers", 0) < cap_workers:
         sc.update(items=cap_items, workers=cap_workers,
                   out=[np.empty(cap_items, np.int32) for _ in range(4)],

@@ -538,8 +538,9 @@ extern "C" int fkv_plan_schedule(const int64_t* seg_len, const int64_t* seg_row0
   using namespace fkv;
   if (n_seg < 0 || !prm || !out_sizes || (n_seg && (!seg_len || !seg_row0 || !seg_qrow || !seg_out_row)))
     return set_error(FKV_ERR_INVALID, "fkv_plan_schedule: bad arguments");
-  if (prm->sms < 1 || prm->ctas_coop < 1 || prm->ctas_wide < 1 || prm->ctas_solo < 1)
-    return set_error(FKV_ERR_INVALID, "fkv_plan_schedule: bad device parameters");
+  if (prm->sms < 1 || prm->ctas_coop < 1 || prm->ctas_wide < 1 || prm->ctas_solo < 1 ||
+      static_cast<int64_t>(prm->sms) * 4 * std::max({prm->ctas_coop, prm->ctas_wide, prm->ctas_solo}) >= 65536)
+    return set_error(FKV_ERR_INVALID, "fkv_plan_schedule: bad device parameters");  // MinHeap packs worker ids in 16 bits
   V len(seg_len, seg_len + n_seg);
   for (i64 x : len)
     if (x < 0) return set_error(FKV_ERR_INVALID, "fkv_plan_schedule: negative segment length");
