@@ -182,6 +182,31 @@ def test_compress_then_decode_end_to_end(cuda_device):
     torch.testing.assert_close(lse.cpu().double(), torch.from_numpy(lse_ref), rtol=1e-4, atol=1e-5)
 
 
+@pytest.mark.parametrize("seed", range(8))
+def test_score_select_random_shapes(cuda_device, seed):
+    """Random shapes through the persistent fused launch (one item per CTA or
+    several, G*w 128 / 256, T not a multiple of the tile, budgets near the
+    floor and near T): budgets and indices bit-exact against the oracle fed
+    the kernel's own scores, scores within tolerance on a sampled head."""
+    from paper_2502_15804_b200 import ops
+    rng = np.random.default_rng(1000 + seed)
+    hq = int(rng.choice([32, 64]))
+    bt = int(rng.choice([1, 2, 5, 19, 23]))
+    T = int(rng.integers(200, 3000))
+    budget = int(rng.integers(33, min(T - 32, 1024) + 1))
+    q, k, _, qn, kn, _ = _inputs(bt, hq, 8, T, 32, 70 + seed, cuda_device, temp=float(rng.uniform(0.5, 3)))
+    sc, hb, off, idx = ops.score_select(q, k, budget, 32)
+    torch.cuda.synchronize()
+    s64 = sc.cpu().double().numpy()
+    heads = [(bt - 1, int(rng.integers(8)))]
+    check_scores(np.stack([s64[b, h] for b, h in heads]), sampled_head_scores(qn, kn, heads))
+    ref_b = okv.ada_budgets(s64, budget, 32, 0.2)
+    np.testing.assert_array_equal(hb.cpu().numpy(), ref_b)
+    ref_off, ref_idx = okv.topk_select(s64, ref_b, 32)
+    np.testing.assert_array_equal(off.cpu().numpy(), ref_off)
+    np.testing.assert_array_equal(idx.cpu().numpy(), ref_idx)
+
+
 def test_compress_stack_matches_per_layer(cuda_device):
     """compress_stack (all layers' fused launches queued, one host round trip,
     then every compaction) builds the same caches as compress_layer per layer:
