@@ -355,9 +355,11 @@ def compact(k: torch.Tensor, v: torch.Tensor, offsets: torch.Tensor, idx: torch.
     seg_lo = np.asarray(seg_lo, dtype=np.int64)
     seg_hi = np.asarray(seg_hi, dtype=np.int64)
     cache = LayerCache.allocate(seg_hi - seg_lo, seg_qrow, seg_out_row, group, k.device, chunk=chunk)
-    dev = k.device
-    i32 = lambda a: torch.as_tensor(np.ascontiguousarray(a, dtype=np.int32), device=dev)  # noqa: E731
-    tabs = (i32(seg_bh), i32(seg_lo), i32(seg_hi))
+    n = len(seg_lo)
+    host = np.empty(3 * n, dtype=np.int32)  # the three segment tables in one host-to-device copy
+    host[:n], host[n:2 * n], host[2 * n:] = seg_bh, seg_lo, seg_hi
+    dev_tabs = torch.from_numpy(host).to(k.device)
+    tabs = (dev_tabs[:n], dev_tabs[n:2 * n], dev_tabs[2 * n:])
     compact_into(cache, k, v, offsets, idx, *tabs,
                  int((seg_hi - seg_lo).max()) if len(seg_lo) else 0)
     cache.host["compact_args"] = tabs  # keep alive until the stream consumes them
