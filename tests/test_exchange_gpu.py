@@ -11,12 +11,12 @@ import torch
 pytestmark = pytest.mark.gpu
 
 
-def _setup(tp, mode, dev, L=3, bt=4, B=256):
+def _setup(tp, mode, dev, L=3, bt=4, B=256, G=8):
     import paper_2502_15804_b200 as fk
     from paper_2502_15804_b200.cache import LayerCache
     from paper_2502_15804_b200.decoder import rank_caches
     from paper_2502_15804_b200.sharding import budgets_profile, plan_layouts, synthetic_budgets
-    G, hkv = 8, 8
+    hkv = 8
     hq = G * hkv
     budgets = synthetic_budgets(L, bt, hkv, B, seed=tp)
     prof = budgets_profile(budgets, B)
@@ -33,11 +33,13 @@ def _setup(tp, mode, dev, L=3, bt=4, B=256):
     return base, per_rank, finals, bt, hq, G
 
 
-@pytest.mark.parametrize("tp,mode", [(2, "sha"), (2, "dp"), (4, "dp"), (8, "free")])
-def test_loopback_exchange_matches_single_gpu(cuda_device, tp, mode):
+@pytest.mark.parametrize("tp,mode,G", [(2, "sha", 8), (2, "dp", 8), (4, "dp", 8), (8, "free", 8), (4, "dp", 4),
+                                        (8, "sha", 4)])
+def test_loopback_exchange_matches_single_gpu(cuda_device, tp, mode, G):
+    """G = 8: Llama-3.3-70B heads; G = 4: Llama-3.1-8B heads."""
     from paper_2502_15804_b200 import ops
     from paper_2502_15804_b200.exchange import P2PGroup, exchange_buffer
-    base, per_rank, finals, bt, hq, G = _setup(tp, mode, cuda_device)
+    base, per_rank, finals, bt, hq, G = _setup(tp, mode, cuda_device, G=G)
     L = len(base)
     slots = max(f.slots for f in finals)
     grp = P2PGroup.loopback(tp, slots, G)
