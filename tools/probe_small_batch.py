@@ -37,7 +37,8 @@ for bt in [int(x) for x in sys.argv[1:]] or [1, 4, 16]:
     line = f"batch {bt:3d}:"
     for name, env in (("auto", {}), ("coop", {"FKV_K4_SCHEDULE": "coop"}), ("wide", {"FKV_K4_SCHEDULE": "wide"}),
                       ("solo", {"FKV_K4_SCHEDULE": "solo"}), ("wide-split", {"FKV_K4_SCHEDULE": "wide", "FKV_K4_WHOLE": "0"}),
-                      ("wide-whole", {"FKV_K4_SCHEDULE": "wide", "FKV_K4_WHOLE": "1"})):
+                      ("wide-whole", {"FKV_K4_SCHEDULE": "wide", "FKV_K4_WHOLE": "1"}),
+                      ("coop-whole", {"FKV_K4_SCHEDULE": "coop", "FKV_K4_WHOLE": "1"})):
         us, fl, w = per_layer(bt, lambda l: budgets[l].reshape(-1), env)
         line += f"  {name} {us:5.2f}us(f{fl},{w}w)"
     print(line, flush=True)
