@@ -13,7 +13,8 @@ from paper_2502_15804_b200.cache import LayerCache
 from paper_2502_15804_b200.sharding import synthetic_budgets
 
 dev = torch.device('cuda:0')
-L, HQ, G, B = 32, 32, 4, 256
+L, HQ, G = 32, 32, 4
+B = int(os.environ.get("PROBE_B", 256))
 
 
 def per_layer(bt, lens_fn, env):
