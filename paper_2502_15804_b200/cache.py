@@ -378,11 +378,6 @@ WHOLE_MODEL = {"wide": (5.6, 3.3, 0.104), "coop": (7.6, 2.6, 0.285)}
 SPLIT_US_PER_MB = 0.165
 WHOLE_MARGIN_US = 0.5   # near a tie the split cut stays (TP=8 uniform TP, B=512: 8.7 vs 9.5 us)
 WHOLE_US_PER_MB = 0.161  # the whole schedule is HBM-bound once every SM is busy (TP=1: 6.2 TB/s)
-# with few busy CTAs (small-batch decode: a handful of segments) each CTA
-# streams alone and its tiles cost less: Llama-3.1-8B shape at batch 1, 8
-# whole segments on 8 CTAs 5.0 us vs the split cut 5.4 (tools/probe_small_batch.py)
-WHOLE_FEW_CTAS = 32
-WHOLE_FEW_PER_TILE_US = 0.045
 # at least two segments per CTA on average (a full grid of 4-warp CTAs, e.g.
 # the Llama-3.1-8B shape at batch >= 128): every SM streams, the per-tile
 # cost is the HBM share -- batch 128: whole 24.1 vs split 28.1 us per layer
@@ -426,9 +421,7 @@ def whole_segments_win(seg_tiles, workers: int, wide: bool, sms: int = NUM_SMS) 
     if not n or n > workers * MAX_WORK_PER_WORKER:
         return False
     s0, w0, per_tile = WHOLE_MODEL["wide" if wide else "coop"]
-    if n <= WHOLE_FEW_CTAS:
-        per_tile = WHOLE_FEW_PER_TILE_US
-    elif not wide and n >= 2 * workers:
+    if not wide and n >= 2 * workers:
         per_tile = WHOLE_FULL_PER_TILE_US
     mb = float(seg_tiles.sum()) * TILE * HEAD_DIM * 4 / 1e6
     crit = float(_whole_cta_tiles(seg_tiles, _whole_owners(seg_tiles, workers, sms)).max())

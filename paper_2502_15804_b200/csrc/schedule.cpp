@@ -40,8 +40,6 @@ constexpr i64 kWideMaxSegments = 128;
 constexpr i64 kWideMinMeanTiles = 6;
 constexpr i64 kPairPieceTilesWhole = 12;  // PAIR_PIECE_TILES in _whole_owners / _whole_cta_tiles
 constexpr double kSplitUsPerMb = 0.165, kWholeMarginUs = 0.5, kWholeUsPerMb = 0.161;
-constexpr i64 kWholeFewCtas = 32;             // cache.py WHOLE_FEW_CTAS
-constexpr double kWholeFewPerTileUs = 0.045;  // cache.py WHOLE_FEW_PER_TILE_US
 constexpr double kWholeFullPerTileUs = 0.20;  // cache.py WHOLE_FULL_PER_TILE_US
 
 struct PlanError {
@@ -401,9 +399,7 @@ bool whole_segments_win(const V& seg_tiles, i64 workers, bool wide, i64 sms, dou
   const i64 n = static_cast<i64>(seg_tiles.size());
   if (!n || n > workers * kMaxWork) return false;
   const double s0 = wide ? 5.6 : 7.6, w0 = wide ? 3.3 : 2.6;
-  const double per_tile = n <= kWholeFewCtas ? kWholeFewPerTileUs
-                          : (!wide && n >= 2 * workers) ? kWholeFullPerTileUs
-                          : (wide ? 0.104 : 0.285);
+  const double per_tile = (!wide && n >= 2 * workers) ? kWholeFullPerTileUs : (wide ? 0.104 : 0.285);
   i64 tsum = 0;
   for (i64 t : seg_tiles) tsum += t;
   const double mb = static_cast<double>(tsum) * kTile * FKV_HEAD_DIM * 4 / 1e6;
