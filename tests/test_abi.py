@@ -54,3 +54,24 @@ def test_ops_refuse_cpu_tensors():
     from paper_2502_15804_b200.errors import NativeError
     with pytest.raises(NativeError):
         ops.budgets(torch.zeros(1, 8, 100), 64, 32)
+
+
+def _prototypes():
+    """name -> parameter count of every function fairkv.h declares."""
+    text = (ROOT / "include" / "fairkv.h").read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    out = {}
+    for m in re.finditer(r"^(?:int|int64_t|const char\*)\s+(fkv_\w+)\(([^;]*?)\);", text, re.M | re.S):
+        params = m.group(2).strip()
+        out[m.group(1)] = 0 if params in ("", "void") else params.count(",") + 1
+    return out
+
+
+def test_ctypes_signatures_match_the_header():
+    """Every function the Python binding declares has the header's argument
+    count (a drifted prototype would pass garbage through ctypes)."""
+    from paper_2502_15804_b200 import _native
+    protos = _prototypes()
+    for name, (_res, args) in _native._SIGS.items():
+        assert name in protos, f"{name} bound in _native.py but not declared in fairkv.h"
+        assert len(args) == protos[name], f"{name}: {len(args)} ctypes args vs {protos[name]} in fairkv.h"
