@@ -167,6 +167,43 @@ int fkv_plan_schedule(const int64_t* seg_len, const int64_t* seg_row0, const int
                       int32_t* item_t0, int32_t* item_t1, int32_t* seg_item_ptr, int32_t* warp_ptr,
                       int32_t* work_list, int32_t* table, int32_t* out_sizes);
 
+/* A layer cache's whole device table set, planned (as fkv_plan_schedule)
+ * and packed into one int32 buffer for one host-to-device copy.  Part i
+ * occupies words [part_off[i], part_off[i+1]) (16-byte aligned; the part's
+ * own length is below that bound):
+ *   SEG_LEN, SEG_QROW, SEG_OUT_ROW [n_seg]; ITEM_SEG, ITEM_T0, ITEM_T1 [n_items];
+ *   SEG_ITEM_PTR [n_seg + 1]; SRC_IDX [n_items] (0..n_items-1, K5's source rows);
+ *   WARP_PTR [busy + 1]; WORK_LIST [n_items]; WORK [rows * K * 8] (fkv_work_t);
+ *   SEG_CAP [n_seg] (null seg_cap: seg_len); APPEND_SRC [n_seg] (null: -1);
+ *   LAST_PIECE [n_seg] (flat work index of each segment's last piece);
+ *   COUNTERS [max(n_items, 1)] and OVERFLOW [1] (zero);
+ *   SEG_ROW0 [n_seg] as int64 (2 words each).
+ * part_off has FKV_CT_PARTS + 1 entries, the last = words used; a buffer
+ * shorter than that: FKV_ERR_INVALID with part_off filled.  out_sizes as
+ * fkv_plan_schedule. */
+#define FKV_CT_SEG_LEN 0
+#define FKV_CT_SEG_QROW 1
+#define FKV_CT_SEG_OUT_ROW 2
+#define FKV_CT_ITEM_SEG 3
+#define FKV_CT_ITEM_T0 4
+#define FKV_CT_ITEM_T1 5
+#define FKV_CT_SEG_ITEM_PTR 6
+#define FKV_CT_SRC_IDX 7
+#define FKV_CT_WARP_PTR 8
+#define FKV_CT_WORK_LIST 9
+#define FKV_CT_WORK 10
+#define FKV_CT_SEG_CAP 11
+#define FKV_CT_APPEND_SRC 12
+#define FKV_CT_LAST_PIECE 13
+#define FKV_CT_COUNTERS 14
+#define FKV_CT_OVERFLOW 15
+#define FKV_CT_SEG_ROW0 16
+#define FKV_CT_PARTS 17
+int fkv_cache_tables(const int64_t* seg_len, const int64_t* seg_row0, const int64_t* seg_qrow,
+                     const int64_t* seg_out_row, const int64_t* seg_cap, const int64_t* append_src,
+                     int32_t n_seg, const fkv_sched_params* prm, int32_t* buf, int64_t buf_words,
+                     int64_t* part_off, int32_t* out_sizes);
+
 /* Exchange records (the per-layer all-gather payload; "XREC"): a block of
  * `slots` rows of `group` heads =
  *     bf16 o[slots * group][128]   (256 bytes per head row)

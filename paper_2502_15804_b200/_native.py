@@ -66,6 +66,7 @@ _SIGS = {
     "fkv_decode_ctas_per_sm": (C.c_int, [_i32]),
     "fkv_plan_schedule": (C.c_int, [_vp, _vp, _vp, _vp, _i32, _vp, _i32, _i32, _i32,
                                     _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "fkv_cache_tables": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _i64, _vp, _vp]),
     "fkv_decode": (C.c_int, [_vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _f32, _vp, _vp,
                              _vp, _vp, _i32, _vp, _vp]),
     "fkv_merge_lse": (C.c_int, [_vp, _i32, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp]),

@@ -469,24 +469,39 @@ def _device_shapes(device):
     return _DEVICE_SHAPES[idx]
 
 
+_SCHED_ENV = ("FKV_K4_SCHEDULE", "FKV_K4_WHOLE", "FKV_SOLO_SMALL", "FKV_SOLO_PIECE", "FKV_SOLO_WHOLE",
+              "FKV_PIECE_COST", "FKV_SM_PAIRING", "FKV_PAIR_PIECE")
+_SCHED_PARAMS: dict = {}  # (device, chunk, planner environment) -> (fkv_sched_params, SMs)
+
+
 def _sched_params(device, chunk):
     """fkv_sched_params of the native planner: the device and the planner's
-    environment knobs, as plan_schedule_py reads them."""
+    environment knobs, as plan_schedule_py reads them (cached per device,
+    chunk and environment: building it costs more than planning a small
+    cache)."""
     import ctypes as C
     from . import _native
+    env = os.environ
+    key = (str(device), chunk, tuple(env.get(k) for k in _SCHED_ENV))
+    hit = _SCHED_PARAMS.get(key)
+    if hit is not None:
+        return hit
     sms, c_coop, c_wide, c_solo = _device_shapes(device)
-    mode = {"auto": 0, "coop": 1, "wide": 2, "solo": 3}.get(os.environ.get("FKV_K4_SCHEDULE", "auto"), 0)
-    whole = os.environ.get("FKV_K4_WHOLE")
+    mode = {"auto": 0, "coop": 1, "wide": 2, "solo": 3}.get(env.get("FKV_K4_SCHEDULE", "auto"), 0)
+    whole = env.get("FKV_K4_WHOLE")
     prm = _native.SchedParams(
         sms=sms, ctas_coop=c_coop, ctas_wide=c_wide, ctas_solo=c_solo, mode=mode,
         whole=-1 if whole is None else (1 if whole == "1" else 0),
-        solo_small=int(os.environ.get("FKV_SOLO_SMALL") == "1"),
-        solo_piece=int(os.environ.get("FKV_SOLO_PIECE", -1)), solo_whole=int(os.environ.get("FKV_SOLO_WHOLE", -1)),
-        piece_cost=int(os.environ.get("FKV_PIECE_COST", PIECE_COST_TILES)),
-        sm_pairing=int(os.environ.get("FKV_SM_PAIRING", "1") == "1"),
+        solo_small=int(env.get("FKV_SOLO_SMALL") == "1"),
+        solo_piece=int(env.get("FKV_SOLO_PIECE", -1)), solo_whole=int(env.get("FKV_SOLO_WHOLE", -1)),
+        piece_cost=int(env.get("FKV_PIECE_COST", PIECE_COST_TILES)),
+        sm_pairing=int(env.get("FKV_SM_PAIRING", "1") == "1"),
         chunk=-1 if chunk is None else int(chunk),
-        pair_piece=float(os.environ.get("FKV_PAIR_PIECE", PAIR_PIECE_TILES)))
-    return C.byref(prm), sms
+        pair_piece=float(env.get("FKV_PAIR_PIECE", PAIR_PIECE_TILES)))
+    if len(_SCHED_PARAMS) > 64:
+        _SCHED_PARAMS.clear()
+    _SCHED_PARAMS[key] = hit = (C.byref(prm), sms)
+    return hit
 
 
 def plan_schedule(seg_len, seg_row0, seg_qrow, seg_out_row, device=None, chunk: int | None = None):
@@ -597,6 +612,90 @@ def plan_schedule_py(seg_len, seg_row0, seg_qrow, seg_out_row, device=None, chun
     return (*plan, tab, flags)
 
 
+CT_PARTS = 17  # FKV_CT_PARTS: the parts of fkv_cache_tables' packed buffer, in its order
+
+
+def _pack_tables_py(seg_len, seg_row0, seg_qrow, seg_out_row, seg_cap, append_src, device, chunk):
+    """Python form of fkv_cache_tables (the checker; FKV_PY_SCHEDULE=1):
+    plan_schedule_py plus the packing, same buffer, offsets and sizes."""
+    seg_len = np.asarray(seg_len, dtype=np.int64)
+    item_seg, t0, t1, ptr, wptr, wlist, tab, flags = plan_schedule_py(seg_len, seg_row0, seg_qrow,
+                                                                      seg_out_row, device, chunk)
+    # flat work-table index of every segment's last piece (append grows it)
+    valid = (tab[:, :, 7] & 0xFFFF) != 0
+    pos_of_item = np.zeros(max(len(item_seg), 1), dtype=np.int64)
+    pos_of_item[tab[:, :, 5][valid]] = np.flatnonzero(valid.reshape(-1))
+    last_piece = pos_of_item[np.asarray(ptr[1:], dtype=np.int64) - 1] if len(seg_len) else np.zeros(0)
+    seg_cap = seg_len if seg_cap is None else np.asarray(seg_cap, dtype=np.int64)
+    append_src = np.full(len(seg_len), -1) if append_src is None else np.asarray(append_src)
+    parts = [np.ascontiguousarray(a, dtype=np.int32).reshape(-1) for a in (
+        seg_len, seg_qrow, seg_out_row, item_seg, t0, t1, ptr, np.arange(ptr[-1]), wptr, wlist, tab,
+        seg_cap, append_src, last_piece, np.zeros(max(len(item_seg), 1)), np.zeros(1),
+        np.ascontiguousarray(seg_row0, dtype=np.int64).view(np.int32))]
+    offs = np.cumsum([0] + [-(-len(a) // 4) * 4 for a in parts])
+    host_buf = np.zeros(int(offs[-1]), dtype=np.int32)
+    for a, o in zip(parts, offs[:-1]):
+        host_buf[o:o + len(a)] = a
+    return host_buf, offs, (len(item_seg), len(wptr) - 1, tab.shape[0], tab.shape[1], flags)
+
+
+def cache_tables(seg_len, seg_row0, seg_qrow, seg_out_row, seg_cap=None, append_src=None, device=None,
+                 chunk: int | None = None):
+    """Plan one cache's K4 schedule and pack every int32 table it keeps on
+    the device into one host buffer (fkv_cache_tables, csrc/schedule.cpp;
+    ``_pack_tables_py`` is its Python form, FKV_PY_SCHEDULE=1).  Returns
+    (int32 buffer, part offsets [CT_PARTS + 1] in words, (n_items, busy,
+    rows, K, flags)).  The buffer is per-thread scratch, valid until the
+    thread's next call."""
+    if os.environ.get("FKV_PY_SCHEDULE") == "1":
+        return _pack_tables_py(seg_len, seg_row0, seg_qrow, seg_out_row, seg_cap, append_src, device, chunk)
+    from . import _native
+    i64 = lambda a: None if a is None else np.ascontiguousarray(a, dtype=np.int64)  # noqa: E731
+    seg_len, seg_row0, seg_qrow, seg_out_row = i64(seg_len), i64(seg_row0), i64(seg_qrow), i64(seg_out_row)
+    seg_cap, append_src = i64(seg_cap), i64(append_src)
+    n = len(seg_len)
+    prm, sms = _sched_params(device, chunk)
+    items = max(1, n * MAX_ITEMS_PER_SEGMENT)
+    words = 10 * n + 6 * items + 8 * sms + 8 * sms * MAX_WORK_PER_WORKER * 8 + 4 * (CT_PARTS + 2)
+    sc = _PLAN_SCRATCH.__dict__
+    if sc.get("ct_words", 0) < words:
+        sc.update(ct_words=words, ct=np.empty(words, np.int32))
+    buf = sc["ct"]
+    offs = np.empty(CT_PARTS + 1, np.int64)
+    sizes = np.zeros(5, np.int32)
+    p = lambda a: None if a is None else a.ctypes.data  # noqa: E731
+    rc = _native.lib.fkv_cache_tables(p(seg_len), p(seg_row0), p(seg_qrow), p(seg_out_row), p(seg_cap),
+                                      p(append_src), n, prm, p(buf), len(buf), p(offs), p(sizes))
+    if rc < 0:  # the same exception as the Python planner (e.g. too many segments for one launch)
+        raise ValueError(_native.last_error())
+    return buf[:int(offs[-1])], offs, tuple(int(x) for x in sizes)
+
+
+def _parts(buf: torch.Tensor, offs, lens):
+    """Views of the packed buffer's parts (one split call: 17 slices cost
+    twice as much host time)."""
+    o = offs.tolist()
+    sizes = []
+    for i, m in enumerate(lens):
+        sizes += (m, o[i + 1] - o[i] - m)
+    sizes.append(buf.numel() - o[-1])
+    return torch.split_with_sizes(buf, sizes)[0:2 * len(lens):2]
+
+
+def to_device_async(host: np.ndarray, device) -> torch.Tensor:
+    """int32 host array -> device tensor with one host-to-device copy that does not stall the host: staged through
+    torch's caching pinned-memory allocator (which keeps the staging block
+    until the copy has run) and issued non-blocking on the current stream,
+    so queuing a layer's tables never waits for the kernels before it."""
+    device = torch.device(device)
+    host = np.ascontiguousarray(host, dtype=np.int32)
+    if device.type != "cuda":
+        return torch.from_numpy(host.copy()).to(device)
+    pin = torch.empty(host.shape, dtype=torch.int32, pin_memory=True)
+    pin.numpy()[...] = host
+    return pin.to(device, non_blocking=True)
+
+
 @dataclass
 class LayerCache:
     """Device-resident compressed cache + decode plan for one layer on one GPU."""
@@ -701,49 +800,84 @@ class LayerCache:
                                  seg_cap=seg_cap, append_src=append_src)
 
     @staticmethod
-    def _build(k, v, seg_row0, seg_len, seg_qrow, seg_out_row, group, chunk, seg_cap=None,
-               append_src=None) -> "LayerCache":
-        dev = k.device
+    def allocate_many(layers, group: int, device, chunk: int | None = None, reserve: int = 0,
+                      extra=None) -> "tuple[list[LayerCache], list[torch.Tensor]]":
+        """``allocate`` (zero storage) for a stack of layers at once: one
+        zero-filled K/V allocation for all of them, every layer's planned
+        tables packed into one pinned buffer and sent in ONE host-to-device
+        copy.  ``layers``: (seg_len, seg_qrow, seg_out_row) per layer.
+        ``extra``: optional int32 host arrays that ride in the same copy (the
+        compaction's segment tables); returned as device views."""
+        dev = torch.device(device)
+        plans, caps = [], []
+        total_rows = 0
+        for seg_len, qrow, orow in layers:
+            seg_len = np.asarray(seg_len, dtype=np.int64)
+            cap = page_rows(seg_len + int(reserve))
+            row0, rows = segment_offsets(seg_len + int(reserve))  # rows of the layer's own K/V view
+            caps.append((total_rows, rows))
+            total_rows += rows
+            plans.append(LayerCache._plan_host(row0, seg_len, qrow, orow, chunk, cap, np.arange(len(seg_len)),
+                                               dev, copy=True))
+        kv = torch.zeros((2, total_rows, HEAD_DIM), dtype=torch.bfloat16, device=dev)
+        extra = [np.ascontiguousarray(e, dtype=np.int32).reshape(-1) for e in (extra or [])]
+        words = [int(pl[1][-1]) for pl in plans] + [-(-len(e) // 4) * 4 for e in extra]
+        host = np.zeros(sum(words), dtype=np.int32)
+        o = 0
+        for x, w in zip([pl[0] for pl in plans] + extra, words):
+            host[o:o + len(x)] = x
+            o += w
+        buf = to_device_async(host, dev)
+        caches = []
+        o = 0
+        for (hb, offs, sizes, meta), (r0, rows), w in zip(plans, caps, words):
+            caches.append(LayerCache._assemble(kv[0, r0:r0 + rows], kv[1, r0:r0 + rows], group,
+                                               buf[o:o + w], offs, sizes, meta))
+            o += w
+        views = []
+        for e, w in zip(extra, words[len(plans):]):
+            views.append(buf[o:o + len(e)])
+            o += w
+        return caches, views
+
+    @staticmethod
+    def _plan_host(seg_row0, seg_len, seg_qrow, seg_out_row, chunk, seg_cap, append_src, dev, copy=False):
         seg_row0 = np.asarray(seg_row0, dtype=np.int64)
         seg_len = np.asarray(seg_len, dtype=np.int64)
-        item_seg, t0, t1, ptr, wptr, wlist, tab, flags = plan_schedule(seg_len, seg_row0, seg_qrow,
-                                                                       seg_out_row, dev, chunk)
-        # flat work-table index of every segment's last piece (append grows it)
-        valid = (tab[:, :, 7] & 0xFFFF) != 0
-        pos_of_item = np.zeros(max(len(item_seg), 1), dtype=np.int64)
-        pos_of_item[tab[:, :, 5][valid]] = np.flatnonzero(valid.reshape(-1))
-        last_piece = pos_of_item[np.asarray(ptr[1:], dtype=np.int64) - 1] if len(seg_len) else np.zeros(0)
         seg_cap = seg_len if seg_cap is None else np.asarray(seg_cap, dtype=np.int64)
-        append_src = np.full(len(seg_len), -1) if append_src is None else np.asarray(append_src)
+        host_buf, offs, sizes = cache_tables(seg_len, seg_row0, seg_qrow, seg_out_row, seg_cap, append_src,
+                                             dev, chunk)
+        meta = {"seg_len": seg_len, "seg_row0": seg_row0, "chunk": chunk, "seg_qrow": np.asarray(seg_qrow),
+                "seg_out_row": np.asarray(seg_out_row), "seg_cap": seg_cap}
+        return (host_buf.copy() if copy else host_buf), offs, sizes, meta
 
-        # every int32 table in one host buffer and one host-to-device copy
-        # (16-byte aligned pieces: the work table is read with int4 loads);
-        # fifteen small copies cost more than the planning itself
-        parts = [np.ascontiguousarray(a, dtype=np.int32).reshape(-1) for a in (
-            seg_len, seg_qrow, seg_out_row, item_seg, t0, t1, ptr, np.arange(ptr[-1]), wptr, wlist, tab,
-            seg_cap, append_src, last_piece, np.zeros(max(len(item_seg), 1)), np.zeros(1),
-            np.ascontiguousarray(seg_row0, dtype=np.int64).view(np.int32))]
-        offs = np.cumsum([0] + [-(-len(a) // 4) * 4 for a in parts])
-        host_buf = np.zeros(int(offs[-1]), dtype=np.int32)
-        for a, o in zip(parts, offs[:-1]):
-            host_buf[o:o + len(a)] = a
-        buf = torch.from_numpy(host_buf).to(dev)
-        view = [buf[int(o):int(o) + len(a)] for a, o in zip(parts, offs[:-1])]
+    @staticmethod
+    def _assemble(k, v, group, buf, offs, sizes, meta) -> "LayerCache":
+        n_items, busy, rows, K, flags = sizes
+        n = len(meta["seg_len"])
+        lens = (n, n, n, n_items, n_items, n_items, n + 1, n_items, busy + 1, n_items, rows * K * 8,
+                n, n, n, max(n_items, 1), 1, 2 * n)
         (seg_len_t, qrow_t, orow_t, iseg_t, t0_t, t1_t, ptr_t, src_t, wptr_t, wlist_t, tab_t, cap_t, asrc_t,
-         lp_t, ctr_t, ovf_t, row0_t) = view
-
+         lp_t, ctr_t, ovf_t, row0_t) = _parts(buf, offs, lens)
         return LayerCache(
             k=k, v=v, group=int(group), seg_row0=row0_t.view(torch.int64),
             seg_len=seg_len_t, seg_qrow=qrow_t, seg_out_row=orow_t,
             item_seg=iseg_t, item_t0=t0_t, item_t1=t1_t, grp_ptr=ptr_t, src_idx=src_t,
-            warp_ptr=wptr_t, work_list=wlist_t, work=tab_t.view(tab.shape),
+            warp_ptr=wptr_t, work_list=wlist_t, work=tab_t.view(rows, K, 8),
             counters=ctr_t,
-            host={"seg_len": seg_len, "seg_row0": seg_row0, "chunk": chunk, "n_workers": len(wptr) - 1,
-                  "seg_qrow": np.asarray(seg_qrow), "seg_out_row": np.asarray(seg_out_row),
-                  "flags": flags, "seg_cap": seg_cap,
+            host={**meta, "n_workers": busy, "flags": flags,
                   "seg_cap_t": cap_t, "append_src_t": asrc_t, "last_piece_t": lp_t,
                   "overflow_t": ovf_t, "table_buf": buf},
         )
+
+    @staticmethod
+    def _build(k, v, seg_row0, seg_len, seg_qrow, seg_out_row, group, chunk, seg_cap=None,
+               append_src=None) -> "LayerCache":
+        # every int32 table in one host buffer and one host-to-device copy
+        # (fifteen small copies cost more than the planning itself)
+        host_buf, offs, sizes, meta = LayerCache._plan_host(seg_row0, seg_len, seg_qrow, seg_out_row, chunk,
+                                                            seg_cap, append_src, k.device)
+        return LayerCache._assemble(k, v, group, to_device_async(host_buf, k.device), offs, sizes, meta)
 
     def sync_lengths(self) -> np.ndarray:
         """Read the device segment lengths back (after appends) into host state."""

@@ -573,3 +573,80 @@ extern "C" int fkv_plan_schedule(const int64_t* seg_len, const int64_t* seg_row0
   std::copy(tab.begin(), tab.end(), table);
   return FKV_OK;
 }
+
+// Every int32 table a layer cache keeps on the device, planned and packed in
+// one host buffer for one host-to-device copy (cache.LayerCache._build;
+// _pack_tables_py is the Python form it replaces, kept as the checker).
+extern "C" int fkv_cache_tables(const int64_t* seg_len, const int64_t* seg_row0, const int64_t* seg_qrow,
+                                const int64_t* seg_out_row, const int64_t* seg_cap, const int64_t* append_src,
+                                int32_t n_seg, const fkv_sched_params* prm, int32_t* buf, int64_t buf_words,
+                                int64_t* part_off, int32_t* out_sizes) {
+  using namespace fkv;
+  if (n_seg < 0 || !prm || !out_sizes || !part_off ||
+      (n_seg && (!seg_len || !seg_row0 || !seg_qrow || !seg_out_row)))
+    return set_error(FKV_ERR_INVALID, "fkv_cache_tables: bad arguments");
+  if (prm->sms < 1 || prm->ctas_coop < 1 || prm->ctas_wide < 1 || prm->ctas_solo < 1 ||
+      static_cast<int64_t>(prm->sms) * 4 * std::max({prm->ctas_coop, prm->ctas_wide, prm->ctas_solo}) >= 65536)
+    return set_error(FKV_ERR_INVALID, "fkv_cache_tables: bad device parameters");
+  V len(seg_len, seg_len + n_seg);
+  for (i64 x : len)
+    if (x < 0) return set_error(FKV_ERR_INVALID, "fkv_cache_tables: negative segment length");
+  Plan plan;
+  std::vector<int32_t> tab;
+  i64 rows = 0, K = 0;
+  int flags = 0;
+  try {
+    plan_schedule(len, seg_row0, seg_qrow, seg_out_row, *prm, plan, tab, rows, K, flags);
+  } catch (const PlanError& e) {
+    return set_error(FKV_ERR_VALIDATION, "fkv_plan_schedule: " + e.msg);
+  }
+  const i64 n = n_seg, n_items = static_cast<i64>(plan.item_seg.size());
+  const i64 busy = static_cast<i64>(plan.warp_ptr.size()) - 1;
+  out_sizes[0] = static_cast<int32_t>(n_items);
+  out_sizes[1] = static_cast<int32_t>(busy);
+  out_sizes[2] = static_cast<int32_t>(rows);
+  out_sizes[3] = static_cast<int32_t>(K);
+  out_sizes[4] = flags;
+  const i64 cnt = std::max<i64>(n_items, 1);
+  const i64 lens[FKV_CT_PARTS] = {n, n, n, n_items, n_items, n_items, n + 1, n_items, busy + 1,
+                                  n_items, rows * K * 8, n, n, n, cnt, 1, 2 * n};
+  part_off[0] = 0;
+  for (int i = 0; i < FKV_CT_PARTS; ++i) part_off[i + 1] = part_off[i] + (lens[i] + 3) / 4 * 4;
+  if (part_off[FKV_CT_PARTS] > buf_words)
+    return set_error(FKV_ERR_INVALID, "fkv_cache_tables: buffer too small (words needed in part_off[17])");
+  if (!buf) return set_error(FKV_ERR_INVALID, "fkv_cache_tables: null buffer");
+  std::fill(buf, buf + part_off[FKV_CT_PARTS], 0);
+  auto put64 = [&](int part, const int64_t* src, i64 m, int64_t dflt) {
+    int32_t* d = buf + part_off[part];
+    for (i64 i = 0; i < m; ++i) d[i] = static_cast<int32_t>(src ? src[i] : dflt);
+  };
+  auto put32 = [&](int part, const std::vector<int32_t>& src) {
+    std::copy(src.begin(), src.end(), buf + part_off[part]);
+  };
+  put64(FKV_CT_SEG_LEN, seg_len, n, 0);
+  put64(FKV_CT_SEG_QROW, seg_qrow, n, 0);
+  put64(FKV_CT_SEG_OUT_ROW, seg_out_row, n, 0);
+  put32(FKV_CT_ITEM_SEG, plan.item_seg);
+  put32(FKV_CT_ITEM_T0, plan.t0);
+  put32(FKV_CT_ITEM_T1, plan.t1);
+  put32(FKV_CT_SEG_ITEM_PTR, plan.seg_item_ptr);
+  std::iota(buf + part_off[FKV_CT_SRC_IDX], buf + part_off[FKV_CT_SRC_IDX] + n_items, 0);
+  put32(FKV_CT_WARP_PTR, plan.warp_ptr);
+  put32(FKV_CT_WORK_LIST, plan.work_list);
+  put32(FKV_CT_WORK, tab);
+  put64(FKV_CT_SEG_CAP, seg_cap ? seg_cap : seg_len, n, 0);
+  put64(FKV_CT_APPEND_SRC, append_src, n, -1);
+  // flat work-table index of every segment's last piece (fkv_append grows it)
+  std::vector<int32_t> pos(cnt, 0);
+  for (i64 e = 0; e < rows * K; ++e)
+    if (tab[e * 8 + 7] & 0xFFFF) pos[tab[e * 8 + 5]] = static_cast<int32_t>(e);
+  int32_t* lp = buf + part_off[FKV_CT_LAST_PIECE];
+  for (i64 s = 0; s < n; ++s) {
+    i64 it = plan.seg_item_ptr[s + 1] - 1;
+    if (it < 0) it += cnt;  // as numpy's index -1
+    lp[s] = pos[it];
+  }
+  // counters and the overflow flag stay zero
+  std::copy(seg_row0, seg_row0 + n, reinterpret_cast<int64_t*>(buf + part_off[FKV_CT_SEG_ROW0]));
+  return FKV_OK;
+}

@@ -23,7 +23,7 @@ import math
 import torch
 
 from . import _native
-from .cache import HEAD_DIM, LayerCache
+from .cache import HEAD_DIM, LayerCache, to_device_async
 from .errors import NativeError
 
 _lib = _native.lib
@@ -358,7 +358,7 @@ def compact(k: torch.Tensor, v: torch.Tensor, offsets: torch.Tensor, idx: torch.
     n = len(seg_lo)
     host = np.empty(3 * n, dtype=np.int32)  # the three segment tables in one host-to-device copy
     host[:n], host[n:2 * n], host[2 * n:] = seg_bh, seg_lo, seg_hi
-    dev_tabs = torch.from_numpy(host).to(k.device)
+    dev_tabs = to_device_async(host, k.device)
     tabs = (dev_tabs[:n], dev_tabs[n:2 * n], dev_tabs[2 * n:])
     compact_into(cache, k, v, offsets, idx, *tabs,
                  int((seg_hi - seg_lo).max()) if len(seg_lo) else 0)
@@ -404,8 +404,18 @@ def compress_stack(q_wins, ks, vs, budget: int, window: int = 32, alpha: float =
     sel = [score_select(q, k, budget, window, alpha, pool_k, workspace=ws) for q, k in zip(q_wins, ks)]
     hbs = torch.stack([x[1] for x in sel])
     hb_host = hbs.cpu().numpy()  # the one host round trip
-    bh = np.arange(bt * hkv)
+    BH = bt * hkv
+    bh = np.arange(BH)
     qrow = (bh // hkv) * hq + (bh % hkv) * group
-    caches = [compact(k, v, x[2], x[3], bh, np.zeros_like(bh), hb_host[l].reshape(-1), qrow, qrow, group)
-              for l, (k, v, x) in enumerate(zip(ks, vs, sel))]
+    lens = hb_host.reshape(len(ks), BH).astype(np.int64)
+    # every layer's cache laid out at once: one K/V allocation, every plan and
+    # the compactions' segment tables in one host-to-device copy
+    caches, (seg_bh, seg_lo, seg_hi) = LayerCache.allocate_many(
+        [(lens[l], qrow, qrow) for l in range(len(ks))], group, dev, extra=[bh, np.zeros(BH), lens])
+    for l, (k, v, x, cache) in enumerate(zip(ks, vs, sel, caches)):
+        _need_cuda(k, v)
+        if k.dtype != torch.bfloat16 or k.shape != v.shape or k.shape[-1] != HEAD_DIM \
+                or not (k.is_contiguous() and v.is_contiguous()):
+            raise NativeError("k/v must be contiguous bf16 [Bt, Hkv, T, 128]")
+        compact_into(cache, k, v, x[2], x[3], seg_bh, seg_lo, seg_hi[l * BH:(l + 1) * BH], int(lens[l].max()))
     return caches, hbs, [x[0] for x in sel]

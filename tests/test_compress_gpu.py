@@ -223,6 +223,12 @@ def test_compress_stack_matches_per_layer(cuda_device):
         assert torch.equal(hbs[l], hb) and torch.equal(scs[l], sc)
         assert torch.equal(caches[l].k, cache.k) and torch.equal(caches[l].v, cache.v)
         assert torch.equal(caches[l].work, cache.work)
+        for name in ("seg_row0", "seg_len", "seg_qrow", "warp_ptr", "work_list", "grp_ptr", "src_idx"):
+            assert torch.equal(getattr(caches[l], name), getattr(cache, name)), name
+        # the stacked caches (views of one K/V allocation) decode identically
+        qd = torch.randn((bt, hq, 128), device=cuda_device).to(torch.bfloat16)
+        (o1, l1), (o2, l2) = ops.decode(qd, caches[l]), ops.decode(qd, cache)
+        assert torch.equal(o1, o2) and torch.equal(l1, l2)
 
 
 def test_selection_agreement_with_oracle_scores(cuda_device):

@@ -83,3 +83,72 @@ def test_native_errors_match():
     from paper_2502_15804_b200.errors import NativeError
     with pytest.raises((ValueError, NativeError)):
         C.plan_schedule(lens, row0, q, q)
+
+
+def _check_tables(lens, chunk=None, cap=None, asrc=None):
+    row0, _ = C.segment_offsets(lens)
+    qrow = np.arange(len(lens), dtype=np.int64) * 8
+    orow = qrow[::-1].copy()
+    got, goff, gsz = C.cache_tables(lens, row0, qrow, orow, cap, asrc, None, chunk)
+    want, woff, wsz = C._pack_tables_py(lens, row0, qrow, orow, cap, asrc, None, chunk)
+    assert gsz == wsz
+    np.testing.assert_array_equal(goff, woff)
+    np.testing.assert_array_equal(got, want)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_packed_tables_match_python(seed):
+    """fkv_cache_tables (schedule + every device table of a LayerCache in one
+    buffer) against the Python packing, with and without append headroom."""
+    rng = np.random.default_rng(100 + seed)
+    for n, mean in ((8, 1024), (64, 500), (512, 1024), (1100, 120), (5, 3)):
+        lens = _segments(rng, n, mean)
+        _check_tables(lens)
+        _check_tables(lens, cap=C.page_rows(lens + 16), asrc=np.arange(n))
+        src = rng.integers(-1, n, n)
+        _check_tables(lens, chunk=256, cap=lens + rng.integers(0, 64, n), asrc=src)
+    _check_tables(np.zeros(0, dtype=np.int64))
+    _check_tables(np.zeros(9, dtype=np.int64))
+
+
+def test_layer_cache_tables_on_cpu():
+    """LayerCache built from the packed buffer: every view equals the Python
+    planner's tables (CPU storage: the packing, not the kernels)."""
+    rng = np.random.default_rng(7)
+    lens = _segments(rng, 96, 700)
+    qrow = np.arange(96, dtype=np.int64) * 8
+    cache = C.LayerCache.allocate(lens, qrow, qrow, 8, "cpu", reserve=16)
+    row0, _ = C.segment_offsets(lens + 16)
+    item_seg, t0, t1, ptr, wptr, wlist, tab, flags = C.plan_schedule_py(lens, row0, qrow, qrow)
+    for t, want in ((cache.item_seg, item_seg), (cache.item_t0, t0), (cache.item_t1, t1), (cache.grp_ptr, ptr),
+                    (cache.warp_ptr, wptr), (cache.work_list, wlist), (cache.work, tab),
+                    (cache.seg_len, lens), (cache.seg_row0, row0), (cache.src_idx, np.arange(len(item_seg)))):
+        np.testing.assert_array_equal(t.numpy(), want)
+    assert cache.flags == flags and cache.n_workers == len(wptr) - 1
+    assert int(cache.counters.abs().sum()) == 0 and int(cache.host["overflow_t"][0]) == 0
+    np.testing.assert_array_equal(cache.host["seg_cap_t"].numpy(), C.page_rows(lens + 16))
+
+
+def test_allocate_many_matches_allocate():
+    """LayerCache.allocate_many (one K/V allocation, every layer's tables in
+    one copy, extra arrays riding along) == allocate per layer."""
+    import torch
+    rng = np.random.default_rng(11)
+    layers = []
+    for n, mean in ((8, 300), (40, 1000), (8, 3)):
+        lens = _segments(rng, n, mean)
+        q = np.arange(n, dtype=np.int64) * 4
+        layers.append((lens, q, q[::-1].copy()))
+    extra = [np.arange(5), np.full(3, 7)]
+    caches, views = C.LayerCache.allocate_many(layers, 4, "cpu", reserve=32, extra=extra)
+    for c, (lens, q, o) in zip(caches, layers):
+        ref = C.LayerCache.allocate(lens, q, o, 4, "cpu", reserve=32)
+        for name in ("seg_row0", "seg_len", "seg_qrow", "seg_out_row", "item_seg", "item_t0", "item_t1",
+                     "grp_ptr", "src_idx", "warp_ptr", "work_list", "work", "counters"):
+            assert torch.equal(getattr(c, name), getattr(ref, name)), name
+        for name in ("seg_cap_t", "append_src_t", "last_piece_t", "overflow_t"):
+            assert torch.equal(c.host[name], ref.host[name]), name
+        assert c.k.shape == ref.k.shape and c.flags == ref.flags and c.n_workers == ref.n_workers
+        assert c.k.is_contiguous() and int(c.k.abs().sum()) == 0
+    for vw, e in zip(views, extra):
+        np.testing.assert_array_equal(vw.numpy(), e)
