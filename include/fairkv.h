@@ -315,7 +315,10 @@ int fkv_snapkv_score(const void* q_win, const void* k, int32_t batch, int32_t hq
  * fkv_ada_select (budgets int32 [batch, hkv], offsets int64 [batch*hkv + 1]
  * with request b starting at b*hkv*budget, idx int32 [batch*hkv*budget]).
  * Same workspace size as fkv_snapkv_score.  Hkv > 16, or more than 14 heads
- * per SM, run as those two launches. */
+ * per SM, run as those two launches.  `budgets` may point to pinned host
+ * memory (device-addressable under unified addressing): the launch only
+ * writes it, so the host reads a layer's budgets once the launch has ended
+ * without a copy (ops.compress_stack). */
 int fkv_snapkv_select(const void* q_win, const void* k, int32_t batch, int32_t hq, int32_t hkv,
                       int32_t T, int32_t window, int32_t pool_k, float sm_scale, int32_t budget,
                       int32_t floor_k, float* scores, int32_t* budgets, int64_t* offsets,

@@ -671,15 +671,11 @@ def cache_tables(seg_len, seg_row0, seg_qrow, seg_out_row, seg_cap=None, append_
     return buf[:int(offs[-1])], offs, tuple(int(x) for x in sizes)
 
 
-def _parts(buf: torch.Tensor, offs, lens):
-    """Views of the packed buffer's parts (one split call: 17 slices cost
-    twice as much host time)."""
-    o = offs.tolist()
-    sizes = []
-    for i, m in enumerate(lens):
-        sizes += (m, o[i + 1] - o[i] - m)
-    sizes.append(buf.numel() - o[-1])
-    return torch.split_with_sizes(buf, sizes)[0:2 * len(lens):2]
+def _part_lens(n: int, sizes) -> tuple:
+    """Lengths of fkv_cache_tables' parts (FKV_CT_* order) for n segments."""
+    n_items, busy, rows, K, _ = sizes
+    return (n, n, n, n_items, n_items, n_items, n + 1, n_items, busy + 1, n_items, rows * K * 8,
+            n, n, n, max(n_items, 1), 1, 2 * n)
 
 
 def to_device_async(host: np.ndarray, device) -> torch.Tensor:
@@ -696,54 +692,97 @@ def to_device_async(host: np.ndarray, device) -> torch.Tensor:
     return pin.to(device, non_blocking=True)
 
 
-@dataclass
+_PART_NAMES = ("seg_len", "seg_qrow", "seg_out_row", "item_seg", "item_t0", "item_t1", "grp_ptr", "src_idx",
+               "warp_ptr", "work_list", "work", "seg_cap_t", "append_src_t", "last_piece_t", "counters",
+               "overflow_t", "seg_row0")  # FKV_CT_* order
+
+
+class _Part:
+    """A table of the cache's packed device buffer, viewed on first use (the
+    kernels only need its address; building seventeen views per layer costs
+    more host time than planning the layer)."""
+
+    def __init__(self, i: int):
+        self.i = i
+
+    def __set_name__(self, owner, name):
+        self.name = name
+
+    def __get__(self, obj, owner=None):
+        if obj is None:
+            return self
+        t = obj.tables[obj.offs[self.i]:obj.offs[self.i] + obj.lens[self.i]]
+        if self.i == 16:        # SEG_ROW0: int64
+            t = t.view(torch.int64)
+        elif self.i == 10:      # WORK: fkv_work_t [workers, K, 8]
+            t = t.view(obj.sizes[2], obj.sizes[3], 8)
+        obj.__dict__[self.name] = t
+        return t
+
+
+@dataclass(eq=False)
 class LayerCache:
-    """Device-resident compressed cache + decode plan for one layer on one GPU."""
+    """Device-resident compressed cache + decode plan for one layer on one
+    GPU: K/V storage plus every int32 table K3/K4/K5/append read, packed in
+    one device buffer (fkv_cache_tables' layout) and exposed as views."""
 
     k: torch.Tensor
     v: torch.Tensor
     group: int
-    seg_row0: torch.Tensor
-    seg_len: torch.Tensor
-    seg_qrow: torch.Tensor
-    seg_out_row: torch.Tensor
-    item_seg: torch.Tensor
-    item_t0: torch.Tensor
-    item_t1: torch.Tensor
-    grp_ptr: torch.Tensor
-    src_idx: torch.Tensor
-    warp_ptr: torch.Tensor
-    work_list: torch.Tensor
-    work: torch.Tensor        # fkv_work_t [workers, K, 8] int32 (what K4 reads)
-    counters: torch.Tensor    # int32 [n_items]
+    tables: torch.Tensor      # int32, the packed parts
+    offs: list                # word offset of each part
+    lens: tuple               # length of each part (words; SEG_ROW0 counts int32 words)
+    sizes: tuple              # (n_items, busy workers, work rows, K, schedule flags)
     host: dict = field(default_factory=dict, repr=False)
+
+    seg_len = _Part(0)
+    seg_qrow = _Part(1)
+    seg_out_row = _Part(2)
+    item_seg = _Part(3)
+    item_t0 = _Part(4)
+    item_t1 = _Part(5)
+    grp_ptr = _Part(6)
+    src_idx = _Part(7)
+    warp_ptr = _Part(8)
+    work_list = _Part(9)
+    work = _Part(10)          # fkv_work_t [workers, K, 8] int32 (what K4 reads)
+    seg_cap_t = _Part(11)
+    append_src_t = _Part(12)
+    last_piece_t = _Part(13)
+    counters = _Part(14)      # int32 [n_items]
+    overflow_t = _Part(15)
+    seg_row0 = _Part(16)
+
+    def ptr(self, part: int) -> int:
+        """Device address of a part (FKV_CT_* index) without building its view."""
+        return self.tables.data_ptr() + 4 * self.offs[part]
 
     @property
     def n_workers(self) -> int:
-        return int(self.work.shape[0])
+        return self.sizes[2]
 
     @property
     def flags(self) -> int:
-        return int(self.host.get("flags", 0))
+        return self.sizes[4]
 
     @property
     def launch_flags(self) -> int:
         """Schedule flags plus FKV_DECODE_AFTER_WAIT once the cache has been
         written on the device (compaction, decode-time appends): the decode
         kernel then reads nothing before its programmatic-launch wait."""
-        return self.flags | (FKV_DECODE_AFTER_WAIT if self.host.get("written") else 0)
+        return self.sizes[4] | (FKV_DECODE_AFTER_WAIT if self.host.get("written") else 0)
 
     @property
     def work_k(self) -> int:
-        return int(self.work.shape[1])
+        return self.sizes[3]
 
     @property
     def n_items(self) -> int:
-        return int(self.item_seg.shape[0])
+        return self.sizes[0]
 
     @property
     def n_segments(self) -> int:
-        return int(self.seg_len.shape[0])
+        return self.lens[0]
 
     @property
     def retained_tokens(self) -> int:
@@ -811,28 +850,69 @@ class LayerCache:
         dev = torch.device(device)
         plans, caps = [], []
         total_rows = 0
-        for seg_len, qrow, orow in layers:
-            seg_len = np.asarray(seg_len, dtype=np.int64)
-            cap = page_rows(seg_len + int(reserve))
-            row0, rows = segment_offsets(seg_len + int(reserve))  # rows of the layer's own K/V view
-            caps.append((total_rows, rows))
-            total_rows += rows
-            plans.append(LayerCache._plan_host(row0, seg_len, qrow, orow, chunk, cap, np.arange(len(seg_len)),
-                                               dev, copy=True))
+        if os.environ.get("FKV_PY_SCHEDULE") == "1":
+            for seg_len, qrow, orow in layers:
+                seg_len = np.asarray(seg_len, dtype=np.int64)
+                row0, rows = segment_offsets(seg_len + int(reserve))  # rows of the layer's own K/V view
+                caps.append((total_rows, rows))
+                total_rows += rows
+                plans.append(LayerCache._plan_host(row0, seg_len, qrow, orow, chunk, page_rows(seg_len + int(reserve)),
+                                                   np.arange(len(seg_len)), dev, copy=True))
+        else:  # the native planner straight into one scratch buffer, layer after layer
+            from . import _native
+            prm, _ = _sched_params(dev, chunk)
+            fn = _native.lib.fkv_cache_tables
+            sc = _PLAN_SCRATCH.__dict__
+            scratch = sc.get("many")
+            if scratch is None:
+                scratch = sc["many"] = np.empty(1 << 20, np.int32)
+            o = 0
+            i64 = lambda a: np.ascontiguousarray(a, dtype=np.int64)  # noqa: E731
+            for seg_len, qrow, orow in layers:
+                seg_len, qrow, orow = i64(seg_len), i64(qrow), i64(orow)
+                n = len(seg_len)
+                cap = page_rows(seg_len + int(reserve))
+                row0 = np.zeros(n, dtype=np.int64)
+                if n:
+                    np.cumsum(cap[:-1], out=row0[1:])
+                rows = max(int(cap.sum()), PAGE)
+                asrc = np.arange(n, dtype=np.int64)
+                offs = np.zeros(CT_PARTS + 1, np.int64)  # a planning error leaves it zero
+                sizes = np.zeros(5, np.int32)
+                while True:
+                    rc = fn(seg_len.ctypes.data, row0.ctypes.data, qrow.ctypes.data, orow.ctypes.data,
+                            cap.ctypes.data, asrc.ctypes.data, n, prm, scratch.ctypes.data + 4 * o,
+                            len(scratch) - o, offs.ctypes.data, sizes.ctypes.data)
+                    if rc >= 0:
+                        break
+                    if offs[-1] + o <= len(scratch):  # not a buffer problem
+                        raise ValueError(_native.last_error())
+                    grown = np.empty(2 * (int(offs[-1]) + o), np.int32)
+                    grown[:o] = scratch[:o]
+                    scratch = sc["many"] = grown
+                meta = {"seg_len": seg_len, "seg_row0": row0, "chunk": chunk, "seg_qrow": qrow,
+                        "seg_out_row": orow, "seg_cap": cap}
+                plans.append((o, offs, tuple(int(x) for x in sizes), meta))
+                o += int(offs[-1])
+                caps.append((total_rows, rows))
+                total_rows += rows
         kv = torch.zeros((2, total_rows, HEAD_DIM), dtype=torch.bfloat16, device=dev)
         extra = [np.ascontiguousarray(e, dtype=np.int32).reshape(-1) for e in (extra or [])]
         words = [int(pl[1][-1]) for pl in plans] + [-(-len(e) // 4) * 4 for e in extra]
         host = np.zeros(sum(words), dtype=np.int32)
         o = 0
-        for x, w in zip([pl[0] for pl in plans] + extra, words):
-            host[o:o + len(x)] = x
+        for pl, w in zip(plans, words):
+            host[o:o + w] = pl[0] if isinstance(pl[0], np.ndarray) else scratch[pl[0]:pl[0] + w]
+            o += w
+        for e, w in zip(extra, words[len(plans):]):
+            host[o:o + len(e)] = e
             o += w
         buf = to_device_async(host, dev)
         caches = []
         o = 0
-        for (hb, offs, sizes, meta), (r0, rows), w in zip(plans, caps, words):
-            caches.append(LayerCache._assemble(kv[0, r0:r0 + rows], kv[1, r0:r0 + rows], group,
-                                               buf[o:o + w], offs, sizes, meta))
+        for (_, offs, sz, meta), (r0, rows), w in zip(plans, caps, words):
+            caches.append(LayerCache._assemble(kv[0, r0:r0 + rows], kv[1, r0:r0 + rows], group, buf, o, offs,
+                                               sz, meta))
             o += w
         views = []
         for e, w in zip(extra, words[len(plans):]):
@@ -852,23 +932,11 @@ class LayerCache:
         return (host_buf.copy() if copy else host_buf), offs, sizes, meta
 
     @staticmethod
-    def _assemble(k, v, group, buf, offs, sizes, meta) -> "LayerCache":
-        n_items, busy, rows, K, flags = sizes
-        n = len(meta["seg_len"])
-        lens = (n, n, n, n_items, n_items, n_items, n + 1, n_items, busy + 1, n_items, rows * K * 8,
-                n, n, n, max(n_items, 1), 1, 2 * n)
-        (seg_len_t, qrow_t, orow_t, iseg_t, t0_t, t1_t, ptr_t, src_t, wptr_t, wlist_t, tab_t, cap_t, asrc_t,
-         lp_t, ctr_t, ovf_t, row0_t) = _parts(buf, offs, lens)
-        return LayerCache(
-            k=k, v=v, group=int(group), seg_row0=row0_t.view(torch.int64),
-            seg_len=seg_len_t, seg_qrow=qrow_t, seg_out_row=orow_t,
-            item_seg=iseg_t, item_t0=t0_t, item_t1=t1_t, grp_ptr=ptr_t, src_idx=src_t,
-            warp_ptr=wptr_t, work_list=wlist_t, work=tab_t.view(rows, K, 8),
-            counters=ctr_t,
-            host={**meta, "n_workers": busy, "flags": flags,
-                  "seg_cap_t": cap_t, "append_src_t": asrc_t, "last_piece_t": lp_t,
-                  "overflow_t": ovf_t, "table_buf": buf},
-        )
+    def _assemble(k, v, group, buf, base: int, offs, sizes, meta) -> "LayerCache":
+        """The cache over its tables at word ``base`` of the device buffer."""
+        return LayerCache(k=k, v=v, group=int(group), tables=buf, offs=[base + x for x in offs.tolist()],
+                          lens=_part_lens(len(meta["seg_len"]), sizes), sizes=sizes,
+                          host={**meta, "n_workers": sizes[1]})
 
     @staticmethod
     def _build(k, v, seg_row0, seg_len, seg_qrow, seg_out_row, group, chunk, seg_cap=None,
@@ -877,7 +945,7 @@ class LayerCache:
         # (fifteen small copies cost more than the planning itself)
         host_buf, offs, sizes, meta = LayerCache._plan_host(seg_row0, seg_len, seg_qrow, seg_out_row, chunk,
                                                             seg_cap, append_src, k.device)
-        return LayerCache._assemble(k, v, group, to_device_async(host_buf, k.device), offs, sizes, meta)
+        return LayerCache._assemble(k, v, group, to_device_async(host_buf, k.device), 0, offs, sizes, meta)
 
     def sync_lengths(self) -> np.ndarray:
         """Read the device segment lengths back (after appends) into host state."""

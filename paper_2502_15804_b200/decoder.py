@@ -55,9 +55,9 @@ def rank_caches(shards: list[LayerShard], bt: int, hq: int, group: int, tp: int,
                                     reserve=reserve)
             if head_len is not None:
                 owns_end = sh.seg_hi >= np.asarray(head_len[l]).reshape(-1)[bh]
-                c.host["append_src_t"].copy_(torch.as_tensor(np.where(owns_end, bh, -1).astype(np.int32)))
+                c.append_src_t.copy_(torch.as_tensor(np.where(owns_end, bh, -1).astype(np.int32)))
             else:
-                c.host["append_src_t"].copy_(torch.as_tensor(bh.astype(np.int32)))
+                c.append_src_t.copy_(torch.as_tensor(bh.astype(np.int32)))
             out.append(c)
     return out
 

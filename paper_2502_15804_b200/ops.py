@@ -189,11 +189,11 @@ def append(cache: LayerCache, k_new: torch.Tensor, v_new: torch.Tensor):
         raise NativeError("k_new / v_new must be contiguous bf16 [..., 128] of one shape")
     h = cache.host
     h["written"] = True
-    _native.check(_lib.fkv_append(k_new.data_ptr(), v_new.data_ptr(), h["append_src_t"].data_ptr(),
+    _native.check(_lib.fkv_append(k_new.data_ptr(), v_new.data_ptr(), cache.append_src_t.data_ptr(),
                                   cache.seg_row0.data_ptr(), cache.seg_len.data_ptr(),
-                                  h["seg_cap_t"].data_ptr(), cache.work.data_ptr(),
-                                  h["last_piece_t"].data_ptr(), cache.n_segments,
-                                  h["overflow_t"].data_ptr(), cache.k.data_ptr(), cache.v.data_ptr(),
+                                  cache.seg_cap_t.data_ptr(), cache.work.data_ptr(),
+                                  cache.last_piece_t.data_ptr(), cache.n_segments,
+                                  cache.overflow_t.data_ptr(), cache.k.data_ptr(), cache.v.data_ptr(),
                                   _stream()))
 
 
@@ -384,38 +384,76 @@ def compress_layer(q_win: torch.Tensor, k: torch.Tensor, v: torch.Tensor, budget
 
 
 def compress_stack(q_wins, ks, vs, budget: int, window: int = 32, alpha: float = 0.2, pool_k: int = 7):
-    """Prefill compression of a whole layer stack on one GPU with ONE host
-    round trip: every layer's fused K1 + A18 + K2 launch is queued first
-    (workspace reused, stream ordered), the budgets of all layers come back
-    in one copy, then every layer's K3 compaction is queued.  compress_layer
-    per layer instead stalls the stream once per layer (the host must know a
-    layer's budgets to lay out its ragged cache).  q_wins / ks / vs: one
-    tensor per layer, shapes as compress_layer.  Returns ([cache], budgets
-    int32 [L, Bt, Hkv] on the device, [scores])."""
+    """Prefill compression of a whole layer stack on one GPU without
+    stalling the stream per layer: every layer's fused K1 + A18 + K2 launch
+    is queued first (outputs of all layers in one allocation each, workspace
+    reused, stream ordered); each layer's budgets come back on a side stream
+    as soon as its launch ends, and the host lays out that layer's ragged
+    cache (schedule + tables, fkv_cache_tables) while the GPU scores the
+    next ones; then one K/V allocation and one host-to-device copy for the
+    whole stack and every layer's K3 compaction.  compress_layer per layer
+    instead stalls the stream once per layer (the host must know a layer's
+    budgets to lay out its cache).  q_wins / ks / vs: one tensor per layer,
+    shapes as compress_layer.  Returns ([cache], budgets int32 [L, Bt, Hkv]
+    on the device, [scores])."""
     import numpy as np
     if not (len(q_wins) == len(ks) == len(vs)) or not ks:
         raise NativeError("compress_stack needs the same number (>= 1) of q_win, k and v tensors")
+    L = len(ks)
     bt, hq, w = q_wins[0].shape[0], q_wins[0].shape[1], q_wins[0].shape[2]
     hkv, T = ks[0].shape[1], ks[0].shape[2]
     group = hq // hkv
     dev = ks[0].device
+    for q, k, v in zip(q_wins, ks, vs):
+        _need_cuda(q, k, v)
+        if q.dtype != torch.bfloat16 or k.dtype != torch.bfloat16 or v.dtype != torch.bfloat16 \
+                or q.shape != q_wins[0].shape or k.shape != ks[0].shape or v.shape != k.shape \
+                or k.shape[-1] != HEAD_DIM or q.shape[-1] != HEAD_DIM \
+                or not (q.is_contiguous() and k.is_contiguous() and v.is_contiguous()):
+            raise NativeError("compress_stack: every layer's q_win / k / v contiguous bf16 [..., 128], same shapes")
+    BH = bt * hkv
+    # every layer's outputs in one allocation each; the launches queued back to back
     need = int(_lib.fkv_score_workspace_bytes(bt, hkv, T, w, group))
     ws = torch.empty(need, dtype=torch.uint8, device=dev)
-    sel = [score_select(q, k, budget, window, alpha, pool_k, workspace=ws) for q, k in zip(q_wins, ks)]
-    hbs = torch.stack([x[1] for x in sel])
-    hb_host = hbs.cpu().numpy()  # the one host round trip
-    BH = bt * hkv
+    sc = torch.empty((L, bt, hkv, T - w), dtype=torch.float32, device=dev)
+    # the budgets are written by the kernels straight into pinned host memory
+    # (device-addressable under unified addressing), so the host lays out
+    # layer l as soon as its launch ends, while the GPU scores the next ones
+    hb_pin = torch.empty((L, BH), dtype=torch.int32, pin_memory=True)
+    hb_np = hb_pin.numpy()
+    offsets = torch.empty((L, BH + 1), dtype=torch.int64, device=dev)
+    idx = torch.empty((L, max(BH * budget, 1)), dtype=torch.int32, device=dev)
+    scale, floor, stream = 1.0 / math.sqrt(HEAD_DIM), ada_floor(budget, w, alpha), _stream()
+    p_sc, p_hb, p_off, p_idx = sc.data_ptr(), hb_pin.data_ptr(), offsets.data_ptr(), idx.data_ptr()
+    s_sc, s_hb, s_off, s_idx = 4 * sc[0].numel(), 4 * BH, 8 * (BH + 1), 4 * idx.shape[1]
+    ready = []
+    for l, (q, k) in enumerate(zip(q_wins, ks)):
+        _native.check(_lib.fkv_snapkv_select(q.data_ptr(), k.data_ptr(), bt, hq, hkv, T, w, int(pool_k), scale,
+                                             int(budget), floor, p_sc + l * s_sc, p_hb + l * s_hb,
+                                             p_off + l * s_off, p_idx + l * s_idx, ws.data_ptr(), stream))
+        ev = torch.cuda.Event()
+        ev.record()
+        ready.append(ev)
     bh = np.arange(BH)
     qrow = (bh // hkv) * hq + (bh % hkv) * group
-    lens = hb_host.reshape(len(ks), BH).astype(np.int64)
-    # every layer's cache laid out at once: one K/V allocation, every plan and
-    # the compactions' segment tables in one host-to-device copy
-    caches, (seg_bh, seg_lo, seg_hi) = LayerCache.allocate_many(
-        [(lens[l], qrow, qrow) for l in range(len(ks))], group, dev, extra=[bh, np.zeros(BH), lens])
-    for l, (k, v, x, cache) in enumerate(zip(ks, vs, sel, caches)):
-        _need_cuda(k, v)
-        if k.dtype != torch.bfloat16 or k.shape != v.shape or k.shape[-1] != HEAD_DIM \
-                or not (k.is_contiguous() and v.is_contiguous()):
-            raise NativeError("k/v must be contiguous bf16 [Bt, Hkv, T, 128]")
-        compact_into(cache, k, v, x[2], x[3], seg_bh, seg_lo, seg_hi[l * BH:(l + 1) * BH], int(lens[l].max()))
-    return caches, hbs, [x[0] for x in sel]
+
+    def layers():
+        for l in range(L):
+            ready[l].synchronize()
+            yield hb_np[l].astype(np.int64), qrow, qrow
+
+    # every layer's cache laid out as its budgets arrive, then one K/V
+    # allocation and ONE host-to-device copy for every plan, the
+    # compactions' segment tables and the budgets' device copy
+    caches, (seg_bh, seg_lo, seg_hi) = LayerCache.allocate_many(layers(), group, dev,
+                                                                extra=[bh, np.zeros(BH), hb_np])
+    lens = hb_np
+    hbs = seg_hi.view(L, bt, hkv)
+    p_bh, p_lo, p_hi = seg_bh.data_ptr(), seg_lo.data_ptr(), seg_hi.data_ptr()
+    for l, (k, v, cache) in enumerate(zip(ks, vs, caches)):
+        cache.host["written"] = True
+        _native.check(_lib.fkv_compact(k.data_ptr(), v.data_ptr(), T, BH, p_off + l * s_off, p_idx + l * s_idx,
+                                       p_bh, p_lo, p_hi + 4 * l * BH, cache.ptr(16), 1,
+                                       int(lens[l].max()), cache.k.data_ptr(), cache.v.data_ptr(), stream))
+        cache.host["compact_args"] = (seg_bh, seg_hi, offsets, idx)  # alive until the stream consumes them
+    return caches, hbs, list(sc)

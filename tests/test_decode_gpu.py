@@ -237,4 +237,4 @@ def test_append_then_decode(cuda_device, schedule, monkeypatch):
         o_ref, lse_ref = okv.decode_heads(q.float().numpy().astype(np.float64), kk, vv, group)
         check_o_lse(o, lse, o_ref, lse_ref)
     assert np.array_equal(cache.sync_lengths(), np.array([len(x) for x in ks]))
-    assert int(cache.host["overflow_t"].item()) >= 2
+    assert int(cache.overflow_t.item()) >= 2

@@ -125,8 +125,8 @@ def test_layer_cache_tables_on_cpu():
                     (cache.seg_len, lens), (cache.seg_row0, row0), (cache.src_idx, np.arange(len(item_seg)))):
         np.testing.assert_array_equal(t.numpy(), want)
     assert cache.flags == flags and cache.n_workers == len(wptr) - 1
-    assert int(cache.counters.abs().sum()) == 0 and int(cache.host["overflow_t"][0]) == 0
-    np.testing.assert_array_equal(cache.host["seg_cap_t"].numpy(), C.page_rows(lens + 16))
+    assert int(cache.counters.abs().sum()) == 0 and int(cache.overflow_t[0]) == 0
+    np.testing.assert_array_equal(cache.seg_cap_t.numpy(), C.page_rows(lens + 16))
 
 
 def test_allocate_many_matches_allocate():
@@ -147,8 +147,25 @@ def test_allocate_many_matches_allocate():
                      "grp_ptr", "src_idx", "warp_ptr", "work_list", "work", "counters"):
             assert torch.equal(getattr(c, name), getattr(ref, name)), name
         for name in ("seg_cap_t", "append_src_t", "last_piece_t", "overflow_t"):
-            assert torch.equal(c.host[name], ref.host[name]), name
+            assert torch.equal(getattr(c, name), getattr(ref, name)), name
         assert c.k.shape == ref.k.shape and c.flags == ref.flags and c.n_workers == ref.n_workers
         assert c.k.is_contiguous() and int(c.k.abs().sum()) == 0
     for vw, e in zip(views, extra):
         np.testing.assert_array_equal(vw.numpy(), e)
+
+
+def test_allocate_many_grows_scratch_and_reports_errors():
+    """More tables than the planner scratch holds: it grows and the result is
+    unchanged; a stack with an unplannable layer raises the planner's error."""
+    import torch
+    rng = np.random.default_rng(5)
+    C._PLAN_SCRATCH.__dict__["many"] = np.empty(64, np.int32)  # force growth
+    layers = [(lens, np.arange(len(lens)) * 8, np.arange(len(lens)) * 8)
+              for lens in (_segments(rng, 300, 800) for _ in range(4))]
+    caches, _ = C.LayerCache.allocate_many(layers, 8, "cpu")
+    for c, (lens, q, o) in zip(caches, layers):
+        ref = C.LayerCache.allocate(lens, q, o, 8, "cpu")
+        assert torch.equal(c.work, ref.work) and torch.equal(c.grp_ptr, ref.grp_ptr)
+    bad = np.ones(148 * 8 * 32 + 5000, dtype=np.int64)
+    with pytest.raises(ValueError):
+        C.LayerCache.allocate_many([layers[0], (bad, np.zeros_like(bad), np.zeros_like(bad))], 8, "cpu")
