@@ -1014,9 +1014,11 @@ def prefill_compress(peaks):
                   "score_select_us": graph_us(lambda: ops.score_select(q, k, B, w, workspace=ws)),
                   "compact_us": graph_us(lambda: ops.compact_into(cache, k, v, off, idx, sbh, slo, shi, mx))}
         # a whole layer stack's compression (8 layers, host-visible wall time):
-        # per layer compress_layer (one host round trip per layer) vs
-        # compress_stack (all fused launches queued, one round trip, then
-        # every compaction)
+        # per layer compress_layer (the host waits for each layer's budgets
+        # before its compaction) vs compress_stack (all fused launches queued,
+        # each layer laid out as its budgets land in pinned host memory, one
+        # table copy, then every compaction); stack8_gpu_us_per_layer = the
+        # same layers' fused launches + compactions alone
         Ls = 8
 
         def per_layer():
@@ -1048,6 +1050,7 @@ def prefill_compress(peaks):
             "graph_replay": dev_us,
             "stack8_compress_layer_us_per_layer": t_pl * 1e6,
             "stack8_compress_stack_us_per_layer": t_st * 1e6,
+            "stack8_gpu_us_per_layer": dev_us["score_select_us"] + dev_us["compact_us"],
             # K1 is bound by the special-function unit, not the tensor cores:
             # two exponentials per (query row, key), at the measured ex2 rate
             "mufu_bound_us": exps / mufu_rate * 1e6,

@@ -369,21 +369,15 @@ def compact(k: torch.Tensor, v: torch.Tensor, offsets: torch.Tensor, idx: torch.
 def compress_layer(q_win: torch.Tensor, k: torch.Tensor, v: torch.Tensor, budget: int,
                    window: int = 32, alpha: float = 0.2, pool_k: int = 7):
     """Prefill of one layer on one GPU: K1 score + A18 budgets + K2 select
-    (one cooperative launch) -> K3 compact (TP=1 layout).  Returns (cache, head_budgets, scores).
-    The host reads the budgets back once to lay out the ragged cache."""
-    import numpy as np
-    bt, hq = q_win.shape[0], q_win.shape[1]
-    hkv = k.shape[1]
-    group = hq // hkv
-    sc, hb, offsets, idx = score_select(q_win, k, budget, window, alpha, pool_k)
-    hb_host = hb.cpu().numpy().reshape(-1)
-    bh = np.arange(bt * hkv)
-    qrow = (bh // hkv) * hq + (bh % hkv) * group
-    cache = compact(k, v, offsets, idx, bh, np.zeros_like(bh), hb_host, qrow, qrow, group)
-    return cache, hb, sc
+    (one cooperative launch) -> K3 compact (TP=1 layout).  Returns (cache,
+    head_budgets, scores).  The host needs the budgets to lay out the ragged
+    cache: the launch writes them to pinned host memory (compress_stack of
+    one layer); the same result as score_select followed by compact."""
+    caches, hbs, scs = compress_stack([q_win], [k], [v], budget, window, alpha, pool_k)
+    return caches[0], hbs[0], scs[0]
 
 
-def compress_stack(q_wins, ks, vs, budget: int, window: int = 32, alpha: float = 0.2, pool_k: int = 7):
+def compress_stack(q_wins, ks, vs, budget: int, window: int | None = 32, alpha: float = 0.2, pool_k: int = 7):
     """Prefill compression of a whole layer stack on one GPU without
     stalling the stream per layer: every layer's fused K1 + A18 + K2 launch
     is queued first (outputs of all layers in one allocation each, workspace
@@ -391,9 +385,9 @@ def compress_stack(q_wins, ks, vs, budget: int, window: int = 32, alpha: float =
     as soon as its launch ends, and the host lays out that layer's ragged
     cache (schedule + tables, fkv_cache_tables) while the GPU scores the
     next ones; then one K/V allocation and one host-to-device copy for the
-    whole stack and every layer's K3 compaction.  compress_layer per layer
-    instead stalls the stream once per layer (the host must know a layer's
-    budgets to lay out its cache).  q_wins / ks / vs: one tensor per layer,
+    whole stack and every layer's K3 compaction (compress_layer is the stack
+    of one layer: the host waits for that layer's budgets before laying out
+    its cache).  q_wins / ks / vs: one tensor per layer,
     shapes as compress_layer.  Returns ([cache], budgets int32 [L, Bt, Hkv]
     on the device, [scores])."""
     import numpy as np
@@ -404,6 +398,8 @@ def compress_stack(q_wins, ks, vs, budget: int, window: int = 32, alpha: float =
     hkv, T = ks[0].shape[1], ks[0].shape[2]
     group = hq // hkv
     dev = ks[0].device
+    if window is not None and window != w:
+        raise NativeError(f"window {window} != q_win.shape[2] {w}")
     for q, k, v in zip(q_wins, ks, vs):
         _need_cuda(q, k, v)
         if q.dtype != torch.bfloat16 or k.dtype != torch.bfloat16 or v.dtype != torch.bfloat16 \

@@ -221,8 +221,15 @@ def test_compress_stack_matches_per_layer(cuda_device, bt, T):
                                           [x[2] for x in layers], B)
     torch.cuda.synchronize()
     for l, (q, k, v) in enumerate(layers):
-        cache, hb, sc = ops.compress_layer(q, k, v, B)
+        # the composition of the public stages, one host round trip
+        sc, hb, offsets, idx = ops.score_select(q, k, B)
+        hb_host = hb.cpu().numpy().reshape(-1)
+        bh = np.arange(bt * hkv)
+        qrow = (bh // hkv) * hq + (bh % hkv) * (hq // hkv)
+        cache = ops.compact(k, v, offsets, idx, bh, np.zeros_like(bh), hb_host, qrow, qrow, hq // hkv)
         torch.cuda.synchronize()
+        one, hb1, sc1 = ops.compress_layer(q, k, v, B)
+        assert torch.equal(hb1, hb) and torch.equal(sc1, sc) and torch.equal(one.k, cache.k)
         assert torch.equal(hbs[l], hb) and torch.equal(scs[l], sc)
         assert torch.equal(caches[l].k, cache.k) and torch.equal(caches[l].v, cache.v)
         assert torch.equal(caches[l].work, cache.work)
