@@ -44,6 +44,7 @@ def segment_offsets(seg_len) -> tuple[np.ndarray, int]:
 
 MAX_ITEMS_PER_SEGMENT = 32  # FKV_MAX_PIECES (kMergeMax in decode.cu)
 MAX_WORK_PER_WORKER = 32    # FKV_MAX_WORK: descriptor entries per worker
+HYBRID_MIN_PIECE_TILES = 32  # whole-segment schedule: shortest piece a long segment is cut into
 TILE = 16
 
 
@@ -448,6 +449,41 @@ def plan_work_whole(seg_len, workers: int, sms: int):
     return item_seg, t0, t1, seg_item_ptr, warp_ptr, work_list
 
 
+def plan_work_hybrid(seg_len, workers: int):
+    """Whole segments, except that the longest are cut into equal pieces so
+    that no CTA streams more than T tiles, T the least (and >=
+    HYBRID_MIN_PIECE_TILES) with sum_s ceil(tiles_s / T) <= workers, one
+    piece per CTA: the longest segment no longer sets the launch's critical
+    path (a lone CTA streams it at one SM's bandwidth), and only the cut
+    segments need an LSE merge.  For at most `workers` segments (the SMs).
+    Same return convention as ``plan_work``."""
+    seg_len = np.asarray(seg_len, dtype=np.int64)
+    n = len(seg_len)
+    tiles = np.maximum((seg_len + TILE - 1) // TILE, 1)
+    hi = int(tiles.max()) if n else 1
+    lo = min(HYBRID_MIN_PIECE_TILES, hi)
+    while lo < hi:
+        T = (lo + hi) // 2
+        if int((-(-tiles // T)).sum()) <= workers:
+            hi = T
+        else:
+            lo = T + 1
+    k = np.minimum(-(-tiles // lo), MAX_ITEMS_PER_SEGMENT)
+    item_seg = np.repeat(np.arange(n), k).astype(np.int32)
+    ptr = np.zeros(n + 1, dtype=np.int64)
+    ptr[1:] = np.cumsum(k)
+    j = np.arange(ptr[-1]) - np.repeat(ptr[:-1], k)
+    kk = np.repeat(k, k)
+    tt = np.repeat(tiles, k)
+    t0 = (j * tt // kk) * TILE
+    t1 = np.minimum(((j + 1) * tt // kk) * TILE, np.repeat(seg_len, k))
+    t0 = np.minimum(t0, t1)
+    n_items = len(item_seg)
+    warp_ptr = np.arange(n_items + 1, dtype=np.int32)
+    return (item_seg, t0.astype(np.int32), t1.astype(np.int32), ptr.astype(np.int32), warp_ptr,
+            np.arange(n_items, dtype=np.int32))
+
+
 _DEVICE_SHAPES: dict = {}  # device index -> (SMs, CTAs per SM of coop / wide / solo)
 _PLAN_SCRATCH = __import__("threading").local()  # output buffers of fkv_plan_schedule, per thread
 
@@ -604,7 +640,10 @@ def plan_schedule_py(seg_len, seg_row0, seg_qrow, seg_out_row, device=None, chun
             whole == "1" or (whole is None and whole_segments_win(seg_tiles, workers, wide, sms))):
         # one whole segment per CTA: no split-segment LSE merges (their
         # record -> acq_rel counter -> L2 round trips sit in the launch's tail)
-        plan = plan_work_whole(seg_len, workers, sms)
+        if n_seg <= sms:  # one CTA per SM: the longest segments cut (few merges)
+            plan = plan_work_hybrid(seg_len, sms)
+        else:
+            plan = plan_work_whole(seg_len, workers, sms)
         tab = work_table(seg_row0, seg_len, seg_qrow, seg_out_row, *plan)
         return (*plan, tab, flags)
     plan = plan_work(seg_len, workers, chunk, sms=workers // ctas_sm if ctas_sm > 1 else None)

@@ -33,6 +33,7 @@ using V = std::vector<i64>;
 constexpr i64 kTile = 16;
 constexpr i64 kMaxItemsPerSegment = 32;  // FKV_MAX_PIECES
 constexpr i64 kMaxWork = 32;             // FKV_MAX_WORK
+constexpr i64 kHybridMinPieceTiles = 32;  // cache.py HYBRID_MIN_PIECE_TILES
 constexpr i64 kMinTilesPerWorker = 8;
 constexpr i64 kMaxPiecesPerSegment = 4;
 constexpr i64 kSoloMaxTilesPerCta = 19;
@@ -415,6 +416,39 @@ bool whole_segments_win(const V& seg_tiles, i64 workers, bool wide, i64 sms, dou
   return whole + kWholeMarginUs <= s0 + kSplitUsPerMb * mb;
 }
 
+// cache.py plan_work_hybrid: whole segments, the longest cut into equal
+// pieces of <= T tiles (T the least >= kHybridMinPieceTiles whose pieces fit
+// one per SM), one piece per CTA
+Plan plan_work_hybrid(const V& seg_len, i64 sms) {
+  const i64 n = static_cast<i64>(seg_len.size());
+  V tiles(n);
+  i64 hi = 1;
+  for (i64 s = 0; s < n; ++s) {
+    tiles[s] = std::max<i64>((seg_len[s] + kTile - 1) / kTile, 1);
+    hi = std::max(hi, tiles[s]);
+  }
+  i64 lo = std::min(kHybridMinPieceTiles, hi);
+  while (lo < hi) {
+    const i64 T = (lo + hi) / 2;
+    i64 pieces = 0;
+    for (i64 t : tiles) pieces += ceil_div(t, T);
+    if (pieces <= sms) hi = T;
+    else lo = T + 1;
+  }
+  V seg_i, t0, t1, owner;
+  for (i64 s = 0; s < n; ++s) {
+    const i64 k = std::min(ceil_div(tiles[s], lo), kMaxItemsPerSegment);
+    for (i64 j = 0; j < k; ++j) {
+      const i64 b = std::min((j + 1) * tiles[s] / k * kTile, seg_len[s]);
+      seg_i.push_back(s);
+      t0.push_back(std::min(j * tiles[s] / k * kTile, b));
+      t1.push_back(b);
+      owner.push_back(static_cast<i64>(owner.size()));
+    }
+  }
+  return finish(n, seg_i, t0, t1, owner, true);
+}
+
 // cache.py plan_work_whole
 Plan plan_work_whole(const V& seg_len, i64 workers, i64 sms, double pair_piece) {
   const i64 n = static_cast<i64>(seg_len.size());
@@ -519,7 +553,8 @@ int plan_schedule(const V& seg_len, const i64* seg_row0, const i64* seg_qrow, co
   const i64 sms_eff = workers / ctas_sm;
   if (prm.chunk <= 0 && n_seg > 0 && n_seg <= workers * kMaxWork &&
       (prm.whole == 1 || (prm.whole < 0 && whole_segments_win(seg_tiles, workers, wide, sms_eff, prm.pair_piece)))) {
-    plan = plan_work_whole(seg_len, workers, sms_eff, prm.pair_piece);
+    plan = n_seg <= sms_eff ? plan_work_hybrid(seg_len, sms_eff)  // one CTA per SM: longest segments cut
+                            : plan_work_whole(seg_len, workers, sms_eff, prm.pair_piece);
     work_table(seg_row0, seg_len, seg_qrow, seg_out_row, plan, 0, tab, rows, K);
     return 0;
   }

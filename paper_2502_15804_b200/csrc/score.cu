@@ -56,7 +56,7 @@ constexpr int kTmaWarp = kEpiWarps, kMmaWarp = kEpiWarps + 1;
 constexpr int kThreads = 32 * (kEpiWarps + 2);
 constexpr int kRawParts = 4;  // column partial sums per key written by pass 2 (one per column quarter)
 // the selection phase runs on epilogue warps 0-7 (named barrier 2)
-constexpr int kSelWarps = 8, kSelThreads = 32 * kSelWarps;
+constexpr int kSelWarps = 16, kSelThreads = 32 * kSelWarps;  // the selection: every epilogue warp
 constexpr float kLog2e = 1.4426950408889634f;
 
 struct ScoreParams {
@@ -324,16 +324,26 @@ __device__ __forceinline__ void warp_suffix8(const uint32_t* gh, int base, int (
 __device__ __forceinline__ void epi_histogram2(const float* sp, int nk, bool ga, uint32_t gp, uint32_t gm,
                                                bool fa, uint32_t fp, uint32_t fm, int shift, uint32_t* h0,
                                                uint32_t* h1) {
-  h0[threadIdx.x] = 0;
-  h1[threadIdx.x] = 0;
+  const int tid = threadIdx.x;
+  (tid < 256 ? h0 : h1)[tid & 255] = 0;
   sel_sync();
-#pragma unroll 4
-  for (int i = threadIdx.x; i < nk; i += kSelThreads) {
-    const uint32_t o = orderable(sp[i]);
+  auto add = [&](uint32_t o) {
     const uint32_t d = (o >> shift) & 255u;
     if (ga && (o & gm) == gp) atomicAdd(&h0[d], 1u);
     if (fa && (o & fm) == fp) atomicAdd(&h1[d], 1u);
+  };
+  // four keys per 16-byte shared load (the staged keys start 16-byte aligned)
+  const float4* s4 = reinterpret_cast<const float4*>(sp);
+  const int n4 = nk >> 2;
+#pragma unroll 2
+  for (int j = tid; j < n4; j += kSelThreads) {
+    const float4 v = s4[j];
+    add(orderable(v.x));
+    add(orderable(v.y));
+    add(orderable(v.z));
+    add(orderable(v.w));
   }
+  if (tid < (nk & 3)) add(orderable(sp[4 * n4 + tid]));
   sel_sync();
 }
 
@@ -381,9 +391,13 @@ __device__ void select_phase(const ScoreParams& p, Smem& sm, int b, int h, int b
     uint32_t* gh = p.hist + (static_cast<int64_t>(pass) * BH + bh) * 512;
     if (ga || fa) {  // add my keys' digit histograms to this pass's global ones
       epi_histogram2(sp, nk, ga, prefix, mask, fa && !same, x.fprefix, x.fmask, shift, x.hist, x.hist2);
-      if (ga && x.hist[tid]) atomicAdd(gh + tid, x.hist[tid]);
-      const uint32_t fc = same ? x.hist[tid] : (fa ? x.hist2[tid] : 0u);
-      if (fc) atomicAdd(gh + 256 + tid, fc);
+      if (tid < 256) {  // global histogram by threads 0..255, floor histogram by 256..511
+        if (ga && x.hist[tid]) atomicAdd(gh + tid, x.hist[tid]);
+      } else {
+        const int d = tid - 256;
+        const uint32_t fc = same ? x.hist[d] : (fa ? x.hist2[d] : 0u);
+        if (fc) atomicAdd(gh + 256 + d, fc);
+      }
     }
     sstamp(2 + 2 * pass);
     epi_grid_sync<2, kSelThreads>(p.gridbar, n_bar);  // fixed pass count: uniform across the grid
@@ -434,8 +448,9 @@ __device__ void select_phase(const ScoreParams& p, Smem& sm, int b, int h, int b
     sstamp(12 + 3 * pass);
     if (exact) continue;
     int32_t gd = 0;
-    for (int hh = 0; hh < HK; ++hh) gd += max(0, x.suf[hh][tid] - f);
-    const int32_t cnt = epi_count(gd >= R, x);
+    if (tid < 256)
+      for (int hh = 0; hh < HK; ++hh) gd += max(0, x.suf[hh][tid] - f);
+    const int32_t cnt = epi_count(tid < 256 && gd >= R, x);
     if (tid == cnt - 1) {
       x.dstar = cnt - 1;
       x.exact = gd == R;
@@ -508,24 +523,34 @@ __device__ void select_phase(const ScoreParams& p, Smem& sm, int b, int h, int b
     ktie = h < hstar ? 0x7fffffff : (h == hstar ? kstar : 0);
   }
   // class of key i: 1 = chosen outright, 2 = tie at thr taken by tie rank
-  auto klass = [&](int i) -> int {
+  auto klass = [&](uint32_t o) -> int {
     if (kind == 2) return 0;
-    const uint32_t o = orderable(sp[i]);
     if (kind == 1) return o >= thr;
     if (o != thr) return o > thr;
     return ktie == 0x7fffffff ? 1 : (ktie > 0 ? 2 : 0);
   };
-  // per-warp (chosen outright, ties) counts of contiguous key segments, kept
-  // in x.suf for the writes; the chunk's totals are published for the CTAs
-  // after it
-  const int seg = ((nk + kSelWarps - 1) / kSelWarps + 31) & ~31;
-  const int s0 = min(nk, wid * seg), s1 = min(nk, s0 + seg);
+  // per-warp (chosen outright, ties) counts of contiguous key segments (in
+  // 4-key units: 16-byte shared loads), kept in x.suf for the writes; the
+  // chunk's totals are published for the CTAs after it
+  const float4* s4 = reinterpret_cast<const float4*>(sp);
+  const int n4 = (nk + 3) >> 2, per4 = (n4 + kSelWarps - 1) / kSelWarps;
+  const int v0 = min(n4, wid * per4), v1 = min(n4, v0 + per4);
+  auto klass4 = [&](int j, int (&k)[4]) {  // unit j: keys 4j .. 4j+3 (those < nk)
+    const float4 v = s4[j];
+    const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int c = 0; c < 4; ++c) k[c] = 4 * j + c < nk ? klass(orderable(e[c])) : 0;
+  };
   int32_t c1 = 0, c2 = 0;
-#pragma unroll 4
-  for (int i = s0 + lane; i < s1; i += 32) {
-    const int k = klass(i);
-    c1 += k == 1;
-    c2 += k == 2;
+#pragma unroll 2
+  for (int j = v0 + lane; j < v1; j += 32) {
+    int k[4];
+    klass4(j, k);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      c1 += k[c] == 1;
+      c2 += k[c] == 2;
+    }
   }
   c1 = __reduce_add_sync(0xffffffffu, c1);
   c2 = __reduce_add_sync(0xffffffffu, c2);
@@ -565,17 +590,37 @@ __device__ void select_phase(const ScoreParams& p, Smem& sm, int b, int h, int b
   for (int j = 0; j < wid; ++j) c1b += x.suf[0][j], tb += x.suf[1][j];
   int tie_run = tie0 + tb;  // tie rank of the warp's next tie in token order
   pos += c1b + min(tie_run, ktie);
-  const uint32_t lt = (1u << lane) - 1u;
-#pragma unroll 4
-  for (int base = s0; base < s1; base += 32) {  // no block barriers: each warp writes its own segment
-    const int i = base + lane;
-    const int k = i < s1 ? klass(i) : 0;
-    const uint32_t ties = __ballot_sync(0xffffffffu, k == 2);
-    const bool take = k == 1 || (k == 2 && tie_run + __popc(ties & lt) < ktie);
-    const uint32_t bal = __ballot_sync(0xffffffffu, take);
-    if (take) out[pos + __popc(bal & lt)] = t_beg + i;
-    pos += __popc(bal);
-    tie_run += __popc(ties);
+  auto warp_excl = [&](int v, int& total) {  // exclusive prefix over lanes
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    total = __shfl_sync(0xffffffffu, incl, 31);
+    return incl - v;
+  };
+  // no block barriers: each warp writes its own segment, 4 keys per lane
+  for (int jb = v0; jb < v1; jb += 32) {
+    const int j = jb + lane;
+    int k[4] = {0, 0, 0, 0};
+    if (j < v1) klass4(j, k);
+    int t_all, n_all;
+    int tr = tie_run + warp_excl((k[0] == 2) + (k[1] == 2) + (k[2] == 2) + (k[3] == 2), t_all);
+    bool tk[4];
+    int nt = 0;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      tk[c] = k[c] == 1;
+      if (k[c] == 2) tk[c] = tr++ < ktie;
+      nt += tk[c];
+    }
+    int64_t q = pos + warp_excl(nt, n_all);
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      if (tk[c]) out[q++] = t_beg + 4 * j + c;
+    pos += n_all;
+    tie_run += t_all;
   }
   sstamp(33);
   if (chunk == 0) {

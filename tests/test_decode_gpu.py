@@ -96,11 +96,13 @@ def test_decode_many_segments_split(cuda_device, schedule, monkeypatch):
 
 @pytest.mark.parametrize("schedule,bt", [("wide", 8), ("coop", 8), ("coop", 24)])
 def test_decode_whole_segment_schedule(cuda_device, schedule, bt, monkeypatch):
-    """One whole segment per CTA (no split-segment merges; every CTA's only
-    piece is combined by all its warps); bt=24 under coop puts 192 segments on
-    148 SMs: the longest get an SM alone, the rest pair longest with shortest."""
+    """Whole-segment schedule: up to one segment per SM, the longest cut into
+    equal pieces (>= 32 tiles) so that every piece has an SM of its own
+    (only those segments merge); bt=24 under coop puts 192 segments on 148
+    SMs: no segment is split, the longest get an SM alone, the rest pair
+    longest with shortest.  Every CTA's pieces are combined by all its warps."""
     from paper_2502_15804_b200 import ops
-    from paper_2502_15804_b200.cache import NUM_SMS, _whole_owners
+    from paper_2502_15804_b200.cache import NUM_SMS, _whole_owners, plan_work_hybrid
     monkeypatch.setenv("FKV_K4_SCHEDULE", schedule)
     monkeypatch.setenv("FKV_K4_WHOLE", "1")
     rng = np.random.default_rng(bt)
@@ -108,7 +110,15 @@ def test_decode_whole_segment_schedule(cuda_device, schedule, bt, monkeypatch):
     seg_lens = rng.integers(0, 900, size=bt * hkv).tolist()
     seg_lens[:4] = [0, 1, 16, 17]
     cache, q, ks, vs = build_cache(seg_lens, group, hkv, bt, cuda_device, seed=bt)
-    assert int(np.diff(cache.grp_ptr.cpu().numpy()).max()) == 1  # no segment is split
+    ptr = cache.grp_ptr.cpu().numpy()
+    if len(seg_lens) <= NUM_SMS:  # one piece per CTA, the longest segments cut
+        want = plan_work_hybrid(np.asarray(seg_lens), NUM_SMS)
+        np.testing.assert_array_equal(ptr, want[3])
+        np.testing.assert_array_equal(cache.item_t1.cpu().numpy(), want[2])
+        assert int(np.diff(ptr).max()) > 1 and len(want[0]) <= NUM_SMS
+        assert int(np.diff(cache.warp_ptr.cpu().numpy()).max()) == 1
+    else:
+        assert int(np.diff(ptr).max()) == 1  # no segment is split
     assert cache.flags == {"coop": 0, "wide": 2}[schedule]
     o, lse = ops.decode(q.to(cuda_device), cache)
     torch.cuda.synchronize()
