@@ -146,7 +146,7 @@ typedef struct fkv_work {
  * count and fkv_decode_ctas_per_sm() of each shape; the remaining fields are
  * the planner's tuning knobs (cache.py: FKV_K4_SCHEDULE, FKV_K4_WHOLE,
  * FKV_SOLO_SMALL, FKV_SOLO_PIECE, FKV_SOLO_WHOLE, FKV_PIECE_COST,
- * FKV_PAIR_PIECE, FKV_SM_PAIRING; chunk <= 0: none). */
+ * FKV_PAIR_PIECE, FKV_SM_PAIRING, FKV_HYBRID_SAVING; chunk <= 0: none). */
 typedef struct {
   int32_t sms, ctas_coop, ctas_wide, ctas_solo;
   int32_t mode;                  /* 0 auto, 1 coop, 2 wide, 3 solo */
@@ -154,6 +154,7 @@ typedef struct {
   int32_t solo_small, solo_piece, solo_whole;  /* solo_piece / solo_whole: -1 = default */
   int32_t piece_cost, sm_pairing, chunk;
   double pair_piece;
+  double hybrid_saving_us;       /* cut a whole-schedule segment only when that saves more (us) */
 } fkv_sched_params;
 
 /* Outputs (int32): item_seg / item_t0 / item_t1 / work_list [n_items],

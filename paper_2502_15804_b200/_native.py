@@ -50,7 +50,7 @@ class SchedParams(C.Structure):
     """fkv_sched_params (include/fairkv.h)."""
     _fields_ = [(n, C.c_int32) for n in ("sms", "ctas_coop", "ctas_wide", "ctas_solo", "mode", "whole",
                                          "solo_small", "solo_piece", "solo_whole", "piece_cost",
-                                         "sm_pairing", "chunk")] + [("pair_piece", C.c_double)]
+                                         "sm_pairing", "chunk")] + [("pair_piece", C.c_double), ("hybrid_saving_us", C.c_double)]
 _pi32, _pi64, _pf64 = C.POINTER(_i32), C.POINTER(_i64), C.POINTER(_f64)
 
 _SIGS = {

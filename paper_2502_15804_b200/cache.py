@@ -45,6 +45,8 @@ def segment_offsets(seg_len) -> tuple[np.ndarray, int]:
 MAX_ITEMS_PER_SEGMENT = 32  # FKV_MAX_PIECES (kMergeMax in decode.cu)
 MAX_WORK_PER_WORKER = 32    # FKV_MAX_WORK: descriptor entries per worker
 HYBRID_MIN_PIECE_TILES = 32  # whole-segment schedule: shortest piece a long segment is cut into
+HYBRID_MIN_SAVING_US = 1.0   # ... and only when the critical path shrinks by more than this (merge cost)
+HYBRID_LONE_TILE_US = 0.045  # per-tile time of a lone streaming CTA (<= 32 segments busy)
 TILE = 16
 
 
@@ -449,18 +451,20 @@ def plan_work_whole(seg_len, workers: int, sms: int):
     return item_seg, t0, t1, seg_item_ptr, warp_ptr, work_list
 
 
-def plan_work_hybrid(seg_len, workers: int):
+def plan_work_hybrid(seg_len, workers: int, per_tile_us: float = 1.0, min_saving_us: float = 0.0):
     """Whole segments, except that the longest are cut into equal pieces so
     that no CTA streams more than T tiles, T the least (and >=
     HYBRID_MIN_PIECE_TILES) with sum_s ceil(tiles_s / T) <= workers, one
     piece per CTA: the longest segment no longer sets the launch's critical
     path (a lone CTA streams it at one SM's bandwidth), and only the cut
-    segments need an LSE merge.  For at most `workers` segments (the SMs).
-    Same return convention as ``plan_work``."""
+    segments need an LSE merge.  The cut is kept only if it shortens the
+    critical path by more than ``min_saving_us`` at ``per_tile_us`` per tile
+    (the merges' cost).  For at most `workers` segments (the SMs).  Same
+    return convention as ``plan_work``."""
     seg_len = np.asarray(seg_len, dtype=np.int64)
     n = len(seg_len)
     tiles = np.maximum((seg_len + TILE - 1) // TILE, 1)
-    hi = int(tiles.max()) if n else 1
+    hi = longest = int(tiles.max()) if n else 1
     lo = min(HYBRID_MIN_PIECE_TILES, hi)
     while lo < hi:
         T = (lo + hi) // 2
@@ -468,6 +472,8 @@ def plan_work_hybrid(seg_len, workers: int):
             hi = T
         else:
             lo = T + 1
+    if per_tile_us * (longest - lo) <= min_saving_us:
+        lo = longest  # the cut would not pay for its merges: whole segments
     k = np.minimum(-(-tiles // lo), MAX_ITEMS_PER_SEGMENT)
     item_seg = np.repeat(np.arange(n), k).astype(np.int32)
     ptr = np.zeros(n + 1, dtype=np.int64)
@@ -506,7 +512,7 @@ def _device_shapes(device):
 
 
 _SCHED_ENV = ("FKV_K4_SCHEDULE", "FKV_K4_WHOLE", "FKV_SOLO_SMALL", "FKV_SOLO_PIECE", "FKV_SOLO_WHOLE",
-              "FKV_PIECE_COST", "FKV_SM_PAIRING", "FKV_PAIR_PIECE")
+              "FKV_PIECE_COST", "FKV_SM_PAIRING", "FKV_PAIR_PIECE", "FKV_HYBRID_SAVING")
 _SCHED_PARAMS: dict = {}  # (device, chunk, planner environment) -> (fkv_sched_params, SMs)
 
 
@@ -533,7 +539,8 @@ def _sched_params(device, chunk):
         piece_cost=int(env.get("FKV_PIECE_COST", PIECE_COST_TILES)),
         sm_pairing=int(env.get("FKV_SM_PAIRING", "1") == "1"),
         chunk=-1 if chunk is None else int(chunk),
-        pair_piece=float(env.get("FKV_PAIR_PIECE", PAIR_PIECE_TILES)))
+        pair_piece=float(env.get("FKV_PAIR_PIECE", PAIR_PIECE_TILES)),
+        hybrid_saving_us=float(env.get("FKV_HYBRID_SAVING", HYBRID_MIN_SAVING_US)))
     if len(_SCHED_PARAMS) > 64:
         _SCHED_PARAMS.clear()
     _SCHED_PARAMS[key] = hit = (C.byref(prm), sms)
@@ -641,7 +648,9 @@ def plan_schedule_py(seg_len, seg_row0, seg_qrow, seg_out_row, device=None, chun
         # one whole segment per CTA: no split-segment LSE merges (their
         # record -> acq_rel counter -> L2 round trips sit in the launch's tail)
         if n_seg <= sms:  # one CTA per SM: the longest segments cut (few merges)
-            plan = plan_work_hybrid(seg_len, sms)
+            per_tile = HYBRID_LONE_TILE_US if n_seg <= 32 else WHOLE_MODEL["wide" if wide else "coop"][2]
+            plan = plan_work_hybrid(seg_len, sms, per_tile,
+                                    float(os.environ.get("FKV_HYBRID_SAVING", HYBRID_MIN_SAVING_US)))
         else:
             plan = plan_work_whole(seg_len, workers, sms)
         tab = work_table(seg_row0, seg_len, seg_qrow, seg_out_row, *plan)

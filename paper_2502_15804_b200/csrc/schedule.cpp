@@ -34,6 +34,7 @@ constexpr i64 kTile = 16;
 constexpr i64 kMaxItemsPerSegment = 32;  // FKV_MAX_PIECES
 constexpr i64 kMaxWork = 32;             // FKV_MAX_WORK
 constexpr i64 kHybridMinPieceTiles = 32;  // cache.py HYBRID_MIN_PIECE_TILES
+constexpr double kHybridLoneTileUs = 0.045;  // cache.py HYBRID_LONE_TILE_US
 constexpr i64 kMinTilesPerWorker = 8;
 constexpr i64 kMaxPiecesPerSegment = 4;
 constexpr i64 kSoloMaxTilesPerCta = 19;
@@ -419,7 +420,7 @@ bool whole_segments_win(const V& seg_tiles, i64 workers, bool wide, i64 sms, dou
 // cache.py plan_work_hybrid: whole segments, the longest cut into equal
 // pieces of <= T tiles (T the least >= kHybridMinPieceTiles whose pieces fit
 // one per SM), one piece per CTA
-Plan plan_work_hybrid(const V& seg_len, i64 sms) {
+Plan plan_work_hybrid(const V& seg_len, i64 sms, double per_tile_us, double min_saving_us) {
   const i64 n = static_cast<i64>(seg_len.size());
   V tiles(n);
   i64 hi = 1;
@@ -427,6 +428,7 @@ Plan plan_work_hybrid(const V& seg_len, i64 sms) {
     tiles[s] = std::max<i64>((seg_len[s] + kTile - 1) / kTile, 1);
     hi = std::max(hi, tiles[s]);
   }
+  const i64 longest = hi;
   i64 lo = std::min(kHybridMinPieceTiles, hi);
   while (lo < hi) {
     const i64 T = (lo + hi) / 2;
@@ -435,6 +437,7 @@ Plan plan_work_hybrid(const V& seg_len, i64 sms) {
     if (pieces <= sms) hi = T;
     else lo = T + 1;
   }
+  if (per_tile_us * static_cast<double>(longest - lo) <= min_saving_us) lo = longest;  // not worth its merges
   V seg_i, t0, t1, owner;
   for (i64 s = 0; s < n; ++s) {
     const i64 k = std::min(ceil_div(tiles[s], lo), kMaxItemsPerSegment);
@@ -553,7 +556,9 @@ int plan_schedule(const V& seg_len, const i64* seg_row0, const i64* seg_qrow, co
   const i64 sms_eff = workers / ctas_sm;
   if (prm.chunk <= 0 && n_seg > 0 && n_seg <= workers * kMaxWork &&
       (prm.whole == 1 || (prm.whole < 0 && whole_segments_win(seg_tiles, workers, wide, sms_eff, prm.pair_piece)))) {
-    plan = n_seg <= sms_eff ? plan_work_hybrid(seg_len, sms_eff)  // one CTA per SM: longest segments cut
+    // one CTA per SM: the longest segments cut when that pays for the merges
+    const double per_tile = n_seg <= 32 ? kHybridLoneTileUs : (wide ? 0.104 : 0.285);  // WHOLE_MODEL
+    plan = n_seg <= sms_eff ? plan_work_hybrid(seg_len, sms_eff, per_tile, prm.hybrid_saving_us)
                             : plan_work_whole(seg_len, workers, sms_eff, prm.pair_piece);
     work_table(seg_row0, seg_len, seg_qrow, seg_out_row, plan, 0, tab, rows, K);
     return 0;

@@ -451,5 +451,8 @@ def compress_stack(q_wins, ks, vs, budget: int, window: int | None = 32, alpha: 
         _native.check(_lib.fkv_compact(k.data_ptr(), v.data_ptr(), T, BH, p_off + l * s_off, p_idx + l * s_idx,
                                        p_bh, p_lo, p_hi + 4 * l * BH, cache.ptr(16), 1,
                                        int(lens[l].max()), cache.k.data_ptr(), cache.v.data_ptr(), stream))
-        cache.host["compact_args"] = (seg_bh, seg_hi, offsets, idx)  # alive until the stream consumes them
+        # the compaction's segment tables (compact_into's arguments), and its
+        # selection alive until the stream consumes it
+        cache.host["compact_args"] = (seg_bh, seg_lo, seg_hi[l * BH:(l + 1) * BH])
+        cache.host["selection"] = (offsets, idx)
     return caches, hbs, list(sc)

@@ -102,7 +102,8 @@ def test_decode_whole_segment_schedule(cuda_device, schedule, bt, monkeypatch):
     SMs: no segment is split, the longest get an SM alone, the rest pair
     longest with shortest.  Every CTA's pieces are combined by all its warps."""
     from paper_2502_15804_b200 import ops
-    from paper_2502_15804_b200.cache import NUM_SMS, _whole_owners, plan_work_hybrid
+    from paper_2502_15804_b200.cache import (HYBRID_MIN_SAVING_US, NUM_SMS, WHOLE_MODEL, _whole_owners,
+                                             plan_work_hybrid)
     monkeypatch.setenv("FKV_K4_SCHEDULE", schedule)
     monkeypatch.setenv("FKV_K4_WHOLE", "1")
     rng = np.random.default_rng(bt)
@@ -112,7 +113,7 @@ def test_decode_whole_segment_schedule(cuda_device, schedule, bt, monkeypatch):
     cache, q, ks, vs = build_cache(seg_lens, group, hkv, bt, cuda_device, seed=bt)
     ptr = cache.grp_ptr.cpu().numpy()
     if len(seg_lens) <= NUM_SMS:  # one piece per CTA, the longest segments cut
-        want = plan_work_hybrid(np.asarray(seg_lens), NUM_SMS)
+        want = plan_work_hybrid(np.asarray(seg_lens), NUM_SMS, WHOLE_MODEL[schedule][2], HYBRID_MIN_SAVING_US)
         np.testing.assert_array_equal(ptr, want[3])
         np.testing.assert_array_equal(cache.item_t1.cpu().numpy(), want[2])
         assert int(np.diff(ptr).max()) > 1 and len(want[0]) <= NUM_SMS
