@@ -47,6 +47,7 @@ MAX_WORK_PER_WORKER = 32    # FKV_MAX_WORK: descriptor entries per worker
 HYBRID_MIN_PIECE_TILES = 32  # whole-segment schedule: shortest piece a long segment is cut into
 HYBRID_MIN_SAVING_US = 1.0   # ... and only when the critical path shrinks by more than this (merge cost)
 HYBRID_LONE_TILE_US = 0.045  # per-tile time of a lone streaming CTA (<= 32 segments busy)
+LONE_PREFETCH_TILES = 28     # tiles a wide CTA's rings hold at once (7 streaming warps x 4 stages)
 TILE = 16
 
 
@@ -426,6 +427,10 @@ def whole_segments_win(seg_tiles, workers: int, wide: bool, sms: int = NUM_SMS) 
     s0, w0, per_tile = WHOLE_MODEL["wide" if wide else "coop"]
     if not wide and n >= 2 * workers:
         per_tile = WHOLE_FULL_PER_TILE_US
+    if wide and n <= 32 and int(seg_tiles.max()) <= LONE_PREFETCH_TILES:
+        # a few short segments: each CTA streams alone and its ring holds the
+        # whole segment (Llama-3.1-8B shape at batch 1), tiles are cheap
+        per_tile = HYBRID_LONE_TILE_US
     mb = float(seg_tiles.sum()) * TILE * HEAD_DIM * 4 / 1e6
     crit = float(_whole_cta_tiles(seg_tiles, _whole_owners(seg_tiles, workers, sms)).max())
     whole = w0 + max(per_tile * crit, WHOLE_US_PER_MB * mb)

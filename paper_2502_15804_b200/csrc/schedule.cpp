@@ -35,6 +35,7 @@ constexpr i64 kMaxItemsPerSegment = 32;  // FKV_MAX_PIECES
 constexpr i64 kMaxWork = 32;             // FKV_MAX_WORK
 constexpr i64 kHybridMinPieceTiles = 32;  // cache.py HYBRID_MIN_PIECE_TILES
 constexpr double kHybridLoneTileUs = 0.045;  // cache.py HYBRID_LONE_TILE_US
+constexpr i64 kLonePrefetchTiles = 28;       // cache.py LONE_PREFETCH_TILES
 constexpr i64 kMinTilesPerWorker = 8;
 constexpr i64 kMaxPiecesPerSegment = 4;
 constexpr i64 kSoloMaxTilesPerCta = 19;
@@ -401,7 +402,9 @@ bool whole_segments_win(const V& seg_tiles, i64 workers, bool wide, i64 sms, dou
   const i64 n = static_cast<i64>(seg_tiles.size());
   if (!n || n > workers * kMaxWork) return false;
   const double s0 = wide ? 5.6 : 7.6, w0 = wide ? 3.3 : 2.6;
-  const double per_tile = (!wide && n >= 2 * workers) ? kWholeFullPerTileUs : (wide ? 0.104 : 0.285);
+  double per_tile = (!wide && n >= 2 * workers) ? kWholeFullPerTileUs : (wide ? 0.104 : 0.285);
+  if (wide && n <= 32 && *std::max_element(seg_tiles.begin(), seg_tiles.end()) <= kLonePrefetchTiles)
+    per_tile = kHybridLoneTileUs;  // a few short segments, each held whole by its CTA's rings
   i64 tsum = 0;
   for (i64 t : seg_tiles) tsum += t;
   const double mb = static_cast<double>(tsum) * kTile * FKV_HEAD_DIM * 4 / 1e6;
