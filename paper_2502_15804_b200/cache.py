@@ -45,7 +45,7 @@ def segment_offsets(seg_len) -> tuple[np.ndarray, int]:
 MAX_ITEMS_PER_SEGMENT = 32  # FKV_MAX_PIECES (kMergeMax in decode.cu)
 MAX_WORK_PER_WORKER = 32    # FKV_MAX_WORK: descriptor entries per worker
 HYBRID_MIN_PIECE_TILES = 32  # whole-segment schedule: shortest piece a long segment is cut into
-HYBRID_MIN_SAVING_US = 1.0   # ... and only when the critical path shrinks by more than this (merge cost)
+HYBRID_MIN_SAVING_US = 0.5   # ... and only when the modelled critical path shrinks by more than this
 HYBRID_LONE_TILE_US = 0.045  # per-tile time of a lone streaming CTA (<= 32 segments busy)
 LONE_PREFETCH_TILES = 28     # tiles a wide CTA's rings hold at once (7 streaming warps x 4 stages)
 TILE = 16
