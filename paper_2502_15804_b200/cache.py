@@ -362,6 +362,12 @@ FKV_DECODE_WIDE = 2
 FKV_DECODE_AFTER_WAIT = 4
 WIDE_MAX_SEGMENTS = 128
 WIDE_MIN_MEAN_TILES = 6  # probe_sched: wide wins from ~6 tiles per segment (TP=8 B=128 SHA), coop below (its AHA-DP copies, ~4)
+# long segments (>= 40 tiles on average, up to 384 of them: TP=2/4 shards at
+# B=1024) also stream faster on the wide shape, whole and packed
+# longest-first (tools/probe_wide.py: TP=2 27.4 -> 24.7 us, TP=4 AHA-DP 17.1
+# -> 15.8); a TP=1 layer (512 segments) stays on the 4-warp shape
+WIDE_LONG_MAX_SEGMENTS = 384
+WIDE_LONG_MIN_MEAN_TILES = 40
 
 
 # Whole-segment schedule (one segment per CTA, no splits) vs the equal-cost
@@ -603,8 +609,9 @@ def plan_schedule_py(seg_len, seg_row0, seg_qrow, seg_out_row, device=None, chun
       to the solo schedule with 4-8-tile pieces (the choice before the
       piece-cost planner).
     * few segments of >= WIDE_MIN_MEAN_TILES tiles on average (<= WIDE_MAX_SEGMENTS, e.g. a TP=4/8
-      rank's KV heads): the cooperative schedule with 8-warp CTAs (one per
-      SM, seven streaming warps per piece).
+      rank's KV heads), or up to WIDE_LONG_MAX_SEGMENTS long ones (>=
+      WIDE_LONG_MIN_MEAN_TILES, TP=2/4 shards at B=1024): the cooperative
+      schedule with 8-warp CTAs (one per SM, seven streaming warps per piece).
     * cooperative schedules: one whole segment per CTA instead of the split
       cut when the model in ``whole_segments_win`` says the saved merge tail
       outweighs the longer critical segment (small TP shards).
@@ -642,7 +649,9 @@ def plan_schedule_py(seg_len, seg_row0, seg_qrow, seg_out_row, device=None, chun
             pass  # too many pieces for the per-CTA tables: cooperative schedule
     # few segments (a TP-sharded rank's cache): 8-warp CTAs, seven streams per
     # piece; otherwise 4-warp CTAs, two per SM (tools/probe_sched.py)
-    wide = mode == "wide" or (mode != "coop" and n_seg <= WIDE_MAX_SEGMENTS and mean >= WIDE_MIN_MEAN_TILES)
+    wide = mode == "wide" or (mode != "coop" and (
+        (n_seg <= WIDE_MAX_SEGMENTS and mean >= WIDE_MIN_MEAN_TILES)
+        or (n_seg <= WIDE_LONG_MAX_SEGMENTS and mean >= WIDE_LONG_MIN_MEAN_TILES)))
     flags = FKV_DECODE_WIDE if wide else 0
     workers = default_workers(device, flags)
     ctas_sm = max(1, workers // default_workers(device, FKV_DECODE_WIDE))

@@ -41,6 +41,8 @@ constexpr i64 kMaxPiecesPerSegment = 4;
 constexpr i64 kSoloMaxTilesPerCta = 19;
 constexpr i64 kWideMaxSegments = 128;
 constexpr i64 kWideMinMeanTiles = 6;
+constexpr i64 kWideLongMaxSegments = 384;  // cache.py WIDE_LONG_MAX_SEGMENTS
+constexpr i64 kWideLongMinMeanTiles = 40;  // cache.py WIDE_LONG_MIN_MEAN_TILES
 constexpr i64 kPairPieceTilesWhole = 12;  // PAIR_PIECE_TILES in _whole_owners / _whole_cta_tiles
 constexpr double kSplitUsPerMb = 0.165, kWholeMarginUs = 0.5, kWholeUsPerMb = 0.161;
 constexpr double kWholeFullPerTileUs = 0.20;  // cache.py WHOLE_FULL_PER_TILE_US
@@ -552,7 +554,8 @@ int plan_schedule(const V& seg_len, const i64* seg_row0, const i64* seg_qrow, co
       // too many pieces for the per-CTA tables: cooperative schedule
     }
   }
-  const bool wide = mode == 2 || (mode != 1 && n_seg <= kWideMaxSegments && mean >= kWideMinMeanTiles);
+  const bool wide = mode == 2 || (mode != 1 && ((n_seg <= kWideMaxSegments && mean >= kWideMinMeanTiles) ||
+                                                 (n_seg <= kWideLongMaxSegments && mean >= kWideLongMinMeanTiles)));
   flags = wide ? FKV_DECODE_WIDE : 0;
   const i64 workers = sms * (wide ? prm.ctas_wide : prm.ctas_coop);
   const i64 ctas_sm = std::max<i64>(1, workers / (sms * prm.ctas_wide));
