@@ -432,9 +432,25 @@ def run_fairkv(args):
     qh.copy_(q)
     oh = torch.empty(o.shape, dtype=o.dtype, pin_memory=True)
     s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
-    cg = int(os.environ.get("FKV_E2E_GROUP", "4"))  # layers per copy (measured best of 1-40)
-    cuts = sorted({0, min(1, args.layers), max(args.layers - 1, 0), args.layers,
-                   *range(1, args.layers - 1, cg)})
+    # layers per copy group: "sym" (default; 17.4k -> 17.8k tokens/s against
+    # uniform groups of 4, the best of 1-40) or a fixed group size
+    cg = os.environ.get("FKV_E2E_GROUP", "sym")
+    if cg.startswith("sym"):
+        # copy groups growing geometrically from each end (1, 2, 4, ...
+        # layers): the first upload and the last download stay short, and the
+        # middle needs few event nodes (each one breaks the layers'
+        # programmatic-launch chain); "sym:<first>:<factor>"
+        w0, fac = (int(x) for x in (cg.split(":")[1:] + ["1", "2"])[:2]) if ":" in cg else (1, 2)
+        cuts, a, b, w = {0, args.layers}, 0, args.layers, w0
+        while a < b:
+            a, b = min(a + w, b), max(b - w, a)
+            cuts |= {a, b}
+            w *= fac
+        cuts = sorted(cuts)
+    else:
+        cg = int(cg)
+        cuts = sorted({0, min(1, args.layers), max(args.layers - 1, 0), args.layers,
+                       *range(1, args.layers - 1, cg)})
     groups = [(a, b) for a, b in zip(cuts, cuts[1:]) if b > a]
     ev_in = [torch.cuda.Event() for _ in groups]
     ev_out = [torch.cuda.Event() for _ in groups]
