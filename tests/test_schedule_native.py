@@ -169,3 +169,34 @@ def test_allocate_many_grows_scratch_and_reports_errors():
     bad = np.ones(148 * 8 * 32 + 5000, dtype=np.int64)
     with pytest.raises(ValueError):
         C.LayerCache.allocate_many([layers[0], (bad, np.zeros_like(bad), np.zeros_like(bad))], 8, "cpu")
+
+
+def test_schedule_shape_rules(monkeypatch):
+    """The CTA-shape / whole-segment rules, identically in both planners:
+    a few short segments that fit a wide CTA's rings -> wide, whole (8B
+    batch 1); up to 384 long segments -> wide (TP=2/4 shards at B=1024); a
+    TP=1 layer of 512 long segments -> the 4-warp shape; at most one
+    segment per SM with a dominant one -> the long one is cut."""
+    rng = np.random.default_rng(3)
+    short = rng.integers(200, 300, 8)                 # 8 segments of ~16 tiles
+    assert _check(short) == C.FKV_DECODE_WIDE
+    row0, _ = C.segment_offsets(short)
+    q = np.arange(8, dtype=np.int64)
+    plan = C.plan_schedule(short, row0, q, q)
+    assert len(plan[0]) == 8                          # whole: one piece per segment
+    long_ = rng.integers(700, 1400, 256)              # 256 segments of ~65 tiles
+    assert _check(long_) == C.FKV_DECODE_WIDE
+    tp1 = rng.integers(700, 1400, 512)
+    assert _check(tp1) == 0
+    # whole-segment schedule, at most one segment per SM: the longest are cut
+    # into equal pieces, one per SM, the dominant one most
+    monkeypatch.setenv("FKV_K4_WHOLE", "1")
+    cut = np.concatenate([rng.integers(600, 700, 120), [3000]])
+    assert _check(cut) == C.FKV_DECODE_WIDE
+    row0, _ = C.segment_offsets(cut)
+    q = np.arange(len(cut), dtype=np.int64)
+    item_seg, t0, t1, _, warp_ptr = C.plan_schedule(cut, row0, q, q)[:5]
+    per_seg = np.bincount(item_seg)
+    assert per_seg[-1] == per_seg.max() > 2 and len(item_seg) <= C.NUM_SMS
+    assert (np.diff(warp_ptr) == 1).all()             # one piece per CTA
+    assert (t1 - t0).max() <= 3000 // 2
