@@ -346,3 +346,19 @@ def test_fused_score_select_bit_exact(cuda_device, bt, hq, hkv, T, budget, temp,
     sc2, hb2, off2, idx2 = ops.score_select(q, k, budget, 32)
     torch.cuda.synchronize()
     assert torch.equal(idx2, idx) and torch.equal(hb2, hb)
+
+
+def test_compress_stack_rejects_bad_inputs(cuda_device):
+    """compress_stack validates every layer before queueing anything: a
+    missing tensor, a layer of another shape, a window that is not q_win's."""
+    from paper_2502_15804_b200 import ops
+    from paper_2502_15804_b200.errors import NativeError
+    q, k, v = _inputs(1, 32, 8, 600, 32, 3, cuda_device)[:3]
+    with pytest.raises(NativeError):
+        ops.compress_stack([q], [k], [], 256)
+    with pytest.raises(NativeError):
+        ops.compress_stack([q, q], [k, k[:, :, :-16].contiguous()], [v, v[:, :, :-16].contiguous()], 256)
+    with pytest.raises(NativeError):
+        ops.compress_stack([q], [k], [v.float()], 256)
+    with pytest.raises(NativeError):
+        ops.compress_stack([q], [k], [v], 256, window=16)
