@@ -293,6 +293,10 @@ int fkv_ipc_get(void* dev_ptr, void* handle /* 64 bytes */);
 int fkv_ipc_open(const void* handle, void** out_ptr);
 int fkv_ipc_close(void* ptr);
 
+/* Device address of pinned host memory (a kernel output the host reads
+ * without a copy, e.g. fkv_snapkv_select's budgets). */
+int fkv_host_device_ptr(void* host_ptr, void** out_ptr);
+
 /* ------------------------------------------- B3 compression (prefill) -- */
 
 /* K1: Ada-SnapKV observation-window scores (two tcgen05/TMEM/TMA passes +

@@ -78,6 +78,7 @@ _SIGS = {
     "fkv_ipc_get": (C.c_int, [_vp, _vp]),
     "fkv_ipc_open": (C.c_int, [_vp, _vp]),
     "fkv_ipc_close": (C.c_int, [_vp]),
+    "fkv_host_device_ptr": (C.c_int, [_vp, _vp]),
     "fkv_snapkv_score": (C.c_int, [_vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _f32, _vp, _vp,
                                    _vp]),
     "fkv_score_workspace_bytes": (C.c_int64, [_i32, _i32, _i32, _i32, _i32]),

@@ -41,3 +41,12 @@ extern "C" int fkv_ipc_open(const void* handle, void** out_ptr) {
 extern "C" int fkv_ipc_close(void* ptr) {
   return fkv::cuda_check(cudaIpcCloseMemHandle(ptr), "cudaIpcCloseMemHandle");
 }
+
+// Device address of pinned host memory (cudaHostAlloc / cudaHostRegister),
+// for kernels that write their small results straight to the host
+// (fkv_snapkv_select's budgets in ops.compress_stack).
+extern "C" int fkv_host_device_ptr(void* host_ptr, void** out_ptr) {
+  using namespace fkv;
+  if (!host_ptr || !out_ptr) return set_error(FKV_ERR_INVALID, "fkv_host_device_ptr: null pointer");
+  return cuda_check(cudaHostGetDevicePointer(out_ptr, host_ptr, 0), "cudaHostGetDevicePointer");
+}

@@ -18,6 +18,7 @@ decode step can be captured in a CUDA graph.
 
 from __future__ import annotations
 
+import ctypes
 import math
 
 import torch
@@ -413,14 +414,16 @@ def compress_stack(q_wins, ks, vs, budget: int, window: int | None = 32, alpha: 
     ws = torch.empty(need, dtype=torch.uint8, device=dev)
     sc = torch.empty((L, bt, hkv, T - w), dtype=torch.float32, device=dev)
     # the budgets are written by the kernels straight into pinned host memory
-    # (device-addressable under unified addressing), so the host lays out
+    # (at its device address, fkv_host_device_ptr), so the host lays out
     # layer l as soon as its launch ends, while the GPU scores the next ones
     hb_pin = torch.empty((L, BH), dtype=torch.int32, pin_memory=True)
     hb_np = hb_pin.numpy()
     offsets = torch.empty((L, BH + 1), dtype=torch.int64, device=dev)
     idx = torch.empty((L, max(BH * budget, 1)), dtype=torch.int32, device=dev)
     scale, floor, stream = 1.0 / math.sqrt(HEAD_DIM), ada_floor(budget, w, alpha), _stream()
-    p_sc, p_hb, p_off, p_idx = sc.data_ptr(), hb_pin.data_ptr(), offsets.data_ptr(), idx.data_ptr()
+    dptr = ctypes.c_void_p()
+    _native.check(_lib.fkv_host_device_ptr(hb_pin.data_ptr(), ctypes.byref(dptr)))
+    p_sc, p_hb, p_off, p_idx = sc.data_ptr(), dptr.value, offsets.data_ptr(), idx.data_ptr()
     s_sc, s_hb, s_off, s_idx = 4 * sc[0].numel(), 4 * BH, 8 * (BH + 1), 4 * idx.shape[1]
     ready = []
     for l, (q, k) in enumerate(zip(q_wins, ks)):
