@@ -444,8 +444,13 @@ def compress_stack(q_wins, ks, vs, budget: int, window: int | None = 32, alpha: 
     # every layer's cache laid out as its budgets arrive, then one K/V
     # allocation and ONE host-to-device copy for every plan, the
     # compactions' segment tables and the budgets' device copy
-    caches, (seg_bh, seg_lo, seg_hi) = LayerCache.allocate_many(layers(), group, dev,
-                                                                extra=[bh, np.zeros(BH), hb_np])
+    try:
+        caches, (seg_bh, seg_lo, seg_hi) = LayerCache.allocate_many(layers(), group, dev,
+                                                                    extra=[bh, np.zeros(BH), hb_np])
+    except BaseException:
+        for ev in ready:  # the launches still write hb_pin: let them land before it is freed
+            ev.synchronize()
+        raise
     lens = hb_np
     hbs = seg_hi.view(L, bt, hkv)
     p_bh, p_lo, p_hi = seg_bh.data_ptr(), seg_lo.data_ptr(), seg_hi.data_ptr()
