@@ -127,6 +127,23 @@ __device__ __forceinline__ float fast_exp2(float x) {
   return y;
 }
 
+// 2^x on the FMA / integer pipes instead of the MUFU (a kernel bound by the
+// special-function unit computes part of its exponentials here): x rounded
+// to an integer with the 1.5 * 2^23 trick, 2^f on [-0.5, 0.5] by a degree-4
+// minimax polynomial (max relative error 2.7e-6, fp32 Horner), the integer
+// part added to the exponent field.  x is clamped at -125 (2^-125 ~ 0 next
+// to any sum of probabilities; -inf maps there too).
+__device__ __forceinline__ float poly_exp2(float x) {
+  x = fmaxf(x, -125.f);
+  const float t = x + 12582912.f;  // low mantissa bits of t: round(x)
+  const float f = x - (t - 12582912.f);
+  float p = fmaf(0.009570100344717503f, f, 0.05591785907745361f);
+  p = fmaf(p, f, 0.240247443318367f);
+  p = fmaf(p, f, 0.6931217908859253f);
+  p = fmaf(p, f, 0.9999992847442627f);
+  return __int_as_float(__float_as_int(p) + ((__float_as_int(t) - 0x4B400000) << 23));
+}
+
 // Physical byte offset of logical 16-B chunk `c` of cache row `r` inside a
 // tile whose first row is 8-aligned (the HBM swizzle of fairkv.h).
 __device__ __forceinline__ uint32_t swz_off(uint32_t r, uint32_t c) {
