@@ -249,3 +249,53 @@ def test_append_then_decode(cuda_device, schedule, monkeypatch):
         check_o_lse(o, lse, o_ref, lse_ref)
     assert np.array_equal(cache.sync_lengths(), np.array([len(x) for x in ks]))
     assert int(cache.overflow_t.item()) >= 2
+
+
+def test_append_on_stacked_caches(cuda_device):
+    """Caches laid out together (LayerCache.allocate_many: one K/V
+    allocation, every layer's tables in one device buffer) grow and decode
+    independently: appends to layer 1 change neither layer 0's nor layer 2's
+    outputs, and every layer matches the oracle over its own rows."""
+    from paper_2502_15804_b200 import ops
+    from paper_2502_15804_b200.cache import LayerCache
+    group, hkv, bt, L = 4, 8, 2, 3
+    hq = hkv * group
+    qrow = np.array([b * hq + h * group for b in range(bt) for h in range(hkv)])
+    rng = np.random.default_rng(5)
+    lens = [rng.integers(1, 700, size=bt * hkv) for _ in range(L)]
+    caches, _ = LayerCache.allocate_many([(n, qrow, qrow) for n in lens], group, cuda_device, reserve=5)
+    g = torch.Generator().manual_seed(6)
+    rows = []
+    for c, n in zip(caches, lens):
+        ks = [torch.randn(int(x), 128, generator=g).to(torch.bfloat16) for x in n]
+        vs = [torch.randn(int(x), 128, generator=g).to(torch.bfloat16) for x in n]
+        kh = torch.zeros(c.k.shape, dtype=torch.bfloat16)
+        vh = torch.zeros(c.v.shape, dtype=torch.bfloat16)
+        for r0, k, v in zip(c.host["seg_row0"], ks, vs):
+            kh[r0:r0 + len(k)] = torch.from_numpy(okv.swizzle_rows(k.view(torch.int16).numpy(), r0)).view(torch.bfloat16)
+            vh[r0:r0 + len(v)] = torch.from_numpy(okv.swizzle_rows(v.view(torch.int16).numpy(), r0)).view(torch.bfloat16)
+        c.k.copy_(kh)
+        c.v.copy_(vh)
+        rows.append((ks, vs))
+    q = torch.randn(bt, hq, 128, generator=g).to(torch.bfloat16)
+    before = [ops.decode(q.to(cuda_device), c) for c in (caches[0], caches[2])]
+    for _ in range(3):  # grow layer 1 only
+        kn = torch.randn(bt, hkv, 128, generator=g).to(torch.bfloat16)
+        vn = torch.randn(bt, hkv, 128, generator=g).to(torch.bfloat16)
+        ops.append(caches[1], kn.to(cuda_device), vn.to(cuda_device))
+        ks, vs = rows[1]
+        for s in range(bt * hkv):
+            b, h = divmod(s, hkv)
+            ks[s] = torch.cat([ks[s], kn[b, h][None]])
+            vs[s] = torch.cat([vs[s], vn[b, h][None]])
+    after = [ops.decode(q.to(cuda_device), c) for c in (caches[0], caches[2])]
+    for (o0, l0), (o1, l1) in zip(before, after):
+        assert torch.equal(o0, o1) and torch.equal(l0, l1)
+    for c, (ks, vs) in zip(caches, rows):
+        o, lse = ops.decode(q.to(cuda_device), c)
+        torch.cuda.synchronize()
+        kk = [x.float().numpy().astype(np.float64) for x in ks]
+        vv = [x.float().numpy().astype(np.float64) for x in vs]
+        o_ref, lse_ref = okv.decode_heads(q.float().numpy().astype(np.float64), kk, vv, group)
+        check_o_lse(o, lse, o_ref, lse_ref)
+    assert np.array_equal(caches[1].sync_lengths(), np.array([len(x) for x in rows[1][0]]))
