@@ -549,7 +549,7 @@ EMU_REPLAYS = 3  # replays per back-to-back emulated timing (min)
 # the quantum and the max over similar ranks picks whichever rounded up; the
 # mean over many replays resolves below the quantum (natural jitter dithers)
 EMU_SPAN_REPLAYS = 16
-EMU_ROUNDS = 3   # interleaved rounds over the placements; the median round is reported
+EMU_ROUNDS = 5   # interleaved rounds over the placements; the median round is reported
 
 
 def _alloc_base(budgets, dev, seed=7):
