@@ -200,3 +200,29 @@ def test_schedule_shape_rules(monkeypatch):
     assert per_seg[-1] == per_seg.max() > 2 and len(item_seg) <= C.NUM_SMS
     assert (np.diff(warp_ptr) == 1).all()             # one piece per CTA
     assert (t1 - t0).max() <= 3000 // 2
+
+
+def test_cache_tables_c_contract():
+    """fkv_cache_tables through the C ABI: a short buffer is refused with the
+    needed size in part_off[FKV_CT_PARTS] (and nothing written), a buffer of
+    exactly that size is accepted; parts are 16-byte aligned and ordered."""
+    from paper_2502_15804_b200 import _native
+    lens = np.array([100, 0, 2000, 33], dtype=np.int64)
+    row0, _ = C.segment_offsets(lens)
+    q = np.arange(4, dtype=np.int64) * 8
+    prm, _ = C._sched_params(None, None)
+    offs = np.zeros(C.CT_PARTS + 1, np.int64)
+    sizes = np.zeros(5, np.int32)
+    small = np.full(8, -7, np.int32)
+    p = lambda a: a.ctypes.data  # noqa: E731
+    rc = _native.lib.fkv_cache_tables(p(lens), p(row0), p(q), p(q), None, None, 4, prm, p(small), len(small),
+                                      p(offs), p(sizes))
+    assert rc == -1 and offs[-1] > len(small) and (small == -7).all()
+    buf = np.empty(int(offs[-1]), np.int32)
+    rc = _native.lib.fkv_cache_tables(p(lens), p(row0), p(q), p(q), None, None, 4, prm, p(buf), len(buf),
+                                      p(offs), p(sizes))
+    assert rc == 0 and (offs % 4 == 0).all() and (np.diff(offs) >= 0).all()
+    np.testing.assert_array_equal(buf[offs[0]:offs[0] + 4], lens)                 # SEG_LEN
+    np.testing.assert_array_equal(buf[offs[11]:offs[11] + 4], lens)               # SEG_CAP defaults to seg_len
+    np.testing.assert_array_equal(buf[offs[12]:offs[12] + 4], [-1] * 4)           # APPEND_SRC defaults to -1
+    np.testing.assert_array_equal(buf[offs[16]:offs[16] + 8].view(np.int64), row0)  # SEG_ROW0 as int64
