@@ -299,3 +299,20 @@ def test_append_on_stacked_caches(cuda_device):
         o_ref, lse_ref = okv.decode_heads(q.float().numpy().astype(np.float64), kk, vv, group)
         check_o_lse(o, lse, o_ref, lse_ref)
     assert np.array_equal(caches[1].sync_lengths(), np.array([len(x) for x in rows[1][0]]))
+
+
+def test_decode_long_segments_wide_shape(cuda_device):
+    """A TP=2-like shard at B=1024 (256 segments of ~65 tiles): the
+    automatic schedule takes the 8-warp CTA shape with whole segments packed
+    longest-first (two per CTA on most SMs); o / lse match the oracle."""
+    from paper_2502_15804_b200 import ops
+    from paper_2502_15804_b200.cache import FKV_DECODE_WIDE
+    rng = np.random.default_rng(17)
+    group, hkv, bt = 8, 4, 64
+    seg_lens = rng.integers(700, 1400, size=bt * hkv).tolist()
+    cache, q, ks, vs = build_cache(seg_lens, group, hkv, bt, cuda_device, seed=17)
+    assert cache.flags == FKV_DECODE_WIDE and cache.n_items == len(seg_lens)
+    o, lse = ops.decode(q.to(cuda_device), cache)
+    torch.cuda.synchronize()
+    o_ref, lse_ref = okv.decode_heads(q.float().numpy().astype(np.float64), ks, vs, group)
+    check_o_lse(o, lse, o_ref, lse_ref)
